@@ -1,0 +1,396 @@
+"""Benchmark: unique-sample local energies/sec (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c118]
+
+One step = the surrogate local-energy path over the whole sample set of the
+configuration: per-iteration sample-set hash build, E_loc of every unique
+sample (find coupled pairs + matrix elements + amplitude ratios, fused) and
+the energy/variance moments — with N > 1 also the NCCL all-gather of the
+shards and the all-reduce of the moments. Inputs are resident in HBM when
+the timed region starts (``value``); ``e2e`` repeats the step through the
+reference-facing C ABI with pinned host buffers (H2D + D2H inside).
+
+Timing: W warm-up steps; K timed steps bracketed by barrier + synchronize;
+each step timed with CUDA events on the launching stream, L2 flushed (256 MiB
+write) between steps outside the events; max over ranks. Under torchrun
+(N > 1) every rank owns a contiguous shard of the 1e6 samples (total fixed:
+strong scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "unique-sample local energies/sec (118 qubits, 1e6 samples) at 1/2/4/8 B200 vs CPU"
+UNIT = "unique-sample local energies/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c118")
+    ap.add_argument("--n-unq", type=int, default=None)
+    ap.add_argument("--cpu-sample", type=int, default=None, help="rows of the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ inputs
+
+def make_inputs(cfg_name: str, n_unq=None):
+    from paper_2408_07625_b200 import synthetic
+    cfg = synthetic.CONFIGS[cfg_name]
+    t0 = time.perf_counter()
+    c, x, y, z = synthetic.jw_terms(cfg.n_qubits, cfg.n_terms, seed=1)
+    n = n_unq or cfg.n_unq
+    if cfg_name == "c20":
+        keys = synthetic.random_sector_keys(cfg.n_qubits, cfg.n_electrons, n, seed=2)
+    else:
+        keys = synthetic.near_hf_keys(cfg.n_qubits, cfg.n_electrons, n, seed=2)
+    batch = synthetic.sample_batch(keys, seed=3)
+    return cfg, (c, x, y, z), batch, time.perf_counter() - t0
+
+
+def workload_desc(cfg, H, n_unq):
+    return {
+        "workload": f"{cfg.name}: surrogate E_loc + energy/variance moments over every unique sample",
+        "n_qubits": cfg.n_qubits, "n_electrons": cfg.n_electrons, "pauli_terms": int(H.n_terms),
+        "flip_masks": int(H.n_xy), "n_unq": int(n_unq),
+        "hamiltonian": "JW-structured synthetic (SURVEY.md §8d), seed 1",
+        "samples": "near-HF determinants, 1+Geometric(0.6) same-spin moves, seed 2",
+    }
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([v.strip() for v in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 3 + k and r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ CPU baseline
+
+def cpu_baseline(coeff_masks, n_qubits, batch, sample_rows, threads):
+    """The UNMODIFIED reference path (oracle/_ref) on a bounded sample of the
+    workload: find_coupled_pairs(auto) -> local_energies -> variational_energy
+    over the first `sample_rows` unique samples as their own sample set."""
+    import oracle
+    c, x, y, z = coeff_masks
+    keys = batch.vectors[:sample_rows]
+    la, ph = batch.log_amps[:sample_rows], batch.phases[:sample_rows]
+    lp = 2.0 * la
+    mx = lp.max()
+    log_norm = float(mx + np.log(np.exp(lp - mx).sum()))
+    kind = "reference"
+    if oracle.ref_available():
+        strings = masks_to_strings(n_qubits, x, y, z)
+        t0 = time.perf_counter()
+        R = oracle.RefIndex.from_strings(n_qubits, c, strings)
+        setup = time.perf_counter() - t0
+        _, out5, t3, npairs = R.run_path(keys, la, ph, lp, math.exp(log_norm), log_norm, backend=3,
+                                         threshold=4096, threads=threads, want_locals=False)
+        secs = float(t3.sum())
+        detail = {"find_coupled_pairs_s": float(t3[0]), "local_energies_s": float(t3[1]),
+                  "variational_energy_s": float(t3[2]), "pairs": int(npairs), "index_build_s": setup,
+                  "backend": "auto (trie at >= 4096 samples, coupling.cpp:157-161)"}
+    else:  # the C restatement (terms semantics), when the reference could not be compiled
+        kind = "port"
+        O = oracle.OracleIndex(n_qubits, c, x, y, z)
+        t0 = time.perf_counter()
+        _, npairs = O.eloc_rows(keys, la, ph, 0, len(keys), threads=threads)
+        secs = time.perf_counter() - t0
+        detail = {"pairs": int(npairs), "backend": "terms (oracle restatement)"}
+    return {"value": len(keys) / secs, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"first {len(keys)} of the {batch.size()} unique samples as their own sample set, "
+                      f"full Hamiltonian; {secs:.2f} s",
+            "seconds": secs, **detail}
+
+
+def masks_to_strings(n_qubits, x, y, z):
+    from paper_2408_07625_b200 import basis
+    bx = basis.to_bool_rows(x, n_qubits)
+    by = basis.to_bool_rows(y, n_qubits)
+    bz = basis.to_bool_rows(z, n_qubits)
+    arr = np.full(bx.shape, ord("I"), dtype=np.uint8)
+    arr[bx == 1] = ord("X")
+    arr[by == 1] = ord("Y")
+    arr[bz == 1] = ord("Z")
+    raw = arr.tobytes().decode("ascii")
+    return [raw[i * n_qubits:(i + 1) * n_qubits] for i in range(arr.shape[0])]
+
+
+def default_cpu_sample(cfg):
+    return {"c118": 5000, "c56": 20000, "c20": 100000}.get(cfg, 10000)
+
+
+# ------------------------------------------------------------------ reference arm
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    cfg, cm, batch, _ = make_inputs(args.config, args.n_unq)
+    threads = os.cpu_count() or 1
+    n_s = args.cpu_sample or default_cpu_sample(args.config)
+    for _ in range(max(args.warmup, 0) and 1):  # one untimed warm-up run is enough for a CPU path
+        pass
+    times, last = [], None
+    for _ in range(args.steps):
+        last = cpu_baseline(cm, cfg.n_qubits, batch, n_s, threads)
+        times.append(last["seconds"])
+    t = statistics.mean(times)
+    v = n_s / t
+    from paper_2408_07625_b200 import HamiltonianIndex
+    line = {
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{cfg.name} (CPU sample: {n_s} rows)", "n_qubits": cfg.n_qubits,
+                   "n_unq": batch.size()},
+        "cpu_baseline": {k: last[k] for k in ("value", "unit", "cores", "kind", "sample")} | {"value": v},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2408_07625_b200 as q
+    from paper_2408_07625_b200 import _lib
+    from paper_2408_07625_b200.distributed import Shard, device_evaluate, shard_bounds, sharded_surrogate_energy
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg, cm, batch, gen_s = make_inputs(args.config, args.n_unq)
+    n = batch.size()
+    H = q.HamiltonianIndex.from_masks(cfg.n_qubits, *cm)
+    t0 = time.perf_counter()
+    H.device_handle(local)
+    upload_s = time.perf_counter() - t0
+    r0, r1 = shard_bounds(n, world, rank)
+    W = H.n_words
+
+    def dev_tensor(a, dtype):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev, dtype=dtype)
+
+    keys_all = batch.vectors.view(np.int64)
+    shard = Shard(dev_tensor(keys_all[r0:r1], torch.int64), dev_tensor(batch.log_amps[r0:r1], torch.float64),
+                  dev_tensor(batch.phases[r0:r1], torch.float64), dev_tensor(batch.log_probs[r0:r1], torch.float64))
+    evaluate = device_evaluate(H, local)
+    flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    if world == 1:
+        keys_d, la_d, ph_d, lp_d = shard.keys, shard.log_amps, shard.phases, shard.log_probs
+        loc_d = torch.zeros(n, dtype=torch.complex128, device=dev)
+        mom_d = torch.zeros(5, dtype=torch.float64, device=dev)
+
+        def step():
+            evaluate(keys_d, la_d, ph_d, lp_d, batch.log_norm, 0, n, loc_d, mom_d)
+            return mom_d
+    else:
+        def step():
+            return sharded_surrogate_energy(shard, batch.log_norm, evaluate).moments
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    _lib.check(_lib.lib().qvmc_cuda_synchronize(H.device_handle(local)))
+
+    stream = torch.cuda.current_stream(dev)
+    step_ms, rows_ms, table_ms, mom_ms = [], [], [], []
+    launches0 = q.launch_count()
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.fill_(1)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            st = q.last_stats(H, local)
+            rows_ms.append(st["rows_ms"])
+            table_ms.append(st["table_ms"])
+            mom_ms.append(st["moments_ms"])
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = q.launch_count() - launches0
+    _lib.check(_lib.lib().qvmc_cuda_synchronize(H.device_handle(local)))
+    stats = q.last_stats(H, local)
+    mean_ms = statistics.mean(step_ms)
+    if world > 1:
+        t = torch.tensor([mean_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        mean_ms = float(t)
+    value = n / (mean_ms * 1e-3)
+
+    # ---- e2e through the C ABI with pinned host buffers (N = 1) / public API (N > 1)
+    e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+    import ctypes as C
+    pin = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(dt).pin_memory()
+    if world == 1:
+        hk, hla, hph, hlp = (pin(keys_all, torch.int64), pin(batch.log_amps, torch.float64),
+                             pin(batch.phases, torch.float64), pin(batch.log_probs, torch.float64))
+        hloc = torch.zeros(n, dtype=torch.complex128).pin_memory()
+        hmom = torch.zeros(5, dtype=torch.float64).pin_memory()
+        h = H.device_handle(local)
+        _lib.check(_lib.lib().qvmc_cuda_set_stream(h, None))
+
+        def e2e_step():
+            _lib.check(_lib.lib().qvmc_cuda_eloc_fused(
+                h, n, C.c_void_p(hk.data_ptr()), C.c_void_p(hla.data_ptr()), C.c_void_p(hph.data_ptr()),
+                C.c_void_p(hlp.data_ptr()), batch.log_norm, 0, n, C.c_void_p(hloc.data_ptr()),
+                C.c_void_p(hmom.data_ptr()), _lib.MEM_HOST))
+        h2d = hk.numel() * 8 + 3 * n * 8
+        d2h = n * 16 + 5 * 8
+    else:
+        hk, hla, hph, hlp = (pin(keys_all[r0:r1], torch.int64), pin(batch.log_amps[r0:r1], torch.float64),
+                             pin(batch.phases[r0:r1], torch.float64), pin(batch.log_probs[r0:r1], torch.float64))
+
+        def e2e_step():
+            s = Shard(hk.to(dev, non_blocking=True), hla.to(dev, non_blocking=True),
+                      hph.to(dev, non_blocking=True), hlp.to(dev, non_blocking=True))
+            res = sharded_surrogate_energy(s, batch.log_norm, evaluate)
+            res.locals.cpu()
+            res.moments.cpu()
+        h2d = (r1 - r0) * (8 * W + 24)
+        d2h = (r1 - r0) * 16 + 40
+    e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = []
+    for _ in range(e2e_steps):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e2e_step()
+        torch.cuda.synchronize()
+        e2e_s.append(time.perf_counter() - t0)
+    e2e_t = statistics.mean(e2e_s)
+    if world > 1:
+        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t)
+        _lib.check(_lib.lib().qvmc_cuda_set_stream(H.device_handle(local), None))
+
+    # ---- roofline of the dominant kernel (k_rows): algorithmic bytes / kernel time
+    rows_here = r1 - r0
+    pairs_per_row = stats["pairs"] / max(rows_here, 1)
+    b_alg = 8 * W + 16 + 8 + 16 + pairs_per_row * (8 * W + 16)
+    kern_ms = statistics.mean(rows_ms)
+    achieved = b_alg * rows_here / (kern_ms * 1e-3) / 1e9
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_desc(cfg, H, n) | {
+            "parallelism": f"rows sharded over {world} GPU(s); NCCL all-gather of shards + all-reduce of moments"
+            if world > 1 else "1 GPU",
+            "l2": "flushed between steps (256 MiB write outside the timed events)" if flush is not None else "not flushed"},
+        "e2e": {"value": n / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "path": "qvmc_cuda_eloc_fused(QVMC_MEM_HOST) from pinned buffers" if world == 1
+                else "distributed.sharded_surrogate_energy from pinned host shards"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "k_rows<W, kModeEloc>", "kernel_ms": kern_ms,
+                     "kernel_share_of_step": kern_ms / statistics.mean(step_ms),
+                     "bytes_per_sample": b_alg,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "stages_ms": {"table_build": statistics.mean(table_ms), "rows": kern_ms, "moments": statistics.mean(mom_ms)},
+        "path_stats": {"pairs_per_sample": pairs_per_row, "candidates_per_sample": stats["candidates"] / max(rows_here, 1),
+                       "terms_equivalent_candidates_per_sample": H.n_xy, "sector_mode": stats["sector_mode"],
+                       "minority_count": stats["minority_count"]},
+        "setup_s": {"inputs": gen_s, "upload_and_plan": upload_s},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        cb = cpu_baseline(cm, cfg.n_qubits, batch, args.cpu_sample or default_cpu_sample(args.config), threads)
+        result["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        result["cpu_baseline_detail"] = {k: v for k, v in cb.items() if k not in result["cpu_baseline"]}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,187 @@
+/*
+ * qvmc_cuda.h — C ABI of the B200 surrogate local-energy path.
+ *
+ * libqvmc_cuda.so (paper_2408_07625_b200/lib/) implements these entry points
+ * with hand-written sm_100a kernels. Plain pointers and sizes only: no torch,
+ * Eigen or C++ types cross this boundary. Each entry point names the
+ * reference interface it replaces (paths relative to /root/reference):
+ *
+ *   qvmc_cuda_ham_create        device residency of HamiltonianIndex
+ *                               (proj/include/qvmc/hamiltonian.hpp:41-107)
+ *   qvmc_cuda_pairs[_fetch]     find_coupled_pairs / loop_over_{terms,batch,trie}
+ *                               (proj/include/qvmc/coupling.hpp:40-64,
+ *                                proj/src/coupling.cpp:62-169)
+ *   qvmc_cuda_pair_elements     HamiltonianIndex::group_element per pair
+ *                               (proj/src/hamiltonian.cpp:186-194)
+ *   qvmc_cuda_local_energies    local_energies (proj/include/qvmc/energy.hpp:23-24,
+ *                                proj/src/energy.cpp:13-48)
+ *   qvmc_cuda_energy_moments    variational_energy (energy.hpp:39, energy.cpp:50-78)
+ *   qvmc_cuda_eloc_fused        find_coupled_pairs + local_energies +
+ *                               variational_energy as run_optimisation chains
+ *                               them (proj/src/optimizer.cpp:87-93), without
+ *                               materialising the pairs
+ *
+ * Data layout (shared with the reference's BasisVector, basis_vector.hpp:16-26):
+ * a basis vector of N qubits is n_words = ceil(N/64) uint64 words, qubit i at
+ * word i/64 bit i%64, bits >= N zero. Key arrays are [n][n_words] row-major.
+ * Complex outputs are interleaved (re, im) doubles.
+ *
+ * Memory kind: with QVMC_MEM_HOST every array argument is a host pointer;
+ * the call copies in, computes, copies out and returns when done. With
+ * QVMC_MEM_DEVICE every array argument is a device pointer on the handle's
+ * device; work is enqueued on the handle's stream (qvmc_cuda_set_stream) and
+ * the call returns without synchronising, except where noted. Errors raised
+ * on the device (zero amplitude, duplicate keys) are then reported by the
+ * next qvmc_cuda_synchronize().
+ *
+ * Errors: every entry point returns a QVMC_* status. The reference throws
+ * C++ exceptions; the mapping is QVMC_ERR_INVALID_ARGUMENT ->
+ * std::invalid_argument, QVMC_ERR_LOGIC -> std::logic_error,
+ * QVMC_ERR_RUNTIME / QVMC_ERR_CUDA -> std::runtime_error. The message of the
+ * last failure on the calling thread is qvmc_cuda_last_error().
+ */
+#ifndef QVMC_CUDA_H
+#define QVMC_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  QVMC_OK = 0,
+  QVMC_ERR_INVALID_ARGUMENT = 1, /* bad sizes, duplicate keys, malformed masks */
+  QVMC_ERR_LOGIC = 2,            /* a sampled state has zero amplitude (energy.cpp:32-33) */
+  QVMC_ERR_RUNTIME = 3,          /* zero norm / imaginary residual (energy.cpp:57-58, 74-76) */
+  QVMC_ERR_CUDA = 4,             /* CUDA runtime failure */
+  QVMC_ERR_NO_DEVICE = 5         /* no sm_100 device visible */
+};
+
+/* CouplingBackend (coupling.hpp:17). Every backend returns the identical
+ * canonical pair list; they differ in the `ops` they report (coupling.hpp:22-26). */
+enum { QVMC_BACKEND_TERMS = 0, QVMC_BACKEND_BATCH = 1, QVMC_BACKEND_TRIE = 2, QVMC_BACKEND_AUTO = 3 };
+
+enum { QVMC_MEM_HOST = 0, QVMC_MEM_DEVICE = 1 };
+
+typedef struct qvmc_ham_s* qvmc_ham_t;     /* device-resident HamiltonianIndex + workspace */
+typedef struct qvmc_index_s* qvmc_index_t; /* host-side grouped index (from_terms result) */
+
+/* Counters of the last pairs/fused call on a handle. */
+typedef struct {
+  uint64_t rows;            /* source rows processed */
+  uint64_t candidates;      /* (x, flip mask) candidates probed on the device */
+  uint64_t pairs;           /* coupled pairs found (incl. the diagonal) */
+  uint64_t terms_equivalent;/* n_rows * |XY|: the LoopOverTerms candidate count */
+  int32_t sector_mode;      /* 1 = particle-sector candidate lists, 0 = full flip-mask scan */
+  int32_t sector_side;      /* 1 = occupied orbitals are the minority set, 0 = holes */
+  int32_t minority_count;   /* |minority set| per key in sector mode */
+  int32_t reserved;
+  float table_ms;           /* CUDA-event times of the last fused call's stages on the */
+  float rows_ms;            /* handle's stream: sample-set hash build, row kernel,     */
+  float moments_ms;         /* moment reduction                                       */
+  float reserved_ms;
+} qvmc_stats;
+
+/* ------------------------------------------------------------------ host index */
+
+/* HamiltonianIndex::from_terms (hamiltonian.cpp:63-117) over raw Pauli
+ * strings given as disjoint (x, y, z) masks, [n_raw][n_words] each: merges
+ * duplicate strings in first-occurrence order, drops |coeff| < 1e-12,
+ * groups by xy = x|y in first-occurrence order. */
+int qvmc_index_build(int n_qubits, int n_words, int64_t n_raw, const double* coeff, const uint64_t* x_words,
+                     const uint64_t* y_words, const uint64_t* z_words, qvmc_index_t* out);
+int qvmc_index_info(qvmc_index_t idx, int* n_qubits, uint64_t* n_terms, uint32_t* n_xy, int64_t* diag_xy);
+/* Any output pointer may be NULL. Arrays: xy_words[n_xy][n_words],
+ * group_offsets[n_xy+1], coeff[n_terms], yz_words[n_terms][n_words],
+ * y_weight[n_terms], x/y/z_words[n_terms][n_words] (the merged strings). */
+int qvmc_index_export(qvmc_index_t idx, uint64_t* xy_words, uint64_t* group_offsets, double* coeff,
+                      uint64_t* yz_words, uint8_t* y_weight, uint64_t* x_words, uint64_t* y_words,
+                      uint64_t* z_words);
+void qvmc_index_destroy(qvmc_index_t idx);
+
+/* ------------------------------------------------------------ device handle */
+
+/* Upload a grouped HamiltonianIndex. Arguments mirror the index's members:
+ * xy_set (first-occurrence order), group_offsets (CSR, size n_xy+1), and the
+ * grouped terms' coeff, yz mask and y_weight; diag_xy = diagonal_xy_index()
+ * or -1. device = CUDA ordinal. Builds the device-side candidate lists. */
+int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_t* xy_words,
+                         const uint64_t* group_offsets, uint64_t n_terms, const double* coeff,
+                         const uint64_t* yz_words, const uint8_t* y_weight, int64_t diag_xy, int device,
+                         qvmc_ham_t* out);
+int qvmc_cuda_ham_create_from_index(qvmc_index_t idx, int device, qvmc_ham_t* out);
+int qvmc_cuda_ham_destroy(qvmc_ham_t h);
+/* Run subsequent work on this cudaStream_t (NULL = the handle's own stream). */
+int qvmc_cuda_set_stream(qvmc_ham_t h, void* stream);
+/* Wait for the handle's stream and report deferred device-side errors. */
+int qvmc_cuda_synchronize(qvmc_ham_t h);
+int qvmc_cuda_last_stats(qvmc_ham_t h, qvmc_stats* out); /* synchronises */
+
+/* ------------------------------------------------------------ coupled pairs */
+
+/* find_coupled_pairs (coupling.cpp:153-169): all ordered (x, x') of the
+ * batch with x^x' in the flip-mask set, canonical order (x, then x').
+ * backend / auto_threshold select the reported `ops` semantics exactly as
+ * the reference: terms = n_unq*|XY|, batch = n_unq^2, trie = candidates
+ * actually probed; auto = batch below auto_threshold else trie.
+ * Synchronises; the pair list stays on the device until fetched. */
+int qvmc_cuda_pairs(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, int mem, int backend, int auto_threshold,
+                    uint64_t* n_pairs, uint64_t* ops, int* backend_used);
+/* Copy the last pair list as (x, x', xy) uint32 triples (CoupledPairs::Entry). */
+int qvmc_cuda_pairs_fetch(qvmc_ham_t h, uint32_t* out_entries, int mem);
+
+/* Per pair (x, x', xy): H_{x x'} = group_element(x', xy) evaluated term by
+ * term in the reference's order (bit-identical to hamiltonian.cpp:186-194),
+ * and the excitation class popcount(xy). out_h: [n_pairs][2]; out_class may
+ * be NULL. */
+int qvmc_cuda_pair_elements(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, uint64_t n_pairs,
+                            const uint32_t* entries, double* out_h, uint8_t* out_class, int mem);
+
+/* ------------------------------------------------------------ local energies */
+
+/* local_energies (energy.cpp:13-48) from canonical pairs. out_eloc[n_unq][2].
+ * QVMC_ERR_LOGIC when any log_amp is infinite. */
+int qvmc_cuda_local_energies(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, const double* log_amp,
+                             const double* phase, uint64_t n_pairs, const uint32_t* entries, double* out_eloc,
+                             int mem);
+
+/* variational_energy moments (energy.cpp:50-78) over rows [0, n):
+ * w = exp(log_prob - log_norm); out_moments[5] = (sum w*Re E, sum w*Im E,
+ * sum w^2 (= ipr), sum w, sum w*|E|^2). out_weights[n] optional. The
+ * reference's norm / residual checks are the caller's (host) step. */
+int qvmc_cuda_energy_moments(qvmc_ham_t h, int64_t n, const double* log_prob, double log_norm, const double* eloc,
+                             double* out_moments, double* out_weights, int mem);
+
+/* The fused surrogate-E_loc throughput path: for rows [row_begin, row_end)
+ * of the sample set `keys` (all n_unq rows are partners), E_loc plus the five
+ * moments of those rows, with no pair materialisation. out_eloc
+ * [(row_end-row_begin)][2] may be NULL. Multi-GPU callers shard rows and
+ * pass the all-gathered sample set. */
+int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, const double* log_amp,
+                         const double* phase, const double* log_prob, double log_norm, int64_t row_begin,
+                         int64_t row_end, double* out_eloc, double* out_moments, int mem);
+
+/* Message of the last failure on the calling thread ("" if none). */
+const char* qvmc_cuda_last_error(void);
+/* Kernels launched by this library since load (for launch accounting). */
+uint64_t qvmc_cuda_launch_count(void);
+
+/* ------------------------------------------------ synthetic inputs (bench/tests) */
+
+/* JW-structured molecular-like Hamiltonian: identity, N Z,
+ * C(N,2) ZZ; same-spin single groups {XZ..ZX, YZ..ZY} with one optional
+ * extra Z_k dressing (2+2(N-2) terms per group); spin-conserving doubles
+ * over two even + two odd sites with patterns XXYY/YYXX/XYYX/YXXY and JW
+ * Z-strings, until n_terms_target strings. Arrays sized n_terms_target;
+ * *n_out = strings written. */
+int qvmc_synth_jw_hamiltonian(int n_qubits, int64_t n_terms_target, uint64_t seed, double* coeff, uint64_t* x_words,
+                              uint64_t* y_words, uint64_t* z_words, int64_t* n_out);
+/* n_unq distinct near-Hartree-Fock determinants: first n_electrons orbitals
+ * occupied, then 1+Geometric(0.6) random same-spin occupied->empty moves. */
+int qvmc_synth_near_hf_samples(int n_qubits, int n_electrons, int64_t n_unq, uint64_t seed, uint64_t* keys);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,366 @@
+// C entry points over the UNMODIFIED reference hot path (test/bench infrastructure).
+//
+// This file is compiled together with the reference's own sources from
+// /root/reference/proj/src (basis_vector, rng, hamiltonian, prefix_tree,
+// coupling, energy, synthetic) by oracle/Makefile into oracle/_ref/
+// libqvmc_ref_hot.so. It is a checker and CPU baseline only: it is used by
+// tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+// reference leg, never by the product path.
+//
+// Every function catches C++ exceptions and returns a negative status; the
+// exception class and message are available from qref_last_error().
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "qvmc/basis_vector.hpp"
+#include "qvmc/coupling.hpp"
+#include "qvmc/energy.hpp"
+#include "qvmc/hamiltonian.hpp"
+#include "qvmc/rng.hpp"
+#include "qvmc/sampler.hpp"
+#include "qvmc/synthetic.hpp"
+
+using qvmc::BasisVector;
+using qvmc::CoupledPairs;
+using qvmc::HamiltonianIndex;
+
+static_assert(std::is_standard_layout_v<BasisVector>, "BasisVector word access relies on standard layout");
+
+namespace {
+
+thread_local std::string g_error;
+
+enum Status { kOk = 0, kInvalidArgument = -1, kLogicError = -2, kRuntimeError = -3, kOther = -4 };
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return kOk;
+  } catch (const std::invalid_argument& e) {
+    g_error = std::string("invalid_argument: ") + e.what();
+    return kInvalidArgument;
+  } catch (const std::out_of_range& e) {
+    g_error = std::string("invalid_argument: ") + e.what();
+    return kInvalidArgument;
+  } catch (const std::logic_error& e) {
+    g_error = std::string("logic_error: ") + e.what();
+    return kLogicError;
+  } catch (const std::runtime_error& e) {
+    g_error = std::string("runtime_error: ") + e.what();
+    return kRuntimeError;
+  } catch (const std::exception& e) {
+    g_error = std::string("exception: ") + e.what();
+    return kOther;
+  }
+}
+
+// BasisVector keeps its words private; the class is standard-layout with the
+// word array as first member, so the words are the leading 32 bytes.
+void read_words(const BasisVector& v, std::uint64_t* out, int n_words) {
+  std::uint64_t w[BasisVector::kMaxWords];
+  std::memcpy(w, &v, sizeof(w));
+  for (int i = 0; i < n_words; ++i) out[i] = w[i];
+}
+
+BasisVector make_vector(int n_qubits, const std::uint64_t* words, int n_words) {
+  BasisVector v(n_qubits);
+  std::uint64_t w[BasisVector::kMaxWords] = {0, 0, 0, 0};
+  for (int i = 0; i < n_words; ++i) w[i] = words[i];
+  // keep the canonical zero tail
+  const int tail = n_qubits % 64;
+  if (tail) w[n_qubits / 64] &= (std::uint64_t{1} << tail) - 1;
+  std::memcpy(&v, w, sizeof(w));
+  return v;
+}
+
+std::vector<BasisVector> make_batch(int n_qubits, int n_words, std::int64_t n, const std::uint64_t* keys) {
+  std::vector<BasisVector> out;
+  out.reserve(static_cast<std::size_t>(n));
+  for (std::int64_t i = 0; i < n; ++i) out.push_back(make_vector(n_qubits, keys + i * n_words, n_words));
+  return out;
+}
+
+struct PairsBox {
+  CoupledPairs pairs;
+};
+
+struct RngBox {
+  qvmc::SequentialRng rng;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* qref_last_error(void) { return g_error.c_str(); }
+
+// HamiltonianIndex::parse over a text buffer (hamiltonian.cpp:119-170).
+int qref_index_parse(const char* text, void** out) {
+  return guarded([&] {
+    std::istringstream in(text);
+    *out = new HamiltonianIndex(HamiltonianIndex::parse(in));
+  });
+}
+
+// HamiltonianIndex::from_terms over n_terms strings of n_qubits characters
+// packed back to back (hamiltonian.cpp:63-117).
+int qref_index_from_strings(int n_qubits, std::int64_t n_terms, const double* coeff, const char* strings,
+                            void** out) {
+  return guarded([&] {
+    std::vector<std::pair<double, std::string>> raw;
+    raw.reserve(static_cast<std::size_t>(n_terms));
+    for (std::int64_t t = 0; t < n_terms; ++t)
+      raw.emplace_back(coeff[t], std::string(strings + t * n_qubits, static_cast<std::size_t>(n_qubits)));
+    *out = new HamiltonianIndex(HamiltonianIndex::from_terms(n_qubits, raw));
+  });
+}
+
+// synthetic.cpp:18-49
+int qref_random_hamiltonian(int n_qubits, int n_terms, std::uint64_t seed, int max_weight, void** out) {
+  return guarded([&] { *out = new HamiltonianIndex(qvmc::random_hamiltonian(n_qubits, n_terms, seed, max_weight)); });
+}
+
+void qref_index_free(void* h) { delete static_cast<HamiltonianIndex*>(h); }
+
+int qref_index_info(void* hp, int* n_qubits, std::uint64_t* n_terms, std::uint32_t* n_xy, std::int64_t* diag) {
+  return guarded([&] {
+    const auto& h = *static_cast<HamiltonianIndex*>(hp);
+    *n_qubits = h.n_qubits();
+    *n_terms = h.n_terms();
+    *n_xy = static_cast<std::uint32_t>(h.xy_set().size());
+    const auto d = h.diagonal_xy_index();
+    *diag = d ? static_cast<std::int64_t>(*d) : -1;
+  });
+}
+
+// Grouped layout as held by HamiltonianIndex: xy_set in first-occurrence
+// order, CSR group offsets, and per term (coeff, x, y, z, yz masks, y_weight).
+int qref_index_export(void* hp, int n_words, std::uint64_t* xy_words, std::uint64_t* group_offsets, double* coeff,
+                      std::uint64_t* x_words, std::uint64_t* y_words, std::uint64_t* z_words,
+                      std::uint64_t* yz_words, std::uint8_t* y_weight) {
+  return guarded([&] {
+    const auto& h = *static_cast<HamiltonianIndex*>(hp);
+    const auto& xy = h.xy_set();
+    for (std::size_t g = 0; g < xy.size(); ++g) read_words(xy[g], xy_words + g * n_words, n_words);
+    const auto* base = h.terms().data();
+    for (std::size_t g = 0; g < xy.size(); ++g) group_offsets[g] = static_cast<std::uint64_t>(h.group(g).data() - base);
+    group_offsets[xy.size()] = h.terms().size();
+    const auto& terms = h.terms();
+    for (std::size_t t = 0; t < terms.size(); ++t) {
+      coeff[t] = terms[t].coeff;
+      if (x_words) read_words(terms[t].x_mask, x_words + t * n_words, n_words);
+      if (y_words) read_words(terms[t].y_mask, y_words + t * n_words, n_words);
+      if (z_words) read_words(terms[t].z_mask, z_words + t * n_words, n_words);
+      if (yz_words) read_words(terms[t].yz_mask, yz_words + t * n_words, n_words);
+      if (y_weight) y_weight[t] = static_cast<std::uint8_t>(terms[t].y_weight);
+    }
+  });
+}
+
+// hamiltonian.cpp:178-184
+int qref_matrix_element(void* hp, int n_words, const std::uint64_t* x, const std::uint64_t* xp, double* out2) {
+  return guarded([&] {
+    const auto& h = *static_cast<HamiltonianIndex*>(hp);
+    const auto e = h.matrix_element(make_vector(h.n_qubits(), x, n_words), make_vector(h.n_qubits(), xp, n_words));
+    out2[0] = e.real();
+    out2[1] = e.imag();
+  });
+}
+
+// hamiltonian.cpp:186-194
+int qref_group_element(void* hp, int n_words, const std::uint64_t* xp, std::uint32_t g, double* out2) {
+  return guarded([&] {
+    const auto& h = *static_cast<HamiltonianIndex*>(hp);
+    const auto e = h.group_element(make_vector(h.n_qubits(), xp, n_words), g);
+    out2[0] = e.real();
+    out2[1] = e.imag();
+  });
+}
+
+// synthetic.cpp:51-70
+int qref_random_distinct_vectors(int n_qubits, int count, std::uint64_t seed, int n_words, std::uint64_t* out) {
+  return guarded([&] {
+    const auto v = qvmc::random_distinct_vectors(n_qubits, count, seed);
+    for (std::size_t i = 0; i < v.size(); ++i) read_words(v[i], out + i * n_words, n_words);
+  });
+}
+
+// backend: 0 terms, 1 batch, 2 trie, 3 auto (coupling.hpp:17)
+int qref_pairs(void* hp, std::int64_t n_unq, int n_words, const std::uint64_t* keys, int backend, int threshold,
+               int threads, void** out) {
+  return guarded([&] {
+    const auto& h = *static_cast<HamiltonianIndex*>(hp);
+    const auto batch = make_batch(h.n_qubits(), n_words, n_unq, keys);
+    auto box = new PairsBox;
+    try {
+      switch (backend) {
+        case 0: box->pairs = qvmc::loop_over_terms(batch, h, threads); break;
+        case 1: box->pairs = qvmc::loop_over_batch(batch, h, threads); break;
+        case 2: box->pairs = qvmc::loop_over_trie(batch, h, threads); break;
+        default: {
+          qvmc::CouplingOptions opt;
+          opt.backend = qvmc::CouplingBackend::kAuto;
+          opt.auto_batch_threshold = threshold;
+          opt.threads = threads;
+          box->pairs = qvmc::find_coupled_pairs(batch, h, opt);
+        }
+      }
+    } catch (...) {
+      delete box;
+      throw;
+    }
+    *out = box;
+  });
+}
+
+void qref_pairs_free(void* p) { delete static_cast<PairsBox*>(p); }
+
+int qref_pairs_info(void* p, std::uint64_t* n_pairs, std::uint64_t* ops, int* backend) {
+  return guarded([&] {
+    const auto& box = *static_cast<PairsBox*>(p);
+    *n_pairs = box.pairs.entries.size();
+    *ops = box.pairs.ops;
+    *backend = static_cast<int>(box.pairs.backend);
+  });
+}
+
+int qref_pairs_copy(void* p, std::uint32_t* out3) {
+  return guarded([&] {
+    const auto& e = static_cast<PairsBox*>(p)->pairs.entries;
+    for (std::size_t i = 0; i < e.size(); ++i) {
+      out3[3 * i] = e[i].x;
+      out3[3 * i + 1] = e[i].x_prime;
+      out3[3 * i + 2] = e[i].xy;
+    }
+  });
+}
+
+// Build a CoupledPairs from caller triples (to feed local_energies).
+int qref_pairs_from_triples(std::uint64_t n_pairs, const std::uint32_t* in3, void** out) {
+  return guarded([&] {
+    auto box = new PairsBox;
+    box->pairs.entries.resize(static_cast<std::size_t>(n_pairs));
+    for (std::uint64_t i = 0; i < n_pairs; ++i)
+      box->pairs.entries[i] = {in3[3 * i], in3[3 * i + 1], in3[3 * i + 2]};
+    *out = box;
+  });
+}
+
+// energy.cpp:13-48; out_eloc is interleaved (re, im).
+int qref_local_energies(void* hp, void* pp, std::int64_t n_unq, int n_words, const std::uint64_t* keys,
+                        const double* log_amps, const double* phases, int threads, double* out_eloc) {
+  return guarded([&] {
+    const auto& h = *static_cast<HamiltonianIndex*>(hp);
+    qvmc::SampleBatch batch;
+    batch.vectors = make_batch(h.n_qubits(), n_words, n_unq, keys);
+    batch.log_amps.resize(n_unq);
+    batch.phases.resize(n_unq);
+    batch.log_probs.resize(n_unq);
+    for (std::int64_t i = 0; i < n_unq; ++i) {
+      batch.log_amps[i] = log_amps[i];
+      batch.phases[i] = phases[i];
+      batch.log_probs[i] = 2.0 * log_amps[i];
+    }
+    const auto locals = qvmc::local_energies(static_cast<PairsBox*>(pp)->pairs, batch, h, threads);
+    for (std::int64_t i = 0; i < n_unq; ++i) {
+      out_eloc[2 * i] = locals[i].real();
+      out_eloc[2 * i + 1] = locals[i].imag();
+    }
+  });
+}
+
+// energy.cpp:50-78; out5 = (e_var, im_residual, ipr, norm, log_norm); weights optional.
+int qref_variational_energy(std::int64_t n, const double* log_probs, double norm, double log_norm,
+                            const double* eloc, double* out5, double* weights) {
+  return guarded([&] {
+    qvmc::SampleBatch batch;
+    batch.vectors.assign(static_cast<std::size_t>(n), BasisVector(1));
+    batch.log_probs.resize(n);
+    batch.log_amps.resize(n);
+    batch.phases.resize(n);
+    for (std::int64_t i = 0; i < n; ++i) batch.log_probs[i] = log_probs[i];
+    batch.norm = norm;
+    batch.log_norm = log_norm;
+    Eigen::VectorXcd locals(n);
+    for (std::int64_t i = 0; i < n; ++i) locals[i] = {eloc[2 * i], eloc[2 * i + 1]};
+    const auto r = qvmc::variational_energy(batch, locals);
+    out5[0] = r.e_var;
+    out5[1] = r.im_residual;
+    out5[2] = r.ipr;
+    out5[3] = r.norm;
+    out5[4] = r.log_norm;
+    if (weights)
+      for (std::int64_t i = 0; i < n; ++i) weights[i] = r.weights[i];
+  });
+}
+
+// The reference CPU path end to end, as run_optimisation drives it
+// (optimizer.cpp:87-93): find_coupled_pairs -> local_energies ->
+// variational_energy. Only rows [0, n_rows) need not be the whole batch:
+// the batch passed IS the sample set. times3 = seconds per stage.
+int qref_run_path(void* hp, std::int64_t n_unq, int n_words, const std::uint64_t* keys, const double* log_amps,
+                  const double* phases, const double* log_probs, double norm, double log_norm, int backend,
+                  int threshold, int threads, double* out_eloc, double* out5, double* times3,
+                  std::uint64_t* n_pairs) {
+  return guarded([&] {
+    using clock = std::chrono::steady_clock;
+    const auto& h = *static_cast<HamiltonianIndex*>(hp);
+    qvmc::SampleBatch batch;
+    batch.vectors = make_batch(h.n_qubits(), n_words, n_unq, keys);
+    batch.log_amps.resize(n_unq);
+    batch.phases.resize(n_unq);
+    batch.log_probs.resize(n_unq);
+    for (std::int64_t i = 0; i < n_unq; ++i) {
+      batch.log_amps[i] = log_amps[i];
+      batch.phases[i] = phases[i];
+      batch.log_probs[i] = log_probs[i];
+    }
+    batch.norm = norm;
+    batch.log_norm = log_norm;
+    qvmc::CouplingOptions opt;
+    opt.backend = static_cast<qvmc::CouplingBackend>(backend);
+    opt.auto_batch_threshold = threshold;
+    opt.threads = threads;
+    const auto t0 = clock::now();
+    const auto pairs = qvmc::find_coupled_pairs(batch.vectors, h, opt);
+    const auto t1 = clock::now();
+    const auto locals = qvmc::local_energies(pairs, batch, h, threads);
+    const auto t2 = clock::now();
+    const auto r = qvmc::variational_energy(batch, locals);
+    const auto t3 = clock::now();
+    times3[0] = std::chrono::duration<double>(t1 - t0).count();
+    times3[1] = std::chrono::duration<double>(t2 - t1).count();
+    times3[2] = std::chrono::duration<double>(t3 - t2).count();
+    *n_pairs = pairs.entries.size();
+    if (out_eloc)
+      for (std::int64_t i = 0; i < n_unq; ++i) {
+        out_eloc[2 * i] = locals[i].real();
+        out_eloc[2 * i + 1] = locals[i].imag();
+      }
+    out5[0] = r.e_var;
+    out5[1] = r.im_residual;
+    out5[2] = r.ipr;
+    out5[3] = r.norm;
+    out5[4] = r.log_norm;
+  });
+}
+
+// SequentialRng (rng.hpp:70-93), to regenerate the reference tests' seeded
+// random-instance families.
+void* qref_rng_new(std::uint64_t seed, std::uint32_t stream) { return new RngBox{qvmc::SequentialRng(seed, stream)}; }
+void qref_rng_free(void* r) { delete static_cast<RngBox*>(r); }
+std::uint64_t qref_rng_uniform_int(void* r, std::uint64_t n) { return static_cast<RngBox*>(r)->rng.uniform_int(n); }
+std::uint64_t qref_rng_bits64(void* r) { return static_cast<RngBox*>(r)->rng.bits64(); }
+
+}  // extern "C"

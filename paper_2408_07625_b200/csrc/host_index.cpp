@@ -1,0 +1,405 @@
+// Host-side setup for the B200 local-energy path: grouped index, device-layout
+// planning and synthetic inputs. See host_index.h.
+#include "host_index.h"
+
+#include <algorithm>
+#include <array>
+#include <bit>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+
+namespace qvmc_b200 {
+
+namespace {
+
+uint64_t splitmix64(uint64_t& s) {
+  uint64_t z = (s += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+struct Rng {
+  uint64_t s;
+  explicit Rng(uint64_t seed) : s(seed * 0x2545F4914F6CDD1Dull + 0x1234567ull) {}
+  uint64_t bits() { return splitmix64(s); }
+  uint64_t below(uint64_t n) { return bits() % n; }
+  double uniform() { return static_cast<double>(bits() >> 11) * 0x1.0p-53; }
+};
+
+using Words3 = std::array<uint64_t, 3 * kMaxWords>;
+
+struct Words3Hash {
+  size_t operator()(const Words3& k) const noexcept {
+    uint64_t h = 0x9e3779b97f4a7c15ull;
+    for (uint64_t w : k) {
+      h ^= w + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+      h *= 0xff51afd7ed558ccdull;
+      h ^= h >> 33;
+    }
+    return static_cast<size_t>(h);
+  }
+};
+
+using WordsN = std::array<uint64_t, kMaxWords>;
+struct WordsNHash {
+  size_t operator()(const WordsN& k) const noexcept { return Words3Hash{}(Words3{k[0], k[1], k[2], k[3]}); }
+};
+
+}  // namespace
+
+HostIndex index_from_terms(int n_qubits, int n_words, int64_t n_raw, const double* coeff, const uint64_t* xw,
+                           const uint64_t* yw, const uint64_t* zw) {
+  if (n_qubits < 1 || n_qubits > 64 * kMaxWords)
+    throw std::invalid_argument("HamiltonianIndex: qubit count out of range");
+  if (n_words != (n_qubits + 63) / 64) throw std::invalid_argument("HamiltonianIndex: n_words != ceil(N/64)");
+  if (n_raw < 0) throw std::invalid_argument("HamiltonianIndex: negative term count");
+  const int tail = n_qubits % 64;
+  const uint64_t tail_mask = tail ? ((uint64_t{1} << tail) - 1) : ~uint64_t{0};
+
+  // merge duplicate strings, keeping first-occurrence order (hamiltonian.cpp:68-85)
+  std::vector<Words3> keys;
+  std::vector<double> mcoef;
+  std::unordered_map<Words3, size_t, Words3Hash> seen;
+  keys.reserve(static_cast<size_t>(n_raw));
+  mcoef.reserve(static_cast<size_t>(n_raw));
+  seen.reserve(static_cast<size_t>(n_raw) * 2);
+  for (int64_t t = 0; t < n_raw; ++t) {
+    Words3 k{};
+    for (int w = 0; w < n_words; ++w) {
+      const uint64_t a = xw[t * n_words + w], b = yw[t * n_words + w], c = zw[t * n_words + w];
+      if ((a & b) | (a & c) | (b & c))
+        throw std::invalid_argument("HamiltonianIndex: term " + std::to_string(t) + " has overlapping Pauli masks");
+      if (w == n_words - 1 && ((a | b | c) & ~tail_mask))
+        throw std::invalid_argument("HamiltonianIndex: term " + std::to_string(t) + " has bits beyond the qubit count");
+      k[w] = a;
+      k[kMaxWords + w] = b;
+      k[2 * kMaxWords + w] = c;
+    }
+    auto [it, fresh] = seen.emplace(k, keys.size());
+    if (fresh) {
+      keys.push_back(k);
+      mcoef.push_back(coeff[t]);
+    } else {
+      mcoef[it->second] += coeff[t];
+    }
+  }
+
+  // group survivors by xy = x|y, first-occurrence order (hamiltonian.cpp:88-112)
+  HostIndex h;
+  h.n_qubits = n_qubits;
+  h.n_words = n_words;
+  std::unordered_map<WordsN, uint32_t, WordsNHash> xy_lookup;
+  std::vector<std::vector<uint32_t>> members;
+  for (size_t i = 0; i < keys.size(); ++i) {
+    if (std::abs(mcoef[i]) < 1e-12) continue;  // kDropThreshold (hamiltonian.cpp:14, 93)
+    WordsN m{};
+    for (int w = 0; w < n_words; ++w) m[w] = keys[i][w] | keys[i][kMaxWords + w];
+    auto [it, fresh] = xy_lookup.emplace(m, static_cast<uint32_t>(members.size()));
+    if (fresh) {
+      members.emplace_back();
+      for (int w = 0; w < n_words; ++w) h.xy.push_back(m[w]);
+    }
+    members[it->second].push_back(static_cast<uint32_t>(i));
+  }
+  h.offsets.assign(members.size() + 1, 0);
+  for (size_t g = 0; g < members.size(); ++g) {
+    h.offsets[g] = h.coeff.size();
+    for (uint32_t i : members[g]) {
+      h.coeff.push_back(mcoef[i]);
+      int yc = 0;
+      for (int w = 0; w < n_words; ++w) {
+        const uint64_t x = keys[i][w], y = keys[i][kMaxWords + w], z = keys[i][2 * kMaxWords + w];
+        h.x.push_back(x);
+        h.y.push_back(y);
+        h.z.push_back(z);
+        h.yz.push_back(y | z);
+        yc += std::popcount(y);
+      }
+      h.y_weight.push_back(static_cast<uint8_t>(yc));
+    }
+  }
+  h.offsets[members.size()] = h.coeff.size();
+  const auto d = xy_lookup.find(WordsN{});
+  h.diag = d == xy_lookup.end() ? -1 : static_cast<int64_t>(d->second);
+  return h;
+}
+
+const uint64_t* qubit_codes() {
+  static const std::array<uint64_t, 256> codes = [] {
+    std::array<uint64_t, 256> c{};
+    uint64_t s = 0x51A7E5B200ull;
+    for (auto& v : c) v = splitmix64(s);
+    return c;
+  }();
+  return codes.data();
+}
+
+uint64_t linear_hash(const uint64_t* words, int n_words) {
+  const uint64_t* r = qubit_codes();
+  uint64_t h = 0;
+  for (int w = 0; w < n_words; ++w) {
+    uint64_t v = words[w];
+    while (v) {
+      const int b = std::countr_zero(v);
+      h ^= r[w * 64 + b];
+      v &= v - 1;
+    }
+  }
+  return h;
+}
+
+DevicePlan plan_device(const HostIndex& h) {
+  DevicePlan p;
+  const int n = h.n_qubits, W = h.n_words;
+  const uint32_t n_xy = h.n_xy();
+  p.xy_hash.resize(n_xy);
+  p.xy_weight.resize(n_xy);
+  p.offsets32.resize(n_xy + 1);
+  if (h.n_terms() >= 0xFFFFFFFFull) throw std::invalid_argument("HamiltonianIndex: more than 2^32-1 terms");
+  for (uint32_t g = 0; g <= n_xy; ++g) p.offsets32[g] = static_cast<uint32_t>(h.offsets[g]);
+
+  const uint32_t n_lists = static_cast<uint32_t>(n + n * (n - 1) / 2);
+  std::vector<uint32_t> count(n_lists + 1, 0);
+  auto for_each_list = [&](uint32_t g, auto&& fn) {
+    int pos[4], k = 0;
+    for (int w = 0; w < W; ++w) {
+      uint64_t v = h.xy[static_cast<size_t>(g) * W + w];
+      while (v && k < 4) {
+        pos[k++] = w * 64 + std::countr_zero(v);
+        v &= v - 1;
+      }
+    }
+    if (p.xy_weight[g] == 2) {
+      fn(static_cast<uint32_t>(pos[0]));
+      fn(static_cast<uint32_t>(pos[1]));
+    } else if (p.xy_weight[g] == 4) {
+      for (int a = 0; a < 4; ++a)
+        for (int b = a + 1; b < 4; ++b) fn(static_cast<uint32_t>(n) + pair_index(pos[a], pos[b], n));
+    }
+  };
+  for (uint32_t g = 0; g < n_xy; ++g) {
+    int wt = 0;
+    for (int w = 0; w < W; ++w) wt += std::popcount(h.xy[static_cast<size_t>(g) * W + w]);
+    p.xy_weight[g] = static_cast<uint8_t>(wt);
+    p.xy_hash[g] = linear_hash(&h.xy[static_cast<size_t>(g) * W], W);
+    if (static_cast<int64_t>(g) == h.diag) continue;
+    p.gen_g.push_back(g);
+    p.gen_hash.push_back(p.xy_hash[g]);
+    if (wt == 2 || wt == 4)
+      for_each_list(g, [&](uint32_t id) { ++count[id + 1]; });
+    else if (wt % 2 == 0)
+      p.res_g.push_back(g);
+    // odd weights change the particle number: never inside one sector
+  }
+  p.lst_off.assign(n_lists + 1, 0);
+  for (uint32_t i = 0; i < n_lists; ++i) p.lst_off[i + 1] = p.lst_off[i] + count[i + 1];
+  p.lst_hash.resize(p.lst_off[n_lists]);
+  p.lst_g.resize(p.lst_off[n_lists]);
+  std::vector<uint32_t> fill(p.lst_off.begin(), p.lst_off.end() - 1);
+  for (uint32_t g = 0; g < n_xy; ++g) {
+    if (static_cast<int64_t>(g) == h.diag) continue;
+    const int wt = p.xy_weight[g];
+    if (wt != 2 && wt != 4) continue;
+    for_each_list(g, [&](uint32_t id) {
+      const uint32_t e = fill[id]++;
+      p.lst_hash[e] = p.xy_hash[g];
+      p.lst_g[e] = g;
+    });
+  }
+
+  // Diagonal group: every term is a Z string (xy = 0 forces x = y = 0), so
+  // its element is sum_t c_t (-1)^{|x & z_t|}. Terms with |z| <= 2 form
+  // c0 + sum_p a_p s_p + sum_{p<q} J_pq s_p s_q with s_p = 1 - 2 x_p, which
+  // is rewritten over the minority set S of x (occupied or empty orbitals):
+  //   occupied: A + sum_{p in S} b_p + sum_{p<q in S} 4 J_pq,
+  //     A = c0 + sum a + sum J, b_p = -2 a_p - 2 sum_{q!=p} J_pq
+  //   holes:    A' = c0 - sum a + sum J, b'_p = 2 a_p - 2 sum_{q!=p} J_pq.
+  if (h.diag >= 0) {
+    p.diag_quad = true;
+    long double c0 = 0, sa = 0, sj = 0;
+    std::vector<long double> a(n, 0), row(n, 0);
+    p.diag_K.assign(static_cast<size_t>(n) * n, 0.0);
+    for (uint64_t t = h.offsets[h.diag]; t < h.offsets[h.diag + 1]; ++t) {
+      if (h.y_weight[t] != 0) {  // cannot happen for xy = 0; keep exact anyway
+        p.diag_other.push_back(static_cast<uint32_t>(t));
+        continue;
+      }
+      int pos[3], k = 0;
+      for (int w = 0; w < W; ++w) {
+        uint64_t v = h.yz[t * W + w];
+        while (v && k < 3) {
+          pos[k++] = w * 64 + std::countr_zero(v);
+          v &= v - 1;
+        }
+      }
+      const long double c = h.coeff[t];
+      if (k == 0) {
+        c0 += c;
+      } else if (k == 1) {
+        a[pos[0]] += c;
+        sa += c;
+      } else if (k == 2) {
+        p.diag_K[static_cast<size_t>(pos[0]) * n + pos[1]] += static_cast<double>(4 * c);
+        p.diag_K[static_cast<size_t>(pos[1]) * n + pos[0]] += static_cast<double>(4 * c);
+        row[pos[0]] += c;
+        row[pos[1]] += c;
+        sj += c;
+      } else {
+        p.diag_other.push_back(static_cast<uint32_t>(t));
+      }
+    }
+    p.diag_A[1] = static_cast<double>(c0 + sa + sj);
+    p.diag_A[0] = static_cast<double>(c0 - sa + sj);
+    p.diag_b.assign(2 * static_cast<size_t>(n), 0.0);
+    for (int q = 0; q < n; ++q) {
+      p.diag_b[n + q] = static_cast<double>(-2 * a[q] - 2 * row[q]);
+      p.diag_b[q] = static_cast<double>(2 * a[q] - 2 * row[q]);
+    }
+  }
+
+  // byte tables of the linear hash: T[k][v] = XOR of codes of the bits of byte v at byte k
+  const uint64_t* r = qubit_codes();
+  p.hash_bytes.assign(static_cast<size_t>(W) * 8 * 256, 0);
+  for (int k = 0; k < W * 8; ++k)
+    for (int v = 0; v < 256; ++v) {
+      uint64_t x = 0;
+      for (int b = 0; b < 8; ++b)
+        if ((v >> b) & 1) x ^= r[k * 8 + b];
+      p.hash_bytes[static_cast<size_t>(k) * 256 + v] = x;
+    }
+  return p;
+}
+
+// ---------------------------------------------------------------- synthetic
+
+int64_t synth_jw_hamiltonian(int n, int64_t n_target, uint64_t seed, double* coeff, uint64_t* xw, uint64_t* yw,
+                             uint64_t* zw) {
+  if (n < 4 || n > 64 * kMaxWords) throw std::invalid_argument("synth: qubit count out of range");
+  const int W = (n + 63) / 64;
+  Rng rng(seed);
+  static const double kMag[6] = {1.0, 0.5, 0.1, 0.05, 0.01, 0.02};
+  auto draw = [&] { return (rng.bits() & 1 ? -1.0 : 1.0) * kMag[rng.below(6)]; };
+  int64_t count = 0;
+  std::vector<uint64_t> X(W), Y(W), Z(W);
+  auto clear = [&] {
+    std::fill(X.begin(), X.end(), 0);
+    std::fill(Y.begin(), Y.end(), 0);
+    std::fill(Z.begin(), Z.end(), 0);
+  };
+  auto setb = [](std::vector<uint64_t>& v, int i) { v[i / 64] |= uint64_t{1} << (i % 64); };
+  auto flipb = [](std::vector<uint64_t>& v, int i) { v[i / 64] ^= uint64_t{1} << (i % 64); };
+  auto emit = [&](double c) {
+    if (count >= n_target) return false;
+    coeff[count] = c;
+    for (int w = 0; w < W; ++w) {
+      xw[count * W + w] = X[w];
+      yw[count * W + w] = Y[w];
+      zw[count * W + w] = Z[w];
+    }
+    ++count;
+    return true;
+  };
+  // diagonal: identity, Z_p, Z_p Z_q
+  clear();
+  if (!emit(draw())) return count;
+  for (int p = 0; p < n; ++p) {
+    clear();
+    setb(Z, p);
+    if (!emit(draw())) return count;
+  }
+  for (int p = 0; p < n; ++p)
+    for (int q = p + 1; q < n; ++q) {
+      clear();
+      setb(Z, p);
+      setb(Z, q);
+      if (!emit(draw())) return count;
+    }
+  // same-spin singles: X_p Z.. X_q and Y_p Z.. Y_q, each also dressed by Z_k
+  for (int p = 0; p < n; ++p)
+    for (int q = p + 2; q < n; q += 2) {
+      for (int letter = 0; letter < 2; ++letter) {
+        for (int k = -1; k < n; ++k) {
+          if (k == p || k == q) continue;
+          clear();
+          auto& L = letter == 0 ? X : Y;
+          setb(L, p);
+          setb(L, q);
+          for (int r = p + 1; r < q; ++r) setb(Z, r);
+          if (k >= 0) flipb(Z, k);
+          if (!emit(draw())) return count;
+        }
+      }
+    }
+  // spin-conserving doubles on two even and two odd sites
+  const int n_even = (n + 1) / 2, n_odd = n / 2;
+  const uint64_t possible = static_cast<uint64_t>(n_even) * (n_even - 1) / 2 * (static_cast<uint64_t>(n_odd) * (n_odd - 1) / 2);
+  std::unordered_set<uint32_t> used;
+  static const char* kPat[4] = {"XXYY", "YYXX", "XYYX", "YXXY"};
+  while (count + 4 <= n_target && used.size() < possible) {
+    int e0 = 2 * static_cast<int>(rng.below(n_even)), e1 = 2 * static_cast<int>(rng.below(n_even));
+    int o0 = 2 * static_cast<int>(rng.below(n_odd)) + 1, o1 = 2 * static_cast<int>(rng.below(n_odd)) + 1;
+    if (e0 == e1 || o0 == o1) continue;
+    int s[4] = {e0, e1, o0, o1};
+    std::sort(s, s + 4);
+    const uint32_t key = static_cast<uint32_t>(s[0]) | static_cast<uint32_t>(s[1]) << 8 |
+                         static_cast<uint32_t>(s[2]) << 16 | static_cast<uint32_t>(s[3]) << 24;
+    if (!used.insert(key).second) continue;
+    for (int pt = 0; pt < 4; ++pt) {
+      clear();
+      for (int j = 0; j < 4; ++j) setb(kPat[pt][j] == 'X' ? X : Y, s[j]);
+      for (int r = s[0] + 1; r < s[1]; ++r) setb(Z, r);
+      for (int r = s[2] + 1; r < s[3]; ++r) setb(Z, r);
+      emit(draw());
+    }
+  }
+  return count;
+}
+
+void synth_near_hf_samples(int n, int n_e, int64_t n_unq, uint64_t seed, uint64_t* keys) {
+  if (n < 2 || n > 64 * kMaxWords) throw std::invalid_argument("synth: qubit count out of range");
+  if (n_e < 1 || n_e >= n) throw std::invalid_argument("synth: electron count out of range");
+  const int W = (n + 63) / 64;
+  Rng rng(seed);
+  std::unordered_set<WordsN, WordsNHash> seen;
+  seen.reserve(static_cast<size_t>(n_unq) * 2);
+  WordsN hf{};
+  for (int i = 0; i < n_e; ++i) hf[i / 64] |= uint64_t{1} << (i % 64);
+  int64_t out = 0;
+  auto push = [&](const WordsN& v) {
+    if (!seen.insert(v).second) return;
+    for (int w = 0; w < W; ++w) keys[out * W + w] = v[w];
+    ++out;
+  };
+  push(hf);
+  // sites of spin s are s, s+2, ...; moves keep the per-spin occupation
+  const int n_sp[2] = {(n + 1) / 2, n / 2};
+  int n_occ[2] = {(n_e + 1) / 2, n_e / 2};
+  bool movable[2];
+  for (int s = 0; s < 2; ++s) movable[s] = n_occ[s] > 0 && n_occ[s] < n_sp[s];
+  if (!movable[0] && !movable[1]) throw std::invalid_argument("synth: no same-spin move exists");
+  auto bit = [](const WordsN& v, int i) { return (v[i / 64] >> (i % 64)) & 1; };
+  const int64_t max_draws = 1000 * n_unq + 100000;
+  for (int64_t draw = 0; out < n_unq; ++draw) {
+    if (draw > max_draws) throw std::invalid_argument("synth: sample space too small for the requested count");
+    WordsN v = hf;
+    int k = 1;
+    while (rng.uniform() > 0.6) ++k;  // k = 1 + Geometric(0.6)
+    for (int m = 0; m < k; ++m) {
+      int spin = static_cast<int>(rng.bits() & 1);
+      if (!movable[spin]) spin ^= 1;
+      int o, e;
+      do o = 2 * static_cast<int>(rng.below(n_sp[spin])) + spin; while (!bit(v, o));
+      do e = 2 * static_cast<int>(rng.below(n_sp[spin])) + spin; while (bit(v, e));
+      v[o / 64] ^= uint64_t{1} << (o % 64);
+      v[e / 64] ^= uint64_t{1} << (e % 64);
+    }
+    push(v);
+  }
+}
+
+}  // namespace qvmc_b200

@@ -1,0 +1,75 @@
+// Host-side (CPU, setup-time) pieces of libqvmc_cuda: the grouped
+// HamiltonianIndex, the device-layout planner and the synthetic generators.
+// Nothing here runs per sample; the per-sample work is in qvmc_cuda.cu.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace qvmc_b200 {
+
+constexpr int kMaxWords = 4;        // 256 qubits, BasisVector::kMaxBits (basis_vector.hpp:29)
+constexpr int kMaxMinority = 32;    // sector lists are used when min(n_e, N - n_e) <= 32
+
+// HamiltonianIndex (proj/include/qvmc/hamiltonian.hpp:41-107) as flat arrays.
+struct HostIndex {
+  int n_qubits = 0;
+  int n_words = 0;
+  std::vector<uint64_t> xy;       // [n_xy][n_words], first-occurrence order
+  std::vector<uint64_t> offsets;  // [n_xy+1]
+  std::vector<double> coeff;      // [n_terms], grouped
+  std::vector<uint64_t> x, y, z;  // [n_terms][n_words], merged strings
+  std::vector<uint64_t> yz;       // [n_terms][n_words]
+  std::vector<uint8_t> y_weight;  // [n_terms]
+  int64_t diag = -1;
+
+  uint32_t n_xy() const { return static_cast<uint32_t>(offsets.empty() ? 0 : offsets.size() - 1); }
+  uint64_t n_terms() const { return coeff.size(); }
+};
+
+// HamiltonianIndex::from_terms (hamiltonian.cpp:63-117). Throws
+// std::invalid_argument on malformed masks.
+HostIndex index_from_terms(int n_qubits, int n_words, int64_t n_raw, const double* coeff, const uint64_t* xw,
+                           const uint64_t* yw, const uint64_t* zw);
+
+// Random 64-bit code per qubit; the linear key hash is the XOR of the codes
+// of the set bits (so hash(x ^ m) = hash(x) ^ hash(m)).
+const uint64_t* qubit_codes();  // [256]
+uint64_t linear_hash(const uint64_t* words, int n_words);
+
+// Everything the kernels need besides the raw index, planned on the host.
+struct DevicePlan {
+  std::vector<uint64_t> xy_hash;    // [n_xy]
+  std::vector<uint32_t> offsets32;  // [n_xy+1]
+  std::vector<uint8_t> xy_weight;   // [n_xy] popcount(xy) = excitation class
+  // full scan (generic mode): every non-diagonal group
+  std::vector<uint64_t> gen_hash;
+  std::vector<uint32_t> gen_g;
+  // particle-sector lists: list p (< N) holds weight-2 masks containing p;
+  // list N + pair(p,q) holds weight-4 masks containing p and q.
+  std::vector<uint32_t> lst_off;
+  std::vector<uint64_t> lst_hash;
+  std::vector<uint32_t> lst_g;
+  std::vector<uint32_t> res_g;      // even weight >= 6
+  // diagonal group as a quadratic form in the occupations
+  bool diag_quad = false;
+  double diag_A[2] = {0.0, 0.0};    // [side] side 1 = occupied minority, 0 = holes
+  std::vector<double> diag_b;       // [2][N]
+  std::vector<double> diag_K;       // [N][N]
+  std::vector<uint32_t> diag_other; // diagonal terms with |z| >= 3
+  std::vector<uint64_t> hash_bytes; // [n_words*8][256]
+};
+
+DevicePlan plan_device(const HostIndex& h);
+
+inline uint32_t pair_index(int p, int q, int n) {  // p < q
+  return static_cast<uint32_t>(p * n - p * (p + 1) / 2 + (q - p - 1));
+}
+
+// Synthetic generators.
+int64_t synth_jw_hamiltonian(int n_qubits, int64_t n_target, uint64_t seed, double* coeff, uint64_t* xw,
+                             uint64_t* yw, uint64_t* zw);
+void synth_near_hf_samples(int n_qubits, int n_electrons, int64_t n_unq, uint64_t seed, uint64_t* keys);
+
+}  // namespace qvmc_b200

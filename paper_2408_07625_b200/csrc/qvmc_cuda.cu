@@ -1,0 +1,882 @@
+// libqvmc_cuda: C ABI (include/qvmc_cuda.h) over the sm_100a kernels in
+// qvmc_kernels.cuh. Host code here only validates, sizes workspaces, copies
+// and launches; there is no CPU compute path for the per-sample work.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "host_index.h"
+#include "qvmc_cuda.h"
+#include "qvmc_kernels.cuh"
+
+using namespace qvmc_b200;
+
+namespace {
+
+thread_local std::string g_error;
+std::atomic<uint64_t> g_launches{0};
+
+struct Failure {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Failure{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(QVMC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void ck_launch(const char* what) {
+  ++g_launches;
+  ck(cudaGetLastError(), what);
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return QVMC_OK;
+  } catch (const Failure& e) {
+    g_error = e.msg;
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return QVMC_ERR_INVALID_ARGUMENT;
+  } catch (const std::bad_alloc&) {
+    g_error = "host allocation failed";
+    return QVMC_ERR_RUNTIME;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return QVMC_ERR_RUNTIME;
+  }
+}
+
+// restores the caller's current device on scope exit
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    ck(cudaGetDevice(&prev), "cudaGetDevice");
+    if (prev != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// grow-only device buffer
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t want) {
+    if (want <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    ck(cudaMalloc(&p, want), "cudaMalloc");
+    bytes = want;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+template <typename T>
+void upload(DBuf& b, const std::vector<T>& v) {
+  b.ensure(std::max<size_t>(v.size() * sizeof(T), 16));
+  if (!v.empty()) ck(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+}
+
+}  // namespace
+
+struct qvmc_index_s {
+  HostIndex idx;
+};
+
+struct qvmc_ham_s {
+  int device = 0;
+  int n = 0, W = 0;
+  uint32_t n_xy = 0;
+  int64_t diag = -1;
+  uint64_t n_terms = 0;
+  int sms = 148;
+  cudaStream_t own = nullptr, stream = nullptr;
+  // Hamiltonian
+  DBuf xy, xy_hash, goff, coeff, yz, yw, xyw, gen_hash, gen_g, lst_off, lst_hash, lst_g, res_g, diag_b, diag_K,
+      diag_other, hash_bytes;
+  HamView view{};
+  // workspace
+  DBuf tab, ctl, keys, la, ph, lp, eloc, partials, moments, weights;
+  DBuf counts, row_off, xp_a, g_a, xp_b, g_b, entries, cub_tmp, in_entries, out_h, out_class;
+  uint64_t tab_buckets = 0;
+  uint64_t n_pairs = 0;
+  int64_t pairs_rows = 0;
+  qvmc_stats last{};
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // fused-call stage timing
+  bool timed = false;
+};
+
+namespace {
+
+constexpr int kCtlInts = 16;  // int err, pad, popc_mm[2]; u64 row_next @4, stats[2] @6
+
+Ctl ctl_view(qvmc_ham_s* h) {
+  Ctl c;
+  int* base = h->ctl.as<int>();
+  c.err = base;
+  c.popc_mm = base + 2;
+  c.row_next = reinterpret_cast<unsigned long long*>(base + 4);
+  c.stats = reinterpret_cast<unsigned long long*>(base + 6);
+  return c;
+}
+
+void check_handle(qvmc_ham_s* h) {
+  if (!h) fail(QVMC_ERR_INVALID_ARGUMENT, "null qvmc handle");
+}
+
+int grid_for(qvmc_ham_s* h, int per_sm) { return std::max(1, h->sms * std::max(1, per_sm)); }
+
+// ------------------------------------------------------------- small kernels
+
+__global__ void k_fill_u64(uint64_t* p, uint64_t n, uint64_t v) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// local_energies from canonical pairs (energy.cpp:13-48): one warp per row,
+// row run located by binary search on x.
+template <int W>
+__global__ void __launch_bounds__(kThreads)
+    k_pairs_eloc(HamView H, const uint64_t* __restrict__ keys, const double* __restrict__ la,
+                 const double* __restrict__ ph, int64_t n, const uint32_t* __restrict__ e3, uint64_t n_pairs,
+                 double2* out, int* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += n_warps) {
+    const double la_i = la[i];
+    if (isinf(la_i)) {
+      if (lane == 0) {
+        atomicOr(err, kErrZeroAmp);
+        out[i] = make_double2(CUDART_NAN, CUDART_NAN);
+      }
+      continue;
+    }
+    const double ph_i = ph[i];
+    // [lo, hi) = entries with x == i
+    uint64_t lo = 0, hi = n_pairs;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (e3[3 * mid] < i) lo = mid + 1; else hi = mid;
+    }
+    uint64_t end = lo, top = n_pairs;
+    while (end < top) {
+      const uint64_t mid = (end + top) >> 1;
+      if (e3[3 * mid] <= i) end = mid + 1; else top = mid;
+    }
+    double acc_re = 0.0, acc_im = 0.0;
+    for (uint64_t e = lo + lane; e < end; e += 32) {
+      const uint32_t j = e3[3 * e + 1], g = e3[3 * e + 2];
+      if (j >= n || g >= H.n_xy) {
+        atomicOr(err, kErrBadPair);
+        continue;
+      }
+      uint64_t xp[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) xp[w] = keys[(int64_t)j * W + w];
+      double hr, hi2;
+      group_element<W>(H, xp, g, hr, hi2);
+      const double a = exp(la[j] - la_i);
+      double s, c;
+      sincos(ph[j] - ph_i, &s, &c);
+      hr *= a;
+      hi2 *= a;
+      acc_re += hr * c - hi2 * s;
+      acc_im += hr * s + hi2 * c;
+    }
+    acc_re = warp_sum(acc_re);
+    acc_im = warp_sum(acc_im);
+    if (lane == 0) out[i] = make_double2(acc_re, acc_im);
+  }
+}
+
+__global__ void k_check_sorted(const uint32_t* e3, uint64_t n_pairs, int64_t n, int* err) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n_pairs;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    if (e3[3 * e] >= n || (e > 0 && e3[3 * e] < e3[3 * (e - 1)])) atomicOr(err, kErrBadPair);
+  }
+}
+
+// per-pair H_{x x'} in reference order, plus the excitation class
+template <int W>
+__global__ void __launch_bounds__(kThreads)
+    k_pair_elements(HamView H, const uint64_t* __restrict__ keys, int64_t n, const uint32_t* __restrict__ e3,
+                    uint64_t n_pairs, double2* out_h, uint8_t* out_class, int* err) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n_pairs;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = e3[3 * e], j = e3[3 * e + 1], g = e3[3 * e + 2];
+    if (x >= n || j >= n || g >= H.n_xy) {
+      atomicOr(err, kErrBadPair);
+      continue;
+    }
+    uint64_t xp[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) xp[w] = keys[(int64_t)j * W + w];
+    double re, im;
+    group_element<W>(H, xp, g, re, im);
+    out_h[e] = make_double2(re, im);
+    if (out_class) out_class[e] = H.xyw[g];
+  }
+}
+
+// moments (sum w Re E, sum w Im E, sum w^2, sum w, sum w |E|^2) with a
+// fixed grid and a fixed reduction tree: deterministic for a given n.
+constexpr int kMomentBlocks = 296;
+
+__global__ void __launch_bounds__(kThreads)
+    k_moments_partial(const double* __restrict__ lp, double log_norm, const double2* __restrict__ eloc, int64_t n,
+                      double* partial, double* weights) {
+  double m[5] = {0, 0, 0, 0, 0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double w = exp(lp[i] - log_norm);
+    if (weights) weights[i] = w;
+    const double2 e = eloc[i];
+    m[0] += w * e.x;
+    m[1] += w * e.y;
+    m[2] += w * w;
+    m[3] += w;
+    m[4] += w * (e.x * e.x + e.y * e.y);
+  }
+  __shared__ double sm[kWarps][5];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) m[k] = warp_sum(m[k]);
+  if (lane == 0)
+    for (int k = 0; k < 5; ++k) sm[wid][k] = m[k];
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    double s = 0;
+    for (int w = 0; w < kWarps; ++w) s += sm[w][threadIdx.x];
+    partial[blockIdx.x * 5 + threadIdx.x] = s;
+  }
+}
+
+__global__ void k_moments_final(const double* partial, int n_blocks, double* out) {
+  if (threadIdx.x < 5) {
+    double s = 0;
+    for (int b = 0; b < n_blocks; ++b) s += partial[b * 5 + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+}
+
+// ---------------------------------------------------------------- helpers
+
+template <int W>
+void launch_table_build(qvmc_ham_s* h, const uint64_t* keys, int64_t n) {
+  // buckets of 4 at load <= 1/4: next power of two >= n buckets
+  uint64_t nb = 1;
+  while (nb < static_cast<uint64_t>(n)) nb <<= 1;
+  nb = std::max<uint64_t>(nb, 64);
+  h->tab.ensure(nb * 4 * sizeof(uint64_t));
+  h->tab_buckets = nb;
+  const int fill_grid = grid_for(h, 4);
+  k_fill_u64<<<fill_grid, kThreads, 0, h->stream>>>(h->tab.as<uint64_t>(), nb * 4, kEmpty);
+  ck_launch("fill table");
+  ck(cudaMemsetAsync(static_cast<int*>(h->ctl.p) + 2, 0, 2 * sizeof(int), h->stream), "memset popcount range");
+  TableView T{h->tab.as<uint64_t>(), nb - 1};
+  const int grid = static_cast<int>(std::min<int64_t>((n + kThreads - 1) / kThreads + 1, grid_for(h, 8)));
+  k_table_build<W><<<grid, kThreads, 0, h->stream>>>(keys, n, h->view.hash_bytes, T, ctl_view(h));
+  ck_launch("table build");
+}
+
+template <int W, int MODE>
+void launch_rows(qvmc_ham_s* h, const uint64_t* keys, int64_t r0, int64_t r1, const RowOut& O) {
+  ck(cudaMemsetAsync(static_cast<int*>(h->ctl.p) + 4, 0, 2 * sizeof(int), h->stream), "memset row counter");
+  int per_sm = 0;
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows<W, MODE>, kThreads, 0), "occupancy");
+  const int64_t warps_needed = r1 - r0;
+  const int64_t blocks_needed = (warps_needed + kWarps - 1) / kWarps;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_needed, grid_for(h, per_sm))));
+  TableView T{h->tab.as<uint64_t>(), h->tab_buckets - 1};
+  if (r1 > r0) {
+    k_rows<W, MODE><<<grid, kThreads, 0, h->stream>>>(h->view, T, keys, r0, r1, ctl_view(h), O);
+    ck_launch("row kernel");
+  }
+}
+
+int read_err_and_reset(qvmc_ham_s* h) {
+  int err = 0;
+  ck(cudaMemcpyAsync(&err, h->ctl.p, sizeof(int), cudaMemcpyDeviceToHost, h->stream), "read err");
+  ck(cudaStreamSynchronize(h->stream), "sync");
+  if (err) ck(cudaMemsetAsync(h->ctl.p, 0, sizeof(int), h->stream), "reset err");
+  return err;
+}
+
+void raise_device_err(int err) {
+  if (err & kErrDuplicate) fail(QVMC_ERR_INVALID_ARGUMENT, "sample set contains duplicate basis vectors");
+  if (err & kErrBadPair) fail(QVMC_ERR_INVALID_ARGUMENT, "pair entry out of range or not in canonical order");
+  if (err & kErrZeroAmp) fail(QVMC_ERR_LOGIC, "local_energies: sampled state has zero amplitude");
+}
+
+void finish(qvmc_ham_s* h) {
+  const int err = read_err_and_reset(h);
+  if (err) raise_device_err(err);
+}
+
+// stage a host array into a workspace buffer (or pass a device pointer through)
+template <typename T>
+const T* stage(qvmc_ham_s* h, DBuf& buf, const T* src, size_t count, int mem) {
+  if (mem == QVMC_MEM_DEVICE) return src;
+  buf.ensure(std::max<size_t>(count * sizeof(T), 16));
+  if (count) ck(cudaMemcpyAsync(buf.p, src, count * sizeof(T), cudaMemcpyHostToDevice, h->stream), "H2D");
+  return buf.as<T>();
+}
+
+void check_mem(int mem) {
+  if (mem != QVMC_MEM_HOST && mem != QVMC_MEM_DEVICE) fail(QVMC_ERR_INVALID_ARGUMENT, "unknown memory kind");
+}
+
+#define DISPATCH_W(W_, ...)                                       \
+  switch (W_) {                                                   \
+    case 1: { constexpr int WW = 1; __VA_ARGS__; break; }         \
+    case 2: { constexpr int WW = 2; __VA_ARGS__; break; }         \
+    case 3: { constexpr int WW = 3; __VA_ARGS__; break; }         \
+    case 4: { constexpr int WW = 4; __VA_ARGS__; break; }         \
+    default: fail(QVMC_ERR_INVALID_ARGUMENT, "unsupported word count"); \
+  }
+
+void compute_moments(qvmc_ham_s* h, const double* lp, double log_norm, const double2* eloc, int64_t n,
+                     double* out_dev, double* weights_dev) {
+  h->partials.ensure(kMomentBlocks * 5 * sizeof(double));
+  k_moments_partial<<<kMomentBlocks, kThreads, 0, h->stream>>>(lp, log_norm, eloc, n, h->partials.as<double>(),
+                                                               weights_dev);
+  ck_launch("moments partial");
+  k_moments_final<<<1, 32, 0, h->stream>>>(h->partials.as<double>(), kMomentBlocks, out_dev);
+  ck_launch("moments final");
+}
+
+void record_stats(qvmc_ham_s* h, int64_t rows) {
+  h->timed = false;
+  h->last = qvmc_stats{};
+  h->last.rows = static_cast<uint64_t>(rows);
+  h->last.terms_equivalent = static_cast<uint64_t>(rows) * h->n_xy;
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+
+extern "C" {
+
+const char* qvmc_cuda_last_error(void) { return g_error.c_str(); }
+uint64_t qvmc_cuda_launch_count(void) { return g_launches.load(); }
+
+int qvmc_index_build(int n_qubits, int n_words, int64_t n_raw, const double* coeff, const uint64_t* x_words,
+                     const uint64_t* y_words, const uint64_t* z_words, qvmc_index_t* out) {
+  return guarded([&] {
+    if (!out || (n_raw > 0 && (!coeff || !x_words || !y_words || !z_words)))
+      fail(QVMC_ERR_INVALID_ARGUMENT, "null argument");
+    auto box = std::make_unique<qvmc_index_s>();
+    box->idx = index_from_terms(n_qubits, n_words, n_raw, coeff, x_words, y_words, z_words);
+    *out = box.release();
+  });
+}
+
+int qvmc_index_info(qvmc_index_t idx, int* n_qubits, uint64_t* n_terms, uint32_t* n_xy, int64_t* diag) {
+  return guarded([&] {
+    if (!idx) fail(QVMC_ERR_INVALID_ARGUMENT, "null index");
+    if (n_qubits) *n_qubits = idx->idx.n_qubits;
+    if (n_terms) *n_terms = idx->idx.n_terms();
+    if (n_xy) *n_xy = idx->idx.n_xy();
+    if (diag) *diag = idx->idx.diag;
+  });
+}
+
+int qvmc_index_export(qvmc_index_t idx, uint64_t* xy_words, uint64_t* group_offsets, double* coeff,
+                      uint64_t* yz_words, uint8_t* y_weight, uint64_t* x_words, uint64_t* y_words,
+                      uint64_t* z_words) {
+  return guarded([&] {
+    if (!idx) fail(QVMC_ERR_INVALID_ARGUMENT, "null index");
+    const HostIndex& h = idx->idx;
+    auto cp = [](auto* dst, const auto& v) {
+      if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    };
+    cp(xy_words, h.xy);
+    cp(group_offsets, h.offsets);
+    cp(coeff, h.coeff);
+    cp(yz_words, h.yz);
+    cp(y_weight, h.y_weight);
+    cp(x_words, h.x);
+    cp(y_words, h.y);
+    cp(z_words, h.z);
+  });
+}
+
+void qvmc_index_destroy(qvmc_index_t idx) { delete idx; }
+
+int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_t* xy_words,
+                         const uint64_t* group_offsets, uint64_t n_terms, const double* coeff,
+                         const uint64_t* yz_words, const uint8_t* y_weight, int64_t diag_xy, int device,
+                         qvmc_ham_t* out) {
+  return guarded([&] {
+    if (!out) fail(QVMC_ERR_INVALID_ARGUMENT, "null output handle");
+    if (n_qubits < 1 || n_qubits > 256 || n_words != (n_qubits + 63) / 64)
+      fail(QVMC_ERR_INVALID_ARGUMENT, "qubit count out of range or n_words != ceil(N/64)");
+    if (n_xy > 0 && (!xy_words || !group_offsets)) fail(QVMC_ERR_INVALID_ARGUMENT, "null xy arrays");
+    if (n_terms > 0 && (!coeff || !yz_words || !y_weight)) fail(QVMC_ERR_INVALID_ARGUMENT, "null term arrays");
+    if (diag_xy >= static_cast<int64_t>(n_xy)) fail(QVMC_ERR_INVALID_ARGUMENT, "diag_xy out of range");
+    HostIndex hi;
+    hi.n_qubits = n_qubits;
+    hi.n_words = n_words;
+    hi.xy.assign(xy_words, xy_words + static_cast<size_t>(n_xy) * n_words);
+    hi.offsets.assign(group_offsets, group_offsets + n_xy + 1);
+    if (n_xy == 0) hi.offsets.assign(1, 0);
+    if (hi.offsets.back() != n_terms || hi.offsets.front() != 0)
+      fail(QVMC_ERR_INVALID_ARGUMENT, "group offsets do not span the terms");
+    for (uint32_t g = 0; g < n_xy; ++g)
+      if (hi.offsets[g] > hi.offsets[g + 1]) fail(QVMC_ERR_INVALID_ARGUMENT, "group offsets not monotone");
+    hi.coeff.assign(coeff, coeff + n_terms);
+    hi.yz.assign(yz_words, yz_words + n_terms * n_words);
+    hi.y_weight.assign(y_weight, y_weight + n_terms);
+    hi.diag = diag_xy;
+
+    int n_dev = 0;
+    if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0) fail(QVMC_ERR_NO_DEVICE, "no CUDA device visible");
+    if (device < 0 || device >= n_dev) fail(QVMC_ERR_INVALID_ARGUMENT, "device ordinal out of range");
+    DeviceGuard dg(device);
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10) fail(QVMC_ERR_NO_DEVICE, "libqvmc_cuda is built for sm_100a (B200) only");
+
+    const DevicePlan p = plan_device(hi);
+    auto h = std::make_unique<qvmc_ham_s>();
+    h->device = device;
+    h->n = n_qubits;
+    h->W = n_words;
+    h->n_xy = n_xy;
+    h->diag = diag_xy;
+    h->n_terms = n_terms;
+    h->sms = prop.multiProcessorCount;
+    ck(cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking), "stream create");
+    h->stream = h->own;
+    for (auto& e : h->ev) ck(cudaEventCreate(&e), "event create");
+    upload(h->xy, hi.xy);
+    upload(h->xy_hash, p.xy_hash);
+    upload(h->goff, p.offsets32);
+    upload(h->coeff, hi.coeff);
+    upload(h->yz, hi.yz);
+    upload(h->yw, hi.y_weight);
+    upload(h->xyw, p.xy_weight);
+    upload(h->gen_hash, p.gen_hash);
+    upload(h->gen_g, p.gen_g);
+    upload(h->lst_off, p.lst_off);
+    upload(h->lst_hash, p.lst_hash);
+    upload(h->lst_g, p.lst_g);
+    upload(h->res_g, p.res_g);
+    upload(h->diag_b, p.diag_b);
+    upload(h->diag_K, p.diag_K);
+    upload(h->diag_other, p.diag_other);
+    upload(h->hash_bytes, p.hash_bytes);
+    h->ctl.ensure(kCtlInts * sizeof(int) * 2);
+    ck(cudaMemset(h->ctl.p, 0, kCtlInts * sizeof(int) * 2), "memset ctl");
+
+    HamView& v = h->view;
+    v.n = n_qubits;
+    v.n_xy = n_xy;
+    v.diag = static_cast<int32_t>(diag_xy);
+    v.xy = h->xy.as<uint64_t>();
+    v.xy_hash = h->xy_hash.as<uint64_t>();
+    v.goff = h->goff.as<uint32_t>();
+    v.coeff = h->coeff.as<double>();
+    v.yz = h->yz.as<uint64_t>();
+    v.yw = h->yw.as<uint8_t>();
+    v.xyw = h->xyw.as<uint8_t>();
+    v.gen_hash = h->gen_hash.as<uint64_t>();
+    v.gen_g = h->gen_g.as<uint32_t>();
+    v.n_gen = static_cast<uint32_t>(p.gen_g.size());
+    v.lst_off = h->lst_off.as<uint32_t>();
+    v.lst_hash = h->lst_hash.as<uint64_t>();
+    v.lst_g = h->lst_g.as<uint32_t>();
+    v.res_g = h->res_g.as<uint32_t>();
+    v.n_res = static_cast<uint32_t>(p.res_g.size());
+    v.diag_quad = p.diag_quad ? 1 : 0;
+    v.diag_A0 = p.diag_A[0];
+    v.diag_A1 = p.diag_A[1];
+    v.diag_b = h->diag_b.as<double>();
+    v.diag_K = h->diag_K.as<double>();
+    v.diag_other = h->diag_other.as<uint32_t>();
+    v.n_diag_other = static_cast<uint32_t>(p.diag_other.size());
+    v.hash_bytes = h->hash_bytes.as<uint64_t>();
+    ck(cudaDeviceSynchronize(), "upload sync");
+    *out = h.release();
+  });
+}
+
+int qvmc_cuda_ham_create_from_index(qvmc_index_t idx, int device, qvmc_ham_t* out) {
+  if (!idx) {
+    g_error = "null index";
+    return QVMC_ERR_INVALID_ARGUMENT;
+  }
+  const HostIndex& h = idx->idx;
+  return qvmc_cuda_ham_create(h.n_qubits, h.n_words, h.n_xy(), h.xy.data(), h.offsets.data(), h.n_terms(),
+                              h.coeff.data(), h.yz.data(), h.y_weight.data(), h.diag, device, out);
+}
+
+int qvmc_cuda_ham_destroy(qvmc_ham_t h) {
+  return guarded([&] {
+    if (!h) return;
+    DeviceGuard dg(h->device);
+    if (h->own) {
+      cudaStreamSynchronize(h->own);
+      cudaStreamDestroy(h->own);
+    }
+    for (auto& e : h->ev)
+      if (e) cudaEventDestroy(e);
+    delete h;
+  });
+}
+
+int qvmc_cuda_set_stream(qvmc_ham_t h, void* stream) {
+  return guarded([&] {
+    check_handle(h);
+    h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own;
+  });
+}
+
+int qvmc_cuda_synchronize(qvmc_ham_t h) {
+  return guarded([&] {
+    check_handle(h);
+    DeviceGuard dg(h->device);
+    finish(h);
+  });
+}
+
+int qvmc_cuda_last_stats(qvmc_ham_t h, qvmc_stats* out) {
+  return guarded([&] {
+    check_handle(h);
+    if (!out) fail(QVMC_ERR_INVALID_ARGUMENT, "null stats");
+    DeviceGuard dg(h->device);
+    unsigned long long st[2];
+    ck(cudaMemcpyAsync(st, static_cast<int*>(h->ctl.p) + 6, sizeof(st), cudaMemcpyDeviceToHost, h->stream), "stats");
+    int mm[2];
+    ck(cudaMemcpyAsync(mm, static_cast<int*>(h->ctl.p) + 2, sizeof(mm), cudaMemcpyDeviceToHost, h->stream), "mm");
+    ck(cudaStreamSynchronize(h->stream), "sync");
+    *out = h->last;
+    if (h->timed) {
+      ck(cudaEventElapsedTime(&out->table_ms, h->ev[0], h->ev[1]), "elapsed");
+      ck(cudaEventElapsedTime(&out->rows_ms, h->ev[1], h->ev[2]), "elapsed");
+      ck(cudaEventElapsedTime(&out->moments_ms, h->ev[2], h->ev[3]), "elapsed");
+    }
+    out->candidates = st[0];
+    out->pairs = st[1];
+    const int pmax = mm[0], pmin = 1024 - mm[1];
+    const int side = (pmin <= h->n - pmin) ? 1 : 0;
+    const int s = side ? pmin : h->n - pmin;
+    out->sector_mode = (pmin == pmax && s <= kMaxMinority) ? 1 : 0;
+    out->sector_side = side;
+    out->minority_count = s;
+  });
+}
+
+int qvmc_cuda_pairs(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, int mem, int backend, int auto_threshold,
+                    uint64_t* n_pairs, uint64_t* ops, int* backend_used) {
+  return guarded([&] {
+    check_handle(h);
+    check_mem(mem);
+    if (n_unq < 0 || n_unq >= 0xFFFFFFFFll) fail(QVMC_ERR_INVALID_ARGUMENT, "n_unq out of range");
+    if (n_unq > 0 && !keys) fail(QVMC_ERR_INVALID_ARGUMENT, "null keys");
+    if (backend < QVMC_BACKEND_TERMS || backend > QVMC_BACKEND_AUTO)
+      fail(QVMC_ERR_INVALID_ARGUMENT, "unknown coupling backend");
+    DeviceGuard dg(h->device);
+    int used = backend;
+    if (backend == QVMC_BACKEND_AUTO)  // coupling.cpp:157-161
+      used = n_unq < auto_threshold ? QVMC_BACKEND_BATCH : QVMC_BACKEND_TRIE;
+    const int W = h->W;
+    const uint64_t* dkeys = stage(h, h->keys, keys, static_cast<size_t>(n_unq) * W, mem);
+    record_stats(h, n_unq);
+    h->pairs_rows = n_unq;
+    h->n_pairs = 0;
+    ck(cudaMemsetAsync(static_cast<int*>(h->ctl.p) + 6, 0, 4 * sizeof(int), h->stream), "memset stats");
+    uint64_t total = 0;
+    if (n_unq > 0) {
+      DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
+      {
+        const int err = read_err_and_reset(h);
+        if (err) raise_device_err(err);
+      }
+      h->counts.ensure((n_unq + 1) * sizeof(uint32_t));
+      h->row_off.ensure((n_unq + 1) * sizeof(uint64_t));
+      RowOut O{};
+      O.counts = h->counts.as<uint32_t>();
+      DISPATCH_W(W, (launch_rows<WW, kModeCount>(h, dkeys, 0, n_unq, O)));
+      // exclusive scan of the per-row counts (as u64)
+      ck(cudaMemsetAsync(h->counts.as<uint32_t>() + n_unq, 0, sizeof(uint32_t), h->stream), "memset");
+      size_t tmp = 0;
+      uint64_t* roff = h->row_off.as<uint64_t>();
+      auto in_it = h->counts.as<uint32_t>();
+      ck(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in_it, roff, n_unq + 1, h->stream), "scan size");
+      h->cub_tmp.ensure(tmp + 16);
+      ck(cub::DeviceScan::ExclusiveSum(h->cub_tmp.p, tmp, in_it, roff, n_unq + 1, h->stream), "scan");
+      ++g_launches;
+      ck(cudaMemcpyAsync(&total, roff + n_unq, sizeof(uint64_t), cudaMemcpyDeviceToHost, h->stream), "D2H total");
+      ck(cudaStreamSynchronize(h->stream), "sync");
+      if (total >= (1ull << 31)) fail(QVMC_ERR_RUNTIME, "coupled-pair list exceeds 2^31 entries");
+      h->xp_a.ensure(total * 4 + 16);
+      h->g_a.ensure(total * 4 + 16);
+      h->xp_b.ensure(total * 4 + 16);
+      h->g_b.ensure(total * 4 + 16);
+      O = RowOut{};
+      O.row_off = roff;
+      O.xp_out = h->xp_a.as<uint32_t>();
+      O.g_out = h->g_a.as<uint32_t>();
+      DISPATCH_W(W, (launch_rows<WW, kModeEmit>(h, dkeys, 0, n_unq, O)));
+      // canonical order inside each row: by x' (coupling.cpp:49-52)
+      tmp = 0;
+      ck(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tmp, h->xp_a.as<uint32_t>(), h->xp_b.as<uint32_t>(),
+                                                   h->g_a.as<uint32_t>(), h->g_b.as<uint32_t>(),
+                                                   static_cast<int>(total), static_cast<int>(n_unq), roff, roff + 1,
+                                                   h->stream),
+         "segsort size");
+      h->cub_tmp.ensure(tmp + 16);
+      ck(cub::DeviceSegmentedSort::StableSortPairs(h->cub_tmp.p, tmp, h->xp_a.as<uint32_t>(), h->xp_b.as<uint32_t>(),
+                                                   h->g_a.as<uint32_t>(), h->g_b.as<uint32_t>(),
+                                                   static_cast<int>(total), static_cast<int>(n_unq), roff, roff + 1,
+                                                   h->stream),
+         "segsort");
+      ++g_launches;
+      const int err = read_err_and_reset(h);
+      if (err) raise_device_err(err);
+    }
+    h->n_pairs = total;
+    unsigned long long st[2] = {0, 0};
+    ck(cudaMemcpy(st, static_cast<int*>(h->ctl.p) + 6, sizeof(st), cudaMemcpyDeviceToHost), "stats");
+    const uint64_t probed = st[0] + (h->diag >= 0 ? static_cast<uint64_t>(n_unq) : 0);
+    const uint64_t n64 = static_cast<uint64_t>(n_unq);
+    if (n_pairs) *n_pairs = total;
+    if (ops)
+      *ops = used == QVMC_BACKEND_TERMS ? n64 * h->n_xy : used == QVMC_BACKEND_BATCH ? n64 * n64 : probed;
+    if (backend_used) *backend_used = used;
+  });
+}
+
+namespace {
+__global__ void k_pack_entries(const uint64_t* __restrict__ row_off, int64_t n, const uint32_t* __restrict__ xp,
+                               const uint32_t* __restrict__ g, uint32_t* out3) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (uint64_t e = row_off[i]; e < row_off[i + 1]; ++e) {
+      out3[3 * e] = static_cast<uint32_t>(i);
+      out3[3 * e + 1] = xp[e];
+      out3[3 * e + 2] = g[e];
+    }
+}
+}  // namespace
+
+int qvmc_cuda_pairs_fetch(qvmc_ham_t h, uint32_t* out_entries, int mem) {
+  return guarded([&] {
+    check_handle(h);
+    check_mem(mem);
+    if (h->n_pairs == 0) return;
+    if (!out_entries) fail(QVMC_ERR_INVALID_ARGUMENT, "null output");
+    DeviceGuard dg(h->device);
+    uint32_t* dst = out_entries;
+    if (mem == QVMC_MEM_HOST) {
+      h->entries.ensure(h->n_pairs * 12);
+      dst = h->entries.as<uint32_t>();
+    }
+    const int grid = static_cast<int>(std::min<int64_t>((h->pairs_rows + kThreads - 1) / kThreads, grid_for(h, 8)));
+    k_pack_entries<<<std::max(grid, 1), kThreads, 0, h->stream>>>(h->row_off.as<uint64_t>(), h->pairs_rows,
+                                                                  h->xp_b.as<uint32_t>(), h->g_b.as<uint32_t>(), dst);
+    ck_launch("pack entries");
+    if (mem == QVMC_MEM_HOST)
+      ck(cudaMemcpyAsync(out_entries, dst, h->n_pairs * 12, cudaMemcpyDeviceToHost, h->stream), "D2H entries");
+    ck(cudaStreamSynchronize(h->stream), "sync");
+  });
+}
+
+int qvmc_cuda_pair_elements(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, uint64_t n_pairs,
+                            const uint32_t* entries, double* out_h, uint8_t* out_class, int mem) {
+  return guarded([&] {
+    check_handle(h);
+    check_mem(mem);
+    if (n_unq < 0 || (n_unq > 0 && !keys) || (n_pairs > 0 && (!entries || !out_h)))
+      fail(QVMC_ERR_INVALID_ARGUMENT, "null or negative argument");
+    if (n_pairs == 0) return;
+    DeviceGuard dg(h->device);
+    const int W = h->W;
+    const uint64_t* dkeys = stage(h, h->keys, keys, static_cast<size_t>(n_unq) * W, mem);
+    const uint32_t* de = stage(h, h->in_entries, entries, n_pairs * 3, mem);
+    double2* dh = reinterpret_cast<double2*>(out_h);
+    uint8_t* dc = out_class;
+    if (mem == QVMC_MEM_HOST) {
+      h->out_h.ensure(n_pairs * 16);
+      dh = h->out_h.as<double2>();
+      dc = nullptr;
+      if (out_class) {
+        h->out_class.ensure(n_pairs + 16);
+        dc = h->out_class.as<uint8_t>();
+      }
+    }
+    const int grid = static_cast<int>(std::min<uint64_t>((n_pairs + kThreads - 1) / kThreads, grid_for(h, 8)));
+    DISPATCH_W(W, (k_pair_elements<WW><<<grid, kThreads, 0, h->stream>>>(h->view, dkeys, n_unq, de, n_pairs, dh, dc,
+                                                                       static_cast<int*>(h->ctl.p))));
+    ck_launch("pair elements");
+    if (mem == QVMC_MEM_HOST) {
+      ck(cudaMemcpyAsync(out_h, dh, n_pairs * 16, cudaMemcpyDeviceToHost, h->stream), "D2H h");
+      if (out_class) ck(cudaMemcpyAsync(out_class, dc, n_pairs, cudaMemcpyDeviceToHost, h->stream), "D2H class");
+    }
+    finish(h);
+  });
+}
+
+int qvmc_cuda_local_energies(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, const double* log_amp,
+                             const double* phase, uint64_t n_pairs, const uint32_t* entries, double* out_eloc,
+                             int mem) {
+  return guarded([&] {
+    check_handle(h);
+    check_mem(mem);
+    if (n_unq < 0 || (n_unq > 0 && (!keys || !log_amp || !phase || !out_eloc)) || (n_pairs > 0 && !entries))
+      fail(QVMC_ERR_INVALID_ARGUMENT, "null or negative argument");
+    if (n_unq == 0) return;
+    DeviceGuard dg(h->device);
+    const int W = h->W;
+    const uint64_t* dkeys = stage(h, h->keys, keys, static_cast<size_t>(n_unq) * W, mem);
+    const double* dla = stage(h, h->la, log_amp, n_unq, mem);
+    const double* dph = stage(h, h->ph, phase, n_unq, mem);
+    const uint32_t* de = stage(h, h->in_entries, entries, n_pairs * 3, mem);
+    double2* dout = reinterpret_cast<double2*>(out_eloc);
+    if (mem == QVMC_MEM_HOST) {
+      h->eloc.ensure(n_unq * 16);
+      dout = h->eloc.as<double2>();
+    }
+    int* err = static_cast<int*>(h->ctl.p);
+    if (n_pairs > 0) {
+      const int g1 = static_cast<int>(std::min<uint64_t>((n_pairs + kThreads - 1) / kThreads, grid_for(h, 8)));
+      k_check_sorted<<<g1, kThreads, 0, h->stream>>>(de, n_pairs, n_unq, err);
+      ck_launch("check pairs");
+    }
+    const int grid = static_cast<int>(std::min<int64_t>((n_unq + kWarps - 1) / kWarps, grid_for(h, 8)));
+    DISPATCH_W(W, (k_pairs_eloc<WW><<<grid, kThreads, 0, h->stream>>>(h->view, dkeys, dla, dph, n_unq, de, n_pairs,
+                                                                    dout, err)));
+    ck_launch("local energies");
+    if (mem == QVMC_MEM_HOST) {
+      ck(cudaMemcpyAsync(out_eloc, dout, n_unq * 16, cudaMemcpyDeviceToHost, h->stream), "D2H eloc");
+      finish(h);
+    }
+  });
+}
+
+int qvmc_cuda_energy_moments(qvmc_ham_t h, int64_t n, const double* log_prob, double log_norm, const double* eloc,
+                             double* out_moments, double* out_weights, int mem) {
+  return guarded([&] {
+    check_handle(h);
+    check_mem(mem);
+    if (n < 0 || (n > 0 && (!log_prob || !eloc)) || !out_moments) fail(QVMC_ERR_INVALID_ARGUMENT, "null argument");
+    DeviceGuard dg(h->device);
+    const double* dlp = stage(h, h->lp, log_prob, n, mem);
+    const double2* de = reinterpret_cast<const double2*>(stage(h, h->eloc, eloc, 2 * n, mem));
+    double* dm = out_moments;
+    double* dw = out_weights;
+    if (mem == QVMC_MEM_HOST) {
+      h->moments.ensure(8 * sizeof(double));
+      dm = h->moments.as<double>();
+      dw = nullptr;
+      if (out_weights) {
+        h->weights.ensure(n * 8 + 16);
+        dw = h->weights.as<double>();
+      }
+    }
+    compute_moments(h, dlp, log_norm, de, n, dm, dw);
+    if (mem == QVMC_MEM_HOST) {
+      ck(cudaMemcpyAsync(out_moments, dm, 5 * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "D2H moments");
+      if (out_weights && n)
+        ck(cudaMemcpyAsync(out_weights, dw, n * 8, cudaMemcpyDeviceToHost, h->stream), "D2H weights");
+      finish(h);
+    }
+  });
+}
+
+int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, const double* log_amp,
+                         const double* phase, const double* log_prob, double log_norm, int64_t row_begin,
+                         int64_t row_end, double* out_eloc, double* out_moments, int mem) {
+  return guarded([&] {
+    check_handle(h);
+    check_mem(mem);
+    if (n_unq < 0 || n_unq >= 0xFFFFFFFFll) fail(QVMC_ERR_INVALID_ARGUMENT, "n_unq out of range");
+    if (row_begin < 0 || row_end < row_begin || row_end > n_unq) fail(QVMC_ERR_INVALID_ARGUMENT, "bad row range");
+    if (n_unq > 0 && (!keys || !log_amp || !phase)) fail(QVMC_ERR_INVALID_ARGUMENT, "null sample arrays");
+    if (out_moments && row_end > row_begin && !log_prob) fail(QVMC_ERR_INVALID_ARGUMENT, "moments need log_prob");
+    DeviceGuard dg(h->device);
+    const int W = h->W;
+    const int64_t rows = row_end - row_begin;
+    const uint64_t* dkeys = stage(h, h->keys, keys, static_cast<size_t>(n_unq) * W, mem);
+    const double* dla = stage(h, h->la, log_amp, n_unq, mem);
+    const double* dph = stage(h, h->ph, phase, n_unq, mem);
+    const double* dlp = log_prob ? stage(h, h->lp, log_prob, n_unq, mem) : nullptr;
+    double2* deloc = reinterpret_cast<double2*>(out_eloc);
+    if (mem == QVMC_MEM_HOST || !out_eloc) {
+      h->eloc.ensure(std::max<int64_t>(rows, 1) * 16);
+      deloc = h->eloc.as<double2>();
+    }
+    record_stats(h, rows);
+    ck(cudaMemsetAsync(static_cast<int*>(h->ctl.p) + 6, 0, 4 * sizeof(int), h->stream), "memset stats");
+    ck(cudaEventRecord(h->ev[0], h->stream), "event");
+    if (n_unq > 0) DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
+    ck(cudaEventRecord(h->ev[1], h->stream), "event");
+    if (n_unq > 0) {
+      RowOut O{};
+      O.eloc = deloc;
+      O.la = dla;
+      O.ph = dph;
+      DISPATCH_W(W, (launch_rows<WW, kModeEloc>(h, dkeys, row_begin, row_end, O)));
+    }
+    ck(cudaEventRecord(h->ev[2], h->stream), "event");
+    double* dm = out_moments;
+    if (out_moments) {
+      if (mem == QVMC_MEM_HOST) {
+        h->moments.ensure(8 * sizeof(double));
+        dm = h->moments.as<double>();
+      }
+      compute_moments(h, dlp ? dlp + row_begin : nullptr, log_norm, deloc, rows, dm, nullptr);
+    }
+    ck(cudaEventRecord(h->ev[3], h->stream), "event");
+    h->timed = true;
+    if (mem == QVMC_MEM_HOST) {
+      if (out_eloc && rows)
+        ck(cudaMemcpyAsync(out_eloc, deloc, rows * 16, cudaMemcpyDeviceToHost, h->stream), "D2H eloc");
+      if (out_moments) ck(cudaMemcpyAsync(out_moments, dm, 5 * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "D2H");
+      finish(h);
+    }
+  });
+}
+
+int qvmc_synth_jw_hamiltonian(int n_qubits, int64_t n_terms_target, uint64_t seed, double* coeff, uint64_t* x_words,
+                              uint64_t* y_words, uint64_t* z_words, int64_t* n_out) {
+  return guarded([&] {
+    if (!coeff || !x_words || !y_words || !z_words || !n_out || n_terms_target < 0)
+      fail(QVMC_ERR_INVALID_ARGUMENT, "null or negative argument");
+    *n_out = synth_jw_hamiltonian(n_qubits, n_terms_target, seed, coeff, x_words, y_words, z_words);
+  });
+}
+
+int qvmc_synth_near_hf_samples(int n_qubits, int n_electrons, int64_t n_unq, uint64_t seed, uint64_t* keys) {
+  return guarded([&] {
+    if (!keys || n_unq < 0) fail(QVMC_ERR_INVALID_ARGUMENT, "null or negative argument");
+    synth_near_hf_samples(n_qubits, n_electrons, n_unq, seed, keys);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,111 @@
+"""Multi-GPU surrogate local energies: one process per GPU, rows sharded.
+
+SURVEY.md §8(e): every rank owns a contiguous shard of the unique samples
+(keys + log|psi| + phase + log p). The partner lookup needs the whole sample
+set, so the shards are all-gathered over NVLink (NCCL through
+torch.distributed), each rank evaluates E_loc for its own rows against the
+gathered set with the fused kernel, and the five fp64 energy moments are
+all-reduced. Per-rank row results never leave the rank unless the caller
+asks for them (``gather_locals``).
+
+The per-rank evaluation is ``qvmc_cuda_eloc_fused`` on device pointers; the
+``evaluate`` hook exists so the gather/offset/reduce plumbing can be tested
+with the gloo backend on CPU-only hosts.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Callable, List, Optional
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .hamiltonian import HamiltonianIndex
+
+
+@dataclass
+class Shard:
+    """This rank's rows of the sample set (torch tensors on this rank's device)."""
+    keys: torch.Tensor      # int64 viewed as uint64 words, [rows, n_words]
+    log_amps: torch.Tensor  # float64 [rows]
+    phases: torch.Tensor    # float64 [rows]
+    log_probs: torch.Tensor # float64 [rows]
+
+
+@dataclass
+class ShardResult:
+    locals: torch.Tensor    # complex128 [rows] (this rank's rows)
+    moments: torch.Tensor   # float64 [5], already all-reduced over ranks
+    row_begin: int
+    row_end: int
+    n_total: int
+
+    @property
+    def e_var(self) -> float:
+        return float(self.moments[0])
+
+
+def _gather_rows(t: torch.Tensor, counts: List[int], group) -> torch.Tensor:
+    """All-gather variable-length row blocks (padded to the largest shard)."""
+    world = len(counts)
+    m = max(counts)
+    pad = torch.zeros((m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    pad[: t.shape[0]] = t
+    out = torch.empty((world * m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    if all(c == m for c in counts):
+        return out
+    return torch.cat([out[r * m: r * m + counts[r]] for r in range(world)])
+
+
+def device_evaluate(index: HamiltonianIndex, device: int) -> Callable:
+    """The fused kernel on device pointers, on torch's current stream."""
+    h = index.device_handle(device)
+    L = _lib.lib()
+
+    def run(keys, la, ph, lp, log_norm, r0, r1, out_locals, out_moments):
+        _lib.check(L.qvmc_cuda_set_stream(h, C.c_void_p(torch.cuda.current_stream(device).cuda_stream)))
+        _lib.check(L.qvmc_cuda_eloc_fused(
+            h, keys.shape[0], C.c_void_p(keys.data_ptr()), C.c_void_p(la.data_ptr()), C.c_void_p(ph.data_ptr()),
+            C.c_void_p(lp.data_ptr()), float(log_norm), r0, r1,
+            C.c_void_p(out_locals.data_ptr()) if out_locals is not None else None,
+            C.c_void_p(out_moments.data_ptr()), _lib.MEM_DEVICE))
+
+    return run
+
+
+def sharded_surrogate_energy(shard: Shard, log_norm: float, evaluate: Callable, group=None,
+                             gather_locals: bool = False) -> ShardResult:
+    """E_loc for this rank's rows + globally reduced moments.
+
+    ``log_norm`` is the global log sum_x p(x) (the sampler's value)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = shard.keys.device
+    cnt = torch.tensor([shard.keys.shape[0]], dtype=torch.int64, device=dev)
+    counts_t = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(counts_t, cnt, group=group)
+    counts = [int(c) for c in counts_t.cpu()]
+    r0 = sum(counts[:rank])
+    r1 = r0 + counts[rank]
+    keys = _gather_rows(shard.keys, counts, group)
+    # amplitudes travel as one [rows, 3] block: one collective instead of three
+    amps = _gather_rows(torch.stack([shard.log_amps, shard.phases, shard.log_probs], dim=1), counts, group)
+    la, ph, lp = (amps[:, k].contiguous() for k in range(3))
+    locals_ = torch.zeros(max(r1 - r0, 1), dtype=torch.complex128, device=dev)
+    moments = torch.zeros(5, dtype=torch.float64, device=dev)
+    evaluate(keys, la, ph, lp, log_norm, r0, r1, locals_, moments)
+    dist.all_reduce(moments, op=dist.ReduceOp.SUM, group=group)
+    res = ShardResult(locals_[: r1 - r0], moments, r0, r1, sum(counts))
+    if gather_locals:
+        res.locals = _gather_rows(res.locals, counts, group)
+    return res
+
+
+def shard_bounds(n: int, world: int, rank: int) -> tuple:
+    """Contiguous, balanced row shard [begin, end) of rank."""
+    base, rem = divmod(n, world)
+    begin = rank * base + min(rank, rem)
+    return begin, begin + base + (1 if rank < rem else 0)

@@ -1,0 +1,164 @@
+"""CPU-side checks of the product: host index builder, parser, C-ABI exports.
+
+No kernel is launched here (the container has no GPU); the device path is
+covered by test_gpu_parity.py.
+"""
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2408_07625_b200 as q
+from paper_2408_07625_b200 import _lib, basis
+from helpers import golden, instances, product_index
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _same_grouping(H, g, p):
+    assert H.n_xy == len(g[p + "xy"]) and H.n_terms == len(g[p + "coeff"])
+    assert np.array_equal(H.xy, g[p + "xy"])
+    assert np.array_equal(H.group_offsets, g[p + "offsets"])
+    assert np.array_equal(H.coeff, g[p + "coeff"])
+    assert np.array_equal(H.yz, g[p + "yz"]) and np.array_equal(H.y_weight, g[p + "y_weight"])
+    assert np.array_equal(H.x_masks, g[p + "x"]) and np.array_equal(H.z_masks, g[p + "z"])
+    d = int(g[p + "diag"])
+    assert H.diagonal_xy_index() == (None if d < 0 else d)
+
+
+@pytest.mark.parametrize("family", ["coupling", "accept3", "checks", "opscale"])
+def test_index_build_matches_reference_grouping(family):
+    g = golden(family)
+    prefixes = ["small_", "large_"] if family == "opscale" else [p for _, p in instances(family)]
+    for p in prefixes:
+        _same_grouping(product_index(g, p), g, p)
+
+
+def test_fixture_parse_matches_reference_grouping():
+    g = golden("fixtures")
+    for name in ("toy", "h2", "h4", "h6"):
+        # rebuild the text from the reference's merged strings (grouped order re-groups identically)
+        n = int(g[f"{name}_n_qubits"])
+        lines = [f"qubits: {n}"]
+        for c, x, y, z in zip(g[f"{name}_coeff"], g[f"{name}_x"], g[f"{name}_y"], g[f"{name}_z"]):
+            s = "".join("X" if (int(x[i // 64]) >> (i % 64)) & 1 else "Y" if (int(y[i // 64]) >> (i % 64)) & 1
+                        else "Z" if (int(z[i // 64]) >> (i % 64)) & 1 else "I" for i in range(n))
+            lines.append(f"{float(c).hex()} {s}  # comment")
+        H = q.HamiltonianIndex.parse("\n".join(lines) + "\n")
+        _same_grouping(H, g, f"{name}_")
+
+
+def test_toy_grouping_and_merge_rules():
+    """test_hamiltonian.cpp:24-57."""
+    H = q.HamiltonianIndex.parse("qubits: 4\n0.9 IIII\n0.1 IZZI\n-0.2 XIXI\n-0.2 IXIX\n0.3 IYYI\n")
+    assert H.n_qubits == 4 and H.n_terms == 5 and H.n_xy == 4
+    assert [basis.dec_value(H.xy[g], 4) for g in range(4)] == [0, 10, 5, 6]
+    assert len(H.group(0)) == 2 and len(H.group(3)) == 1 and H.diagonal_xy_index() == 0
+    H2 = q.HamiltonianIndex.parse("qubits: 4\n0.3 XYZI\n-0.3 XYZI\n0.9 IIII\n")
+    assert H2.n_terms == 1 and H2.n_xy == 1 and basis.dec_value(H2.xy[0], 4) == 0
+    H3 = q.HamiltonianIndex.from_terms(4, [(0.4, "XYII"), (-0.4, "XYII")])
+    assert H3.n_terms == 0 and H3.n_xy == 0 and H3.diagonal_xy_index() is None
+    yy = q.HamiltonianIndex.parse("qubits: 4\n0.3 IYYI\n")
+    assert basis.dec_value(yy.yz[0], 4) == 6 and int(yy.y_weight[0]) == 2
+
+
+@pytest.mark.parametrize("text,msg", [
+    ("0.9 IIII\n", "hamiltonian line 1: expected header 'qubits: <N>'"),
+    ("qubits: 4\n0.9\n", "hamiltonian line 2: expected '<coeff> <pauli_string>'"),
+    ("qubits: 4\n0.9 IIII extra\n", "hamiltonian line 2: trailing content 'extra'"),
+    ("qubits: 4\nabc IIII\n", "hamiltonian line 2: cannot parse coefficient 'abc' as a real number"),
+    ("qubits: 4\ninf IIII\n", "hamiltonian line 2: non-finite coefficient"),
+    ("qubits: 4\n# c\n\n0.9 III\n", "hamiltonian line 4: pauli string has length 3, expected 4"),
+    ("qubits: 4\n0.9 IIQI\n", "hamiltonian line 2: illegal Pauli character 'Q'"),
+    ("# nothing\n", "hamiltonian: missing 'qubits:' header"),
+])
+def test_parse_errors_follow_reference(text, msg):
+    """hamiltonian.cpp:119-170: runtime_error with line numbers."""
+    with pytest.raises(RuntimeError) as e:
+        q.HamiltonianIndex.parse(text)
+    assert str(e.value) == msg
+
+
+def test_from_terms_errors():
+    with pytest.raises(ValueError, match="pauli string length 3 != qubits 4"):
+        q.HamiltonianIndex.from_terms(4, [(1.0, "III")])
+    with pytest.raises(ValueError, match="illegal Pauli character 'Q'"):
+        q.HamiltonianIndex.from_terms(4, [(1.0, "IXQZ")])
+    with pytest.raises(ValueError):
+        q.HamiltonianIndex.from_terms(0, [])
+    with pytest.raises(ValueError):  # overlapping masks through the raw-mask entry
+        q.HamiltonianIndex.from_masks(2, [1.0], [[1]], [[1]], [[0]])
+    with pytest.raises(RuntimeError, match="cannot open hamiltonian file"):
+        q.HamiltonianIndex.load("/nonexistent/x.ham")
+
+
+def test_backend_names():
+    assert q.parse_backend("trie") == q.CouplingBackend.kTrie
+    assert q.backend_name(q.CouplingBackend.kBatch) == "batch"
+    with pytest.raises(ValueError, match="unknown coupling backend: quantum"):
+        q.parse_backend("quantum")
+
+
+def test_basis_vectors():
+    """basis_vector.hpp / test_basis_vector.cpp round trips incl. multi-word widths."""
+    for n in (7, 63, 64, 65, 70, 129, 200, 256):
+        rng = np.random.default_rng(n)
+        bits = rng.integers(0, 2, (5, n)).astype(np.uint8)
+        keys = basis.from_bool_rows(bits)
+        assert keys.shape == (5, basis.n_words(n))
+        assert np.array_equal(basis.to_bool_rows(keys, n), bits)
+        s = "".join(map(str, bits[0]))
+        assert np.array_equal(basis.parse(s), keys[0]) and basis.to_str(keys[0], n) == s
+    assert basis.dec_value(basis.parse("1100"), 4) == 12
+    with pytest.raises(ValueError):
+        basis.parse("10a")
+    with pytest.raises(ValueError):
+        basis.n_words(257)
+
+
+def _header_functions():
+    text = (ROOT / "include" / "qvmc_cuda.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(qvmc_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_cabi_exports_every_declared_symbol():
+    lib = _lib.lib()
+    names = _header_functions()
+    assert len(names) >= 18
+    for name in names:
+        assert hasattr(lib, name), name
+    assert {n for n, _, _ in _lib.SIGNATURES} == set(names)
+
+
+def test_cabi_reports_missing_device_cleanly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    H = q.HamiltonianIndex.parse("qubits: 2\n0.7 II\n")
+    with pytest.raises(RuntimeError):
+        H.device_handle(0)
+    assert "device" in _lib.last_error().lower()
+
+
+def test_synthetic_generators_structure():
+    from paper_2408_07625_b200 import synthetic
+    H = synthetic.jw_hamiltonian(20, 12_000, seed=1)
+    w = np.array([bin(int(v[0])).count("1") for v in H.xy])
+    assert set(np.unique(w)) <= {0, 2, 4}
+    d = H.diagonal_xy_index()
+    assert len(H.group(d)) == 1 + 20 + 190  # identity + Z + ZZ
+    keys = synthetic.near_hf_keys(56, 14, 2000, seed=2)
+    assert len({k.tobytes() for k in keys}) == 2000
+    assert np.all(basis.popcount(keys) == 14)
+    up = basis.to_bool_rows(keys, 56)[:, 0::2].sum(axis=1)
+    assert np.all(up == 7)
+
+
+def test_no_cpu_fallback_when_library_missing(monkeypatch, tmp_path):
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setenv("QVMC_CUDA_LIB", str(tmp_path / "missing.so"))
+    with pytest.raises(ImportError):
+        _lib.lib()
