@@ -176,7 +176,7 @@ def masks_to_strings(n_qubits, x, y, z):
 
 
 def default_cpu_sample(cfg):
-    return {"c118": 5000, "c56": 20000, "c20": 100000}.get(cfg, 10000)
+    return {"c118": 20000, "c56": 50000, "c20": 100000}.get(cfg, 20000)
 
 
 # ------------------------------------------------------------------ reference arm
@@ -187,8 +187,6 @@ def run_reference(args, rank):
     cfg, cm, batch, _ = make_inputs(args.config, args.n_unq)
     threads = os.cpu_count() or 1
     n_s = args.cpu_sample or default_cpu_sample(args.config)
-    for _ in range(max(args.warmup, 0) and 1):  # one untimed warm-up run is enough for a CPU path
-        pass
     times, last = [], None
     for _ in range(args.steps):
         last = cpu_baseline(cm, cfg.n_qubits, batch, n_s, threads)

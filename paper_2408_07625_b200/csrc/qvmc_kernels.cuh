@@ -146,34 +146,56 @@ __global__ void __launch_bounds__(kThreads) k_table_build(const uint64_t* __rest
   }
 }
 
-// Find the row whose key is x ^ xy[g], given f = fmix(hash(x ^ xy[g])).
-// b0/b1 are the first bucket's two 16-byte halves, already loaded.
 template <int W>
-__device__ __forceinline__ int64_t resolve(const TableView& T, const uint64_t* __restrict__ keys,
-                                           const uint64_t* __restrict__ xym, const uint64_t* x, uint64_t f,
-                                           uint32_t g, ulonglong2 b0, ulonglong2 b1, uint64_t* xp) {
+struct Key {
+  uint64_t w[W];
+};
+
+// Bucket scan outcome without touching keys: bit k of `tag_hits` = entry k
+// matches the tag (entries after the first empty slot excluded); `full` =
+// no empty slot, so the key may continue in the next bucket.
+__device__ __forceinline__ void bucket_test(ulonglong2 b0, ulonglong2 b1, uint32_t tag, unsigned& tag_hits,
+                                            bool& full) {
+  const uint64_t e[4] = {b0.x, b0.y, b1.x, b1.y};
+  unsigned empt = 0, tm = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    empt |= (e[k] == kEmpty ? 1u : 0u) << k;
+    tm |= (static_cast<uint32_t>(e[k] >> 32) == tag ? 1u : 0u) << k;
+  }
+  const unsigned first_empty = empt ? __ffs(empt) - 1 : 4;
+  tag_hits = tm & ((1u << first_empty) - 1u);
+  full = empt == 0;
+}
+
+// Slow path of a probe (tag match or full bucket): verify candidates
+// against the stored keys and follow the bucket chain. Returns the row of
+// x ^ xy[g] or -1.
+template <int W>
+__device__ __noinline__ int64_t probe_slow(Key<W> x, uint64_t f, uint32_t g, const uint64_t* __restrict__ tab,
+                                           uint64_t mask, const uint64_t* __restrict__ keys,
+                                           const uint64_t* __restrict__ xym) {
   const uint32_t tag = static_cast<uint32_t>(f >> 32);
-  uint64_t b = f & T.mask;
+  uint64_t want[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) want[w] = x.w[w] ^ __ldg(xym + (int64_t)g * W + w);
+  uint64_t b = f & mask;
   for (;;) {
-    const uint64_t e[4] = {b0.x, b0.y, b1.x, b1.y};
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(tab + b * 4);
+    unsigned tm;
+    bool full;
+    bucket_test(__ldg(p), __ldg(p + 1), tag, tm, full);
+    while (tm) {
+      const int k = __ffs(tm) - 1;
+      tm &= tm - 1;
+      const uint32_t j = static_cast<uint32_t>(__ldg(tab + b * 4 + k));
+      bool same = true;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (e[k] == kEmpty) return -1;
-      if (static_cast<uint32_t>(e[k] >> 32) == tag) {
-        const uint32_t j = static_cast<uint32_t>(e[k]);
-        bool same = true;
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          xp[w] = __ldg(keys + (int64_t)j * W + w);
-          same &= xp[w] == (x[w] ^ __ldg(xym + (int64_t)g * W + w));
-        }
-        if (same) return j;
-      }
+      for (int w = 0; w < W; ++w) same &= __ldg(keys + (int64_t)j * W + w) == want[w];
+      if (same) return j;
     }
-    b = (b + 1) & T.mask;  // bucket full: continue (rare at load <= 1/4)
-    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.tab + b * 4);
-    b0 = __ldg(p);
-    b1 = __ldg(p + 1);
+    if (!full) return -1;
+    b = (b + 1) & mask;
   }
 }
 
@@ -211,87 +233,133 @@ struct RowOut {
   const double* ph;           // phases
 };
 
-template <int W, int MODE>
-struct RowState {
-  uint64_t x[W];
-  uint64_t hx;
-  double la_i, ph_i;
-  double acc_re, acc_im;
-  uint32_t hits;
-  uint64_t cand;
-  int64_t row;
+// sector mode enumerates, per row, one list per minority orbital (single
+// flips) and one per pair of minority orbitals (double flips)
+constexpr int kMaxMinorityDev = 24;
+constexpr int kMaxRanges = kMaxMinorityDev + kMaxMinorityDev * (kMaxMinorityDev - 1) / 2;
+
+// Per-warp hit queue (kModeEloc). Probing only records (x', group); the FP64
+// work (matrix element, exp, sincos) runs when the queue is drained, so the
+// probe loop stays small in registers and all lanes share the FP64 work:
+// small groups one hit per lane, large groups (the 2+2(N-2)-term single
+// excitations, 234 terms at 118 qubits) cooperatively over the warp.
+constexpr int kQueue = 256;
+constexpr int kDrainAt = kQueue - 32 * kUnroll;  // one scan step adds at most 32*kUnroll hits
+constexpr uint32_t kSmallGroup = 16;
+
+struct WarpSmem {
+  uint32_t qj[kQueue];
+  uint32_t qg[kQueue];
+  uint32_t r_lo[kMaxRanges];   // candidate-list ranges of the current row
+  uint32_t r_len[kMaxRanges];
+  uint16_t pos[32];            // minority orbitals of the current row
+  unsigned qn;
+  unsigned cursor;             // kModeEmit output cursor
 };
 
+__device__ __forceinline__ void add_ratio(const double* __restrict__ la, const double* __restrict__ ph, double la_i,
+                                          double ph_i, uint32_t j, double hr, double hi, double2& acc) {
+  // h * exp(dlog) * (cos dphase + i sin dphase)   (energy.cpp:38-43)
+  const double a = exp(__ldg(la + j) - la_i);
+  double s, c;
+  sincos(__ldg(ph + j) - ph_i, &s, &c);
+  hr *= a;
+  hi *= a;
+  acc.x += hr * c - hi * s;
+  acc.y += hr * s + hi * c;
+}
+
+// Drain the warp's hit queue: returns this lane's share of sum H_{xx'} psi(x')/psi(x).
+template <int W>
+__device__ __noinline__ double2 drain(const HamView& H, const uint64_t* __restrict__ keys,
+                                      const double* __restrict__ la, const double* __restrict__ ph, double la_i,
+                                      double ph_i, WarpSmem* sm, int lane) {
+  double2 acc = make_double2(0.0, 0.0);
+  __syncwarp();
+  const unsigned n = sm->qn;
+  for (unsigned k0 = 0; k0 < n; k0 += 32) {
+    const unsigned k = k0 + lane;
+    uint32_t j = 0, g = 0, t0 = 0, t1 = 0;
+    if (k < n) {
+      j = sm->qj[k];
+      g = sm->qg[k];
+      t0 = __ldg(H.goff + g);
+      t1 = __ldg(H.goff + g + 1);
+    }
+    const bool large = k < n && t1 - t0 > kSmallGroup;
+    // small groups: one hit per lane, term by term in the reference order
+    if (k < n && !large) {
+      uint64_t xp[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) xp[w] = __ldg(keys + (int64_t)j * W + w);
+      double hr, hi;
+      group_element<W>(H, xp, g, hr, hi);
+      add_ratio(la, ph, la_i, ph_i, j, hr, hi, acc);
+    }
+    // large groups: the warp splits the terms; the element is parked in lane src
+    double mine_r = 0.0, mine_i = 0.0;
+    unsigned mask = __ballot_sync(0xffffffffu, large);
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const uint32_t sj = __shfl_sync(0xffffffffu, j, src);
+      const uint32_t st0 = __shfl_sync(0xffffffffu, t0, src);
+      const uint32_t st1 = __shfl_sync(0xffffffffu, t1, src);
+      uint64_t xp[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) xp[w] = __ldg(keys + (int64_t)sj * W + w);
+      double re = 0.0, im = 0.0;
+      for (uint32_t t = st0 + lane; t < st1; t += 32) {
+        int pc = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) pc += __popcll(xp[w] & __ldg(H.yz + (int64_t)t * W + w));
+        const int qt = (__ldg(H.yw + t) + 2 * pc) & 3;
+        const double c = __ldg(H.coeff + t);
+        if (qt == 0) re += c;
+        else if (qt == 2) re -= c;
+        else if (qt == 1) im += c;
+        else im -= c;
+      }
+      re = warp_sum(re);
+      im = warp_sum(im);
+      if (lane == src) {
+        mine_r = re;
+        mine_i = im;
+      }
+    }
+    if (large) add_ratio(la, ph, la_i, ph_i, j, mine_r, mine_i, acc);
+  }
+  __syncwarp();
+  if (lane == 0) sm->qn = 0;
+  __syncwarp();
+  return acc;
+}
+
 template <int W, int MODE>
-__device__ __forceinline__ void on_hit(const HamView& H, const RowOut& O, RowState<W, MODE>& st, int64_t j,
-                                       const uint64_t* xp, uint32_t g, unsigned* s_cursor) {
+__device__ __forceinline__ void on_hit(const RowOut& O, int64_t row, int64_t j, uint32_t g, WarpSmem* sm) {
   if (MODE == kModeEloc) {
-    double hr, hi;
-    group_element<W>(H, xp, g, hr, hi);
-    const double a = exp(__ldg(O.la + j) - st.la_i);
-    double s, c;
-    sincos(__ldg(O.ph + j) - st.ph_i, &s, &c);
-    hr *= a;
-    hi *= a;
-    st.acc_re += hr * c - hi * s;
-    st.acc_im += hr * s + hi * c;
+    const unsigned k = atomicAdd(&sm->qn, 1u);  // < kQueue: drained at kDrainAt
+    sm->qj[k] = static_cast<uint32_t>(j);
+    sm->qg[k] = g;
   } else if (MODE == kModeEmit) {
-    const unsigned k = atomicAdd(s_cursor, 1u);
-    const uint64_t at = O.row_off[st.row] + k;
+    const unsigned k = atomicAdd(&sm->cursor, 1u);
+    const uint64_t at = O.row_off[row] + k;
     O.xp_out[at] = static_cast<uint32_t>(j);
     O.g_out[at] = g;
   }
-  ++st.hits;
-}
-
-// Probe every mask of list entries [lo, hi) (hash + group id arrays).
-template <int W, int MODE>
-__device__ __forceinline__ void scan_list(const HamView& H, const TableView& T, const uint64_t* __restrict__ keys,
-                                          const RowOut& O, RowState<W, MODE>& st, const uint64_t* __restrict__ hs,
-                                          const uint32_t* __restrict__ gs, uint32_t lo, uint32_t hi, int lane,
-                                          unsigned* s_cursor) {
-  for (uint32_t base = lo; base < hi; base += 32 * kUnroll) {
-    uint64_t f[kUnroll];
-    uint32_t g[kUnroll];
-    ulonglong2 b0[kUnroll], b1[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint32_t e = base + u * 32 + lane;
-      g[u] = 0xffffffffu;
-      f[u] = 0;
-      if (e < hi) {
-        g[u] = __ldg(gs + e);
-        f[u] = fmix(st.hx ^ __ldg(hs + e));
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (g[u] != 0xffffffffu) {
-        const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.tab + (f[u] & T.mask) * 4);
-        b0[u] = __ldg(p);
-        b1[u] = __ldg(p + 1);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (g[u] != 0xffffffffu) {
-        ++st.cand;
-        uint64_t xp[W];
-        const int64_t j = resolve<W>(T, keys, H.xy, st.x, f[u], g[u], b0[u], b1[u], xp);
-        if (j >= 0) on_hit<W, MODE>(H, O, st, j, xp, g[u], s_cursor);
-      }
-    }
-  }
 }
 
 template <int W, int MODE>
-__global__ void __launch_bounds__(kThreads) k_rows(HamView H, TableView T, const uint64_t* __restrict__ keys,
-                                                   int64_t row_begin, int64_t row_end, Ctl C, RowOut O) {
-  __shared__ uint16_t s_pos[kWarps][32];
-  __shared__ unsigned s_cursor[kWarps];
+__global__ void __launch_bounds__(kThreads) k_rows(const __grid_constant__ HamView H, const TableView T,
+                                                   const uint64_t* __restrict__ keys, int64_t row_begin,
+                                                   int64_t row_end, const __grid_constant__ Ctl C,
+                                                   const __grid_constant__ RowOut O) {
+  __shared__ WarpSmem s_w[kWarps];
   const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
+  WarpSmem* sm = &s_w[threadIdx.x >> 5];
   const int n = H.n;
+  if (lane == 0) sm->qn = 0;
+  __syncwarp();
 
   // sector mode: every key has the same popcount, so x' = x ^ m can be in
   // the sample set only if |m & S(x)| = |m|/2 for the minority set S(x)
@@ -299,7 +367,7 @@ __global__ void __launch_bounds__(kThreads) k_rows(HamView H, TableView T, const
   const int pmin = 1024 - C.popc_mm[1];
   const int side = (pmin <= n - pmin) ? 1 : 0;  // 1: occupied orbitals are the minority
   const int s = side ? pmin : n - pmin;
-  const bool sector = H.lst_off != nullptr && pmin == pmax && s <= 32;
+  const bool sector = H.lst_off != nullptr && pmin == pmax && s <= kMaxMinorityDev;
 
   uint64_t tot_cand = 0, tot_hits = 0;
   for (;;) {
@@ -309,17 +377,14 @@ __global__ void __launch_bounds__(kThreads) k_rows(HamView H, TableView T, const
     const int64_t row = row_begin + static_cast<int64_t>(r);
     if (row >= row_end) break;
 
-    RowState<W, MODE> st;
-    st.row = row;
-    st.acc_re = st.acc_im = 0.0;
-    st.hits = 0;
-    st.cand = 0;
+    uint64_t x[W];
 #pragma unroll
-    for (int w = 0; w < W; ++w) st.x[w] = __ldg(keys + row * W + w);
+    for (int w = 0; w < W; ++w) x[w] = __ldg(keys + row * W + w);
+    double la_i = 0.0, ph_i = 0.0;
     if (MODE == kModeEloc) {
-      st.la_i = __ldg(O.la + row);
-      st.ph_i = __ldg(O.ph + row);
-      if (isinf(st.la_i)) {  // energy.cpp:32-33
+      la_i = __ldg(O.la + row);
+      ph_i = __ldg(O.ph + row);
+      if (isinf(la_i)) {  // energy.cpp:32-33
         if (lane == 0) {
           atomicOr(C.err, kErrZeroAmp);
           O.eloc[row - row_begin] = make_double2(CUDART_NAN, CUDART_NAN);
@@ -327,21 +392,23 @@ __global__ void __launch_bounds__(kThreads) k_rows(HamView H, TableView T, const
         continue;
       }
     }
-    if (MODE == kModeEmit && lane == 0) s_cursor[wid] = 0;
-    st.hx = key_hash_warp<W>(st.x, H.hash_bytes, lane);
-    __syncwarp();
+    if (MODE == kModeEmit && lane == 0) sm->cursor = 0;
+    const uint64_t hx = key_hash_warp<W>(x, H.hash_bytes, lane);
 
-    double d_re = 0.0, d_im = 0.0;  // diagonal element, split over lanes
-    if (sector) {
-      uint64_t S[W];
+    // ---- the candidate lists of this row, as (offset, length) ranges
+    const uint64_t* hs = H.gen_hash;
+    const uint32_t* gs = H.gen_g;
+    int n_ranges = 1;
+    int pos = 0;
+    uint64_t S[W];
 #pragma unroll
-      for (int w = 0; w < W; ++w) {
-        S[w] = side ? st.x[w] : ~st.x[w];
-        const int hi_bit = n - 64 * w;
-        if (hi_bit < 64) S[w] &= (hi_bit <= 0) ? 0ull : ((1ull << hi_bit) - 1);
-      }
-      // lane a < s holds the a-th minority orbital
-      int pos = 0, c = 0;
+    for (int w = 0; w < W; ++w) {
+      S[w] = side ? x[w] : ~x[w];
+      const int hi_bit = n - 64 * w;
+      if (hi_bit < 64) S[w] &= (hi_bit <= 0) ? 0ull : ((1ull << hi_bit) - 1);
+    }
+    if (sector) {
+      int c = 0;  // lane a < s holds the a-th minority orbital
 #pragma unroll
       for (int w = 0; w < W; ++w) {
         uint64_t v = S[w];
@@ -352,25 +419,99 @@ __global__ void __launch_bounds__(kThreads) k_rows(HamView H, TableView T, const
         }
         c += pc;
       }
-      if (lane < s) s_pos[wid][lane] = static_cast<uint16_t>(pos);
+      if (lane < s) sm->pos[lane] = static_cast<uint16_t>(pos);
       __syncwarp();
-      // single flips: weight-2 masks through one minority orbital
-      for (int a = 0; a < s; ++a) {
-        const int id = s_pos[wid][a];
-        scan_list<W, MODE>(H, T, keys, O, st, H.lst_hash, H.lst_g, __ldg(H.lst_off + id), __ldg(H.lst_off + id + 1),
-                           lane, &s_cursor[wid]);
+      hs = H.lst_hash;
+      gs = H.lst_g;
+      n_ranges = s + s * (s - 1) / 2;
+      // range k < s: single-flip list of orbital pos[k]; then pairs (a < b), pi = b(b-1)/2 + a
+      for (int k = lane; k < n_ranges; k += 32) {
+        int id;
+        if (k < s) {
+          id = sm->pos[k];
+        } else {
+          const int pi = k - s;
+          int b = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * pi)) * 0.5f);
+          while (b * (b - 1) / 2 > pi) --b;
+          while ((b + 1) * b / 2 <= pi) ++b;
+          const int pa = sm->pos[pi - b * (b - 1) / 2], pb = sm->pos[b];
+          id = n + pa * n - pa * (pa + 1) / 2 + (pb - pa - 1);
+        }
+        const uint32_t lo = __ldg(H.lst_off + id);
+        sm->r_lo[k] = lo;
+        sm->r_len[k] = __ldg(H.lst_off + id + 1) - lo;
       }
-      // double flips: weight-4 masks through two minority orbitals
-      for (int b = 1; b < s; ++b) {
-        const int pb = s_pos[wid][b];
-        for (int a = 0; a < b; ++a) {
-          const int pa = s_pos[wid][a];
-          const int id = n + pa * n - pa * (pa + 1) / 2 + (pb - pa - 1);
-          scan_list<W, MODE>(H, T, keys, O, st, H.lst_hash, H.lst_g, __ldg(H.lst_off + id),
-                             __ldg(H.lst_off + id + 1), lane, &s_cursor[wid]);
+    } else if (lane == 0) {
+      sm->r_lo[0] = 0;
+      sm->r_len[0] = H.n_gen;
+    }
+    __syncwarp();
+
+    // ---- walk the concatenated ranges: lane l takes elements l, l+32, ...;
+    // its cursor (rg, off) advances by 32 per probe
+    double2 acc = make_double2(0.0, 0.0);
+    uint32_t hits = 0;
+    uint64_t cand = 0;
+    int rg = 0;
+    uint32_t off = lane;
+    uint32_t len = sm->r_len[0];
+    while (rg < n_ranges && off >= len) {
+      off -= len;
+      if (++rg < n_ranges) len = sm->r_len[rg];
+    }
+    while (__any_sync(0xffffffffu, rg < n_ranges)) {
+      uint64_t f[kUnroll];
+      uint32_t g[kUnroll];
+      ulonglong2 b0[kUnroll], b1[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        g[u] = 0xffffffffu;
+        f[u] = 0;
+        if (rg < n_ranges) {
+          const uint32_t e = sm->r_lo[rg] + off;
+          g[u] = __ldg(gs + e);
+          f[u] = fmix(hx ^ __ldg(hs + e));
+          const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.tab + (f[u] & T.mask) * 4);
+          b0[u] = __ldg(p);
+          b1[u] = __ldg(p + 1);
+          off += 32;
+          while (rg < n_ranges && off >= len) {
+            off -= len;
+            if (++rg < n_ranges) len = sm->r_len[rg];
+          }
         }
       }
-      // even weight >= 6: filter by the popcount condition, then probe
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        if (g[u] != 0xffffffffu) {
+          ++cand;
+          unsigned tm;
+          bool full;
+          bucket_test(b0[u], b1[u], static_cast<uint32_t>(f[u] >> 32), tm, full);
+          if (tm || full) {
+            Key<W> xk;
+#pragma unroll
+            for (int w = 0; w < W; ++w) xk.w[w] = x[w];
+            const int64_t j = probe_slow<W>(xk, f[u], g[u], T.tab, T.mask, keys, H.xy);
+            if (j >= 0) {
+              on_hit<W, MODE>(O, row, j, g[u], sm);
+              ++hits;
+            }
+          }
+        }
+      }
+      if (MODE == kModeEloc) {
+        __syncwarp();
+        if (sm->qn >= kDrainAt) {
+          const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane);
+          acc.x += d.x;
+          acc.y += d.y;
+        }
+      }
+    }
+
+    // ---- even flip masks of weight >= 6 (none for two-body Hamiltonians)
+    if (sector) {
       for (uint32_t base = 0; base < H.n_res; base += 32) {
         const uint32_t e = base + lane;
         if (e < H.n_res) {
@@ -383,75 +524,92 @@ __global__ void __launch_bounds__(kThreads) k_rows(HamView H, TableView T, const
             wt += __popcll(m);
           }
           if (2 * in_s == wt) {
-            const uint64_t f = fmix(st.hx ^ __ldg(H.xy_hash + g));
-            const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.tab + (f & T.mask) * 4);
-            uint64_t xp[W];
-            ++st.cand;
-            const int64_t j = resolve<W>(T, keys, H.xy, st.x, f, g, __ldg(p), __ldg(p + 1), xp);
-            if (j >= 0) on_hit<W, MODE>(H, O, st, j, xp, g, &s_cursor[wid]);
+            Key<W> xk;
+#pragma unroll
+            for (int w = 0; w < W; ++w) xk.w[w] = x[w];
+            ++cand;
+            const int64_t j = probe_slow<W>(xk, fmix(hx ^ __ldg(H.xy_hash + g)), g, T.tab, T.mask, keys, H.xy);
+            if (j >= 0) {
+              on_hit<W, MODE>(O, row, j, g, sm);
+              ++hits;
+            }
+          }
+        }
+        if (MODE == kModeEloc) {
+          __syncwarp();
+          if (sm->qn >= kDrainAt) {
+            const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane);
+            acc.x += d.x;
+            acc.y += d.y;
           }
         }
       }
-      if (MODE == kModeEloc && H.diag >= 0 && H.diag_quad) {
-        if (lane == 0) d_re += side ? H.diag_A1 : H.diag_A0;
-        if (lane < s) d_re += __ldg(H.diag_b + side * n + pos);
+    }
+
+    // ---- diagonal element (x' = x, ratio exactly 1), split over lanes
+    if (MODE == kModeEloc && H.diag >= 0) {
+      if (sector && H.diag_quad) {
+        if (lane == 0) acc.x += side ? H.diag_A1 : H.diag_A0;
+        if (lane < s) acc.x += __ldg(H.diag_b + side * n + pos);
         const int np = s * (s - 1) / 2;
         for (int pi = lane; pi < np; pi += 32) {
-          // pairs ordered by b then a: pi = b(b-1)/2 + a
           int b = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * pi)) * 0.5f);
           while (b * (b - 1) / 2 > pi) --b;
           while ((b + 1) * b / 2 <= pi) ++b;
-          const int a = pi - b * (b - 1) / 2;
-          d_re += __ldg(H.diag_K + s_pos[wid][a] * n + s_pos[wid][b]);
+          acc.x += __ldg(H.diag_K + sm->pos[pi - b * (b - 1) / 2] * n + sm->pos[b]);
         }
         for (uint32_t e = lane; e < H.n_diag_other; e += 32) {
           const uint32_t t = __ldg(H.diag_other + e);
           int pc = 0;
 #pragma unroll
-          for (int w = 0; w < W; ++w) pc += __popcll(st.x[w] & __ldg(H.yz + (int64_t)t * W + w));
-          const int q = (__ldg(H.yw + t) + 2 * pc) & 3;
+          for (int w = 0; w < W; ++w) pc += __popcll(x[w] & __ldg(H.yz + (int64_t)t * W + w));
+          const int qt = (__ldg(H.yw + t) + 2 * pc) & 3;
           const double cf = __ldg(H.coeff + t);
-          if (q == 0) d_re += cf;
-          else if (q == 2) d_re -= cf;
-          else if (q == 1) d_im += cf;
-          else d_im -= cf;
+          if (qt == 0) acc.x += cf;
+          else if (qt == 2) acc.x -= cf;
+          else if (qt == 1) acc.y += cf;
+          else acc.y -= cf;
         }
-      }
-    } else {
-      scan_list<W, MODE>(H, T, keys, O, st, H.gen_hash, H.gen_g, 0, H.n_gen, lane, &s_cursor[wid]);
-    }
-    if (MODE == kModeEloc && H.diag >= 0 && !(sector && H.diag_quad)) {
-      const uint32_t t1 = __ldg(H.goff + H.diag + 1);
-      for (uint32_t t = __ldg(H.goff + H.diag) + lane; t < t1; t += 32) {
-        int pc = 0;
+      } else {
+        const uint32_t t1 = __ldg(H.goff + H.diag + 1);
+        for (uint32_t t = __ldg(H.goff + H.diag) + lane; t < t1; t += 32) {
+          int pc = 0;
 #pragma unroll
-        for (int w = 0; w < W; ++w) pc += __popcll(st.x[w] & __ldg(H.yz + (int64_t)t * W + w));
-        const int q = (__ldg(H.yw + t) + 2 * pc) & 3;
-        const double cf = __ldg(H.coeff + t);
-        if (q == 0) d_re += cf;
-        else if (q == 2) d_re -= cf;
-        else if (q == 1) d_im += cf;
-        else d_im -= cf;
+          for (int w = 0; w < W; ++w) pc += __popcll(x[w] & __ldg(H.yz + (int64_t)t * W + w));
+          const int qt = (__ldg(H.yw + t) + 2 * pc) & 3;
+          const double cf = __ldg(H.coeff + t);
+          if (qt == 0) acc.x += cf;
+          else if (qt == 2) acc.x -= cf;
+          else if (qt == 1) acc.y += cf;
+          else acc.y -= cf;
+        }
       }
     }
 
     if (MODE == kModeEloc) {
-      const double re = warp_sum(st.acc_re + d_re);
-      const double im = warp_sum(st.acc_im + d_im);
+      __syncwarp();
+      if (sm->qn > 0) {
+        const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane);
+        acc.x += d.x;
+        acc.y += d.y;
+      }
+      const double re = warp_sum(acc.x);
+      const double im = warp_sum(acc.y);
       if (lane == 0) O.eloc[row - row_begin] = make_double2(re, im);
     }
-    const uint32_t hits = warp_sum(st.hits) + (H.diag >= 0 ? 1u : 0u);
-    if (MODE == kModeCount && lane == 0) O.counts[row] = hits;
+    const uint32_t row_hits = warp_sum(hits) + (H.diag >= 0 ? 1u : 0u);
+    if (MODE == kModeCount && lane == 0) O.counts[row] = row_hits;
     if (MODE == kModeEmit) {
       __syncwarp();
       if (lane == 0 && H.diag >= 0) {
-        const uint64_t at = O.row_off[row] + s_cursor[wid];
+        const uint64_t at = O.row_off[row] + sm->cursor;
         O.xp_out[at] = static_cast<uint32_t>(row);
         O.g_out[at] = static_cast<uint32_t>(H.diag);
       }
+      __syncwarp();
     }
-    tot_cand += st.cand;
-    tot_hits += hits;  // warp total, identical on every lane
+    tot_cand += cand;
+    tot_hits += row_hits;  // warp total, identical on every lane
   }
   tot_cand = warp_sum(tot_cand);
   if (lane == 0) {

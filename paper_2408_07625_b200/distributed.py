@@ -66,7 +66,10 @@ def device_evaluate(index: HamiltonianIndex, device: int) -> Callable:
     L = _lib.lib()
 
     def run(keys, la, ph, lp, log_norm, r0, r1, out_locals, out_moments):
-        _lib.check(L.qvmc_cuda_set_stream(h, C.c_void_p(torch.cuda.current_stream(device).cuda_stream)))
+        # torch's default stream is the legacy NULL stream: pass cudaStreamLegacy (0x1), since
+        # NULL selects the handle's own non-blocking stream
+        raw = torch.cuda.current_stream(device).cuda_stream or 0x1
+        _lib.check(L.qvmc_cuda_set_stream(h, C.c_void_p(raw)))
         _lib.check(L.qvmc_cuda_eloc_fused(
             h, keys.shape[0], C.c_void_p(keys.data_ptr()), C.c_void_p(la.data_ptr()), C.c_void_p(ph.data_ptr()),
             C.c_void_p(lp.data_ptr()), float(log_norm), r0, r1,

@@ -162,3 +162,41 @@ def test_no_cpu_fallback_when_library_missing(monkeypatch, tmp_path):
     monkeypatch.setenv("QVMC_CUDA_LIB", str(tmp_path / "missing.so"))
     with pytest.raises(ImportError):
         _lib.lib()
+
+
+DROPIN = ROOT / "paper_2408_07625_b200" / "lib" / "libqvmc_dropin.so"
+REF_SRC = Path("/root/reference/proj/src")
+
+
+def _defined_symbols(path, demangle=True, kinds="TW"):
+    import subprocess
+    args = ["nm", "-g", "--defined-only"] + (["-C"] if demangle else []) + [str(path)]
+    out = subprocess.run(args, capture_output=True, text=True, check=True).stdout
+    return {line.split(" ", 2)[2].replace("[abi:cxx11]", "") for line in out.splitlines()
+            if line.count(" ") >= 2 and line.split(" ")[1] in kinds}
+
+
+@pytest.mark.skipif(not DROPIN.exists(), reason="drop-in is built only where the reference headers exist")
+def test_dropin_defines_the_replaced_translation_units():
+    """libqvmc_dropin.so defines every global function of coupling.cpp and energy.cpp."""
+    syms = _defined_symbols(DROPIN)
+    want = ["qvmc::parse_backend(", "qvmc::backend_name(", "qvmc::loop_over_terms(", "qvmc::loop_over_batch(",
+            "qvmc::loop_over_trie(", "qvmc::find_coupled_pairs(", "qvmc::local_energies(",
+            "qvmc::variational_energy(", "qvmc::energy_gradient(", "qvmc::GradientAccumulator::add(",
+            "qvmc::GradientAccumulator::take(", "qvmc::GradientAccumulator::GradientAccumulator("]
+    for w in want:
+        assert any(s.startswith(w) for s in syms), w
+    if REF_SRC.exists():
+        import subprocess
+        import tempfile
+        with tempfile.TemporaryDirectory() as d:
+            for tu in ("coupling", "energy"):
+                obj = Path(d) / f"{tu}.o"
+                subprocess.run(["g++", "-std=c++20", "-c", "-w", "-I/root/reference/proj/include",
+                                f"-I{ROOT / 'paper_2408_07625_b200' / 'dropin' / 'eigen_shim'}",
+                                str(REF_SRC / f"{tu}.cpp"), "-o", str(obj)], check=True)
+                # strong definitions only: inline header functions are weak in every TU
+                ref_syms = {s for s in _defined_symbols(obj, demangle=False, kinds="T") if s.startswith("_ZN4qvmc")}
+                mine = _defined_symbols(DROPIN, demangle=False)
+                missing = {s for s in ref_syms if s not in mine}
+                assert not missing, missing
