@@ -70,13 +70,14 @@ typedef struct qvmc_index_s* qvmc_index_t; /* host-side grouped index (from_term
 /* Counters of the last pairs/fused call on a handle. */
 typedef struct {
   uint64_t rows;            /* source rows processed */
-  uint64_t candidates;      /* (x, flip mask) candidates probed on the device */
+  uint64_t candidates;      /* candidates visited on the device: (x, flip mask) probes, or
+                               bucket members in join mode */
   uint64_t pairs;           /* coupled pairs found (incl. the diagonal) */
   uint64_t terms_equivalent;/* n_rows * |XY|: the LoopOverTerms candidate count */
   int32_t sector_mode;      /* 1 = particle-sector candidate lists, 0 = full flip-mask scan */
   int32_t sector_side;      /* 1 = occupied orbitals are the minority set, 0 = holes */
   int32_t minority_count;   /* |minority set| per key in sector mode */
-  int32_t reserved;
+  int32_t join_mode;        /* 1 = candidates from the per-call deletion index (join path) */
   float table_ms;           /* CUDA-event times of the last fused call's stages on the */
   float rows_ms;            /* handle's stream: sample-set hash build, row kernel,     */
   float moments_ms;         /* moment reduction                                       */

@@ -38,7 +38,7 @@ class QvmcStats(C.Structure):
         ("sector_mode", C.c_int32),
         ("sector_side", C.c_int32),
         ("minority_count", C.c_int32),
-        ("reserved", C.c_int32),
+        ("join_mode", C.c_int32),
         ("table_ms", C.c_float),
         ("rows_ms", C.c_float),
         ("moments_ms", C.c_float),

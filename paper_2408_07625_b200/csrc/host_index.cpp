@@ -262,6 +262,28 @@ DevicePlan plan_device(const HostIndex& h) {
     }
   }
 
+  // flip-mask hash table for the join path, same bucket layout as the
+  // device-built sample-set table (load <= 1/4)
+  {
+    uint64_t nb = 64;
+    while (nb < n_xy) nb <<= 1;
+    p.xy_tab.assign(nb * 4, ~uint64_t{0});
+    p.xy_tab_mask = nb - 1;
+    for (uint32_t g = 0; g < n_xy; ++g) {
+      if (static_cast<int64_t>(g) == h.diag) continue;
+      const uint64_t f = fmix_host(p.xy_hash[g]);
+      const uint64_t entry = (f >> 32) << 32 | g;
+      for (uint64_t b = f & p.xy_tab_mask;; b = (b + 1) & p.xy_tab_mask) {
+        int k = 0;
+        while (k < 4 && p.xy_tab[b * 4 + k] != ~uint64_t{0}) ++k;
+        if (k < 4) {
+          p.xy_tab[b * 4 + k] = entry;
+          break;
+        }
+      }
+    }
+  }
+
   // byte tables of the linear hash: T[k][v] = XOR of codes of the bits of byte v at byte k
   const uint64_t* r = qubit_codes();
   p.hash_bytes.assign(static_cast<size_t>(W) * 8 * 256, 0);

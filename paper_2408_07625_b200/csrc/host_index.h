@@ -59,7 +59,18 @@ struct DevicePlan {
   std::vector<double> diag_K;       // [N][N]
   std::vector<uint32_t> diag_other; // diagonal terms with |z| >= 3
   std::vector<uint64_t> hash_bytes; // [n_words*8][256]
+  // flip-mask hash table (join path): buckets of 4 x (tag32 << 32 | group)
+  std::vector<uint64_t> xy_tab;
+  uint64_t xy_tab_mask = 0;
 };
+
+// bucket-chain finaliser shared with the device (qvmc_kernels.cuh fmix)
+inline uint64_t fmix_host(uint64_t h) {
+  h ^= h >> 29;
+  h *= 0xbf58476d1ce4e5b9ull;
+  h ^= h >> 32;
+  return h;
+}
 
 DevicePlan plan_device(const HostIndex& h);
 

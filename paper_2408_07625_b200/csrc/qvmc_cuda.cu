@@ -6,7 +6,10 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <memory>
@@ -16,6 +19,7 @@
 
 #include "host_index.h"
 #include "qvmc_cuda.h"
+#include "qvmc_join.cuh"
 #include "qvmc_kernels.cuh"
 
 using namespace qvmc_b200;
@@ -117,8 +121,12 @@ struct qvmc_ham_s {
   cudaStream_t own = nullptr, stream = nullptr;
   // Hamiltonian
   DBuf xy, xy_hash, goff, coeff, yz, yw, xyw, gen_hash, gen_g, lst_off, lst_hash, lst_g, res_g, diag_b, diag_K,
-      diag_other, hash_bytes;
+      diag_other, hash_bytes, xy_tab, codes;
+  uint64_t xy_tab_mask = 0;
   HamView view{};
+  // join path (per call): deletion-index workspace
+  DBuf j_hsh, j_key, j_val, j_key2, j_val2, j_rng, j_uniq, j_cnt, j_off, j_nruns, j_tmp;
+  bool use_join = true;
   // workspace
   DBuf tab, ctl, keys, la, ph, lp, eloc, partials, moments, weights;
   DBuf counts, row_off, xp_a, g_a, xp_b, g_b, entries, cub_tmp, in_entries, out_h, out_class;
@@ -318,6 +326,119 @@ void launch_rows(qvmc_ham_s* h, const uint64_t* keys, int64_t r0, int64_t r1, co
   }
 }
 
+// How the rows of this call enumerate candidates (needs the popcount range
+// the table build just computed: one 8-byte device->host read).
+struct RowPlan {
+  bool sector = false;
+  bool join = false;
+  int side = 0;
+  int s = 0;
+};
+
+RowPlan plan_rows(qvmc_ham_s* h, int64_t n) {
+  int mm[2] = {0, 0};
+  ck(cudaMemcpyAsync(mm, static_cast<int*>(h->ctl.p) + 2, sizeof(mm), cudaMemcpyDeviceToHost, h->stream), "mm");
+  ck(cudaStreamSynchronize(h->stream), "sync");
+  RowPlan P;
+  const int pmax = mm[0], pmin = 1024 - mm[1];
+  P.side = (pmin <= h->n - pmin) ? 1 : 0;
+  P.s = P.side ? pmin : h->n - pmin;
+  P.sector = n > 0 && pmin == pmax && P.s <= kMaxMinorityDev;
+  const uint64_t entries = static_cast<uint64_t>(n) * (P.s * (P.s - 1) / 2);
+  P.join = h->use_join && P.sector && P.s >= 2 && P.s <= kJoinMaxMinority && entries < (1ull << 31);
+  return P;
+}
+
+// deletion index: keys -> radix sort -> runs -> per-entry bucket ranges
+template <int W>
+void build_join_index(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowPlan& P) {
+  const uint32_t C = static_cast<uint32_t>(P.s * (P.s - 1) / 2);
+  const uint64_t E = static_cast<uint64_t>(n) * C;
+  h->j_hsh.ensure(n * 8 + 16);
+  h->j_key.ensure(E * 4 + 16);
+  h->j_val.ensure(E * 4 + 16);
+  h->j_key2.ensure(E * 4 + 16);
+  h->j_val2.ensure(E * 4 + 16);
+  h->j_rng.ensure(E * 8 + 16);
+  h->j_uniq.ensure(E * 4 + 16);
+  h->j_cnt.ensure(E * 4 + 16);
+  h->j_off.ensure(E * 4 + 16);
+  h->j_nruns.ensure(16);
+  const int grid = static_cast<int>(std::min<int64_t>((n + kThreads - 1) / kThreads, grid_for(h, 8)));
+  k_join_keys<W><<<std::max(grid, 1), kThreads, 0, h->stream>>>(
+      keys, n, h->n, P.side, P.s, h->view.hash_bytes, h->codes.as<uint64_t>(), h->j_hsh.as<uint64_t>(),
+      h->j_key.as<uint32_t>(), h->j_val.as<uint32_t>());
+  ck_launch("join keys");
+  const int ne = static_cast<int>(E);
+  size_t b1 = 0, b2 = 0, b3 = 0;
+  ck(cub::DeviceRadixSort::SortPairs(nullptr, b1, h->j_key.as<uint32_t>(), h->j_key2.as<uint32_t>(),
+                                     h->j_val.as<uint32_t>(), h->j_val2.as<uint32_t>(), ne, 0, 32, h->stream),
+     "sort size");
+  ck(cub::DeviceRunLengthEncode::Encode(nullptr, b2, h->j_key2.as<uint32_t>(), h->j_uniq.as<uint32_t>(),
+                                        h->j_cnt.as<uint32_t>(), h->j_nruns.as<int>(), ne, h->stream),
+     "rle size");
+  ck(cub::DeviceScan::ExclusiveSum(nullptr, b3, h->j_cnt.as<uint32_t>(), h->j_off.as<uint32_t>(), ne, h->stream),
+     "scan size");
+  h->j_tmp.ensure(std::max({b1, b2, b3}) + 16);
+  ck(cub::DeviceRadixSort::SortPairs(h->j_tmp.p, b1, h->j_key.as<uint32_t>(), h->j_key2.as<uint32_t>(),
+                                     h->j_val.as<uint32_t>(), h->j_val2.as<uint32_t>(), ne, 0, 32, h->stream),
+     "sort");
+  ck(cub::DeviceRunLengthEncode::Encode(h->j_tmp.p, b2, h->j_key2.as<uint32_t>(), h->j_uniq.as<uint32_t>(),
+                                        h->j_cnt.as<uint32_t>(), h->j_nruns.as<int>(), ne, h->stream),
+     "rle");
+  ck(cub::DeviceScan::ExclusiveSum(h->j_tmp.p, b3, h->j_cnt.as<uint32_t>(), h->j_off.as<uint32_t>(), ne, h->stream),
+     "scan");
+  g_launches += 3;
+  const int rgrid = static_cast<int>(std::min<uint64_t>((E + kThreads - 1) / kThreads, grid_for(h, 8)));
+  k_join_ranges<<<std::max(rgrid, 1), kThreads, 0, h->stream>>>(h->j_off.as<uint32_t>(), h->j_cnt.as<uint32_t>(),
+                                                                h->j_nruns.as<int>(), h->j_val2.as<uint32_t>(),
+                                                                h->j_rng.as<uint2>());
+  ck_launch("join ranges");
+}
+
+JoinView join_view(qvmc_ham_s* h, const RowPlan& P) {
+  JoinView J{};
+  J.C = static_cast<uint32_t>(P.s * (P.s - 1) / 2);
+  J.rng = h->j_rng.as<uint2>();
+  J.vals = h->j_val2.as<uint32_t>();
+  J.hsh = h->j_hsh.as<uint64_t>();
+  J.xy_tab = h->xy_tab.as<uint64_t>();
+  J.xy_mask = h->xy_tab_mask;
+  J.codes = h->codes.as<uint64_t>();
+  return J;
+}
+
+template <int W, int MODE>
+void launch_rows_join(qvmc_ham_s* h, const uint64_t* keys, int64_t r0, int64_t r1, const RowPlan& P,
+                      const RowOut& O) {
+  ck(cudaMemsetAsync(static_cast<int*>(h->ctl.p) + 4, 0, 2 * sizeof(int), h->stream), "memset row counter");
+  int per_sm = 0;
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_join<W, MODE>, kThreads, 0), "occupancy");
+  const int64_t blocks_needed = (r1 - r0 + kWarps - 1) / kWarps;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_needed, grid_for(h, per_sm))));
+  TableView T{h->tab.as<uint64_t>(), h->tab_buckets - 1};
+  if (r1 > r0) {
+    k_rows_join<W, MODE><<<grid, kThreads, 0, h->stream>>>(h->view, T, join_view(h, P), keys, r0, r1, P.side, P.s,
+                                                         ctl_view(h), O);
+    ck_launch("row kernel (join)");
+  }
+}
+
+template <int W, int MODE>
+void run_rows(qvmc_ham_s* h, const uint64_t* keys, int64_t r0, int64_t r1, const RowPlan& P, const RowOut& O) {
+  if (P.join)
+    launch_rows_join<W, MODE>(h, keys, r0, r1, P, O);
+  else
+    launch_rows<W, MODE>(h, keys, r0, r1, O);
+}
+
+void note_plan(qvmc_ham_s* h, const RowPlan& P) {
+  h->last.sector_mode = P.sector ? 1 : 0;
+  h->last.sector_side = P.side;
+  h->last.minority_count = P.s;
+  h->last.join_mode = P.join ? 1 : 0;
+}
+
 int read_err_and_reset(qvmc_ham_s* h) {
   int err = 0;
   ck(cudaMemcpyAsync(&err, h->ctl.p, sizeof(int), cudaMemcpyDeviceToHost, h->stream), "read err");
@@ -491,6 +612,10 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     upload(h->diag_K, p.diag_K);
     upload(h->diag_other, p.diag_other);
     upload(h->hash_bytes, p.hash_bytes);
+    upload(h->xy_tab, p.xy_tab);
+    h->xy_tab_mask = p.xy_tab_mask;
+    upload(h->codes, std::vector<uint64_t>(qubit_codes(), qubit_codes() + 256));
+    if (const char* e = std::getenv("QVMC_JOIN")) h->use_join = std::atoi(e) != 0;
     h->ctl.ensure(kCtlInts * sizeof(int) * 2);
     ck(cudaMemset(h->ctl.p, 0, kCtlInts * sizeof(int) * 2), "memset ctl");
 
@@ -583,12 +708,6 @@ int qvmc_cuda_last_stats(qvmc_ham_t h, qvmc_stats* out) {
     }
     out->candidates = st[0];
     out->pairs = st[1];
-    const int pmax = mm[0], pmin = 1024 - mm[1];
-    const int side = (pmin <= h->n - pmin) ? 1 : 0;
-    const int s = side ? pmin : h->n - pmin;
-    out->sector_mode = (pmin == pmax && s <= kMaxMinority) ? 1 : 0;
-    out->sector_side = side;
-    out->minority_count = s;
   });
 }
 
@@ -618,11 +737,14 @@ int qvmc_cuda_pairs(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, int mem, 
         const int err = read_err_and_reset(h);
         if (err) raise_device_err(err);
       }
+      const RowPlan P = plan_rows(h, n_unq);
+      note_plan(h, P);
+      if (P.join) DISPATCH_W(W, build_join_index<WW>(h, dkeys, n_unq, P));
       h->counts.ensure((n_unq + 1) * sizeof(uint32_t));
       h->row_off.ensure((n_unq + 1) * sizeof(uint64_t));
       RowOut O{};
       O.counts = h->counts.as<uint32_t>();
-      DISPATCH_W(W, (launch_rows<WW, kModeCount>(h, dkeys, 0, n_unq, O)));
+      DISPATCH_W(W, (run_rows<WW, kModeCount>(h, dkeys, 0, n_unq, P, O)));
       // exclusive scan of the per-row counts (as u64)
       ck(cudaMemsetAsync(h->counts.as<uint32_t>() + n_unq, 0, sizeof(uint32_t), h->stream), "memset");
       size_t tmp = 0;
@@ -643,7 +765,7 @@ int qvmc_cuda_pairs(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, int mem, 
       O.row_off = roff;
       O.xp_out = h->xp_a.as<uint32_t>();
       O.g_out = h->g_a.as<uint32_t>();
-      DISPATCH_W(W, (launch_rows<WW, kModeEmit>(h, dkeys, 0, n_unq, O)));
+      DISPATCH_W(W, (run_rows<WW, kModeEmit>(h, dkeys, 0, n_unq, P, O)));
       // canonical order inside each row: by x' (coupling.cpp:49-52)
       tmp = 0;
       ck(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tmp, h->xp_a.as<uint32_t>(), h->xp_b.as<uint32_t>(),
@@ -834,14 +956,20 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
     record_stats(h, rows);
     ck(cudaMemsetAsync(static_cast<int*>(h->ctl.p) + 6, 0, 4 * sizeof(int), h->stream), "memset stats");
     ck(cudaEventRecord(h->ev[0], h->stream), "event");
-    if (n_unq > 0) DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
+    RowPlan P;
+    if (n_unq > 0) {
+      DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
+      P = plan_rows(h, n_unq);
+      note_plan(h, P);
+      if (P.join) DISPATCH_W(W, build_join_index<WW>(h, dkeys, n_unq, P));
+    }
     ck(cudaEventRecord(h->ev[1], h->stream), "event");
     if (n_unq > 0) {
       RowOut O{};
       O.eloc = deloc;
       O.la = dla;
       O.ph = dph;
-      DISPATCH_W(W, (launch_rows<WW, kModeEloc>(h, dkeys, row_begin, row_end, O)));
+      DISPATCH_W(W, (run_rows<WW, kModeEloc>(h, dkeys, row_begin, row_end, P, O)));
     }
     ck(cudaEventRecord(h->ev[2], h->stream), "event");
     double* dm = out_moments;
