@@ -262,6 +262,67 @@ DevicePlan plan_device(const HostIndex& h) {
     }
   }
 
+  // family compression of the large groups (the 2+2(N-2)-term single
+  // excitations of JW Hamiltonians: an XX and a YY family, each with one
+  // optional Z dressing per term)
+  p.comp_of.assign(n_xy, -1);
+  p.fam_off.push_back(0);
+  for (uint32_t g = 0; g < n_xy; ++g) {
+    if (static_cast<int64_t>(g) == h.diag) continue;
+    const uint64_t t0 = h.offsets[g], t1 = h.offsets[g + 1];
+    if (t1 - t0 <= kSmallGroupHost) continue;
+    struct Fam {
+      std::vector<uint64_t> B;
+      uint8_t q;
+      long double u = 0;
+      std::vector<long double> v;
+    };
+    std::vector<Fam> fams;
+    bool ok = true;
+    for (uint64_t t = t0; t < t1 && ok; ++t) {
+      const uint8_t q = h.y_weight[t] & 3;
+      const uint64_t* yz = &h.yz[t * W];
+      int pick = -1, bitpos = -1;
+      for (size_t f = 0; f < fams.size() && pick < 0; ++f) {
+        if (fams[f].q != q) continue;
+        int pc = 0, bp = -1;
+        for (int w = 0; w < W; ++w) {
+          const uint64_t d = yz[w] ^ fams[f].B[w];
+          pc += std::popcount(d);
+          if (d) bp = w * 64 + std::countr_zero(d);
+        }
+        if (pc <= 1) {
+          pick = static_cast<int>(f);
+          bitpos = pc ? bp : -1;
+        }
+      }
+      if (pick < 0) {
+        if (static_cast<int>(fams.size()) == kMaxFamilies) {
+          ok = false;
+          break;
+        }
+        fams.push_back(Fam{std::vector<uint64_t>(yz, yz + W), q, 0, std::vector<long double>(n, 0)});
+        pick = static_cast<int>(fams.size()) - 1;
+      }
+      if (bitpos < 0) fams[pick].u += h.coeff[t];
+      else fams[pick].v[bitpos] += h.coeff[t];
+    }
+    if (!ok) continue;
+    p.comp_of[g] = static_cast<int32_t>(p.fam_off.size() - 1);
+    for (const Fam& f : fams) {
+      p.fam_B.insert(p.fam_B.end(), f.B.begin(), f.B.end());
+      p.fam_q.push_back(f.q);
+      p.fam_u.push_back(static_cast<double>(f.u));
+      long double V = 0;
+      for (int k = 0; k < n; ++k) {
+        V += f.v[k];
+        p.fam_v.push_back(static_cast<double>(f.v[k]));
+      }
+      p.fam_V.push_back(static_cast<double>(V));
+    }
+    p.fam_off.push_back(static_cast<uint32_t>(p.fam_q.size()));
+  }
+
   // flip-mask hash table for the join path, same bucket layout as the
   // device-built sample-set table (load <= 1/4)
   {

@@ -11,6 +11,8 @@ namespace qvmc_b200 {
 
 constexpr int kMaxWords = 4;        // 256 qubits, BasisVector::kMaxBits (basis_vector.hpp:29)
 constexpr int kMaxMinority = 32;    // sector lists are used when min(n_e, N - n_e) <= 32
+constexpr uint32_t kSmallGroupHost = 16;  // groups above this size are candidates for compression
+constexpr int kMaxFamilies = 4;
 
 // HamiltonianIndex (proj/include/qvmc/hamiltonian.hpp:41-107) as flat arrays.
 struct HostIndex {
@@ -59,6 +61,15 @@ struct DevicePlan {
   std::vector<double> diag_K;       // [N][N]
   std::vector<uint32_t> diag_other; // diagonal terms with |z| >= 3
   std::vector<uint64_t> hash_bytes; // [n_words*8][256]
+  // compressed large groups: a group whose terms share a few base yz masks
+  // (differing by at most one Z per term) is summed as families
+  //   i^q_f (-1)^{|x' & B_f|} [u_f + sum_k v_f[k] (-1)^{x'_k}]
+  std::vector<int32_t> comp_of;     // [n_xy] compressed-group id or -1
+  std::vector<uint32_t> fam_off;    // [n_comp+1]
+  std::vector<uint64_t> fam_B;      // [n_fam][W]
+  std::vector<uint8_t> fam_q;       // [n_fam] y-weight mod 4
+  std::vector<double> fam_u, fam_V; // [n_fam] constant part, sum_k v_f[k]
+  std::vector<double> fam_v;        // [n_fam][N]
   // flip-mask hash table (join path): buckets of 4 x (tag32 << 32 | group)
   std::vector<uint64_t> xy_tab;
   uint64_t xy_tab_mask = 0;

@@ -121,11 +121,11 @@ struct qvmc_ham_s {
   cudaStream_t own = nullptr, stream = nullptr;
   // Hamiltonian
   DBuf xy, xy_hash, goff, coeff, yz, yw, xyw, gen_hash, gen_g, lst_off, lst_hash, lst_g, res_g, diag_b, diag_K,
-      diag_other, hash_bytes, xy_tab, codes;
+      diag_other, hash_bytes, xy_tab, codes, comp_of, fam_off, fam_B, fam_q, fam_u, fam_V, fam_v;
   uint64_t xy_tab_mask = 0;
   HamView view{};
   // join path (per call): deletion-index workspace
-  DBuf j_hsh, j_key, j_val, j_key2, j_val2, j_rng, j_uniq, j_cnt, j_off, j_nruns, j_tmp;
+  DBuf j_hsh, j_rec, j_key, j_val, j_key2, j_val2, j_rng, j_uniq, j_cnt, j_off, j_nruns, j_tmp;
   bool use_join = true;
   // workspace
   DBuf tab, ctl, keys, la, ph, lp, eloc, partials, moments, weights;
@@ -355,6 +355,7 @@ void build_join_index(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowP
   const uint32_t C = static_cast<uint32_t>(P.s * (P.s - 1) / 2);
   const uint64_t E = static_cast<uint64_t>(n) * C;
   h->j_hsh.ensure(n * 8 + 16);
+  h->j_rec.ensure(n * 8 * rec_words<W>() + 16);
   h->j_key.ensure(E * 4 + 16);
   h->j_val.ensure(E * 4 + 16);
   h->j_key2.ensure(E * 4 + 16);
@@ -367,7 +368,7 @@ void build_join_index(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowP
   const int grid = static_cast<int>(std::min<int64_t>((n + kThreads - 1) / kThreads, grid_for(h, 8)));
   k_join_keys<W><<<std::max(grid, 1), kThreads, 0, h->stream>>>(
       keys, n, h->n, P.side, P.s, h->view.hash_bytes, h->codes.as<uint64_t>(), h->j_hsh.as<uint64_t>(),
-      h->j_key.as<uint32_t>(), h->j_val.as<uint32_t>());
+      h->j_rec.as<uint64_t>(), h->j_key.as<uint32_t>(), h->j_val.as<uint32_t>());
   ck_launch("join keys");
   const int ne = static_cast<int>(E);
   size_t b1 = 0, b2 = 0, b3 = 0;
@@ -402,6 +403,7 @@ JoinView join_view(qvmc_ham_s* h, const RowPlan& P) {
   J.rng = h->j_rng.as<uint2>();
   J.vals = h->j_val2.as<uint32_t>();
   J.hsh = h->j_hsh.as<uint64_t>();
+  J.rec = h->j_rec.as<uint64_t>();
   J.xy_tab = h->xy_tab.as<uint64_t>();
   J.xy_mask = h->xy_tab_mask;
   J.codes = h->codes.as<uint64_t>();
@@ -613,6 +615,13 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     upload(h->diag_other, p.diag_other);
     upload(h->hash_bytes, p.hash_bytes);
     upload(h->xy_tab, p.xy_tab);
+    upload(h->comp_of, p.comp_of);
+    upload(h->fam_off, p.fam_off);
+    upload(h->fam_B, p.fam_B);
+    upload(h->fam_q, p.fam_q);
+    upload(h->fam_u, p.fam_u);
+    upload(h->fam_V, p.fam_V);
+    upload(h->fam_v, p.fam_v);
     h->xy_tab_mask = p.xy_tab_mask;
     upload(h->codes, std::vector<uint64_t>(qubit_codes(), qubit_codes() + 256));
     if (const char* e = std::getenv("QVMC_JOIN")) h->use_join = std::atoi(e) != 0;
@@ -646,6 +655,13 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     v.diag_other = h->diag_other.as<uint32_t>();
     v.n_diag_other = static_cast<uint32_t>(p.diag_other.size());
     v.hash_bytes = h->hash_bytes.as<uint64_t>();
+    v.comp_of = h->comp_of.as<int32_t>();
+    v.fam_off = h->fam_off.as<uint32_t>();
+    v.fam_B = h->fam_B.as<uint64_t>();
+    v.fam_q = h->fam_q.as<uint8_t>();
+    v.fam_u = h->fam_u.as<double>();
+    v.fam_V = h->fam_V.as<double>();
+    v.fam_v = h->fam_v.as<double>();
     ck(cudaDeviceSynchronize(), "upload sync");
     *out = h.release();
   });

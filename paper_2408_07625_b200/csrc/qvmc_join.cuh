@@ -22,6 +22,10 @@
 
 namespace qvmc_b200 {
 
+#ifndef QVMC_JOIN_MINB
+#define QVMC_JOIN_MINB 4  // 64 registers: 32 resident warps per SM (measured best)
+#endif
+
 constexpr int kJoinMaxMinority = 16;  // s <= 16: at most 120 buckets per row
 constexpr int kJoinMaxRanges = kJoinMaxMinority * (kJoinMaxMinority - 1) / 2;
 
@@ -30,6 +34,7 @@ struct JoinView {
   const uint2* rng;               // [N*C] (lo, hi) bucket range in vals, entry id y*C + t
   const uint32_t* vals;           // sorted entry ids
   const uint64_t* hsh;            // [N] linear key hash of each sample
+  const uint64_t* rec;            // [N][RW]: key words + hash (one 32 B sector for W <= 3)
   const uint64_t* xy_tab;         // flip-mask hash table, buckets of 4 x (tag32 | group)
   uint64_t xy_mask;
   const uint64_t* codes;          // [256] qubit codes of the linear hash
@@ -45,16 +50,31 @@ __device__ __forceinline__ uint32_t pair_b(int pi) {  // pairs ordered by b then
 // Per sample: its linear hash and, for every pair T of its minority set, the
 // 32-bit bucket key fmix(hash(S(y) - T)) with value y*C + t.
 template <int W>
+constexpr int rec_words() {  // key words + hash word, padded to 16 B
+  return (W + 2) & ~1;
+}
+
+template <int W>
 __global__ void __launch_bounds__(kThreads)
     k_join_keys(const uint64_t* __restrict__ keys, int64_t n, int n_qubits, int side, int s,
                 const uint64_t* __restrict__ hb, const uint64_t* __restrict__ codes, uint64_t* __restrict__ hsh,
-                uint32_t* __restrict__ bkey, uint32_t* __restrict__ bval) {
+                uint64_t* __restrict__ rec, uint32_t* __restrict__ bkey, uint32_t* __restrict__ bval) {
   const uint32_t C = static_cast<uint32_t>(s * (s - 1) / 2);
   for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < n; y += (int64_t)gridDim.x * blockDim.x) {
     uint64_t x[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) x[w] = keys[y * W + w];
-    hsh[y] = key_hash_thread<W>(x, hb);
+    const uint64_t hy = key_hash_thread<W>(x, hb);
+    hsh[y] = hy;
+    {
+      constexpr int RW = rec_words<W>();
+      uint64_t r[RW];
+#pragma unroll
+      for (int w = 0; w < RW; ++w) r[w] = w < W ? x[w] : (w == W ? hy : 0ull);
+      ulonglong2* dst = reinterpret_cast<ulonglong2*>(rec + y * RW);
+#pragma unroll
+      for (int w = 0; w < RW; w += 2) dst[w / 2] = make_ulonglong2(r[w], r[w + 1]);
+    }
     uint8_t pos[kJoinMaxMinority];
     uint64_t hs = 0;
     int k = 0;
@@ -127,7 +147,7 @@ __device__ __forceinline__ bool bit_at(const uint64_t* v, int p) {
 }
 
 template <int W, int MODE>
-__global__ void __launch_bounds__(kThreads) k_rows_join(const __grid_constant__ HamView H, const TableView T,
+__global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __grid_constant__ HamView H, const TableView T,
                                                         const __grid_constant__ JoinView J,
                                                         const uint64_t* __restrict__ keys, int64_t row_begin,
                                                         int64_t row_end, int side, int s,
@@ -154,6 +174,9 @@ __global__ void __launch_bounds__(kThreads) k_rows_join(const __grid_constant__ 
     uint64_t x[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) x[w] = __ldg(keys + row * W + w);
+    Key<W> xrow;
+#pragma unroll
+    for (int w = 0; w < W; ++w) xrow.w[w] = x[w];
     double la_i = 0.0, ph_i = 0.0;
     if (MODE == kModeEloc) {
       la_i = __ldg(O.la + row);
@@ -228,14 +251,23 @@ __global__ void __launch_bounds__(kThreads) k_rows_join(const __grid_constant__ 
           }
         }
       }
+      constexpr int RW = rec_words<W>();
       uint64_t yk[U][W];
       uint64_t hy[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (y[u] != 0xffffffffu) {
+          const ulonglong2* src = reinterpret_cast<const ulonglong2*>(J.rec + (int64_t)y[u] * RW);
+          uint64_t r[RW];
 #pragma unroll
-          for (int w = 0; w < W; ++w) yk[u][w] = __ldg(keys + (int64_t)y[u] * W + w);
-          hy[u] = __ldg(J.hsh + y[u]);
+          for (int w = 0; w < RW; w += 2) {
+            const ulonglong2 v = __ldg(src + w / 2);
+            r[w] = v.x;
+            r[w + 1] = v.y;
+          }
+#pragma unroll
+          for (int w = 0; w < W; ++w) yk[u][w] = r[w];
+          hy[u] = r[W];
         }
       }
 #pragma unroll
@@ -281,7 +313,7 @@ __global__ void __launch_bounds__(kThreads) k_rows_join(const __grid_constant__ 
       if (MODE == kModeEloc) {
         __syncwarp();
         if (sm->qn >= kDrainAt) {
-          const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane);
+          const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane, xrow, s, side);
           acc.x += d.x;
           acc.y += d.y;
         }
@@ -315,7 +347,7 @@ __global__ void __launch_bounds__(kThreads) k_rows_join(const __grid_constant__ 
       if (MODE == kModeEloc) {
         __syncwarp();
         if (sm->qn >= kDrainAt) {
-          const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane);
+          const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane, xrow, s, side);
           acc.x += d.x;
           acc.y += d.y;
         }
@@ -359,7 +391,7 @@ __global__ void __launch_bounds__(kThreads) k_rows_join(const __grid_constant__ 
     if (MODE == kModeEloc) {
       __syncwarp();
       if (sm->qn > 0) {
-        const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane);
+        const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane, xrow, s, side);
         acc.x += d.x;
         acc.y += d.y;
       }

@@ -50,6 +50,13 @@ struct HamView {
   const uint32_t* diag_other;
   uint32_t n_diag_other;
   const uint64_t* hash_bytes;  // [W*8][256]
+  const int32_t* comp_of;      // compressed large groups (host_index.h DevicePlan)
+  const uint32_t* fam_off;
+  const uint64_t* fam_B;
+  const uint8_t* fam_q;
+  const double* fam_u;
+  const double* fam_V;
+  const double* fam_v;
 };
 
 struct TableView {
@@ -269,11 +276,55 @@ __device__ __forceinline__ void add_ratio(const double* __restrict__ la, const d
   acc.y += hr * s + hi * c;
 }
 
+// H_{xx'} of a compressed group (sector mode): per family f,
+//   i^q_f (-1)^{|x' & B_f|} (u_f + sum_k v_f[k] (-1)^{x'_k}),
+// with sum_k v_f[k] (-1)^{x'_k} = +-(V_f - 2 sum_{k in S(x')} v_f[k]) over the
+// minority set S(x') = S(x) ^ (x ^ x'): s + |m| loads instead of the terms.
+template <int W>
+__device__ __forceinline__ void comp_element(const HamView& H, const uint64_t* x, const uint64_t* xp, int32_t c,
+                                             const uint16_t* pos, int s, int side, double& re, double& im) {
+  re = 0.0;
+  im = 0.0;
+  const int n = H.n;
+  uint64_t m[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) m[w] = x[w] ^ xp[w];
+  const uint32_t f1 = __ldg(H.fam_off + c + 1);
+  for (uint32_t f = __ldg(H.fam_off + c); f < f1; ++f) {
+    const double* v = H.fam_v + static_cast<int64_t>(f) * n;
+    double sv = 0.0;
+    for (int a = 0; a < s; ++a) sv += __ldg(v + pos[a]);
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      uint64_t bits = m[w];
+      while (bits) {
+        const int k = 64 * w + __ffsll(static_cast<long long>(bits)) - 1;
+        bits &= bits - 1;
+        const bool in_s = ((x[w] >> (k & 63)) & 1ull) == static_cast<uint64_t>(side);
+        sv += in_s ? -__ldg(v + k) : __ldg(v + k);
+      }
+    }
+    const double V = __ldg(H.fam_V + f);
+    double val = __ldg(H.fam_u + f) + (side ? V - 2.0 * sv : 2.0 * sv - V);
+    int pc = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) pc += __popcll(xp[w] & __ldg(H.fam_B + static_cast<int64_t>(f) * W + w));
+    if (pc & 1) val = -val;
+    const int q = __ldg(H.fam_q + f);
+    if (q == 0) re += val;
+    else if (q == 1) im += val;
+    else if (q == 2) re -= val;
+    else im -= val;
+  }
+}
+
 // Drain the warp's hit queue: returns this lane's share of sum H_{xx'} psi(x')/psi(x).
+// s > 0: sector mode with the row's minority orbitals in sm->pos (enables
+// compressed groups); s == 0: every group term by term.
 template <int W>
 __device__ __noinline__ double2 drain(const HamView& H, const uint64_t* __restrict__ keys,
                                       const double* __restrict__ la, const double* __restrict__ ph, double la_i,
-                                      double ph_i, WarpSmem* sm, int lane) {
+                                      double ph_i, WarpSmem* sm, int lane, Key<W> xrow, int s, int side) {
   double2 acc = make_double2(0.0, 0.0);
   __syncwarp();
   const unsigned n = sm->qn;
@@ -286,14 +337,19 @@ __device__ __noinline__ double2 drain(const HamView& H, const uint64_t* __restri
       t0 = __ldg(H.goff + g);
       t1 = __ldg(H.goff + g + 1);
     }
-    const bool large = k < n && t1 - t0 > kSmallGroup;
-    // small groups: one hit per lane, term by term in the reference order
+    const int32_t comp = (k < n && s > 0 && t1 - t0 > kSmallGroup) ? __ldg(H.comp_of + g) : -1;
+    const bool large = k < n && t1 - t0 > kSmallGroup && comp < 0;
+    // small groups: one hit per lane, term by term in the reference order;
+    // compressed groups: one hit per lane through the family sums
     if (k < n && !large) {
       uint64_t xp[W];
 #pragma unroll
       for (int w = 0; w < W; ++w) xp[w] = __ldg(keys + (int64_t)j * W + w);
       double hr, hi;
-      group_element<W>(H, xp, g, hr, hi);
+      if (comp >= 0)
+        comp_element<W>(H, xrow.w, xp, comp, sm->pos, s, side, hr, hi);
+      else
+        group_element<W>(H, xp, g, hr, hi);
       add_ratio(la, ph, la_i, ph_i, j, hr, hi, acc);
     }
     // large groups: the warp splits the terms; the element is parked in lane src
@@ -380,6 +436,9 @@ __global__ void __launch_bounds__(kThreads) k_rows(const __grid_constant__ HamVi
     uint64_t x[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) x[w] = __ldg(keys + row * W + w);
+    Key<W> xrow;
+#pragma unroll
+    for (int w = 0; w < W; ++w) xrow.w[w] = x[w];
     double la_i = 0.0, ph_i = 0.0;
     if (MODE == kModeEloc) {
       la_i = __ldg(O.la + row);
@@ -503,7 +562,7 @@ __global__ void __launch_bounds__(kThreads) k_rows(const __grid_constant__ HamVi
       if (MODE == kModeEloc) {
         __syncwarp();
         if (sm->qn >= kDrainAt) {
-          const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane);
+          const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane, xrow, sector ? s : 0, side);
           acc.x += d.x;
           acc.y += d.y;
         }
@@ -538,7 +597,7 @@ __global__ void __launch_bounds__(kThreads) k_rows(const __grid_constant__ HamVi
         if (MODE == kModeEloc) {
           __syncwarp();
           if (sm->qn >= kDrainAt) {
-            const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane);
+            const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane, xrow, sector ? s : 0, side);
             acc.x += d.x;
             acc.y += d.y;
           }
@@ -589,7 +648,7 @@ __global__ void __launch_bounds__(kThreads) k_rows(const __grid_constant__ HamVi
     if (MODE == kModeEloc) {
       __syncwarp();
       if (sm->qn > 0) {
-        const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane);
+        const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane, xrow, sector ? s : 0, side);
         acc.x += d.x;
         acc.y += d.y;
       }
