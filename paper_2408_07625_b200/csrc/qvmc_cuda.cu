@@ -11,6 +11,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
 #include <cub/device/device_segmented_sort.cuh>
 #include <memory>
 #include <stdexcept>
@@ -125,7 +127,8 @@ struct qvmc_ham_s {
   uint64_t xy_tab_mask = 0;
   HamView view{};
   // join path (per call): deletion-index workspace
-  DBuf j_hsh, j_rec, j_key, j_val, j_key2, j_val2, j_rng, j_uniq, j_cnt, j_off, j_nruns, j_tmp;
+  DBuf l_key, l_key2, l_idx, l_perm, l_keys, l_la, l_ph, l_flags, l_list, l_nsel;
+  DBuf j_key, j_val, j_key2, j_val2, j_rng, j_uniq, j_cnt, j_off, j_nruns, j_tmp;
   bool use_join = true;
   // workspace
   DBuf tab, ctl, keys, la, ph, lp, eloc, partials, moments, weights;
@@ -354,8 +357,6 @@ template <int W>
 void build_join_index(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowPlan& P) {
   const uint32_t C = static_cast<uint32_t>(P.s * (P.s - 1) / 2);
   const uint64_t E = static_cast<uint64_t>(n) * C;
-  h->j_hsh.ensure(n * 8 + 16);
-  h->j_rec.ensure(n * 8 * rec_words<W>() + 16);
   h->j_key.ensure(E * 4 + 16);
   h->j_val.ensure(E * 4 + 16);
   h->j_key2.ensure(E * 4 + 16);
@@ -367,8 +368,7 @@ void build_join_index(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowP
   h->j_nruns.ensure(16);
   const int grid = static_cast<int>(std::min<int64_t>((n + kThreads - 1) / kThreads, grid_for(h, 8)));
   k_join_keys<W><<<std::max(grid, 1), kThreads, 0, h->stream>>>(
-      keys, n, h->n, P.side, P.s, h->view.hash_bytes, h->codes.as<uint64_t>(), h->j_hsh.as<uint64_t>(),
-      h->j_rec.as<uint64_t>(), h->j_key.as<uint32_t>(), h->j_val.as<uint32_t>());
+      keys, n, h->n, P.side, P.s, h->codes.as<uint64_t>(), h->j_key.as<uint32_t>(), h->j_val.as<uint32_t>());
   ck_launch("join keys");
   const int ne = static_cast<int>(E);
   size_t b1 = 0, b2 = 0, b3 = 0;
@@ -392,7 +392,7 @@ void build_join_index(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowP
   g_launches += 3;
   const int rgrid = static_cast<int>(std::min<uint64_t>((E + kThreads - 1) / kThreads, grid_for(h, 8)));
   k_join_ranges<<<std::max(rgrid, 1), kThreads, 0, h->stream>>>(h->j_off.as<uint32_t>(), h->j_cnt.as<uint32_t>(),
-                                                                h->j_nruns.as<int>(), h->j_val2.as<uint32_t>(),
+                                                                h->j_nruns.as<int>(), h->j_val2.as<uint32_t>(), C,
                                                                 h->j_rng.as<uint2>());
   ck_launch("join ranges");
 }
@@ -402,8 +402,6 @@ JoinView join_view(qvmc_ham_s* h, const RowPlan& P) {
   J.C = static_cast<uint32_t>(P.s * (P.s - 1) / 2);
   J.rng = h->j_rng.as<uint2>();
   J.vals = h->j_val2.as<uint32_t>();
-  J.hsh = h->j_hsh.as<uint64_t>();
-  J.rec = h->j_rec.as<uint64_t>();
   J.xy_tab = h->xy_tab.as<uint64_t>();
   J.xy_mask = h->xy_tab_mask;
   J.codes = h->codes.as<uint64_t>();
@@ -411,16 +409,15 @@ JoinView join_view(qvmc_ham_s* h, const RowPlan& P) {
 }
 
 template <int W, int MODE>
-void launch_rows_join(qvmc_ham_s* h, const uint64_t* keys, int64_t r0, int64_t r1, const RowPlan& P,
-                      const RowOut& O) {
+void launch_rows_join(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const RowPlan& P, const RowOut& O) {
   ck(cudaMemsetAsync(static_cast<int*>(h->ctl.p) + 4, 0, 2 * sizeof(int), h->stream), "memset row counter");
   int per_sm = 0;
   ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_join<W, MODE>, kThreads, 0), "occupancy");
-  const int64_t blocks_needed = (r1 - r0 + kWarps - 1) / kWarps;
+  const int64_t blocks_needed = (R.n_rows + kWarps - 1) / kWarps;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_needed, grid_for(h, per_sm))));
   TableView T{h->tab.as<uint64_t>(), h->tab_buckets - 1};
-  if (r1 > r0) {
-    k_rows_join<W, MODE><<<grid, kThreads, 0, h->stream>>>(h->view, T, join_view(h, P), keys, r0, r1, P.side, P.s,
+  if (R.n_rows > 0) {
+    k_rows_join<W, MODE><<<grid, kThreads, 0, h->stream>>>(h->view, T, join_view(h, P), keys, R, P.side, P.s,
                                                          ctl_view(h), O);
     ck_launch("row kernel (join)");
   }
@@ -429,9 +426,67 @@ void launch_rows_join(qvmc_ham_s* h, const uint64_t* keys, int64_t r0, int64_t r
 template <int W, int MODE>
 void run_rows(qvmc_ham_s* h, const uint64_t* keys, int64_t r0, int64_t r1, const RowPlan& P, const RowOut& O) {
   if (P.join)
-    launch_rows_join<W, MODE>(h, keys, r0, r1, P, O);
+    launch_rows_join<W, MODE>(h, keys, RowSet{r1 - r0, r0, nullptr, nullptr, r0}, P, O);
   else
     launch_rows<W, MODE>(h, keys, r0, r1, O);
+}
+
+// Join mode of the fused call: sort the sample set by minority orbitals
+// (locality), rebuild the index on the sorted copy, process rows in that
+// order. Returns the row set; keys/la/ph are redirected to the sorted copies.
+template <int W>
+RowSet sort_for_locality(qvmc_ham_s* h, const uint64_t*& keys, const double*& la, const double*& ph, int64_t n,
+                         int64_t r0, int64_t r1, const RowPlan& P) {
+  h->l_key.ensure(n * 8 + 16);
+  h->l_key2.ensure(n * 8 + 16);
+  h->l_idx.ensure(n * 4 + 16);
+  h->l_perm.ensure(n * 4 + 16);
+  h->l_keys.ensure(n * 8 * W + 16);
+  h->l_la.ensure(n * 8 + 16);
+  h->l_ph.ensure(n * 8 + 16);
+  const int grid = static_cast<int>(std::min<int64_t>((n + kThreads - 1) / kThreads, grid_for(h, 8)));
+  k_locality_keys<W><<<std::max(grid, 1), kThreads, 0, h->stream>>>(keys, n, h->n, P.side, h->l_key.as<uint64_t>(),
+                                                                    h->l_idx.as<uint32_t>());
+  ck_launch("locality keys");
+  size_t bytes = 0;
+  const int ni = static_cast<int>(n);
+  ck(cub::DeviceRadixSort::SortPairs(nullptr, bytes, h->l_key.as<uint64_t>(), h->l_key2.as<uint64_t>(),
+                                     h->l_idx.as<uint32_t>(), h->l_perm.as<uint32_t>(), ni, 0, 64, h->stream),
+     "sort size");
+  h->j_tmp.ensure(bytes + 16);
+  ck(cub::DeviceRadixSort::SortPairs(h->j_tmp.p, bytes, h->l_key.as<uint64_t>(), h->l_key2.as<uint64_t>(),
+                                     h->l_idx.as<uint32_t>(), h->l_perm.as<uint32_t>(), ni, 0, 64, h->stream),
+     "sort");
+  ++g_launches;
+  k_gather_sorted<W><<<std::max(grid, 1), kThreads, 0, h->stream>>>(
+      h->l_perm.as<uint32_t>(), n, keys, la, ph, h->l_keys.as<uint64_t>(), h->l_la.as<double>(),
+      h->l_ph.as<double>());
+  ck_launch("gather sorted");
+  keys = h->l_keys.as<uint64_t>();
+  la = h->l_la.as<double>();
+  ph = h->l_ph.as<double>();
+  RowSet R{n, 0, nullptr, h->l_perm.as<uint32_t>(), r0};
+  if (r0 != 0 || r1 != n) {  // a row shard: the sorted positions of its rows
+    h->l_flags.ensure(n + 16);
+    h->l_list.ensure(n * 4 + 16);
+    h->l_nsel.ensure(16);
+    k_flag_rows<<<std::max(grid, 1), kThreads, 0, h->stream>>>(h->l_perm.as<uint32_t>(), n, r0, r1,
+                                                               h->l_flags.as<uint8_t>());
+    ck_launch("flag rows");
+    bytes = 0;
+    thrust::counting_iterator<uint32_t> it(0);
+    ck(cub::DeviceSelect::Flagged(nullptr, bytes, it, h->l_flags.as<uint8_t>(), h->l_list.as<uint32_t>(),
+                                  h->l_nsel.as<int>(), ni, h->stream),
+       "select size");
+    h->j_tmp.ensure(bytes + 16);
+    ck(cub::DeviceSelect::Flagged(h->j_tmp.p, bytes, it, h->l_flags.as<uint8_t>(), h->l_list.as<uint32_t>(),
+                                  h->l_nsel.as<int>(), ni, h->stream),
+       "select");
+    ++g_launches;
+    R.list = h->l_list.as<uint32_t>();
+    R.n_rows = r1 - r0;
+  }
+  return R;
 }
 
 void note_plan(qvmc_ham_s* h, const RowPlan& P) {
@@ -973,19 +1028,31 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
     ck(cudaMemsetAsync(static_cast<int*>(h->ctl.p) + 6, 0, 4 * sizeof(int), h->stream), "memset stats");
     ck(cudaEventRecord(h->ev[0], h->stream), "event");
     RowPlan P;
+    RowSet R{};
+    const uint64_t* rkeys = dkeys;
+    const double* rla = dla;
+    const double* rph = dph;
     if (n_unq > 0) {
       DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
       P = plan_rows(h, n_unq);
       note_plan(h, P);
-      if (P.join) DISPATCH_W(W, build_join_index<WW>(h, dkeys, n_unq, P));
+      if (P.join) {
+        DISPATCH_W(W, R = sort_for_locality<WW>(h, rkeys, rla, rph, n_unq, row_begin, row_end, P));
+        if (h->view.n_res) DISPATCH_W(W, launch_table_build<WW>(h, rkeys, n_unq));  // residual probes: sorted ids
+        DISPATCH_W(W, build_join_index<WW>(h, rkeys, n_unq, P));
+      }
     }
     ck(cudaEventRecord(h->ev[1], h->stream), "event");
     if (n_unq > 0) {
       RowOut O{};
       O.eloc = deloc;
-      O.la = dla;
-      O.ph = dph;
-      DISPATCH_W(W, (run_rows<WW, kModeEloc>(h, dkeys, row_begin, row_end, P, O)));
+      O.la = rla;
+      O.ph = rph;
+      if (P.join) {
+        DISPATCH_W(W, (launch_rows_join<WW, kModeEloc>(h, rkeys, R, P, O)));
+      } else {
+        DISPATCH_W(W, (launch_rows<WW, kModeEloc>(h, dkeys, row_begin, row_end, O)));
+      }
     }
     ck(cudaEventRecord(h->ev[2], h->stream), "event");
     double* dm = out_moments;

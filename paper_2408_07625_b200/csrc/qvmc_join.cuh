@@ -26,6 +26,10 @@ namespace qvmc_b200 {
 #define QVMC_JOIN_MINB 4  // 64 registers: 32 resident warps per SM (measured best)
 #endif
 
+#ifndef QVMC_JOIN_UNROLL
+#define QVMC_JOIN_UNROLL 4  // bucket members in flight per lane
+#endif
+
 constexpr int kJoinMaxMinority = 16;  // s <= 16: at most 120 buckets per row
 constexpr int kJoinMaxRanges = kJoinMaxMinority * (kJoinMaxMinority - 1) / 2;
 
@@ -33,8 +37,6 @@ struct JoinView {
   uint32_t C;                     // buckets per sample = s(s-1)/2
   const uint2* rng;               // [N*C] (lo, hi) bucket range in vals, entry id y*C + t
   const uint32_t* vals;           // sorted entry ids
-  const uint64_t* hsh;            // [N] linear key hash of each sample
-  const uint64_t* rec;            // [N][RW]: key words + hash (one 32 B sector for W <= 3)
   const uint64_t* xy_tab;         // flip-mask hash table, buckets of 4 x (tag32 | group)
   uint64_t xy_mask;
   const uint64_t* codes;          // [256] qubit codes of the linear hash
@@ -49,32 +51,70 @@ __device__ __forceinline__ uint32_t pair_b(int pi) {  // pairs ordered by b then
 
 // Per sample: its linear hash and, for every pair T of its minority set, the
 // 32-bit bucket key fmix(hash(S(y) - T)) with value y*C + t.
+// Rows of one call. Rows are processed in the order of the (locality-sorted)
+// key arrays; `perm` maps a key-array position back to the caller's row.
+struct RowSet {
+  int64_t n_rows;          // rows to process
+  int64_t base;            // position = base + r when list is null
+  const uint32_t* list;    // else position = list[r]
+  const uint32_t* perm;    // position -> caller row (null: identity)
+  int64_t out_base;        // outputs are indexed by caller row - out_base
+};
+
+// Locality order for the join: samples sorted by their minority orbitals,
+// highest first (top 8 packed into 64 bits), so that rows processed together
+// and the members of their buckets sit close in memory and in L2.
 template <int W>
-constexpr int rec_words() {  // key words + hash word, padded to 16 B
-  return (W + 2) & ~1;
+__global__ void __launch_bounds__(kThreads)
+    k_locality_keys(const uint64_t* __restrict__ keys, int64_t n, int n_qubits, int side, uint64_t* __restrict__ skey,
+                    uint32_t* __restrict__ sidx) {
+  for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < n; y += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = 0;
+    int got = 0;
+#pragma unroll
+    for (int w = W - 1; w >= 0; --w) {
+      uint64_t v = side ? keys[y * W + w] : ~keys[y * W + w];
+      const int hi_bit = n_qubits - 64 * w;
+      if (hi_bit < 64) v &= (hi_bit <= 0) ? 0ull : ((1ull << hi_bit) - 1);
+      while (v && got < 8) {
+        const int p = 64 * w + 63 - __clzll(static_cast<long long>(v));
+        k |= static_cast<uint64_t>(p) << (56 - 8 * got);
+        ++got;
+        v &= ~(1ull << (p & 63));
+      }
+    }
+    skey[y] = k;
+    sidx[y] = static_cast<uint32_t>(y);
+  }
+}
+
+template <int W>
+__global__ void k_gather_sorted(const uint32_t* __restrict__ perm, int64_t n, const uint64_t* __restrict__ keys,
+                                const double* __restrict__ la, const double* __restrict__ ph, uint64_t* keys_s,
+                                double* la_s, double* ph_s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t o = perm[i];
+#pragma unroll
+    for (int w = 0; w < W; ++w) keys_s[i * W + w] = keys[(int64_t)o * W + w];
+    la_s[i] = la[o];
+    ph_s[i] = ph[o];
+  }
+}
+
+__global__ void k_flag_rows(const uint32_t* __restrict__ perm, int64_t n, int64_t r0, int64_t r1, uint8_t* flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = perm[i] >= r0 && perm[i] < r1;
 }
 
 template <int W>
 __global__ void __launch_bounds__(kThreads)
     k_join_keys(const uint64_t* __restrict__ keys, int64_t n, int n_qubits, int side, int s,
-                const uint64_t* __restrict__ hb, const uint64_t* __restrict__ codes, uint64_t* __restrict__ hsh,
-                uint64_t* __restrict__ rec, uint32_t* __restrict__ bkey, uint32_t* __restrict__ bval) {
+                const uint64_t* __restrict__ codes, uint32_t* __restrict__ bkey, uint32_t* __restrict__ bval) {
   const uint32_t C = static_cast<uint32_t>(s * (s - 1) / 2);
   for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < n; y += (int64_t)gridDim.x * blockDim.x) {
     uint64_t x[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) x[w] = keys[y * W + w];
-    const uint64_t hy = key_hash_thread<W>(x, hb);
-    hsh[y] = hy;
-    {
-      constexpr int RW = rec_words<W>();
-      uint64_t r[RW];
-#pragma unroll
-      for (int w = 0; w < RW; ++w) r[w] = w < W ? x[w] : (w == W ? hy : 0ull);
-      ulonglong2* dst = reinterpret_cast<ulonglong2*>(rec + y * RW);
-#pragma unroll
-      for (int w = 0; w < RW; w += 2) dst[w / 2] = make_ulonglong2(r[w], r[w + 1]);
-    }
     uint8_t pos[kJoinMaxMinority];
     uint64_t hs = 0;
     int k = 0;
@@ -104,11 +144,15 @@ __global__ void __launch_bounds__(kThreads)
 // Per bucket (run of equal keys in the sorted array): store the range on
 // every member entry.
 __global__ void k_join_ranges(const uint32_t* __restrict__ run_off, const uint32_t* __restrict__ run_cnt,
-                              const int* __restrict__ n_runs, const uint32_t* __restrict__ vals, uint2* rng) {
+                              const int* __restrict__ n_runs, uint32_t* __restrict__ vals, uint32_t C, uint2* rng) {
   const int nr = *n_runs;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += gridDim.x * blockDim.x) {
     const uint32_t lo = run_off[r], hi = lo + run_cnt[r];
-    for (uint32_t p = lo; p < hi; ++p) rng[vals[p]] = make_uint2(lo, hi);
+    for (uint32_t p = lo; p < hi; ++p) {
+      const uint32_t e = vals[p];
+      rng[e] = make_uint2(lo, hi);
+      vals[p] = e / C;  // entry id -> sample
+    }
   }
 }
 
@@ -149,8 +193,8 @@ __device__ __forceinline__ bool bit_at(const uint64_t* v, int p) {
 template <int W, int MODE>
 __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __grid_constant__ HamView H, const TableView T,
                                                         const __grid_constant__ JoinView J,
-                                                        const uint64_t* __restrict__ keys, int64_t row_begin,
-                                                        int64_t row_end, int side, int s,
+                                                        const uint64_t* __restrict__ keys, const RowSet R,
+                                                        int side, int s,
                                                         const __grid_constant__ Ctl C,
                                                         const __grid_constant__ RowOut O) {
   __shared__ WarpSmem s_w[kWarps];
@@ -168,8 +212,9 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
     unsigned long long r = 0;
     if (lane == 0) r = atomicAdd(C.row_next, 1ull);
     r = __shfl_sync(0xffffffffu, r, 0);
-    const int64_t row = row_begin + static_cast<int64_t>(r);
-    if (row >= row_end) break;
+    if (static_cast<int64_t>(r) >= R.n_rows) break;
+    const int64_t row = R.list ? static_cast<int64_t>(__ldg(R.list + r)) : R.base + static_cast<int64_t>(r);
+    const int64_t orow = R.perm ? static_cast<int64_t>(__ldg(R.perm + row)) : row;  // caller's row
 
     uint64_t x[W];
 #pragma unroll
@@ -184,13 +229,12 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
       if (isinf(la_i)) {  // energy.cpp:32-33
         if (lane == 0) {
           atomicOr(C.err, kErrZeroAmp);
-          O.eloc[row - row_begin] = make_double2(CUDART_NAN, CUDART_NAN);
+          O.eloc[orow - R.out_base] = make_double2(CUDART_NAN, CUDART_NAN);
         }
         continue;
       }
     }
     if (MODE == kModeEmit && lane == 0) sm->cursor = 0;
-    const uint64_t hx = __ldg(J.hsh + row);
 
     uint64_t S[W];
 #pragma unroll
@@ -235,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
       if (++rg < n_ranges) len = sm->r_len[rg];
     }
     while (__any_sync(0xffffffffu, rg < n_ranges)) {
-      constexpr int U = kUnroll;
+      constexpr int U = QVMC_JOIN_UNROLL;
       uint32_t y[U];
       int tr[U];
 #pragma unroll
@@ -243,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
         y[u] = 0xffffffffu;
         tr[u] = rg;
         if (rg < n_ranges) {
-          y[u] = __ldg(J.vals + sm->r_lo[rg] + off) / J.C;
+          y[u] = __ldg(J.vals + sm->r_lo[rg] + off);
           off += 32;
           while (rg < n_ranges && off >= len) {
             off -= len;
@@ -251,23 +295,12 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
           }
         }
       }
-      constexpr int RW = rec_words<W>();
       uint64_t yk[U][W];
-      uint64_t hy[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (y[u] != 0xffffffffu) {
-          const ulonglong2* src = reinterpret_cast<const ulonglong2*>(J.rec + (int64_t)y[u] * RW);
-          uint64_t r[RW];
 #pragma unroll
-          for (int w = 0; w < RW; w += 2) {
-            const ulonglong2 v = __ldg(src + w / 2);
-            r[w] = v.x;
-            r[w + 1] = v.y;
-          }
-#pragma unroll
-          for (int w = 0; w < W; ++w) yk[u][w] = r[w];
-          hy[u] = r[W];
+          for (int w = 0; w < W; ++w) yk[u][w] = __ldg(keys + (int64_t)y[u] * W + w);
         }
       }
 #pragma unroll
@@ -297,7 +330,16 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
         }
         if (!ok) continue;
         ++cand;
-        const uint64_t f = fmix(hx ^ hy[u]);
+        uint64_t hm = 0;  // linear hash of the 2 or 4 flipped orbitals
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          uint64_t bits = m.w[w];
+          while (bits) {
+            hm ^= __ldg(J.codes + 64 * w + __ffsll(static_cast<long long>(bits)) - 1);
+            bits &= bits - 1;
+          }
+        }
+        const uint64_t f = fmix(hm);
         const ulonglong2* p = reinterpret_cast<const ulonglong2*>(J.xy_tab + (f & J.xy_mask) * 4);
         unsigned tm;
         bool full;
@@ -305,7 +347,8 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
         if (tm || full) {
           const int64_t g = xy_probe_slow<W>(m, f, J.xy_tab, J.xy_mask, H.xy);
           if (g >= 0) {
-            on_hit<W, MODE>(O, row, y[u], static_cast<uint32_t>(g), sm);
+            const int64_t jj = (MODE == kModeEmit && R.perm) ? static_cast<int64_t>(__ldg(R.perm + y[u])) : y[u];
+            on_hit<W, MODE>(O, orow, jj, static_cast<uint32_t>(g), sm);
             ++hits;
           }
         }
@@ -321,6 +364,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
     }
 
     // even flip masks of weight >= 6: popcount filter + sample-set probe
+    const uint64_t hx_res = H.n_res ? key_hash_warp<W>(x, H.hash_bytes, lane) : 0ull;
     for (uint32_t base = 0; base < H.n_res; base += 32) {
       const uint32_t e = base + lane;
       if (e < H.n_res) {
@@ -337,9 +381,9 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
 #pragma unroll
           for (int w = 0; w < W; ++w) xk.w[w] = x[w];
           ++cand;
-          const int64_t j = probe_slow<W>(xk, fmix(hx ^ __ldg(H.xy_hash + g)), g, T.tab, T.mask, keys, H.xy);
+          const int64_t j = probe_slow<W>(xk, fmix(hx_res ^ __ldg(H.xy_hash + g)), g, T.tab, T.mask, keys, H.xy);
           if (j >= 0) {
-            on_hit<W, MODE>(O, row, j, g, sm);
+            on_hit<W, MODE>(O, orow, (MODE == kModeEmit && R.perm) ? static_cast<int64_t>(__ldg(R.perm + j)) : j, g, sm);
             ++hits;
           }
         }
@@ -397,15 +441,15 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
       }
       const double re = warp_sum(acc.x);
       const double im = warp_sum(acc.y);
-      if (lane == 0) O.eloc[row - row_begin] = make_double2(re, im);
+      if (lane == 0) O.eloc[orow - R.out_base] = make_double2(re, im);
     }
     const uint32_t row_hits = warp_sum(hits) + (H.diag >= 0 ? 1u : 0u);
-    if (MODE == kModeCount && lane == 0) O.counts[row] = row_hits;
+    if (MODE == kModeCount && lane == 0) O.counts[orow] = row_hits;
     if (MODE == kModeEmit) {
       __syncwarp();
       if (lane == 0 && H.diag >= 0) {
-        const uint64_t at = O.row_off[row] + sm->cursor;
-        O.xp_out[at] = static_cast<uint32_t>(row);
+        const uint64_t at = O.row_off[orow] + sm->cursor;
+        O.xp_out[at] = static_cast<uint32_t>(orow);
         O.g_out[at] = static_cast<uint32_t>(H.diag);
       }
       __syncwarp();
