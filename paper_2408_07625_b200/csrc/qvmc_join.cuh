@@ -27,7 +27,7 @@ namespace qvmc_b200 {
 #endif
 
 #ifndef QVMC_JOIN_UNROLL
-#define QVMC_JOIN_UNROLL 4  // bucket members in flight per lane
+#define QVMC_JOIN_UNROLL 2  // bucket members in flight per lane (2 beat 4 and 8: fewer spills at 64 regs)
 #endif
 
 constexpr int kJoinMaxMinority = 16;  // s <= 16: at most 120 buckets per row
