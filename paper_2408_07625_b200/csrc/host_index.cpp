@@ -139,6 +139,21 @@ const uint64_t* qubit_codes() {
   return codes.data();
 }
 
+uint32_t xy_position_key(const uint64_t* words, int n_words) {
+  uint32_t key = 0xFFFFFFFFu;
+  int k = 0;
+  for (int w = 0; w < n_words && k < 4; ++w) {
+    uint64_t v = words[w];
+    while (v && k < 4) {
+      const uint32_t p = static_cast<uint32_t>(w * 64 + std::countr_zero(v));
+      key = (key & ~(0xFFu << (8 * k))) | (p << (8 * k));
+      ++k;
+      v &= v - 1;
+    }
+  }
+  return key;
+}
+
 uint64_t linear_hash(const uint64_t* words, int n_words) {
   const uint64_t* r = qubit_codes();
   uint64_t h = 0;
@@ -323,18 +338,21 @@ DevicePlan plan_device(const HostIndex& h) {
     p.fam_off.push_back(static_cast<uint32_t>(p.fam_q.size()));
   }
 
-  // flip-mask hash table for the join path, same bucket layout as the
-  // device-built sample-set table (load <= 1/4)
+  // flip-mask table for the join path: weight-2/4 masks keyed EXACTLY by
+  // their sorted orbital positions packed into 32 bits (0xFF pads weight 2),
+  // so a lookup needs no mask compare; buckets of 4 x (key32 << 32 | group),
+  // load <= 1/4, chained to the next bucket when full
   {
     uint64_t nb = 64;
     while (nb < n_xy) nb <<= 1;
     p.xy_tab.assign(nb * 4, ~uint64_t{0});
     p.xy_tab_mask = nb - 1;
     for (uint32_t g = 0; g < n_xy; ++g) {
-      if (static_cast<int64_t>(g) == h.diag) continue;
-      const uint64_t f = fmix_host(p.xy_hash[g]);
-      const uint64_t entry = (f >> 32) << 32 | g;
-      for (uint64_t b = f & p.xy_tab_mask;; b = (b + 1) & p.xy_tab_mask) {
+      const int wt = p.xy_weight[g];
+      if (static_cast<int64_t>(g) == h.diag || (wt != 2 && wt != 4)) continue;
+      const uint32_t key = xy_position_key(&h.xy[static_cast<size_t>(g) * W], W);
+      const uint64_t entry = static_cast<uint64_t>(key) << 32 | g;
+      for (uint64_t b = fmix_host(key) & p.xy_tab_mask;; b = (b + 1) & p.xy_tab_mask) {
         int k = 0;
         while (k < 4 && p.xy_tab[b * 4 + k] != ~uint64_t{0}) ++k;
         if (k < 4) {

@@ -39,6 +39,8 @@ HostIndex index_from_terms(int n_qubits, int n_words, int64_t n_raw, const doubl
 // of the set bits (so hash(x ^ m) = hash(x) ^ hash(m)).
 const uint64_t* qubit_codes();  // [256]
 uint64_t linear_hash(const uint64_t* words, int n_words);
+// orbital positions of a weight-2/4 mask, ascending, 8 bits each, 0xFF padded
+uint32_t xy_position_key(const uint64_t* words, int n_words);
 
 // Everything the kernels need besides the raw index, planned on the host.
 struct DevicePlan {
@@ -70,7 +72,7 @@ struct DevicePlan {
   std::vector<uint8_t> fam_q;       // [n_fam] y-weight mod 4
   std::vector<double> fam_u, fam_V; // [n_fam] constant part, sum_k v_f[k]
   std::vector<double> fam_v;        // [n_fam][N]
-  // flip-mask hash table (join path): buckets of 4 x (tag32 << 32 | group)
+  // flip-mask table (join path): buckets of 4 x (position key32 << 32 | group)
   std::vector<uint64_t> xy_tab;
   uint64_t xy_tab_mask = 0;
 };

@@ -156,29 +156,27 @@ __global__ void k_join_ranges(const uint32_t* __restrict__ run_off, const uint32
   }
 }
 
-// flip-mask table lookup: group of mask m (hash hm) or -1
-template <int W>
-__device__ __noinline__ int64_t xy_probe_slow(Key<W> m, uint64_t f, const uint64_t* __restrict__ tab, uint64_t mask,
-                                              const uint64_t* __restrict__ xym) {
-  const uint32_t tag = static_cast<uint32_t>(f >> 32);
-  uint64_t b = f & mask;
+// flip-mask table lookup by exact position key (host_index.cpp xy_position_key):
+// group of the mask or -1
+__device__ __forceinline__ int64_t xy_lookup(uint32_t key, const uint64_t* __restrict__ tab, uint64_t mask) {
+  uint64_t b = fmix(key) & mask;
   for (;;) {
     const ulonglong2* p = reinterpret_cast<const ulonglong2*>(tab + b * 4);
-    unsigned tm;
-    bool full;
-    bucket_test(__ldg(p), __ldg(p + 1), tag, tm, full);
-    while (tm) {
-      const int k = __ffs(tm) - 1;
-      tm &= tm - 1;
-      const uint32_t g = static_cast<uint32_t>(__ldg(tab + b * 4 + k));
-      bool same = true;
+    const ulonglong2 b0 = __ldg(p), b1 = __ldg(p + 1);
+    const uint64_t e[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
-      for (int w = 0; w < W; ++w) same &= __ldg(xym + (int64_t)g * W + w) == m.w[w];
-      if (same) return g;
+    for (int k = 0; k < 4; ++k) {
+      if (e[k] == kEmpty) return -1;
+      if (static_cast<uint32_t>(e[k] >> 32) == key) return static_cast<uint32_t>(e[k]);
     }
-    if (!full) return -1;
-    b = (b + 1) & mask;
+    b = (b + 1) & mask;  // full bucket: the chain continues
   }
+}
+
+__device__ __forceinline__ void sort2(int& a, int& b) {
+  const int lo = min(a, b), hi = max(a, b);
+  a = lo;
+  b = hi;
 }
 
 template <int W>
@@ -317,40 +315,52 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
           ps += __popcll(ms[w]);
         }
         const int ta = s_ta[wid][tr[u]], tb = s_tb[wid][tr[u]];
+        // accept rule (header comment) and the mask's exact position key
+        uint32_t key = 0;
         bool ok = false;
         if (pw == 4) {
-          ok = ps == 2 && bit_at<W>(ms, ta) && bit_at<W>(ms, tb);
-        } else if (pw == 2 && ps == 1) {
-          int cpos = 0;
+          if (ps == 2 && bit_at<W>(ms, ta) && bit_at<W>(ms, tb)) {
+            int o0 = -1, o1 = -1;  // the two created orbitals: bits of m outside S(x)
 #pragma unroll
-          for (int w = 0; w < W; ++w)
+            for (int w = 0; w < W; ++w) {
+              uint64_t v = m.w[w] & ~ms[w];
+              while (v) {
+                const int pp = 64 * w + __ffsll(static_cast<long long>(v)) - 1;
+                if (o0 < 0) o0 = pp; else o1 = pp;
+                v &= v - 1;
+              }
+            }
+            int p0 = ta, p1 = tb, p2 = o0, p3 = o1;  // ta < tb, o0 < o1: merge
+            sort2(p0, p2);
+            sort2(p1, p3);
+            sort2(p1, p2);
+            key = static_cast<uint32_t>(p0) | static_cast<uint32_t>(p1) << 8 | static_cast<uint32_t>(p2) << 16 |
+                  static_cast<uint32_t>(p3) << 24;
+            ok = true;
+          }
+        } else if (pw == 2 && ps == 1) {
+          int cpos = 0, apos = 0;
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
             if (ms[w]) cpos = 64 * w + __ffsll(static_cast<long long>(ms[w])) - 1;
+            const uint64_t o = m.w[w] & ~ms[w];
+            if (o) apos = 64 * w + __ffsll(static_cast<long long>(o)) - 1;
+          }
           const int other = cpos == ta ? tb : (cpos == tb ? ta : -1);
-          ok = other >= 0 && other == (cpos == pos0 ? pos1 : pos0);
+          if (other >= 0 && other == (cpos == pos0 ? pos1 : pos0)) {
+            int p0 = cpos, p1 = apos;
+            sort2(p0, p1);
+            key = static_cast<uint32_t>(p0) | static_cast<uint32_t>(p1) << 8 | 0xFFFF0000u;
+            ok = true;
+          }
         }
         if (!ok) continue;
         ++cand;
-        uint64_t hm = 0;  // linear hash of the 2 or 4 flipped orbitals
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          uint64_t bits = m.w[w];
-          while (bits) {
-            hm ^= __ldg(J.codes + 64 * w + __ffsll(static_cast<long long>(bits)) - 1);
-            bits &= bits - 1;
-          }
-        }
-        const uint64_t f = fmix(hm);
-        const ulonglong2* p = reinterpret_cast<const ulonglong2*>(J.xy_tab + (f & J.xy_mask) * 4);
-        unsigned tm;
-        bool full;
-        bucket_test(__ldg(p), __ldg(p + 1), static_cast<uint32_t>(f >> 32), tm, full);
-        if (tm || full) {
-          const int64_t g = xy_probe_slow<W>(m, f, J.xy_tab, J.xy_mask, H.xy);
-          if (g >= 0) {
-            const int64_t jj = (MODE == kModeEmit && R.perm) ? static_cast<int64_t>(__ldg(R.perm + y[u])) : y[u];
-            on_hit<W, MODE>(O, orow, jj, static_cast<uint32_t>(g), sm);
-            ++hits;
-          }
+        const int64_t g = xy_lookup(key, J.xy_tab, J.xy_mask);
+        if (g >= 0) {
+          const int64_t jj = (MODE == kModeEmit && R.perm) ? static_cast<int64_t>(__ldg(R.perm + y[u])) : y[u];
+          on_hit<W, MODE>(O, orow, jj, static_cast<uint32_t>(g), sm);
+          ++hits;
         }
       }
       if (MODE == kModeEloc) {
