@@ -173,6 +173,43 @@ __device__ __forceinline__ int64_t xy_lookup(uint32_t key, const uint64_t* __res
   }
 }
 
+constexpr uint32_t kNoKey = 0xFFFFFFFFu;
+
+// resolve a flip-mask lookup given its first bucket (already loaded)
+__device__ __forceinline__ int64_t xy_resolve(uint32_t key, uint64_t b, ulonglong2 b0, ulonglong2 b1,
+                                              const uint64_t* __restrict__ tab, uint64_t mask) {
+  for (;;) {
+    const uint64_t e[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (e[k] == kEmpty) return -1;
+      if (static_cast<uint32_t>(e[k] >> 32) == key) return static_cast<uint32_t>(e[k]);
+    }
+    b = (b + 1) & mask;  // full bucket: the chain continues
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(tab + b * 4);
+    b0 = __ldg(p);
+    b1 = __ldg(p + 1);
+  }
+}
+
+template <int W>
+__device__ __forceinline__ int lowest_bit(const uint64_t* v) {  // v != 0
+  int r = 0;
+#pragma unroll
+  for (int w = W - 1; w >= 0; --w)
+    if (v[w]) r = 64 * w + __ffsll(static_cast<long long>(v[w])) - 1;
+  return r;
+}
+
+template <int W>
+__device__ __forceinline__ int highest_bit(const uint64_t* v) {  // v != 0
+  int r = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w)
+    if (v[w]) r = 64 * w + 63 - __clzll(static_cast<long long>(v[w]));
+  return r;
+}
+
 __device__ __forceinline__ void sort2(int& a, int& b) {
   const int lo = min(a, b), hi = max(a, b);
   a = lo;
@@ -301,66 +338,88 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
           for (int w = 0; w < W; ++w) yk[u][w] = __ldg(keys + (int64_t)y[u] * W + w);
         }
       }
+      // accept rule (header comment) -> exact position key of the flip mask
+      uint32_t key[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
+        key[u] = kNoKey;
         if (y[u] == 0xffffffffu) continue;
-        Key<W> m;
-        uint64_t ms[W];
+        uint64_t ms[W], o[W];
         int pw = 0, ps = 0;
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-          m.w[w] = x[w] ^ yk[u][w];
-          ms[w] = m.w[w] & S[w];
-          pw += __popcll(m.w[w]);
+          const uint64_t m = x[w] ^ yk[u][w];
+          ms[w] = m & S[w];  // annihilated minority orbitals
+          o[w] = m & ~S[w];  // created ones
+          pw += __popcll(m);
           ps += __popcll(ms[w]);
         }
         const int ta = s_ta[wid][tr[u]], tb = s_tb[wid][tr[u]];
-        // accept rule (header comment) and the mask's exact position key
-        uint32_t key = 0;
-        bool ok = false;
-        if (pw == 4) {
-          if (ps == 2 && bit_at<W>(ms, ta) && bit_at<W>(ms, tb)) {
-            int o0 = -1, o1 = -1;  // the two created orbitals: bits of m outside S(x)
+        if (pw == 4 && ps == 2) {
+          bool is_t = true;  // m & S(x) == T
 #pragma unroll
-            for (int w = 0; w < W; ++w) {
-              uint64_t v = m.w[w] & ~ms[w];
-              while (v) {
-                const int pp = 64 * w + __ffsll(static_cast<long long>(v)) - 1;
-                if (o0 < 0) o0 = pp; else o1 = pp;
-                v &= v - 1;
-              }
-            }
-            int p0 = ta, p1 = tb, p2 = o0, p3 = o1;  // ta < tb, o0 < o1: merge
+          for (int w = 0; w < W; ++w) {
+            const uint64_t t = ((ta >> 6) == w ? 1ull << (ta & 63) : 0ull) | ((tb >> 6) == w ? 1ull << (tb & 63) : 0ull);
+            is_t &= ms[w] == t;
+          }
+          if (is_t) {
+            int p0 = ta, p1 = tb, p2 = lowest_bit<W>(o), p3 = highest_bit<W>(o);  // merge two sorted pairs
             sort2(p0, p2);
             sort2(p1, p3);
             sort2(p1, p2);
-            key = static_cast<uint32_t>(p0) | static_cast<uint32_t>(p1) << 8 | static_cast<uint32_t>(p2) << 16 |
-                  static_cast<uint32_t>(p3) << 24;
-            ok = true;
+            key[u] = static_cast<uint32_t>(p0) | static_cast<uint32_t>(p1) << 8 | static_cast<uint32_t>(p2) << 16 |
+                     static_cast<uint32_t>(p3) << 24;
           }
         } else if (pw == 2 && ps == 1) {
-          int cpos = 0, apos = 0;
-#pragma unroll
-          for (int w = 0; w < W; ++w) {
-            if (ms[w]) cpos = 64 * w + __ffsll(static_cast<long long>(ms[w])) - 1;
-            const uint64_t o = m.w[w] & ~ms[w];
-            if (o) apos = 64 * w + __ffsll(static_cast<long long>(o)) - 1;
-          }
+          const int cpos = lowest_bit<W>(ms), apos = lowest_bit<W>(o);
           const int other = cpos == ta ? tb : (cpos == tb ? ta : -1);
           if (other >= 0 && other == (cpos == pos0 ? pos1 : pos0)) {
             int p0 = cpos, p1 = apos;
             sort2(p0, p1);
-            key = static_cast<uint32_t>(p0) | static_cast<uint32_t>(p1) << 8 | 0xFFFF0000u;
-            ok = true;
+            key[u] = static_cast<uint32_t>(p0) | static_cast<uint32_t>(p1) << 8 | 0xFFFF0000u;
           }
         }
-        if (!ok) continue;
-        ++cand;
-        const int64_t g = xy_lookup(key, J.xy_tab, J.xy_mask);
-        if (g >= 0) {
-          const int64_t jj = (MODE == kModeEmit && R.perm) ? static_cast<int64_t>(__ldg(R.perm + y[u])) : y[u];
-          on_hit<W, MODE>(O, orow, jj, static_cast<uint32_t>(g), sm);
-          ++hits;
+      }
+      // flip-mask lookups: first buckets of all U in flight, then resolve
+      ulonglong2 b0[U], b1[U];
+      uint64_t bk[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (key[u] != kNoKey) {
+          bk[u] = fmix(key[u]) & J.xy_mask;
+          const ulonglong2* p = reinterpret_cast<const ulonglong2*>(J.xy_tab + bk[u] * 4);
+          b0[u] = __ldg(p);
+          b1[u] = __ldg(p + 1);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        int64_t g = -1;
+        if (key[u] != kNoKey) {
+          ++cand;
+          g = xy_resolve(key[u], bk[u], b0[u], b1[u], J.xy_tab, J.xy_mask);
+        }
+        // warp-aggregated append of the hits
+        const bool hit = g >= 0;
+        const unsigned hm = __ballot_sync(0xffffffffu, hit);
+        if (hm) {
+          if (MODE == kModeEloc || MODE == kModeEmit) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(MODE == kModeEloc ? &sm->qn : &sm->cursor, __popc(hm));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (hit) {
+              const unsigned k = base + __popc(hm & ((1u << lane) - 1u));
+              if (MODE == kModeEloc) {
+                sm->qj[k] = y[u];
+                sm->qg[k] = static_cast<uint32_t>(g);
+              } else {
+                const uint64_t at = O.row_off[orow] + k;
+                O.xp_out[at] = R.perm ? __ldg(R.perm + y[u]) : y[u];
+                O.g_out[at] = static_cast<uint32_t>(g);
+              }
+            }
+          }
+          hits += hit ? 1u : 0u;
         }
       }
       if (MODE == kModeEloc) {
