@@ -803,6 +803,7 @@ int qvmc_cuda_pairs(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, int mem, 
     ck(cudaMemsetAsync(static_cast<int*>(h->ctl.p) + 6, 0, 4 * sizeof(int), h->stream), "memset stats");
     uint64_t total = 0;
     if (n_unq > 0) {
+      ck(cudaEventRecord(h->ev[0], h->stream), "event");
       DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
       {
         const int err = read_err_and_reset(h);
@@ -811,11 +812,13 @@ int qvmc_cuda_pairs(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, int mem, 
       const RowPlan P = plan_rows(h, n_unq);
       note_plan(h, P);
       if (P.join) DISPATCH_W(W, build_join_index<WW>(h, dkeys, n_unq, P));
+      ck(cudaEventRecord(h->ev[1], h->stream), "event");
       h->counts.ensure((n_unq + 1) * sizeof(uint32_t));
       h->row_off.ensure((n_unq + 1) * sizeof(uint64_t));
       RowOut O{};
       O.counts = h->counts.as<uint32_t>();
       DISPATCH_W(W, (run_rows<WW, kModeCount>(h, dkeys, 0, n_unq, P, O)));
+      ck(cudaEventRecord(h->ev[2], h->stream), "event");  // stats: rows_ms = the counting pass
       // exclusive scan of the per-row counts (as u64)
       ck(cudaMemsetAsync(h->counts.as<uint32_t>() + n_unq, 0, sizeof(uint32_t), h->stream), "memset");
       size_t tmp = 0;
@@ -851,6 +854,8 @@ int qvmc_cuda_pairs(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, int mem, 
                                                    h->stream),
          "segsort");
       ++g_launches;
+      ck(cudaEventRecord(h->ev[3], h->stream), "event");
+      h->timed = true;
       const int err = read_err_and_reset(h);
       if (err) raise_device_err(err);
     }
