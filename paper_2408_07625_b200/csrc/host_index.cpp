@@ -338,6 +338,40 @@ DevicePlan plan_device(const HostIndex& h) {
     p.fam_off.push_back(static_cast<uint32_t>(p.fam_q.size()));
   }
 
+  // one-load records for the drain
+  {
+    const int TW = term_words(W), FW = fam_words(W);
+    p.ginfo.assign(static_cast<size_t>(n_xy) * 4, 0);
+    for (uint32_t g = 0; g < n_xy; ++g) {
+      uint32_t* gi = &p.ginfo[static_cast<size_t>(g) * 4];
+      gi[0] = static_cast<uint32_t>(h.offsets[g]);
+      gi[1] = static_cast<uint32_t>(h.offsets[g + 1] - h.offsets[g]);
+      gi[2] = 0xFFFFFFFFu;
+      const int32_t c = p.comp_of[g];
+      if (c >= 0) {
+        const uint32_t f0 = p.fam_off[c], f1 = p.fam_off[c + 1];
+        gi[2] = f0;
+        gi[3] = f1 - f0;
+        for (uint32_t f = f0; f < f1; ++f) gi[3] |= static_cast<uint32_t>(p.fam_q[f] & 3) << (8 + 2 * (f - f0));
+      }
+    }
+    p.trec.assign(h.n_terms() * TW, 0);
+    for (uint64_t t = 0; t < h.n_terms(); ++t) {
+      uint64_t* r = &p.trec[t * TW];
+      for (int w = 0; w < W; ++w) r[w] = h.yz[t * W + w];
+      std::memcpy(&r[W], &h.coeff[t], 8);
+      r[W + 1] = h.y_weight[t];
+    }
+    const size_t nf = p.fam_q.size();
+    p.famrec.assign(nf * FW, 0);
+    for (size_t f = 0; f < nf; ++f) {
+      uint64_t* r = &p.famrec[f * FW];
+      std::memcpy(&r[0], &p.fam_u[f], 8);
+      std::memcpy(&r[1], &p.fam_V[f], 8);
+      for (int w = 0; w < W; ++w) r[2 + w] = p.fam_B[f * W + w];
+    }
+  }
+
   // flip-mask table for the join path: weight-2/4 masks keyed EXACTLY by
   // their sorted orbital positions packed into 32 bits (0xFF pads weight 2),
   // so a lookup needs no mask compare; buckets of 4 x (key32 << 32 | group),

@@ -72,6 +72,12 @@ struct DevicePlan {
   std::vector<uint8_t> fam_q;       // [n_fam] y-weight mod 4
   std::vector<double> fam_u, fam_V; // [n_fam] constant part, sum_k v_f[k]
   std::vector<double> fam_v;        // [n_fam][N]
+  // hot-path records (one load each): per group (t0, n_terms, first family or
+  // ~0, n_families | q_f << (8 + 2f)); per term (yz words, coeff bits, y_weight)
+  // padded to 16 B; per family (u_f, V_f, B_f words) padded to 16 B
+  std::vector<uint32_t> ginfo;      // [n_xy][4]
+  std::vector<uint64_t> trec;       // [n_terms][term_words(W)]
+  std::vector<uint64_t> famrec;     // [n_fam][fam_words(W)]
   // flip-mask table (join path): buckets of 4 x (position key32 << 32 | group)
   std::vector<uint64_t> xy_tab;
   uint64_t xy_tab_mask = 0;
@@ -86,6 +92,9 @@ inline uint64_t fmix_host(uint64_t h) {
 }
 
 DevicePlan plan_device(const HostIndex& h);
+
+constexpr int term_words(int W) { return (W + 2 + 1) & ~1; }
+constexpr int fam_words(int W) { return (W + 2 + 1) & ~1; }
 
 inline uint32_t pair_index(int p, int q, int n) {  // p < q
   return static_cast<uint32_t>(p * n - p * (p + 1) / 2 + (q - p - 1));

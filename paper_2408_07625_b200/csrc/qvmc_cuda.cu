@@ -123,11 +123,12 @@ struct qvmc_ham_s {
   cudaStream_t own = nullptr, stream = nullptr;
   // Hamiltonian
   DBuf xy, xy_hash, goff, coeff, yz, yw, xyw, gen_hash, gen_g, lst_off, lst_hash, lst_g, res_g, diag_b, diag_K,
-      diag_other, hash_bytes, xy_tab, codes, comp_of, fam_off, fam_B, fam_q, fam_u, fam_V, fam_v;
+      diag_other, hash_bytes, xy_tab, codes, comp_of, fam_off, fam_B, fam_q, fam_u, fam_V, fam_v, ginfo, trec,
+      famrec;
   uint64_t xy_tab_mask = 0;
   HamView view{};
   // join path (per call): deletion-index workspace
-  DBuf l_key, l_key2, l_idx, l_perm, l_keys, l_la, l_ph, l_flags, l_list, l_nsel;
+  DBuf l_key, l_key2, l_idx, l_perm, l_keys, l_la, l_ph, l_cs, l_flags, l_list, l_nsel, cs;
   DBuf j_key, j_val, j_key2, j_val2, j_rng, j_uniq, j_cnt, j_off, j_nruns, j_tmp;
   bool use_join = true;
   // workspace
@@ -435,8 +436,8 @@ void run_rows(qvmc_ham_s* h, const uint64_t* keys, int64_t r0, int64_t r1, const
 // (locality), rebuild the index on the sorted copy, process rows in that
 // order. Returns the row set; keys/la/ph are redirected to the sorted copies.
 template <int W>
-RowSet sort_for_locality(qvmc_ham_s* h, const uint64_t*& keys, const double*& la, const double*& ph, int64_t n,
-                         int64_t r0, int64_t r1, const RowPlan& P) {
+RowSet sort_for_locality(qvmc_ham_s* h, const uint64_t*& keys, const double*& la, const double*& ph,
+                         const double2*& cs, int64_t n, int64_t r0, int64_t r1, const RowPlan& P) {
   h->l_key.ensure(n * 8 + 16);
   h->l_key2.ensure(n * 8 + 16);
   h->l_idx.ensure(n * 4 + 16);
@@ -444,6 +445,7 @@ RowSet sort_for_locality(qvmc_ham_s* h, const uint64_t*& keys, const double*& la
   h->l_keys.ensure(n * 8 * W + 16);
   h->l_la.ensure(n * 8 + 16);
   h->l_ph.ensure(n * 8 + 16);
+  h->l_cs.ensure(n * 16 + 16);
   const int grid = static_cast<int>(std::min<int64_t>((n + kThreads - 1) / kThreads, grid_for(h, 8)));
   k_locality_keys<W><<<std::max(grid, 1), kThreads, 0, h->stream>>>(keys, n, h->n, P.side, h->l_key.as<uint64_t>(),
                                                                     h->l_idx.as<uint32_t>());
@@ -460,11 +462,12 @@ RowSet sort_for_locality(qvmc_ham_s* h, const uint64_t*& keys, const double*& la
   ++g_launches;
   k_gather_sorted<W><<<std::max(grid, 1), kThreads, 0, h->stream>>>(
       h->l_perm.as<uint32_t>(), n, keys, la, ph, h->l_keys.as<uint64_t>(), h->l_la.as<double>(),
-      h->l_ph.as<double>());
+      h->l_ph.as<double>(), h->l_cs.as<double2>());
   ck_launch("gather sorted");
   keys = h->l_keys.as<uint64_t>();
   la = h->l_la.as<double>();
   ph = h->l_ph.as<double>();
+  cs = h->l_cs.as<double2>();
   RowSet R{n, 0, nullptr, h->l_perm.as<uint32_t>(), r0};
   if (r0 != 0 || r1 != n) {  // a row shard: the sorted positions of its rows
     h->l_flags.ensure(n + 16);
@@ -677,6 +680,9 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     upload(h->fam_u, p.fam_u);
     upload(h->fam_V, p.fam_V);
     upload(h->fam_v, p.fam_v);
+    upload(h->ginfo, p.ginfo);
+    upload(h->trec, p.trec);
+    upload(h->famrec, p.famrec);
     h->xy_tab_mask = p.xy_tab_mask;
     upload(h->codes, std::vector<uint64_t>(qubit_codes(), qubit_codes() + 256));
     if (const char* e = std::getenv("QVMC_JOIN")) h->use_join = std::atoi(e) != 0;
@@ -717,6 +723,9 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     v.fam_u = h->fam_u.as<double>();
     v.fam_V = h->fam_V.as<double>();
     v.fam_v = h->fam_v.as<double>();
+    v.ginfo = h->ginfo.as<uint4>();
+    v.trec = h->trec.as<uint64_t>();
+    v.famrec = h->famrec.as<uint64_t>();
     ck(cudaDeviceSynchronize(), "upload sync");
     *out = h.release();
   });
@@ -1037,14 +1046,21 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
     const uint64_t* rkeys = dkeys;
     const double* rla = dla;
     const double* rph = dph;
+    const double2* rcs = nullptr;
     if (n_unq > 0) {
       DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
       P = plan_rows(h, n_unq);
       note_plan(h, P);
       if (P.join) {
-        DISPATCH_W(W, R = sort_for_locality<WW>(h, rkeys, rla, rph, n_unq, row_begin, row_end, P));
+        DISPATCH_W(W, R = sort_for_locality<WW>(h, rkeys, rla, rph, rcs, n_unq, row_begin, row_end, P));
         if (h->view.n_res) DISPATCH_W(W, launch_table_build<WW>(h, rkeys, n_unq));  // residual probes: sorted ids
         DISPATCH_W(W, build_join_index<WW>(h, rkeys, n_unq, P));
+      } else {
+        h->cs.ensure(n_unq * 16 + 16);
+        const int grid = static_cast<int>(std::min<int64_t>((n_unq + kThreads - 1) / kThreads, grid_for(h, 8)));
+        k_cos_sin<<<std::max(grid, 1), kThreads, 0, h->stream>>>(dph, n_unq, h->cs.as<double2>());
+        ck_launch("cos sin");
+        rcs = h->cs.as<double2>();
       }
     }
     ck(cudaEventRecord(h->ev[1], h->stream), "event");
@@ -1053,6 +1069,7 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       O.eloc = deloc;
       O.la = rla;
       O.ph = rph;
+      O.cs = rcs;
       if (P.join) {
         DISPATCH_W(W, (launch_rows_join<WW, kModeEloc>(h, rkeys, R, P, O)));
       } else {

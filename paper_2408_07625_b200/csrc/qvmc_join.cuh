@@ -91,13 +91,17 @@ __global__ void __launch_bounds__(kThreads)
 template <int W>
 __global__ void k_gather_sorted(const uint32_t* __restrict__ perm, int64_t n, const uint64_t* __restrict__ keys,
                                 const double* __restrict__ la, const double* __restrict__ ph, uint64_t* keys_s,
-                                double* la_s, double* ph_s) {
+                                double* la_s, double* ph_s, double2* cs_s) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t o = perm[i];
 #pragma unroll
     for (int w = 0; w < W; ++w) keys_s[i * W + w] = keys[(int64_t)o * W + w];
     la_s[i] = la[o];
-    ph_s[i] = ph[o];
+    const double p = ph[o];
+    ph_s[i] = p;
+    double sn, c;
+    sincos(p, &sn, &c);
+    cs_s[i] = make_double2(c, sn);
   }
 }
 
@@ -257,10 +261,11 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
     Key<W> xrow;
 #pragma unroll
     for (int w = 0; w < W; ++w) xrow.w[w] = x[w];
-    double la_i = 0.0, ph_i = 0.0;
+    double la_i = 0.0;
+    double2 cs_i = make_double2(1.0, 0.0);
     if (MODE == kModeEloc) {
       la_i = __ldg(O.la + row);
-      ph_i = __ldg(O.ph + row);
+      cs_i = __ldg(O.cs + row);
       if (isinf(la_i)) {  // energy.cpp:32-33
         if (lane == 0) {
           atomicOr(C.err, kErrZeroAmp);
@@ -425,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
       if (MODE == kModeEloc) {
         __syncwarp();
         if (sm->qn >= kDrainAt) {
-          const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane, xrow, s, side);
+          const double2 d = drain<W>(H, keys, O.la, O.cs, la_i, cs_i, sm, lane, xrow, s, side);
           acc.x += d.x;
           acc.y += d.y;
         }
@@ -460,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
       if (MODE == kModeEloc) {
         __syncwarp();
         if (sm->qn >= kDrainAt) {
-          const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane, xrow, s, side);
+          const double2 d = drain<W>(H, keys, O.la, O.cs, la_i, cs_i, sm, lane, xrow, s, side);
           acc.x += d.x;
           acc.y += d.y;
         }
@@ -504,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
     if (MODE == kModeEloc) {
       __syncwarp();
       if (sm->qn > 0) {
-        const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane, xrow, s, side);
+        const double2 d = drain<W>(H, keys, O.la, O.cs, la_i, cs_i, sm, lane, xrow, s, side);
         acc.x += d.x;
         acc.y += d.y;
       }

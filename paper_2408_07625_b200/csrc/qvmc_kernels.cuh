@@ -57,7 +57,13 @@ struct HamView {
   const double* fam_u;
   const double* fam_V;
   const double* fam_v;
+  const uint4* ginfo;          // per group (t0, n_terms, first family, n_fam | q bits)
+  const uint64_t* trec;        // per term (yz words, coeff, y_weight), term_words(W) words
+  const uint64_t* famrec;      // per family (u, V, B words), fam_words(W) words
 };
+
+constexpr int term_words_dev(int W) { return (W + 2 + 1) & ~1; }
+constexpr int fam_words_dev(int W) { return (W + 2 + 1) & ~1; }
 
 struct TableView {
   uint64_t* tab;  // buckets of 4 entries: (tag << 32) | row, kEmpty when free
@@ -238,7 +244,16 @@ struct RowOut {
   uint32_t* g_out;            // kModeEmit
   const double* la;           // log amplitudes
   const double* ph;           // phases
+  const double2* cs;          // (cos, sin) of the phases
 };
+
+__global__ void k_cos_sin(const double* __restrict__ ph, int64_t n, double2* cs) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double s, c;
+    sincos(ph[i], &s, &c);
+    cs[i] = make_double2(c, s);
+  }
+}
 
 // sector mode enumerates, per row, one list per minority orbital (single
 // flips) and one per pair of minority orbitals (double flips)
@@ -264,12 +279,13 @@ struct WarpSmem {
   unsigned cursor;             // kModeEmit output cursor
 };
 
-__device__ __forceinline__ void add_ratio(const double* __restrict__ la, const double* __restrict__ ph, double la_i,
-                                          double ph_i, uint32_t j, double hr, double hi, double2& acc) {
-  // h * exp(dlog) * (cos dphase + i sin dphase)   (energy.cpp:38-43)
-  const double a = exp(__ldg(la + j) - la_i);
-  double s, c;
-  sincos(__ldg(ph + j) - ph_i, &s, &c);
+// h * psi(x')/psi(x) = h * exp(la_j - la_i) * (cos, sin)(ph_j - ph_i), the
+// angle difference expanded from per-sample (cos, sin) (energy.cpp:38-43)
+__device__ __forceinline__ void add_ratio(double la_j, double2 cs_j, double la_i, double2 cs_i, double hr, double hi,
+                                          double2& acc) {
+  const double a = exp(la_j - la_i);
+  const double c = cs_j.x * cs_i.x + cs_j.y * cs_i.y;
+  const double s = cs_j.y * cs_i.x - cs_j.x * cs_i.y;
   hr *= a;
   hi *= a;
   acc.x += hr * c - hi * s;
@@ -281,16 +297,26 @@ __device__ __forceinline__ void add_ratio(const double* __restrict__ la, const d
 // with sum_k v_f[k] (-1)^{x'_k} = +-(V_f - 2 sum_{k in S(x')} v_f[k]) over the
 // minority set S(x') = S(x) ^ (x ^ x'): s + |m| loads instead of the terms.
 template <int W>
-__device__ __forceinline__ void comp_element(const HamView& H, const uint64_t* x, const uint64_t* xp, int32_t c,
+__device__ __forceinline__ void comp_element(const HamView& H, const uint64_t* x, const uint64_t* xp, uint4 gi,
                                              const uint16_t* pos, int s, int side, double& re, double& im) {
+  constexpr int FW = fam_words_dev(W);
   re = 0.0;
   im = 0.0;
   const int n = H.n;
   uint64_t m[W];
 #pragma unroll
   for (int w = 0; w < W; ++w) m[w] = x[w] ^ xp[w];
-  const uint32_t f1 = __ldg(H.fam_off + c + 1);
-  for (uint32_t f = __ldg(H.fam_off + c); f < f1; ++f) {
+  const uint32_t nf = gi.w & 0xFFu;
+  for (uint32_t k = 0; k < nf; ++k) {
+    const uint32_t f = gi.z + k;
+    const ulonglong2* fr = reinterpret_cast<const ulonglong2*>(H.famrec + static_cast<int64_t>(f) * FW);
+    uint64_t r[FW];
+#pragma unroll
+    for (int w = 0; w < FW; w += 2) {
+      const ulonglong2 v = __ldg(fr + w / 2);
+      r[w] = v.x;
+      r[w + 1] = v.y;
+    }
     const double* v = H.fam_v + static_cast<int64_t>(f) * n;
     double sv = 0.0;
     for (int a = 0; a < s; ++a) sv += __ldg(v + pos[a]);
@@ -298,19 +324,19 @@ __device__ __forceinline__ void comp_element(const HamView& H, const uint64_t* x
     for (int w = 0; w < W; ++w) {
       uint64_t bits = m[w];
       while (bits) {
-        const int k = 64 * w + __ffsll(static_cast<long long>(bits)) - 1;
+        const int b = 64 * w + __ffsll(static_cast<long long>(bits)) - 1;
         bits &= bits - 1;
-        const bool in_s = ((x[w] >> (k & 63)) & 1ull) == static_cast<uint64_t>(side);
-        sv += in_s ? -__ldg(v + k) : __ldg(v + k);
+        const bool in_s = ((x[w] >> (b & 63)) & 1ull) == static_cast<uint64_t>(side);
+        sv += in_s ? -__ldg(v + b) : __ldg(v + b);
       }
     }
-    const double V = __ldg(H.fam_V + f);
-    double val = __ldg(H.fam_u + f) + (side ? V - 2.0 * sv : 2.0 * sv - V);
+    const double V = __longlong_as_double(static_cast<long long>(r[1]));
+    double val = __longlong_as_double(static_cast<long long>(r[0])) + (side ? V - 2.0 * sv : 2.0 * sv - V);
     int pc = 0;
 #pragma unroll
-    for (int w = 0; w < W; ++w) pc += __popcll(xp[w] & __ldg(H.fam_B + static_cast<int64_t>(f) * W + w));
+    for (int w = 0; w < W; ++w) pc += __popcll(xp[w] & r[2 + w]);
     if (pc & 1) val = -val;
-    const int q = __ldg(H.fam_q + f);
+    const uint32_t q = (gi.w >> (8 + 2 * k)) & 3u;
     if (q == 0) re += val;
     else if (q == 1) im += val;
     else if (q == 2) re -= val;
@@ -318,57 +344,91 @@ __device__ __forceinline__ void comp_element(const HamView& H, const uint64_t* x
   }
 }
 
+// group_element from the packed term records (same terms, same order, same
+// exact +-c adds as group_element: bit-identical)
+template <int W>
+__device__ __forceinline__ void small_element(const HamView& H, const uint64_t* xp, uint4 gi, double& re, double& im) {
+  constexpr int TW = term_words_dev(W);
+  re = 0.0;
+  im = 0.0;
+  const ulonglong2* tr = reinterpret_cast<const ulonglong2*>(H.trec + static_cast<int64_t>(gi.x) * TW);
+  for (uint32_t t = 0; t < gi.y; ++t) {
+    uint64_t r[TW];
+#pragma unroll
+    for (int w = 0; w < TW; w += 2) {
+      const ulonglong2 v = __ldg(tr + (static_cast<int64_t>(t) * TW + w) / 2);
+      r[w] = v.x;
+      r[w + 1] = v.y;
+    }
+    int pc = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) pc += __popcll(xp[w] & r[w]);
+    const int q = (static_cast<int>(r[W + 1]) + 2 * pc) & 3;
+    const double c = __longlong_as_double(static_cast<long long>(r[W]));
+    if (q == 0) re += c;
+    else if (q == 2) re -= c;
+    else if (q == 1) im += c;
+    else im -= c;
+  }
+}
+
 // Drain the warp's hit queue: returns this lane's share of sum H_{xx'} psi(x')/psi(x).
 // s > 0: sector mode with the row's minority orbitals in sm->pos (enables
 // compressed groups); s == 0: every group term by term.
+#ifdef QVMC_DRAIN_INLINE
+#define QVMC_DRAIN_ATTR __forceinline__
+#else
+#define QVMC_DRAIN_ATTR __noinline__
+#endif
 template <int W>
-__device__ __noinline__ double2 drain(const HamView& H, const uint64_t* __restrict__ keys,
-                                      const double* __restrict__ la, const double* __restrict__ ph, double la_i,
-                                      double ph_i, WarpSmem* sm, int lane, Key<W> xrow, int s, int side) {
+__device__ QVMC_DRAIN_ATTR double2 drain(const HamView& H, const uint64_t* __restrict__ keys,
+                                      const double* __restrict__ la, const double2* __restrict__ cs, double la_i,
+                                      double2 cs_i, WarpSmem* sm, int lane, Key<W> xrow, int s, int side) {
   double2 acc = make_double2(0.0, 0.0);
   __syncwarp();
   const unsigned n = sm->qn;
   for (unsigned k0 = 0; k0 < n; k0 += 32) {
     const unsigned k = k0 + lane;
-    uint32_t j = 0, g = 0, t0 = 0, t1 = 0;
-    if (k < n) {
+    const bool valid = k < n;
+    uint32_t j = 0;
+    uint4 gi = make_uint4(0, 0, 0xFFFFFFFFu, 0);
+    uint64_t xp[W];
+    double la_j = 0.0;
+    double2 cs_j = make_double2(1.0, 0.0);
+    if (valid) {  // independent loads first
       j = sm->qj[k];
-      g = sm->qg[k];
-      t0 = __ldg(H.goff + g);
-      t1 = __ldg(H.goff + g + 1);
-    }
-    const int32_t comp = (k < n && s > 0 && t1 - t0 > kSmallGroup) ? __ldg(H.comp_of + g) : -1;
-    const bool large = k < n && t1 - t0 > kSmallGroup && comp < 0;
-    // small groups: one hit per lane, term by term in the reference order;
-    // compressed groups: one hit per lane through the family sums
-    if (k < n && !large) {
-      uint64_t xp[W];
+      gi = __ldg(H.ginfo + sm->qg[k]);
 #pragma unroll
       for (int w = 0; w < W; ++w) xp[w] = __ldg(keys + (int64_t)j * W + w);
-      double hr, hi;
-      if (comp >= 0)
-        comp_element<W>(H, xrow.w, xp, comp, sm->pos, s, side, hr, hi);
-      else
-        group_element<W>(H, xp, g, hr, hi);
-      add_ratio(la, ph, la_i, ph_i, j, hr, hi, acc);
+      la_j = __ldg(la + j);
+      cs_j = __ldg(cs + j);
     }
-    // large groups: the warp splits the terms; the element is parked in lane src
+    const bool comp = gi.z != 0xFFFFFFFFu && s > 0;
+    const bool large = valid && gi.y > kSmallGroup && !comp;
+    if (valid && !large) {
+      double hr, hi;
+      if (comp)
+        comp_element<W>(H, xrow.w, xp, gi, sm->pos, s, side, hr, hi);
+      else
+        small_element<W>(H, xp, gi, hr, hi);
+      add_ratio(la_j, cs_j, la_i, cs_i, hr, hi, acc);
+    }
+    // large uncompressed groups: the warp splits the terms; element parked in lane src
     double mine_r = 0.0, mine_i = 0.0;
     unsigned mask = __ballot_sync(0xffffffffu, large);
     while (mask) {
       const int src = __ffs(mask) - 1;
       mask &= mask - 1;
-      const uint32_t sj = __shfl_sync(0xffffffffu, j, src);
-      const uint32_t st0 = __shfl_sync(0xffffffffu, t0, src);
-      const uint32_t st1 = __shfl_sync(0xffffffffu, t1, src);
-      uint64_t xp[W];
+      const uint32_t st0 = __shfl_sync(0xffffffffu, gi.x, src);
+      const uint32_t st1 = st0 + __shfl_sync(0xffffffffu, gi.y, src);
+      uint64_t sx[W];
 #pragma unroll
-      for (int w = 0; w < W; ++w) xp[w] = __ldg(keys + (int64_t)sj * W + w);
+      for (int w = 0; w < W; ++w) sx[w] = __shfl_sync(0xffffffffu, xp[w], src);
       double re = 0.0, im = 0.0;
       for (uint32_t t = st0 + lane; t < st1; t += 32) {
         int pc = 0;
 #pragma unroll
-        for (int w = 0; w < W; ++w) pc += __popcll(xp[w] & __ldg(H.yz + (int64_t)t * W + w));
+        for (int w = 0; w < W; ++w) pc += __popcll(sx[w] & __ldg(H.yz + (int64_t)t * W + w));
         const int qt = (__ldg(H.yw + t) + 2 * pc) & 3;
         const double c = __ldg(H.coeff + t);
         if (qt == 0) re += c;
@@ -383,7 +443,7 @@ __device__ __noinline__ double2 drain(const HamView& H, const uint64_t* __restri
         mine_i = im;
       }
     }
-    if (large) add_ratio(la, ph, la_i, ph_i, j, mine_r, mine_i, acc);
+    if (large) add_ratio(la_j, cs_j, la_i, cs_i, mine_r, mine_i, acc);
   }
   __syncwarp();
   if (lane == 0) sm->qn = 0;
@@ -439,10 +499,11 @@ __global__ void __launch_bounds__(kThreads) k_rows(const __grid_constant__ HamVi
     Key<W> xrow;
 #pragma unroll
     for (int w = 0; w < W; ++w) xrow.w[w] = x[w];
-    double la_i = 0.0, ph_i = 0.0;
+    double la_i = 0.0;
+    double2 cs_i = make_double2(1.0, 0.0);
     if (MODE == kModeEloc) {
       la_i = __ldg(O.la + row);
-      ph_i = __ldg(O.ph + row);
+      cs_i = __ldg(O.cs + row);
       if (isinf(la_i)) {  // energy.cpp:32-33
         if (lane == 0) {
           atomicOr(C.err, kErrZeroAmp);
@@ -562,7 +623,7 @@ __global__ void __launch_bounds__(kThreads) k_rows(const __grid_constant__ HamVi
       if (MODE == kModeEloc) {
         __syncwarp();
         if (sm->qn >= kDrainAt) {
-          const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane, xrow, sector ? s : 0, side);
+          const double2 d = drain<W>(H, keys, O.la, O.cs, la_i, cs_i, sm, lane, xrow, sector ? s : 0, side);
           acc.x += d.x;
           acc.y += d.y;
         }
@@ -597,7 +658,7 @@ __global__ void __launch_bounds__(kThreads) k_rows(const __grid_constant__ HamVi
         if (MODE == kModeEloc) {
           __syncwarp();
           if (sm->qn >= kDrainAt) {
-            const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane, xrow, sector ? s : 0, side);
+            const double2 d = drain<W>(H, keys, O.la, O.cs, la_i, cs_i, sm, lane, xrow, sector ? s : 0, side);
             acc.x += d.x;
             acc.y += d.y;
           }
@@ -648,7 +709,7 @@ __global__ void __launch_bounds__(kThreads) k_rows(const __grid_constant__ HamVi
     if (MODE == kModeEloc) {
       __syncwarp();
       if (sm->qn > 0) {
-        const double2 d = drain<W>(H, keys, O.la, O.ph, la_i, ph_i, sm, lane, xrow, sector ? s : 0, side);
+        const double2 d = drain<W>(H, keys, O.la, O.cs, la_i, cs_i, sm, lane, xrow, sector ? s : 0, side);
         acc.x += d.x;
         acc.y += d.y;
       }
