@@ -168,6 +168,20 @@ uint64_t linear_hash(const uint64_t* words, int n_words) {
   return h;
 }
 
+std::vector<uint64_t> binomial_table() {
+  constexpr uint64_t kSat = ~uint64_t{0};
+  std::vector<uint64_t> c(static_cast<size_t>(257) * kBinomKHost, 0);
+  for (int n = 0; n <= 256; ++n) {
+    c[static_cast<size_t>(n) * kBinomKHost] = 1;
+    for (int k = 1; k < kBinomKHost && n > 0; ++k) {
+      const uint64_t a = c[static_cast<size_t>(n - 1) * kBinomKHost + k - 1];
+      const uint64_t b = c[static_cast<size_t>(n - 1) * kBinomKHost + k];
+      c[static_cast<size_t>(n) * kBinomKHost + k] = (a == kSat || b == kSat || a > kSat - b) ? kSat : a + b;
+    }
+  }
+  return c;
+}
+
 DevicePlan plan_device(const HostIndex& h) {
   DevicePlan p;
   const int n = h.n_qubits, W = h.n_words;
@@ -369,6 +383,52 @@ DevicePlan plan_device(const HostIndex& h) {
       std::memcpy(&r[0], &p.fam_u[f], 8);
       std::memcpy(&r[1], &p.fam_V[f], 8);
       for (int w = 0; w < W; ++w) r[2 + w] = p.fam_B[f * W + w];
+    }
+  }
+
+  // join-path drain records, 8 words per group (qvmc_join.cuh kGrec*):
+  // A = small weight-2/4 group whose terms share one Z string (all JW double
+  // excitations), B = family-compressed, C = anything else
+  {
+    p.grec.assign(static_cast<size_t>(n_xy) * kGrecWordsHost, 0);
+    for (uint32_t g = 0; g < n_xy; ++g) {
+      uint64_t* r = &p.grec[static_cast<size_t>(g) * kGrecWordsHost];
+      const uint64_t t0 = h.offsets[g], t1 = h.offsets[g + 1], k = t1 - t0;
+      const int32_t c = p.comp_of[g];
+      if (c >= 0) {
+        const uint32_t f0 = p.fam_off[c], f1 = p.fam_off[c + 1];
+        uint64_t qb = 0;
+        for (uint32_t f = f0; f < f1; ++f) qb |= static_cast<uint64_t>(p.fam_q[f] & 3) << (2 * (f - f0));
+        r[0] = 1 | static_cast<uint64_t>(f1 - f0) << 8 | qb << 16;
+        r[1] = f0;
+        continue;
+      }
+      const uint64_t* xy = &h.xy[static_cast<size_t>(g) * W];
+      const int wt = p.xy_weight[g];
+      bool a_ok = static_cast<int64_t>(g) != h.diag && (wt == 2 || wt == 4) && k >= 1 &&
+                  k <= static_cast<uint64_t>(kGrecWordsHost - 2 - W);
+      int xpos[4], np = 0;
+      for (int w = 0; w < W && a_ok; ++w)
+        for (uint64_t v = xy[w]; v; v &= v - 1) xpos[np++] = w * 64 + std::countr_zero(v);
+      uint64_t meta = static_cast<uint64_t>(k) << 2;
+      for (uint64_t t = t0; t < t1 && a_ok; ++t) {
+        const uint64_t* yz = &h.yz[t * W];
+        for (int w = 0; w < W; ++w)
+          if ((yz[w] & ~xy[w]) != (h.yz[t0 * W + w] & ~xy[w])) a_ok = false;  // Z strings differ
+        uint64_t ypat = 0;
+        for (int i = 0; i < np; ++i)
+          if ((yz[xpos[i] >> 6] >> (xpos[i] & 63)) & 1) ypat |= 1ull << i;
+        meta |= (ypat | static_cast<uint64_t>(h.y_weight[t] & 3) << 4) << (8 + 6 * (t - t0));
+      }
+      if (a_ok) {
+        r[0] = meta;  // kind A = 0
+        for (int w = 0; w < W; ++w) r[2 + w] = h.yz[t0 * W + w] & ~xy[w];
+        for (uint64_t t = t0; t < t1; ++t) std::memcpy(&r[2 + W + (t - t0)], &h.coeff[t], 8);
+      } else {
+        if (k >= (1ull << 32)) throw std::invalid_argument("HamiltonianIndex: group with 2^32 or more terms");
+        r[0] = 2;
+        r[1] = t0 | k << 32;
+      }
     }
   }
 

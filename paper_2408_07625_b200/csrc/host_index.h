@@ -13,6 +13,12 @@ constexpr int kMaxWords = 4;        // 256 qubits, BasisVector::kMaxBits (basis_
 constexpr int kMaxMinority = 32;    // sector lists are used when min(n_e, N - n_e) <= 32
 constexpr uint32_t kSmallGroupHost = 16;  // groups above this size are candidates for compression
 constexpr int kMaxFamilies = 4;
+constexpr int kGrecWordsHost = 8;   // qvmc_join.cuh kGrecWords
+constexpr int kBinomKHost = 17;     // qvmc_join.cuh kBinomK
+
+// C(n, k) for n <= 256, k < kBinomKHost, saturating at UINT64_MAX
+// ([257][kBinomKHost], the combinadic ranks of the join's bucket keys)
+std::vector<uint64_t> binomial_table();
 
 // HamiltonianIndex (proj/include/qvmc/hamiltonian.hpp:41-107) as flat arrays.
 struct HostIndex {
@@ -78,6 +84,8 @@ struct DevicePlan {
   std::vector<uint32_t> ginfo;      // [n_xy][4]
   std::vector<uint64_t> trec;       // [n_terms][term_words(W)]
   std::vector<uint64_t> famrec;     // [n_fam][fam_words(W)]
+  // join-path drain records (qvmc_join.cuh): [n_xy][kGrecWordsHost]
+  std::vector<uint64_t> grec;
   // flip-mask table (join path): buckets of 4 x (position key32 << 32 | group)
   std::vector<uint64_t> xy_tab;
   uint64_t xy_tab_mask = 0;

@@ -124,12 +124,13 @@ struct qvmc_ham_s {
   // Hamiltonian
   DBuf xy, xy_hash, goff, coeff, yz, yw, xyw, gen_hash, gen_g, lst_off, lst_hash, lst_g, res_g, diag_b, diag_K,
       diag_other, hash_bytes, xy_tab, codes, comp_of, fam_off, fam_B, fam_q, fam_u, fam_V, fam_v, ginfo, trec,
-      famrec;
+      famrec, grec, binom;
+  std::vector<uint64_t> binom_host;
   uint64_t xy_tab_mask = 0;
   HamView view{};
   // join path (per call): deletion-index workspace
-  DBuf l_key, l_key2, l_idx, l_perm, l_keys, l_la, l_ph, l_cs, l_flags, l_list, l_nsel, cs;
-  DBuf j_key, j_val, j_key2, j_val2, j_rng, j_uniq, j_cnt, j_off, j_nruns, j_tmp;
+  DBuf l_key, l_key2, l_idx, l_perm, l_keys, l_rec, l_flags, l_list, l_nsel, cs;
+  DBuf j_key, j_val, j_key2, j_val2, j_head, j_rid, j_lo, j_hi, j_mem, j_rng, j_tmp;
   bool use_join = true;
   // workspace
   DBuf tab, ctl, keys, la, ph, lp, eloc, partials, moments, weights;
@@ -337,6 +338,7 @@ struct RowPlan {
   bool join = false;
   int side = 0;
   int s = 0;
+  int key_bits = 0;  // join: bits of the exact bucket rank, ceil(log2 C(n, s - 2))
 };
 
 RowPlan plan_rows(qvmc_ham_s* h, int64_t n) {
@@ -350,62 +352,77 @@ RowPlan plan_rows(qvmc_ham_s* h, int64_t n) {
   P.sector = n > 0 && pmin == pmax && P.s <= kMaxMinorityDev;
   const uint64_t entries = static_cast<uint64_t>(n) * (P.s * (P.s - 1) / 2);
   P.join = h->use_join && P.sector && P.s >= 2 && P.s <= kJoinMaxMinority && entries < (1ull << 31);
+  if (P.join) {  // exact bucket keys need C(n, s - 2) < 2^64
+    const uint64_t nb = h->binom_host[static_cast<size_t>(h->n) * kBinomK + (P.s - 2)];
+    if (nb == ~uint64_t{0}) P.join = false;
+    P.key_bits = nb <= 1 ? 1 : 64 - __builtin_clzll(nb - 1);
+  }
   return P;
 }
 
-// deletion index: keys -> radix sort -> runs -> per-entry bucket ranges
-template <int W>
-void build_join_index(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowPlan& P) {
+// deletion index: exact keys -> radix sort -> runs -> member array + per-(sample, pair) bucket ranges
+template <int W, typename K>
+void build_join_index_k(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowPlan& P) {
   const uint32_t C = static_cast<uint32_t>(P.s * (P.s - 1) / 2);
   const uint64_t E = static_cast<uint64_t>(n) * C;
-  h->j_key.ensure(E * 4 + 16);
-  h->j_val.ensure(E * 4 + 16);
-  h->j_key2.ensure(E * 4 + 16);
-  h->j_val2.ensure(E * 4 + 16);
+  h->j_key.ensure(E * sizeof(K) + 16);
+  h->j_key2.ensure(E * sizeof(K) + 16);
+  h->j_val.ensure(E * 8 + 16);
+  h->j_val2.ensure(E * 8 + 16);
+  h->j_head.ensure(E * 4 + 16);
+  h->j_rid.ensure(E * 4 + 16);
+  h->j_lo.ensure(E * 4 + 16);
+  h->j_hi.ensure(E * 4 + 16);
+  h->j_mem.ensure(E * 8 + 16);
   h->j_rng.ensure(E * 8 + 16);
-  h->j_uniq.ensure(E * 4 + 16);
-  h->j_cnt.ensure(E * 4 + 16);
-  h->j_off.ensure(E * 4 + 16);
-  h->j_nruns.ensure(16);
   const int grid = static_cast<int>(std::min<int64_t>((n + kThreads - 1) / kThreads, grid_for(h, 8)));
-  k_join_keys<W><<<std::max(grid, 1), kThreads, 0, h->stream>>>(
-      keys, n, h->n, P.side, P.s, h->codes.as<uint64_t>(), h->j_key.as<uint32_t>(), h->j_val.as<uint32_t>());
+  k_join_keys<W, K><<<std::max(grid, 1), kThreads, 0, h->stream>>>(keys, n, h->n, P.side, P.s, h->binom.as<uint64_t>(),
+                                                                   h->j_key.as<K>(), h->j_val.as<uint64_t>());
   ck_launch("join keys");
   const int ne = static_cast<int>(E);
-  size_t b1 = 0, b2 = 0, b3 = 0;
-  ck(cub::DeviceRadixSort::SortPairs(nullptr, b1, h->j_key.as<uint32_t>(), h->j_key2.as<uint32_t>(),
-                                     h->j_val.as<uint32_t>(), h->j_val2.as<uint32_t>(), ne, 0, 32, h->stream),
+  size_t b1 = 0, b2 = 0;
+  ck(cub::DeviceRadixSort::SortPairs(nullptr, b1, h->j_key.as<K>(), h->j_key2.as<K>(), h->j_val.as<uint64_t>(),
+                                     h->j_val2.as<uint64_t>(), ne, 0, P.key_bits, h->stream),
      "sort size");
-  ck(cub::DeviceRunLengthEncode::Encode(nullptr, b2, h->j_key2.as<uint32_t>(), h->j_uniq.as<uint32_t>(),
-                                        h->j_cnt.as<uint32_t>(), h->j_nruns.as<int>(), ne, h->stream),
-     "rle size");
-  ck(cub::DeviceScan::ExclusiveSum(nullptr, b3, h->j_cnt.as<uint32_t>(), h->j_off.as<uint32_t>(), ne, h->stream),
+  ck(cub::DeviceScan::InclusiveSum(nullptr, b2, h->j_head.as<uint32_t>(), h->j_rid.as<uint32_t>(), ne, h->stream),
      "scan size");
-  h->j_tmp.ensure(std::max({b1, b2, b3}) + 16);
-  ck(cub::DeviceRadixSort::SortPairs(h->j_tmp.p, b1, h->j_key.as<uint32_t>(), h->j_key2.as<uint32_t>(),
-                                     h->j_val.as<uint32_t>(), h->j_val2.as<uint32_t>(), ne, 0, 32, h->stream),
+  h->j_tmp.ensure(std::max(b1, b2) + 16);
+  ck(cub::DeviceRadixSort::SortPairs(h->j_tmp.p, b1, h->j_key.as<K>(), h->j_key2.as<K>(), h->j_val.as<uint64_t>(),
+                                     h->j_val2.as<uint64_t>(), ne, 0, P.key_bits, h->stream),
      "sort");
-  ck(cub::DeviceRunLengthEncode::Encode(h->j_tmp.p, b2, h->j_key2.as<uint32_t>(), h->j_uniq.as<uint32_t>(),
-                                        h->j_cnt.as<uint32_t>(), h->j_nruns.as<int>(), ne, h->stream),
-     "rle");
-  ck(cub::DeviceScan::ExclusiveSum(h->j_tmp.p, b3, h->j_cnt.as<uint32_t>(), h->j_off.as<uint32_t>(), ne, h->stream),
+  ++g_launches;
+  const int egrid = static_cast<int>(std::min<uint64_t>((E + kThreads - 1) / kThreads, grid_for(h, 16)));
+  k_run_heads<K><<<std::max(egrid, 1), kThreads, 0, h->stream>>>(h->j_key2.as<K>(), E, h->j_head.as<uint32_t>());
+  ck_launch("run heads");
+  ck(cub::DeviceScan::InclusiveSum(h->j_tmp.p, b2, h->j_head.as<uint32_t>(), h->j_rid.as<uint32_t>(), ne, h->stream),
      "scan");
-  g_launches += 3;
-  const int rgrid = static_cast<int>(std::min<uint64_t>((E + kThreads - 1) / kThreads, grid_for(h, 8)));
-  k_join_ranges<<<std::max(rgrid, 1), kThreads, 0, h->stream>>>(h->j_off.as<uint32_t>(), h->j_cnt.as<uint32_t>(),
-                                                                h->j_nruns.as<int>(), h->j_val2.as<uint32_t>(), C,
-                                                                h->j_rng.as<uint2>());
-  ck_launch("join ranges");
+  ++g_launches;
+  k_run_bounds<<<std::max(egrid, 1), kThreads, 0, h->stream>>>(h->j_rid.as<uint32_t>(), E, h->j_lo.as<uint32_t>(),
+                                                                h->j_hi.as<uint32_t>());
+  ck_launch("run bounds");
+  k_join_fill<<<std::max(egrid, 1), kThreads, 0, h->stream>>>(h->j_val2.as<uint64_t>(), h->j_rid.as<uint32_t>(), E,
+                                                               C, h->j_lo.as<uint32_t>(), h->j_hi.as<uint32_t>(),
+                                                               h->j_mem.as<uint64_t>(), h->j_rng.as<uint2>());
+  ck_launch("join fill");
+}
+
+template <int W>
+void build_join_index(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowPlan& P) {
+  if (P.key_bits <= 32)
+    build_join_index_k<W, uint32_t>(h, keys, n, P);
+  else
+    build_join_index_k<W, uint64_t>(h, keys, n, P);
 }
 
 JoinView join_view(qvmc_ham_s* h, const RowPlan& P) {
   JoinView J{};
   J.C = static_cast<uint32_t>(P.s * (P.s - 1) / 2);
   J.rng = h->j_rng.as<uint2>();
-  J.vals = h->j_val2.as<uint32_t>();
+  J.mem = h->j_mem.as<uint64_t>();
   J.xy_tab = h->xy_tab.as<uint64_t>();
   J.xy_mask = h->xy_tab_mask;
-  J.codes = h->codes.as<uint64_t>();
+  J.rec = h->l_rec.as<uint64_t>();
+  J.grec = h->grec.as<uint64_t>();
   return J;
 }
 
@@ -436,16 +453,14 @@ void run_rows(qvmc_ham_s* h, const uint64_t* keys, int64_t r0, int64_t r1, const
 // (locality), rebuild the index on the sorted copy, process rows in that
 // order. Returns the row set; keys/la/ph are redirected to the sorted copies.
 template <int W>
-RowSet sort_for_locality(qvmc_ham_s* h, const uint64_t*& keys, const double*& la, const double*& ph,
-                         const double2*& cs, int64_t n, int64_t r0, int64_t r1, const RowPlan& P) {
+RowSet sort_for_locality(qvmc_ham_s* h, const uint64_t*& keys, const double* la, const double* ph, int64_t n,
+                         int64_t r0, int64_t r1, const RowPlan& P) {
   h->l_key.ensure(n * 8 + 16);
   h->l_key2.ensure(n * 8 + 16);
   h->l_idx.ensure(n * 4 + 16);
   h->l_perm.ensure(n * 4 + 16);
   h->l_keys.ensure(n * 8 * W + 16);
-  h->l_la.ensure(n * 8 + 16);
-  h->l_ph.ensure(n * 8 + 16);
-  h->l_cs.ensure(n * 16 + 16);
+  h->l_rec.ensure(n * 32 + 32);
   const int grid = static_cast<int>(std::min<int64_t>((n + kThreads - 1) / kThreads, grid_for(h, 8)));
   k_locality_keys<W><<<std::max(grid, 1), kThreads, 0, h->stream>>>(keys, n, h->n, P.side, h->l_key.as<uint64_t>(),
                                                                     h->l_idx.as<uint32_t>());
@@ -461,13 +476,9 @@ RowSet sort_for_locality(qvmc_ham_s* h, const uint64_t*& keys, const double*& la
      "sort");
   ++g_launches;
   k_gather_sorted<W><<<std::max(grid, 1), kThreads, 0, h->stream>>>(
-      h->l_perm.as<uint32_t>(), n, keys, la, ph, h->l_keys.as<uint64_t>(), h->l_la.as<double>(),
-      h->l_ph.as<double>(), h->l_cs.as<double2>());
+      h->l_perm.as<uint32_t>(), n, keys, la, ph, h->l_keys.as<uint64_t>(), h->l_rec.as<double>());
   ck_launch("gather sorted");
   keys = h->l_keys.as<uint64_t>();
-  la = h->l_la.as<double>();
-  ph = h->l_ph.as<double>();
-  cs = h->l_cs.as<double2>();
   RowSet R{n, 0, nullptr, h->l_perm.as<uint32_t>(), r0};
   if (r0 != 0 || r1 != n) {  // a row shard: the sorted positions of its rows
     h->l_flags.ensure(n + 16);
@@ -683,6 +694,9 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     upload(h->ginfo, p.ginfo);
     upload(h->trec, p.trec);
     upload(h->famrec, p.famrec);
+    upload(h->grec, p.grec);
+    h->binom_host = binomial_table();
+    upload(h->binom, h->binom_host);
     h->xy_tab_mask = p.xy_tab_mask;
     upload(h->codes, std::vector<uint64_t>(qubit_codes(), qubit_codes() + 256));
     if (const char* e = std::getenv("QVMC_JOIN")) h->use_join = std::atoi(e) != 0;
@@ -1044,15 +1058,13 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
     RowPlan P;
     RowSet R{};
     const uint64_t* rkeys = dkeys;
-    const double* rla = dla;
-    const double* rph = dph;
     const double2* rcs = nullptr;
     if (n_unq > 0) {
       DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
       P = plan_rows(h, n_unq);
       note_plan(h, P);
       if (P.join) {
-        DISPATCH_W(W, R = sort_for_locality<WW>(h, rkeys, rla, rph, rcs, n_unq, row_begin, row_end, P));
+        DISPATCH_W(W, R = sort_for_locality<WW>(h, rkeys, dla, dph, n_unq, row_begin, row_end, P));
         if (h->view.n_res) DISPATCH_W(W, launch_table_build<WW>(h, rkeys, n_unq));  // residual probes: sorted ids
         DISPATCH_W(W, build_join_index<WW>(h, rkeys, n_unq, P));
       } else {
@@ -1067,8 +1079,8 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
     if (n_unq > 0) {
       RowOut O{};
       O.eloc = deloc;
-      O.la = rla;
-      O.ph = rph;
+      O.la = dla;
+      O.ph = dph;
       O.cs = rcs;
       if (P.join) {
         DISPATCH_W(W, (launch_rows_join<WW, kModeEloc>(h, rkeys, R, P, O)));

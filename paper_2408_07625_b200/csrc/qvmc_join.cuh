@@ -3,19 +3,23 @@
 // For a single-sector sample set with minority sets S(x) of size s, every
 // partner x' of x through a weight-2 or weight-4 flip mask shares at least
 // s-2 minority orbitals with x. Each sample y is entered into the buckets
-// keyed by S(y) - T for every pair T of S(y) ("deletion index", N*s(s-1)/2
-// entries, rebuilt per call: key generation + one CUB radix sort). For row x
-// and pair T the members of bucket S(x) - T are exactly the samples sharing
-// S(x) - T, i.e. the candidates; the pair's flip mask m = x ^ y is then
-// looked up in the (static) flip-mask hash table. At 118 qubits this visits
-// ~2.1k candidates per row instead of the ~14k masks of the sector lists.
+// keyed by S(y) - T_y for every pair T_y of S(y) ("deletion index", N*s(s-1)/2
+// entries, rebuilt per call). The bucket key is the EXACT combinadic rank of
+// the (s-2)-subset S(y) - T_y, so a bucket holds exactly the samples sharing
+// that subset, and a member entry carries (y, T_y). For row x and its pair
+// T_x the members y of bucket S(x) - T_x satisfy
+//   S(y) = (S(x) - T_x) + T_y   =>   x ^ y = T_x ^ T_y   (as orbital sets),
+// so the flip mask of every candidate is known from the two pairs alone: no
+// key of y is ever loaded during the search. The mask is then looked up in
+// the (static) flip-mask hash table by its exact position key.
 //
 // Each coupled pair is accepted exactly once:
-//   |m| = 4: m & S(x) == T (holds for exactly one pair T of S(x));
-//   |m| = 2: m & S(x) = {c} with c in T, and T's other orbital is the smallest
-//            orbital of S(x) other than c (one of the s-1 buckets holding y);
-//   anything else (y == x, or a 32-bit bucket-key collision) is skipped.
-// Masks of weight >= 6 go through the residual scan of the list path.
+//   T_x and T_y disjoint (|m| = 4): the unique bucket T_x = m & S(x);
+//   |T_x & T_y| = 1 (|m| = 2, x loses c, gains a): the bucket whose other
+//     orbital o is the smallest orbital of S(x) other than c (y sits in the
+//     s-1 buckets {c, o} of x);
+//   T_x = T_y: y = x, skipped (the diagonal is evaluated separately).
+// Masks of weight >= 6 go through the residual scan (sample-set hash probes).
 #pragma once
 
 #include "qvmc_kernels.cuh"
@@ -23,24 +27,62 @@
 namespace qvmc_b200 {
 
 #ifndef QVMC_JOIN_MINB
-#define QVMC_JOIN_MINB 4  // 64 registers: 32 resident warps per SM (measured best)
+#define QVMC_JOIN_MINB 3  // 80 registers: 24 resident warps per SM (measured best with the inlined drain)
 #endif
 
 #ifndef QVMC_JOIN_UNROLL
-#define QVMC_JOIN_UNROLL 2  // bucket members in flight per lane (2 beat 4 and 8: fewer spills at 64 regs)
+#define QVMC_JOIN_UNROLL 4  // bucket members in flight per lane
+#endif
+
+#ifndef QVMC_JOIN_DRAIN_ATTR
+#define QVMC_JOIN_DRAIN_ATTR __forceinline__
 #endif
 
 constexpr int kJoinMaxMinority = 16;  // s <= 16: at most 120 buckets per row
 constexpr int kJoinMaxRanges = kJoinMaxMinority * (kJoinMaxMinority - 1) / 2;
+constexpr int kBinomK = kJoinMaxMinority + 1;  // binomial table C[n][k], k <= 16
+constexpr uint32_t kNoKey = 0xFFFFFFFFu;
+
+// Per-group drain record, 8 words (two 32-byte sectors), host_index.cpp:
+//   kind A (small group, one shared Z string): w0 = 0 | k << 2 | per term t
+//     (ypat_t | (y_weight_t & 3) << 4) << (8 + 6t), ypat_t = Y positions among
+//     the sorted flip positions; w2.. = z words, then the k coefficients
+//   kind B (family-compressed large group): w0 = 1 | n_fam << 8 | q bits << 16,
+//     w1 = first family
+//   kind C (generic): w0 = 2, w1 = t0 | n_terms << 32
+constexpr int kGrecWords = 8;
+enum : uint32_t { kGrecA = 0, kGrecB = 1, kGrecC = 2 };
 
 struct JoinView {
-  uint32_t C;                     // buckets per sample = s(s-1)/2
-  const uint2* rng;               // [N*C] (lo, hi) bucket range in vals, entry id y*C + t
-  const uint32_t* vals;           // sorted entry ids
-  const uint64_t* xy_tab;         // flip-mask hash table, buckets of 4 x (tag32 | group)
+  uint32_t C;              // buckets per sample = s(s-1)/2
+  const uint2* rng;        // [N*C] (lo, hi) of the bucket of (sample y, pair t) in mem
+  const uint64_t* mem;     // bucket members grouped by bucket: y | ta << 32 | tb << 40
+  const uint64_t* xy_tab;  // flip-mask hash table, buckets of 4 x (position key32 << 32 | group)
   uint64_t xy_mask;
-  const uint64_t* codes;          // [256] qubit codes of the linear hash
+  const uint64_t* rec;     // [N][4] per sample (log psi, cos phase, sin phase, 0) bits
+  const uint64_t* grec;    // [n_xy][8] drain records
 };
+
+// Rows of one call. Rows are processed in the order of the (locality-sorted)
+// key arrays; `perm` maps a key-array position back to the caller's row.
+struct RowSet {
+  int64_t n_rows;        // rows to process
+  int64_t base;          // position = base + r when list is null
+  const uint32_t* list;  // else position = list[r]
+  const uint32_t* perm;  // position -> caller row (null: identity)
+  int64_t out_base;      // outputs are indexed by caller row - out_base
+};
+
+struct U64x4 {
+  uint64_t a, b, c, d;
+};
+
+// one 256-bit load (LDG.E.256 on sm_100a); p must be 32-byte aligned
+__device__ __forceinline__ U64x4 ldg256(const uint64_t* p) {
+  U64x4 r;
+  asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(r.a), "=l"(r.b), "=l"(r.c), "=l"(r.d) : "l"(p));
+  return r;
+}
 
 __device__ __forceinline__ uint32_t pair_b(int pi) {  // pairs ordered by b then a: pi = b(b-1)/2 + a
   int b = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * pi)) * 0.5f);
@@ -48,18 +90,6 @@ __device__ __forceinline__ uint32_t pair_b(int pi) {  // pairs ordered by b then
   while ((b + 1) * b / 2 <= pi) ++b;
   return static_cast<uint32_t>(b);
 }
-
-// Per sample: its linear hash and, for every pair T of its minority set, the
-// 32-bit bucket key fmix(hash(S(y) - T)) with value y*C + t.
-// Rows of one call. Rows are processed in the order of the (locality-sorted)
-// key arrays; `perm` maps a key-array position back to the caller's row.
-struct RowSet {
-  int64_t n_rows;          // rows to process
-  int64_t base;            // position = base + r when list is null
-  const uint32_t* list;    // else position = list[r]
-  const uint32_t* perm;    // position -> caller row (null: identity)
-  int64_t out_base;        // outputs are indexed by caller row - out_base
-};
 
 // Locality order for the join: samples sorted by their minority orbitals,
 // highest first (top 8 packed into 64 bits), so that rows processed together
@@ -88,86 +118,107 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Sorted copies of the keys and the per-sample records (log psi, cos, sin).
 template <int W>
 __global__ void k_gather_sorted(const uint32_t* __restrict__ perm, int64_t n, const uint64_t* __restrict__ keys,
                                 const double* __restrict__ la, const double* __restrict__ ph, uint64_t* keys_s,
-                                double* la_s, double* ph_s, double2* cs_s) {
+                                double* rec) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t o = perm[i];
 #pragma unroll
     for (int w = 0; w < W; ++w) keys_s[i * W + w] = keys[(int64_t)o * W + w];
-    la_s[i] = la[o];
-    const double p = ph[o];
-    ph_s[i] = p;
     double sn, c;
-    sincos(p, &sn, &c);
-    cs_s[i] = make_double2(c, sn);
+    sincos(ph[o], &sn, &c);
+    reinterpret_cast<double4*>(rec)[i] = make_double4(la[o], c, sn, 0.0);
   }
 }
 
+// per-sample records in the caller's order (pairs-free fused path without the
+// locality sort is not used; kept for the row-shard gather)
 __global__ void k_flag_rows(const uint32_t* __restrict__ perm, int64_t n, int64_t r0, int64_t r1, uint8_t* flags) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     flags[i] = perm[i] >= r0 && perm[i] < r1;
 }
 
-template <int W>
+// Deletion-index entries: for sample y and pair t = (a < b) of its minority
+// orbitals, key = combinadic rank of S(y) - {pos_a, pos_b} (exact), value =
+// y | pos_a << 32 | pos_b << 40 | t << 48. With the remaining orbitals
+// r_0 < r_1 < ..., rank = sum_i C(r_i, i + 1); an orbital at index j of S(y)
+// has index j (j < a), j - 1 (a < j < b) or j - 2 (j > b) after the removal,
+// so the rank is three prefix-sum differences.
+template <int W, typename K>
 __global__ void __launch_bounds__(kThreads)
     k_join_keys(const uint64_t* __restrict__ keys, int64_t n, int n_qubits, int side, int s,
-                const uint64_t* __restrict__ codes, uint32_t* __restrict__ bkey, uint32_t* __restrict__ bval) {
+                const uint64_t* __restrict__ binom, K* __restrict__ bkey, uint64_t* __restrict__ bval) {
   const uint32_t C = static_cast<uint32_t>(s * (s - 1) / 2);
   for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < n; y += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t x[W];
-#pragma unroll
-    for (int w = 0; w < W; ++w) x[w] = keys[y * W + w];
     uint8_t pos[kJoinMaxMinority];
-    uint64_t hs = 0;
+    uint64_t P0[kJoinMaxMinority + 1], P1[kJoinMaxMinority + 1], P2[kJoinMaxMinority + 1];
     int k = 0;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      uint64_t v = side ? x[w] : ~x[w];
+      uint64_t v = side ? keys[y * W + w] : ~keys[y * W + w];
       const int hi_bit = n_qubits - 64 * w;
       if (hi_bit < 64) v &= (hi_bit <= 0) ? 0ull : ((1ull << hi_bit) - 1);
       while (v && k < kJoinMaxMinority) {
-        const int p = 64 * w + __ffsll(static_cast<long long>(v)) - 1;
-        pos[k++] = static_cast<uint8_t>(p);
-        hs ^= __ldg(codes + p);
+        pos[k++] = static_cast<uint8_t>(64 * w + __ffsll(static_cast<long long>(v)) - 1);
         v &= v - 1;
       }
+    }
+    P0[0] = P1[0] = P2[0] = 0;
+    for (int j = 0; j < s; ++j) {
+      const uint64_t* row = binom + static_cast<int64_t>(pos[j]) * kBinomK;
+      P0[j + 1] = P0[j] + __ldg(row + j + 1);
+      P1[j + 1] = P1[j] + (j >= 1 ? __ldg(row + j) : 0ull);
+      P2[j + 1] = P2[j] + (j >= 2 ? __ldg(row + j - 1) : 0ull);
     }
     const uint64_t base = static_cast<uint64_t>(y) * C;
     uint32_t t = 0;
     for (int b = 1; b < s; ++b)
       for (int a = 0; a < b; ++a, ++t) {
-        const uint64_t hk = hs ^ __ldg(codes + pos[a]) ^ __ldg(codes + pos[b]);
-        bkey[base + t] = static_cast<uint32_t>(fmix(hk));
-        bval[base + t] = static_cast<uint32_t>(base + t);
+        const uint64_t rank = P0[a] + (P1[b] - P1[a + 1]) + (P2[s] - P2[b + 1]);
+        bkey[base + t] = static_cast<K>(rank);
+        bval[base + t] = static_cast<uint64_t>(y) | static_cast<uint64_t>(pos[a]) << 32 |
+                         static_cast<uint64_t>(pos[b]) << 40 | static_cast<uint64_t>(t) << 48;
       }
   }
 }
 
-// Per bucket (run of equal keys in the sorted array): store the range on
-// every member entry.
-__global__ void k_join_ranges(const uint32_t* __restrict__ run_off, const uint32_t* __restrict__ run_cnt,
-                              const int* __restrict__ n_runs, uint32_t* __restrict__ vals, uint32_t C, uint2* rng) {
-  const int nr = *n_runs;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += gridDim.x * blockDim.x) {
-    const uint32_t lo = run_off[r], hi = lo + run_cnt[r];
-    for (uint32_t p = lo; p < hi; ++p) {
-      const uint32_t e = vals[p];
-      rng[e] = make_uint2(lo, hi);
-      vals[p] = e / C;  // entry id -> sample
-    }
+template <typename K>
+__global__ void k_run_heads(const K* __restrict__ key, uint64_t E, uint32_t* __restrict__ head) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < E; p += (uint64_t)gridDim.x * blockDim.x)
+    head[p] = (p == 0 || key[p] != key[p - 1]) ? 1u : 0u;
+}
+
+// rid = inclusive scan of the heads (1-based run id of every sorted entry)
+__global__ void k_run_bounds(const uint32_t* __restrict__ rid, uint64_t E, uint32_t* __restrict__ lo,
+                             uint32_t* __restrict__ hi) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < E; p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = rid[p];
+    if (p == 0 || rid[p - 1] != r) lo[r - 1] = static_cast<uint32_t>(p);
+    if (p + 1 == E || rid[p + 1] != r) hi[r - 1] = static_cast<uint32_t>(p + 1);
   }
 }
 
-// flip-mask table lookup by exact position key (host_index.cpp xy_position_key):
-// group of the mask or -1
-__device__ __forceinline__ int64_t xy_lookup(uint32_t key, const uint64_t* __restrict__ tab, uint64_t mask) {
+// member array + per-(sample, pair) bucket range
+__global__ void k_join_fill(const uint64_t* __restrict__ val, const uint32_t* __restrict__ rid, uint64_t E, uint32_t C,
+                            const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi,
+                            uint64_t* __restrict__ mem, uint2* __restrict__ rng) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < E; p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = val[p];
+    const uint32_t r = rid[p] - 1;
+    const uint64_t y = v & 0xFFFFFFFFull, t = v >> 48;
+    rng[y * C + t] = make_uint2(lo[r], hi[r]);
+    mem[p] = v & 0x0000FFFFFFFFFFFFull;
+  }
+}
+
+// group of a flip mask by its exact position key (host_index.cpp xy_position_key), or -1
+__device__ __forceinline__ int64_t xy_find(uint32_t key, const uint64_t* __restrict__ tab, uint64_t mask) {
   uint64_t b = fmix(key) & mask;
   for (;;) {
-    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(tab + b * 4);
-    const ulonglong2 b0 = __ldg(p), b1 = __ldg(p + 1);
-    const uint64_t e[4] = {b0.x, b0.y, b1.x, b1.y};
+    const U64x4 q = ldg256(tab + b * 4);
+    const uint64_t e[4] = {q.a, q.b, q.c, q.d};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (e[k] == kEmpty) return -1;
@@ -175,49 +226,29 @@ __device__ __forceinline__ int64_t xy_lookup(uint32_t key, const uint64_t* __res
     }
     b = (b + 1) & mask;  // full bucket: the chain continues
   }
-}
-
-constexpr uint32_t kNoKey = 0xFFFFFFFFu;
-
-// resolve a flip-mask lookup given its first bucket (already loaded)
-__device__ __forceinline__ int64_t xy_resolve(uint32_t key, uint64_t b, ulonglong2 b0, ulonglong2 b1,
-                                              const uint64_t* __restrict__ tab, uint64_t mask) {
-  for (;;) {
-    const uint64_t e[4] = {b0.x, b0.y, b1.x, b1.y};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (e[k] == kEmpty) return -1;
-      if (static_cast<uint32_t>(e[k] >> 32) == key) return static_cast<uint32_t>(e[k]);
-    }
-    b = (b + 1) & mask;  // full bucket: the chain continues
-    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(tab + b * 4);
-    b0 = __ldg(p);
-    b1 = __ldg(p + 1);
-  }
-}
-
-template <int W>
-__device__ __forceinline__ int lowest_bit(const uint64_t* v) {  // v != 0
-  int r = 0;
-#pragma unroll
-  for (int w = W - 1; w >= 0; --w)
-    if (v[w]) r = 64 * w + __ffsll(static_cast<long long>(v[w])) - 1;
-  return r;
-}
-
-template <int W>
-__device__ __forceinline__ int highest_bit(const uint64_t* v) {  // v != 0
-  int r = 0;
-#pragma unroll
-  for (int w = 0; w < W; ++w)
-    if (v[w]) r = 64 * w + 63 - __clzll(static_cast<long long>(v[w]));
-  return r;
 }
 
 __device__ __forceinline__ void sort2(int& a, int& b) {
   const int lo = min(a, b), hi = max(a, b);
   a = lo;
   b = hi;
+}
+
+// flip mask of a position key (weight 2: upper half 0xFFFF)
+template <int W>
+__device__ __forceinline__ void key_mask(uint32_t key, uint64_t* m) {
+#pragma unroll
+  for (int w = 0; w < W; ++w) m[w] = 0;
+  const int np = (key >> 16) == 0xFFFFu ? 2 : 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i < np) {
+      const int p = (key >> (8 * i)) & 0xFF;
+#pragma unroll
+      for (int w = 0; w < W; ++w)
+        if ((p >> 6) == w) m[w] |= 1ull << (p & 63);
+    }
+  }
 }
 
 template <int W>
@@ -229,18 +260,166 @@ __device__ __forceinline__ bool bit_at(const uint64_t* v, int p) {
   return (w >> (p & 63)) & 1ull;
 }
 
+// H_{x x'} of a kind-A group: sum_t c_t i^{(y_t + 2|x' & z| + 2|b & ypat_t|) mod 4}
+// in term order, b = occupations of x' at the sorted flip positions. Same
+// terms, same order, same exact +-c adds as group_element: bit-identical.
+template <int W>
+__device__ __forceinline__ void kind_a_element(const uint64_t* r, const uint64_t* xp, uint32_t key, double& re,
+                                               double& im) {
+  re = 0.0;
+  im = 0.0;
+  const uint64_t meta = r[0];
+  const int k = static_cast<int>((meta >> 2) & 7);
+  int pz = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) pz += __popcll(xp[w] & r[2 + w]);
+  const int np = (key >> 16) == 0xFFFFu ? 2 : 4;
+  uint32_t bp = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i < np) bp |= (bit_at<W>(xp, (key >> (8 * i)) & 0xFF) ? 1u : 0u) << i;
+#pragma unroll
+  for (int t = 0; t < kGrecWords - 2 - W; ++t) {
+    if (t < k) {
+      const uint32_t f = static_cast<uint32_t>(meta >> (8 + 6 * t)) & 63u;
+      const int q = (static_cast<int>(f >> 4) + 2 * (pz + __popc(bp & f & 15u))) & 3;
+      const double c = __longlong_as_double(static_cast<long long>(r[2 + W + t]));
+      if (q == 0) re += c;
+      else if (q == 2) re -= c;
+      else if (q == 1) im += c;
+      else im -= c;
+    }
+  }
+}
+
+// Per-warp state of the join kernel.
+constexpr int kJQueue = 256;
+constexpr int kJDrainAt = kJQueue - 32 * QVMC_JOIN_UNROLL;  // one scan step adds at most 32*U hits
+
+struct JoinSmem {
+  uint32_t qy[kJQueue];  // hit queue: partner (sorted position), group, flip position key
+  uint32_t qg[kJQueue];
+  uint32_t qk[kJQueue];
+  uint32_t r_lo[kJoinMaxRanges];  // bucket ranges of the current row
+  uint32_t r_len[kJoinMaxRanges];
+  uint8_t ta[kJoinMaxRanges];     // the row's pair T_x of each bucket
+  uint8_t tb[kJoinMaxRanges];
+  uint64_t x[4];                  // the current row: key, log psi, (cos, sin) of its phase; kept here
+  double la, cs_c, cs_s;          // (not in registers) across the candidate walk
+  uint16_t pos[32];               // minority orbitals of the current row
+  unsigned qn;
+  unsigned cursor;                // kModeEmit output cursor
+};
+
+// warp-uniform row state, re-read from shared memory (volatile: not forwarded
+// from registers, so it is not live across the candidate walk)
+template <int W>
+__device__ __forceinline__ Key<W> row_key(const JoinSmem* sm) {
+  Key<W> k;
+#pragma unroll
+  for (int w = 0; w < W; ++w) k.w[w] = reinterpret_cast<const volatile uint64_t*>(sm->x)[w];
+  return k;
+}
+
+// Drain the warp's hit queue: this lane's share of sum H_{xx'} psi(x')/psi(x).
+template <int W>
+__device__ QVMC_JOIN_DRAIN_ATTR double2 join_drain(const HamView& H, const JoinView& J, JoinSmem* sm, int lane, int s,
+                                                   int side) {
+  double2 acc = make_double2(0.0, 0.0);
+  __syncwarp();
+  const Key<W> xrow = row_key<W>(sm);
+  const double la_i = *reinterpret_cast<const volatile double*>(&sm->la);
+  const double2 cs_i = make_double2(*reinterpret_cast<const volatile double*>(&sm->cs_c),
+                                    *reinterpret_cast<const volatile double*>(&sm->cs_s));
+  const unsigned n = sm->qn;
+  for (unsigned k0 = 0; k0 < n; k0 += 32) {
+    const unsigned k = k0 + lane;
+    const bool valid = k < n;
+    uint32_t key = kNoKey;
+    uint64_t r[kGrecWords];
+    U64x4 sr = {0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < kGrecWords; ++i) r[i] = 0;
+    if (valid) {  // independent loads first: sample record + both halves of the group record
+      const uint32_t y = sm->qy[k], g = sm->qg[k];
+      key = sm->qk[k];
+      sr = ldg256(J.rec + static_cast<int64_t>(y) * 4);
+      const U64x4 g0 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords);
+      const U64x4 g1 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords + 4);
+      r[0] = g0.a; r[1] = g0.b; r[2] = g0.c; r[3] = g0.d;
+      r[4] = g1.a; r[5] = g1.b; r[6] = g1.c; r[7] = g1.d;
+    }
+    uint64_t xp[W];
+    {
+      uint64_t m[W];
+      key_mask<W>(key, m);
+#pragma unroll
+      for (int w = 0; w < W; ++w) xp[w] = xrow.w[w] ^ m[w];
+    }
+    const uint32_t kind = static_cast<uint32_t>(r[0]) & 3u;
+    const uint32_t nt = static_cast<uint32_t>(r[1] >> 32);
+    const bool large = valid && kind == kGrecC && nt > kSmallGroup;
+    double hr = 0.0, hi = 0.0;
+    if (valid && !large) {
+      if (kind == kGrecA) {
+        kind_a_element<W>(r, xp, key, hr, hi);
+      } else if (kind == kGrecB) {
+        const uint4 gi = make_uint4(0, 0, static_cast<uint32_t>(r[1]), static_cast<uint32_t>(r[0] >> 8));
+        comp_element<W>(H, xrow.w, xp, gi, sm->pos, s, side, hr, hi);
+      } else {
+        const uint4 gi = make_uint4(static_cast<uint32_t>(r[1]), nt, 0xFFFFFFFFu, 0);
+        small_element<W>(H, xp, gi, hr, hi);
+      }
+    }
+    // large generic groups: the warp splits the terms; element parked in lane src
+    unsigned mask = __ballot_sync(0xffffffffu, large);
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const uint32_t st0 = __shfl_sync(0xffffffffu, static_cast<uint32_t>(r[1]), src);
+      const uint32_t st1 = st0 + __shfl_sync(0xffffffffu, nt, src);
+      uint64_t sx[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) sx[w] = __shfl_sync(0xffffffffu, xp[w], src);
+      double re = 0.0, im = 0.0;
+      for (uint32_t t = st0 + lane; t < st1; t += 32) {
+        int pc = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) pc += __popcll(sx[w] & __ldg(H.yz + (int64_t)t * W + w));
+        const int qt = (__ldg(H.yw + t) + 2 * pc) & 3;
+        const double c = __ldg(H.coeff + t);
+        if (qt == 0) re += c;
+        else if (qt == 2) re -= c;
+        else if (qt == 1) im += c;
+        else im -= c;
+      }
+      re = warp_sum(re);
+      im = warp_sum(im);
+      if (lane == src) {
+        hr = re;
+        hi = im;
+      }
+    }
+    if (valid) {
+      const double2 cs_j = make_double2(__longlong_as_double(static_cast<long long>(sr.b)),
+                                        __longlong_as_double(static_cast<long long>(sr.c)));
+      add_ratio(__longlong_as_double(static_cast<long long>(sr.a)), cs_j, la_i, cs_i, hr, hi, acc);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) sm->qn = 0;
+  __syncwarp();
+  return acc;
+}
+
 template <int W, int MODE>
-__global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __grid_constant__ HamView H, const TableView T,
-                                                        const __grid_constant__ JoinView J,
-                                                        const uint64_t* __restrict__ keys, const RowSet R,
-                                                        int side, int s,
-                                                        const __grid_constant__ Ctl C,
-                                                        const __grid_constant__ RowOut O) {
-  __shared__ WarpSmem s_w[kWarps];
-  __shared__ uint16_t s_ta[kWarps][kJoinMaxRanges], s_tb[kWarps][kJoinMaxRanges];
+__global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
+    k_rows_join(const __grid_constant__ HamView H, const TableView T, const __grid_constant__ JoinView J,
+                const uint64_t* __restrict__ keys, const RowSet R, int side, int s, const __grid_constant__ Ctl C,
+                const __grid_constant__ RowOut O) {
+  __shared__ JoinSmem s_w[kWarps];
   const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
-  WarpSmem* sm = &s_w[wid];
+  JoinSmem* sm = &s_w[threadIdx.x >> 5];
   const int n = H.n;
   const int n_ranges = s * (s - 1) / 2;
   if (lane == 0) sm->qn = 0;
@@ -255,18 +434,35 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
     const int64_t row = R.list ? static_cast<int64_t>(__ldg(R.list + r)) : R.base + static_cast<int64_t>(r);
     const int64_t orow = R.perm ? static_cast<int64_t>(__ldg(R.perm + row)) : row;  // caller's row
 
-    uint64_t x[W];
+    uint64_t S[W];
+    {
+      Key<W> xrow;
 #pragma unroll
-    for (int w = 0; w < W; ++w) x[w] = __ldg(keys + row * W + w);
-    Key<W> xrow;
+      for (int w = 0; w < W; ++w) xrow.w[w] = __ldg(keys + row * W + w);
+      double la_i = 0.0;
+      U64x4 sr = {0, 0, 0, 0};
+      if (MODE == kModeEloc) {
+        sr = ldg256(J.rec + row * 4);
+        la_i = __longlong_as_double(static_cast<long long>(sr.a));
+      }
+      __syncwarp();
+      if (lane == 0) {
 #pragma unroll
-    for (int w = 0; w < W; ++w) xrow.w[w] = x[w];
-    double la_i = 0.0;
-    double2 cs_i = make_double2(1.0, 0.0);
+        for (int w = 0; w < W; ++w) sm->x[w] = xrow.w[w];
+        sm->la = la_i;
+        sm->cs_c = __longlong_as_double(static_cast<long long>(sr.b));
+        sm->cs_s = __longlong_as_double(static_cast<long long>(sr.c));
+      }
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        S[w] = side ? xrow.w[w] : ~xrow.w[w];
+        const int hi_bit = n - 64 * w;
+        if (hi_bit < 64) S[w] &= (hi_bit <= 0) ? 0ull : ((1ull << hi_bit) - 1);
+      }
+    }
+    __syncwarp();
     if (MODE == kModeEloc) {
-      la_i = __ldg(O.la + row);
-      cs_i = __ldg(O.cs + row);
-      if (isinf(la_i)) {  // energy.cpp:32-33
+      if (isinf(*reinterpret_cast<const volatile double*>(&sm->la))) {  // energy.cpp:32-33
         if (lane == 0) {
           atomicOr(C.err, kErrZeroAmp);
           O.eloc[orow - R.out_base] = make_double2(CUDART_NAN, CUDART_NAN);
@@ -276,13 +472,6 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
     }
     if (MODE == kModeEmit && lane == 0) sm->cursor = 0;
 
-    uint64_t S[W];
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-      S[w] = side ? x[w] : ~x[w];
-      const int hi_bit = n - 64 * w;
-      if (hi_bit < 64) S[w] &= (hi_bit <= 0) ? 0ull : ((1ull << hi_bit) - 1);
-    }
     int pos = 0, c = 0;  // lane a < s holds the a-th minority orbital
 #pragma unroll
     for (int w = 0; w < W; ++w) {
@@ -300,8 +489,8 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
     // bucket t of this row: pair (a, b) of S(x), range from the index
     for (int t = lane; t < n_ranges; t += 32) {
       const uint32_t b = pair_b(t);
-      s_ta[wid][t] = sm->pos[t - b * (b - 1) / 2];
-      s_tb[wid][t] = sm->pos[b];
+      sm->ta[t] = static_cast<uint8_t>(sm->pos[t - b * (b - 1) / 2]);
+      sm->tb[t] = static_cast<uint8_t>(sm->pos[b]);
       const uint2 rg = __ldg(J.rng + static_cast<uint64_t>(row) * J.C + t);
       sm->r_lo[t] = rg.x;
       sm->r_len[t] = rg.y - rg.x;
@@ -320,14 +509,14 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
     }
     while (__any_sync(0xffffffffu, rg < n_ranges)) {
       constexpr int U = QVMC_JOIN_UNROLL;
-      uint32_t y[U];
+      uint64_t v[U];
       int tr[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        y[u] = 0xffffffffu;
+        v[u] = ~0ull;
         tr[u] = rg;
         if (rg < n_ranges) {
-          y[u] = __ldg(J.vals + sm->r_lo[rg] + off);
+          v[u] = __ldg(J.mem + sm->r_lo[rg] + off);
           off += 32;
           while (rg < n_ranges && off >= len) {
             off -= len;
@@ -335,66 +524,30 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
           }
         }
       }
-      uint64_t yk[U][W];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (y[u] != 0xffffffffu) {
-#pragma unroll
-          for (int w = 0; w < W; ++w) yk[u][w] = __ldg(keys + (int64_t)y[u] * W + w);
-        }
-      }
       // accept rule (header comment) -> exact position key of the flip mask
       uint32_t key[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         key[u] = kNoKey;
-        if (y[u] == 0xffffffffu) continue;
-        uint64_t ms[W], o[W];
-        int pw = 0, ps = 0;
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          const uint64_t m = x[w] ^ yk[u][w];
-          ms[w] = m & S[w];  // annihilated minority orbitals
-          o[w] = m & ~S[w];  // created ones
-          pw += __popcll(m);
-          ps += __popcll(ms[w]);
-        }
-        const int ta = s_ta[wid][tr[u]], tb = s_tb[wid][tr[u]];
-        if (pw == 4 && ps == 2) {
-          bool is_t = true;  // m & S(x) == T
-#pragma unroll
-          for (int w = 0; w < W; ++w) {
-            const uint64_t t = ((ta >> 6) == w ? 1ull << (ta & 63) : 0ull) | ((tb >> 6) == w ? 1ull << (tb & 63) : 0ull);
-            is_t &= ms[w] == t;
-          }
-          if (is_t) {
-            int p0 = ta, p1 = tb, p2 = lowest_bit<W>(o), p3 = highest_bit<W>(o);  // merge two sorted pairs
-            sort2(p0, p2);
-            sort2(p1, p3);
-            sort2(p1, p2);
-            key[u] = static_cast<uint32_t>(p0) | static_cast<uint32_t>(p1) << 8 | static_cast<uint32_t>(p2) << 16 |
-                     static_cast<uint32_t>(p3) << 24;
-          }
-        } else if (pw == 2 && ps == 1) {
-          const int cpos = lowest_bit<W>(ms), apos = lowest_bit<W>(o);
-          const int other = cpos == ta ? tb : (cpos == tb ? ta : -1);
-          if (other >= 0 && other == (cpos == pos0 ? pos1 : pos0)) {
-            int p0 = cpos, p1 = apos;
+        if (v[u] == ~0ull) continue;
+        const int ya = static_cast<int>(v[u] >> 32) & 0xFF, yb = static_cast<int>(v[u] >> 40) & 0xFF;
+        const int ta = sm->ta[tr[u]], tb = sm->tb[tr[u]];
+        const bool ea = ya == ta || ya == tb, eb = yb == ta || yb == tb;
+        if (!ea && !eb) {  // disjoint pairs: double excitation; merge two sorted pairs
+          int p0 = ta, p1 = tb, p2 = ya, p3 = yb;
+          sort2(p0, p2);
+          sort2(p1, p3);
+          sort2(p1, p2);
+          key[u] = static_cast<uint32_t>(p0) | static_cast<uint32_t>(p1) << 8 | static_cast<uint32_t>(p2) << 16 |
+                   static_cast<uint32_t>(p3) << 24;
+        } else if (ea != eb) {  // one shared orbital o: x loses c, gains a
+          const int o = ea ? ya : yb, a = ea ? yb : ya;
+          const int cc = (o == ta) ? tb : ta;
+          if (o == (cc == pos0 ? pos1 : pos0)) {
+            int p0 = cc, p1 = a;
             sort2(p0, p1);
             key[u] = static_cast<uint32_t>(p0) | static_cast<uint32_t>(p1) << 8 | 0xFFFF0000u;
           }
-        }
-      }
-      // flip-mask lookups: first buckets of all U in flight, then resolve
-      ulonglong2 b0[U], b1[U];
-      uint64_t bk[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (key[u] != kNoKey) {
-          bk[u] = fmix(key[u]) & J.xy_mask;
-          const ulonglong2* p = reinterpret_cast<const ulonglong2*>(J.xy_tab + bk[u] * 4);
-          b0[u] = __ldg(p);
-          b1[u] = __ldg(p + 1);
         }
       }
 #pragma unroll
@@ -402,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
         int64_t g = -1;
         if (key[u] != kNoKey) {
           ++cand;
-          g = xy_resolve(key[u], bk[u], b0[u], b1[u], J.xy_tab, J.xy_mask);
+          g = xy_find(key[u], J.xy_tab, J.xy_mask);
         }
         // warp-aggregated append of the hits
         const bool hit = g >= 0;
@@ -414,12 +567,14 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
             base = __shfl_sync(0xffffffffu, base, 0);
             if (hit) {
               const unsigned k = base + __popc(hm & ((1u << lane) - 1u));
+              const uint32_t y = static_cast<uint32_t>(v[u]);
               if (MODE == kModeEloc) {
-                sm->qj[k] = y[u];
+                sm->qy[k] = y;
                 sm->qg[k] = static_cast<uint32_t>(g);
+                sm->qk[k] = key[u];
               } else {
                 const uint64_t at = O.row_off[orow] + k;
-                O.xp_out[at] = R.perm ? __ldg(R.perm + y[u]) : y[u];
+                O.xp_out[at] = R.perm ? __ldg(R.perm + y) : y;
                 O.g_out[at] = static_cast<uint32_t>(g);
               }
             }
@@ -429,45 +584,60 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
       }
       if (MODE == kModeEloc) {
         __syncwarp();
-        if (sm->qn >= kDrainAt) {
-          const double2 d = drain<W>(H, keys, O.la, O.cs, la_i, cs_i, sm, lane, xrow, s, side);
+        if (sm->qn >= kJDrainAt) {
+          const double2 d = join_drain<W>(H, J, sm, lane, s, side);
           acc.x += d.x;
           acc.y += d.y;
         }
       }
     }
 
+    const Key<W> xrow = row_key<W>(sm);
     // even flip masks of weight >= 6: popcount filter + sample-set probe
-    const uint64_t hx_res = H.n_res ? key_hash_warp<W>(x, H.hash_bytes, lane) : 0ull;
-    for (uint32_t base = 0; base < H.n_res; base += 32) {
-      const uint32_t e = base + lane;
-      if (e < H.n_res) {
-        const uint32_t g = __ldg(H.res_g + e);
-        int in_s = 0, wt = 0;
+    if (H.n_res) {
+      uint64_t S[W];
 #pragma unroll
-        for (int w = 0; w < W; ++w) {
-          const uint64_t mm = __ldg(H.xy + (int64_t)g * W + w);
-          in_s += __popcll(mm & S[w]);
-          wt += __popcll(mm);
-        }
-        if (2 * in_s == wt) {
-          Key<W> xk;
-#pragma unroll
-          for (int w = 0; w < W; ++w) xk.w[w] = x[w];
-          ++cand;
-          const int64_t j = probe_slow<W>(xk, fmix(hx_res ^ __ldg(H.xy_hash + g)), g, T.tab, T.mask, keys, H.xy);
-          if (j >= 0) {
-            on_hit<W, MODE>(O, orow, (MODE == kModeEmit && R.perm) ? static_cast<int64_t>(__ldg(R.perm + j)) : j, g, sm);
-            ++hits;
-          }
-        }
+      for (int w = 0; w < W; ++w) {
+        S[w] = side ? xrow.w[w] : ~xrow.w[w];
+        const int hi_bit = n - 64 * w;
+        if (hi_bit < 64) S[w] &= (hi_bit <= 0) ? 0ull : ((1ull << hi_bit) - 1);
       }
-      if (MODE == kModeEloc) {
-        __syncwarp();
-        if (sm->qn >= kDrainAt) {
-          const double2 d = drain<W>(H, keys, O.la, O.cs, la_i, cs_i, sm, lane, xrow, s, side);
-          acc.x += d.x;
-          acc.y += d.y;
+      const uint64_t hx_res = key_hash_warp<W>(xrow.w, H.hash_bytes, lane);
+      for (uint32_t base = 0; base < H.n_res; base += 32) {
+        const uint32_t e = base + lane;
+        if (e < H.n_res) {
+          const uint32_t g = __ldg(H.res_g + e);
+          int in_s = 0, wt = 0;
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            const uint64_t mm = __ldg(H.xy + (int64_t)g * W + w);
+            in_s += __popcll(mm & S[w]);
+            wt += __popcll(mm);
+          }
+          if (2 * in_s == wt) {
+            ++cand;
+            const int64_t j = probe_slow<W>(xrow, fmix(hx_res ^ __ldg(H.xy_hash + g)), g, T.tab, T.mask, keys, H.xy);
+            if (j >= 0) {
+              ++hits;
+              if (MODE == kModeEmit) {
+                const unsigned k = atomicAdd(&sm->cursor, 1u);
+                const uint64_t at = O.row_off[orow] + k;
+                O.xp_out[at] = R.perm ? __ldg(R.perm + j) : static_cast<uint32_t>(j);
+                O.g_out[at] = g;
+              } else if (MODE == kModeEloc) {  // rare: evaluated in place, term by term
+                uint64_t xp[W];
+#pragma unroll
+                for (int w = 0; w < W; ++w) xp[w] = __ldg(keys + j * W + w);
+                double hr, hi;
+                group_element<W>(H, xp, g, hr, hi);
+                const U64x4 sr = ldg256(J.rec + j * 4);
+                add_ratio(__longlong_as_double(static_cast<long long>(sr.a)),
+                          make_double2(__longlong_as_double(static_cast<long long>(sr.b)),
+                                       __longlong_as_double(static_cast<long long>(sr.c))),
+                          sm->la, make_double2(sm->cs_c, sm->cs_s), hr, hi, acc);
+              }
+            }
+          }
         }
       }
     }
@@ -477,12 +647,12 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
       if (H.diag_quad) {
         if (lane == 0) acc.x += side ? H.diag_A1 : H.diag_A0;
         if (lane < s) acc.x += __ldg(H.diag_b + side * n + pos);
-        for (int pi = lane; pi < n_ranges; pi += 32) acc.x += __ldg(H.diag_K + s_ta[wid][pi] * n + s_tb[wid][pi]);
+        for (int pi = lane; pi < n_ranges; pi += 32) acc.x += __ldg(H.diag_K + sm->ta[pi] * n + sm->tb[pi]);
         for (uint32_t e = lane; e < H.n_diag_other; e += 32) {
           const uint32_t t = __ldg(H.diag_other + e);
           int pc = 0;
 #pragma unroll
-          for (int w = 0; w < W; ++w) pc += __popcll(x[w] & __ldg(H.yz + (int64_t)t * W + w));
+          for (int w = 0; w < W; ++w) pc += __popcll(xrow.w[w] & __ldg(H.yz + (int64_t)t * W + w));
           const int qt = (__ldg(H.yw + t) + 2 * pc) & 3;
           const double cf = __ldg(H.coeff + t);
           if (qt == 0) acc.x += cf;
@@ -495,7 +665,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
         for (uint32_t t = __ldg(H.goff + H.diag) + lane; t < t1; t += 32) {
           int pc = 0;
 #pragma unroll
-          for (int w = 0; w < W; ++w) pc += __popcll(x[w] & __ldg(H.yz + (int64_t)t * W + w));
+          for (int w = 0; w < W; ++w) pc += __popcll(xrow.w[w] & __ldg(H.yz + (int64_t)t * W + w));
           const int qt = (__ldg(H.yw + t) + 2 * pc) & 3;
           const double cf = __ldg(H.coeff + t);
           if (qt == 0) acc.x += cf;
@@ -509,7 +679,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB) k_rows_join(const __
     if (MODE == kModeEloc) {
       __syncwarp();
       if (sm->qn > 0) {
-        const double2 d = drain<W>(H, keys, O.la, O.cs, la_i, cs_i, sm, lane, xrow, s, side);
+        const double2 d = join_drain<W>(H, J, sm, lane, s, side);
         acc.x += d.x;
         acc.y += d.y;
       }
