@@ -395,16 +395,46 @@ DevicePlan plan_device(const HostIndex& h) {
       uint64_t* r = &p.grec[static_cast<size_t>(g) * kGrecWordsHost];
       const uint64_t t0 = h.offsets[g], t1 = h.offsets[g + 1], k = t1 - t0;
       const int32_t c = p.comp_of[g];
-      if (c >= 0) {
-        const uint32_t f0 = p.fam_off[c], f1 = p.fam_off[c + 1];
-        uint64_t qb = 0;
-        for (uint32_t f = f0; f < f1; ++f) qb |= static_cast<uint64_t>(p.fam_q[f] & 3) << (2 * (f - f0));
-        r[0] = 1 | static_cast<uint64_t>(f1 - f0) << 8 | qb << 16;
-        r[1] = f0;
-        continue;
-      }
       const uint64_t* xy = &h.xy[static_cast<size_t>(g) * W];
       const int wt = p.xy_weight[g];
+      if (c >= 0) {
+        const uint32_t f0 = p.fam_off[c], f1 = p.fam_off[c + 1], nf = f1 - f0;
+        uint64_t qb = 0;
+        for (uint32_t f = f0; f < f1; ++f) qb |= static_cast<uint64_t>(p.fam_q[f] & 3) << (2 * (f - f0));
+        // compact form: every family base B_f = (shared Z string) | (Y positions among the flip positions)
+        bool compact = wt == 2 && 2 + W + 2 * static_cast<int>(nf) <= kGrecWordsHost;
+        int xpos[2], np = 0;
+        for (int w = 0; w < W && compact; ++w)
+          for (uint64_t v = xy[w]; v && np < 2; v &= v - 1) xpos[np++] = w * 64 + std::countr_zero(v);
+        uint64_t ypats = 0;
+        for (uint32_t f = f0; f < f1 && compact; ++f) {
+          const uint64_t* B = &p.fam_B[static_cast<size_t>(f) * W];
+          for (int w = 0; w < W; ++w)
+            if ((B[w] & ~xy[w]) != (p.fam_B[static_cast<size_t>(f0) * W + w] & ~xy[w])) compact = false;
+          uint64_t yp = 0;
+          for (int i = 0; i < np; ++i)
+            if ((B[xpos[i] >> 6] >> (xpos[i] & 63)) & 1) yp |= 1ull << i;
+          ypats |= yp << (4 * (f - f0));
+        }
+        if (compact) {
+          const uint32_t nfp = nf == 1 ? 1 : nf == 2 ? 2 : 4;
+          while (p.famvi.size() % 4) p.famvi.push_back(0.0);  // 32-byte aligned blocks
+          r[0] = 1 | static_cast<uint64_t>(nf) << 8 | qb << 16 | ypats << 24;
+          r[1] = p.famvi.size();
+          for (int w = 0; w < W; ++w) r[2 + w] = p.fam_B[static_cast<size_t>(f0) * W + w] & ~xy[w];
+          for (uint32_t f = f0; f < f1; ++f) {
+            std::memcpy(&r[2 + W + 2 * (f - f0)], &p.fam_u[f], 8);
+            std::memcpy(&r[3 + W + 2 * (f - f0)], &p.fam_V[f], 8);
+          }
+          for (int k = 0; k < n; ++k)
+            for (uint32_t j = 0; j < nfp; ++j)
+              p.famvi.push_back(j < nf ? p.fam_v[static_cast<size_t>(f0 + j) * n + k] : 0.0);
+        } else {
+          r[0] = 3 | static_cast<uint64_t>(nf) << 8 | qb << 16;
+          r[1] = f0;
+        }
+        continue;
+      }
       bool a_ok = static_cast<int64_t>(g) != h.diag && (wt == 2 || wt == 4) && k >= 1 &&
                   k <= static_cast<uint64_t>(kGrecWordsHost - 2 - W);
       int xpos[4], np = 0;
@@ -432,13 +462,41 @@ DevicePlan plan_device(const HostIndex& h) {
     }
   }
 
+  // existence bitmaps of the weight-2/4 masks over orbital pairs (join-path
+  // prefilter: a candidate's mask is looked up only when its bit is set)
+  if (n <= 128) {
+    const uint64_t P = static_cast<uint64_t>(n) * (n - 1) / 2;
+    p.pbits_P = static_cast<uint32_t>(P);
+    p.pbits.assign((P + P * P + 31) / 32, 0);
+    auto pid = [](int a, int b) { return static_cast<uint64_t>(b) * (b - 1) / 2 + a; };  // a < b
+    auto set = [&](uint64_t i) { p.pbits[i >> 5] |= 1u << (i & 31); };
+    for (uint32_t g = 0; g < n_xy; ++g) {
+      const int wt = p.xy_weight[g];
+      if (static_cast<int64_t>(g) == h.diag || (wt != 2 && wt != 4)) continue;
+      int q[4], k = 0;
+      for (int w = 0; w < W; ++w)
+        for (uint64_t v = h.xy[static_cast<size_t>(g) * W + w]; v && k < 4; v &= v - 1) q[k++] = w * 64 + std::countr_zero(v);
+      if (wt == 2) {
+        set(pid(q[0], q[1]));
+        continue;
+      }
+      for (int a = 0; a < 4; ++a)
+        for (int b = a + 1; b < 4; ++b) {
+          int o[2], m = 0;
+          for (int c = 0; c < 4; ++c)
+            if (c != a && c != b) o[m++] = q[c];
+          set(P + pid(q[a], q[b]) * P + pid(o[0], o[1]));
+        }
+    }
+  }
+
   // flip-mask table for the join path: weight-2/4 masks keyed EXACTLY by
   // their sorted orbital positions packed into 32 bits (0xFF pads weight 2),
   // so a lookup needs no mask compare; buckets of 4 x (key32 << 32 | group),
-  // load <= 1/4, chained to the next bucket when full
+  // chained to the next bucket when full
   {
-    uint64_t nb = 64;
-    while (nb < n_xy) nb <<= 1;
+    uint64_t nb = 64;  // about one entry per 4-slot bucket: 32 B per probe, chains ~1% of buckets
+    while (nb * 2 < n_xy) nb <<= 1;
     p.xy_tab.assign(nb * 4, ~uint64_t{0});
     p.xy_tab_mask = nb - 1;
     for (uint32_t g = 0; g < n_xy; ++g) {
@@ -446,7 +504,7 @@ DevicePlan plan_device(const HostIndex& h) {
       if (static_cast<int64_t>(g) == h.diag || (wt != 2 && wt != 4)) continue;
       const uint32_t key = xy_position_key(&h.xy[static_cast<size_t>(g) * W], W);
       const uint64_t entry = static_cast<uint64_t>(key) << 32 | g;
-      for (uint64_t b = fmix_host(key) & p.xy_tab_mask;; b = (b + 1) & p.xy_tab_mask) {
+      for (uint64_t b = xy_bucket_host(key, static_cast<uint32_t>(p.xy_tab_mask));; b = (b + 1) & p.xy_tab_mask) {
         int k = 0;
         while (k < 4 && p.xy_tab[b * 4 + k] != ~uint64_t{0}) ++k;
         if (k < 4) {

@@ -86,6 +86,10 @@ struct DevicePlan {
   std::vector<uint64_t> famrec;     // [n_fam][fam_words(W)]
   // join-path drain records (qvmc_join.cuh): [n_xy][kGrecWordsHost]
   std::vector<uint64_t> grec;
+  // join-path existence bitmaps over orbital pairs (n <= 128): [P bits singles][P*P bits doubles]
+  std::vector<uint32_t> pbits;
+  uint32_t pbits_P = 0;
+  std::vector<double> famvi;        // compact kind-B groups: v_f[k] interleaved [N][nf padded to 1/2/4]
   // flip-mask table (join path): buckets of 4 x (position key32 << 32 | group)
   std::vector<uint64_t> xy_tab;
   uint64_t xy_tab_mask = 0;
@@ -97,6 +101,16 @@ inline uint64_t fmix_host(uint64_t h) {
   h *= 0xbf58476d1ce4e5b9ull;
   h ^= h >> 32;
   return h;
+}
+
+// first flip-table bucket of a position key, shared with the device (qvmc_join.cuh xy_bucket)
+inline uint32_t xy_bucket_host(uint32_t key, uint32_t mask) {
+  key ^= key >> 16;
+  key *= 0x85ebca6bu;
+  key ^= key >> 13;
+  key *= 0xc2b2ae35u;
+  key ^= key >> 16;
+  return key & mask;
 }
 
 DevicePlan plan_device(const HostIndex& h);

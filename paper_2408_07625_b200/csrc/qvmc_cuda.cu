@@ -124,9 +124,10 @@ struct qvmc_ham_s {
   // Hamiltonian
   DBuf xy, xy_hash, goff, coeff, yz, yw, xyw, gen_hash, gen_g, lst_off, lst_hash, lst_g, res_g, diag_b, diag_K,
       diag_other, hash_bytes, xy_tab, codes, comp_of, fam_off, fam_B, fam_q, fam_u, fam_V, fam_v, ginfo, trec,
-      famrec, grec, binom;
+      famrec, grec, famvi, pbits, binom;
   std::vector<uint64_t> binom_host;
   uint64_t xy_tab_mask = 0;
+  uint32_t pbits_P = 0;
   HamView view{};
   // join path (per call): deletion-index workspace
   DBuf l_key, l_key2, l_idx, l_perm, l_keys, l_rec, l_flags, l_list, l_nsel, cs;
@@ -375,7 +376,7 @@ void build_join_index_k(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const Ro
   h->j_hi.ensure(E * 4 + 16);
   h->j_mem.ensure(E * 8 + 16);
   h->j_rng.ensure(E * 8 + 16);
-  const int grid = static_cast<int>(std::min<int64_t>((n + kThreads - 1) / kThreads, grid_for(h, 8)));
+  const int grid = static_cast<int>(std::min<int64_t>((n + kWarps - 1) / kWarps, grid_for(h, 8)));
   k_join_keys<W, K><<<std::max(grid, 1), kThreads, 0, h->stream>>>(keys, n, h->n, P.side, P.s, h->binom.as<uint64_t>(),
                                                                    h->j_key.as<K>(), h->j_val.as<uint64_t>());
   ck_launch("join keys");
@@ -423,6 +424,9 @@ JoinView join_view(qvmc_ham_s* h, const RowPlan& P) {
   J.xy_mask = h->xy_tab_mask;
   J.rec = h->l_rec.as<uint64_t>();
   J.grec = h->grec.as<uint64_t>();
+  J.famvi = h->famvi.as<double>();
+  J.pbits = h->pbits_P ? h->pbits.as<uint32_t>() : nullptr;
+  J.P = h->pbits_P;
   return J;
 }
 
@@ -695,6 +699,9 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     upload(h->trec, p.trec);
     upload(h->famrec, p.famrec);
     upload(h->grec, p.grec);
+    upload(h->famvi, p.famvi);
+    upload(h->pbits, p.pbits);
+    h->pbits_P = p.pbits_P;
     h->binom_host = binomial_table();
     upload(h->binom, h->binom_host);
     h->xy_tab_mask = p.xy_tab_mask;

@@ -27,11 +27,11 @@
 namespace qvmc_b200 {
 
 #ifndef QVMC_JOIN_MINB
-#define QVMC_JOIN_MINB 3  // 80 registers: 24 resident warps per SM (measured best with the inlined drain)
+#define QVMC_JOIN_MINB 4  // 64 registers: 32 resident warps per SM (measured best, r01k)
 #endif
 
 #ifndef QVMC_JOIN_UNROLL
-#define QVMC_JOIN_UNROLL 4  // bucket members in flight per lane
+#define QVMC_JOIN_UNROLL 2  // bucket members in flight per lane
 #endif
 
 #ifndef QVMC_JOIN_DRAIN_ATTR
@@ -47,21 +47,40 @@ constexpr uint32_t kNoKey = 0xFFFFFFFFu;
 //   kind A (small group, one shared Z string): w0 = 0 | k << 2 | per term t
 //     (ypat_t | (y_weight_t & 3) << 4) << (8 + 6t), ypat_t = Y positions among
 //     the sorted flip positions; w2.. = z words, then the k coefficients
-//   kind B (family-compressed large group): w0 = 1 | n_fam << 8 | q bits << 16,
-//     w1 = first family
+//   kind B (family-compressed single excitation, every family base B_f = shared
+//     Z string | Y positions among the two flip positions): w0 = 1 | n_fam << 8
+//     | q bits << 16 | ypat_f << (24 + 4f), w1 = offset of the group's
+//     interleaved v block in famvi ([N][n_fam padded to 1/2/4]), w2.. = z
+//     words, then (u_f, V_f) per family
 //   kind C (generic): w0 = 2, w1 = t0 | n_terms << 32
+//   kind D (family-compressed, general): w0 = 3 | n_fam << 8 | q bits << 16,
+//     w1 = first family (famrec / fam_v)
 constexpr int kGrecWords = 8;
-enum : uint32_t { kGrecA = 0, kGrecB = 1, kGrecC = 2 };
+enum : uint32_t { kGrecA = 0, kGrecB = 1, kGrecC = 2, kGrecD = 3 };
 
 struct JoinView {
   uint32_t C;              // buckets per sample = s(s-1)/2
   const uint2* rng;        // [N*C] (lo, hi) of the bucket of (sample y, pair t) in mem
-  const uint64_t* mem;     // bucket members grouped by bucket: y | ta << 32 | tb << 40
+  const uint64_t* mem;     // bucket members grouped by bucket: y | ta << 32 | tb << 40 | pidx(ta, tb) << 48
   const uint64_t* xy_tab;  // flip-mask hash table, buckets of 4 x (position key32 << 32 | group)
   uint64_t xy_mask;
   const uint64_t* rec;     // [N][4] per sample (log psi, cos phase, sin phase, 0) bits
   const uint64_t* grec;    // [n_xy][8] drain records
+  const double* famvi;     // kind-B interleaved family coefficients
+  // existence bitmaps of the weight-2/4 flip masks over orbital pairs (n <= 128,
+  // else null): bit pidx(c, a) of the first P bits = single {c, a}; bit
+  // P + pidx(A) * P + pidx(B) = double A u B (every split into two pairs)
+  const uint32_t* pbits;
+  uint32_t P;              // n(n-1)/2
 };
+
+__device__ __forceinline__ uint32_t pidx(int a, int b) {  // a < b
+  return static_cast<uint32_t>(b * (b - 1) / 2 + a);
+}
+
+__device__ __forceinline__ bool pbit(const uint32_t* __restrict__ bits, uint32_t i) {
+  return (__ldg(bits + (i >> 5)) >> (i & 31)) & 1u;
+}
 
 // Rows of one call. Rows are processed in the order of the (locality-sorted)
 // key arrays; `perm` maps a key-array position back to the caller's row.
@@ -145,42 +164,66 @@ __global__ void k_flag_rows(const uint32_t* __restrict__ perm, int64_t n, int64_
 // y | pos_a << 32 | pos_b << 40 | t << 48. With the remaining orbitals
 // r_0 < r_1 < ..., rank = sum_i C(r_i, i + 1); an orbital at index j of S(y)
 // has index j (j < a), j - 1 (a < j < b) or j - 2 (j > b) after the removal,
-// so the rank is three prefix-sum differences.
+// so the rank is three prefix-sum differences. One warp per sample: lane j
+// holds orbital j and the three prefix sums (warp scans); lanes write
+// consecutive pairs (coalesced).
 template <int W, typename K>
 __global__ void __launch_bounds__(kThreads)
     k_join_keys(const uint64_t* __restrict__ keys, int64_t n, int n_qubits, int side, int s,
                 const uint64_t* __restrict__ binom, K* __restrict__ bkey, uint64_t* __restrict__ bval) {
   const uint32_t C = static_cast<uint32_t>(s * (s - 1) / 2);
-  for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < n; y += (int64_t)gridDim.x * blockDim.x) {
-    uint8_t pos[kJoinMaxMinority];
-    uint64_t P0[kJoinMaxMinority + 1], P1[kJoinMaxMinority + 1], P2[kJoinMaxMinority + 1];
-    int k = 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t y = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; y < n; y += n_warps) {
+    int pos = 0, cnt = 0;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       uint64_t v = side ? keys[y * W + w] : ~keys[y * W + w];
       const int hi_bit = n_qubits - 64 * w;
       if (hi_bit < 64) v &= (hi_bit <= 0) ? 0ull : ((1ull << hi_bit) - 1);
-      while (v && k < kJoinMaxMinority) {
-        pos[k++] = static_cast<uint8_t>(64 * w + __ffsll(static_cast<long long>(v)) - 1);
-        v &= v - 1;
+      const int pc = __popcll(v);
+      if (lane >= cnt && lane < cnt + pc) {
+        for (int k = 0; k < lane - cnt; ++k) v &= v - 1;
+        pos = 64 * w + __ffsll(static_cast<long long>(v)) - 1;
+      }
+      cnt += pc;
+    }
+    const uint64_t* row = binom + static_cast<int64_t>(pos) * kBinomK;
+    const bool in = lane < s;
+    const uint64_t c0 = in ? __ldg(row + lane + 1) : 0ull;
+    const uint64_t c1 = (in && lane >= 1) ? __ldg(row + lane) : 0ull;
+    const uint64_t c2 = (in && lane >= 2) ? __ldg(row + lane - 1) : 0ull;
+    uint64_t i0 = c0, i1 = c1, i2 = c2;  // inclusive scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t t0 = __shfl_up_sync(0xffffffffu, i0, o), t1 = __shfl_up_sync(0xffffffffu, i1, o),
+                     t2 = __shfl_up_sync(0xffffffffu, i2, o);
+      if (lane >= o) {
+        i0 += t0;
+        i1 += t1;
+        i2 += t2;
       }
     }
-    P0[0] = P1[0] = P2[0] = 0;
-    for (int j = 0; j < s; ++j) {
-      const uint64_t* row = binom + static_cast<int64_t>(pos[j]) * kBinomK;
-      P0[j + 1] = P0[j] + __ldg(row + j + 1);
-      P1[j + 1] = P1[j] + (j >= 1 ? __ldg(row + j) : 0ull);
-      P2[j + 1] = P2[j] + (j >= 2 ? __ldg(row + j - 1) : 0ull);
-    }
-    const uint64_t base = static_cast<uint64_t>(y) * C;
-    uint32_t t = 0;
-    for (int b = 1; b < s; ++b)
-      for (int a = 0; a < b; ++a, ++t) {
-        const uint64_t rank = P0[a] + (P1[b] - P1[a + 1]) + (P2[s] - P2[b + 1]);
-        bkey[base + t] = static_cast<K>(rank);
-        bval[base + t] = static_cast<uint64_t>(y) | static_cast<uint64_t>(pos[a]) << 32 |
-                         static_cast<uint64_t>(pos[b]) << 40 | static_cast<uint64_t>(t) << 48;
+    const uint64_t total2 = __shfl_sync(0xffffffffu, i2, 31);
+    const uint64_t e0 = i0 - c0, e1 = i1 - c1;  // exclusive: P0[j], P1[j]
+    for (uint32_t base = 0; base < C; base += 32) {
+      const uint32_t t = base + lane;
+      const bool valid = t < C;
+      const int b = valid ? static_cast<int>(pair_b(static_cast<int>(t))) : 1;
+      const int a = valid ? static_cast<int>(t) - b * (b - 1) / 2 : 0;
+      const uint64_t P0a = __shfl_sync(0xffffffffu, e0, a);
+      const uint64_t P1a1 = __shfl_sync(0xffffffffu, i1, a);
+      const uint64_t P1b = __shfl_sync(0xffffffffu, e1, b);
+      const uint64_t P2b1 = __shfl_sync(0xffffffffu, i2, b);
+      const int pa = __shfl_sync(0xffffffffu, pos, a), pb = __shfl_sync(0xffffffffu, pos, b);
+      if (valid) {
+        const uint64_t rank = P0a + (P1b - P1a1) + (total2 - P2b1);
+        const uint64_t at = static_cast<uint64_t>(y) * C + t;
+        bkey[at] = static_cast<K>(rank);
+        bval[at] = static_cast<uint64_t>(y) | static_cast<uint64_t>(pa) << 32 | static_cast<uint64_t>(pb) << 40 |
+                   static_cast<uint64_t>(t) << 48;
       }
+    }
   }
 }
 
@@ -209,22 +252,42 @@ __global__ void k_join_fill(const uint64_t* __restrict__ val, const uint32_t* __
     const uint32_t r = rid[p] - 1;
     const uint64_t y = v & 0xFFFFFFFFull, t = v >> 48;
     rng[y * C + t] = make_uint2(lo[r], hi[r]);
-    mem[p] = v & 0x0000FFFFFFFFFFFFull;
+    const uint32_t a = static_cast<uint32_t>(v >> 32) & 0xFF, b = static_cast<uint32_t>(v >> 40) & 0xFF;
+    mem[p] = (v & 0x0000FFFFFFFFFFFFull) | static_cast<uint64_t>(b * (b - 1) / 2 + a) << 48;
   }
 }
 
-// group of a flip mask by its exact position key (host_index.cpp xy_position_key), or -1
-__device__ __forceinline__ int64_t xy_find(uint32_t key, const uint64_t* __restrict__ tab, uint64_t mask) {
-  uint64_t b = fmix(key) & mask;
-  for (;;) {
-    const U64x4 q = ldg256(tab + b * 4);
-    const uint64_t e[4] = {q.a, q.b, q.c, q.d};
+// first bucket of a flip-mask position key (host_index.cpp xy_bucket_host): murmur3 fmix32
+__device__ __forceinline__ uint32_t xy_bucket(uint32_t key, uint32_t mask) {
+  key ^= key >> 16;
+  key *= 0x85ebca6bu;
+  key ^= key >> 13;
+  key *= 0xc2b2ae35u;
+  key ^= key >> 16;
+  return key & mask;
+}
+
+constexpr int64_t kChain = -2;
+
+// one loaded bucket: the group of `key`, -1 (absent: the bucket has a free
+// slot before any match) or kChain (full bucket without a match)
+__device__ __forceinline__ int64_t xy_resolve(uint32_t key, const U64x4& q) {
+  const uint64_t e[4] = {q.a, q.b, q.c, q.d};
+  int64_t g = kChain;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (e[k] == kEmpty) return -1;
-      if (static_cast<uint32_t>(e[k] >> 32) == key) return static_cast<uint32_t>(e[k]);
-    }
-    b = (b + 1) & mask;  // full bucket: the chain continues
+  for (int k = 3; k >= 0; --k) {  // the first match or free slot in slot order wins
+    if (e[k] == kEmpty) g = -1;
+    if (static_cast<uint32_t>(e[k] >> 32) == key) g = static_cast<uint32_t>(e[k]);
+  }
+  return g;
+}
+
+// rare path: follow the chain after the full bucket b
+__device__ __noinline__ int64_t xy_chain(uint32_t key, uint32_t b, const uint64_t* __restrict__ tab, uint32_t mask) {
+  for (;;) {
+    b = (b + 1) & mask;
+    const int64_t g = xy_resolve(key, ldg256(tab + static_cast<uint64_t>(b) * 4));
+    if (g != kChain) return g;
   }
 }
 
@@ -292,6 +355,67 @@ __device__ __forceinline__ void kind_a_element(const uint64_t* r, const uint64_t
   }
 }
 
+// H_{x x'} of a kind-B group (a single excitation x -> x' = x - c + a over the
+// minority set): per family f,
+//   i^q_f (-1)^{|x' & z| + |b & ypat_f|} (u_f + sum_k v_f[k] (-1)^{x'_k}),
+//   sum_k v_f[k] (-1)^{x'_k} = +-(V_f - 2 sum_{k in S(x')} v_f[k]),
+// S(x') = S(x) - c + a: s + 2 interleaved loads (all families of an orbital
+// in one vector load) instead of the 2 + 2(N-2) terms.
+template <int W>
+__device__ __forceinline__ void kind_b_element(const double* __restrict__ famvi, const uint64_t* r, const uint64_t* x,
+                                               const uint64_t* xp, uint32_t key, const uint16_t* pos, int s,
+                                               int side, double& re, double& im) {
+  re = 0.0;
+  im = 0.0;
+  const uint64_t meta = r[0];
+  const int nf = static_cast<int>(meta >> 8) & 0xFF;
+  const double* v = famvi + r[1];
+  const int p0 = key & 0xFF, p1 = (key >> 8) & 0xFF;
+  const bool p0_in_s = bit_at<W>(x, p0) == (side != 0);
+  const int c = p0_in_s ? p0 : p1, a = p0_in_s ? p1 : p0;
+  double sv[4] = {0.0, 0.0, 0.0, 0.0};
+  if (nf == 2) {
+    const double2* v2 = reinterpret_cast<const double2*>(v);
+#pragma unroll 4
+    for (int i = 0; i < s; ++i) {
+      const double2 t = __ldg(v2 + pos[i]);
+      sv[0] += t.x;
+      sv[1] += t.y;
+    }
+    const double2 tc = __ldg(v2 + c), ta = __ldg(v2 + a);
+    sv[0] += ta.x - tc.x;
+    sv[1] += ta.y - tc.y;
+  } else {
+    const int nfp = nf == 1 ? 1 : 4;
+    for (int i = 0; i < s; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < nf) sv[j] += __ldg(v + pos[i] * nfp + j);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j < nf) sv[j] += __ldg(v + a * nfp + j) - __ldg(v + c * nfp + j);
+  }
+  int pz = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) pz += __popcll(xp[w] & r[2 + w]);
+  const uint32_t bp = (bit_at<W>(xp, p0) ? 1u : 0u) | (bit_at<W>(xp, p1) ? 2u : 0u);
+#pragma unroll
+  for (int j = 0; 2 + W + 2 * j + 1 < kGrecWords; ++j) {
+    if (j < nf) {
+      const double u = __longlong_as_double(static_cast<long long>(r[2 + W + 2 * j]));
+      const double V = __longlong_as_double(static_cast<long long>(r[3 + W + 2 * j]));
+      double val = u + (side ? V - 2.0 * sv[j] : 2.0 * sv[j] - V);
+      const uint32_t yp = static_cast<uint32_t>(meta >> (24 + 4 * j)) & 15u;
+      if ((pz + __popc(bp & yp)) & 1) val = -val;
+      const uint32_t q = static_cast<uint32_t>(meta >> (16 + 2 * j)) & 3u;
+      if (q == 0) re += val;
+      else if (q == 1) im += val;
+      else if (q == 2) re -= val;
+      else im -= val;
+    }
+  }
+}
+
 // Per-warp state of the join kernel.
 constexpr int kJQueue = 256;
 constexpr int kJDrainAt = kJQueue - 32 * QVMC_JOIN_UNROLL;  // one scan step adds at most 32*U hits
@@ -304,6 +428,7 @@ struct JoinSmem {
   uint32_t r_len[kJoinMaxRanges];
   uint8_t ta[kJoinMaxRanges];     // the row's pair T_x of each bucket
   uint8_t tb[kJoinMaxRanges];
+  uint32_t dbase[kJoinMaxRanges]; // P + pidx(T_x) * P: the doubles-bitmap row of each bucket
   uint64_t x[4];                  // the current row: key, log psi, (cos, sin) of its phase; kept here
   double la, cs_c, cs_s;          // (not in registers) across the candidate walk
   uint16_t pos[32];               // minority orbitals of the current row
@@ -321,90 +446,126 @@ __device__ __forceinline__ Key<W> row_key(const JoinSmem* sm) {
   return k;
 }
 
+#ifndef QVMC_JOIN_DRAIN_HITS
+#define QVMC_JOIN_DRAIN_HITS 1  // queued hits per lane whose records are loaded together (2+ spills)
+#endif
+
+// one queued hit: its sample record and drain record (loaded together)
+struct JoinHit {
+  uint32_t key;
+  bool valid;
+  U64x4 sr;  // log psi, cos, sin of the partner
+  uint64_t r[kGrecWords];
+};
+
+__device__ __forceinline__ void load_hit(const JoinView& J, const JoinSmem* sm, unsigned k, unsigned n, JoinHit& h) {
+  h.valid = k < n;
+  h.key = kNoKey;
+  h.sr = U64x4{0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < kGrecWords; ++i) h.r[i] = 0;
+  if (h.valid) {
+    const uint32_t y = sm->qy[k], g = sm->qg[k];
+    h.key = sm->qk[k];
+    h.sr = ldg256(J.rec + static_cast<int64_t>(y) * 4);
+    const U64x4 g0 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords);
+    const U64x4 g1 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords + 4);
+    h.r[0] = g0.a; h.r[1] = g0.b; h.r[2] = g0.c; h.r[3] = g0.d;
+    h.r[4] = g1.a; h.r[5] = g1.b; h.r[6] = g1.c; h.r[7] = g1.d;
+  }
+}
+
+// H_{x x'} psi(x')/psi(x) of one loaded hit, added to acc (warp-collective:
+// large generic groups are split over the lanes)
+template <int W>
+__device__ __forceinline__ void eval_hit(const HamView& H, const JoinView& J, const JoinSmem* sm, const JoinHit& h,
+                                         const Key<W>& xrow, double la_i, double2 cs_i, int lane, int s, int side,
+                                         double2& acc) {
+  uint64_t xp[W];
+  {
+    uint64_t m[W];
+    key_mask<W>(h.key, m);
+#pragma unroll
+    for (int w = 0; w < W; ++w) xp[w] = xrow.w[w] ^ m[w];
+  }
+  const uint32_t kind = static_cast<uint32_t>(h.r[0]) & 3u;
+  const uint32_t nt = static_cast<uint32_t>(h.r[1] >> 32);
+  const bool large = h.valid && kind == kGrecC && nt > kSmallGroup;
+  double hr = 0.0, hi = 0.0;
+  if (h.valid && !large) {
+    if (kind == kGrecA) {
+      kind_a_element<W>(h.r, xp, h.key, hr, hi);
+    } else if (kind == kGrecB) {
+      kind_b_element<W>(J.famvi, h.r, xrow.w, xp, h.key, sm->pos, s, side, hr, hi);
+    } else if (kind == kGrecD) {
+      const uint4 gi = make_uint4(0, 0, static_cast<uint32_t>(h.r[1]), static_cast<uint32_t>(h.r[0] >> 8));
+      comp_element<W>(H, xrow.w, xp, gi, sm->pos, s, side, hr, hi);
+    } else {
+      const uint4 gi = make_uint4(static_cast<uint32_t>(h.r[1]), nt, 0xFFFFFFFFu, 0);
+      small_element<W>(H, xp, gi, hr, hi);
+    }
+  }
+  // large generic groups: the warp splits the terms; element parked in lane src
+  unsigned mask = __ballot_sync(0xffffffffu, large);
+  while (mask) {
+    const int src = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const uint32_t st0 = __shfl_sync(0xffffffffu, static_cast<uint32_t>(h.r[1]), src);
+    const uint32_t st1 = st0 + __shfl_sync(0xffffffffu, nt, src);
+    uint64_t sx[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) sx[w] = __shfl_sync(0xffffffffu, xp[w], src);
+    double re = 0.0, im = 0.0;
+    for (uint32_t t = st0 + lane; t < st1; t += 32) {
+      int pc = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) pc += __popcll(sx[w] & __ldg(H.yz + (int64_t)t * W + w));
+      const int qt = (__ldg(H.yw + t) + 2 * pc) & 3;
+      const double c = __ldg(H.coeff + t);
+      if (qt == 0) re += c;
+      else if (qt == 2) re -= c;
+      else if (qt == 1) im += c;
+      else im -= c;
+    }
+    re = warp_sum(re);
+    im = warp_sum(im);
+    if (lane == src) {
+      hr = re;
+      hi = im;
+    }
+  }
+  if (h.valid) {
+    const double2 cs_j = make_double2(__longlong_as_double(static_cast<long long>(h.sr.b)),
+                                      __longlong_as_double(static_cast<long long>(h.sr.c)));
+    add_ratio(__longlong_as_double(static_cast<long long>(h.sr.a)), cs_j, la_i, cs_i, hr, hi, acc);
+  }
+}
+
 // Drain the warp's hit queue: this lane's share of sum H_{xx'} psi(x')/psi(x).
+// QVMC_JOIN_DRAIN_HITS hits per lane per round have all their records in
+// flight before any is evaluated (the drain is load-latency bound).
 template <int W>
 __device__ QVMC_JOIN_DRAIN_ATTR double2 join_drain(const HamView& H, const JoinView& J, JoinSmem* sm, int lane, int s,
                                                    int side) {
+  constexpr int DH = QVMC_JOIN_DRAIN_HITS;
   double2 acc = make_double2(0.0, 0.0);
   __syncwarp();
+#ifdef QVMC_EXP_NO_DRAIN
+  if (lane == 0) sm->qn = 0;
+  __syncwarp();
+  return acc;
+#endif
   const Key<W> xrow = row_key<W>(sm);
   const double la_i = *reinterpret_cast<const volatile double*>(&sm->la);
   const double2 cs_i = make_double2(*reinterpret_cast<const volatile double*>(&sm->cs_c),
                                     *reinterpret_cast<const volatile double*>(&sm->cs_s));
   const unsigned n = sm->qn;
-  for (unsigned k0 = 0; k0 < n; k0 += 32) {
-    const unsigned k = k0 + lane;
-    const bool valid = k < n;
-    uint32_t key = kNoKey;
-    uint64_t r[kGrecWords];
-    U64x4 sr = {0, 0, 0, 0};
+  for (unsigned k0 = 0; k0 < n; k0 += 32 * DH) {
+    JoinHit h[DH];
 #pragma unroll
-    for (int i = 0; i < kGrecWords; ++i) r[i] = 0;
-    if (valid) {  // independent loads first: sample record + both halves of the group record
-      const uint32_t y = sm->qy[k], g = sm->qg[k];
-      key = sm->qk[k];
-      sr = ldg256(J.rec + static_cast<int64_t>(y) * 4);
-      const U64x4 g0 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords);
-      const U64x4 g1 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords + 4);
-      r[0] = g0.a; r[1] = g0.b; r[2] = g0.c; r[3] = g0.d;
-      r[4] = g1.a; r[5] = g1.b; r[6] = g1.c; r[7] = g1.d;
-    }
-    uint64_t xp[W];
-    {
-      uint64_t m[W];
-      key_mask<W>(key, m);
+    for (int d = 0; d < DH; ++d) load_hit(J, sm, k0 + 32 * d + lane, n, h[d]);
 #pragma unroll
-      for (int w = 0; w < W; ++w) xp[w] = xrow.w[w] ^ m[w];
-    }
-    const uint32_t kind = static_cast<uint32_t>(r[0]) & 3u;
-    const uint32_t nt = static_cast<uint32_t>(r[1] >> 32);
-    const bool large = valid && kind == kGrecC && nt > kSmallGroup;
-    double hr = 0.0, hi = 0.0;
-    if (valid && !large) {
-      if (kind == kGrecA) {
-        kind_a_element<W>(r, xp, key, hr, hi);
-      } else if (kind == kGrecB) {
-        const uint4 gi = make_uint4(0, 0, static_cast<uint32_t>(r[1]), static_cast<uint32_t>(r[0] >> 8));
-        comp_element<W>(H, xrow.w, xp, gi, sm->pos, s, side, hr, hi);
-      } else {
-        const uint4 gi = make_uint4(static_cast<uint32_t>(r[1]), nt, 0xFFFFFFFFu, 0);
-        small_element<W>(H, xp, gi, hr, hi);
-      }
-    }
-    // large generic groups: the warp splits the terms; element parked in lane src
-    unsigned mask = __ballot_sync(0xffffffffu, large);
-    while (mask) {
-      const int src = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const uint32_t st0 = __shfl_sync(0xffffffffu, static_cast<uint32_t>(r[1]), src);
-      const uint32_t st1 = st0 + __shfl_sync(0xffffffffu, nt, src);
-      uint64_t sx[W];
-#pragma unroll
-      for (int w = 0; w < W; ++w) sx[w] = __shfl_sync(0xffffffffu, xp[w], src);
-      double re = 0.0, im = 0.0;
-      for (uint32_t t = st0 + lane; t < st1; t += 32) {
-        int pc = 0;
-#pragma unroll
-        for (int w = 0; w < W; ++w) pc += __popcll(sx[w] & __ldg(H.yz + (int64_t)t * W + w));
-        const int qt = (__ldg(H.yw + t) + 2 * pc) & 3;
-        const double c = __ldg(H.coeff + t);
-        if (qt == 0) re += c;
-        else if (qt == 2) re -= c;
-        else if (qt == 1) im += c;
-        else im -= c;
-      }
-      re = warp_sum(re);
-      im = warp_sum(im);
-      if (lane == src) {
-        hr = re;
-        hi = im;
-      }
-    }
-    if (valid) {
-      const double2 cs_j = make_double2(__longlong_as_double(static_cast<long long>(sr.b)),
-                                        __longlong_as_double(static_cast<long long>(sr.c)));
-      add_ratio(__longlong_as_double(static_cast<long long>(sr.a)), cs_j, la_i, cs_i, hr, hi, acc);
-    }
+    for (int d = 0; d < DH; ++d) eval_hit<W>(H, J, sm, h[d], xrow, la_i, cs_i, lane, s, side, acc);
   }
   __syncwarp();
   if (lane == 0) sm->qn = 0;
@@ -489,8 +650,10 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
     // bucket t of this row: pair (a, b) of S(x), range from the index
     for (int t = lane; t < n_ranges; t += 32) {
       const uint32_t b = pair_b(t);
-      sm->ta[t] = static_cast<uint8_t>(sm->pos[t - b * (b - 1) / 2]);
-      sm->tb[t] = static_cast<uint8_t>(sm->pos[b]);
+      const int pa = sm->pos[t - b * (b - 1) / 2], pb = sm->pos[b];
+      sm->ta[t] = static_cast<uint8_t>(pa);
+      sm->tb[t] = static_cast<uint8_t>(pb);
+      sm->dbase[t] = J.P + pidx(pa, pb) * J.P;
       const uint2 rg = __ldg(J.rng + static_cast<uint64_t>(row) * J.C + t);
       sm->r_lo[t] = rg.x;
       sm->r_len[t] = rg.y - rg.x;
@@ -507,7 +670,9 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
       off -= len;
       if (++rg < n_ranges) len = sm->r_len[rg];
     }
-    while (__any_sync(0xffffffffu, rg < n_ranges)) {
+    for (;;) {  // one drain call site: inside the walk when the queue fills, and once at its end
+      const bool walking = __any_sync(0xffffffffu, rg < n_ranges);
+      if (walking) {
       constexpr int U = QVMC_JOIN_UNROLL;
       uint64_t v[U];
       int tr[U];
@@ -534,6 +699,8 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
         const int ta = sm->ta[tr[u]], tb = sm->tb[tr[u]];
         const bool ea = ya == ta || ya == tb, eb = yb == ta || yb == tb;
         if (!ea && !eb) {  // disjoint pairs: double excitation; merge two sorted pairs
+          ++cand;
+          if (J.pbits && !pbit(J.pbits, sm->dbase[tr[u]] + static_cast<uint32_t>(v[u] >> 48))) continue;
           int p0 = ta, p1 = tb, p2 = ya, p3 = yb;
           sort2(p0, p2);
           sort2(p1, p3);
@@ -546,16 +713,23 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
           if (o == (cc == pos0 ? pos1 : pos0)) {
             int p0 = cc, p1 = a;
             sort2(p0, p1);
+            ++cand;
+            if (J.pbits && !pbit(J.pbits, pidx(p0, p1))) continue;
             key[u] = static_cast<uint32_t>(p0) | static_cast<uint32_t>(p1) << 8 | 0xFFFF0000u;
           }
         }
       }
+      // flip-mask lookups, one at a time (hoisting all U bucket loads first
+      // measured slower: the extra live registers spill)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         int64_t g = -1;
         if (key[u] != kNoKey) {
-          ++cand;
-          g = xy_find(key[u], J.xy_tab, J.xy_mask);
+#ifndef QVMC_EXP_NO_LOOKUP
+          const uint32_t bk = xy_bucket(key[u], static_cast<uint32_t>(J.xy_mask));
+          g = xy_resolve(key[u], ldg256(J.xy_tab + static_cast<uint64_t>(bk) * 4));
+          if (g == kChain) g = xy_chain(key[u], bk, J.xy_tab, static_cast<uint32_t>(J.xy_mask));
+#endif
         }
         // warp-aggregated append of the hits
         const bool hit = g >= 0;
@@ -582,14 +756,16 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
           hits += hit ? 1u : 0u;
         }
       }
+      }
       if (MODE == kModeEloc) {
         __syncwarp();
-        if (sm->qn >= kJDrainAt) {
+        if (sm->qn >= (walking ? static_cast<unsigned>(kJDrainAt) : 1u)) {
           const double2 d = join_drain<W>(H, J, sm, lane, s, side);
           acc.x += d.x;
           acc.y += d.y;
         }
       }
+      if (!walking) break;
     }
 
     const Key<W> xrow = row_key<W>(sm);
@@ -676,13 +852,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
       }
     }
 
-    if (MODE == kModeEloc) {
-      __syncwarp();
-      if (sm->qn > 0) {
-        const double2 d = join_drain<W>(H, J, sm, lane, s, side);
-        acc.x += d.x;
-        acc.y += d.y;
-      }
+    if (MODE == kModeEloc) {  // the walk drained the queue; residual hits were evaluated in place
       const double re = warp_sum(acc.x);
       const double im = warp_sum(acc.y);
       if (lane == 0) O.eloc[orow - R.out_base] = make_double2(re, im);
