@@ -133,6 +133,10 @@ struct qvmc_ham_s {
   DBuf l_key, l_key2, l_idx, l_perm, l_keys, l_rec, l_flags, l_list, l_nsel, cs;
   DBuf j_key, j_val, j_key2, j_val2, j_head, j_rid, j_lo, j_hi, j_mem, j_rng, j_tmp;
   bool use_join = true;
+  bool join_split = true;  // split evaluation (search -> hit chunks -> eval -> finalize)
+  // split-evaluation workspace
+  DBuf s_hy, s_hg, s_hk, s_chunk, s_row_last, s_base, s_part;
+  uint64_t hit_cap = 0, chunk_cap = 0;
   // workspace
   DBuf tab, ctl, keys, la, ph, lp, eloc, partials, moments, weights;
   DBuf counts, row_off, xp_a, g_a, xp_b, g_b, entries, cub_tmp, in_entries, out_h, out_class;
@@ -146,7 +150,7 @@ struct qvmc_ham_s {
 
 namespace {
 
-constexpr int kCtlInts = 16;  // int err, pad, popc_mm[2]; u64 row_next @4, stats[2] @6
+constexpr int kCtlInts = 16;  // int err, pad, popc_mm[2]; u64 row_next @4, stats[2] @6, hit/chunk cursors @10/@12
 
 Ctl ctl_view(qvmc_ham_s* h) {
   Ctl c;
@@ -445,6 +449,80 @@ void launch_rows_join(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, cons
   }
 }
 
+// Join rows with split evaluation: the search kernel streams each row's hits
+// into chunks, k_eval_chunks evaluates them (its own register budget), and
+// k_finalize_rows sums base + chunks per row in a fixed order. The hit
+// buffers grow (and the search reruns) when a call overflows them.
+template <int W>
+void run_join_split(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const RowPlan& P, double2* eloc) {
+  const int64_t rows = R.n_rows;
+  if (rows <= 0) return;
+  if (h->hit_cap == 0) {
+    h->hit_cap = std::max<uint64_t>(static_cast<uint64_t>(rows) * 320, 1u << 16);
+    h->chunk_cap = h->hit_cap / 64 + static_cast<uint64_t>(rows) + 1024;
+  }
+  h->s_row_last.ensure(rows * 4 + 16);
+  h->s_base.ensure(rows * 16 + 16);
+  int* ctl = static_cast<int*>(h->ctl.p);
+  unsigned long long cur[2] = {0, 0};
+  for (int attempt = 0;; ++attempt) {
+    h->hit_cap = std::min<uint64_t>(h->hit_cap, 0xFFFFFFFFull);
+    h->s_hy.ensure(h->hit_cap * 4 + 16);
+    h->s_hg.ensure(h->hit_cap * 4 + 16);
+    h->s_hk.ensure(h->hit_cap * 4 + 16);
+    h->s_chunk.ensure(h->chunk_cap * 16 + 16);
+    h->s_part.ensure(h->chunk_cap * 16 + 16);
+    ck(cudaMemsetAsync(ctl + 4, 0, 2 * sizeof(int), h->stream), "memset row counter");
+    ck(cudaMemsetAsync(ctl + 6, 0, 8 * sizeof(int), h->stream), "memset stats + cursors");
+    RowOut O{};
+    O.hy = h->s_hy.as<uint32_t>();
+    O.hg = h->s_hg.as<uint32_t>();
+    O.hk = h->s_hk.as<uint32_t>();
+    O.chunk = h->s_chunk.as<uint4>();
+    O.row_last = h->s_row_last.as<uint32_t>();
+    O.base = h->s_base.as<double2>();
+    O.hit_cursor = reinterpret_cast<unsigned long long*>(ctl + 10);
+    O.chunk_cursor = reinterpret_cast<unsigned long long*>(ctl + 12);
+    O.hit_cap = h->hit_cap;
+    O.chunk_cap = h->chunk_cap;
+    int per_sm = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_join<W, kModeHits>, kThreads, 0), "occupancy");
+    const int64_t blocks_needed = (rows + kWarps - 1) / kWarps;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_needed, grid_for(h, per_sm))));
+    TableView T{h->tab.as<uint64_t>(), h->tab_buckets - 1};
+    k_rows_join<W, kModeHits><<<grid, kThreads, 0, h->stream>>>(h->view, T, join_view(h, P), keys, R, P.side, P.s,
+                                                                ctl_view(h), O);
+    ck_launch("row kernel (join search)");
+    ck(cudaMemcpyAsync(cur, ctl + 10, sizeof(cur), cudaMemcpyDeviceToHost, h->stream), "D2H cursors");
+    ck(cudaStreamSynchronize(h->stream), "sync");
+    if (cur[0] <= h->hit_cap && cur[1] <= h->chunk_cap) break;
+    if (attempt >= 3) fail(QVMC_ERR_RUNTIME, "join hit buffers keep overflowing");
+    // grow to the demand seen (cursors count every reservation) and rerun
+    h->hit_cap = std::max<uint64_t>(h->hit_cap, cur[0] + cur[0] / 4 + 1024);
+    h->chunk_cap = std::max<uint64_t>(h->chunk_cap, cur[1] + cur[1] / 4 + 1024);
+    int err = 0;
+    ck(cudaMemcpy(&err, ctl, sizeof(int), cudaMemcpyDeviceToHost), "read err");
+    err &= ~kErrHitOverflow;
+    ck(cudaMemcpy(ctl, &err, sizeof(int), cudaMemcpyHostToDevice), "reset overflow");
+  }
+  const uint64_t nc = cur[1];
+  if (nc > 0) {
+    int per_sm = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_chunks<W>, kThreads, 0), "occupancy");
+    const int grid = static_cast<int>(
+        std::max<uint64_t>(1, std::min<uint64_t>((nc + kWarps - 1) / kWarps, static_cast<uint64_t>(grid_for(h, per_sm)))));
+    k_eval_chunks<W><<<grid, kThreads, 0, h->stream>>>(
+        h->view, join_view(h, P), keys, h->s_chunk.as<uint4>(), reinterpret_cast<unsigned long long*>(ctl + 12),
+        h->s_hy.as<uint32_t>(), h->s_hg.as<uint32_t>(), h->s_hk.as<uint32_t>(), P.side, P.s, h->s_part.as<double2>());
+    ck_launch("eval chunks");
+  }
+  const int fgrid = static_cast<int>(std::min<int64_t>((rows + kThreads - 1) / kThreads, grid_for(h, 8)));
+  k_finalize_rows<<<std::max(fgrid, 1), kThreads, 0, h->stream>>>(h->s_row_last.as<uint32_t>(), h->s_chunk.as<uint4>(),
+                                                                   h->s_part.as<double2>(), h->s_base.as<double2>(),
+                                                                   rows, eloc);
+  ck_launch("finalize rows");
+}
+
 template <int W, int MODE>
 void run_rows(qvmc_ham_s* h, const uint64_t* keys, int64_t r0, int64_t r1, const RowPlan& P, const RowOut& O) {
   if (P.join)
@@ -707,6 +785,7 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     h->xy_tab_mask = p.xy_tab_mask;
     upload(h->codes, std::vector<uint64_t>(qubit_codes(), qubit_codes() + 256));
     if (const char* e = std::getenv("QVMC_JOIN")) h->use_join = std::atoi(e) != 0;
+    if (const char* e = std::getenv("QVMC_JOIN_SPLIT")) h->join_split = std::atoi(e) != 0;
     h->ctl.ensure(kCtlInts * sizeof(int) * 2);
     ck(cudaMemset(h->ctl.p, 0, kCtlInts * sizeof(int) * 2), "memset ctl");
 
@@ -1089,7 +1168,9 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       O.la = dla;
       O.ph = dph;
       O.cs = rcs;
-      if (P.join) {
+      if (P.join && h->join_split) {
+        DISPATCH_W(W, (run_join_split<WW>(h, rkeys, R, P, deloc)));
+      } else if (P.join) {
         DISPATCH_W(W, (launch_rows_join<WW, kModeEloc>(h, rkeys, R, P, O)));
       } else {
         DISPATCH_W(W, (launch_rows<WW, kModeEloc>(h, dkeys, row_begin, row_end, O)));

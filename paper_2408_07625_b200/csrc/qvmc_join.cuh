@@ -478,7 +478,7 @@ __device__ __forceinline__ void load_hit(const JoinView& J, const JoinSmem* sm, 
 // H_{x x'} psi(x')/psi(x) of one loaded hit, added to acc (warp-collective:
 // large generic groups are split over the lanes)
 template <int W>
-__device__ __forceinline__ void eval_hit(const HamView& H, const JoinView& J, const JoinSmem* sm, const JoinHit& h,
+__device__ __forceinline__ void eval_hit(const HamView& H, const JoinView& J, const uint16_t* pos, const JoinHit& h,
                                          const Key<W>& xrow, double la_i, double2 cs_i, int lane, int s, int side,
                                          double2& acc) {
   uint64_t xp[W];
@@ -496,10 +496,10 @@ __device__ __forceinline__ void eval_hit(const HamView& H, const JoinView& J, co
     if (kind == kGrecA) {
       kind_a_element<W>(h.r, xp, h.key, hr, hi);
     } else if (kind == kGrecB) {
-      kind_b_element<W>(J.famvi, h.r, xrow.w, xp, h.key, sm->pos, s, side, hr, hi);
+      kind_b_element<W>(J.famvi, h.r, xrow.w, xp, h.key, pos, s, side, hr, hi);
     } else if (kind == kGrecD) {
       const uint4 gi = make_uint4(0, 0, static_cast<uint32_t>(h.r[1]), static_cast<uint32_t>(h.r[0] >> 8));
-      comp_element<W>(H, xrow.w, xp, gi, sm->pos, s, side, hr, hi);
+      comp_element<W>(H, xrow.w, xp, gi, pos, s, side, hr, hi);
     } else {
       const uint4 gi = make_uint4(static_cast<uint32_t>(h.r[1]), nt, 0xFFFFFFFFu, 0);
       small_element<W>(H, xp, gi, hr, hi);
@@ -565,7 +565,7 @@ __device__ QVMC_JOIN_DRAIN_ATTR double2 join_drain(const HamView& H, const JoinV
 #pragma unroll
     for (int d = 0; d < DH; ++d) load_hit(J, sm, k0 + 32 * d + lane, n, h[d]);
 #pragma unroll
-    for (int d = 0; d < DH; ++d) eval_hit<W>(H, J, sm, h[d], xrow, la_i, cs_i, lane, s, side, acc);
+    for (int d = 0; d < DH; ++d) eval_hit<W>(H, J, sm->pos, h[d], xrow, la_i, cs_i, lane, s, side, acc);
   }
   __syncwarp();
   if (lane == 0) sm->qn = 0;
@@ -573,11 +573,16 @@ __device__ QVMC_JOIN_DRAIN_ATTR double2 join_drain(const HamView& H, const JoinV
   return acc;
 }
 
+#ifndef QVMC_SEARCH_MINB
+#define QVMC_SEARCH_MINB 5  // split search kernel (no drain): 48 registers, 40 warps per SM (measured best)
+#endif
+
 template <int W, int MODE>
-__global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
+__global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB : QVMC_JOIN_MINB)
     k_rows_join(const __grid_constant__ HamView H, const TableView T, const __grid_constant__ JoinView J,
                 const uint64_t* __restrict__ keys, const RowSet R, int side, int s, const __grid_constant__ Ctl C,
                 const __grid_constant__ RowOut O) {
+  constexpr bool kEval = MODE == kModeEloc || MODE == kModeHits;  // E_loc rows (fused or split)
   __shared__ JoinSmem s_w[kWarps];
   const int lane = threadIdx.x & 31;
   JoinSmem* sm = &s_w[threadIdx.x >> 5];
@@ -602,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
       for (int w = 0; w < W; ++w) xrow.w[w] = __ldg(keys + row * W + w);
       double la_i = 0.0;
       U64x4 sr = {0, 0, 0, 0};
-      if (MODE == kModeEloc) {
+      if (kEval) {
         sr = ldg256(J.rec + row * 4);
         la_i = __longlong_as_double(static_cast<long long>(sr.a));
       }
@@ -622,11 +627,16 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
       }
     }
     __syncwarp();
-    if (MODE == kModeEloc) {
+    if (kEval) {
       if (isinf(*reinterpret_cast<const volatile double*>(&sm->la))) {  // energy.cpp:32-33
         if (lane == 0) {
           atomicOr(C.err, kErrZeroAmp);
-          O.eloc[orow - R.out_base] = make_double2(CUDART_NAN, CUDART_NAN);
+          if (MODE == kModeEloc) {
+            O.eloc[orow - R.out_base] = make_double2(CUDART_NAN, CUDART_NAN);
+          } else {
+            O.base[orow - R.out_base] = make_double2(CUDART_NAN, CUDART_NAN);
+            O.row_last[orow - R.out_base] = ~0u;
+          }
         }
         continue;
       }
@@ -663,6 +673,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
     double2 acc = make_double2(0.0, 0.0);
     uint32_t hits = 0;
     uint64_t cand = 0;
+    uint32_t prev_chunk = ~0u;  // kModeHits: last flushed chunk of this row
     int rg = 0;
     uint32_t off = lane;
     uint32_t len = sm->r_len[0];
@@ -735,14 +746,14 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
         const bool hit = g >= 0;
         const unsigned hm = __ballot_sync(0xffffffffu, hit);
         if (hm) {
-          if (MODE == kModeEloc || MODE == kModeEmit) {
+          if (kEval || MODE == kModeEmit) {
             unsigned base = 0;
-            if (lane == 0) base = atomicAdd(MODE == kModeEloc ? &sm->qn : &sm->cursor, __popc(hm));
+            if (lane == 0) base = atomicAdd(kEval ? &sm->qn : &sm->cursor, __popc(hm));
             base = __shfl_sync(0xffffffffu, base, 0);
             if (hit) {
               const unsigned k = base + __popc(hm & ((1u << lane) - 1u));
               const uint32_t y = static_cast<uint32_t>(v[u]);
-              if (MODE == kModeEloc) {
+              if (kEval) {
                 sm->qy[k] = y;
                 sm->qg[k] = static_cast<uint32_t>(g);
                 sm->qk[k] = key[u];
@@ -757,12 +768,38 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
         }
       }
       }
-      if (MODE == kModeEloc) {
+      if (kEval) {
         __syncwarp();
-        if (sm->qn >= (walking ? static_cast<unsigned>(kJDrainAt) : 1u)) {
-          const double2 d = join_drain<W>(H, J, sm, lane, s, side);
-          acc.x += d.x;
-          acc.y += d.y;
+        const unsigned qn = sm->qn;
+        if (qn >= (walking ? static_cast<unsigned>(kJDrainAt) : 1u)) {
+          if (MODE == kModeEloc) {
+            const double2 d = join_drain<W>(H, J, sm, lane, s, side);
+            acc.x += d.x;
+            acc.y += d.y;
+          } else {  // split evaluation: the queue becomes one chunk of this row
+            unsigned long long off = 0, cid = 0;
+            if (lane == 0) {
+              off = atomicAdd(O.hit_cursor, static_cast<unsigned long long>(qn));
+              cid = atomicAdd(O.chunk_cursor, 1ull);
+            }
+            off = __shfl_sync(0xffffffffu, off, 0);
+            cid = __shfl_sync(0xffffffffu, cid, 0);
+            if (off + qn <= O.hit_cap && cid < O.chunk_cap) {
+              for (unsigned k = lane; k < qn; k += 32) {
+                O.hy[off + k] = sm->qy[k];
+                O.hg[off + k] = sm->qg[k];
+                O.hk[off + k] = sm->qk[k];
+              }
+              if (lane == 0)
+                O.chunk[cid] = make_uint4(static_cast<uint32_t>(row), static_cast<uint32_t>(off), qn, prev_chunk);
+              prev_chunk = static_cast<uint32_t>(cid);
+            } else if (lane == 0) {
+              atomicOr(C.err, kErrHitOverflow);  // the host grows the buffers and reruns
+            }
+            __syncwarp();
+            if (lane == 0) sm->qn = 0;
+            __syncwarp();
+          }
         }
       }
       if (!walking) break;
@@ -800,7 +837,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
                 const uint64_t at = O.row_off[orow] + k;
                 O.xp_out[at] = R.perm ? __ldg(R.perm + j) : static_cast<uint32_t>(j);
                 O.g_out[at] = g;
-              } else if (MODE == kModeEloc) {  // rare: evaluated in place, term by term
+              } else if (kEval) {  // rare: evaluated in place, term by term
                 uint64_t xp[W];
 #pragma unroll
                 for (int w = 0; w < W; ++w) xp[w] = __ldg(keys + j * W + w);
@@ -819,7 +856,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
     }
 
     // diagonal element as the quadratic form over S(x)
-    if (MODE == kModeEloc && H.diag >= 0) {
+    if (kEval && H.diag >= 0) {
       if (H.diag_quad) {
         if (lane == 0) acc.x += side ? H.diag_A1 : H.diag_A0;
         if (lane < s) acc.x += __ldg(H.diag_b + side * n + pos);
@@ -852,10 +889,17 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
       }
     }
 
-    if (MODE == kModeEloc) {  // the walk drained the queue; residual hits were evaluated in place
+    if (kEval) {  // the walk drained the queue; residual hits were evaluated in place
       const double re = warp_sum(acc.x);
       const double im = warp_sum(acc.y);
-      if (lane == 0) O.eloc[orow - R.out_base] = make_double2(re, im);
+      if (lane == 0) {
+        if (MODE == kModeEloc) {
+          O.eloc[orow - R.out_base] = make_double2(re, im);
+        } else {
+          O.base[orow - R.out_base] = make_double2(re, im);
+          O.row_last[orow - R.out_base] = prev_chunk;
+        }
+      }
     }
     const uint32_t row_hits = warp_sum(hits) + (H.diag >= 0 ? 1u : 0u);
     if (MODE == kModeCount && lane == 0) O.counts[orow] = row_hits;
@@ -875,6 +919,107 @@ __global__ void __launch_bounds__(kThreads, QVMC_JOIN_MINB)
   if (lane == 0) {
     atomicAdd(C.stats, static_cast<unsigned long long>(tot_cand));
     atomicAdd(C.stats + 1, static_cast<unsigned long long>(tot_hits));
+  }
+}
+
+#ifndef QVMC_EVAL_MINB
+#define QVMC_EVAL_MINB 4
+#endif
+#ifndef QVMC_EVAL_HITS
+#define QVMC_EVAL_HITS 1  // hits per lane with records in flight together (2+: fewer warps, slower)
+#endif
+
+// Split evaluation, part 2: one warp per hit chunk (one row's hits in walk
+// order). Row context once per chunk, then QVMC_JOIN_DRAIN_HITS hits per lane
+// with all their records in flight; the chunk's sum goes to part[chunk].
+template <int W>
+__global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
+    k_eval_chunks(const __grid_constant__ HamView H, const __grid_constant__ JoinView J,
+                  const uint64_t* __restrict__ keys, const uint4* __restrict__ chunk,
+                  const unsigned long long* __restrict__ n_chunks, const uint32_t* __restrict__ hy,
+                  const uint32_t* __restrict__ hg, const uint32_t* __restrict__ hk, int side, int s,
+                  double2* __restrict__ part) {
+  constexpr int DH = QVMC_EVAL_HITS;
+  __shared__ uint16_t s_pos[kWarps][32];
+  const int lane = threadIdx.x & 31;
+  uint16_t* spos = s_pos[threadIdx.x >> 5];
+  const int n = H.n;
+  const uint64_t nc = *n_chunks;
+  const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t c = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; c < nc; c += n_warps) {
+    const uint4 ch = __ldg(chunk + c);
+    const int64_t row = ch.x;
+    Key<W> xrow;
+#pragma unroll
+    for (int w = 0; w < W; ++w) xrow.w[w] = __ldg(keys + row * W + w);
+    const U64x4 sr = ldg256(J.rec + row * 4);
+    const double la_i = __longlong_as_double(static_cast<long long>(sr.a));
+    const double2 cs_i = make_double2(__longlong_as_double(static_cast<long long>(sr.b)),
+                                      __longlong_as_double(static_cast<long long>(sr.c)));
+    // minority orbitals of the row (kind B elements)
+    int pos = 0, cnt = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      uint64_t v = side ? xrow.w[w] : ~xrow.w[w];
+      const int hi_bit = n - 64 * w;
+      if (hi_bit < 64) v &= (hi_bit <= 0) ? 0ull : ((1ull << hi_bit) - 1);
+      const int pc = __popcll(v);
+      if (lane >= cnt && lane < cnt + pc) {
+        for (int k = 0; k < lane - cnt; ++k) v &= v - 1;
+        pos = 64 * w + __ffsll(static_cast<long long>(v)) - 1;
+      }
+      cnt += pc;
+    }
+    __syncwarp();
+    if (lane < s) spos[lane] = static_cast<uint16_t>(pos);
+    __syncwarp();
+    double2 acc = make_double2(0.0, 0.0);
+    const unsigned n_hits = ch.z;
+    for (unsigned k0 = 0; k0 < n_hits; k0 += 32 * DH) {
+      JoinHit h[DH];
+#pragma unroll
+      for (int d = 0; d < DH; ++d) {
+        const unsigned k = k0 + 32 * d + lane;
+        JoinHit& q = h[d];
+        q.valid = k < n_hits;
+        q.key = kNoKey;
+        q.sr = U64x4{0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < kGrecWords; ++i) q.r[i] = 0;
+        if (q.valid) {
+          const uint64_t at = static_cast<uint64_t>(ch.y) + k;
+          const uint32_t y = __ldg(hy + at), g = __ldg(hg + at);
+          q.key = __ldg(hk + at);
+          q.sr = ldg256(J.rec + static_cast<int64_t>(y) * 4);
+          const U64x4 g0 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords);
+          const U64x4 g1 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords + 4);
+          q.r[0] = g0.a; q.r[1] = g0.b; q.r[2] = g0.c; q.r[3] = g0.d;
+          q.r[4] = g1.a; q.r[5] = g1.b; q.r[6] = g1.c; q.r[7] = g1.d;
+        }
+      }
+#pragma unroll
+      for (int d = 0; d < DH; ++d) eval_hit<W>(H, J, spos, h[d], xrow, la_i, cs_i, lane, s, side, acc);
+    }
+    const double re = warp_sum(acc.x);
+    const double im = warp_sum(acc.y);
+    if (lane == 0) part[c] = make_double2(re, im);
+  }
+}
+
+// Split evaluation, part 3: E_loc = base + the row's chunk sums, newest chunk
+// first (a fixed order: deterministic).
+__global__ void k_finalize_rows(const uint32_t* __restrict__ row_last, const uint4* __restrict__ chunk,
+                                const double2* __restrict__ part, const double2* __restrict__ base, int64_t rows,
+                                double2* __restrict__ eloc) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double2 e = base[r];
+    for (uint32_t c = row_last[r]; c != ~0u; c = __ldg(chunk + c).w) {
+      const double2 p = part[c];
+      e.x += p.x;
+      e.y += p.y;
+    }
+    eloc[r] = e;
   }
 }
 

@@ -21,8 +21,8 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kUnroll = 4;  // independent probes in flight per lane
 
-enum : int { kErrDuplicate = 1, kErrZeroAmp = 2, kErrBadPair = 4 };
-enum : int { kModeEloc = 0, kModeCount = 1, kModeEmit = 2 };
+enum : int { kErrDuplicate = 1, kErrZeroAmp = 2, kErrBadPair = 4, kErrHitOverflow = 8 };
+enum : int { kModeEloc = 0, kModeCount = 1, kModeEmit = 2, kModeHits = 3 };
 
 struct HamView {
   int n;        // qubits
@@ -245,6 +245,17 @@ struct RowOut {
   const double* la;           // log amplitudes
   const double* ph;           // phases
   const double2* cs;          // (cos, sin) of the phases
+  // kModeHits (join path, split evaluation): hit chunks for k_eval_chunks
+  uint32_t* hy;               // [hit_cap] partner (key-array position)
+  uint32_t* hg;               // [hit_cap] group
+  uint32_t* hk;               // [hit_cap] flip position key
+  uint4* chunk;               // [chunk_cap] (row position, first hit, hits, previous chunk of the row or ~0)
+  uint32_t* row_last;         // [row - out_base] last chunk of the row or ~0
+  double2* base;              // [row - out_base] diagonal + residual part of E_loc
+  unsigned long long* hit_cursor;
+  unsigned long long* chunk_cursor;
+  uint64_t hit_cap;
+  uint64_t chunk_cap;
 };
 
 __global__ void k_cos_sin(const double* __restrict__ ph, int64_t n, double2* cs) {
