@@ -326,8 +326,10 @@ __device__ __forceinline__ bool bit_at(const uint64_t* v, int p) {
 // H_{x x'} of a kind-A group: sum_t c_t i^{(y_t + 2|x' & z| + 2|b & ypat_t|) mod 4}
 // in term order, b = occupations of x' at the sorted flip positions. Same
 // terms, same order, same exact +-c adds as group_element: bit-identical.
+// (x' = x ^ m never needs forming: z avoids the flip positions, so
+// |x' & z| = |x & z|, and x' at a flip position is the complement of x.)
 template <int W>
-__device__ __forceinline__ void kind_a_element(const uint64_t* r, const uint64_t* xp, uint32_t key, double& re,
+__device__ __forceinline__ void kind_a_element(const uint64_t* r, const uint64_t* x, uint32_t key, double& re,
                                                double& im) {
   re = 0.0;
   im = 0.0;
@@ -335,12 +337,12 @@ __device__ __forceinline__ void kind_a_element(const uint64_t* r, const uint64_t
   const int k = static_cast<int>((meta >> 2) & 7);
   int pz = 0;
 #pragma unroll
-  for (int w = 0; w < W; ++w) pz += __popcll(xp[w] & r[2 + w]);
+  for (int w = 0; w < W; ++w) pz += __popcll(x[w] & r[2 + w]);
   const int np = (key >> 16) == 0xFFFFu ? 2 : 4;
   uint32_t bp = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
-    if (i < np) bp |= (bit_at<W>(xp, (key >> (8 * i)) & 0xFF) ? 1u : 0u) << i;
+    if (i < np) bp |= (bit_at<W>(x, (key >> (8 * i)) & 0xFF) ? 0u : 1u) << i;
 #pragma unroll
   for (int t = 0; t < kGrecWords - 2 - W; ++t) {
     if (t < k) {
@@ -363,8 +365,8 @@ __device__ __forceinline__ void kind_a_element(const uint64_t* r, const uint64_t
 // in one vector load) instead of the 2 + 2(N-2) terms.
 template <int W>
 __device__ __forceinline__ void kind_b_element(const double* __restrict__ famvi, const uint64_t* r, const uint64_t* x,
-                                               const uint64_t* xp, uint32_t key, const uint16_t* pos, int s,
-                                               int side, double& re, double& im) {
+                                               uint32_t key, const uint16_t* pos, int s, int side, double& re,
+                                               double& im) {
   re = 0.0;
   im = 0.0;
   const uint64_t meta = r[0];
@@ -397,8 +399,8 @@ __device__ __forceinline__ void kind_b_element(const double* __restrict__ famvi,
   }
   int pz = 0;
 #pragma unroll
-  for (int w = 0; w < W; ++w) pz += __popcll(xp[w] & r[2 + w]);
-  const uint32_t bp = (bit_at<W>(xp, p0) ? 1u : 0u) | (bit_at<W>(xp, p1) ? 2u : 0u);
+  for (int w = 0; w < W; ++w) pz += __popcll(x[w] & r[2 + w]);
+  const uint32_t bp = (bit_at<W>(x, p0) ? 0u : 1u) | (bit_at<W>(x, p1) ? 0u : 2u);
 #pragma unroll
   for (int j = 0; 2 + W + 2 * j + 1 < kGrecWords; ++j) {
     if (j < nf) {
@@ -481,22 +483,24 @@ template <int W>
 __device__ __forceinline__ void eval_hit(const HamView& H, const JoinView& J, const uint16_t* pos, const JoinHit& h,
                                          const Key<W>& xrow, double la_i, double2 cs_i, int lane, int s, int side,
                                          double2& acc) {
-  uint64_t xp[W];
-  {
+  const uint32_t kind = static_cast<uint32_t>(h.r[0]) & 3u;
+  const uint32_t nt = static_cast<uint32_t>(h.r[1] >> 32);
+  const bool large = h.valid && kind == kGrecC && nt > kSmallGroup;
+  uint64_t xp[W];  // x' = x ^ m: only the generic kinds C / D form it
+#pragma unroll
+  for (int w = 0; w < W; ++w) xp[w] = 0;
+  if (kind >= kGrecC) {
     uint64_t m[W];
     key_mask<W>(h.key, m);
 #pragma unroll
     for (int w = 0; w < W; ++w) xp[w] = xrow.w[w] ^ m[w];
   }
-  const uint32_t kind = static_cast<uint32_t>(h.r[0]) & 3u;
-  const uint32_t nt = static_cast<uint32_t>(h.r[1] >> 32);
-  const bool large = h.valid && kind == kGrecC && nt > kSmallGroup;
   double hr = 0.0, hi = 0.0;
   if (h.valid && !large) {
     if (kind == kGrecA) {
-      kind_a_element<W>(h.r, xp, h.key, hr, hi);
+      kind_a_element<W>(h.r, xrow.w, h.key, hr, hi);
     } else if (kind == kGrecB) {
-      kind_b_element<W>(J.famvi, h.r, xrow.w, xp, h.key, pos, s, side, hr, hi);
+      kind_b_element<W>(J.famvi, h.r, xrow.w, h.key, pos, s, side, hr, hi);
     } else if (kind == kGrecD) {
       const uint4 gi = make_uint4(0, 0, static_cast<uint32_t>(h.r[1]), static_cast<uint32_t>(h.r[0] >> 8));
       comp_element<W>(H, xrow.w, xp, gi, pos, s, side, hr, hi);
