@@ -21,6 +21,7 @@
 
 #include "host_index.h"
 #include "qvmc_cuda.h"
+#include "qvmc_bucket.cuh"
 #include "qvmc_join.cuh"
 #include "qvmc_kernels.cuh"
 
@@ -131,11 +132,11 @@ struct qvmc_ham_s {
   HamView view{};
   // join path (per call): deletion-index workspace
   DBuf l_key, l_key2, l_idx, l_perm, l_keys, l_rec, l_flags, l_list, l_nsel, cs;
-  DBuf j_key, j_val, j_key2, j_val2, j_head, j_rid, j_lo, j_hi, j_mem, j_rng, j_tmp;
+  DBuf j_key, j_val, j_key2, j_val2, j_head, j_rid, j_lo, j_hi, j_mem, j_rng, j_tmp, j_pos_of;
   bool use_join = true;
-  bool join_split = true;  // split evaluation (search -> hit chunks -> eval -> finalize)
+  int join_mode = 1;  // 0 fused row kernel, 1 row search + chunk eval (measured best), 2 bucket-centric search + row eval
   // split-evaluation workspace
-  DBuf s_hy, s_hg, s_hk, s_chunk, s_row_last, s_base, s_part;
+  DBuf s_hy, s_hg, s_hk, s_chunk, s_row_last, s_base, s_part, s_head, b_icnt, b_iincl, b_items;
   uint64_t hit_cap = 0, chunk_cap = 0;
   // workspace
   DBuf tab, ctl, keys, la, ph, lp, eloc, partials, moments, weights;
@@ -344,6 +345,7 @@ struct RowPlan {
   int side = 0;
   int s = 0;
   int key_bits = 0;  // join: bits of the exact bucket rank, ceil(log2 C(n, s - 2))
+  bool want_pos_of = false;  // bucket-centric evaluation needs the entry position of every (sample, pair)
 };
 
 RowPlan plan_rows(qvmc_ham_s* h, int64_t n) {
@@ -380,6 +382,7 @@ void build_join_index_k(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const Ro
   h->j_hi.ensure(E * 4 + 16);
   h->j_mem.ensure(E * 8 + 16);
   h->j_rng.ensure(E * 8 + 16);
+  if (P.want_pos_of) h->j_pos_of.ensure(E * 4 + 16);
   const int grid = static_cast<int>(std::min<int64_t>((n + kWarps - 1) / kWarps, grid_for(h, 8)));
   k_join_keys<W, K><<<std::max(grid, 1), kThreads, 0, h->stream>>>(keys, n, h->n, P.side, P.s, h->binom.as<uint64_t>(),
                                                                    h->j_key.as<K>(), h->j_val.as<uint64_t>());
@@ -407,7 +410,8 @@ void build_join_index_k(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const Ro
   ck_launch("run bounds");
   k_join_fill<<<std::max(egrid, 1), kThreads, 0, h->stream>>>(h->j_val2.as<uint64_t>(), h->j_rid.as<uint32_t>(), E,
                                                                C, h->j_lo.as<uint32_t>(), h->j_hi.as<uint32_t>(),
-                                                               h->j_mem.as<uint64_t>(), h->j_rng.as<uint2>());
+                                                               h->j_mem.as<uint64_t>(), h->j_rng.as<uint2>(),
+                                                               P.want_pos_of ? h->j_pos_of.as<uint32_t>() : nullptr);
   ck_launch("join fill");
 }
 
@@ -521,6 +525,104 @@ void run_join_split(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const 
                                                                    h->s_part.as<double2>(), h->s_base.as<double2>(),
                                                                    rows, eloc);
   ck_launch("finalize rows");
+}
+
+// Bucket-centric join (qvmc_bucket.cuh): work items over the deletion-index
+// buckets, the bucket search (hits chained per member entry; buffers grow and
+// the search reruns on overflow), then one warp per row evaluates.
+template <int W>
+void run_join_bucket(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, const RowSet& R, const RowPlan& P,
+                     int64_t r_begin, int64_t r_end, double2* eloc) {
+  const int64_t rows = R.n_rows;
+  if (rows <= 0) return;
+  const uint32_t C = static_cast<uint32_t>(P.s * (P.s - 1) / 2);
+  const uint64_t E = static_cast<uint64_t>(n_all) * C;
+  int* ctl = static_cast<int*>(h->ctl.p);
+  // work items
+  h->b_icnt.ensure(E * 4 + 16);
+  h->b_iincl.ensure(E * 4 + 16);
+  const int egrid = static_cast<int>(std::min<uint64_t>((E + kThreads - 1) / kThreads, grid_for(h, 16)));
+  k_item_count<<<std::max(egrid, 1), kThreads, 0, h->stream>>>(h->j_lo.as<uint32_t>(), h->j_hi.as<uint32_t>(),
+                                                                h->j_rid.as<uint32_t>(), E, h->b_icnt.as<uint32_t>());
+  ck_launch("item count");
+  size_t tmp = 0;
+  ck(cub::DeviceScan::InclusiveSum(nullptr, tmp, h->b_icnt.as<uint32_t>(), h->b_iincl.as<uint32_t>(),
+                                   static_cast<int>(E), h->stream),
+     "scan size");
+  h->j_tmp.ensure(tmp + 16);
+  ck(cub::DeviceScan::InclusiveSum(h->j_tmp.p, tmp, h->b_icnt.as<uint32_t>(), h->b_iincl.as<uint32_t>(),
+                                   static_cast<int>(E), h->stream),
+     "scan");
+  ++g_launches;
+  uint32_t n_items = 0;
+  ck(cudaMemcpyAsync(&n_items, h->b_iincl.as<uint32_t>() + (E - 1), 4, cudaMemcpyDeviceToHost, h->stream), "D2H items");
+  ck(cudaStreamSynchronize(h->stream), "sync");
+  h->b_items.ensure(static_cast<size_t>(n_items) * 16 + 16);
+  k_item_emit<<<std::max(egrid, 1), kThreads, 0, h->stream>>>(h->j_lo.as<uint32_t>(), h->j_hi.as<uint32_t>(),
+                                                               h->b_icnt.as<uint32_t>(), h->b_iincl.as<uint32_t>(), E,
+                                                               h->b_items.as<uint4>());
+  ck_launch("item emit");
+  // search
+  if (h->hit_cap == 0) {
+    h->hit_cap = std::max<uint64_t>(static_cast<uint64_t>(rows) * 320, 1u << 16);
+    h->chunk_cap = h->hit_cap / 8 + static_cast<uint64_t>(rows) + 1024;
+  }
+  h->s_head.ensure(E * 4 + 16);
+  unsigned long long cur[2] = {0, 0};
+  const bool shard = r_begin != 0 || r_end != n_all;
+  for (int attempt = 0;; ++attempt) {
+    h->hit_cap = std::min<uint64_t>(h->hit_cap, 0xFFFFFFFFull);
+    h->chunk_cap = std::min<uint64_t>(h->chunk_cap, 0xFFFFFFFEull);
+    h->s_hy.ensure(h->hit_cap * 4 + 16);
+    h->s_hg.ensure(h->hit_cap * 4 + 16);
+    h->s_hk.ensure(h->hit_cap * 4 + 16);
+    h->s_chunk.ensure(h->chunk_cap * 16 + 16);
+    ck(cudaMemsetAsync(h->s_head.p, 0xFF, E * 4, h->stream), "memset heads");
+    ck(cudaMemsetAsync(ctl + 4, 0, 2 * sizeof(int), h->stream), "memset item counter");
+    ck(cudaMemsetAsync(ctl + 6, 0, 8 * sizeof(int), h->stream), "memset stats + cursors");
+    BucketOut O{};
+    O.hy = h->s_hy.as<uint32_t>();
+    O.hg = h->s_hg.as<uint32_t>();
+    O.hk = h->s_hk.as<uint32_t>();
+    O.chunk = h->s_chunk.as<uint4>();
+    O.head = h->s_head.as<uint32_t>();
+    O.hit_cursor = reinterpret_cast<unsigned long long*>(ctl + 10);
+    O.chunk_cursor = reinterpret_cast<unsigned long long*>(ctl + 12);
+    O.hit_cap = h->hit_cap;
+    O.chunk_cap = h->chunk_cap;
+    int per_sm = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bucket_search<W>, kThreads, 0), "occupancy");
+    const int grid = static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>((n_items + kWarps - 1) / kWarps, static_cast<uint64_t>(grid_for(h, per_sm)))));
+    if (n_items > 0) {
+      k_bucket_search<W><<<grid, kThreads, 0, h->stream>>>(join_view(h, P), keys, h->n, h->b_items.as<uint4>(),
+                                                           h->b_iincl.as<uint32_t>() + (E - 1), P.side,
+                                                           shard ? R.perm : nullptr, r_begin, r_end, ctl_view(h), O);
+      ck_launch("bucket search");
+    }
+    ck(cudaMemcpyAsync(cur, ctl + 10, sizeof(cur), cudaMemcpyDeviceToHost, h->stream), "D2H cursors");
+    ck(cudaStreamSynchronize(h->stream), "sync");
+    if (cur[0] <= h->hit_cap && cur[1] <= h->chunk_cap) break;
+    if (attempt >= 3) fail(QVMC_ERR_RUNTIME, "join hit buffers keep overflowing");
+    h->hit_cap = std::max<uint64_t>(h->hit_cap, cur[0] + cur[0] / 4 + 1024);
+    h->chunk_cap = std::max<uint64_t>(h->chunk_cap, cur[1] + cur[1] / 4 + 1024);
+    int err = 0;
+    ck(cudaMemcpy(&err, ctl, sizeof(int), cudaMemcpyDeviceToHost), "read err");
+    err &= ~kErrHitOverflow;
+    ck(cudaMemcpy(ctl, &err, sizeof(int), cudaMemcpyHostToDevice), "reset overflow");
+  }
+  // evaluation, one warp per row
+  ck(cudaMemsetAsync(ctl + 4, 0, 2 * sizeof(int), h->stream), "memset row counter");
+  int per_sm = 0;
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bucket_eval<W>, kThreads, 0), "occupancy");
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((rows + kWarps - 1) / kWarps,
+                                                                           grid_for(h, per_sm))));
+  TableView T{h->tab.as<uint64_t>(), h->tab_buckets - 1};
+  k_bucket_eval<W><<<grid, kThreads, 0, h->stream>>>(h->view, T, join_view(h, P), keys, R, P.side, P.s,
+                                                     h->j_pos_of.as<uint32_t>(), h->s_head.as<uint32_t>(),
+                                                     h->s_chunk.as<uint4>(), h->s_hy.as<uint32_t>(),
+                                                     h->s_hg.as<uint32_t>(), h->s_hk.as<uint32_t>(), ctl_view(h), eloc);
+  ck_launch("bucket eval");
 }
 
 template <int W, int MODE>
@@ -785,7 +887,11 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     h->xy_tab_mask = p.xy_tab_mask;
     upload(h->codes, std::vector<uint64_t>(qubit_codes(), qubit_codes() + 256));
     if (const char* e = std::getenv("QVMC_JOIN")) h->use_join = std::atoi(e) != 0;
-    if (const char* e = std::getenv("QVMC_JOIN_SPLIT")) h->join_split = std::atoi(e) != 0;
+    if (const char* e = std::getenv("QVMC_JOIN_MODE")) h->join_mode = std::atoi(e);
+    if (const char* e = std::getenv("QVMC_HIT_CAP")) {  // test hook: a small first capacity exercises the regrow path
+      h->hit_cap = std::strtoull(e, nullptr, 10);
+      h->chunk_cap = h->hit_cap / 8 + 64;
+    }
     h->ctl.ensure(kCtlInts * sizeof(int) * 2);
     ck(cudaMemset(h->ctl.p, 0, kCtlInts * sizeof(int) * 2), "memset ctl");
 
@@ -1150,6 +1256,7 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       P = plan_rows(h, n_unq);
       note_plan(h, P);
       if (P.join) {
+        P.want_pos_of = h->join_mode == 2;
         DISPATCH_W(W, R = sort_for_locality<WW>(h, rkeys, dla, dph, n_unq, row_begin, row_end, P));
         if (h->view.n_res) DISPATCH_W(W, launch_table_build<WW>(h, rkeys, n_unq));  // residual probes: sorted ids
         DISPATCH_W(W, build_join_index<WW>(h, rkeys, n_unq, P));
@@ -1168,7 +1275,9 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       O.la = dla;
       O.ph = dph;
       O.cs = rcs;
-      if (P.join && h->join_split) {
+      if (P.join && h->join_mode == 2) {
+        DISPATCH_W(W, (run_join_bucket<WW>(h, rkeys, n_unq, R, P, row_begin, row_end, deloc)));
+      } else if (P.join && h->join_mode == 1) {
         DISPATCH_W(W, (run_join_split<WW>(h, rkeys, R, P, deloc)));
       } else if (P.join) {
         DISPATCH_W(W, (launch_rows_join<WW, kModeEloc>(h, rkeys, R, P, O)));

@@ -31,7 +31,7 @@ namespace qvmc_b200 {
 #endif
 
 #ifndef QVMC_JOIN_UNROLL
-#define QVMC_JOIN_UNROLL 2  // bucket members in flight per lane
+#define QVMC_JOIN_UNROLL 4  // bucket members in flight per lane
 #endif
 
 #ifndef QVMC_JOIN_DRAIN_ATTR
@@ -244,14 +244,16 @@ __global__ void k_run_bounds(const uint32_t* __restrict__ rid, uint64_t E, uint3
 }
 
 // member array + per-(sample, pair) bucket range
+// (pos_of, optional: the member position of every (sample, pair) entry)
 __global__ void k_join_fill(const uint64_t* __restrict__ val, const uint32_t* __restrict__ rid, uint64_t E, uint32_t C,
                             const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi,
-                            uint64_t* __restrict__ mem, uint2* __restrict__ rng) {
+                            uint64_t* __restrict__ mem, uint2* __restrict__ rng, uint32_t* __restrict__ pos_of) {
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < E; p += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t v = val[p];
     const uint32_t r = rid[p] - 1;
     const uint64_t y = v & 0xFFFFFFFFull, t = v >> 48;
     rng[y * C + t] = make_uint2(lo[r], hi[r]);
+    if (pos_of) pos_of[y * C + t] = static_cast<uint32_t>(p);
     const uint32_t a = static_cast<uint32_t>(v >> 32) & 0xFF, b = static_cast<uint32_t>(v >> 40) & 0xFF;
     mem[p] = (v & 0x0000FFFFFFFFFFFFull) | static_cast<uint64_t>(b * (b - 1) / 2 + a) << 48;
   }
@@ -420,7 +422,8 @@ __device__ __forceinline__ void kind_b_element(const double* __restrict__ famvi,
 
 // Per-warp state of the join kernel.
 constexpr int kJQueue = 256;
-constexpr int kJDrainAt = kJQueue - 32 * QVMC_JOIN_UNROLL;  // one scan step adds at most 32*U hits
+constexpr int kJDrainAt = kJQueue - 32 * (QVMC_JOIN_UNROLL + 1);  // one step: <= U+1 lookup batches of 32
+constexpr int kJSurv = 128;  // ring of candidates that passed the accept rule and the bitmap
 
 struct JoinSmem {
   uint32_t qy[kJQueue];  // hit queue: partner (sorted position), group, flip position key
@@ -434,6 +437,8 @@ struct JoinSmem {
   uint64_t x[4];                  // the current row: key, log psi, (cos, sin) of its phase; kept here
   double la, cs_c, cs_s;          // (not in registers) across the candidate walk
   uint16_t pos[32];               // minority orbitals of the current row
+  uint32_t sy[kJSurv];            // survivor ring: partner, flip position key (looked up 32 at a time)
+  uint32_t sk[kJSurv];
   unsigned qn;
   unsigned cursor;                // kModeEmit output cursor
 };
@@ -578,7 +583,7 @@ __device__ QVMC_JOIN_DRAIN_ATTR double2 join_drain(const HamView& H, const JoinV
 }
 
 #ifndef QVMC_SEARCH_MINB
-#define QVMC_SEARCH_MINB 5  // split search kernel (no drain): 48 registers, 40 warps per SM (measured best)
+#define QVMC_SEARCH_MINB 4  // split search kernel (no drain): 64 registers, 32 warps per SM (measured best, r01x)
 #endif
 
 template <int W, int MODE>
@@ -678,6 +683,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
     uint32_t hits = 0;
     uint64_t cand = 0;
     uint32_t prev_chunk = ~0u;  // kModeHits: last flushed chunk of this row
+    uint32_t s_head = 0, s_tail = 0;  // survivor ring (warp-uniform)
     int rg = 0;
     uint32_t off = lane;
     uint32_t len = sm->r_len[0];
@@ -734,18 +740,37 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
           }
         }
       }
-      // flip-mask lookups, one at a time (hoisting all U bucket loads first
-      // measured slower: the extra live registers spill)
+      // survivors -> ring; the flip-table lookups then run 32 at a time with
+      // every lane busy (a lookup per candidate would execute on nearly every
+      // step for the ~1 in 7 candidates that survive)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        int64_t g = -1;
+        const unsigned smk = __ballot_sync(0xffffffffu, key[u] != kNoKey);
         if (key[u] != kNoKey) {
+          const uint32_t e = (s_tail + __popc(smk & ((1u << lane) - 1u))) & (kJSurv - 1);
+          sm->sy[e] = static_cast<uint32_t>(v[u]);
+          sm->sk[e] = key[u];
+        }
+        s_tail += __popc(smk);
+      }
+      __syncwarp();
+      }
+      while (s_tail - s_head >= 32 || (!walking && s_tail != s_head)) {
+        const uint32_t cntl = min(s_tail - s_head, 32u);
+        const bool valid = static_cast<uint32_t>(lane) < cntl;
+        uint32_t y = 0, kk = kNoKey;
+        int64_t g = -1;
+        if (valid) {
+          const uint32_t e = (s_head + lane) & (kJSurv - 1);
+          y = sm->sy[e];
+          kk = sm->sk[e];
 #ifndef QVMC_EXP_NO_LOOKUP
-          const uint32_t bk = xy_bucket(key[u], static_cast<uint32_t>(J.xy_mask));
-          g = xy_resolve(key[u], ldg256(J.xy_tab + static_cast<uint64_t>(bk) * 4));
-          if (g == kChain) g = xy_chain(key[u], bk, J.xy_tab, static_cast<uint32_t>(J.xy_mask));
+          const uint32_t bk = xy_bucket(kk, static_cast<uint32_t>(J.xy_mask));
+          g = xy_resolve(kk, ldg256(J.xy_tab + static_cast<uint64_t>(bk) * 4));
+          if (g == kChain) g = xy_chain(kk, bk, J.xy_tab, static_cast<uint32_t>(J.xy_mask));
 #endif
         }
+        s_head += cntl;
         // warp-aggregated append of the hits
         const bool hit = g >= 0;
         const unsigned hm = __ballot_sync(0xffffffffu, hit);
@@ -756,11 +781,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
             base = __shfl_sync(0xffffffffu, base, 0);
             if (hit) {
               const unsigned k = base + __popc(hm & ((1u << lane) - 1u));
-              const uint32_t y = static_cast<uint32_t>(v[u]);
               if (kEval) {
                 sm->qy[k] = y;
                 sm->qg[k] = static_cast<uint32_t>(g);
-                sm->qk[k] = key[u];
+                sm->qk[k] = kk;
               } else {
                 const uint64_t at = O.row_off[orow] + k;
                 O.xp_out[at] = R.perm ? __ldg(R.perm + y) : y;
@@ -770,7 +794,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
           }
           hits += hit ? 1u : 0u;
         }
-      }
+        __syncwarp();
       }
       if (kEval) {
         __syncwarp();
