@@ -264,7 +264,7 @@ def main():
     _lib.check(_lib.lib().qvmc_cuda_synchronize(H.device_handle(local)))
 
     stream = torch.cuda.current_stream(dev)
-    step_ms, rows_ms, table_ms, mom_ms = [], [], [], []
+    step_ms, rows_ms, table_ms, mom_ms, search_ms, eval_ms = [], [], [], [], [], []
     launches0 = q.launch_count()
     with ClockSampler(local) as clk:
         if world > 1:
@@ -284,6 +284,8 @@ def main():
             rows_ms.append(st["rows_ms"])
             table_ms.append(st["table_ms"])
             mom_ms.append(st["moments_ms"])
+            search_ms.append(st["search_ms"])
+            eval_ms.append(st["eval_ms"])
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -345,7 +347,9 @@ def main():
         e2e_t = float(t)
         _lib.check(_lib.lib().qvmc_cuda_set_stream(H.device_handle(local), None))
 
-    # ---- roofline of the dominant kernel (k_rows): algorithmic bytes / kernel time
+    # ---- roofline of the E_loc stage (the hot path: search kernel + chunk
+    # evaluation kernel + per-row finalize, timed together with CUDA events on
+    # the handle's stream): algorithmic bytes / stage time
     rows_here = r1 - r0
     pairs_per_row = stats["pairs"] / max(rows_here, 1)
     b_alg = 8 * W + 16 + 8 + 16 + pairs_per_row * (8 * W + 16)
@@ -353,6 +357,14 @@ def main():
     achieved = b_alg * rows_here / (kern_ms * 1e-3) / 1e9
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("hbm_gbs", 6650.0)
+    # DRAM traffic of the same kernels from one `ncu --set full` capture each (profiles/ncu_traffic.json)
+    traffic, traffic_src = None, None
+    tj = ROOT / "profiles" / "ncu_traffic.json"
+    if tj.exists() and args.n_unq is None:
+        t = json.loads(tj.read_text()).get(args.config, {})
+        if "search" in t and "eval" in t:
+            traffic = t["search"]["dram_bytes"] + t["eval"]["dram_bytes"]
+            traffic_src = f"profiles/ncu_traffic.json ({t['search']['report']}, {t['eval']['report']})"
 
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -366,10 +378,12 @@ def main():
                 "path": "qvmc_cuda_eloc_fused(QVMC_MEM_HOST) from pinned buffers" if world == 1
                 else "distributed.sharded_surrogate_energy from pinned host shards"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
-                     "kernel": "k_rows<W, kModeEloc>", "kernel_ms": kern_ms,
-                     "kernel_share_of_step": kern_ms / statistics.mean(step_ms),
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "kernel": "E_loc stage: k_rows_join<W,kModeHits> search + k_eval_chunks<W> + k_finalize_rows",
+                     "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / statistics.mean(step_ms),
+                     "search_ms": statistics.mean(search_ms), "eval_ms": statistics.mean(eval_ms),
                      "bytes_per_sample": b_alg,
+                     "note": "integer/L2-latency bound, not HBM: see DESIGN.md section 4 and profiles/",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),

@@ -81,7 +81,8 @@ typedef struct {
   float table_ms;           /* CUDA-event times of the last fused call's stages on the */
   float rows_ms;            /* handle's stream: sample-set hash build, row kernel,     */
   float moments_ms;         /* moment reduction                                       */
-  float reserved_ms;
+  float search_ms;          /* join path, split evaluation: the search kernel and the  */
+  float eval_ms;            /* chunk evaluation kernel inside rows_ms (else 0)         */
 } qvmc_stats;
 
 /* ------------------------------------------------------------------ host index */

@@ -42,7 +42,8 @@ class QvmcStats(C.Structure):
         ("table_ms", C.c_float),
         ("rows_ms", C.c_float),
         ("moments_ms", C.c_float),
-        ("reserved_ms", C.c_float),
+        ("search_ms", C.c_float),
+        ("eval_ms", C.c_float),
     ]
 
 

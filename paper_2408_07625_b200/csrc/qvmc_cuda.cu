@@ -146,12 +146,15 @@ struct qvmc_ham_s {
   int64_t pairs_rows = 0;
   qvmc_stats last{};
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // fused-call stage timing
+  cudaEvent_t ev_k[3] = {nullptr, nullptr, nullptr};         // split evaluation: search | eval
+  bool timed_k = false;
   bool timed = false;
 };
 
 namespace {
 
-constexpr int kCtlInts = 16;  // int err, pad, popc_mm[2]; u64 row_next @4, stats[2] @6, hit/chunk cursors @10/@12
+constexpr int kCtlInts = 16;  // int err, pad, popc_mm[2]; u64 row_next @4, stats[2] @6, hit/chunk cursors @10/@12,
+                              // int exp flag @14 (some |log psi| > 700)
 
 Ctl ctl_view(qvmc_ham_s* h) {
   Ctl c;
@@ -494,8 +497,10 @@ void run_join_split(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const 
     const int64_t blocks_needed = (rows + kWarps - 1) / kWarps;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_needed, grid_for(h, per_sm))));
     TableView T{h->tab.as<uint64_t>(), h->tab_buckets - 1};
+    ck(cudaEventRecord(h->ev_k[0], h->stream), "event");
     k_rows_join<W, kModeHits><<<grid, kThreads, 0, h->stream>>>(h->view, T, join_view(h, P), keys, R, P.side, P.s,
                                                                 ctl_view(h), O);
+    ck(cudaEventRecord(h->ev_k[1], h->stream), "event");
     ck_launch("row kernel (join search)");
     ck(cudaMemcpyAsync(cur, ctl + 10, sizeof(cur), cudaMemcpyDeviceToHost, h->stream), "D2H cursors");
     ck(cudaStreamSynchronize(h->stream), "sync");
@@ -517,9 +522,12 @@ void run_join_split(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const 
         std::max<uint64_t>(1, std::min<uint64_t>((nc + kWarps - 1) / kWarps, static_cast<uint64_t>(grid_for(h, per_sm)))));
     k_eval_chunks<W><<<grid, kThreads, 0, h->stream>>>(
         h->view, join_view(h, P), keys, h->s_chunk.as<uint4>(), reinterpret_cast<unsigned long long*>(ctl + 12),
-        h->s_hy.as<uint32_t>(), h->s_hg.as<uint32_t>(), h->s_hk.as<uint32_t>(), P.side, P.s, h->s_part.as<double2>());
+        h->s_hy.as<uint32_t>(), h->s_hg.as<uint32_t>(), h->s_hk.as<uint32_t>(), P.side, P.s, ctl + 14,
+        h->s_part.as<double2>());
     ck_launch("eval chunks");
   }
+  ck(cudaEventRecord(h->ev_k[2], h->stream), "event");
+  h->timed_k = true;
   const int fgrid = static_cast<int>(std::min<int64_t>((rows + kThreads - 1) / kThreads, grid_for(h, 8)));
   k_finalize_rows<<<std::max(fgrid, 1), kThreads, 0, h->stream>>>(h->s_row_last.as<uint32_t>(), h->s_chunk.as<uint4>(),
                                                                    h->s_part.as<double2>(), h->s_base.as<double2>(),
@@ -659,8 +667,10 @@ RowSet sort_for_locality(qvmc_ham_s* h, const uint64_t*& keys, const double* la,
                                      h->l_idx.as<uint32_t>(), h->l_perm.as<uint32_t>(), ni, 0, 64, h->stream),
      "sort");
   ++g_launches;
+  ck(cudaMemsetAsync(static_cast<int*>(h->ctl.p) + 14, 0, sizeof(int), h->stream), "memset exp flag");
   k_gather_sorted<W><<<std::max(grid, 1), kThreads, 0, h->stream>>>(
-      h->l_perm.as<uint32_t>(), n, keys, la, ph, h->l_keys.as<uint64_t>(), h->l_rec.as<double>());
+      h->l_perm.as<uint32_t>(), n, keys, la, ph, h->l_keys.as<uint64_t>(), h->l_rec.as<double>(),
+      static_cast<int*>(h->ctl.p) + 14);
   ck_launch("gather sorted");
   keys = h->l_keys.as<uint64_t>();
   RowSet R{n, 0, nullptr, h->l_perm.as<uint32_t>(), r0};
@@ -747,6 +757,7 @@ void compute_moments(qvmc_ham_s* h, const double* lp, double log_norm, const dou
 
 void record_stats(qvmc_ham_s* h, int64_t rows) {
   h->timed = false;
+  h->timed_k = false;
   h->last = qvmc_stats{};
   h->last.rows = static_cast<uint64_t>(rows);
   h->last.terms_equivalent = static_cast<uint64_t>(rows) * h->n_xy;
@@ -850,6 +861,7 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     ck(cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking), "stream create");
     h->stream = h->own;
     for (auto& e : h->ev) ck(cudaEventCreate(&e), "event create");
+    for (auto& e : h->ev_k) ck(cudaEventCreate(&e), "event create");
     upload(h->xy, hi.xy);
     upload(h->xy_hash, p.xy_hash);
     upload(h->goff, p.offsets32);
@@ -957,6 +969,8 @@ int qvmc_cuda_ham_destroy(qvmc_ham_t h) {
     }
     for (auto& e : h->ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : h->ev_k)
+      if (e) cudaEventDestroy(e);
     delete h;
   });
 }
@@ -991,6 +1005,10 @@ int qvmc_cuda_last_stats(qvmc_ham_t h, qvmc_stats* out) {
       ck(cudaEventElapsedTime(&out->table_ms, h->ev[0], h->ev[1]), "elapsed");
       ck(cudaEventElapsedTime(&out->rows_ms, h->ev[1], h->ev[2]), "elapsed");
       ck(cudaEventElapsedTime(&out->moments_ms, h->ev[2], h->ev[3]), "elapsed");
+    }
+    if (h->timed_k) {
+      ck(cudaEventElapsedTime(&out->search_ms, h->ev_k[0], h->ev_k[1]), "elapsed");
+      ck(cudaEventElapsedTime(&out->eval_ms, h->ev_k[1], h->ev_k[2]), "elapsed");
     }
     out->candidates = st[0];
     out->pairs = st[1];

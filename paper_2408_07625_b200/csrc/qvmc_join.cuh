@@ -137,18 +137,23 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// Sorted copies of the keys and the per-sample records (log psi, cos, sin).
+// Sorted copies of the keys and the per-sample records (log psi, cos, sin, e^{log psi}).
+// Record slot 3 = psi magnitude e^{log psi}: amplitude ratios become one
+// multiply by the row's 1/e^{log psi} instead of an exp per pair, unless some
+// |log psi| > 700 (then exp_flag is set and the exp path is used).
 template <int W>
 __global__ void k_gather_sorted(const uint32_t* __restrict__ perm, int64_t n, const uint64_t* __restrict__ keys,
                                 const double* __restrict__ la, const double* __restrict__ ph, uint64_t* keys_s,
-                                double* rec) {
+                                double* rec, int* exp_flag) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t o = perm[i];
 #pragma unroll
     for (int w = 0; w < W; ++w) keys_s[i * W + w] = keys[(int64_t)o * W + w];
     double sn, c;
     sincos(ph[o], &sn, &c);
-    reinterpret_cast<double4*>(rec)[i] = make_double4(la[o], c, sn, 0.0);
+    const double l = la[o];
+    if (isfinite(l) && fabs(l) > 700.0) atomicOr(exp_flag, 1);
+    reinterpret_cast<double4*>(rec)[i] = make_double4(l, c, sn, exp(l));
   }
 }
 
@@ -440,6 +445,7 @@ struct JoinSmem {
   uint32_t sy[kJSurv];            // survivor ring: partner, flip position key (looked up 32 at a time)
   uint32_t sk[kJSurv];
   unsigned qn;
+  unsigned qs;                    // kModeHits: single excitations, queued from the top (a chunk = doubles, then singles)
   unsigned cursor;                // kModeEmit output cursor
 };
 
@@ -487,7 +493,7 @@ __device__ __forceinline__ void load_hit(const JoinView& J, const JoinSmem* sm, 
 template <int W>
 __device__ __forceinline__ void eval_hit(const HamView& H, const JoinView& J, const uint16_t* pos, const JoinHit& h,
                                          const Key<W>& xrow, double la_i, double2 cs_i, int lane, int s, int side,
-                                         double2& acc) {
+                                         double2& acc, double inv_ai = 0.0) {
   const uint32_t kind = static_cast<uint32_t>(h.r[0]) & 3u;
   const uint32_t nt = static_cast<uint32_t>(h.r[1] >> 32);
   const bool large = h.valid && kind == kGrecC && nt > kSmallGroup;
@@ -546,7 +552,11 @@ __device__ __forceinline__ void eval_hit(const HamView& H, const JoinView& J, co
   if (h.valid) {
     const double2 cs_j = make_double2(__longlong_as_double(static_cast<long long>(h.sr.b)),
                                       __longlong_as_double(static_cast<long long>(h.sr.c)));
-    add_ratio(__longlong_as_double(static_cast<long long>(h.sr.a)), cs_j, la_i, cs_i, hr, hi, acc);
+    if (inv_ai != 0.0) {  // psi(x')/psi(x) magnitude = e^{la_j} * (1 / e^{la_i})
+      add_ratio_mag(__longlong_as_double(static_cast<long long>(h.sr.d)) * inv_ai, cs_j, cs_i, hr, hi, acc);
+    } else {
+      add_ratio(__longlong_as_double(static_cast<long long>(h.sr.a)), cs_j, la_i, cs_i, hr, hi, acc);
+    }
   }
 }
 
@@ -597,7 +607,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
   JoinSmem* sm = &s_w[threadIdx.x >> 5];
   const int n = H.n;
   const int n_ranges = s * (s - 1) / 2;
-  if (lane == 0) sm->qn = 0;
+  if (lane == 0) {
+    sm->qn = 0;
+    sm->qs = 0;
+  }
   __syncwarp();
 
   uint64_t tot_cand = 0, tot_hits = 0;
@@ -775,7 +788,23 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
         const bool hit = g >= 0;
         const unsigned hm = __ballot_sync(0xffffffffu, hit);
         if (hm) {
-          if (kEval || MODE == kModeEmit) {
+          if (MODE == kModeHits) {  // doubles fill the queue from the bottom, singles from the top
+            const bool is_s = (kk >> 16) == 0xFFFFu;
+            const unsigned lt = (1u << lane) - 1u;
+            const unsigned hs = __ballot_sync(0xffffffffu, hit && is_s), hd = hm & ~hs;
+            const unsigned bd = sm->qn, bs = sm->qs;
+            if (hit) {
+              const unsigned k = is_s ? kJQueue - 1 - (bs + __popc(hs & lt)) : bd + __popc(hd & lt);
+              sm->qy[k] = y;
+              sm->qg[k] = static_cast<uint32_t>(g);
+              sm->qk[k] = kk;
+            }
+            __syncwarp();
+            if (lane == 0) {
+              sm->qn = bd + __popc(hd);
+              sm->qs = bs + __popc(hs);
+            }
+          } else if (kEval || MODE == kModeEmit) {
             unsigned base = 0;
             if (lane == 0) base = atomicAdd(kEval ? &sm->qn : &sm->cursor, __popc(hm));
             base = __shfl_sync(0xffffffffu, base, 0);
@@ -798,7 +827,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
       }
       if (kEval) {
         __syncwarp();
-        const unsigned qn = sm->qn;
+        const unsigned qd = sm->qn, qsn = MODE == kModeHits ? sm->qs : 0u;
+        const unsigned qn = qd + qsn;
         if (qn >= (walking ? static_cast<unsigned>(kJDrainAt) : 1u)) {
           if (MODE == kModeEloc) {
             const double2 d = join_drain<W>(H, J, sm, lane, s, side);
@@ -814,9 +844,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
             cid = __shfl_sync(0xffffffffu, cid, 0);
             if (off + qn <= O.hit_cap && cid < O.chunk_cap) {
               for (unsigned k = lane; k < qn; k += 32) {
-                O.hy[off + k] = sm->qy[k];
-                O.hg[off + k] = sm->qg[k];
-                O.hk[off + k] = sm->qk[k];
+                const unsigned src = k < qd ? k : kJQueue - 1 - (k - qd);
+                O.hy[off + k] = sm->qy[src];
+                O.hg[off + k] = sm->qg[src];
+                O.hk[off + k] = sm->qk[src];
               }
               if (lane == 0)
                 O.chunk[cid] = make_uint4(static_cast<uint32_t>(row), static_cast<uint32_t>(off), qn, prev_chunk);
@@ -825,7 +856,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
               atomicOr(C.err, kErrHitOverflow);  // the host grows the buffers and reruns
             }
             __syncwarp();
-            if (lane == 0) sm->qn = 0;
+            if (lane == 0) {
+              sm->qn = 0;
+              sm->qs = 0;
+            }
             __syncwarp();
           }
         }
@@ -951,7 +985,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
 }
 
 #ifndef QVMC_EVAL_MINB
-#define QVMC_EVAL_MINB 4
+#define QVMC_EVAL_MINB 3  // 80 registers (measured best, r01z)
 #endif
 #ifndef QVMC_EVAL_HITS
 #define QVMC_EVAL_HITS 1  // hits per lane with records in flight together (2+: fewer warps, slower)
@@ -966,13 +1000,14 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
                   const uint64_t* __restrict__ keys, const uint4* __restrict__ chunk,
                   const unsigned long long* __restrict__ n_chunks, const uint32_t* __restrict__ hy,
                   const uint32_t* __restrict__ hg, const uint32_t* __restrict__ hk, int side, int s,
-                  double2* __restrict__ part) {
+                  const int* __restrict__ exp_flag, double2* __restrict__ part) {
   constexpr int DH = QVMC_EVAL_HITS;
   __shared__ uint16_t s_pos[kWarps][32];
   const int lane = threadIdx.x & 31;
   uint16_t* spos = s_pos[threadIdx.x >> 5];
   const int n = H.n;
   const uint64_t nc = *n_chunks;
+  const bool mag = *exp_flag == 0;  // amplitude magnitudes from the records (k_gather_sorted)
   const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t c = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; c < nc; c += n_warps) {
     const uint4 ch = __ldg(chunk + c);
@@ -984,6 +1019,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
     const double la_i = __longlong_as_double(static_cast<long long>(sr.a));
     const double2 cs_i = make_double2(__longlong_as_double(static_cast<long long>(sr.b)),
                                       __longlong_as_double(static_cast<long long>(sr.c)));
+    const double inv_ai = mag ? 1.0 / __longlong_as_double(static_cast<long long>(sr.d)) : 0.0;
     // minority orbitals of the row (kind B elements)
     int pos = 0, cnt = 0;
 #pragma unroll
@@ -1026,7 +1062,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
         }
       }
 #pragma unroll
-      for (int d = 0; d < DH; ++d) eval_hit<W>(H, J, spos, h[d], xrow, la_i, cs_i, lane, s, side, acc);
+      for (int d = 0; d < DH; ++d) eval_hit<W>(H, J, spos, h[d], xrow, la_i, cs_i, lane, s, side, acc, inv_ai);
     }
     const double re = warp_sum(acc.x);
     const double im = warp_sum(acc.y);

@@ -303,6 +303,17 @@ __device__ __forceinline__ void add_ratio(double la_j, double2 cs_j, double la_i
   acc.y += hr * s + hi * c;
 }
 
+// the same with the magnitude |psi(x')/psi(x)| given
+__device__ __forceinline__ void add_ratio_mag(double a, double2 cs_j, double2 cs_i, double hr, double hi,
+                                              double2& acc) {
+  const double c = cs_j.x * cs_i.x + cs_j.y * cs_i.y;
+  const double s = cs_j.y * cs_i.x - cs_j.x * cs_i.y;
+  hr *= a;
+  hi *= a;
+  acc.x += hr * c - hi * s;
+  acc.y += hr * s + hi * c;
+}
+
 // H_{xx'} of a compressed group (sector mode): per family f,
 //   i^q_f (-1)^{|x' & B_f|} (u_f + sum_k v_f[k] (-1)^{x'_k}),
 // with sum_k v_f[k] (-1)^{x'_k} = +-(V_f - 2 sum_{k in S(x')} v_f[k]) over the
