@@ -138,6 +138,7 @@ struct qvmc_ham_s {
   // split-evaluation workspace
   DBuf s_hy, s_hg, s_hk, s_chunk, s_row_last, s_base, s_part, s_head, b_icnt, b_iincl, b_items;
   uint64_t hit_cap = 0, chunk_cap = 0;
+  uint64_t hits_per_row = 320;  // split evaluation: running estimate that sizes the row batches
   // workspace
   DBuf tab, ctl, keys, la, ph, lp, eloc, partials, moments, weights;
   DBuf counts, row_off, xp_a, g_a, xp_b, g_b, entries, cub_tmp, in_entries, out_h, out_class;
@@ -461,17 +462,12 @@ void launch_rows_join(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, cons
 // k_finalize_rows sums base + chunks per row in a fixed order. The hit
 // buffers grow (and the search reruns) when a call overflows them.
 template <int W>
-void run_join_split(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const RowPlan& P, double2* eloc) {
+void run_join_split_batch(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const RowPlan& P, double2* eloc,
+                          uint64_t& hits_seen, unsigned long long* stats_before) {
   const int64_t rows = R.n_rows;
-  if (rows <= 0) return;
-  if (h->hit_cap == 0) {
-    h->hit_cap = std::max<uint64_t>(static_cast<uint64_t>(rows) * 320, 1u << 16);
-    h->chunk_cap = h->hit_cap / 64 + static_cast<uint64_t>(rows) + 1024;
-  }
-  h->s_row_last.ensure(rows * 4 + 16);
-  h->s_base.ensure(rows * 16 + 16);
   int* ctl = static_cast<int*>(h->ctl.p);
-  unsigned long long cur[2] = {0, 0};
+  unsigned long long rd[4] = {0, 0, 0, 0};  // stats[2] (candidates, pairs), hit and chunk cursors
+  unsigned long long* cur = rd + 2;
   for (int attempt = 0;; ++attempt) {
     h->hit_cap = std::min<uint64_t>(h->hit_cap, 0xFFFFFFFFull);
     h->s_hy.ensure(h->hit_cap * 4 + 16);
@@ -480,7 +476,7 @@ void run_join_split(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const 
     h->s_chunk.ensure(h->chunk_cap * 16 + 16);
     h->s_part.ensure(h->chunk_cap * 16 + 16);
     ck(cudaMemsetAsync(ctl + 4, 0, 2 * sizeof(int), h->stream), "memset row counter");
-    ck(cudaMemsetAsync(ctl + 6, 0, 8 * sizeof(int), h->stream), "memset stats + cursors");
+    ck(cudaMemsetAsync(ctl + 10, 0, 4 * sizeof(int), h->stream), "memset cursors");
     RowOut O{};
     O.hy = h->s_hy.as<uint32_t>();
     O.hg = h->s_hg.as<uint32_t>();
@@ -502,11 +498,16 @@ void run_join_split(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const 
                                                                 ctl_view(h), O);
     ck(cudaEventRecord(h->ev_k[1], h->stream), "event");
     ck_launch("row kernel (join search)");
-    ck(cudaMemcpyAsync(cur, ctl + 10, sizeof(cur), cudaMemcpyDeviceToHost, h->stream), "D2H cursors");
+    ck(cudaMemcpyAsync(rd, ctl + 6, sizeof(rd), cudaMemcpyDeviceToHost, h->stream), "D2H stats + cursors");
     ck(cudaStreamSynchronize(h->stream), "sync");
-    if (cur[0] <= h->hit_cap && cur[1] <= h->chunk_cap) break;
-    if (attempt >= 3) fail(QVMC_ERR_RUNTIME, "join hit buffers keep overflowing");
-    // grow to the demand seen (cursors count every reservation) and rerun
+    if (cur[0] <= h->hit_cap && cur[1] <= h->chunk_cap) {
+      stats_before[0] = rd[0];
+      stats_before[1] = rd[1];
+      break;
+    }
+    // grow to the demand seen and rerun (counters restored); a batch never needs more than 2^32 hits
+    if (attempt >= 3 || h->hit_cap >= 0xFFFFFFFFull) fail(QVMC_ERR_RUNTIME, "join hit buffers keep overflowing");
+    ck(cudaMemcpy(ctl + 6, stats_before, 2 * sizeof(unsigned long long), cudaMemcpyHostToDevice), "restore stats");
     h->hit_cap = std::max<uint64_t>(h->hit_cap, cur[0] + cur[0] / 4 + 1024);
     h->chunk_cap = std::max<uint64_t>(h->chunk_cap, cur[1] + cur[1] / 4 + 1024);
     int err = 0;
@@ -514,6 +515,7 @@ void run_join_split(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const 
     err &= ~kErrHitOverflow;
     ck(cudaMemcpy(ctl, &err, sizeof(int), cudaMemcpyHostToDevice), "reset overflow");
   }
+  hits_seen += cur[0];
   const uint64_t nc = cur[1];
   if (nc > 0) {
     int per_sm = 0;
@@ -530,9 +532,43 @@ void run_join_split(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const 
   h->timed_k = true;
   const int fgrid = static_cast<int>(std::min<int64_t>((rows + kThreads - 1) / kThreads, grid_for(h, 8)));
   k_finalize_rows<<<std::max(fgrid, 1), kThreads, 0, h->stream>>>(h->s_row_last.as<uint32_t>(), h->s_chunk.as<uint4>(),
-                                                                   h->s_part.as<double2>(), h->s_base.as<double2>(),
-                                                                   rows, eloc);
+                                                                   h->s_part.as<double2>(), h->s_base.as<double2>(), R,
+                                                                   eloc);
   ck_launch("finalize rows");
+}
+
+// Join rows with split evaluation: the search kernel streams each row's hits
+// into chunks, k_eval_chunks evaluates them (its own register budget), and
+// k_finalize_rows sums base + chunks per row in a fixed order. Rows run in
+// batches of at most ~2^31 expected hits (32-bit hit offsets, bounded hit
+// buffers); the buffers grow (and the batch's search reruns) on overflow.
+template <int W>
+void run_join_split(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const RowPlan& P, double2* eloc) {
+  const int64_t rows = R.n_rows;
+  if (rows <= 0) return;
+  constexpr uint64_t kBatchHits = 1ull << 31;
+  const uint64_t per_row = std::max<uint64_t>(h->hits_per_row, 64);
+  const int64_t batch = static_cast<int64_t>(std::max<uint64_t>(1, std::min<uint64_t>(rows, kBatchHits / per_row)));
+  if (h->hit_cap == 0) {
+    h->hit_cap = std::max<uint64_t>(static_cast<uint64_t>(batch) * per_row * 5 / 4, 1u << 16);
+    h->chunk_cap = h->hit_cap / 64 + static_cast<uint64_t>(batch) + 1024;
+  }
+  h->s_row_last.ensure(rows * 4 + 16);
+  h->s_base.ensure(rows * 16 + 16);
+  uint64_t hits_seen = 0;
+  unsigned long long stats_before[2] = {0, 0};
+  ck(cudaMemcpyAsync(stats_before, static_cast<int*>(h->ctl.p) + 6, sizeof(stats_before), cudaMemcpyDeviceToHost,
+                     h->stream),
+     "D2H stats");
+  ck(cudaStreamSynchronize(h->stream), "sync");
+  for (int64_t b0 = 0; b0 < rows; b0 += batch) {
+    RowSet Rb = R;
+    Rb.n_rows = std::min<int64_t>(batch, rows - b0);
+    if (R.list) Rb.list = R.list + b0;
+    else Rb.base = R.base + b0;
+    run_join_split_batch<W>(h, keys, Rb, P, eloc, hits_seen, stats_before);
+  }
+  h->hits_per_row = std::max<uint64_t>(h->hits_per_row, hits_seen / static_cast<uint64_t>(rows) + 1);
 }
 
 // Bucket-centric join (qvmc_bucket.cuh): work items over the deletion-index

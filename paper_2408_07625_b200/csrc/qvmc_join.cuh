@@ -1071,19 +1071,21 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
 }
 
 // Split evaluation, part 3: E_loc = base + the row's chunk sums, newest chunk
-// first (a fixed order: deterministic).
+// first (a fixed order: deterministic). Rows of one batch (RowSet).
 __global__ void k_finalize_rows(const uint32_t* __restrict__ row_last, const uint4* __restrict__ chunk,
-                                const double2* __restrict__ part, const double2* __restrict__ base, int64_t rows,
+                                const double2* __restrict__ part, const double2* __restrict__ base, const RowSet R,
                                 double2* __restrict__ eloc) {
-  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < rows;
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < R.n_rows;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    double2 e = base[r];
-    for (uint32_t c = row_last[r]; c != ~0u; c = __ldg(chunk + c).w) {
+    const int64_t row = R.list ? static_cast<int64_t>(__ldg(R.list + r)) : R.base + r;
+    const int64_t i = (R.perm ? static_cast<int64_t>(__ldg(R.perm + row)) : row) - R.out_base;
+    double2 e = base[i];
+    for (uint32_t c = row_last[i]; c != ~0u; c = __ldg(chunk + c).w) {
       const double2 p = part[c];
       e.x += p.x;
       e.y += p.y;
     }
-    eloc[r] = e;
+    eloc[i] = e;
   }
 }
 
