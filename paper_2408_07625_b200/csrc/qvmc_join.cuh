@@ -426,9 +426,10 @@ __device__ __forceinline__ void kind_b_element(const double* __restrict__ famvi,
 }
 
 // Per-warp state of the join kernel.
-constexpr int kJQueue = 256;
-constexpr int kJDrainAt = kJQueue - 32 * (QVMC_JOIN_UNROLL + 1);  // one step: <= U+1 lookup batches of 32
-constexpr int kJSurv = 128;  // ring of candidates that passed the accept rule and the bitmap
+constexpr int kJQueue = 128;
+constexpr int kJDrainAt = kJQueue - 32;  // checked after every lookup batch (<= 32 hits)
+constexpr int kJSurv = 256;  // ring of candidates that passed the accept rule and the bitmap: >= 31 + 32 U
+static_assert(kJSurv >= 31 + 32 * QVMC_JOIN_UNROLL, "survivor ring too small for the unroll");
 
 struct JoinSmem {
   uint32_t qy[kJQueue];  // hit queue: partner (sorted position), group, flip position key
@@ -704,7 +705,50 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
       off -= len;
       if (++rg < n_ranges) len = sm->r_len[rg];
     }
-    for (;;) {  // one drain call site: inside the walk when the queue fills, and once at its end
+    // the queue becomes E_loc (fused drain) or one chunk of this row (split
+    // evaluation) once it holds `thresh` hits
+    auto emit = [&](unsigned thresh) {
+      if (kEval) {
+        __syncwarp();
+        const unsigned qd = sm->qn, qsn = MODE == kModeHits ? sm->qs : 0u;
+        const unsigned qn = qd + qsn;
+        if (qn >= thresh) {
+          if (MODE == kModeEloc) {
+            const double2 d = join_drain<W>(H, J, sm, lane, s, side);
+            acc.x += d.x;
+            acc.y += d.y;
+          } else {  // split evaluation: the queue becomes one chunk of this row
+            unsigned long long off = 0, cid = 0;
+            if (lane == 0) {
+              off = atomicAdd(O.hit_cursor, static_cast<unsigned long long>(qn));
+              cid = atomicAdd(O.chunk_cursor, 1ull);
+            }
+            off = __shfl_sync(0xffffffffu, off, 0);
+            cid = __shfl_sync(0xffffffffu, cid, 0);
+            if (off + qn <= O.hit_cap && cid < O.chunk_cap) {
+              for (unsigned k = lane; k < qn; k += 32) {
+                const unsigned src = k < qd ? k : kJQueue - 1 - (k - qd);
+                O.hy[off + k] = sm->qy[src];
+                O.hg[off + k] = sm->qg[src];
+                O.hk[off + k] = sm->qk[src];
+              }
+              if (lane == 0)
+                O.chunk[cid] = make_uint4(static_cast<uint32_t>(row), static_cast<uint32_t>(off), qn, prev_chunk);
+              prev_chunk = static_cast<uint32_t>(cid);
+            } else if (lane == 0) {
+              atomicOr(C.err, kErrHitOverflow);  // the host grows the buffers and reruns
+            }
+            __syncwarp();
+            if (lane == 0) {
+              sm->qn = 0;
+              sm->qs = 0;
+            }
+            __syncwarp();
+          }
+        }
+      }
+    };
+    for (;;) {  // the walk: members -> accept rule + bitmap -> survivor ring -> lookups in batches of 32
       const bool walking = __any_sync(0xffffffffu, rg < n_ranges);
       if (walking) {
       constexpr int U = QVMC_JOIN_UNROLL;
@@ -723,6 +767,16 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
           }
         }
       }
+      // doubles-bitmap words of all U members in flight before the accept rule
+      uint32_t dw[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        dw[u] = ~0u;
+        if (J.pbits && v[u] != ~0ull) {
+          const uint32_t bi = sm->dbase[tr[u]] + static_cast<uint32_t>(v[u] >> 48);
+          dw[u] = __ldg(J.pbits + (bi >> 5)) >> (bi & 31);
+        }
+      }
       // accept rule (header comment) -> exact position key of the flip mask
       uint32_t key[U];
 #pragma unroll
@@ -734,7 +788,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
         const bool ea = ya == ta || ya == tb, eb = yb == ta || yb == tb;
         if (!ea && !eb) {  // disjoint pairs: double excitation; merge two sorted pairs
           ++cand;
-          if (J.pbits && !pbit(J.pbits, sm->dbase[tr[u]] + static_cast<uint32_t>(v[u] >> 48))) continue;
+          if (!(dw[u] & 1u)) continue;
           int p0 = ta, p1 = tb, p2 = ya, p3 = yb;
           sort2(p0, p2);
           sort2(p1, p3);
@@ -824,48 +878,11 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
           hits += hit ? 1u : 0u;
         }
         __syncwarp();
-      }
-      if (kEval) {
-        __syncwarp();
-        const unsigned qd = sm->qn, qsn = MODE == kModeHits ? sm->qs : 0u;
-        const unsigned qn = qd + qsn;
-        if (qn >= (walking ? static_cast<unsigned>(kJDrainAt) : 1u)) {
-          if (MODE == kModeEloc) {
-            const double2 d = join_drain<W>(H, J, sm, lane, s, side);
-            acc.x += d.x;
-            acc.y += d.y;
-          } else {  // split evaluation: the queue becomes one chunk of this row
-            unsigned long long off = 0, cid = 0;
-            if (lane == 0) {
-              off = atomicAdd(O.hit_cursor, static_cast<unsigned long long>(qn));
-              cid = atomicAdd(O.chunk_cursor, 1ull);
-            }
-            off = __shfl_sync(0xffffffffu, off, 0);
-            cid = __shfl_sync(0xffffffffu, cid, 0);
-            if (off + qn <= O.hit_cap && cid < O.chunk_cap) {
-              for (unsigned k = lane; k < qn; k += 32) {
-                const unsigned src = k < qd ? k : kJQueue - 1 - (k - qd);
-                O.hy[off + k] = sm->qy[src];
-                O.hg[off + k] = sm->qg[src];
-                O.hk[off + k] = sm->qk[src];
-              }
-              if (lane == 0)
-                O.chunk[cid] = make_uint4(static_cast<uint32_t>(row), static_cast<uint32_t>(off), qn, prev_chunk);
-              prev_chunk = static_cast<uint32_t>(cid);
-            } else if (lane == 0) {
-              atomicOr(C.err, kErrHitOverflow);  // the host grows the buffers and reruns
-            }
-            __syncwarp();
-            if (lane == 0) {
-              sm->qn = 0;
-              sm->qs = 0;
-            }
-            __syncwarp();
-          }
-        }
+        emit(kJDrainAt);
       }
       if (!walking) break;
     }
+    emit(1u);
 
     const Key<W> xrow = row_key<W>(sm);
     // even flip masks of weight >= 6: popcount filter + sample-set probe
