@@ -287,3 +287,29 @@ def test_join_evaluation_modes_agree(cuda_ok, monkeypatch, mode, hit_cap):
     assert abs(got.e_var - ref.e_var) <= 1e-12 * max(1.0, abs(ref.e_var))
     half = q.surrogate_energy(H, b, 5_000, 15_000, check=False)  # a row shard: same rows, same values
     assert np.array_equal(half.locals, got.locals[5_000:15_000])
+
+
+@pytest.mark.parametrize("n_qubits,n_e,n_terms,n_unq,join", [
+    (48, 24, 200_000, 5_000, 0),    # minority set of 24 > 16: sector candidate lists (k_rows), not the join
+    (130, 122, 400_000, 10_000, 1),  # 3 key words, n > 128: join without the pair-existence bitmaps
+    (20, 10, 12_000, 20_000, 1),     # BASELINE config 2 shape (c20), random sector states
+])
+def test_other_row_paths_match_oracle(cuda_ok, n_qubits, n_e, n_terms, n_unq, join):
+    if n_qubits == 20:
+        c, x, y, z = synthetic.jw_terms(20, n_terms, seed=1)
+        H = q.HamiltonianIndex.from_masks(20, c, x, y, z)
+        O = oracle.OracleIndex(20, c, x, y, z)
+        keys = synthetic.random_sector_keys(20, 10, n_unq, seed=2)
+        b = synthetic.sample_batch(keys, seed=3)
+        rep = q.surrogate_energy(H, b)
+        st = q.last_stats(H)
+        rows = np.arange(0, n_unq, 97)
+        want = np.zeros(len(rows), dtype=np.complex128)
+        scale = np.zeros(len(rows))
+        for k, r in enumerate(rows):
+            e, _, s = O.eloc_rows(keys, b.log_amps, b.phases, int(r), int(r) + 1, with_scale=True)
+            want[k], scale[k] = e[0], s[0]
+        assert_eloc_close(rep.locals[rows], want, scale)
+    else:
+        _, rep, st = _synthetic_rows_vs_oracle(n_qubits, n_e, n_terms, n_unq, 64, seed=n_qubits)
+    assert st["join_mode"] == join
