@@ -698,12 +698,23 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
     uint64_t cand = 0;
     uint32_t prev_chunk = ~0u;  // kModeHits: last flushed chunk of this row
     uint32_t s_head = 0, s_tail = 0;  // survivor ring (warp-uniform)
+    // per-lane cursor over the concatenated ranges: member pointer and the
+    // current range's (T_x, bitmap row) in registers, reloaded on a range change
     int rg = 0;
     uint32_t off = lane;
     uint32_t len = sm->r_len[0];
     while (rg < n_ranges && off >= len) {
       off -= len;
       if (++rg < n_ranges) len = sm->r_len[rg];
+    }
+    const uint64_t* mp = nullptr;
+    int c_ta = 0, c_tb = 0;
+    uint32_t c_db = 0;
+    if (rg < n_ranges) {
+      mp = J.mem + sm->r_lo[rg] + off;
+      c_ta = sm->ta[rg];
+      c_tb = sm->tb[rg];
+      c_db = sm->dbase[rg];
     }
     // the queue becomes E_loc (fused drain) or one chunk of this row (split
     // evaluation) once it holds `thresh` hits
@@ -753,17 +764,29 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
       if (walking) {
       constexpr int U = QVMC_JOIN_UNROLL;
       uint64_t v[U];
-      int tr[U];
+      int uta[U], utb[U];
+      uint32_t udb[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         v[u] = ~0ull;
-        tr[u] = rg;
+        uta[u] = c_ta;
+        utb[u] = c_tb;
+        udb[u] = c_db;
         if (rg < n_ranges) {
-          v[u] = __ldg(J.mem + sm->r_lo[rg] + off);
+          v[u] = __ldg(mp);
           off += 32;
-          while (rg < n_ranges && off >= len) {
-            off -= len;
-            if (++rg < n_ranges) len = sm->r_len[rg];
+          mp += 32;
+          if (off >= len) {
+            do {
+              off -= len;
+              if (++rg < n_ranges) len = sm->r_len[rg];
+            } while (rg < n_ranges && off >= len);
+            if (rg < n_ranges) {
+              mp = J.mem + sm->r_lo[rg] + off;
+              c_ta = sm->ta[rg];
+              c_tb = sm->tb[rg];
+              c_db = sm->dbase[rg];
+            }
           }
         }
       }
@@ -773,7 +796,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
       for (int u = 0; u < U; ++u) {
         dw[u] = ~0u;
         if (J.pbits && v[u] != ~0ull) {
-          const uint32_t bi = sm->dbase[tr[u]] + static_cast<uint32_t>(v[u] >> 48);
+          const uint32_t bi = udb[u] + static_cast<uint32_t>(v[u] >> 48);
           dw[u] = __ldg(J.pbits + (bi >> 5)) >> (bi & 31);
         }
       }
@@ -784,7 +807,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
         key[u] = kNoKey;
         if (v[u] == ~0ull) continue;
         const int ya = static_cast<int>(v[u] >> 32) & 0xFF, yb = static_cast<int>(v[u] >> 40) & 0xFF;
-        const int ta = sm->ta[tr[u]], tb = sm->tb[tr[u]];
+        const int ta = uta[u], tb = utb[u];
         const bool ea = ya == ta || ya == tb, eb = yb == ta || yb == tb;
         if (!ea && !eb) {  // disjoint pairs: double excitation; merge two sorted pairs
           ++cand;
