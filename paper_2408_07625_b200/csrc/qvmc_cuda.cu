@@ -136,7 +136,7 @@ struct qvmc_ham_s {
   bool use_join = true;
   int join_mode = 1;  // 0 fused row kernel, 1 row search + chunk eval (measured best), 2 bucket-centric search + row eval
   // split-evaluation workspace
-  DBuf s_hy, s_hg, s_hk, s_chunk, s_row_last, s_base, s_part, s_head, b_icnt, b_iincl, b_items;
+  DBuf s_hy, s_hg, s_hk, s_chunk, s_row_last, s_base, s_part, s_head, b_icnt, b_iincl, b_items, s_rowpos;
   uint64_t hit_cap = 0, chunk_cap = 0;
   uint64_t hits_per_row = 320;  // split evaluation: running estimate that sizes the row batches
   // workspace
@@ -488,6 +488,7 @@ void run_join_split_batch(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, 
     O.chunk_cursor = reinterpret_cast<unsigned long long*>(ctl + 12);
     O.hit_cap = h->hit_cap;
     O.chunk_cap = h->chunk_cap;
+    O.rowpos = h->s_rowpos.as<uint8_t>();
     int per_sm = 0;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_join<W, kModeHits>, kThreads, 0), "occupancy");
     const int64_t blocks_needed = (rows + kWarps - 1) / kWarps;
@@ -525,7 +526,7 @@ void run_join_split_batch(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, 
     k_eval_chunks<W><<<grid, kThreads, 0, h->stream>>>(
         h->view, join_view(h, P), keys, h->s_chunk.as<uint4>(), reinterpret_cast<unsigned long long*>(ctl + 12),
         h->s_hy.as<uint32_t>(), h->s_hg.as<uint32_t>(), h->s_hk.as<uint32_t>(), P.side, P.s, ctl + 14,
-        h->s_part.as<double2>());
+        h->s_rowpos.as<uint8_t>(), h->s_part.as<double2>());
     ck_launch("eval chunks");
   }
   ck(cudaEventRecord(h->ev_k[2], h->stream), "event");
@@ -543,7 +544,8 @@ void run_join_split_batch(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, 
 // batches of at most ~2^31 expected hits (32-bit hit offsets, bounded hit
 // buffers); the buffers grow (and the batch's search reruns) on overflow.
 template <int W>
-void run_join_split(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const RowPlan& P, double2* eloc) {
+void run_join_split(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, const RowSet& R, const RowPlan& P,
+                    double2* eloc) {
   const int64_t rows = R.n_rows;
   if (rows <= 0) return;
   constexpr uint64_t kBatchHits = 1ull << 31;
@@ -555,6 +557,7 @@ void run_join_split(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const 
   }
   h->s_row_last.ensure(rows * 4 + 16);
   h->s_base.ensure(rows * 16 + 16);
+  h->s_rowpos.ensure(static_cast<size_t>(n_all) * 16 + 16);
   uint64_t hits_seen = 0;
   unsigned long long stats_before[2] = {0, 0};
   ck(cudaMemcpyAsync(stats_before, static_cast<int*>(h->ctl.p) + 6, sizeof(stats_before), cudaMemcpyDeviceToHost,
@@ -1332,7 +1335,7 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       if (P.join && h->join_mode == 2) {
         DISPATCH_W(W, (run_join_bucket<WW>(h, rkeys, n_unq, R, P, row_begin, row_end, deloc)));
       } else if (P.join && h->join_mode == 1) {
-        DISPATCH_W(W, (run_join_split<WW>(h, rkeys, R, P, deloc)));
+        DISPATCH_W(W, (run_join_split<WW>(h, rkeys, n_unq, R, P, deloc)));
       } else if (P.join) {
         DISPATCH_W(W, (launch_rows_join<WW, kModeEloc>(h, rkeys, R, P, O)));
       } else {

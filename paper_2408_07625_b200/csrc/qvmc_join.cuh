@@ -677,7 +677,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
       }
       c += pc;
     }
-    if (lane < s) sm->pos[lane] = static_cast<uint16_t>(pos);
+    if (lane < s) {
+      sm->pos[lane] = static_cast<uint16_t>(pos);
+      if (MODE == kModeHits) O.rowpos[row * 16 + lane] = static_cast<uint8_t>(pos);
+    }
     __syncwarp();
     const int pos0 = sm->pos[0], pos1 = sm->pos[1];
     // bucket t of this row: pair (a, b) of S(x), range from the index
@@ -1040,7 +1043,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
                   const uint64_t* __restrict__ keys, const uint4* __restrict__ chunk,
                   const unsigned long long* __restrict__ n_chunks, const uint32_t* __restrict__ hy,
                   const uint32_t* __restrict__ hg, const uint32_t* __restrict__ hk, int side, int s,
-                  const int* __restrict__ exp_flag, double2* __restrict__ part) {
+                  const int* __restrict__ exp_flag, const uint8_t* __restrict__ rowpos, double2* __restrict__ part) {
   constexpr int DH = QVMC_EVAL_HITS;
   __shared__ uint16_t s_pos[kWarps][32];
   const int lane = threadIdx.x & 31;
@@ -1060,22 +1063,9 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
     const double2 cs_i = make_double2(__longlong_as_double(static_cast<long long>(sr.b)),
                                       __longlong_as_double(static_cast<long long>(sr.c)));
     const double inv_ai = mag ? 1.0 / __longlong_as_double(static_cast<long long>(sr.d)) : 0.0;
-    // minority orbitals of the row (kind B elements)
-    int pos = 0, cnt = 0;
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-      uint64_t v = side ? xrow.w[w] : ~xrow.w[w];
-      const int hi_bit = n - 64 * w;
-      if (hi_bit < 64) v &= (hi_bit <= 0) ? 0ull : ((1ull << hi_bit) - 1);
-      const int pc = __popcll(v);
-      if (lane >= cnt && lane < cnt + pc) {
-        for (int k = 0; k < lane - cnt; ++k) v &= v - 1;
-        pos = 64 * w + __ffsll(static_cast<long long>(v)) - 1;
-      }
-      cnt += pc;
-    }
+    // minority orbitals of the row (kind B elements), as the search kernel listed them
     __syncwarp();
-    if (lane < s) spos[lane] = static_cast<uint16_t>(pos);
+    if (lane < s) spos[lane] = __ldg(rowpos + row * 16 + lane);
     __syncwarp();
     double2 acc = make_double2(0.0, 0.0);
     const unsigned n_hits = ch.z;

@@ -256,6 +256,7 @@ struct RowOut {
   unsigned long long* chunk_cursor;
   uint64_t hit_cap;
   uint64_t chunk_cap;
+  uint8_t* rowpos;            // [key position][16] the row's minority orbitals (for the chunk evaluation)
 };
 
 __global__ void k_cos_sin(const double* __restrict__ ph, int64_t n, double2* cs) {
