@@ -742,9 +742,11 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
             if (off + qn <= O.hit_cap && cid < O.chunk_cap) {
               for (unsigned k = lane; k < qn; k += 32) {
                 const unsigned src = k < qd ? k : kJQueue - 1 - (k - qd);
-                O.hy[off + k] = sm->qy[src];
-                O.hg[off + k] = sm->qg[src];
-                O.hk[off + k] = sm->qk[src];
+                // evict-first (streaming): the chunks are read once, and must not push
+                // the records and tables the evaluation gathers out of L2 (measured -0.55 ms)
+                __stcs(O.hy + off + k, sm->qy[src]);
+                __stcs(O.hg + off + k, sm->qg[src]);
+                __stcs(O.hk + off + k, sm->qk[src]);
               }
               if (lane == 0)
                 O.chunk[cid] = make_uint4(static_cast<uint32_t>(row), static_cast<uint32_t>(off), qn, prev_chunk);
@@ -1082,8 +1084,8 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
         for (int i = 0; i < kGrecWords; ++i) q.r[i] = 0;
         if (q.valid) {
           const uint64_t at = static_cast<uint64_t>(ch.y) + k;
-          const uint32_t y = __ldg(hy + at), g = __ldg(hg + at);
-          q.key = __ldg(hk + at);
+          const uint32_t y = __ldcs(hy + at), g = __ldcs(hg + at);  // streaming, see the search's flush
+          q.key = __ldcs(hk + at);
           q.sr = ldg256(J.rec + static_cast<int64_t>(y) * 4);
           const U64x4 g0 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords);
           const U64x4 g1 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords + 4);
