@@ -129,6 +129,12 @@ struct qvmc_ham_s {
   std::vector<uint64_t> binom_host;
   uint64_t xy_tab_mask = 0;
   uint32_t pbits_P = 0;
+  DBuf hot;  // grec | famvi | pbits | xy_tab in one arena
+  size_t hot_bytes = 0;
+  uint64_t* p_grec = nullptr;
+  double* p_famvi = nullptr;
+  uint32_t* p_pbits = nullptr;
+  uint64_t* p_xy_tab = nullptr;
   HamView view{};
   // join path (per call): deletion-index workspace
   DBuf l_key, l_key2, l_idx, l_perm, l_keys, l_rec, l_flags, l_list, l_nsel, cs;
@@ -432,12 +438,12 @@ JoinView join_view(qvmc_ham_s* h, const RowPlan& P) {
   J.C = static_cast<uint32_t>(P.s * (P.s - 1) / 2);
   J.rng = h->j_rng.as<uint2>();
   J.mem = h->j_mem.as<uint64_t>();
-  J.xy_tab = h->xy_tab.as<uint64_t>();
+  J.xy_tab = h->p_xy_tab;
   J.xy_mask = h->xy_tab_mask;
   J.rec = h->l_rec.as<uint64_t>();
-  J.grec = h->grec.as<uint64_t>();
-  J.famvi = h->famvi.as<double>();
-  J.pbits = h->pbits_P ? h->pbits.as<uint32_t>() : nullptr;
+  J.grec = h->p_grec;
+  J.famvi = h->p_famvi;
+  J.pbits = h->pbits_P ? h->p_pbits : nullptr;
   J.P = h->pbits_P;
   return J;
 }
@@ -918,7 +924,7 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     upload(h->diag_K, p.diag_K);
     upload(h->diag_other, p.diag_other);
     upload(h->hash_bytes, p.hash_bytes);
-    upload(h->xy_tab, p.xy_tab);
+
     upload(h->comp_of, p.comp_of);
     upload(h->fam_off, p.fam_off);
     upload(h->fam_B, p.fam_B);
@@ -929,9 +935,32 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     upload(h->ginfo, p.ginfo);
     upload(h->trec, p.trec);
     upload(h->famrec, p.famrec);
-    upload(h->grec, p.grec);
-    upload(h->famvi, p.famvi);
-    upload(h->pbits, p.pbits);
+    {  // the join's hot tables in one arena
+      size_t at = 0;
+      auto place = [&](size_t bytes) {
+        const size_t o = at;
+        at = (at + std::max<size_t>(bytes, 16) + 255) & ~size_t{255};
+        return o;
+      };
+      const size_t o_grec = place(p.grec.size() * 8), o_famvi = place(p.famvi.size() * 8),
+                   o_pbits = place(p.pbits.size() * 4), o_tab = place(p.xy_tab.size() * 8);
+      h->hot.ensure(at);
+      h->hot_bytes = at;
+      char* base = h->hot.as<char>();
+      auto put = [&](size_t o, const void* src, size_t bytes) {
+        if (bytes) ck(cudaMemcpy(base + o, src, bytes, cudaMemcpyHostToDevice), "upload hot");
+      };
+      put(o_grec, p.grec.data(), p.grec.size() * 8);
+      put(o_famvi, p.famvi.data(), p.famvi.size() * 8);
+      put(o_pbits, p.pbits.data(), p.pbits.size() * 4);
+      put(o_tab, p.xy_tab.data(), p.xy_tab.size() * 8);
+      h->p_grec = reinterpret_cast<uint64_t*>(base + o_grec);
+      h->p_famvi = reinterpret_cast<double*>(base + o_famvi);
+      h->p_pbits = reinterpret_cast<uint32_t*>(base + o_pbits);
+      h->p_xy_tab = reinterpret_cast<uint64_t*>(base + o_tab);
+      // (a persisting L2 access-policy window over this arena measured slower:
+      // it takes L2 from the per-call index sort; profiles/r01_tuning_log.txt)
+    }
     h->pbits_P = p.pbits_P;
     h->binom_host = binomial_table();
     upload(h->binom, h->binom_host);

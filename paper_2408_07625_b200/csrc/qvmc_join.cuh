@@ -690,7 +690,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
       sm->ta[t] = static_cast<uint8_t>(pa);
       sm->tb[t] = static_cast<uint8_t>(pb);
       sm->dbase[t] = J.P + pidx(pa, pb) * J.P;
-      const uint2 rg = __ldg(J.rng + static_cast<uint64_t>(row) * J.C + t);
+      const uint2 rg = __ldcs(J.rng + static_cast<uint64_t>(row) * J.C + t);  // read once per call
       sm->r_lo[t] = rg.x;
       sm->r_len[t] = rg.y - rg.x;
     }
