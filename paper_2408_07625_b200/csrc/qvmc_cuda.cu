@@ -384,8 +384,8 @@ void build_join_index_k(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const Ro
   const uint64_t E = static_cast<uint64_t>(n) * C;
   h->j_key.ensure(E * sizeof(K) + 16);
   h->j_key2.ensure(E * sizeof(K) + 16);
-  h->j_val.ensure(E * 8 + 16);
-  h->j_val2.ensure(E * 8 + 16);
+  h->j_val.ensure(E * 4 + 16);
+  h->j_val2.ensure(E * 4 + 16);
   h->j_head.ensure(E * 4 + 16);
   h->j_rid.ensure(E * 4 + 16);
   h->j_lo.ensure(E * 4 + 16);
@@ -395,18 +395,18 @@ void build_join_index_k(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const Ro
   if (P.want_pos_of) h->j_pos_of.ensure(E * 4 + 16);
   const int grid = static_cast<int>(std::min<int64_t>((n + kWarps - 1) / kWarps, grid_for(h, 8)));
   k_join_keys<W, K><<<std::max(grid, 1), kThreads, 0, h->stream>>>(keys, n, h->n, P.side, P.s, h->binom.as<uint64_t>(),
-                                                                   h->j_key.as<K>(), h->j_val.as<uint64_t>());
+                                                                   h->j_key.as<K>(), h->j_val.as<uint32_t>());
   ck_launch("join keys");
   const int ne = static_cast<int>(E);
   size_t b1 = 0, b2 = 0;
-  ck(cub::DeviceRadixSort::SortPairs(nullptr, b1, h->j_key.as<K>(), h->j_key2.as<K>(), h->j_val.as<uint64_t>(),
-                                     h->j_val2.as<uint64_t>(), ne, 0, P.key_bits, h->stream),
+  ck(cub::DeviceRadixSort::SortPairs(nullptr, b1, h->j_key.as<K>(), h->j_key2.as<K>(), h->j_val.as<uint32_t>(),
+                                     h->j_val2.as<uint32_t>(), ne, 0, P.key_bits, h->stream),
      "sort size");
   ck(cub::DeviceScan::InclusiveSum(nullptr, b2, h->j_head.as<uint32_t>(), h->j_rid.as<uint32_t>(), ne, h->stream),
      "scan size");
   h->j_tmp.ensure(std::max(b1, b2) + 16);
-  ck(cub::DeviceRadixSort::SortPairs(h->j_tmp.p, b1, h->j_key.as<K>(), h->j_key2.as<K>(), h->j_val.as<uint64_t>(),
-                                     h->j_val2.as<uint64_t>(), ne, 0, P.key_bits, h->stream),
+  ck(cub::DeviceRadixSort::SortPairs(h->j_tmp.p, b1, h->j_key.as<K>(), h->j_key2.as<K>(), h->j_val.as<uint32_t>(),
+                                     h->j_val2.as<uint32_t>(), ne, 0, P.key_bits, h->stream),
      "sort");
   ++g_launches;
   const int egrid = static_cast<int>(std::min<uint64_t>((E + kThreads - 1) / kThreads, grid_for(h, 16)));
@@ -418,8 +418,9 @@ void build_join_index_k(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const Ro
   k_run_bounds<<<std::max(egrid, 1), kThreads, 0, h->stream>>>(h->j_rid.as<uint32_t>(), E, h->j_lo.as<uint32_t>(),
                                                                 h->j_hi.as<uint32_t>());
   ck_launch("run bounds");
-  k_join_fill<<<std::max(egrid, 1), kThreads, 0, h->stream>>>(h->j_val2.as<uint64_t>(), h->j_rid.as<uint32_t>(), E,
+  k_join_fill<W><<<std::max(egrid, 1), kThreads, 0, h->stream>>>(h->j_val2.as<uint32_t>(), h->j_rid.as<uint32_t>(), E,
                                                                C, h->j_lo.as<uint32_t>(), h->j_hi.as<uint32_t>(),
+                                                               keys, h->n, P.side,
                                                                h->j_mem.as<uint64_t>(), h->j_rng.as<uint2>(),
                                                                P.want_pos_of ? h->j_pos_of.as<uint32_t>() : nullptr);
   ck_launch("join fill");

@@ -175,7 +175,7 @@ __global__ void k_flag_rows(const uint32_t* __restrict__ perm, int64_t n, int64_
 template <int W, typename K>
 __global__ void __launch_bounds__(kThreads)
     k_join_keys(const uint64_t* __restrict__ keys, int64_t n, int n_qubits, int side, int s,
-                const uint64_t* __restrict__ binom, K* __restrict__ bkey, uint64_t* __restrict__ bval) {
+                const uint64_t* __restrict__ binom, K* __restrict__ bkey, uint32_t* __restrict__ bval) {
   const uint32_t C = static_cast<uint32_t>(s * (s - 1) / 2);
   const int lane = threadIdx.x & 31;
   const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -220,13 +220,12 @@ __global__ void __launch_bounds__(kThreads)
       const uint64_t P1a1 = __shfl_sync(0xffffffffu, i1, a);
       const uint64_t P1b = __shfl_sync(0xffffffffu, e1, b);
       const uint64_t P2b1 = __shfl_sync(0xffffffffu, i2, b);
-      const int pa = __shfl_sync(0xffffffffu, pos, a), pb = __shfl_sync(0xffffffffu, pos, b);
+
       if (valid) {
         const uint64_t rank = P0a + (P1b - P1a1) + (total2 - P2b1);
         const uint64_t at = static_cast<uint64_t>(y) * C + t;
         bkey[at] = static_cast<K>(rank);
-        bval[at] = static_cast<uint64_t>(y) | static_cast<uint64_t>(pa) << 32 | static_cast<uint64_t>(pb) << 40 |
-                   static_cast<uint64_t>(t) << 48;
+        bval[at] = static_cast<uint32_t>(at);  // entry id y*C + t (32 bits: sorts as a 4-byte value)
       }
     }
   }
@@ -249,18 +248,49 @@ __global__ void k_run_bounds(const uint32_t* __restrict__ rid, uint64_t E, uint3
 }
 
 // member array + per-(sample, pair) bucket range
-// (pos_of, optional: the member position of every (sample, pair) entry)
-__global__ void k_join_fill(const uint64_t* __restrict__ val, const uint32_t* __restrict__ rid, uint64_t E, uint32_t C,
+// k-th (0-based) set bit of a W-word mask
+template <int W>
+__device__ __forceinline__ int select_bit(const uint64_t* v, int k) {
+  int base = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const int pc = __popcll(v[w]);
+    if (k < pc) {
+      const uint32_t lo = static_cast<uint32_t>(v[w]), hi = static_cast<uint32_t>(v[w] >> 32);
+      const int pl = __popc(lo);
+      return base + (k < pl ? static_cast<int>(__fns(lo, 0, k + 1)) : 32 + static_cast<int>(__fns(hi, 0, k - pl + 1)));
+    }
+    k -= pc;
+    base += 64;
+  }
+  return -1;
+}
+
+// Member array + per-(sample, pair) bucket range (+ pos_of, optional: the
+// member position of every (sample, pair) entry). The sort carried only the
+// entry id y*C + t; the pair's orbitals come from y's key.
+template <int W>
+__global__ void k_join_fill(const uint32_t* __restrict__ val, const uint32_t* __restrict__ rid, uint64_t E, uint32_t C,
                             const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi,
-                            uint64_t* __restrict__ mem, uint2* __restrict__ rng, uint32_t* __restrict__ pos_of) {
+                            const uint64_t* __restrict__ keys, int n_qubits, int side, uint64_t* __restrict__ mem,
+                            uint2* __restrict__ rng, uint32_t* __restrict__ pos_of) {
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < E; p += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t v = val[p];
+    const uint32_t e = val[p];
     const uint32_t r = rid[p] - 1;
-    const uint64_t y = v & 0xFFFFFFFFull, t = v >> 48;
-    rng[y * C + t] = make_uint2(lo[r], hi[r]);
-    if (pos_of) pos_of[y * C + t] = static_cast<uint32_t>(p);
-    const uint32_t a = static_cast<uint32_t>(v >> 32) & 0xFF, b = static_cast<uint32_t>(v >> 40) & 0xFF;
-    mem[p] = (v & 0x0000FFFFFFFFFFFFull) | static_cast<uint64_t>(b * (b - 1) / 2 + a) << 48;
+    const uint32_t y = e / C, t = e - y * C;
+    rng[e] = make_uint2(lo[r], hi[r]);
+    if (pos_of) pos_of[e] = static_cast<uint32_t>(p);
+    uint64_t S[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      S[w] = side ? __ldg(keys + static_cast<uint64_t>(y) * W + w) : ~__ldg(keys + static_cast<uint64_t>(y) * W + w);
+      const int hi_bit = n_qubits - 64 * w;
+      if (hi_bit < 64) S[w] &= (hi_bit <= 0) ? 0ull : ((1ull << hi_bit) - 1);
+    }
+    const int b = static_cast<int>(pair_b(static_cast<int>(t))), a = static_cast<int>(t) - b * (b - 1) / 2;
+    const uint32_t pa = static_cast<uint32_t>(select_bit<W>(S, a)), pb = static_cast<uint32_t>(select_bit<W>(S, b));
+    mem[p] = static_cast<uint64_t>(y) | static_cast<uint64_t>(pa) << 32 | static_cast<uint64_t>(pb) << 40 |
+             static_cast<uint64_t>(pb * (pb - 1) / 2 + pa) << 48;
   }
 }
 
