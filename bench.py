@@ -358,13 +358,15 @@ def main():
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("hbm_gbs", 6650.0)
     # DRAM traffic of the same kernels from one `ncu --set full` capture each (profiles/ncu_traffic.json)
-    traffic, traffic_src = None, None
+    traffic, traffic_src, issue = None, None, None
     tj = ROOT / "profiles" / "ncu_traffic.json"
     if tj.exists() and args.n_unq is None:
         t = json.loads(tj.read_text()).get(args.config, {})
         if "search" in t and "eval" in t:
             traffic = t["search"]["dram_bytes"] + t["eval"]["dram_bytes"]
             traffic_src = f"profiles/ncu_traffic.json ({t['search']['report']}, {t['eval']['report']})"
+            # the binding resource: issue slots (ncu smsp__issue_active, per kernel)
+            issue = {k: t[k].get("issue_active_pct", 0.0) / 100.0 for k in ("search", "eval")}
 
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -383,7 +385,8 @@ def main():
                      "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / statistics.mean(step_ms),
                      "search_ms": statistics.mean(search_ms), "eval_ms": statistics.mean(eval_ms),
                      "bytes_per_sample": b_alg,
-                     "note": "integer/L2-latency bound, not HBM: see DESIGN.md section 4 and profiles/",
+                     "issue_slot_frac_ncu": issue,
+                     "note": "integer-issue / L2-latency bound, not HBM: see DESIGN.md section 4.6 and profiles/",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),

@@ -25,8 +25,15 @@ def metrics(rep):
     wr, wu = get("dram__bytes_write.sum")
     du, dun = get("gpu__time_duration.sum")
     l2, _ = get("lts__t_sectors_srcunit_tex_op_read.sum")
-    return {"kernel": vals[names.index("Kernel Name")], "dram_bytes": rd * SCALE[ru] + wr * SCALE[wu],
-            "duration_ms": du * TSCALE[dun], "l2_read_sectors": l2}
+    out = {"kernel": vals[names.index("Kernel Name")], "dram_bytes": rd * SCALE[ru] + wr * SCALE[wu],
+           "duration_ms": du * TSCALE[dun], "l2_read_sectors": l2}
+    for key, metric in (("issue_active_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                        ("inst_executed", "smsp__inst_executed.sum"),
+                        ("alu_pipe_pct", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                        ("l2_throughput_pct", "lts__t_sectors.avg.pct_of_peak_sustained_elapsed")):
+        if metric in names:
+            out[key] = get(metric)[0]
+    return out
 
 
 def main(cfg, specs):
