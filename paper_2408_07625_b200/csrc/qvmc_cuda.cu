@@ -145,6 +145,15 @@ struct qvmc_ham_s {
   DBuf s_hy, s_hg, s_hk, s_chunk, s_row_last, s_base, s_part, s_head, b_icnt, b_iincl, b_items, s_rowpos;
   uint64_t hit_cap = 0, chunk_cap = 0;
   uint64_t hits_per_row = 320;  // split evaluation: running estimate that sizes the row batches
+  // pipelined split evaluation (run_join_pipelined)
+  DBuf p_hy[2], p_hg[2], p_hk[2], p_chunk[2], p_part[2];
+  uint64_t p_hit_cap = 0, p_chunk_cap = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_p[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  unsigned long long* log_host = nullptr;
+  uint64_t log_cap = 0;
+  int pipe_batches = 2, pipe_search_blocks = 0, pipe_eval_blocks = 0;  // measured: 2-3 batches best
+  bool pipelined = true;
   // workspace
   DBuf tab, ctl, keys, la, ph, lp, eloc, partials, moments, weights;
   DBuf counts, row_off, xp_a, g_a, xp_b, g_b, entries, cub_tmp, in_entries, out_h, out_class;
@@ -533,7 +542,7 @@ void run_join_split_batch(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, 
     k_eval_chunks<W><<<grid, kThreads, 0, h->stream>>>(
         h->view, join_view(h, P), keys, h->s_chunk.as<uint4>(), reinterpret_cast<unsigned long long*>(ctl + 12),
         h->s_hy.as<uint32_t>(), h->s_hg.as<uint32_t>(), h->s_hk.as<uint32_t>(), P.side, P.s, ctl + 14,
-        h->s_rowpos.as<uint8_t>(), h->s_part.as<double2>());
+        h->s_rowpos.as<uint8_t>(), h->s_part.as<double2>(), h->chunk_cap);
     ck_launch("eval chunks");
   }
   ck(cudaEventRecord(h->ev_k[2], h->stream), "event");
@@ -579,6 +588,131 @@ void run_join_split(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, const Ro
     run_join_split_batch<W>(h, keys, Rb, P, eloc, hits_seen, stats_before);
   }
   h->hits_per_row = std::max<uint64_t>(h->hits_per_row, hits_seen / static_cast<uint64_t>(rows) + 1);
+}
+
+// Pipelined split evaluation: rows in NB batches, the search of batch b+1
+// (stream A) overlaps the evaluation of batch b (stream B), two buffer sets in
+// turn. The search is issue-bound and the evaluation latency-bound, so the
+// two fill each other's idle issue slots when they share SMs. Overflow of a
+// batch's buffers is detected after the last batch (no mid-call sync); the
+// whole pipeline then reruns with larger buffers.
+template <int W>
+void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, const RowSet& R, const RowPlan& P,
+                        double2* eloc) {
+  const int64_t rows = R.n_rows;
+  if (rows <= 0) return;
+  constexpr uint64_t kBatchHits = 1ull << 31;
+  const uint64_t per_row = std::max<uint64_t>(h->hits_per_row, 64);
+  const int64_t nb_min = static_cast<int64_t>((static_cast<uint64_t>(rows) * per_row + kBatchHits - 1) / kBatchHits);
+  const int64_t NB = std::min<int64_t>(rows, std::max<int64_t>(h->pipe_batches, nb_min));
+  const int64_t batch = (rows + NB - 1) / NB;
+  if (h->p_hit_cap == 0) {
+    h->p_hit_cap = std::min<uint64_t>(static_cast<uint64_t>(batch) * per_row * 5 / 4 + (1u << 16), 0xFFFFFFFFull);
+    h->p_chunk_cap = h->p_hit_cap / 32 + static_cast<uint64_t>(batch) + 1024;
+  }
+  h->s_row_last.ensure(rows * 4 + 16);
+  h->s_base.ensure(rows * 16 + 16);
+  h->s_rowpos.ensure(static_cast<size_t>(n_all) * 16 + 16);
+  if (!h->side) {
+    ck(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking), "stream create");
+    for (auto& e : h->ev_p) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+  }
+  if (static_cast<int64_t>(h->log_cap) < NB) {
+    if (h->log_host) cudaFreeHost(h->log_host);
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h->log_host), NB * 2 * sizeof(unsigned long long), cudaHostAllocDefault),
+       "pinned log");
+    h->log_cap = static_cast<uint64_t>(NB);
+  }
+  int* ctl = static_cast<int*>(h->ctl.p);
+  cudaStream_t A = h->stream, B = h->side;
+  cudaEvent_t ev_start = h->ev_p[0], ev_join = h->ev_p[1], ev_s[2] = {h->ev_p[2], h->ev_p[3]},
+              ev_e[2] = {h->ev_p[4], h->ev_p[5]};
+  for (int attempt = 0;; ++attempt) {
+    for (int k = 0; k < 2; ++k) {
+      h->p_hy[k].ensure(h->p_hit_cap * 4 + 16);
+      h->p_hg[k].ensure(h->p_hit_cap * 4 + 16);
+      h->p_hk[k].ensure(h->p_hit_cap * 4 + 16);
+      h->p_chunk[k].ensure(h->p_chunk_cap * 16 + 16);
+      h->p_part[k].ensure(h->p_chunk_cap * 16 + 16);
+    }
+    int per_sm_s = 0, per_sm_e = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, k_rows_join<W, kModeHits>, kThreads, 0), "occupancy");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_e, k_eval_chunks<W>, kThreads, 0), "occupancy");
+    if (h->pipe_search_blocks > 0) per_sm_s = std::min(per_sm_s, h->pipe_search_blocks);
+    if (h->pipe_eval_blocks > 0) per_sm_e = std::min(per_sm_e, h->pipe_eval_blocks);
+    ck(cudaEventRecord(ev_start, A), "event");
+    ck(cudaStreamWaitEvent(B, ev_start, 0), "wait");
+    TableView T{h->tab.as<uint64_t>(), h->tab_buckets - 1};
+    for (int64_t b = 0; b < NB; ++b) {
+      const int k = static_cast<int>(b & 1);
+      RowSet Rb = R;
+      Rb.n_rows = std::min<int64_t>(batch, rows - b * batch);
+      if (Rb.n_rows <= 0) {
+        h->log_host[2 * b] = h->log_host[2 * b + 1] = 0;
+        continue;
+      }
+      if (R.list) Rb.list = R.list + b * batch;
+      else Rb.base = R.base + b * batch;
+      int* cur = ctl + 16 + 4 * k;  // this set's hit / chunk cursors (u64 each)
+      if (b >= 2) ck(cudaStreamWaitEvent(A, ev_e[k], 0), "wait");
+      ck(cudaMemsetAsync(ctl + 4, 0, 2 * sizeof(int), A), "memset row counter");
+      ck(cudaMemsetAsync(cur, 0, 4 * sizeof(int), A), "memset cursors");
+      RowOut O{};
+      O.hy = h->p_hy[k].as<uint32_t>();
+      O.hg = h->p_hg[k].as<uint32_t>();
+      O.hk = h->p_hk[k].as<uint32_t>();
+      O.chunk = h->p_chunk[k].as<uint4>();
+      O.row_last = h->s_row_last.as<uint32_t>();
+      O.base = h->s_base.as<double2>();
+      O.hit_cursor = reinterpret_cast<unsigned long long*>(cur);
+      O.chunk_cursor = reinterpret_cast<unsigned long long*>(cur + 2);
+      O.hit_cap = h->p_hit_cap;
+      O.chunk_cap = h->p_chunk_cap;
+      O.rowpos = h->s_rowpos.as<uint8_t>();
+      const int grid_s = static_cast<int>(
+          std::max<int64_t>(1, std::min<int64_t>((Rb.n_rows + kWarps - 1) / kWarps, grid_for(h, per_sm_s))));
+      k_rows_join<W, kModeHits><<<grid_s, kThreads, 0, A>>>(h->view, T, join_view(h, P), keys, Rb, P.side, P.s,
+                                                            ctl_view(h), O);
+      ck_launch("row kernel (join search)");
+      ck(cudaMemcpyAsync(h->log_host + 2 * b, cur, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, A),
+         "D2H cursors");
+      ck(cudaEventRecord(ev_s[k], A), "event");
+      ck(cudaStreamWaitEvent(B, ev_s[k], 0), "wait");
+      k_eval_chunks<W><<<grid_for(h, per_sm_e), kThreads, 0, B>>>(
+          h->view, join_view(h, P), keys, h->p_chunk[k].as<uint4>(), reinterpret_cast<unsigned long long*>(cur + 2),
+          h->p_hy[k].as<uint32_t>(), h->p_hg[k].as<uint32_t>(), h->p_hk[k].as<uint32_t>(), P.side, P.s, ctl + 14,
+          h->s_rowpos.as<uint8_t>(), h->p_part[k].as<double2>(), h->p_chunk_cap);
+      ck_launch("eval chunks");
+      const int fgrid = static_cast<int>(std::min<int64_t>((Rb.n_rows + kThreads - 1) / kThreads, grid_for(h, 8)));
+      k_finalize_rows<<<std::max(fgrid, 1), kThreads, 0, B>>>(h->s_row_last.as<uint32_t>(), h->p_chunk[k].as<uint4>(),
+                                                              h->p_part[k].as<double2>(), h->s_base.as<double2>(), Rb,
+                                                              eloc);
+      ck_launch("finalize rows");
+      ck(cudaEventRecord(ev_e[k], B), "event");
+    }
+    ck(cudaEventRecord(ev_join, B), "event");
+    ck(cudaStreamWaitEvent(A, ev_join, 0), "wait");
+    ck(cudaStreamSynchronize(A), "sync");
+    uint64_t need_h = 0, need_c = 0, hits = 0;
+    for (int64_t b = 0; b < NB; ++b) {
+      need_h = std::max<uint64_t>(need_h, h->log_host[2 * b]);
+      need_c = std::max<uint64_t>(need_c, h->log_host[2 * b + 1]);
+      hits += h->log_host[2 * b];
+    }
+    h->timed_k = false;
+    if (need_h <= h->p_hit_cap && need_c <= h->p_chunk_cap) {
+      h->hits_per_row = std::max<uint64_t>(h->hits_per_row, hits / static_cast<uint64_t>(rows) + 1);
+      break;
+    }
+    if (attempt >= 3 || h->p_hit_cap >= 0xFFFFFFFFull) fail(QVMC_ERR_RUNTIME, "join hit buffers keep overflowing");
+    h->p_hit_cap = std::min<uint64_t>(std::max<uint64_t>(h->p_hit_cap, need_h + need_h / 4 + 1024), 0xFFFFFFFFull);
+    h->p_chunk_cap = std::max<uint64_t>(h->p_chunk_cap, need_c + need_c / 4 + 1024);
+    int err = 0;  // rerun from scratch: counters of the overflowed attempt dropped
+    ck(cudaMemcpy(&err, ctl, sizeof(int), cudaMemcpyDeviceToHost), "read err");
+    err &= ~kErrHitOverflow;
+    ck(cudaMemcpy(ctl, &err, sizeof(int), cudaMemcpyHostToDevice), "reset overflow");
+    ck(cudaMemset(ctl + 6, 0, 4 * sizeof(int)), "reset stats");
+  }
 }
 
 // Bucket-centric join (qvmc_bucket.cuh): work items over the deletion-index
@@ -969,9 +1103,15 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     upload(h->codes, std::vector<uint64_t>(qubit_codes(), qubit_codes() + 256));
     if (const char* e = std::getenv("QVMC_JOIN")) h->use_join = std::atoi(e) != 0;
     if (const char* e = std::getenv("QVMC_JOIN_MODE")) h->join_mode = std::atoi(e);
+    if (const char* e = std::getenv("QVMC_PIPELINE")) h->pipelined = std::atoi(e) != 0;
+    if (const char* e = std::getenv("QVMC_PIPE_BATCHES")) h->pipe_batches = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("QVMC_PIPE_SEARCH_BLOCKS")) h->pipe_search_blocks = std::atoi(e);
+    if (const char* e = std::getenv("QVMC_PIPE_EVAL_BLOCKS")) h->pipe_eval_blocks = std::atoi(e);
     if (const char* e = std::getenv("QVMC_HIT_CAP")) {  // test hook: a small first capacity exercises the regrow path
       h->hit_cap = std::strtoull(e, nullptr, 10);
       h->chunk_cap = h->hit_cap / 8 + 64;
+      h->p_hit_cap = h->hit_cap;
+      h->p_chunk_cap = h->chunk_cap;
     }
     h->ctl.ensure(kCtlInts * sizeof(int) * 2);
     ck(cudaMemset(h->ctl.p, 0, kCtlInts * sizeof(int) * 2), "memset ctl");
@@ -1040,6 +1180,13 @@ int qvmc_cuda_ham_destroy(qvmc_ham_t h) {
       if (e) cudaEventDestroy(e);
     for (auto& e : h->ev_k)
       if (e) cudaEventDestroy(e);
+    for (auto& e : h->ev_p)
+      if (e) cudaEventDestroy(e);
+    if (h->side) {
+      cudaStreamSynchronize(h->side);
+      cudaStreamDestroy(h->side);
+    }
+    if (h->log_host) cudaFreeHost(h->log_host);
     delete h;
   });
 }
@@ -1364,6 +1511,8 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       O.cs = rcs;
       if (P.join && h->join_mode == 2) {
         DISPATCH_W(W, (run_join_bucket<WW>(h, rkeys, n_unq, R, P, row_begin, row_end, deloc)));
+      } else if (P.join && h->join_mode == 1 && h->pipelined) {
+        DISPATCH_W(W, (run_join_pipelined<WW>(h, rkeys, n_unq, R, P, deloc)));
       } else if (P.join && h->join_mode == 1) {
         DISPATCH_W(W, (run_join_split<WW>(h, rkeys, n_unq, R, P, deloc)));
       } else if (P.join) {

@@ -1075,13 +1075,14 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
                   const uint64_t* __restrict__ keys, const uint4* __restrict__ chunk,
                   const unsigned long long* __restrict__ n_chunks, const uint32_t* __restrict__ hy,
                   const uint32_t* __restrict__ hg, const uint32_t* __restrict__ hk, int side, int s,
-                  const int* __restrict__ exp_flag, const uint8_t* __restrict__ rowpos, double2* __restrict__ part) {
+                  const int* __restrict__ exp_flag, const uint8_t* __restrict__ rowpos, double2* __restrict__ part,
+                  uint64_t chunk_cap) {
   constexpr int DH = QVMC_EVAL_HITS;
   __shared__ uint16_t s_pos[kWarps][32];
   const int lane = threadIdx.x & 31;
   uint16_t* spos = s_pos[threadIdx.x >> 5];
   const int n = H.n;
-  const uint64_t nc = *n_chunks;
+  const uint64_t nc = min(static_cast<uint64_t>(*n_chunks), chunk_cap);  // an overflowed batch is rerun
   const bool mag = *exp_flag == 0;  // amplitude magnitudes from the records (k_gather_sorted)
   const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t c = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; c < nc; c += n_warps) {
