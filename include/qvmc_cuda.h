@@ -102,6 +102,20 @@ int qvmc_index_export(qvmc_index_t idx, uint64_t* xy_words, uint64_t* group_offs
                       uint64_t* z_words);
 void qvmc_index_destroy(qvmc_index_t idx);
 
+/* Device-layout plan of an index, computed on the host (no device needed),
+ * for tests and diagnostics: groups per join drain-record kind (A: weight-2/4
+ * group whose terms share one Z string and fit one 64-byte record; B: compact
+ * family-compressed single excitation; C: term by term; D: general family
+ * compression), set bits of the pair-existence bitmaps (0 when N > 128),
+ * weight-2 / weight-4 flip masks and flip-table buckets. */
+typedef struct {
+  uint64_t kind_a, kind_b, kind_c, kind_d;
+  uint64_t bitmap_bits;
+  uint64_t singles, doubles;
+  uint64_t xy_tab_buckets;
+} qvmc_plan_summary;
+int qvmc_index_plan_summary(qvmc_index_t idx, qvmc_plan_summary* out);
+
 /* ------------------------------------------------------------ device handle */
 
 /* Upload a grouped HamiltonianIndex. Arguments mirror the index's members:

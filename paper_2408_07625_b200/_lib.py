@@ -47,6 +47,11 @@ class QvmcStats(C.Structure):
     ]
 
 
+class QvmcPlanSummary(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in ("kind_a", "kind_b", "kind_c", "kind_d", "bitmap_bits", "singles",
+                                          "doubles", "xy_tab_buckets")]
+
+
 _P = C.c_void_p
 _I64 = C.c_int64
 _U64 = C.c_uint64
@@ -58,6 +63,7 @@ SIGNATURES = [
     ("qvmc_index_info", _INT, [_P, C.POINTER(_INT), C.POINTER(_U64), C.POINTER(C.c_uint32), C.POINTER(_I64)]),
     ("qvmc_index_export", _INT, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
     ("qvmc_index_destroy", None, [_P]),
+    ("qvmc_index_plan_summary", _INT, [_P, _P]),
     ("qvmc_cuda_ham_create", _INT, [_INT, _INT, C.c_uint32, _P, _P, _U64, _P, _P, _P, _I64, _INT, C.POINTER(_P)]),
     ("qvmc_cuda_ham_create_from_index", _INT, [_P, _INT, C.POINTER(_P)]),
     ("qvmc_cuda_ham_destroy", _INT, [_P]),

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <bit>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -994,6 +995,25 @@ int qvmc_index_export(qvmc_index_t idx, uint64_t* xy_words, uint64_t* group_offs
 }
 
 void qvmc_index_destroy(qvmc_index_t idx) { delete idx; }
+
+int qvmc_index_plan_summary(qvmc_index_t idx, qvmc_plan_summary* out) {
+  return guarded([&] {
+    if (!idx || !out) fail(QVMC_ERR_INVALID_ARGUMENT, "null argument");
+    const HostIndex& hi = idx->idx;
+    const DevicePlan p = plan_device(hi);
+    qvmc_plan_summary r{};
+    for (uint32_t g = 0; g < hi.n_xy(); ++g) {
+      if (static_cast<int64_t>(g) == hi.diag) continue;
+      const uint64_t kind = p.grec[static_cast<size_t>(g) * kGrecWordsHost] & 3;
+      (kind == 0 ? r.kind_a : kind == 1 ? r.kind_b : kind == 2 ? r.kind_c : r.kind_d) += 1;
+      if (p.xy_weight[g] == 2) ++r.singles;
+      if (p.xy_weight[g] == 4) ++r.doubles;
+    }
+    for (uint32_t w : p.pbits) r.bitmap_bits += static_cast<uint64_t>(std::popcount(w));
+    r.xy_tab_buckets = p.xy_tab_mask + 1;
+    *out = r;
+  });
+}
 
 int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_t* xy_words,
                          const uint64_t* group_offsets, uint64_t n_terms, const double* coeff,

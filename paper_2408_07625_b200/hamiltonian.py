@@ -75,6 +75,13 @@ class HamiltonianIndex:
         self._xy_lookup = {self.xy[g].tobytes(): g for g in range(G)}
         self._device = {}
 
+    def plan_summary(self) -> dict:
+        """The device-layout plan of this index, computed on the host
+        (``qvmc_index_plan_summary``): join drain-record kinds, bitmap bits."""
+        out = _lib.QvmcPlanSummary()
+        _lib.check(_lib.lib().qvmc_index_plan_summary(self._handle, C.byref(out)))
+        return {k: int(getattr(out, k)) for k, _ in _lib.QvmcPlanSummary._fields_}
+
     # ------------------------------------------------------------ builders
     @staticmethod
     def from_masks(n_qubits: int, coeff, x, y, z) -> "HamiltonianIndex":

@@ -200,3 +200,51 @@ def test_dropin_defines_the_replaced_translation_units():
                 mine = _defined_symbols(DROPIN, demangle=False)
                 missing = {s for s in ref_syms if s not in mine}
                 assert not missing, missing
+
+
+def _expected_plan(H):
+    """Python restatement of the planner's record rules (host_index.cpp plan_device):
+    kind A = weight-2/4 group, one shared Z string, 2 + W + terms <= 8 words."""
+    W = H.n_words
+    diag = H.diagonal_xy_index()
+    a = singles = doubles = 0
+    for g in range(H.n_xy):
+        if g == diag:
+            continue
+        xy = [int(v) for v in H.xy[g]]
+        wt = sum(bin(v).count("1") for v in xy)
+        singles += wt == 2
+        doubles += wt == 4
+        t0, t1 = int(H.group_offsets[g]), int(H.group_offsets[g + 1])
+        zs = {tuple(int(H.yz[t][w]) & ~xy[w] for w in range(W)) for t in range(t0, t1)}
+        a += wt in (2, 4) and 1 <= t1 - t0 <= 6 - W and len(zs) == 1
+    return a, singles, doubles
+
+
+@pytest.mark.parametrize("name", ["h4", "h6"])
+def test_device_plan_records_and_bitmaps(name):
+    """The host-side device plan (no GPU): every group gets exactly one drain
+    record kind, kind A exactly where the shared-Z rule holds, and the pair
+    bitmaps hold one bit per single and six (every split into two pairs) per double."""
+    g = golden("fixtures")
+    H = product_index(g, f"{name}_")
+    ps = H.plan_summary()
+    a, singles, doubles = _expected_plan(H)
+    n_groups = H.n_xy - (0 if H.diagonal_xy_index() is None else 1)
+    assert ps["kind_a"] + ps["kind_b"] + ps["kind_c"] + ps["kind_d"] == n_groups
+    assert ps["kind_a"] == a
+    assert (ps["singles"], ps["doubles"]) == (singles, doubles)
+    assert ps["bitmap_bits"] == singles + 6 * doubles
+    assert ps["xy_tab_buckets"] >= 64 and ps["xy_tab_buckets"] * 2 >= H.n_xy
+
+
+def test_device_plan_synthetic_jw_structure():
+    """JW-structured synthetic H: doubles share their Z string (kind A), the
+    2 + 2(N-2)-term singles compress to two families (kind B)."""
+    from paper_2408_07625_b200 import synthetic
+    H = synthetic.jw_hamiltonian(56, 20_000, seed=1)
+    ps = H.plan_summary()
+    assert ps["kind_a"] == ps["doubles"] and ps["kind_b"] == ps["singles"] and ps["kind_c"] == ps["kind_d"] == 0
+    assert ps["bitmap_bits"] == ps["singles"] + 6 * ps["doubles"]
+    big = synthetic.jw_hamiltonian(130, 2_000, seed=1)  # N > 128: no pair bitmaps
+    assert big.plan_summary()["bitmap_bits"] == 0
