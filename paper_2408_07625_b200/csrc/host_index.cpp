@@ -306,7 +306,31 @@ DevicePlan plan_device(const HostIndex& h) {
       long double u = 0;
       std::vector<long double> v;
     };
+    // family bases: per y-weight class the bitwise majority of the terms' yz
+    // masks (the undressed string, even when a Z-dressed term comes first in
+    // the group, as in real molecular Hamiltonians); terms then attach to the
+    // base within one bit, new bases are opened greedily if needed
     std::vector<Fam> fams;
+    {
+      std::vector<uint8_t> qs;
+      for (uint64_t t = t0; t < t1; ++t)
+        if (std::find(qs.begin(), qs.end(), h.y_weight[t] & 3) == qs.end()) qs.push_back(h.y_weight[t] & 3);
+      for (uint8_t q : qs) {
+        if (static_cast<int>(fams.size()) == kMaxFamilies) break;
+        std::vector<uint64_t> maj(W, 0);
+        uint64_t cnt = 0;
+        std::vector<uint32_t> ones(static_cast<size_t>(W) * 64, 0);
+        for (uint64_t t = t0; t < t1; ++t) {
+          if ((h.y_weight[t] & 3) != q) continue;
+          ++cnt;
+          for (int w = 0; w < W; ++w)
+            for (uint64_t v = h.yz[t * W + w]; v; v &= v - 1) ++ones[w * 64 + std::countr_zero(v)];
+        }
+        for (int b = 0; b < W * 64; ++b)
+          if (2 * ones[b] > cnt) maj[b / 64] |= 1ull << (b % 64);
+        fams.push_back(Fam{maj, q, 0, std::vector<long double>(n, 0)});
+      }
+    }
     bool ok = true;
     for (uint64_t t = t0; t < t1 && ok; ++t) {
       const uint8_t q = h.y_weight[t] & 3;
@@ -436,7 +460,7 @@ DevicePlan plan_device(const HostIndex& h) {
         continue;
       }
       bool a_ok = static_cast<int64_t>(g) != h.diag && (wt == 2 || wt == 4) && k >= 1 &&
-                  k <= static_cast<uint64_t>(kGrecWordsHost - 2 - W);
+                  k <= static_cast<uint64_t>(kGrecWordsHost - 1 - W);
       int xpos[4], np = 0;
       for (int w = 0; w < W && a_ok; ++w)
         for (uint64_t v = xy[w]; v; v &= v - 1) xpos[np++] = w * 64 + std::countr_zero(v);
@@ -452,8 +476,8 @@ DevicePlan plan_device(const HostIndex& h) {
       }
       if (a_ok) {
         r[0] = meta;  // kind A = 0
-        for (int w = 0; w < W; ++w) r[2 + w] = h.yz[t0 * W + w] & ~xy[w];
-        for (uint64_t t = t0; t < t1; ++t) std::memcpy(&r[2 + W + (t - t0)], &h.coeff[t], 8);
+        for (int w = 0; w < W; ++w) r[1 + w] = h.yz[t0 * W + w] & ~xy[w];
+        for (uint64_t t = t0; t < t1; ++t) std::memcpy(&r[1 + W + (t - t0)], &h.coeff[t], 8);
       } else {
         if (k >= (1ull << 32)) throw std::invalid_argument("HamiltonianIndex: group with 2^32 or more terms");
         r[0] = 2;

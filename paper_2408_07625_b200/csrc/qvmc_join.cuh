@@ -46,7 +46,7 @@ constexpr uint32_t kNoKey = 0xFFFFFFFFu;
 // Per-group drain record, 8 words (two 32-byte sectors), host_index.cpp:
 //   kind A (small group, one shared Z string): w0 = 0 | k << 2 | per term t
 //     (ypat_t | (y_weight_t & 3) << 4) << (8 + 6t), ypat_t = Y positions among
-//     the sorted flip positions; w2.. = z words, then the k coefficients
+//     the sorted flip positions; w1.. = z words, then the k coefficients
 //   kind B (family-compressed single excitation, every family base B_f = shared
 //     Z string | Y positions among the two flip positions): w0 = 1 | n_fam << 8
 //     | q bits << 16 | ypat_f << (24 + 4f), w1 = offset of the group's
@@ -374,18 +374,18 @@ __device__ __forceinline__ void kind_a_element(const uint64_t* r, const uint64_t
   const int k = static_cast<int>((meta >> 2) & 7);
   int pz = 0;
 #pragma unroll
-  for (int w = 0; w < W; ++w) pz += __popcll(x[w] & r[2 + w]);
+  for (int w = 0; w < W; ++w) pz += __popcll(x[w] & r[1 + w]);
   const int np = (key >> 16) == 0xFFFFu ? 2 : 4;
   uint32_t bp = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
     if (i < np) bp |= (bit_at<W>(x, (key >> (8 * i)) & 0xFF) ? 0u : 1u) << i;
 #pragma unroll
-  for (int t = 0; t < kGrecWords - 2 - W; ++t) {
+  for (int t = 0; t < kGrecWords - 1 - W; ++t) {
     if (t < k) {
       const uint32_t f = static_cast<uint32_t>(meta >> (8 + 6 * t)) & 63u;
       const int q = (static_cast<int>(f >> 4) + 2 * (pz + __popc(bp & f & 15u))) & 3;
-      const double c = __longlong_as_double(static_cast<long long>(r[2 + W + t]));
+      const double c = __longlong_as_double(static_cast<long long>(r[1 + W + t]));
       if (q == 0) re += c;
       else if (q == 2) re -= c;
       else if (q == 1) im += c;

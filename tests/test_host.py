@@ -204,7 +204,7 @@ def test_dropin_defines_the_replaced_translation_units():
 
 def _expected_plan(H):
     """Python restatement of the planner's record rules (host_index.cpp plan_device):
-    kind A = weight-2/4 group, one shared Z string, 2 + W + terms <= 8 words."""
+    kind A = weight-2/4 group, one shared Z string, 1 + W + terms <= 8 words."""
     W = H.n_words
     diag = H.diagonal_xy_index()
     a = singles = doubles = 0
@@ -217,7 +217,7 @@ def _expected_plan(H):
         doubles += wt == 4
         t0, t1 = int(H.group_offsets[g]), int(H.group_offsets[g + 1])
         zs = {tuple(int(H.yz[t][w]) & ~xy[w] for w in range(W)) for t in range(t0, t1)}
-        a += wt in (2, 4) and 1 <= t1 - t0 <= 6 - W and len(zs) == 1
+        a += wt in (2, 4) and 1 <= t1 - t0 <= 7 - W and len(zs) == 1
     return a, singles, doubles
 
 
@@ -236,6 +236,8 @@ def test_device_plan_records_and_bitmaps(name):
     assert (ps["singles"], ps["doubles"]) == (singles, doubles)
     assert ps["bitmap_bits"] == singles + 6 * doubles
     assert ps["xy_tab_buckets"] >= 64 and ps["xy_tab_buckets"] * 2 >= H.n_xy
+    if name == "h6":  # the 2 + 2(N-2)-term single excitations compress to families (kind B)
+        assert ps["kind_b"] == 12 and ps["kind_c"] == ps["doubles"] - ps["kind_a"]
 
 
 def test_device_plan_synthetic_jw_structure():
