@@ -150,7 +150,7 @@ struct qvmc_ham_s {
   DBuf p_hy[2], p_hg[2], p_hk[2], p_chunk[2], p_part[2];
   uint64_t p_hit_cap = 0, p_chunk_cap = 0;
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_p[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_p[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   unsigned long long* log_host = nullptr;
   uint64_t log_cap = 0;
   int pipe_batches = 2, pipe_search_blocks = 0, pipe_eval_blocks = 0;  // measured: 2-3 batches best
@@ -1490,9 +1490,28 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
     const int W = h->W;
     const int64_t rows = row_end - row_begin;
     const uint64_t* dkeys = stage(h, h->keys, keys, static_cast<size_t>(n_unq) * W, mem);
+    // host amplitudes: copied on a second stream while the sample-set index is built from the keys
+    cudaStream_t main_stream = h->stream;
+    if (mem == QVMC_MEM_HOST && n_unq > 0) {
+      if (!h->side) {
+        ck(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking), "stream create");
+        for (auto& e : h->ev_p) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+      }
+      ck(cudaEventRecord(h->ev_p[6], main_stream), "event");  // after earlier work on the buffers
+      ck(cudaStreamWaitEvent(h->side, h->ev_p[6], 0), "wait");
+      h->stream = h->side;
+    }
     const double* dla = stage(h, h->la, log_amp, n_unq, mem);
     const double* dph = stage(h, h->ph, phase, n_unq, mem);
     const double* dlp = log_prob ? stage(h, h->lp, log_prob, n_unq, mem) : nullptr;
+    const bool h2d_async = h->stream != main_stream;
+    if (h2d_async) {
+      ck(cudaEventRecord(h->ev_p[7], h->side), "event");
+      h->stream = main_stream;
+    }
+    auto wait_amplitudes = [&] {
+      if (h2d_async) ck(cudaStreamWaitEvent(h->stream, h->ev_p[7], 0), "wait");
+    };
     double2* deloc = reinterpret_cast<double2*>(out_eloc);
     if (mem == QVMC_MEM_HOST || !out_eloc) {
       h->eloc.ensure(std::max<int64_t>(rows, 1) * 16);
@@ -1509,6 +1528,7 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
       P = plan_rows(h, n_unq);
       note_plan(h, P);
+      wait_amplitudes();
       if (P.join) {
         P.want_pos_of = h->join_mode == 2;
         DISPATCH_W(W, R = sort_for_locality<WW>(h, rkeys, dla, dph, n_unq, row_begin, row_end, P));
