@@ -1525,9 +1525,16 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
     const uint64_t* rkeys = dkeys;
     const double2* rcs = nullptr;
     if (n_unq > 0) {
-      DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
+      // sector test first: the join path (row search, modes 0/1) needs no sample
+      // hash table (duplicate keys are caught by the search), other paths build it
+      ck(cudaMemsetAsync(static_cast<int*>(h->ctl.p) + 2, 0, 2 * sizeof(int), h->stream), "memset popcount range");
+      const int pgrid = static_cast<int>(std::min<int64_t>((n_unq + kThreads - 1) / kThreads, grid_for(h, 4)));
+      DISPATCH_W(W, (k_popc_range<WW><<<std::max(pgrid, 1), kThreads, 0, h->stream>>>(dkeys, n_unq,
+                                                                                      static_cast<int*>(h->ctl.p) + 2)));
+      ck_launch("popcount range");
       P = plan_rows(h, n_unq);
       note_plan(h, P);
+      if (!P.join || h->join_mode == 2) DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
       wait_amplitudes();
       if (P.join) {
         P.want_pos_of = h->join_mode == 2;

@@ -110,6 +110,28 @@ __device__ __forceinline__ uint32_t pair_b(int pi) {  // pairs ordered by b then
   return static_cast<uint32_t>(b);
 }
 
+// popcount range of the keys (the sector test; the join path needs no sample hash table)
+template <int W>
+__global__ void __launch_bounds__(kThreads) k_popc_range(const uint64_t* __restrict__ keys, int64_t n, int* popc_mm) {
+  int mx = 0, mn = 1024;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int pc = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) pc += __popcll(keys[i * W + w]);
+    mx = max(mx, pc);
+    mn = min(mn, pc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(popc_mm, mx);
+    atomicMax(popc_mm + 1, 1024 - mn);
+  }
+}
+
 // Locality order for the join: samples sorted by their minority orbitals,
 // highest first (top 8 packed into 64 bits), so that rows processed together
 // and the members of their buckets sit close in memory and in L2.
@@ -730,6 +752,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
     uint32_t hits = 0;
     uint64_t cand = 0;
     uint32_t prev_chunk = ~0u;  // kModeHits: last flushed chunk of this row
+    bool dup = false;           // a duplicate of this row's key in the sample set
     uint32_t s_head = 0, s_tail = 0;  // survivor ring (warp-uniform)
     // per-lane cursor over the concatenated ranges: member pointer and the
     // current range's (T_x, bitmap row) in registers, reloaded on a range change
@@ -783,6 +806,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
               prev_chunk = static_cast<uint32_t>(cid);
             } else if (lane == 0) {
               atomicOr(C.err, kErrHitOverflow);  // the host grows the buffers and reruns
+              if (cid < O.chunk_cap)             // a reserved chunk is always defined (empty)
+                O.chunk[cid] = make_uint4(static_cast<uint32_t>(row), 0u, 0u, ~0u);
             }
             __syncwarp();
             if (lane == 0) {
@@ -863,6 +888,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
             if (J.pbits && !pbit(J.pbits, pidx(p0, p1))) continue;
             key[u] = static_cast<uint32_t>(p0) | static_cast<uint32_t>(p1) << 8 | 0xFFFF0000u;
           }
+        } else if (static_cast<uint32_t>(v[u]) != static_cast<uint32_t>(row)) {
+          dup = true;  // T_y = T_x in an exact bucket: the same key at another position
         }
       }
       // survivors -> ring; the flip-table lookups then run 32 at a time with
@@ -1051,6 +1078,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
     }
     tot_cand += cand;
     tot_hits += row_hits;
+    if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr(C.err, kErrDuplicate);
   }
   tot_cand = warp_sum(tot_cand);
   if (lane == 0) {
