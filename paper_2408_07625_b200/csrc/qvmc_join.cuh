@@ -622,11 +622,6 @@ __device__ QVMC_JOIN_DRAIN_ATTR double2 join_drain(const HamView& H, const JoinV
   constexpr int DH = QVMC_JOIN_DRAIN_HITS;
   double2 acc = make_double2(0.0, 0.0);
   __syncwarp();
-#ifdef QVMC_EXP_NO_DRAIN
-  if (lane == 0) sm->qn = 0;
-  __syncwarp();
-  return acc;
-#endif
   const Key<W> xrow = row_key<W>(sm);
   const double la_i = *reinterpret_cast<const volatile double*>(&sm->la);
   const double2 cs_i = make_double2(*reinterpret_cast<const volatile double*>(&sm->cs_c),
@@ -916,11 +911,9 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
           const uint32_t e = (s_head + lane) & (kJSurv - 1);
           y = sm->sy[e];
           kk = sm->sk[e];
-#ifndef QVMC_EXP_NO_LOOKUP
           const uint32_t bk = xy_bucket(kk, static_cast<uint32_t>(J.xy_mask));
           g = xy_resolve(kk, ldg256(J.xy_tab + static_cast<uint64_t>(bk) * 4));
           if (g == kChain) g = xy_chain(kk, bk, J.xy_tab, static_cast<uint32_t>(J.xy_mask));
-#endif
         }
         s_head += cntl;
         // warp-aggregated append of the hits
