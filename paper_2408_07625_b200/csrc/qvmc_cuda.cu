@@ -146,6 +146,7 @@ struct qvmc_ham_s {
   DBuf s_hy, s_hg, s_hk, s_chunk, s_row_last, s_base, s_part, s_head, b_icnt, b_iincl, b_items, s_rowpos;
   uint64_t hit_cap = 0, chunk_cap = 0;
   uint64_t hits_per_row = 320;  // split evaluation: running estimate that sizes the row batches
+  DBuf gkey, p_rlo, p_rhi;      // per-group position key (pairs-based local_energies), row ranges
   // pipelined split evaluation (run_join_pipelined)
   DBuf p_hy[2], p_hg[2], p_hk[2], p_chunk[2], p_part[2];
   uint64_t p_hit_cap = 0, p_chunk_cap = 0;
@@ -250,6 +251,154 @@ __global__ void __launch_bounds__(kThreads)
     acc_re = warp_sum(acc_re);
     acc_im = warp_sum(acc_im);
     if (lane == 0) out[i] = make_double2(acc_re, acc_im);
+  }
+}
+
+// row ranges of a canonical pair list (sorted by x): row_lo / row_hi (memset 0 first)
+__global__ void k_pair_rows(const uint32_t* __restrict__ e3, uint64_t n_pairs, int64_t n, uint32_t* row_lo,
+                            uint32_t* row_hi) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n_pairs;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = e3[3 * e];
+    if (x >= n) continue;  // reported by k_check_sorted
+    if (e == 0 || e3[3 * (e - 1)] != x) row_lo[x] = static_cast<uint32_t>(e);
+    if (e + 1 == n_pairs || e3[3 * (e + 1)] != x) row_hi[x] = static_cast<uint32_t>(e + 1);
+  }
+}
+
+// local_energies from a canonical pair list (energy.cpp:13-48), one warp per
+// row: H_{x x'} from the 64-byte drain records when x' = x ^ xy (kind A
+// bit-identical to group_element; kind B for single moves within the row's
+// minority set), term by term otherwise (the reference evaluates whatever x'
+// an entry names); phases from per-sample (cos, sin).
+template <int W>
+__global__ void __launch_bounds__(kThreads)
+    k_pairs_eloc2(const __grid_constant__ HamView H, const __grid_constant__ JoinView J, const uint32_t* __restrict__ gkey,
+                  const uint64_t* __restrict__ keys, const double* __restrict__ la, const double2* __restrict__ cs,
+                  int64_t n, const uint32_t* __restrict__ e3, const uint32_t* __restrict__ row_lo,
+                  const uint32_t* __restrict__ row_hi, double2* out, int* err) {
+  __shared__ uint16_t s_pos[kWarps][32];
+  const int lane = threadIdx.x & 31;
+  uint16_t* spos = s_pos[threadIdx.x >> 5];
+  const int nq = H.n;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += n_warps) {
+    const double la_i = la[i];
+    if (isinf(la_i)) {
+      if (lane == 0) {
+        atomicOr(err, kErrZeroAmp);
+        out[i] = make_double2(CUDART_NAN, CUDART_NAN);
+      }
+      continue;
+    }
+    const double2 cs_i = cs[i];
+    Key<W> xrow;
+    int pc = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      xrow.w[w] = keys[i * W + w];
+      pc += __popcll(xrow.w[w]);
+    }
+    const int side = 2 * pc <= nq ? 1 : 0;
+    const int s = side ? pc : nq - pc;
+    if (s <= 32) {  // the row's minority orbitals (kind B)
+      int pos = 0, cnt = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        uint64_t v = side ? xrow.w[w] : ~xrow.w[w];
+        const int hi_bit = nq - 64 * w;
+        if (hi_bit < 64) v &= (hi_bit <= 0) ? 0ull : ((1ull << hi_bit) - 1);
+        const int c = __popcll(v);
+        if (lane >= cnt && lane < cnt + c) {
+          for (int k = 0; k < lane - cnt; ++k) v &= v - 1;
+          pos = 64 * w + __ffsll(static_cast<long long>(v)) - 1;
+        }
+        cnt += c;
+      }
+      __syncwarp();
+      if (lane < s) spos[lane] = static_cast<uint16_t>(pos);
+      __syncwarp();
+    }
+    const uint32_t lo = row_lo[i], hi = row_hi[i];
+    double2 acc = make_double2(0.0, 0.0);
+    const bool quad = H.diag >= 0 && H.diag_quad && s <= 32;
+    bool has_diag = false;  // the (x, x, diagonal) entry: the warp evaluates it as the quadratic form
+    for (uint32_t e0 = lo; e0 < hi; e0 += 32) {
+      const uint32_t e = e0 + lane;
+      bool valid = e < hi;
+      uint32_t j = 0, g = 0;
+      if (valid) {
+        j = e3[3 * static_cast<uint64_t>(e) + 1];
+        g = e3[3 * static_cast<uint64_t>(e) + 2];
+        if (j >= n || g >= H.n_xy) {
+          atomicOr(err, kErrBadPair);
+          valid = false;
+        } else if (quad && static_cast<int64_t>(g) == H.diag && static_cast<int64_t>(j) == i) {
+          has_diag = true;
+          valid = false;
+        }
+      }
+      double hr = 0.0, hi2 = 0.0, la_j = 0.0;
+      double2 cs_j = make_double2(1.0, 0.0);
+      if (valid) {
+        uint64_t xp[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) xp[w] = __ldg(keys + static_cast<int64_t>(j) * W + w);
+        la_j = __ldg(la + j);
+        cs_j = __ldg(cs + j);
+        const uint32_t key = __ldg(gkey + g);
+        const U64x4 g0 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords);
+        const uint32_t kind = static_cast<uint32_t>(g0.a) & 3u;
+        bool fast = false;
+        if (key != kNoKey && (kind == kGrecA || kind == kGrecB)) {
+          uint64_t m[W];
+          key_mask<W>(key, m);
+          bool is_move = true;  // x' = x ^ xy
+#pragma unroll
+          for (int w = 0; w < W; ++w) is_move &= xp[w] == (xrow.w[w] ^ m[w]);
+          if (kind == kGrecB) {  // a single move inside the minority picture: one flip bit in S(x)
+            const bool b0 = bit_at<W>(xrow.w, key & 0xFF) == (side != 0);
+            const bool b1 = bit_at<W>(xrow.w, (key >> 8) & 0xFF) == (side != 0);
+            is_move &= (b0 != b1) && s <= 32;
+          }
+          fast = is_move;
+        }
+        if (fast) {
+          const U64x4 g1 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords + 4);
+          const uint64_t r[kGrecWords] = {g0.a, g0.b, g0.c, g0.d, g1.a, g1.b, g1.c, g1.d};
+          if (kind == kGrecA) kind_a_element<W>(r, xrow.w, key, hr, hi2);
+          else kind_b_element<W>(J.famvi, r, xrow.w, key, spos, s, side, hr, hi2);
+        } else {
+          group_element<W>(H, xp, g, hr, hi2);
+        }
+        add_ratio(la_j, cs_j, la_i, cs_i, hr, hi2, acc);
+      }
+    }
+    if (__any_sync(0xffffffffu, has_diag)) {  // A + sum_S b_p + sum_{p<q in S} K_pq (+ |z| >= 3 terms)
+      if (lane == 0) acc.x += side ? H.diag_A1 : H.diag_A0;
+      if (lane < s) acc.x += __ldg(H.diag_b + side * nq + spos[lane]);
+      const int np = s * (s - 1) / 2;
+      for (int pi = lane; pi < np; pi += 32) {
+        const int b = static_cast<int>(pair_b(pi)), a = pi - b * (b - 1) / 2;
+        acc.x += __ldg(H.diag_K + spos[a] * nq + spos[b]);
+      }
+      for (uint32_t e = lane; e < H.n_diag_other; e += 32) {
+        const uint32_t t = __ldg(H.diag_other + e);
+        int c = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) c += __popcll(xrow.w[w] & __ldg(H.yz + (int64_t)t * W + w));
+        const int qt = (__ldg(H.yw + t) + 2 * c) & 3;
+        const double cf = __ldg(H.coeff + t);
+        if (qt == 0) acc.x += cf;
+        else if (qt == 2) acc.x -= cf;
+        else if (qt == 1) acc.y += cf;
+        else acc.y -= cf;
+      }
+    }
+    acc.x = warp_sum(acc.x);
+    acc.y = warp_sum(acc.y);
+    if (lane == 0) out[i] = acc;
   }
 }
 
@@ -1121,6 +1270,12 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     upload(h->binom, h->binom_host);
     h->xy_tab_mask = p.xy_tab_mask;
     upload(h->codes, std::vector<uint64_t>(qubit_codes(), qubit_codes() + 256));
+    {
+      std::vector<uint32_t> gk(std::max<uint32_t>(n_xy, 1), 0xFFFFFFFFu);
+      for (uint32_t g = 0; g < n_xy; ++g)
+        if (p.xy_weight[g] == 2 || p.xy_weight[g] == 4) gk[g] = xy_position_key(&hi.xy[static_cast<size_t>(g) * n_words], n_words);
+      upload(h->gkey, gk);
+    }
     if (const char* e = std::getenv("QVMC_JOIN")) h->use_join = std::atoi(e) != 0;
     if (const char* e = std::getenv("QVMC_JOIN_MODE")) h->join_mode = std::atoi(e);
     if (const char* e = std::getenv("QVMC_PIPELINE")) h->pipelined = std::atoi(e) != 0;
@@ -1430,14 +1585,28 @@ int qvmc_cuda_local_energies(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, 
       dout = h->eloc.as<double2>();
     }
     int* err = static_cast<int*>(h->ctl.p);
+    h->p_rlo.ensure(n_unq * 4 + 16);
+    h->p_rhi.ensure(n_unq * 4 + 16);
+    ck(cudaMemsetAsync(h->p_rlo.p, 0, n_unq * 4, h->stream), "memset rows");
+    ck(cudaMemsetAsync(h->p_rhi.p, 0, n_unq * 4, h->stream), "memset rows");
     if (n_pairs > 0) {
       const int g1 = static_cast<int>(std::min<uint64_t>((n_pairs + kThreads - 1) / kThreads, grid_for(h, 8)));
       k_check_sorted<<<g1, kThreads, 0, h->stream>>>(de, n_pairs, n_unq, err);
       ck_launch("check pairs");
+      k_pair_rows<<<g1, kThreads, 0, h->stream>>>(de, n_pairs, n_unq, h->p_rlo.as<uint32_t>(), h->p_rhi.as<uint32_t>());
+      ck_launch("pair rows");
+    }
+    h->cs.ensure(n_unq * 16 + 16);
+    {
+      const int grid = static_cast<int>(std::min<int64_t>((n_unq + kThreads - 1) / kThreads, grid_for(h, 8)));
+      k_cos_sin<<<std::max(grid, 1), kThreads, 0, h->stream>>>(dph, n_unq, h->cs.as<double2>());
+      ck_launch("cos sin");
     }
     const int grid = static_cast<int>(std::min<int64_t>((n_unq + kWarps - 1) / kWarps, grid_for(h, 8)));
-    DISPATCH_W(W, (k_pairs_eloc<WW><<<grid, kThreads, 0, h->stream>>>(h->view, dkeys, dla, dph, n_unq, de, n_pairs,
-                                                                    dout, err)));
+    RowPlan P0{};
+    DISPATCH_W(W, (k_pairs_eloc2<WW><<<grid, kThreads, 0, h->stream>>>(
+                      h->view, join_view(h, P0), h->gkey.as<uint32_t>(), dkeys, dla, h->cs.as<double2>(), n_unq, de,
+                      h->p_rlo.as<uint32_t>(), h->p_rhi.as<uint32_t>(), dout, err)));
     ck_launch("local energies");
     if (mem == QVMC_MEM_HOST) {
       ck(cudaMemcpyAsync(out_eloc, dout, n_unq * 16, cudaMemcpyDeviceToHost, h->stream), "D2H eloc");
