@@ -197,63 +197,6 @@ __global__ void k_fill_u64(uint64_t* p, uint64_t n, uint64_t v) {
     p[i] = v;
 }
 
-// local_energies from canonical pairs (energy.cpp:13-48): one warp per row,
-// row run located by binary search on x.
-template <int W>
-__global__ void __launch_bounds__(kThreads)
-    k_pairs_eloc(HamView H, const uint64_t* __restrict__ keys, const double* __restrict__ la,
-                 const double* __restrict__ ph, int64_t n, const uint32_t* __restrict__ e3, uint64_t n_pairs,
-                 double2* out, int* err) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < n; i += n_warps) {
-    const double la_i = la[i];
-    if (isinf(la_i)) {
-      if (lane == 0) {
-        atomicOr(err, kErrZeroAmp);
-        out[i] = make_double2(CUDART_NAN, CUDART_NAN);
-      }
-      continue;
-    }
-    const double ph_i = ph[i];
-    // [lo, hi) = entries with x == i
-    uint64_t lo = 0, hi = n_pairs;
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if (e3[3 * mid] < i) lo = mid + 1; else hi = mid;
-    }
-    uint64_t end = lo, top = n_pairs;
-    while (end < top) {
-      const uint64_t mid = (end + top) >> 1;
-      if (e3[3 * mid] <= i) end = mid + 1; else top = mid;
-    }
-    double acc_re = 0.0, acc_im = 0.0;
-    for (uint64_t e = lo + lane; e < end; e += 32) {
-      const uint32_t j = e3[3 * e + 1], g = e3[3 * e + 2];
-      if (j >= n || g >= H.n_xy) {
-        atomicOr(err, kErrBadPair);
-        continue;
-      }
-      uint64_t xp[W];
-#pragma unroll
-      for (int w = 0; w < W; ++w) xp[w] = keys[(int64_t)j * W + w];
-      double hr, hi2;
-      group_element<W>(H, xp, g, hr, hi2);
-      const double a = exp(la[j] - la_i);
-      double s, c;
-      sincos(ph[j] - ph_i, &s, &c);
-      hr *= a;
-      hi2 *= a;
-      acc_re += hr * c - hi2 * s;
-      acc_im += hr * s + hi2 * c;
-    }
-    acc_re = warp_sum(acc_re);
-    acc_im = warp_sum(acc_im);
-    if (lane == 0) out[i] = make_double2(acc_re, acc_im);
-  }
-}
-
 // row ranges of a canonical pair list (sorted by x): row_lo / row_hi (memset 0 first)
 __global__ void k_pair_rows(const uint32_t* __restrict__ e3, uint64_t n_pairs, int64_t n, uint32_t* row_lo,
                             uint32_t* row_hi) {
