@@ -363,7 +363,7 @@ def main():
     if tj.exists() and args.n_unq is None:
         t = json.loads(tj.read_text()).get(args.config, {})
         if "search" in t and "eval" in t:
-            traffic = t["search"]["dram_bytes"] + t["eval"]["dram_bytes"]
+            traffic = sum(t[k]["dram_bytes"] * t[k].get("launches_per_step", 1) for k in ("search", "eval"))
             traffic_src = f"profiles/ncu_traffic.json ({t['search']['report']}, {t['eval']['report']})"
             # the binding resource: issue slots (ncu smsp__issue_active, per kernel)
             issue = {k: t[k].get("issue_active_pct", 0.0) / 100.0 for k in ("search", "eval")}

@@ -1,8 +1,9 @@
 """DRAM traffic per launch of profiled kernels -> profiles/ncu_traffic.json (read by bench.py).
 
-usage: python tools/ncu_traffic.py CONFIG NAME=report.ncu-rep [NAME=report.ncu-rep ...]
+usage: python tools/ncu_traffic.py CONFIG [--launches-per-step K] NAME=report.ncu-rep [...]
 Each report is one `ncu --set full` capture of one launch; the entry records
-dram__bytes_read.sum + dram__bytes_write.sum, the kernel's duration and L2 read sectors.
+dram__bytes_read.sum + dram__bytes_write.sum, the kernel's duration and L2 read
+sectors, and how many such launches one bench step makes (row batches).
 """
 import csv
 import io
@@ -37,11 +38,14 @@ def metrics(rep):
 
 
 def main(cfg, specs):
+    per_step = 1
+    if specs and specs[0] == "--launches-per-step":
+        per_step, specs = int(specs[1]), specs[2:]
     data = json.loads(OUT.read_text()) if OUT.exists() else {}
     entry = data.setdefault(cfg, {})
     for spec in specs:
         name, rep = spec.split("=", 1)
-        entry[name] = metrics(rep) | {"report": Path(rep).name}
+        entry[name] = metrics(rep) | {"report": Path(rep).name, "launches_per_step": per_step}
     OUT.write_text(json.dumps(data, indent=1) + "\n")
     print(json.dumps(entry, indent=1))
 
