@@ -384,6 +384,9 @@ def main():
                      "kernel": "E_loc stage: k_rows_join<W,kModeHits> search + k_eval_chunks<W> + k_finalize_rows",
                      "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / statistics.mean(step_ms),
                      "search_ms": statistics.mean(search_ms), "eval_ms": statistics.mean(eval_ms),
+                     "per_kernel_note": "search_ms / eval_ms: CUDA-event time of every search / evaluation launch "
+                                        "summed over the step's row batches (the two streams overlap, so their sum "
+                                        "can exceed kernel_ms)",
                      "bytes_per_sample": b_alg,
                      "issue_slot_frac_ncu": issue,
                      "note": "integer-issue / L2-latency bound, not HBM: see DESIGN.md section 4.6 and profiles/",

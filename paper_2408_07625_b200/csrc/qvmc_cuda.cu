@@ -167,6 +167,8 @@ struct qvmc_ham_s {
   cudaEvent_t ev_k[3] = {nullptr, nullptr, nullptr};         // split evaluation: search | eval
   bool timed_k = false;
   bool timed = false;
+  std::vector<cudaEvent_t> ev_b;  // pipelined split evaluation: per batch search start/end, eval start/end
+  int64_t timed_b = 0;            // batches timed by ev_b in the last call
 };
 
 namespace {
@@ -720,6 +722,12 @@ void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
   cudaStream_t A = h->stream, B = h->side;
   cudaEvent_t ev_start = h->ev_p[0], ev_join = h->ev_p[1], ev_s[2] = {h->ev_p[2], h->ev_p[3]},
               ev_e[2] = {h->ev_p[4], h->ev_p[5]};
+  while (static_cast<int64_t>(h->ev_b.size()) < 4 * NB) {
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "event create");
+    h->ev_b.push_back(e);
+  }
+  h->timed_b = 0;
   for (int attempt = 0;; ++attempt) {
     for (int k = 0; k < 2; ++k) {
       h->p_hy[k].ensure(h->p_hit_cap * 4 + 16);
@@ -764,18 +772,22 @@ void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
       O.rowpos = h->s_rowpos.as<uint8_t>();
       const int grid_s = static_cast<int>(
           std::max<int64_t>(1, std::min<int64_t>((Rb.n_rows + kWarps - 1) / kWarps, grid_for(h, per_sm_s))));
+      ck(cudaEventRecord(h->ev_b[4 * b], A), "event");
       k_rows_join<W, kModeHits><<<grid_s, kThreads, 0, A>>>(h->view, T, join_view(h, P), keys, Rb, P.side, P.s,
                                                             ctl_view(h), O);
       ck_launch("row kernel (join search)");
+      ck(cudaEventRecord(h->ev_b[4 * b + 1], A), "event");
       ck(cudaMemcpyAsync(h->log_host + 2 * b, cur, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, A),
          "D2H cursors");
       ck(cudaEventRecord(ev_s[k], A), "event");
       ck(cudaStreamWaitEvent(B, ev_s[k], 0), "wait");
+      ck(cudaEventRecord(h->ev_b[4 * b + 2], B), "event");
       k_eval_chunks<W><<<grid_for(h, per_sm_e), kThreads, 0, B>>>(
           h->view, join_view(h, P), keys, h->p_chunk[k].as<uint4>(), reinterpret_cast<unsigned long long*>(cur + 2),
           h->p_hy[k].as<uint32_t>(), h->p_hg[k].as<uint32_t>(), h->p_hk[k].as<uint32_t>(), P.side, P.s, ctl + 14,
           h->s_rowpos.as<uint8_t>(), h->p_part[k].as<double2>(), h->p_chunk_cap);
       ck_launch("eval chunks");
+      ck(cudaEventRecord(h->ev_b[4 * b + 3], B), "event");
       const int fgrid = static_cast<int>(std::min<int64_t>((Rb.n_rows + kThreads - 1) / kThreads, grid_for(h, 8)));
       k_finalize_rows<<<std::max(fgrid, 1), kThreads, 0, B>>>(h->s_row_last.as<uint32_t>(), h->p_chunk[k].as<uint4>(),
                                                               h->p_part[k].as<double2>(), h->s_base.as<double2>(), Rb,
@@ -793,6 +805,7 @@ void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
       hits += h->log_host[2 * b];
     }
     h->timed_k = false;
+    h->timed_b = (rows + batch - 1) / batch;  // non-empty batches (each recorded its four events)
     if (need_h <= h->p_hit_cap && need_c <= h->p_chunk_cap) {
       h->hits_per_row = std::max<uint64_t>(h->hits_per_row, hits / static_cast<uint64_t>(rows) + 1);
       break;
@@ -1031,6 +1044,7 @@ void compute_moments(qvmc_ham_s* h, const double* lp, double log_norm, const dou
 void record_stats(qvmc_ham_s* h, int64_t rows) {
   h->timed = false;
   h->timed_k = false;
+  h->timed_b = 0;
   h->last = qvmc_stats{};
   h->last.rows = static_cast<uint64_t>(rows);
   h->last.terms_equivalent = static_cast<uint64_t>(rows) * h->n_xy;
@@ -1300,6 +1314,7 @@ int qvmc_cuda_ham_destroy(qvmc_ham_t h) {
       if (e) cudaEventDestroy(e);
     for (auto& e : h->ev_p)
       if (e) cudaEventDestroy(e);
+    for (auto& e : h->ev_b) cudaEventDestroy(e);
     if (h->side) {
       cudaStreamSynchronize(h->side);
       cudaStreamDestroy(h->side);
@@ -1343,6 +1358,15 @@ int qvmc_cuda_last_stats(qvmc_ham_t h, qvmc_stats* out) {
     if (h->timed_k) {
       ck(cudaEventElapsedTime(&out->search_ms, h->ev_k[0], h->ev_k[1]), "elapsed");
       ck(cudaEventElapsedTime(&out->eval_ms, h->ev_k[1], h->ev_k[2]), "elapsed");
+    } else if (h->timed_b > 0) {  // pipelined: per-launch kernel times summed over the row batches
+      out->search_ms = out->eval_ms = 0.f;
+      for (int64_t b = 0; b < h->timed_b; ++b) {
+        float ts = 0.f, te = 0.f;
+        ck(cudaEventElapsedTime(&ts, h->ev_b[4 * b], h->ev_b[4 * b + 1]), "elapsed");
+        ck(cudaEventElapsedTime(&te, h->ev_b[4 * b + 2], h->ev_b[4 * b + 3]), "elapsed");
+        out->search_ms += ts;
+        out->eval_ms += te;
+      }
     }
     out->candidates = st[0];
     out->pairs = st[1];
