@@ -179,6 +179,36 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
                          int64_t row_end, double* out_eloc, double* out_moments, int mem);
 
 /* Message of the last failure on the calling thread ("" if none). */
+/* ------------------------------------------------------------------ amplitude model */
+
+/* AnqsModel (proj/include/qvmc/model.hpp:47-157, proj/src/model.cpp) on the
+ * device: the qudit-grouped autoregressive ansatz whose log ψ / φ feed the
+ * local-energy path. Create = QuditLayout::make +
+ * AnqsModel::AnqsModel (model.cpp:33-58), same argument checks and messages;
+ * the device path additionally requires hidden = 64 and bits_per_qudit <= 6
+ * (the reference defaults, model.hpp:24,61) and says so otherwise. */
+typedef struct qvmc_model_s* qvmc_model_t;
+int qvmc_cuda_model_create(int n_qubits, int bits_per_qudit, int n_electrons, int spin_constraint, int hidden,
+                           int device, qvmc_model_t* out);
+int qvmc_cuda_model_destroy(qvmc_model_t m);
+/* AnqsModel::n_params (model.hpp:67) */
+int qvmc_cuda_model_n_params(qvmc_model_t m, int64_t* out);
+/* AnqsModel::set_params (model.cpp:99-103): host array in the reference's flat
+ * layout (model.cpp:65-80: per qudit the amplitude block then the phase block,
+ * each W1[hidden][n] b1 W2[hidden][hidden] b2 W3[2^k][hidden] b3, row-major). */
+int qvmc_cuda_model_set_params(qvmc_model_t m, int64_t n_params, const double* params);
+int qvmc_cuda_model_set_stream(qvmc_model_t m, void* stream);
+/* AnqsModel::log_psi (model.cpp:262-271) per key, keys [n][ceil(N/64)];
+ * out-of-sector keys give (-inf, 0) like the reference. */
+int qvmc_cuda_log_psi(qvmc_model_t m, int64_t n, const uint64_t* keys, int mem, double* out_log_amp,
+                      double* out_phase);
+/* fill_amplitudes (proj/src/sampler.cpp:104-120): log_psi of every key and
+ * out_norm2 = (norm, log_norm) = logsumexp(log_probs), out_norm2 on the host.
+ * Synchronises. */
+int qvmc_cuda_fill_amplitudes(qvmc_model_t m, int64_t n, const uint64_t* keys, const double* log_probs, int mem,
+                              double* out_log_amp, double* out_phase, double* out_norm2);
+int qvmc_cuda_model_synchronize(qvmc_model_t m);
+
 const char* qvmc_cuda_last_error(void);
 /* Kernels launched by this library since load (for launch accounting). */
 uint64_t qvmc_cuda_launch_count(void);

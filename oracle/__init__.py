@@ -193,6 +193,15 @@ def rlib():
         L.qref_rng_uniform_int.argtypes = [_P, _U64]
         L.qref_rng_bits64.restype = _U64
         L.qref_rng_bits64.argtypes = [_P]
+        L.qref_model_create.argtypes = [_INT, _INT, _INT, _INT, _INT, C.POINTER(_P)]
+        L.qref_model_free.argtypes = [_P]
+        L.qref_model_n_params.restype = _I64
+        L.qref_model_n_params.argtypes = [_P]
+        L.qref_model_init_params.argtypes = [_P, _U64]
+        L.qref_model_get_params.argtypes = [_P, _P]
+        L.qref_model_set_params.argtypes = [_P, _I64, _P]
+        L.qref_model_log_psi.argtypes = [_P, _I64, _INT, _P, _INT, _P, _P]
+        L.qref_fill_amplitudes.argtypes = [_P, _I64, _INT, _P, _P, _INT, _P, _P, _P]
         _rlib = L
     return _rlib
 
@@ -332,3 +341,50 @@ class RefRng:
 
     def uniform_int(self, n):
         return int(rlib().qref_rng_uniform_int(self._r, n))
+
+
+class RefModel:
+    """The reference AnqsModel (model.cpp) compiled from the reference sources."""
+
+    def __init__(self, n_qubits, bits_per_qudit, n_electrons, spin_constraint=False, hidden=64):
+        self.n_qubits = n_qubits
+        self.W = (n_qubits + 63) // 64
+        h = _P()
+        _rcheck(rlib().qref_model_create(n_qubits, bits_per_qudit, n_electrons, int(spin_constraint), hidden,
+                                         C.byref(h)))
+        self._h = h
+        self.n_params = int(rlib().qref_model_n_params(h))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            rlib().qref_model_free(self._h)
+            self._h = None
+
+    def init_params(self, seed: int) -> None:
+        _rcheck(rlib().qref_model_init_params(self._h, seed))
+
+    @property
+    def params(self) -> np.ndarray:
+        p = np.zeros(self.n_params)
+        _rcheck(rlib().qref_model_get_params(self._h, _ptr(p)))
+        return p
+
+    def set_params(self, p) -> None:
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        _rcheck(rlib().qref_model_set_params(self._h, p.size, _ptr(p)))
+
+    def log_psi(self, keys, threads: int = 1):
+        keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, self.W)
+        n = keys.shape[0]
+        la, ph = np.zeros(n), np.zeros(n)
+        _rcheck(rlib().qref_model_log_psi(self._h, n, self.W, _ptr(keys), threads, _ptr(la), _ptr(ph)))
+        return la, ph
+
+    def fill_amplitudes(self, keys, log_probs, threads: int = 1):
+        keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, self.W)
+        lp = np.ascontiguousarray(log_probs, dtype=np.float64)
+        n = keys.shape[0]
+        la, ph, out2 = np.zeros(n), np.zeros(n), np.zeros(2)
+        _rcheck(rlib().qref_fill_amplitudes(self._h, n, self.W, _ptr(keys), _ptr(lp), threads, _ptr(la), _ptr(ph),
+                                            _ptr(out2)))
+        return la, ph, float(out2[0]), float(out2[1])

@@ -1,0 +1,131 @@
+"""CPU restatement of the reference amplitude evaluation — TEST INFRASTRUCTURE ONLY.
+
+numpy restatement (fp64, vectorised over samples) of ``AnqsModel`` and
+``fill_amplitudes`` from /root/reference/proj:
+
+* ``QuditLayout::make``          src/model.cpp:33-45
+* parameter block layout         src/model.cpp:65-80 (per qudit: amplitude block, then phase block;
+                                 W1 [hidden][n] row-major, b1, W2 [hidden][hidden], b2, W3 [2^k][hidden], b3)
+* ``QuditInfo``                  src/model.cpp:82-93
+* ``allowed_values``             src/model.cpp:129-151
+* ``encode_prefix``              src/model.cpp:153-158 (+/-1 on the prefix bits, 0 elsewhere)
+* ``mlp_forward``                src/model.cpp:160-175 (tanh, residual h1 into the 2nd pre-activation)
+* ``conditional``                src/model.cpp:203-252 (mean shift, log-softmax of 2*amp over allowed values)
+* ``in_sector`` / ``log_psi``    src/model.cpp:254-271
+* ``fill_amplitudes``            src/sampler.cpp:104-120
+
+It is pinned against the reference itself (``oracle/_ref``, model.cpp and
+sampler.cpp compiled with the Eigen shim) by tests/test_model.py. Only tests/,
+``__graft_entry__.smoke()`` and bench.py's CPU legs may import it.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def layout(n_qubits: int, bits_per_qudit: int):
+    """QuditLayout::make (model.cpp:33-45): (offsets, sizes)."""
+    if not 1 <= n_qubits <= 256:
+        raise ValueError("QuditLayout: qubit count out of range")
+    if not 1 <= bits_per_qudit <= 8:
+        raise ValueError("QuditLayout: bits_per_qudit must be in [1, 8]")
+    offs = list(range(0, n_qubits, bits_per_qudit))
+    return offs, [min(bits_per_qudit, n_qubits - o) for o in offs]
+
+
+class ModelOracle:
+    def __init__(self, n_qubits, bits_per_qudit, n_electrons, spin_constraint, hidden, params):
+        self.n, self.hidden = n_qubits, hidden
+        self.n_e, self.spin = n_electrons, bool(spin_constraint)
+        self.n_up = n_electrons // 2 if self.spin else 0
+        self.offsets, self.sizes = layout(n_qubits, bits_per_qudit)
+        self.params = np.asarray(params, dtype=np.float64)
+        self.blocks = []  # per qudit: (amp, phase), each a dict of views
+        cur = 0
+        for o, k in zip(self.offsets, self.sizes):
+            pair = []
+            for _ in range(2):  # model.cpp:65-80
+                b = {}
+                for name, shape in (("W1", (hidden, n_qubits)), ("b1", (hidden,)), ("W2", (hidden, hidden)),
+                                    ("b2", (hidden,)), ("W3", (1 << k, hidden)), ("b3", (1 << k,))):
+                    size = int(np.prod(shape))
+                    b[name] = self.params[cur:cur + size].reshape(shape)
+                    cur += size
+                pair.append(b)
+            self.blocks.append(pair)
+        self.n_params = cur
+        if self.params.size != cur:
+            raise ValueError("params size mismatch")
+
+    def _info(self, j):  # model.cpp:82-93
+        o, k = self.offsets[j], self.sizes[j]
+        rem_after = self.n - o - k
+        rem_up_after = sum(1 for i in range(o + k, self.n) if i % 2 == 0)
+        up_value_mask = 0
+        for t in range(k):
+            if (o + t) % 2 == 0:
+                up_value_mask |= 1 << (k - 1 - t)
+        return rem_after, rem_up_after, up_value_mask
+
+    def allowed(self, j, prefix_weight, prefix_up):
+        """allowed_values (model.cpp:129-151), vectorised: bool [N][2^k]."""
+        k = self.sizes[j]
+        rem_after, rem_up_after, upm = self._info(j)
+        v = np.arange(1 << k)
+        pv = np.array([bin(a).count("1") for a in v])
+        pu = np.array([bin(a & upm).count("1") for a in v])
+        w = prefix_weight[:, None] + pv[None, :]
+        ok = (w <= self.n_e) & (w + rem_after >= self.n_e)
+        if self.spin:
+            wu = prefix_up[:, None] + pu[None, :]
+            wd = w - wu
+            n_down = self.n_e - self.n_up
+            rem_down = rem_after - rem_up_after
+            ok &= (wu <= self.n_up) & (wu + rem_up_after >= self.n_up) & (wd <= n_down) & (wd + rem_down >= n_down)
+        return ok
+
+    @staticmethod
+    def _mlp(b, e):  # model.cpp:160-175
+        h1 = np.tanh(e @ b["W1"].T + b["b1"])
+        h2 = np.tanh(h1 @ b["W2"].T + b["b2"] + h1)
+        return h2 @ b["W3"].T + b["b3"]
+
+    def log_psi(self, keys):
+        """log_psi (model.cpp:262-271) for keys uint64 [N][W]: (log_amp, phase)."""
+        keys = np.ascontiguousarray(keys, dtype=np.uint64)
+        N = keys.shape[0]
+        bits = np.unpackbits(keys.view(np.uint8).reshape(N, -1), axis=1, bitorder="little")[:, :self.n].astype(np.int64)
+        la = np.zeros(N)
+        ph = np.zeros(N)
+        pop = bits.sum(1)
+        ins = pop == self.n_e  # in_sector (model.cpp:254-259)
+        if self.spin:
+            ins &= bits[:, 0::2].sum(1) == self.n_up
+        for j, (o, k) in enumerate(zip(self.offsets, self.sizes)):
+            e = np.zeros((N, self.n))
+            e[:, :o] = np.where(bits[:, :o] == 1, 1.0, -1.0)  # encode_prefix
+            amp = self._mlp(self.blocks[j][0], e)
+            phase = self._mlp(self.blocks[j][1], e)
+            amp = amp - amp.mean(axis=1, keepdims=True)  # global activation
+            ok = self.allowed(j, bits[:, :o].sum(1), bits[:, 0:o:2].sum(1))
+            two = np.where(ok, 2.0 * amp, -np.inf)
+            mx = two.max(axis=1)
+            with np.errstate(invalid="ignore", over="ignore"):
+                lse = mx + np.log(np.where(ok, np.exp(two - mx[:, None]), 0.0).sum(1))
+            v = np.zeros(N, dtype=np.int64)
+            for t in range(k):  # extract_bits (basis_vector.cpp:40-45): qubit o+t -> bit k-1-t
+                v |= bits[:, o + t] << (k - 1 - t)
+            rows = np.arange(N)
+            la += 0.5 * (2.0 * amp[rows, v] - lse)
+            ph += phase[rows, v]
+        la = np.where(ins, la, -np.inf)
+        ph = np.where(ins, ph, 0.0)
+        return la, ph
+
+    def fill_amplitudes(self, keys, log_probs):
+        """fill_amplitudes (sampler.cpp:104-120): (log_amps, phases, norm, log_norm)."""
+        la, ph = self.log_psi(keys)
+        lp = np.asarray(log_probs, dtype=np.float64)
+        mx = lp.max()
+        log_norm = mx + np.log(np.exp(lp - mx).sum())
+        return la, ph, float(np.exp(log_norm)), float(log_norm)

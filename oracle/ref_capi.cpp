@@ -26,6 +26,8 @@
 #include "qvmc/coupling.hpp"
 #include "qvmc/energy.hpp"
 #include "qvmc/hamiltonian.hpp"
+#include "qvmc/model.hpp"
+#include "qvmc/parallel.hpp"
 #include "qvmc/rng.hpp"
 #include "qvmc/sampler.hpp"
 #include "qvmc/synthetic.hpp"
@@ -362,5 +364,64 @@ void* qref_rng_new(std::uint64_t seed, std::uint32_t stream) { return new RngBox
 void qref_rng_free(void* r) { delete static_cast<RngBox*>(r); }
 std::uint64_t qref_rng_uniform_int(void* r, std::uint64_t n) { return static_cast<RngBox*>(r)->rng.uniform_int(n); }
 std::uint64_t qref_rng_bits64(void* r) { return static_cast<RngBox*>(r)->rng.bits64(); }
+
+// ---- AnqsModel (model.cpp) and fill_amplitudes (sampler.cpp:104-120): the
+// amplitude evaluation that feeds the local-energy path.
+int qref_model_create(int n_qubits, int bits_per_qudit, int n_electrons, int spin_constraint, int hidden,
+                      void** out) {
+  return guarded([&] {
+    *out = new qvmc::AnqsModel(qvmc::QuditLayout::make(n_qubits, bits_per_qudit),
+                               qvmc::SectorConstraint{n_electrons, spin_constraint != 0}, hidden);
+  });
+}
+void qref_model_free(void* m) { delete static_cast<qvmc::AnqsModel*>(m); }
+std::int64_t qref_model_n_params(void* m) { return static_cast<qvmc::AnqsModel*>(m)->n_params(); }
+int qref_model_init_params(void* m, std::uint64_t seed) {
+  return guarded([&] { static_cast<qvmc::AnqsModel*>(m)->init_params(seed); });
+}
+int qref_model_get_params(void* m, double* out) {
+  return guarded([&] {
+    const auto& p = static_cast<qvmc::AnqsModel*>(m)->params();
+    for (Eigen::Index i = 0; i < p.size(); ++i) out[i] = p[i];
+  });
+}
+int qref_model_set_params(void* m, std::int64_t n, const double* in) {
+  return guarded([&] {
+    Eigen::VectorXd p(n);
+    for (std::int64_t i = 0; i < n; ++i) p[i] = in[i];
+    static_cast<qvmc::AnqsModel*>(m)->set_params(p);
+  });
+}
+// AnqsModel::log_psi (model.cpp:262-271) per vector, parallel_for over threads
+int qref_model_log_psi(void* m, std::int64_t n, int n_words, const std::uint64_t* keys, int threads,
+                       double* out_log_amp, double* out_phase) {
+  return guarded([&] {
+    const auto& model = *static_cast<qvmc::AnqsModel*>(m);
+    const auto vs = make_batch(model.layout().n_qubits, n_words, n, keys);
+    qvmc::parallel_for(static_cast<int>(n), threads, [&](int i) {
+      const auto a = model.log_psi(vs[static_cast<std::size_t>(i)]);
+      out_log_amp[i] = a.log_amp;
+      out_phase[i] = a.phase;
+    });
+  });
+}
+// fill_amplitudes (sampler.cpp:104-120); out2 = (norm, log_norm)
+int qref_fill_amplitudes(void* m, std::int64_t n, int n_words, const std::uint64_t* keys, const double* log_probs,
+                         int threads, double* out_log_amp, double* out_phase, double* out2) {
+  return guarded([&] {
+    const auto& model = *static_cast<qvmc::AnqsModel*>(m);
+    qvmc::SampleBatch batch;
+    batch.vectors = make_batch(model.layout().n_qubits, n_words, n, keys);
+    batch.log_probs.resize(n);
+    for (std::int64_t i = 0; i < n; ++i) batch.log_probs[i] = log_probs[i];
+    qvmc::fill_amplitudes(batch, model, threads);
+    for (std::int64_t i = 0; i < n; ++i) {
+      out_log_amp[i] = batch.log_amps[i];
+      out_phase[i] = batch.phases[i];
+    }
+    out2[0] = batch.norm;
+    out2[1] = batch.log_norm;
+  });
+}
 
 }  // extern "C"

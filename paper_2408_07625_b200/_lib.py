@@ -80,6 +80,14 @@ SIGNATURES = [
     ("qvmc_cuda_launch_count", _U64, []),
     ("qvmc_synth_jw_hamiltonian", _INT, [_INT, _I64, _U64, _P, _P, _P, _P, C.POINTER(_I64)]),
     ("qvmc_synth_near_hf_samples", _INT, [_INT, _INT, _I64, _U64, _P]),
+    ("qvmc_cuda_model_create", _INT, [_INT, _INT, _INT, _INT, _INT, _INT, C.POINTER(_P)]),
+    ("qvmc_cuda_model_destroy", _INT, [_P]),
+    ("qvmc_cuda_model_n_params", _INT, [_P, C.POINTER(_I64)]),
+    ("qvmc_cuda_model_set_params", _INT, [_P, _I64, _P]),
+    ("qvmc_cuda_model_set_stream", _INT, [_P, _P]),
+    ("qvmc_cuda_log_psi", _INT, [_P, _I64, _P, _INT, _P, _P]),
+    ("qvmc_cuda_fill_amplitudes", _INT, [_P, _I64, _P, _P, _INT, _P, _P, _P]),
+    ("qvmc_cuda_model_synchronize", _INT, [_P]),
 ]
 
 _lib = None

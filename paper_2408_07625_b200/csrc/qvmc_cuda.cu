@@ -25,6 +25,7 @@
 #include "qvmc_bucket.cuh"
 #include "qvmc_join.cuh"
 #include "qvmc_kernels.cuh"
+#include "qvmc_model.cuh"
 
 using namespace qvmc_b200;
 
@@ -1737,6 +1738,240 @@ int qvmc_synth_near_hf_samples(int n_qubits, int n_electrons, int64_t n_unq, uin
   return guarded([&] {
     if (!keys || n_unq < 0) fail(QVMC_ERR_INVALID_ARGUMENT, "null or negative argument");
     synth_near_hf_samples(n_qubits, n_electrons, n_unq, seed, keys);
+  });
+}
+
+
+// ------------------------------------------------------------------ amplitude model
+// AnqsModel (model.cpp) on the device: layout + sector checks as in the
+// reference constructor (model.cpp:33-45, :47-97), parameters re-laid out per
+// set_params (qvmc_model.cuh BlockLayout).
+}  // extern "C"
+
+struct qvmc_model_s {
+  int device = 0;
+  int n = 0, W = 0, bits = 6, n_e = 0, spin = 0, n_up = 0, hidden = 64, n_qudits = 0;
+  int64_t n_params = 0;
+  bool has_params = false;
+  cudaStream_t own = nullptr, stream = nullptr;
+  DBuf P, keys, la, ph, lp, part, out2;
+};
+
+namespace {
+void check_model(qvmc_model_s* m) {
+  if (!m) fail(QVMC_ERR_INVALID_ARGUMENT, "null model handle");
+}
+
+int64_t model_param_count(int n, int bits, int hidden) {
+  int64_t c = 0;
+  for (int o = 0; o < n; o += bits) {
+    const int out = 1 << std::min(bits, n - o);
+    c += 2 * (static_cast<int64_t>(hidden) * n + hidden + static_cast<int64_t>(hidden) * hidden + hidden +
+              static_cast<int64_t>(out) * hidden + out);
+  }
+  return c;
+}
+
+void launch_log_psi(qvmc_model_s* m, const uint64_t* keys, int64_t n, double* la, double* ph) {
+  if (n == 0) return;
+  using namespace qvmc_model;
+  ModelView V{m->P.as<double>(), m->n, m->n_qudits, m->bits, m->n_e, m->spin, m->n_up};
+  const int grid = static_cast<int>((n + kTile - 1) / kTile);
+  const size_t dyn = static_cast<size_t>(3 * kHid * kTile) * sizeof(double);
+  DISPATCH_W(m->W, {
+    ck(cudaFuncSetAttribute(k_log_psi<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)),
+       "smem attribute");
+    k_log_psi<WW><<<grid, kMThreads, dyn, m->stream>>>(V, keys, n, la, ph);
+  });
+  ck_launch("log_psi");
+}
+}  // namespace
+
+extern "C" {
+
+int qvmc_cuda_model_create(int n_qubits, int bits_per_qudit, int n_electrons, int spin_constraint, int hidden,
+                           int device, qvmc_model_t* out) {
+  return guarded([&] {
+    if (!out) fail(QVMC_ERR_INVALID_ARGUMENT, "null output handle");
+    // QuditLayout::make (model.cpp:33-37), AnqsModel::AnqsModel (model.cpp:49-58)
+    if (n_qubits < 1 || n_qubits > 256) fail(QVMC_ERR_INVALID_ARGUMENT, "QuditLayout: qubit count out of range");
+    if (bits_per_qudit < 1 || bits_per_qudit > 8)
+      fail(QVMC_ERR_INVALID_ARGUMENT, "QuditLayout: bits_per_qudit must be in [1, 8]");
+    if (n_electrons < 0 || n_electrons > n_qubits) fail(QVMC_ERR_INVALID_ARGUMENT, "AnqsModel: electron count out of range");
+    if (spin_constraint && n_electrons % 2 != 0)
+      fail(QVMC_ERR_INVALID_ARGUMENT, "AnqsModel: spin constraint requires even n_electrons");
+    if (hidden < 1) fail(QVMC_ERR_INVALID_ARGUMENT, "AnqsModel: hidden width must be positive");
+    if (hidden != qvmc_model::kHid || bits_per_qudit > qvmc_model::kMaxK)
+      fail(QVMC_ERR_INVALID_ARGUMENT, "device amplitude path supports hidden = 64 and bits_per_qudit <= 6");
+    int n_dev = 0;
+    if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0) fail(QVMC_ERR_NO_DEVICE, "no CUDA device visible");
+    if (device < 0 || device >= n_dev) fail(QVMC_ERR_INVALID_ARGUMENT, "device ordinal out of range");
+    DeviceGuard dg(device);
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10) fail(QVMC_ERR_NO_DEVICE, "libqvmc_cuda is built for sm_100a (B200) only");
+    auto m = std::make_unique<qvmc_model_s>();
+    m->device = device;
+    m->n = n_qubits;
+    m->W = (n_qubits + 63) / 64;
+    m->bits = bits_per_qudit;
+    m->n_e = n_electrons;
+    m->spin = spin_constraint ? 1 : 0;
+    m->n_up = spin_constraint ? n_electrons / 2 : 0;
+    m->hidden = hidden;
+    m->n_qudits = (n_qubits + bits_per_qudit - 1) / bits_per_qudit;
+    m->n_params = model_param_count(n_qubits, bits_per_qudit, hidden);
+    ck(cudaStreamCreateWithFlags(&m->own, cudaStreamNonBlocking), "stream create");
+    m->stream = m->own;
+    *out = m.release();
+  });
+}
+
+int qvmc_cuda_model_destroy(qvmc_model_t m) {
+  return guarded([&] {
+    if (!m) return;
+    DeviceGuard dg(m->device);
+    if (m->own) {
+      cudaStreamSynchronize(m->own);
+      cudaStreamDestroy(m->own);
+    }
+    delete m;
+  });
+}
+
+int qvmc_cuda_model_n_params(qvmc_model_t m, int64_t* out) {
+  return guarded([&] {
+    check_model(m);
+    if (!out) fail(QVMC_ERR_INVALID_ARGUMENT, "null output");
+    *out = m->n_params;
+  });
+}
+
+int qvmc_cuda_model_set_stream(qvmc_model_t m, void* stream) {
+  return guarded([&] {
+    check_model(m);
+    m->stream = stream ? static_cast<cudaStream_t>(stream) : m->own;
+  });
+}
+
+// AnqsModel::set_params (model.cpp:99-103): host vector in the reference's flat
+// layout (model.cpp:65-80); re-laid out for the kernel and uploaded.
+int qvmc_cuda_model_set_params(qvmc_model_t m, int64_t n_params, const double* params) {
+  return guarded([&] {
+    check_model(m);
+    if (n_params != m->n_params) fail(QVMC_ERR_INVALID_ARGUMENT, "AnqsModel::set_params: size mismatch");
+    if (!params) fail(QVMC_ERR_INVALID_ARGUMENT, "null params");
+    using namespace qvmc_model;
+    const int n = m->n, H = kHid;
+    const BlockLayout L{n};
+    std::vector<double> dev(static_cast<size_t>(m->n_qudits) * 2 * L.size(), 0.0);
+    int64_t cur = 0;
+    for (int j = 0; j < m->n_qudits; ++j) {
+      const int off = j * m->bits, k = std::min(m->bits, n - off), out = 1 << k;
+      for (int hd = 0; hd < 2; ++hd) {
+        const double* w1 = params + cur;
+        const double* b1 = w1 + static_cast<int64_t>(H) * n;
+        const double* w2 = b1 + H;
+        const double* b2 = w2 + H * H;
+        const double* w3 = b2 + H;
+        const double* b3 = w3 + out * H;
+        cur += static_cast<int64_t>(H) * n + H + H * H + H + out * H + out;
+        double* B = dev.data() + static_cast<size_t>(2 * j + hd) * L.size();
+        for (int h = 0; h < H; ++h) {
+          double c = 0.0;
+          for (int i = 0; i < n; ++i) {
+            B[L.w1t() + i * H + h] = w1[static_cast<int64_t>(h) * n + i];
+            if (i < off) c += w1[static_cast<int64_t>(h) * n + i];
+          }
+          B[L.csum() + h] = c;
+          B[L.b1() + h] = b1[h];
+          B[L.b2() + h] = b2[h];
+          for (int kk = 0; kk < H; ++kk) B[L.w2t() + kk * H + h] = w2[h * H + kk];
+        }
+        for (int v = 0; v < out; ++v) {
+          B[L.b3() + v] = b3[v];
+          for (int kk = 0; kk < H; ++kk) B[L.w3t() + kk * H + v] = w3[v * H + kk];
+        }
+      }
+    }
+    if (cur != m->n_params) fail(QVMC_ERR_RUNTIME, "parameter layout mismatch");
+    DeviceGuard dg(m->device);
+    m->P.ensure(dev.size() * sizeof(double));
+    ck(cudaMemcpyAsync(m->P.p, dev.data(), dev.size() * sizeof(double), cudaMemcpyHostToDevice, m->stream), "H2D params");
+    ck(cudaStreamSynchronize(m->stream), "sync");  // the host staging vector goes out of scope
+    m->has_params = true;
+  });
+}
+
+// AnqsModel::log_psi (model.cpp:262-271) for every key: the loop of
+// fill_amplitudes (sampler.cpp:104-112).
+int qvmc_cuda_log_psi(qvmc_model_t m, int64_t n, const uint64_t* keys, int mem, double* out_log_amp,
+                      double* out_phase) {
+  return guarded([&] {
+    check_model(m);
+    check_mem(mem);
+    if (n < 0) fail(QVMC_ERR_INVALID_ARGUMENT, "negative batch size");
+    if (n > 0 && (!keys || !out_log_amp || !out_phase)) fail(QVMC_ERR_INVALID_ARGUMENT, "null array");
+    if (!m->has_params) fail(QVMC_ERR_INVALID_ARGUMENT, "model parameters not set");
+    DeviceGuard dg(m->device);
+    const uint64_t* dk = keys;
+    double *dla = out_log_amp, *dph = out_phase;
+    if (mem == QVMC_MEM_HOST) {
+      m->keys.ensure(std::max<size_t>(n * m->W * 8, 16));
+      m->la.ensure(std::max<size_t>(n * 8, 16));
+      m->ph.ensure(std::max<size_t>(n * 8, 16));
+      if (n) ck(cudaMemcpyAsync(m->keys.p, keys, n * m->W * 8, cudaMemcpyHostToDevice, m->stream), "H2D keys");
+      dk = m->keys.as<uint64_t>();
+      dla = m->la.as<double>();
+      dph = m->ph.as<double>();
+    }
+    launch_log_psi(m, dk, n, dla, dph);
+    if (mem == QVMC_MEM_HOST) {
+      if (n) {
+        ck(cudaMemcpyAsync(out_log_amp, dla, n * 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
+        ck(cudaMemcpyAsync(out_phase, dph, n * 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
+      }
+      ck(cudaStreamSynchronize(m->stream), "sync");
+    }
+  });
+}
+
+// fill_amplitudes (sampler.cpp:104-120): log_psi of every key plus
+// (norm, log_norm) = logsumexp of the sampler's log_probs. out_norm2 is a host
+// pointer in either memory kind (the call synchronises).
+int qvmc_cuda_fill_amplitudes(qvmc_model_t m, int64_t n, const uint64_t* keys, const double* log_probs, int mem,
+                              double* out_log_amp, double* out_phase, double* out_norm2) {
+  return guarded([&] {
+    check_model(m);
+    check_mem(mem);
+    if (n < 1) fail(QVMC_ERR_INVALID_ARGUMENT, "empty sample batch");
+    if (!log_probs || !out_norm2) fail(QVMC_ERR_INVALID_ARGUMENT, "null array");
+    const int st = qvmc_cuda_log_psi(m, n, keys, mem, out_log_amp, out_phase);
+    if (st != QVMC_OK) throw Failure{st, g_error};
+    DeviceGuard dg(m->device);
+    const double* dlp = log_probs;
+    if (mem == QVMC_MEM_HOST) {
+      m->lp.ensure(n * 8);
+      ck(cudaMemcpyAsync(m->lp.p, log_probs, n * 8, cudaMemcpyHostToDevice, m->stream), "H2D log_probs");
+      dlp = m->lp.as<double>();
+    }
+    using namespace qvmc_model;
+    m->part.ensure(kLseBlocks * sizeof(double2));
+    m->out2.ensure(2 * sizeof(double));
+    k_lse_partial<<<kLseBlocks, 256, 0, m->stream>>>(dlp, n, m->part.as<double2>());
+    ck_launch("lse partial");
+    k_lse_final<<<1, 32, 0, m->stream>>>(m->part.as<double2>(), kLseBlocks, m->out2.as<double>());
+    ck_launch("lse final");
+    ck(cudaMemcpyAsync(out_norm2, m->out2.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, m->stream), "D2H norm");
+    ck(cudaStreamSynchronize(m->stream), "sync");
+  });
+}
+
+int qvmc_cuda_model_synchronize(qvmc_model_t m) {
+  return guarded([&] {
+    check_model(m);
+    DeviceGuard dg(m->device);
+    ck(cudaStreamSynchronize(m->stream), "sync");
   });
 }
 

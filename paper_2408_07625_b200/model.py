@@ -1,0 +1,185 @@
+"""The amplitude model on the device (reference: proj/include/qvmc/model.hpp, proj/src/model.cpp).
+
+Mirrors the reference interface for the stage that feeds the local-energy
+path: ``QuditLayout`` (model.hpp:21-30), ``SectorConstraint``
+(model.hpp:32-37), ``AnqsModel`` (model.hpp:47-148: ``n_params``, ``params``,
+``set_params``, ``log_psi``, ``in_sector``), the text checkpoint
+(``save_checkpoint`` model.cpp:345-357 / ``load_checkpoint`` model.cpp:359-396)
+and ``fill_amplitudes`` (sampler.cpp:104-120). ``log_psi`` / ``fill_amplitudes``
+run in ``k_log_psi`` (csrc/qvmc_model.cuh) through the C ABI; there is no CPU
+path. Errors follow the reference: ``std::invalid_argument`` -> ValueError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List
+
+import numpy as np
+
+from . import _lib
+from .hamiltonian import _ptr
+
+
+@dataclass
+class QuditLayout:
+    """QuditLayout::make (model.cpp:33-45)."""
+    n_qubits: int = 0
+    bits_per_qudit: int = 6
+    sizes: List[int] = field(default_factory=list)
+    offsets: List[int] = field(default_factory=list)
+
+    @staticmethod
+    def make(n_qubits: int, bits_per_qudit: int = 6) -> "QuditLayout":
+        if not 1 <= n_qubits <= 256:
+            raise ValueError("QuditLayout: qubit count out of range")
+        if not 1 <= bits_per_qudit <= 8:
+            raise ValueError("QuditLayout: bits_per_qudit must be in [1, 8]")
+        offs = list(range(0, n_qubits, bits_per_qudit))
+        return QuditLayout(n_qubits, bits_per_qudit, [min(bits_per_qudit, n_qubits - o) for o in offs], offs)
+
+    def count(self) -> int:
+        return len(self.sizes)
+
+
+@dataclass
+class SectorConstraint:
+    """SectorConstraint (model.hpp:32-37)."""
+    n_electrons: int = 0
+    spin_constraint: bool = False
+
+
+class AnqsModel:
+    """Device-resident AnqsModel: parameters in the reference's flat layout (model.cpp:65-80)."""
+
+    def __init__(self, layout: QuditLayout, sector: SectorConstraint, hidden: int = 64, device: int = 0):
+        self.layout, self.sector, self.hidden, self.device = layout, sector, hidden, device
+        self.W = (layout.n_qubits + 63) // 64
+        h = C.c_void_p()
+        _lib.check(_lib.lib().qvmc_cuda_model_create(layout.n_qubits, layout.bits_per_qudit, sector.n_electrons,
+                                                     int(sector.spin_constraint), hidden, device, C.byref(h)))
+        self._h = h
+        n = C.c_int64()
+        _lib.check(_lib.lib().qvmc_cuda_model_n_params(h, C.byref(n)))
+        self._n_params = int(n.value)
+        self._params = np.zeros(self._n_params)
+        _lib.check(_lib.lib().qvmc_cuda_model_set_params(h, self._n_params, _ptr(self._params)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.lib().qvmc_cuda_model_destroy(h)
+            self._h = None
+
+    def n_params(self) -> int:
+        return self._n_params
+
+    @property
+    def params(self) -> np.ndarray:
+        return self._params.copy()
+
+    def set_params(self, p) -> None:
+        """AnqsModel::set_params (model.cpp:99-103)."""
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        if p.shape != (self._n_params,):
+            raise ValueError("AnqsModel::set_params: size mismatch")
+        _lib.check(_lib.lib().qvmc_cuda_model_set_params(self._h, p.size, _ptr(p)))
+        self._params = p.copy()
+
+    def set_stream(self, stream) -> None:
+        """Run on a torch/CUDA stream (an int handle or None for the model's own)."""
+        _lib.check(_lib.lib().qvmc_cuda_model_set_stream(self._h, C.c_void_p(stream or 0)))
+
+    def in_sector(self, keys: np.ndarray) -> np.ndarray:
+        """AnqsModel::in_sector (model.cpp:254-259), vectorised (host arithmetic on the keys)."""
+        keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, self.W)
+        pop = np.zeros(keys.shape[0], dtype=np.int64)
+        up = np.zeros(keys.shape[0], dtype=np.int64)
+        for w in range(self.W):
+            pop += np.bitwise_count(keys[:, w]).astype(np.int64)
+            up += np.bitwise_count(keys[:, w] & np.uint64(0x5555555555555555)).astype(np.int64)
+        ok = pop == self.sector.n_electrons
+        if self.sector.spin_constraint:
+            ok &= up == self.sector.n_electrons // 2
+        return ok
+
+    def log_psi(self, keys: np.ndarray):
+        """AnqsModel::log_psi (model.cpp:262-271) for every key: (log|psi|, phase) arrays."""
+        keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, self.W)
+        n = keys.shape[0]
+        la, ph = np.empty(n), np.empty(n)
+        _lib.check(_lib.lib().qvmc_cuda_log_psi(self._h, n, _ptr(keys), _lib.QVMC_MEM_HOST, _ptr(la), _ptr(ph)))
+        return la, ph
+
+    def log_psi_device(self, keys_ptr: int, n: int, out_log_amp_ptr: int, out_phase_ptr: int) -> None:
+        """Device pointers (e.g. torch tensors' data_ptr()), enqueued on the model's stream."""
+        _lib.check(_lib.lib().qvmc_cuda_log_psi(self._h, n, C.c_void_p(keys_ptr), _lib.QVMC_MEM_DEVICE,
+                                                C.c_void_p(out_log_amp_ptr), C.c_void_p(out_phase_ptr)))
+
+    def synchronize(self) -> None:
+        _lib.check(_lib.lib().qvmc_cuda_model_synchronize(self._h))
+
+    def save_checkpoint(self, seed: int) -> str:
+        """Text checkpoint, format of AnqsModel::save_checkpoint (model.cpp:345-357)."""
+        lines = ["qvmc-checkpoint v1", f"n_qubits {self.layout.n_qubits}",
+                 f"bits_per_qudit {self.layout.bits_per_qudit}", f"hidden {self.hidden}",
+                 f"n_electrons {self.sector.n_electrons}", f"spin_constraint {int(self.sector.spin_constraint)}",
+                 f"seed {seed}", f"n_params {self._n_params}"]
+        lines += [_hexfloat(float(v)) for v in self._params]
+        return "\n".join(lines) + "\n"
+
+
+def _hexfloat(v: float) -> str:
+    """std::hexfloat spelling of a double (e.g. 0x1.8p+1), as the reference writes it."""
+    if v == 0.0:
+        return "-0x0p+0" if np.signbit(v) else "0x0p+0"
+    h = float.hex(v)  # '0x1.8000000000000p+1'
+    sign = "-" if h.startswith("-") else ""
+    mant, exp = h.lstrip("-")[2:].split("p")
+    mant = mant.rstrip("0").rstrip(".")
+    return f"{sign}0x{mant}p{exp if exp.startswith('-') else exp}"
+
+
+def load_checkpoint(text: str, device: int = 0):
+    """load_checkpoint (model.cpp:359-396): (AnqsModel, seed); RuntimeError on malformed input."""
+    toks = text.split()
+    if not text.startswith("qvmc-checkpoint v1"):
+        raise RuntimeError("checkpoint: bad magic line")
+    it = iter(toks[2:])
+
+    def kv(key):
+        try:
+            k, v = next(it), next(it)
+        except StopIteration:
+            raise RuntimeError(f"checkpoint: expected key '{key}'") from None
+        if k != key:
+            raise RuntimeError(f"checkpoint: expected key '{key}'")
+        return int(v)
+
+    n_qubits, bits, hidden = kv("n_qubits"), kv("bits_per_qudit"), kv("hidden")
+    n_e, spin, seed, n_params = kv("n_electrons"), kv("spin_constraint") != 0, kv("seed"), kv("n_params")
+    model = AnqsModel(QuditLayout.make(n_qubits, bits), SectorConstraint(n_e, spin), hidden, device)
+    if model.n_params() != n_params:
+        raise RuntimeError("checkpoint: parameter count mismatch")
+    vals = []
+    for _ in range(n_params):
+        try:
+            vals.append(float.fromhex(next(it)))
+        except StopIteration:
+            raise RuntimeError("checkpoint: truncated parameters") from None
+    model.set_params(np.array(vals))
+    return model, seed
+
+
+def fill_amplitudes(batch, model: AnqsModel, threads: int = 1) -> None:
+    """fill_amplitudes (sampler.cpp:104-120): log_amps, phases, norm, log_norm of a SampleBatch, on the device."""
+    keys = np.ascontiguousarray(batch.vectors, dtype=np.uint64).reshape(-1, model.W)
+    lp = np.ascontiguousarray(batch.log_probs, dtype=np.float64)
+    n = keys.shape[0]
+    if lp.shape != (n,):
+        raise ValueError("fill_amplitudes: log_probs size mismatch")
+    la, ph, out2 = np.empty(n), np.empty(n), np.zeros(2)
+    _lib.check(_lib.lib().qvmc_cuda_fill_amplitudes(model._h, n, _ptr(keys), _ptr(lp), _lib.QVMC_MEM_HOST,
+                                                    _ptr(la), _ptr(ph), _ptr(out2)))
+    batch.log_amps, batch.phases = la, ph
+    batch.norm, batch.log_norm = float(out2[0]), float(out2[1])
