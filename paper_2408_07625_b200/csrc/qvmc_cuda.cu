@@ -1753,8 +1753,10 @@ struct qvmc_model_s {
   int n = 0, W = 0, bits = 6, n_e = 0, spin = 0, n_up = 0, hidden = 64, n_qudits = 0;
   int64_t n_params = 0;
   bool has_params = false;
+  bool tiled = true;  // warp-tiled (qudit, head) CTAs (default); QVMC_MODEL_TILED=0: one CTA per sample tile
+  int sms = 148;
   cudaStream_t own = nullptr, stream = nullptr;
-  DBuf P, keys, la, ph, lp, part, out2;
+  DBuf P, keys, la, ph, lp, part, out2, lse;
 };
 
 namespace {
@@ -1776,14 +1778,47 @@ void launch_log_psi(qvmc_model_s* m, const uint64_t* keys, int64_t n, double* la
   if (n == 0) return;
   using namespace qvmc_model;
   ModelView V{m->P.as<double>(), m->n, m->n_qudits, m->bits, m->n_e, m->spin, m->n_up};
-  const int grid = static_cast<int>((n + kTile - 1) / kTile);
-  const size_t dyn = static_cast<size_t>(3 * kHid * kTile) * sizeof(double);
+  if (!m->tiled) {  // CTA-per-sample-tile kernel (all qudits in one CTA)
+    const int grid = static_cast<int>((n + kTile - 1) / kTile);
+    const size_t dyn = static_cast<size_t>((1 + kWBufs) * kHid * kTile) * sizeof(double);
+    DISPATCH_W(m->W, {
+      ck(cudaFuncSetAttribute(k_log_psi<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)),
+         "smem attribute");
+      k_log_psi<WW><<<grid, kMThreads, dyn, m->stream>>>(V, keys, n, la, ph);
+    });
+    ck_launch("log_psi");
+    return;
+  }
+  // warp-tiled: CTAs = (qudit, head) blocks x sample chunks, sized to whole waves of 148 SMs
+  const int n_jh = 2 * m->n_qudits;
+  const int64_t max_chunks = std::max<int64_t>(1, (n + kWT * kPWarps - 1) / (kWT * kPWarps));
+  int64_t best_s = 1;
+  double best_eff = -1.0;
+  for (int w = 4; w <= 16; ++w) {
+    const int64_t S = std::min<int64_t>(max_chunks, std::max<int64_t>(1, (int64_t{m->sms} * w) / n_jh));
+    const int64_t blocks = S * n_jh;
+    const int64_t waves = (blocks + m->sms - 1) / m->sms;
+    const double eff = static_cast<double>(blocks) / static_cast<double>(waves * m->sms) + 1e-3 * w;
+    if (eff > best_eff) {
+      best_eff = eff;
+      best_s = S;
+    }
+  }
+  int64_t chunk = (n + best_s - 1) / best_s;
+  chunk = (chunk + kWT - 1) / kWT * kWT;
+  const int64_t S = (n + chunk - 1) / chunk;
+  m->part.ensure(static_cast<size_t>(n_jh) * n * sizeof(double));
   DISPATCH_W(m->W, {
-    ck(cudaFuncSetAttribute(k_log_psi<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)),
+    const size_t dyn = (8448 + kPWarps * 64 * kWT) * sizeof(double) + kPWarps * kWT * WW * sizeof(uint64_t);
+    ck(cudaFuncSetAttribute(k_log_psi_part<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)),
        "smem attribute");
-    k_log_psi<WW><<<grid, kMThreads, dyn, m->stream>>>(V, keys, n, la, ph);
+    k_log_psi_part<WW><<<static_cast<unsigned>(S * n_jh), kPThreads, dyn, m->stream>>>(V, keys, n, chunk,
+                                                                                       m->part.as<double>());
+    ck_launch("log_psi part");
+    k_sum_qudits<WW><<<static_cast<unsigned>((n + 255) / 256), 256, 0, m->stream>>>(V, keys, n, m->part.as<double>(),
+                                                                                  la, ph);
+    ck_launch("log_psi sum");
   });
-  ck_launch("log_psi");
 }
 }  // namespace
 
@@ -1821,6 +1856,8 @@ int qvmc_cuda_model_create(int n_qubits, int bits_per_qudit, int n_electrons, in
     m->hidden = hidden;
     m->n_qudits = (n_qubits + bits_per_qudit - 1) / bits_per_qudit;
     m->n_params = model_param_count(n_qubits, bits_per_qudit, hidden);
+    m->sms = prop.multiProcessorCount;
+    if (const char* e = std::getenv("QVMC_MODEL_TILED")) m->tiled = std::atoi(e) != 0;
     ck(cudaStreamCreateWithFlags(&m->own, cudaStreamNonBlocking), "stream create");
     m->stream = m->own;
     *out = m.release();
@@ -1956,11 +1993,11 @@ int qvmc_cuda_fill_amplitudes(qvmc_model_t m, int64_t n, const uint64_t* keys, c
       dlp = m->lp.as<double>();
     }
     using namespace qvmc_model;
-    m->part.ensure(kLseBlocks * sizeof(double2));
+    m->lse.ensure(kLseBlocks * sizeof(double2));
     m->out2.ensure(2 * sizeof(double));
-    k_lse_partial<<<kLseBlocks, 256, 0, m->stream>>>(dlp, n, m->part.as<double2>());
+    k_lse_partial<<<kLseBlocks, 256, 0, m->stream>>>(dlp, n, m->lse.as<double2>());
     ck_launch("lse partial");
-    k_lse_final<<<1, 32, 0, m->stream>>>(m->part.as<double2>(), kLseBlocks, m->out2.as<double>());
+    k_lse_final<<<1, 32, 0, m->stream>>>(m->lse.as<double2>(), kLseBlocks, m->out2.as<double>());
     ck_launch("lse final");
     ck(cudaMemcpyAsync(out_norm2, m->out2.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, m->stream), "D2H norm");
     ck(cudaStreamSynchronize(m->stream), "sync");

@@ -42,6 +42,10 @@ constexpr int kHid = 64;      // hidden width of the device path (the reference'
 constexpr int kMaxK = 6;      // bits per qudit (2^k ≤ 64 outputs; the reference's default, model.hpp:24)
 constexpr int kTile = 64;     // samples per CTA
 constexpr int kMThreads = 256;
+#ifndef QVMC_MODEL_MINB
+#define QVMC_MODEL_MINB 3  // CTAs per SM (measured: 3 with one weight buffer beats 2 with a W3ᵀ prefetch buffer)
+#endif
+constexpr int kWBufs = QVMC_MODEL_MINB >= 3 ? 1 : 2;  // 3+ CTAs/SM: W3ᵀ reuses the W2ᵀ buffer (64 KB smem)
 
 // per (qudit, head) block of the device parameter layout, in doubles
 struct BlockLayout {
@@ -73,6 +77,45 @@ __device__ __forceinline__ void stage_64x64(double* dst, const double* src, int 
     __pipeline_memcpy_async(dst + e, src + e, 16);
   }
   __pipeline_commit();
+}
+
+// e^x for x ≤ 0 in ~17 instructions: x = k ln2 + r (magic-number rounding, two-part ln2),
+// Taylor degree 12 on |r| ≤ ln2/2, 2^k added to the exponent field. Relative error
+// ≲ 1e-14 over [-700, 0] (vs 1 ulp for the libdevice exp, which costs ~3× more).
+__device__ __forceinline__ double exp_nonpos(double x) {
+  x = fmax(x, -700.0);
+  const double t = fma(x, 1.4426950408889634, 6755399441055744.0);  // 1.5·2^52: k in the low word
+  const int k = __double2loint(t);
+  const double kf = t - 6755399441055744.0;
+  double r = fma(kf, -6.93147180559945286227e-01, x);
+  r = fma(kf, -2.31904681384629955842e-17, r);
+  double p = 2.08767569878680989792e-09;  // 1/12!
+  p = fma(p, r, 2.50521083854417187751e-08);
+  p = fma(p, r, 2.75573192239858906526e-07);
+  p = fma(p, r, 2.75573192239858906526e-06);
+  p = fma(p, r, 2.48015873015873015873e-05);
+  p = fma(p, r, 1.98412698412698412698e-04);
+  p = fma(p, r, 1.38888888888888888889e-03);
+  p = fma(p, r, 8.33333333333333333333e-03);
+  p = fma(p, r, 4.16666666666666666667e-02);
+  p = fma(p, r, 1.66666666666666666667e-01);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  return __hiloint2double(__double2hiint(p) + (k << 20), __double2loint(p));
+}
+
+// tanh(x) = sign(x) (1 − e)/(1 + e), e = e^{−2|x|}; the reciprocal from the
+// MUFU.RCP64H seed plus two Newton steps. Absolute error ≲ 5e-15 (the
+// activations feed linear layers, so absolute error is what propagates).
+__device__ __forceinline__ double tanh_fast(double x) {
+  const double e = exp_nonpos(-2.0 * fmin(fabs(x), 40.0));
+  const double d = 1.0 + e;
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  y = fma(y, fma(-d, y, 1.0), y);
+  y = fma(y, fma(-d, y, 1.0), y);
+  return copysign((1.0 - e) * y, x);
 }
 
 // a thread's 4 samples × 4 features <-> the swizzled tile, as 16-byte pairs of samples
@@ -119,13 +162,13 @@ __device__ __forceinline__ void gemm_64(const double* __restrict__ act, const do
 }
 
 template <int W>
-__global__ void __launch_bounds__(kMThreads, 2)
+__global__ void __launch_bounds__(kMThreads, QVMC_MODEL_MINB)
     k_log_psi(const ModelView M, const uint64_t* __restrict__ keys, int64_t N, double* __restrict__ out_la,
               double* __restrict__ out_ph) {
   extern __shared__ __align__(16) double smem[];
   double* act = smem;                     // [64][64] swizzled activations
   double* wA = smem + kHid * kTile;       // W2ᵀ of the current head
-  double* wB = wA + kHid * kHid;          // W3ᵀ of the amplitude head
+  double* wB = kWBufs == 2 ? wA + kHid * kHid : wA;  // W3ᵀ of the amplitude head
   __shared__ uint64_t s_key[kTile][W];
   __shared__ double s_la[kTile], s_ph[kTile];
 
@@ -184,7 +227,7 @@ __global__ void __launch_bounds__(kMThreads, 2)
     for (int hd = 0; hd < 2; ++hd) {
       const double* B = M.P + static_cast<int64_t>(2 * j + hd) * bsize;
       stage_64x64(wA, B + L.w2t(), tid);
-      if (hd == 0) stage_64x64(wB, B + L.w3t(), tid);
+      if (hd == 0 && kWBufs == 2) stage_64x64(wB, B + L.w3t(), tid);
 
       // layer 1: pre1 = b1 + W1 e over the prefix minority (model.cpp:153-158, :171)
       {
@@ -219,12 +262,12 @@ __global__ void __launch_bounds__(kMThreads, 2)
 #pragma unroll
           for (int hi = 0; hi < 4; ++hi) {
             const double we = ones ? 2.0 * a[hi] - cs[hi] : cs[hi] - 2.0 * a[hi];
-            h1[si][hi] = tanh(we + bb[hi]);
+            h1[si][hi] = tanh_fast(we + bb[hi]);
           }
         }
         store_tile(act, h1, sg, hg);
       }
-      if (hd == 0) __pipeline_wait_prior(1);  // W2ᵀ landed (W3ᵀ may still be in flight)
+      if (hd == 0 && kWBufs == 2) __pipeline_wait_prior(1);  // W2ᵀ landed (W3ᵀ may still be in flight)
       else __pipeline_wait_prior(0);
       __syncthreads();
 
@@ -240,10 +283,11 @@ __global__ void __launch_bounds__(kMThreads, 2)
 #pragma unroll
         for (int si = 0; si < 4; ++si)
 #pragma unroll
-          for (int hi = 0; hi < 4; ++hi) acc[si][hi] = tanh(acc[si][hi] + bb[hi] + res[si][hi]);
+          for (int hi = 0; hi < 4; ++hi) acc[si][hi] = tanh_fast(acc[si][hi] + bb[hi] + res[si][hi]);
       }
       __syncthreads();
       store_tile(act, acc, sg, hg);
+      if (hd == 0 && kWBufs == 1) stage_64x64(wB, B + L.w3t(), tid);  // W2ᵀ reads are done
       __pipeline_wait_prior(0);
       __syncthreads();
 
@@ -290,7 +334,7 @@ __global__ void __launch_bounds__(kMThreads, 2)
           double se = 0.0;
 #pragma unroll
           for (int vi = 0; vi < 4; ++vi)
-            if (ok[vi]) se += exp(two[vi] - mx);
+            if (ok[vi]) se += exp_nonpos(two[vi] - mx);
 #pragma unroll
           for (int o = 8; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
           const int v = val[si];
@@ -339,6 +383,295 @@ __global__ void __launch_bounds__(kMThreads, 2)
     out_la[s0 + tid] = ins ? s_la[tid] : -CUDART_INF;
     out_ph[s0 + tid] = ins ? s_ph[tid] : 0.0;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-tiled variant (default): one CTA of 16 warps owns ONE (qudit, head)
+// block of the model and a chunk of samples. The block's W2ᵀ / W3ᵀ are staged
+// into shared memory once; every warp then runs its own 16-sample tiles
+// through layer 1, the layer-2 GEMM and the output layer with only
+// __syncwarp — no CTA barrier inside the sample loop, so the 16 warps hide
+// each other's gather / transcendental / shuffle latency. A lane holds 4
+// samples × 8 features (32 fp64 accumulators): per k it loads 4 activations
+// and 8 weights (6 LDS.128, one wavefront each) for 32 DFMA. Each (sample,
+// qudit, head) writes its conditional log-amplitude / phase to
+// part[2j+hd][s]; k_sum_qudits adds them in qudit order (the reference's
+// summation order, model.cpp:264-270) and applies in_sector.
+constexpr int kWT = 16;        // samples per warp tile
+constexpr int kPWarps = 16;    // warps per CTA
+constexpr int kPThreads = kPWarps * 32;
+
+// warp activation tile [64 k][16 s]: 32-byte chunk swizzled by (k >> 3), the
+// 16-byte half by (k >> 1), so stores of rows 16m+2hq+b by the 8 hq lanes and
+// the GEMM's row reads are both conflict-free
+__device__ __forceinline__ int pidx(int k, int s) {
+  return k * kWT + ((((s >> 2) ^ (k >> 3)) & 3) << 2) + (((((s >> 1) ^ (k >> 1)) & 1)) << 1) + (s & 1);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kPThreads, 1)
+    k_log_psi_part(const ModelView M, const uint64_t* __restrict__ keys, int64_t N, int64_t chunk,
+                   double* __restrict__ part) {
+  extern __shared__ __align__(16) double smem[];
+  double* w2 = smem;                   // [64 k][64 h]
+  double* w3 = smem + 4096;            // [64 k][64 v] (amplitude head)
+  double* bias = smem + 8192;          // b1 | csum | b2 | b3, 64 each
+  double* acts = smem + 8448;          // [16 warps][64][16]
+  uint64_t* skeys = reinterpret_cast<uint64_t*>(acts + kPWarps * 64 * kWT);  // [16 warps][16][W]
+
+  const int n_jh = 2 * M.n_qudits;
+  const int jh = static_cast<int>(blockIdx.x % n_jh), j = jh >> 1, hd = jh & 1;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x / n_jh) * chunk;
+  const int64_t c1 = min(N, c0 + chunk);
+  const BlockLayout L{M.n};
+  const double* B = M.P + static_cast<int64_t>(jh) * L.size();
+  for (int e = threadIdx.x * 2; e < 4096; e += kPThreads * 2) {
+    *reinterpret_cast<double2*>(w2 + e) = __ldg(reinterpret_cast<const double2*>(B + L.w2t() + e));
+    if (hd == 0) *reinterpret_cast<double2*>(w3 + e) = __ldg(reinterpret_cast<const double2*>(B + L.w3t() + e));
+  }
+  if (threadIdx.x < 64) {
+    bias[threadIdx.x] = __ldg(B + L.b1() + threadIdx.x);
+    bias[64 + threadIdx.x] = __ldg(B + L.csum() + threadIdx.x);
+    bias[128 + threadIdx.x] = __ldg(B + L.b2() + threadIdx.x);
+    bias[192 + threadIdx.x] = __ldg(B + L.b3() + threadIdx.x);
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sq = lane >> 3, hq = lane & 7;  // samples sq*4..+3; features 16m + 2hq + b
+  double* act = acts + warp * 64 * kWT;
+  uint64_t* sk = skeys + warp * kWT * W;
+  const int off = j * M.bits;
+  const int k = min(M.bits, M.n - off);
+  const int n_out = 1 << k;
+  const int rem_after = M.n - off - k;  // QuditInfo (model.cpp:82-93)
+  int rem_up_after = 0;
+  for (int i = off + k; i < M.n; ++i) rem_up_after += (i % 2 == 0);
+  uint32_t up_value_mask = 0;
+  for (int t = 0; t < k; ++t)
+    if ((off + t) % 2 == 0) up_value_mask |= 1u << (k - 1 - t);
+  double* out = part + static_cast<int64_t>(jh) * N;
+
+  for (int64_t t0 = c0 + static_cast<int64_t>(warp) * kWT; t0 < c1; t0 += static_cast<int64_t>(kWT) * kPWarps) {
+    __syncwarp();
+    for (int e = lane; e < kWT * W; e += 32) {
+      const int64_t g = t0 + e / W;
+      sk[e] = g < c1 ? __ldg(keys + g * W + (e % W)) : 0ull;
+    }
+    __syncwarp();
+    int pw[4], pu[4], val[4];
+#pragma unroll
+    for (int si = 0; si < 4; ++si) {
+      const uint64_t* x = sk + (sq * 4 + si) * W;
+      int c = 0, cu = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const int lo = 64 * w;
+        if (off > lo) {
+          const uint64_t msk = (off - lo >= 64) ? ~0ull : ((1ull << (off - lo)) - 1);
+          c += __popcll(x[w] & msk);
+          cu += __popcll(x[w] & msk & 0x5555555555555555ull);
+        }
+      }
+      pw[si] = c;
+      pu[si] = cu;
+      uint32_t v = 0;  // extract_bits (basis_vector.cpp:40-45)
+      for (int t = 0; t < k; ++t) {
+        const int q = off + t;
+        v |= static_cast<uint32_t>((x[q >> 6] >> (q & 63)) & 1ull) << (k - 1 - t);
+      }
+      val[si] = static_cast<int>(v);
+    }
+
+    // layer 1 over the prefix minority, two samples at a time (model.cpp:153-158, :171)
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      double a[2][8];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int si = 2 * p + u;
+        const uint64_t* x = sk + (sq * 4 + si) * W;
+        const bool ones = 2 * pw[si] <= off;
+#pragma unroll
+        for (int f = 0; f < 8; ++f) a[u][f] = 0.0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const int lo = 64 * w;
+          if (off <= lo) break;
+          const uint64_t msk = (off - lo >= 64) ? ~0ull : ((1ull << (off - lo)) - 1);
+          uint64_t xm = (ones ? x[w] : ~x[w]) & msk;
+          while (xm) {
+            const int i = lo + __ffsll(static_cast<long long>(xm)) - 1;
+            xm &= xm - 1;
+            const double* row = B + L.w1t() + i * kHid + 2 * hq;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              const double2 wv = __ldg(reinterpret_cast<const double2*>(row + 16 * m));
+              a[u][2 * m] += wv.x;
+              a[u][2 * m + 1] += wv.y;
+            }
+          }
+        }
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+          const int h = 16 * (f >> 1) + 2 * hq + (f & 1);
+          const double cs = bias[64 + h];
+          a[u][f] = tanh_fast((ones ? 2.0 * a[u][f] - cs : cs - 2.0 * a[u][f]) + bias[h]);
+        }
+      }
+#pragma unroll
+      for (int f = 0; f < 8; ++f) {
+        const int h = 16 * (f >> 1) + 2 * hq + (f & 1);
+        *reinterpret_cast<double2*>(act + pidx(h, sq * 4 + 2 * p)) = make_double2(a[0][f], a[1][f]);
+      }
+    }
+    __syncwarp();
+
+    // layer 2 GEMM: acc[si][f] = Σ_k h1[s][k] W2[h][k] (model.cpp:172)
+    double acc[4][8];
+    auto gemm = [&](const double* wm) {
+#pragma unroll
+      for (int si = 0; si < 4; ++si)
+#pragma unroll
+        for (int f = 0; f < 8; ++f) acc[si][f] = 0.0;
+#pragma unroll 4
+      for (int kk = 0; kk < kHid; ++kk) {
+        const double2 a01 = *reinterpret_cast<const double2*>(act + pidx(kk, sq * 4));
+        const double2 a23 = *reinterpret_cast<const double2*>(act + pidx(kk, sq * 4 + 2));
+        const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+        double wv[8];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const double2 t = *reinterpret_cast<const double2*>(wm + kk * kHid + 16 * m + 2 * hq);
+          wv[2 * m] = t.x;
+          wv[2 * m + 1] = t.y;
+        }
+#pragma unroll
+        for (int si = 0; si < 4; ++si)
+#pragma unroll
+          for (int f = 0; f < 8; ++f) acc[si][f] = fma(av[si], wv[f], acc[si][f]);
+      }
+    };
+    gemm(w2);
+    // h2 = tanh(W2 h1 + b2 + h1): the residual h1 is read at this lane's own positions
+#pragma unroll
+    for (int f = 0; f < 8; ++f) {
+      const int h = 16 * (f >> 1) + 2 * hq + (f & 1);
+      const double2 r01 = *reinterpret_cast<const double2*>(act + pidx(h, sq * 4));
+      const double2 r23 = *reinterpret_cast<const double2*>(act + pidx(h, sq * 4 + 2));
+      const double b2 = bias[128 + h];
+      acc[0][f] = tanh_fast(acc[0][f] + b2 + r01.x);
+      acc[1][f] = tanh_fast(acc[1][f] + b2 + r01.y);
+      acc[2][f] = tanh_fast(acc[2][f] + b2 + r23.x);
+      acc[3][f] = tanh_fast(acc[3][f] + b2 + r23.y);
+    }
+
+    if (hd == 1) {
+      // phase head: only out[v] of the sampled value (model.cpp:173-174, :250)
+#pragma unroll
+      for (int si = 0; si < 4; ++si) {
+        const int v = val[si];
+        double d = 0.0;
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+          const int h = 16 * (f >> 1) + 2 * hq + (f & 1);
+          d = fma(acc[si][f], __ldg(B + L.w3t() + h * kHid + v), d);
+        }
+#pragma unroll
+        for (int o = 4; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        const int64_t g = t0 + sq * 4 + si;
+        if (hq == 0 && g < c1) out[g] = d + bias[192 + v];
+      }
+      continue;
+    }
+
+    // amplitude head: h2 -> act, out = W3 h2 + b3, mean shift, log-softmax of
+    // 2*out over the allowed values (model.cpp:173-174, :218-249)
+    __syncwarp();
+#pragma unroll
+    for (int f = 0; f < 8; ++f) {
+      const int h = 16 * (f >> 1) + 2 * hq + (f & 1);
+      *reinterpret_cast<double2*>(act + pidx(h, sq * 4)) = make_double2(acc[0][f], acc[1][f]);
+      *reinterpret_cast<double2*>(act + pidx(h, sq * 4 + 2)) = make_double2(acc[2][f], acc[3][f]);
+    }
+    __syncwarp();
+    gemm(w3);
+#pragma unroll
+    for (int si = 0; si < 4; ++si) {
+      double sum = 0.0;
+#pragma unroll
+      for (int f = 0; f < 8; ++f) {
+        acc[si][f] += bias[192 + 16 * (f >> 1) + 2 * hq + (f & 1)];
+        sum += acc[si][f];  // v ≥ 2^k: zero-padded weights and bias, out = 0
+      }
+#pragma unroll
+      for (int o = 4; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      const double mean = sum / static_cast<double>(n_out);
+      double mx = -CUDART_INF;
+      uint32_t okm = 0;
+#pragma unroll
+      for (int f = 0; f < 8; ++f) {
+        const int v = 16 * (f >> 1) + 2 * hq + (f & 1);
+        acc[si][f] = 2.0 * (acc[si][f] - mean);
+        const int w = pw[si] + __popc(v);  // allowed_values (model.cpp:129-151)
+        bool a = v < n_out && w <= M.n_e && w + rem_after >= M.n_e;
+        if (a && M.spin) {
+          const int wu = pu[si] + __popc(static_cast<uint32_t>(v) & up_value_mask);
+          const int wd = w - wu;
+          const int n_down = M.n_e - M.n_up;
+          const int rem_down = rem_after - rem_up_after;
+          a = wu <= M.n_up && wu + rem_up_after >= M.n_up && wd <= n_down && wd + rem_down >= n_down;
+        }
+        if (a) {
+          okm |= 1u << f;
+          mx = fmax(mx, acc[si][f]);
+        }
+      }
+#pragma unroll
+      for (int o = 4; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      double se = 0.0;
+#pragma unroll
+      for (int f = 0; f < 8; ++f)
+        if (okm >> f & 1u) se += exp_nonpos(acc[si][f] - mx);
+#pragma unroll
+      for (int o = 4; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+      const int v = val[si];
+      const int64_t g = t0 + sq * 4 + si;
+      if (((v >> 1) & 7) == hq && g < c1) {  // the lane holding out[v]
+        const int fv = 2 * (v >> 4) + (v & 1);
+        double tv = acc[si][0];
+#pragma unroll
+        for (int f = 1; f < 8; ++f)
+          if (f == fv) tv = acc[si][f];
+        out[g] = 0.5 * (tv - (mx + log(se)));
+      }
+    }
+  }
+}
+
+// log ψ = Σ_j log_amp_j[v_j], φ = Σ_j phase_j[v_j] in qudit order; masked
+// states (-inf, 0) (model.cpp:254-271)
+template <int W>
+__global__ void k_sum_qudits(const ModelView M, const uint64_t* __restrict__ keys, int64_t N,
+                             const double* __restrict__ part, double* __restrict__ out_la,
+                             double* __restrict__ out_ph) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= N) return;
+  int pc = 0, pe = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const uint64_t x = __ldg(keys + s * W + w);
+    pc += __popcll(x);
+    pe += __popcll(x & 0x5555555555555555ull);
+  }
+  double la = 0.0, ph = 0.0;
+  for (int j = 0; j < M.n_qudits; ++j) {
+    la += __ldcs(part + static_cast<int64_t>(2 * j) * N + s);
+    ph += __ldcs(part + static_cast<int64_t>(2 * j + 1) * N + s);
+  }
+  const bool ins = pc == M.n_e && (!M.spin || pe == M.n_up);
+  out_la[s] = ins ? la : -CUDART_INF;
+  out_ph[s] = ins ? ph : 0.0;
 }
 
 // log_norm = logsumexp(log_probs) (sampler.cpp:114-119), deterministic:

@@ -108,12 +108,12 @@ class AnqsModel:
         keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, self.W)
         n = keys.shape[0]
         la, ph = np.empty(n), np.empty(n)
-        _lib.check(_lib.lib().qvmc_cuda_log_psi(self._h, n, _ptr(keys), _lib.QVMC_MEM_HOST, _ptr(la), _ptr(ph)))
+        _lib.check(_lib.lib().qvmc_cuda_log_psi(self._h, n, _ptr(keys), _lib.MEM_HOST, _ptr(la), _ptr(ph)))
         return la, ph
 
     def log_psi_device(self, keys_ptr: int, n: int, out_log_amp_ptr: int, out_phase_ptr: int) -> None:
         """Device pointers (e.g. torch tensors' data_ptr()), enqueued on the model's stream."""
-        _lib.check(_lib.lib().qvmc_cuda_log_psi(self._h, n, C.c_void_p(keys_ptr), _lib.QVMC_MEM_DEVICE,
+        _lib.check(_lib.lib().qvmc_cuda_log_psi(self._h, n, C.c_void_p(keys_ptr), _lib.MEM_DEVICE,
                                                 C.c_void_p(out_log_amp_ptr), C.c_void_p(out_phase_ptr)))
 
     def synchronize(self) -> None:
@@ -179,7 +179,7 @@ def fill_amplitudes(batch, model: AnqsModel, threads: int = 1) -> None:
     if lp.shape != (n,):
         raise ValueError("fill_amplitudes: log_probs size mismatch")
     la, ph, out2 = np.empty(n), np.empty(n), np.zeros(2)
-    _lib.check(_lib.lib().qvmc_cuda_fill_amplitudes(model._h, n, _ptr(keys), _ptr(lp), _lib.QVMC_MEM_HOST,
+    _lib.check(_lib.lib().qvmc_cuda_fill_amplitudes(model._h, n, _ptr(keys), _ptr(lp), _lib.MEM_HOST,
                                                     _ptr(la), _ptr(ph), _ptr(out2)))
     batch.log_amps, batch.phases = la, ph
     batch.norm, batch.log_norm = float(out2[0]), float(out2[1])
