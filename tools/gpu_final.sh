@@ -8,6 +8,9 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 
 timeout 900 python bench.py > $OUT/bench_c118.json 2> $OUT/bench_c118.err
 timeout 600 python bench.py --config c56 > $OUT/bench_c56.json 2> $OUT/bench_c56.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref_c118.json 2> $OUT/bench_ref_c118.err
+for cfg in c118 c56; do
+  timeout 300 python tools/bench_model.py --config $cfg > $OUT/bench_model_$cfg.json 2> $OUT/bench_model_$cfg.err
+done
 # (gpurun brings back <= 64 MiB: the ncu captures go in separate calls, tools/gpu_ncu.sh)
 for cfg in c118 c56; do
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$cfg.csv \
