@@ -15,6 +15,7 @@
 #include <cub/device/device_select.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <cub/device/device_segmented_sort.cuh>
+#include <limits>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -1981,8 +1982,13 @@ int qvmc_cuda_fill_amplitudes(qvmc_model_t m, int64_t n, const uint64_t* keys, c
   return guarded([&] {
     check_model(m);
     check_mem(mem);
-    if (n < 1) fail(QVMC_ERR_INVALID_ARGUMENT, "empty sample batch");
-    if (!log_probs || !out_norm2) fail(QVMC_ERR_INVALID_ARGUMENT, "null array");
+    if (n < 0) fail(QVMC_ERR_INVALID_ARGUMENT, "negative batch size");
+    if ((n > 0 && !log_probs) || !out_norm2) fail(QVMC_ERR_INVALID_ARGUMENT, "null array");
+    if (n == 0) {  // sampler.cpp:114-119 over no samples: log_norm = -inf + log(0), norm = 0
+      out_norm2[0] = 0.0;
+      out_norm2[1] = -std::numeric_limits<double>::infinity();
+      return;
+    }
     const int st = qvmc_cuda_log_psi(m, n, keys, mem, out_log_amp, out_phase);
     if (st != QVMC_OK) throw Failure{st, g_error};
     DeviceGuard dg(m->device);

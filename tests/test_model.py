@@ -170,6 +170,9 @@ def test_gpu_model_errors(cuda_ok):
     # empty batch is a no-op; all-zero parameters give the uniform distribution over allowed values
     la, ph = M.log_psi(np.zeros((0, 1), dtype=np.uint64))
     assert la.size == 0
+    b = q.SampleBatch(np.zeros((0, 1), dtype=np.uint64), np.zeros(0), np.zeros(0), np.zeros(0))
+    q.fill_amplitudes(b, M)  # the reference's empty-batch arithmetic (sampler.cpp:114-119)
+    assert b.norm == 0.0 and b.log_norm == -math.inf
     from paper_2408_07625_b200 import synthetic
     keys = synthetic.sector_keys(12, 6, spin_balanced=True)
     la, ph = M.log_psi(keys)
