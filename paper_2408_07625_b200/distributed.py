@@ -11,10 +11,17 @@ asks for them (``gather_locals``).
 The per-rank evaluation is ``qvmc_cuda_eloc_fused`` on device pointers; the
 ``evaluate`` hook exists so the gather/offset/reduce plumbing can be tested
 with the gloo backend on CPU-only hosts.
+
+``sharded_fill_amplitudes`` is the stage before it (fill_amplitudes,
+sampler.cpp:104-120) on the same shards: log|psi| and phase of a rank's own
+rows only (independent rows, no data-path collective), and the global
+log_norm = logsumexp of the sampler's log_probs merged from per-rank
+(max, scaled sum) pairs gathered in rank order (deterministic).
 """
 from __future__ import annotations
 
 import ctypes as C
+import math
 from dataclasses import dataclass
 from typing import Callable, List, Optional
 
@@ -112,3 +119,40 @@ def shard_bounds(n: int, world: int, rank: int) -> tuple:
     base, rem = divmod(n, world)
     begin = rank * base + min(rank, rem)
     return begin, begin + base + (1 if rank < rem else 0)
+
+
+def model_evaluate(model, device: int) -> Callable:
+    """k_log_psi_part on device pointers, on torch's current stream."""
+
+    def run(keys, out_la, out_ph):
+        raw = torch.cuda.current_stream(device).cuda_stream or 0x1  # 0x1 = cudaStreamLegacy
+        _lib.check(_lib.lib().qvmc_cuda_model_set_stream(model._h, C.c_void_p(raw)))
+        model.log_psi_device(keys.data_ptr(), keys.shape[0], out_la.data_ptr(), out_ph.data_ptr())
+
+    return run
+
+
+def sharded_fill_amplitudes(shard: Shard, evaluate: Callable, group=None) -> float:
+    """fill_amplitudes (sampler.cpp:104-120) for this rank's rows: writes shard.log_amps /
+    shard.phases in place and returns the global log_norm of the sampler's log_probs."""
+    world = dist.get_world_size(group)
+    dev = shard.keys.device
+    if shard.keys.shape[0]:
+        evaluate(shard.keys, shard.log_amps, shard.phases)
+    lp = shard.log_probs
+    m = lp.max() if lp.numel() else torch.tensor(float("-inf"), dtype=torch.float64, device=dev)
+    s = torch.exp(lp - m).sum() if lp.numel() and torch.isfinite(m) else torch.zeros((), dtype=torch.float64,
+                                                                                       device=dev)
+    pair = torch.stack([m.to(torch.float64), s.to(torch.float64)])
+    flat = torch.empty(2 * world, dtype=torch.float64, device=dev)
+    dist.all_gather_into_tensor(flat, pair, group=group)
+    pairs = flat.view(world, 2).cpu()
+    gm, gs = float("-inf"), 0.0
+    for r in range(world):  # merge in rank order
+        mr, sr = float(pairs[r, 0]), float(pairs[r, 1])
+        mm = max(gm, mr)
+        if mm == float("-inf"):
+            continue
+        gs = gs * math.exp(gm - mm) + sr * math.exp(mr - mm)
+        gm = mm
+    return gm + math.log(gs) if gs > 0 else float("-inf")

@@ -94,3 +94,61 @@ def test_shard_bounds_cover_rows():
             assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
             sizes = [b - a for a, b in spans]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _amp_worker(rank, world, port, splits, out_q):
+    """sharded_fill_amplitudes with the model oracle as the per-shard evaluator, then
+    sharded_surrogate_energy on the amplitudes it produced."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.model_oracle import ModelOracle
+        from paper_2408_07625_b200.distributed import Shard, sharded_fill_amplitudes, sharded_surrogate_energy
+        masks, b = _problem()
+        p = np.random.default_rng(4).uniform(-0.2, 0.2, ModelOracle(12, 6, 6, True, 64, np.zeros(36608)).n_params)
+        O = ModelOracle(12, 6, 6, True, 64, p)
+
+        def evaluate(keys, out_la, out_ph):
+            la, ph = O.log_psi(keys.numpy().view(np.uint64))
+            out_la.copy_(torch.from_numpy(la))
+            out_ph.copy_(torch.from_numpy(ph))
+
+        r0, r1 = splits[rank], splits[rank + 1]
+        lp = b.log_probs[r0:r1].copy()
+        sh = Shard(torch.from_numpy(b.vectors[r0:r1].view(np.int64).copy()), torch.zeros(r1 - r0, dtype=torch.float64),
+                   torch.zeros(r1 - r0, dtype=torch.float64), torch.from_numpy(lp))
+        log_norm = sharded_fill_amplitudes(sh, evaluate)
+        res = sharded_surrogate_energy(sh, log_norm, _oracle_evaluator(masks), gather_locals=True)
+        out_q.put((rank, log_norm, sh.log_amps.numpy(), sh.phases.numpy(), res.locals.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("splits", [[0, 200, 400], [0, 0, 400], [0, 311, 400]])
+def test_two_rank_fill_amplitudes_matches_unsharded(splits):
+    """Rows are independent: each rank's log|psi|/phase equal the unsharded oracle's rows, the
+    merged log_norm equals the single-process logsumexp (sampler.cpp:114-119), and the chained
+    E_loc matches the unsharded E_loc on those amplitudes (an empty shard included)."""
+    import oracle
+    from oracle.model_oracle import ModelOracle
+    masks, b = _problem()
+    p = np.random.default_rng(4).uniform(-0.2, 0.2, ModelOracle(12, 6, 6, True, 64, np.zeros(36608)).n_params)
+    O = ModelOracle(12, 6, 6, True, 64, p)
+    la, ph, _, log_norm = O.fill_amplitudes(b.vectors, b.log_probs)
+    full, _ = oracle.OracleIndex(12, *masks).eloc_rows(b.vectors, la, ph, 0, 400, threads=1)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_amp_worker, args=(r, 2, port, splits, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    outs = sorted(q.get(timeout=300) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for rank, ln, la_r, ph_r, locals_ in outs:
+        r0, r1 = splits[rank], splits[rank + 1]
+        assert np.array_equal(la_r, la[r0:r1]) and np.array_equal(ph_r, ph[r0:r1])
+        assert abs(ln - log_norm) <= 1e-13 * max(1.0, abs(log_norm))
+        assert np.allclose(locals_, full, rtol=0, atol=1e-12)
+    assert outs[0][1] == outs[1][1]

@@ -207,3 +207,36 @@ def test_gpu_log_psi_device_pointers(cuda_ok):
     M.synchronize()
     _close(la.cpu().numpy(), GOLD["h56_la"])
     _close(ph.cpu().numpy(), GOLD["h56_ph"])
+
+
+@pytest.mark.gpu
+def test_gpu_sharded_fill_amplitudes_world1(cuda_ok):
+    """distributed.sharded_fill_amplitudes with the device evaluator on an NCCL group of one rank."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    import paper_2408_07625_b200 as q
+    from paper_2408_07625_b200.distributed import Shard, model_evaluate, sharded_fill_amplitudes
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        n, bits, ne, spin, hidden, _ = (int(v) for v in GOLD["h56_cfg"])
+        M = q.AnqsModel(q.QuditLayout.make(n, bits), q.SectorConstraint(ne, bool(spin)), hidden)
+        M.set_params(_params("h56"))
+        keys = GOLD["h56_keys"]
+        dev = torch.device("cuda:0")
+        sh = Shard(torch.from_numpy(keys.view(np.int64)).to(dev), torch.zeros(len(keys), dtype=torch.float64, device=dev),
+                   torch.zeros(len(keys), dtype=torch.float64, device=dev), torch.from_numpy(GOLD["h56_lp"]).to(dev))
+        log_norm = sharded_fill_amplitudes(sh, model_evaluate(M, 0))
+        torch.cuda.synchronize()
+        _close(sh.log_amps.cpu().numpy(), GOLD["h56_la"])
+        _close(sh.phases.cpu().numpy(), GOLD["h56_ph"])
+        want = GOLD["h56_norm"][1]
+        assert abs(log_norm - want) <= 1e-12 * max(1.0, abs(want))
+    finally:
+        dist.destroy_process_group()
