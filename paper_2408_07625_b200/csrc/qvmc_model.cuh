@@ -82,8 +82,11 @@ __device__ __forceinline__ void stage_64x64(double* dst, const double* src, int 
 // e^x for x ≤ 0 in ~17 instructions: x = k ln2 + r (magic-number rounding, two-part ln2),
 // Taylor degree 12 on |r| ≤ ln2/2, 2^k added to the exponent field. Relative error
 // ≲ 1e-14 over [-700, 0] (vs 1 ulp for the libdevice exp, which costs ~3× more).
+__device__ __forceinline__ double exp_core(double x);  // x in [-700, 0], no clamp
 __device__ __forceinline__ double exp_nonpos(double x) {
-  x = fmax(x, -700.0);
+  return exp_core(x < -700.0 ? -700.0 : x);  // a select, not fmax (no NaN handling needed)
+}
+__device__ __forceinline__ double exp_core(double x) {
   const double t = fma(x, 1.4426950408889634, 6755399441055744.0);  // 1.5·2^52: k in the low word
   const int k = __double2loint(t);
   const double kf = t - 6755399441055744.0;
@@ -109,7 +112,8 @@ __device__ __forceinline__ double exp_nonpos(double x) {
 // MUFU.RCP64H seed plus two Newton steps. Absolute error ≲ 5e-15 (the
 // activations feed linear layers, so absolute error is what propagates).
 __device__ __forceinline__ double tanh_fast(double x) {
-  const double e = exp_nonpos(-2.0 * fmin(fabs(x), 40.0));
+  const double ax = fabs(x);
+  const double e = exp_core(-2.0 * (ax < 40.0 ? ax : 40.0));  // tanh(40) = 1 in fp64
   const double d = 1.0 + e;
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
