@@ -479,12 +479,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
       }
       pw[si] = c;
       pu[si] = cu;
-      uint32_t v = 0;  // extract_bits (basis_vector.cpp:40-45)
-      for (int t = 0; t < k; ++t) {
-        const int q = off + t;
-        v |= static_cast<uint32_t>((x[q >> 6] >> (q & 63)) & 1ull) << (k - 1 - t);
-      }
-      val[si] = static_cast<int>(v);
+      // extract_bits (basis_vector.cpp:40-45): qubit off+t -> bit k-1-t, i.e. the
+      // k-bit field at off (spanning at most two words) bit-reversed
+      const int wq = off >> 6, bq = off & 63;
+      uint64_t fld = x[wq] >> bq;
+      if (bq + k > 64 && wq + 1 < W) fld |= x[wq + 1] << (64 - bq);
+      val[si] = static_cast<int>(__brev(static_cast<uint32_t>(fld)) >> (32 - k));
     }
 
     // layer 1 over the prefix minority, two samples at a time (model.cpp:153-158, :171)
