@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                    double* __restrict__ part) {
   extern __shared__ __align__(16) double smem[];
   double* w2 = smem;                   // [64 k][64 h]
-  double* w3 = smem + 4096;            // [64 k][64 v] (amplitude head)
+  double* w3 = smem + 4096;            // [64 k][64 v]
   double* bias = smem + 8192;          // b1 | csum | b2 | b3, 64 each
   double* acts = smem + 8448;          // [16 warps][64][16]
   uint64_t* skeys = reinterpret_cast<uint64_t*>(acts + kPWarps * 64 * kWT);  // [16 warps][16][W]
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const double* B = M.P + static_cast<int64_t>(jh) * L.size();
   for (int e = threadIdx.x * 2; e < 4096; e += kPThreads * 2) {
     *reinterpret_cast<double2*>(w2 + e) = __ldg(reinterpret_cast<const double2*>(B + L.w2t() + e));
-    if (hd == 0) *reinterpret_cast<double2*>(w3 + e) = __ldg(reinterpret_cast<const double2*>(B + L.w3t() + e));
+    *reinterpret_cast<double2*>(w3 + e) = __ldg(reinterpret_cast<const double2*>(B + L.w3t() + e));  // both heads
   }
   if (threadIdx.x < 64) {
     bias[threadIdx.x] = __ldg(B + L.b1() + threadIdx.x);
@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
         for (int f = 0; f < 8; ++f) {
           const int h = 16 * (f >> 1) + 2 * hq + (f & 1);
-          d = fma(acc[si][f], __ldg(B + L.w3t() + h * kHid + v), d);
+          d = fma(acc[si][f], w3[h * kHid + v], d);
         }
 #pragma unroll
         for (int o = 4; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
