@@ -69,11 +69,11 @@ def make_inputs(cfg_name: str, n_unq=None):
     return cfg, (c, x, y, z), batch, time.perf_counter() - t0
 
 
-def workload_desc(cfg, H, n_unq):
+def workload_desc(cfg, n_terms, n_xy, n_unq):
     return {
         "workload": f"{cfg.name}: surrogate E_loc + energy/variance moments over every unique sample",
-        "n_qubits": cfg.n_qubits, "n_electrons": cfg.n_electrons, "pauli_terms": int(H.n_terms),
-        "flip_masks": int(H.n_xy), "n_unq": int(n_unq),
+        "n_qubits": cfg.n_qubits, "n_electrons": cfg.n_electrons, "pauli_terms": int(n_terms),
+        "flip_masks": int(n_xy), "n_unq": int(n_unq),
         "hamiltonian": "JW-structured synthetic (SURVEY.md §8d), seed 1",
         "samples": "near-HF determinants, 1+Geometric(0.6) same-spin moves, seed 2",
     }
@@ -126,40 +126,62 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ CPU baseline
 
-def cpu_baseline(coeff_masks, n_qubits, batch, sample_rows, threads):
-    """The UNMODIFIED reference path (oracle/_ref) on a bounded sample of the
-    workload: find_coupled_pairs(auto) -> local_energies -> variational_energy
-    over the first `sample_rows` unique samples as their own sample set."""
-    import oracle
-    c, x, y, z = coeff_masks
-    keys = batch.vectors[:sample_rows]
-    la, ph = batch.log_amps[:sample_rows], batch.phases[:sample_rows]
-    lp = 2.0 * la
-    mx = lp.max()
-    log_norm = float(mx + np.log(np.exp(lp - mx).sum()))
-    kind = "reference"
-    if oracle.ref_available():
-        strings = masks_to_strings(n_qubits, x, y, z)
+class CpuReference:
+    """The reference CPU path (oracle/_ref: the unmodified reference sources) on a
+    bounded sample of the SAME workload: `sample_rows` rows spread evenly over the
+    whole sample set, each against the whole sample set, so every row does the
+    same pair work as in the GPU arm's full job. Per step: the per-row pair
+    search of loop_over_trie (coupling.cpp:116-149) over the reference's
+    PrefixTree builds of the full sample set and of xy_set, the unmodified
+    local_energies and variational_energy (energy.cpp:13-78) over the whole
+    batch. The two tree builds (once per find_coupled_pairs call in the
+    reference, coupling.cpp:110-111) are timed once and prorated by rows/N."""
+
+    def __init__(self, cfg, coeff_masks, batch, sample_rows, threads):
+        import oracle
+        if not oracle.ref_available():
+            raise RuntimeError("oracle/_ref/libqvmc_ref_hot.so is missing (built with /root/reference present)")
+        c, x, y, z = coeff_masks
+        self.n = batch.size()
+        self.threads = threads
         t0 = time.perf_counter()
-        R = oracle.RefIndex.from_strings(n_qubits, c, strings)
-        setup = time.perf_counter() - t0
-        _, out5, t3, npairs = R.run_path(keys, la, ph, lp, math.exp(log_norm), log_norm, backend=3,
-                                         threshold=4096, threads=threads, want_locals=False)
-        secs = float(t3.sum())
-        detail = {"find_coupled_pairs_s": float(t3[0]), "local_energies_s": float(t3[1]),
-                  "variational_energy_s": float(t3[2]), "pairs": int(npairs), "index_build_s": setup,
-                  "backend": "auto (trie at >= 4096 samples, coupling.cpp:157-161)"}
-    else:  # the C restatement (terms semantics), when the reference could not be compiled
-        kind = "port"
-        O = oracle.OracleIndex(n_qubits, c, x, y, z)
-        t0 = time.perf_counter()
-        _, npairs = O.eloc_rows(keys, la, ph, 0, len(keys), threads=threads)
-        secs = time.perf_counter() - t0
-        detail = {"pairs": int(npairs), "backend": "terms (oracle restatement)"}
-    return {"value": len(keys) / secs, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"first {len(keys)} of the {batch.size()} unique samples as their own sample set, "
-                      f"full Hamiltonian; {secs:.2f} s",
-            "seconds": secs, **detail}
+        self.R = oracle.RefIndex.from_strings(cfg.n_qubits, c, masks_to_strings(cfg.n_qubits, x, y, z))
+        self.index_s = time.perf_counter() - t0
+        self.S = self.R.row_session(batch.vectors, batch.log_amps, batch.phases, batch.log_probs, batch.norm,
+                                    batch.log_norm)
+        k = max(1, min(sample_rows, self.n))
+        self.rows = np.unique(np.linspace(0, self.n - 1, k).astype(np.int64))
+        self.k = len(self.rows)
+
+    def step(self):
+        t3, npairs, _ = self.S.run(self.rows, threads=self.threads)
+        build = self.S.build_seconds * self.k / self.n
+        var = float(t3[2]) * self.k / self.n  # over the whole batch: one job's worth, prorated like the builds
+        secs = float(t3[0] + t3[1]) + var + build
+        return secs, {"search_s": float(t3[0]), "local_energies_s": float(t3[1]),
+                      "variational_energy_s_prorated": var, "tree_builds_s_prorated": build, "pairs": int(npairs),
+                      "pairs_per_row": npairs / self.k}
+
+    def describe(self, secs):
+        return (f"{self.k} rows spread evenly over all {self.n} unique samples, each against the whole sample "
+                f"set (same pairs per row as the full job); {secs:.2f} s per step incl. prorated trie builds")
+
+    def summary(self, secs, detail):
+        return {"value": self.k / secs, "unit": UNIT, "cores": self.threads, "kind": "reference",
+                "sample": self.describe(secs), "seconds": secs, "rows": self.k, **detail,
+                "tree_builds_s_full": self.S.build_seconds, "index_build_s": self.index_s,
+                "backend": "trie (auto at >= 4096 samples, coupling.cpp:157-161)"}
+
+
+def full_size_reference(cfg_name):
+    """A capped full-size run of the unmodified reference path (1e6 rows, all
+    host threads), measured once by tools/cpu_full_reference.py."""
+    f = ROOT / "profiles" / f"cpu_full_reference_{cfg_name}.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        d["source"] = str(f.relative_to(ROOT))
+        return d
+    return None
 
 
 def masks_to_strings(n_qubits, x, y, z):
@@ -175,8 +197,11 @@ def masks_to_strings(n_qubits, x, y, z):
     return [raw[i * n_qubits:(i + 1) * n_qubits] for i in range(arr.shape[0])]
 
 
-def default_cpu_sample(cfg):
-    return {"c118": 20000, "c56": 50000, "c20": 100000}.get(cfg, 20000)
+def default_cpu_sample(cfg, arm="reference"):
+    """Rows per CPU step: ~2-4 s of 16 host threads per step on the reference arm."""
+    if arm == "reference":
+        return {"c118": 2000, "c56": 20000, "c20": 100000}.get(cfg, 2000)
+    return {"c118": 1000, "c56": 10000, "c20": 100000}.get(cfg, 1000)
 
 
 # ------------------------------------------------------------------ reference arm
@@ -186,23 +211,32 @@ def run_reference(args, rank):
         return
     cfg, cm, batch, _ = make_inputs(args.config, args.n_unq)
     threads = os.cpu_count() or 1
-    n_s = args.cpu_sample or default_cpu_sample(args.config)
+    ref = CpuReference(cfg, cm, batch, args.cpu_sample or default_cpu_sample(args.config), threads)
+    for _ in range(min(args.warmup, 1)):
+        ref.step()
     times, last = [], None
     for _ in range(args.steps):
-        last = cpu_baseline(cm, cfg.n_qubits, batch, n_s, threads)
-        times.append(last["seconds"])
+        secs, last = ref.step()
+        times.append(secs)
     t = statistics.mean(times)
-    v = n_s / t
-    from paper_2408_07625_b200 import HamiltonianIndex
+    v = ref.k / t
+    cb = ref.summary(t, last)
     line = {
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"{cfg.name} (CPU sample: {n_s} rows)", "n_qubits": cfg.n_qubits,
-                   "n_unq": batch.size()},
-        "cpu_baseline": {k: last[k] for k in ("value", "unit", "cores", "kind", "sample")} | {"value": v},
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": workload_desc(cfg, ref.R.n_terms, ref.R.n_xy, batch.size()) | {
+            "cpu_rows_per_step": ref.k, "parallelism": f"{threads} host threads (std::thread parallel_for)"},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_baseline_detail": {k: val for k, val in cb.items() if k not in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "a step = cpu_rows_per_step rows of the job, each against the whole sample set; "
+                "job_ms_extrapolated = the same per-row rate over all n_unq rows",
+        "job_ms_extrapolated": t * 1e3 * batch.size() / ref.k,
     }
+    full = full_size_reference(args.config)
+    if full:
+        line["cpu_baseline_detail"]["full_size_run"] = full
     print(json.dumps(line), flush=True)
 
 
@@ -372,7 +406,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_desc(cfg, H, n) | {
+        "config": workload_desc(cfg, H.n_terms, H.n_xy, n) | {
             "parallelism": f"rows sharded over {world} GPU(s); NCCL all-gather of shards + all-reduce of moments"
             if world > 1 else "1 GPU",
             "l2": "flushed between steps (256 MiB write outside the timed events)" if flush is not None else "not flushed"},
@@ -401,9 +435,14 @@ def main():
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        cb = cpu_baseline(cm, cfg.n_qubits, batch, args.cpu_sample or default_cpu_sample(args.config), threads)
+        ref = CpuReference(cfg, cm, batch, args.cpu_sample or default_cpu_sample(args.config, "ours"), threads)
+        secs, detail = ref.step()
+        cb = ref.summary(secs, detail)
         result["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         result["cpu_baseline_detail"] = {k: v for k, v in cb.items() if k not in result["cpu_baseline"]}
+        full = full_size_reference(args.config)
+        if full:
+            result["cpu_baseline_detail"]["full_size_run"] = full
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:

@@ -154,6 +154,16 @@ int qvmc_cuda_pairs_fetch(qvmc_ham_t h, uint32_t* out_entries, int mem);
 int qvmc_cuda_pair_elements(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, uint64_t n_pairs,
                             const uint32_t* entries, double* out_h, uint8_t* out_class, int mem);
 
+/* Per pair (x, x', xy): H_{x x'} through the evaluators of the fused path
+ * (qvmc_cuda_eloc_fused): the 64-byte drain records of weight-2/4 flip masks
+ * (kinds A-D) and the diagonal quadratic form, with out_kind[e] = 0-3 (drain
+ * record kind A-D), 4 (term by term, as group_element) or 5 (diagonal
+ * quadratic form). Kind A is bit-identical to group_element
+ * (hamiltonian.cpp:186-194); the family forms B/D and the quadratic form
+ * reorder the fp64 sum. Exposes the fused arithmetic for parity tests. */
+int qvmc_cuda_pair_elements_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, uint64_t n_pairs,
+                                  const uint32_t* entries, double* out_h, uint8_t* out_kind, int mem);
+
 /* ------------------------------------------------------------ local energies */
 
 /* local_energies (energy.cpp:13-48) from canonical pairs. out_eloc[n_unq][2].
@@ -212,20 +222,6 @@ int qvmc_cuda_model_synchronize(qvmc_model_t m);
 const char* qvmc_cuda_last_error(void);
 /* Kernels launched by this library since load (for launch accounting). */
 uint64_t qvmc_cuda_launch_count(void);
-
-/* ------------------------------------------------ synthetic inputs (bench/tests) */
-
-/* JW-structured molecular-like Hamiltonian: identity, N Z,
- * C(N,2) ZZ; same-spin single groups {XZ..ZX, YZ..ZY} with one optional
- * extra Z_k dressing (2+2(N-2) terms per group); spin-conserving doubles
- * over two even + two odd sites with patterns XXYY/YYXX/XYYX/YXXY and JW
- * Z-strings, until n_terms_target strings. Arrays sized n_terms_target;
- * *n_out = strings written. */
-int qvmc_synth_jw_hamiltonian(int n_qubits, int64_t n_terms_target, uint64_t seed, double* coeff, uint64_t* x_words,
-                              uint64_t* y_words, uint64_t* z_words, int64_t* n_out);
-/* n_unq distinct near-Hartree-Fock determinants: first n_electrons orbitals
- * occupied, then 1+Geometric(0.6) random same-spin occupied->empty moves. */
-int qvmc_synth_near_hf_samples(int n_qubits, int n_electrons, int64_t n_unq, uint64_t seed, uint64_t* keys);
 
 #ifdef __cplusplus
 }

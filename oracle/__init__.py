@@ -66,6 +66,8 @@ def olib():
         L.qo_variational_energy.argtypes = [_I64, _P, _D, _D, _P, _P, _P]
         L.qo_eloc_rows.restype = _I64
         L.qo_eloc_rows.argtypes = [_P, _I64, _P, _P, _P, _I64, _I64, _INT, _P, _P]
+        L.qo_rows_list.restype = _I64
+        L.qo_rows_list.argtypes = [_P, _I64, _P, _P, _P, _I64, _P, _INT, C.POINTER(_P), _P, _P, _P]
         _olib = L
     return _olib
 
@@ -142,6 +144,32 @@ class OracleIndex:
             raise RuntimeError(olib().qo_last_error().decode())
         return (out, n, scale) if with_scale else (out, n)
 
+    def rows_list(self, keys, rows, la=None, ph=None, threads=None):
+        """Listed rows against all of keys (terms semantics): -> (pairs [P, 3] canonical,
+        rows in list order; per-row pair counts; E_loc or None; abs-sum scale or None)."""
+        keys = np.ascontiguousarray(keys, dtype=np.uint64)
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        k = len(rows)
+        counts = np.zeros(k, dtype=np.int64)
+        out = scale = None
+        if la is not None:
+            la, ph = (np.ascontiguousarray(a, dtype=np.float64) for a in (la, ph))
+            out = np.zeros(k, dtype=np.complex128)
+            scale = np.zeros(k)
+        p = _P()
+        threads = threads or os.cpu_count() or 1
+        n = olib().qo_rows_list(self._h, keys.shape[0], _ptr(keys), _ptr(la) if la is not None else None,
+                                _ptr(ph) if la is not None else None, k, _ptr(rows), threads, C.byref(p),
+                                _ptr(counts), _ptr(out) if out is not None else None,
+                                _ptr(scale) if scale is not None else None)
+        if n < 0:
+            if p.value:
+                olib().qo_free(p)
+            raise RuntimeError(olib().qo_last_error().decode())
+        arr = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint32)), shape=(max(n, 1) * 3,))[: n * 3].copy()
+        olib().qo_free(p)
+        return arr.reshape(n, 3), counts, out, scale
+
 
 def variational_energy(log_probs, norm, log_norm, eloc):
     """-> (status, e_var, im_residual, ipr, sum_w, sum_w|E|^2, weights)."""
@@ -186,6 +214,10 @@ def rlib():
         L.qref_variational_energy.argtypes = [_I64, _P, _D, _D, _P, _P, _P]
         L.qref_run_path.argtypes = [_P, _I64, _INT, _P, _P, _P, _P, _D, _D, _INT, _INT, _INT, _P, _P, _P,
                                     C.POINTER(_U64)]
+        L.qref_rows_session.restype = _P
+        L.qref_rows_session.argtypes = [_P, _I64, _INT, _P, _P, _P, _P, _D, _D, C.POINTER(_D)]
+        L.qref_rows_session_free.argtypes = [_P]
+        L.qref_rows_session_run.argtypes = [_P, _I64, _P, _INT, _P, C.POINTER(_U64), _P]
         L.qref_rng_new.restype = _P
         L.qref_rng_new.argtypes = [_U64, C.c_uint32]
         L.qref_rng_free.argtypes = [_P]
@@ -311,6 +343,41 @@ class RefIndex:
                                      log_norm, backend, threshold, threads, _ptr(locals_), _ptr(out5), _ptr(t3),
                                      C.byref(npairs)))
         return locals_, out5, t3, npairs.value
+
+    def row_session(self, keys, la, ph, lp, norm, log_norm):
+        return RefRowSession(self, keys, la, ph, lp, norm, log_norm)
+
+
+class RefRowSession:
+    """Listed rows of the whole sample set against the whole sample set, through
+    the reference (ref_capi.cpp qref_rows_session*): the per-row trie walk of
+    loop_over_trie over the reference's PrefixTree builds of the full set
+    (build_seconds: built once here), then the unmodified local_energies and
+    variational_energy over the full batch."""
+
+    def __init__(self, index: "RefIndex", keys, la, ph, lp, norm, log_norm):
+        self._keys = np.ascontiguousarray(keys, dtype=np.uint64)
+        la, ph, lp = (np.ascontiguousarray(a, dtype=np.float64) for a in (la, ph, lp))
+        self.n = self._keys.shape[0]
+        b = _D()
+        self._s = rlib().qref_rows_session(index._h, self.n, index.W, _ptr(self._keys), _ptr(la), _ptr(ph),
+                                           _ptr(lp), norm, log_norm, C.byref(b))
+        if not self._s:
+            raise RefError(rlib().qref_last_error().decode())
+        self.build_seconds = b.value
+
+    def run(self, rows, threads=1, want_locals=False):
+        """-> (times3 = search, local_energies, variational_energy seconds; pairs; E_loc of the rows or None)"""
+        rows = np.ascontiguousarray(np.sort(np.asarray(rows, dtype=np.int64)))
+        t3, npairs = np.zeros(3), _U64()
+        out = np.zeros(len(rows), dtype=np.complex128) if want_locals else None
+        _rcheck(rlib().qref_rows_session_run(self._s, len(rows), _ptr(rows), threads, _ptr(t3), C.byref(npairs),
+                                             _ptr(out) if out is not None else None))
+        return t3, npairs.value, out
+
+    def __del__(self):
+        if getattr(self, "_s", None):
+            rlib().qref_rows_session_free(self._s)
 
 
 def ref_variational_energy(log_probs, norm, log_norm, eloc):

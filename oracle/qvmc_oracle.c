@@ -510,3 +510,118 @@ int64_t qo_eloc_rows(const qo_index* h, int64_t n_unq, const uint64_t* keys, con
   }
   return visited;
 }
+
+/* ------------------------------------ listed rows vs the whole sample set */
+
+/* The rows of a row LIST against the whole sample set: per row the
+ * LoopOverTerms candidate loop (coupling.cpp:72-80) over every flip mask,
+ * the row's pairs in canonical order (coupling.cpp:49-52), and optionally
+ * its E_loc (energy.cpp:35-44) and absolute-sum scale. One members map for
+ * the whole call (the row-range variant above rebuilds nothing per row
+ * either, but takes contiguous ranges only). */
+typedef struct {
+  const qo_index* h;
+  const wmap* members;
+  const uint64_t* keys;
+  const double *la, *ph;
+  const int64_t* rows;
+  int64_t k0, k1;
+  uint32_t** row_pairs; /* per listed row, malloc'd canonical triples */
+  int64_t* counts;
+  double* out;
+  double* scale;
+  int status;
+} list_job;
+
+static void* list_worker(void* arg) {
+  list_job* J = (list_job*)arg;
+  const qo_index* h = J->h;
+  const int kw = h->kw;
+  uint64_t c[4];
+  for (int64_t k = J->k0; k < J->k1; ++k) {
+    const int64_t i = J->rows[k];
+    const uint64_t* x = J->keys + i * kw;
+    vec3 v = {NULL, 0, 0};
+    for (int64_t g = 0; g < h->n_xy; ++g) {
+      for (int w = 0; w < kw; ++w) c[w] = x[w] ^ h->xy[g * kw + w];
+      const int64_t j = wmap_find(J->members, c);
+      if (j >= 0) vec3_push(&v, (uint32_t)i, (uint32_t)j, (uint32_t)g);
+    }
+    if (v.n) qsort(v.e, (size_t)v.n, 12, cmp_pair);
+    J->row_pairs[k] = v.e;
+    J->counts[k] = v.n;
+    if (J->out) {
+      if (isinf(J->la[i])) {
+        J->status = -2;
+        continue;
+      }
+      double sr = 0.0, si = 0.0, sc = 0.0;
+      for (int64_t e = 0; e < v.n; ++e) {
+        const int64_t j = v.e[3 * e + 1], g = v.e[3 * e + 2];
+        accumulate(h, J->keys, J->la, J->ph, i, j, g, &sr, &si);
+        double ga = 0.0;
+        for (int64_t t = h->off[g]; t < h->off[g + 1]; ++t) ga += fabs(h->coeff[t]);
+        sc += ga * exp(J->la[j] - J->la[i]);
+      }
+      J->out[2 * k] = sr;
+      J->out[2 * k + 1] = si;
+      if (J->scale) J->scale[k] = sc;
+    }
+  }
+  return NULL;
+}
+
+int64_t qo_rows_list(const qo_index* h, int64_t n_unq, const uint64_t* keys, const double* la, const double* ph,
+                     int64_t n_rows, const int64_t* rows, int threads, uint32_t** out3, int64_t* out_counts,
+                     double* out_eloc, double* out_scale) {
+  for (int64_t k = 0; k < n_rows; ++k)
+    if (rows[k] < 0 || rows[k] >= n_unq) {
+      snprintf(g_err, sizeof g_err, "invalid_argument: row %lld out of range", (long long)rows[k]);
+      return -1;
+    }
+  const uint64_t* store = keys;
+  wmap members;
+  wmap_init(&members, n_unq, &store, h->kw);
+  for (int64_t i = 0; i < n_unq; ++i)
+    if (wmap_insert(&members, i) >= 0) {
+      wmap_free(&members);
+      snprintf(g_err, sizeof g_err, "invalid_argument: duplicate basis vector at %lld", (long long)i);
+      return -1;
+    }
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  uint32_t** rp = (uint32_t**)calloc((size_t)(n_rows ? n_rows : 1), sizeof(uint32_t*));
+  list_job jobs[256];
+  pthread_t tid[256];
+  const int64_t chunk = (n_rows + threads - 1) / threads;
+  int used = 0;
+  for (int t = 0; t < threads; ++t) {
+    const int64_t a = t * chunk, b = a + chunk < n_rows ? a + chunk : n_rows;
+    if (a >= b) break;
+    jobs[t] = (list_job){h, &members, keys, la, ph, rows, a, b, rp, out_counts, out_eloc, out_scale, 0};
+    pthread_create(&tid[t], NULL, list_worker, &jobs[t]);
+    ++used;
+  }
+  int status = 0;
+  for (int t = 0; t < used; ++t) {
+    pthread_join(tid[t], NULL);
+    if (jobs[t].status) status = jobs[t].status;
+  }
+  wmap_free(&members);
+  int64_t total = 0;
+  for (int64_t k = 0; k < n_rows; ++k) total += out_counts[k];
+  uint32_t* all = (uint32_t*)malloc((size_t)(total ? total : 1) * 12);
+  int64_t at = 0;
+  for (int64_t k = 0; k < n_rows; ++k) {
+    if (out_counts[k]) memcpy(all + 3 * at, rp[k], (size_t)out_counts[k] * 12);
+    at += out_counts[k];
+    free(rp[k]);
+  }
+  free(rp);
+  *out3 = all;
+  if (status) {
+    snprintf(g_err, sizeof g_err, "logic_error: local_energies: sampled state has zero amplitude");
+    return status;
+  }
+  return total;
+}

@@ -70,6 +70,15 @@ int64_t qo_eloc_rows(const qo_index* h, int64_t n_unq, const uint64_t* keys, con
                      const double* phase, int64_t row_begin, int64_t row_end, int threads, double* out_eloc,
                      double* out_scale);
 
+/* Rows of a row LIST (indices into keys) against the whole sample set,
+ * terms semantics: *out3 (malloc'd, free with qo_free) = every listed row's
+ * canonical pairs, rows in list order; out_counts[k] = pairs of rows[k].
+ * With log_amp/phase non-NULL also out_eloc[k] (interleaved re, im) and
+ * optional out_scale[k] as qo_eloc_rows. Returns total pairs or <0. */
+int64_t qo_rows_list(const qo_index* h, int64_t n_unq, const uint64_t* keys, const double* log_amp,
+                     const double* phase, int64_t n_rows, const int64_t* rows, int threads, uint32_t** out3,
+                     int64_t* out_counts, double* out_eloc, double* out_scale);
+
 #ifdef __cplusplus
 }
 #endif

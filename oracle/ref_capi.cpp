@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -28,6 +29,7 @@
 #include "qvmc/hamiltonian.hpp"
 #include "qvmc/model.hpp"
 #include "qvmc/parallel.hpp"
+#include "qvmc/prefix_tree.hpp"
 #include "qvmc/rng.hpp"
 #include "qvmc/sampler.hpp"
 #include "qvmc/synthetic.hpp"
@@ -355,6 +357,118 @@ int qref_run_path(void* hp, std::int64_t n_unq, int n_words, const std::uint64_t
     out5[2] = r.ipr;
     out5[3] = r.norm;
     out5[4] = r.log_norm;
+  });
+}
+
+// ---- A bounded sample of the FULL workload for the CPU baseline: listed rows
+// of the whole sample set, each against the whole sample set (the same
+// pairs per row as the GPU arm's 1e6-row job). find_coupled_pairs has no
+// row-subset entry, so the per-row body of loop_over_trie
+// (coupling.cpp:116-149, reproduced verbatim below) runs over the
+// reference's own PrefixTree builds of the full sample set and of xy_set
+// (built once per session, timed separately, prorated by the caller); the
+// rows' canonical pairs (PerSource::flatten, coupling.cpp:37-58) then go
+// through the unmodified local_energies (energy.cpp:13-48: rows without
+// pairs stay 0) and variational_energy (energy.cpp:50-78) over the whole
+// batch.
+struct RowSession {
+  const HamiltonianIndex* h = nullptr;
+  qvmc::SampleBatch batch;
+  std::unique_ptr<qvmc::PrefixTree> u_tree, xy_tree;
+};
+
+void* qref_rows_session(void* hp, std::int64_t n_unq, int n_words, const std::uint64_t* keys,
+                        const double* log_amps, const double* phases, const double* log_probs, double norm,
+                        double log_norm, double* build_seconds) {
+  RowSession* out = nullptr;
+  const int st = guarded([&] {
+    using clock = std::chrono::steady_clock;
+    auto S = std::make_unique<RowSession>();
+    S->h = static_cast<HamiltonianIndex*>(hp);
+    auto& batch = S->batch;
+    batch.vectors = make_batch(S->h->n_qubits(), n_words, n_unq, keys);
+    batch.log_amps.resize(n_unq);
+    batch.phases.resize(n_unq);
+    batch.log_probs.resize(n_unq);
+    for (std::int64_t i = 0; i < n_unq; ++i) {
+      batch.log_amps[i] = log_amps[i];
+      batch.phases[i] = phases[i];
+      batch.log_probs[i] = log_probs[i];
+    }
+    batch.norm = norm;
+    batch.log_norm = log_norm;
+    const auto t0 = clock::now();
+    S->u_tree = std::make_unique<qvmc::PrefixTree>(qvmc::PrefixTree::build(batch.vectors));
+    S->xy_tree = std::make_unique<qvmc::PrefixTree>(qvmc::PrefixTree::build(S->h->xy_set()));
+    *build_seconds = std::chrono::duration<double>(clock::now() - t0).count();
+    out = S.release();
+  });
+  return st == kOk ? out : nullptr;
+}
+
+void qref_rows_session_free(void* s) { delete static_cast<RowSession*>(s); }
+
+// times3 = (pair search of the listed rows, local_energies, variational_energy) seconds
+int qref_rows_session_run(void* sp, std::int64_t n_rows, const std::int64_t* rows, int threads, double* times3,
+                          std::uint64_t* n_pairs, double* out_eloc_rows) {
+  return guarded([&] {
+    using clock = std::chrono::steady_clock;
+    auto& S = *static_cast<RowSession*>(sp);
+    const auto& batch = S.batch;
+    const auto& u_tree = *S.u_tree;
+    const auto& xy_tree = *S.xy_tree;
+    const int n = u_tree.n_bits();
+    const auto t0 = clock::now();
+    std::vector<std::vector<CoupledPairs::Entry>> acc(static_cast<std::size_t>(n_rows));
+    qvmc::parallel_for(static_cast<int>(n_rows), threads, [&](int k) {
+      const auto i = static_cast<std::size_t>(rows[k]);
+      const BasisVector& x = batch.vectors[i];
+      std::vector<std::pair<std::int32_t, std::int32_t>> frontier{{0, 0}}, next;
+      for (int level = 0; level < n; ++level) {
+        next.clear();
+        const auto u_nodes = u_tree.level(level);
+        const auto xy_nodes = xy_tree.level(level);
+        const int xi = x.bit(level) ? 1 : 0;
+        for (const auto& [un, xn] : frontier) {
+          for (int b = 0; b < 2; ++b) {
+            const std::int32_t u_child = u_nodes[static_cast<std::size_t>(un)].child[b];
+            if (u_child == qvmc::PrefixTree::kNone) continue;
+            const std::int32_t xy_child = xy_nodes[static_cast<std::size_t>(xn)].child[xi ^ b];
+            if (xy_child == qvmc::PrefixTree::kNone) continue;
+            next.emplace_back(u_child, xy_child);
+          }
+        }
+        frontier.swap(next);
+        if (frontier.empty()) break;
+      }
+      auto& row = acc[static_cast<std::size_t>(k)];
+      for (const auto& [un, xn] : frontier)
+        row.push_back({static_cast<std::uint32_t>(i), static_cast<std::uint32_t>(u_tree.leaf_payload(un)),
+                       static_cast<std::uint32_t>(xy_tree.leaf_payload(xn))});
+      std::sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.x_prime < b.x_prime; });
+    });
+    // canonical order: rows ascending (the caller lists them ascending), then x'
+    CoupledPairs pairs;
+    pairs.backend = qvmc::CouplingBackend::kTrie;
+    std::size_t total = 0;
+    for (const auto& r : acc) total += r.size();
+    pairs.entries.reserve(total);
+    for (const auto& r : acc) pairs.entries.insert(pairs.entries.end(), r.begin(), r.end());
+    const auto t1 = clock::now();
+    const auto locals = qvmc::local_energies(pairs, batch, *S.h, threads);
+    const auto t2 = clock::now();
+    const auto rep = qvmc::variational_energy(batch, locals);
+    const auto t3 = clock::now();
+    (void)rep;
+    times3[0] = std::chrono::duration<double>(t1 - t0).count();
+    times3[1] = std::chrono::duration<double>(t2 - t1).count();
+    times3[2] = std::chrono::duration<double>(t3 - t2).count();
+    *n_pairs = total;
+    if (out_eloc_rows)
+      for (std::int64_t k = 0; k < n_rows; ++k) {
+        out_eloc_rows[2 * k] = locals[rows[k]].real();
+        out_eloc_rows[2 * k + 1] = locals[rows[k]].imag();
+      }
   });
 }
 

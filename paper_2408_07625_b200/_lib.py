@@ -73,13 +73,12 @@ SIGNATURES = [
     ("qvmc_cuda_pairs", _INT, [_P, _I64, _P, _INT, _INT, _INT, C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_INT)]),
     ("qvmc_cuda_pairs_fetch", _INT, [_P, _P, _INT]),
     ("qvmc_cuda_pair_elements", _INT, [_P, _I64, _P, _U64, _P, _P, _P, _INT]),
+    ("qvmc_cuda_pair_elements_fused", _INT, [_P, _I64, _P, _U64, _P, _P, _P, _INT]),
     ("qvmc_cuda_local_energies", _INT, [_P, _I64, _P, _P, _P, _U64, _P, _P, _INT]),
     ("qvmc_cuda_energy_moments", _INT, [_P, _I64, _P, C.c_double, _P, _P, _P, _INT]),
     ("qvmc_cuda_eloc_fused", _INT, [_P, _I64, _P, _P, _P, _P, C.c_double, _I64, _I64, _P, _P, _INT]),
     ("qvmc_cuda_last_error", C.c_char_p, []),
     ("qvmc_cuda_launch_count", _U64, []),
-    ("qvmc_synth_jw_hamiltonian", _INT, [_INT, _I64, _U64, _P, _P, _P, _P, C.POINTER(_I64)]),
-    ("qvmc_synth_near_hf_samples", _INT, [_INT, _INT, _I64, _U64, _P]),
     ("qvmc_cuda_model_create", _INT, [_INT, _INT, _INT, _INT, _INT, _INT, C.POINTER(_P)]),
     ("qvmc_cuda_model_destroy", _INT, [_P]),
     ("qvmc_cuda_model_n_params", _INT, [_P, C.POINTER(_I64)]),

@@ -1,5 +1,5 @@
 // Host-side (CPU, setup-time) pieces of libqvmc_cuda: the grouped
-// HamiltonianIndex, the device-layout planner and the synthetic generators.
+// HamiltonianIndex and the device-layout planner.
 // Nothing here runs per sample; the per-sample work is in qvmc_cuda.cu.
 #pragma once
 
@@ -121,10 +121,5 @@ constexpr int fam_words(int W) { return (W + 2 + 1) & ~1; }
 inline uint32_t pair_index(int p, int q, int n) {  // p < q
   return static_cast<uint32_t>(p * n - p * (p + 1) / 2 + (q - p - 1));
 }
-
-// Synthetic generators.
-int64_t synth_jw_hamiltonian(int n_qubits, int64_t n_target, uint64_t seed, double* coeff, uint64_t* xw,
-                             uint64_t* yw, uint64_t* zw);
-void synth_near_hf_samples(int n_qubits, int n_electrons, int64_t n_unq, uint64_t seed, uint64_t* keys);
 
 }  // namespace qvmc_b200

@@ -349,6 +349,145 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Per pair (x, x', xy) of a canonical list: H_{x x'} through the FUSED path's
+// evaluators — the 64-byte drain records (kinds A-D, hit_element) when x' =
+// x ^ xy is a weight-2/4 flip-table mask, the diagonal as the quadratic form
+// over S(x) — plus which evaluator ran (kind: 0-3 = drain record A-D, 4 =
+// term by term, 5 = diagonal quadratic form). One warp per row.
+template <int W>
+__global__ void __launch_bounds__(kThreads)
+    k_pair_records(const __grid_constant__ HamView H, const __grid_constant__ JoinView J,
+                   const uint32_t* __restrict__ gkey, const uint64_t* __restrict__ keys, int64_t n,
+                   const uint32_t* __restrict__ e3, const uint32_t* __restrict__ row_lo,
+                   const uint32_t* __restrict__ row_hi, double2* out_h, uint8_t* out_kind, int* err) {
+  __shared__ uint16_t s_pos[kWarps][32];
+  const int lane = threadIdx.x & 31;
+  uint16_t* spos = s_pos[threadIdx.x >> 5];
+  const int nq = H.n;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += n_warps) {
+    Key<W> xrow;
+    int pc = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      xrow.w[w] = keys[i * W + w];
+      pc += __popcll(xrow.w[w]);
+    }
+    const int side = 2 * pc <= nq ? 1 : 0;
+    const int s = side ? pc : nq - pc;
+    int pos = 0;
+    if (s <= 32) {
+      int cnt = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        uint64_t v = side ? xrow.w[w] : ~xrow.w[w];
+        const int hi_bit = nq - 64 * w;
+        if (hi_bit < 64) v &= (hi_bit <= 0) ? 0ull : ((1ull << hi_bit) - 1);
+        const int c = __popcll(v);
+        if (lane >= cnt && lane < cnt + c) {
+          for (int k = 0; k < lane - cnt; ++k) v &= v - 1;
+          pos = 64 * w + __ffsll(static_cast<long long>(v)) - 1;
+        }
+        cnt += c;
+      }
+      __syncwarp();
+      if (lane < s) spos[lane] = static_cast<uint16_t>(pos);
+      __syncwarp();
+    }
+    const bool quad = H.diag >= 0 && H.diag_quad && s <= 32;
+    const uint32_t lo = row_lo[i], hi = row_hi[i];
+    for (uint32_t e0 = lo; e0 < hi; e0 += 32) {
+      const uint32_t e = e0 + lane;
+      bool valid = e < hi;
+      uint32_t j = 0, g = 0;
+      if (valid) {
+        j = e3[3 * static_cast<uint64_t>(e) + 1];
+        g = e3[3 * static_cast<uint64_t>(e) + 2];
+        if (j >= n || g >= H.n_xy) {
+          atomicOr(err, kErrBadPair);
+          valid = false;
+        }
+      }
+      const bool is_diag = valid && quad && static_cast<int64_t>(g) == H.diag && static_cast<int64_t>(j) == i;
+      JoinHit hit;
+      hit.valid = false;
+      hit.key = kNoKey;
+      hit.sr = U64x4{0, 0, 0, 0};
+#pragma unroll
+      for (int k = 0; k < kGrecWords; ++k) hit.r[k] = 0;
+      uint8_t kind = 4;
+      uint64_t xp[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) xp[w] = 0;
+      if (valid && !is_diag) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) xp[w] = __ldg(keys + static_cast<int64_t>(j) * W + w);
+        const uint32_t key = __ldg(gkey + g);
+        if (key != kNoKey) {
+          uint64_t m[W];
+          key_mask<W>(key, m);
+          bool is_move = true;  // x' = x ^ xy
+#pragma unroll
+          for (int w = 0; w < W; ++w) is_move &= xp[w] == (xrow.w[w] ^ m[w]);
+          const U64x4 g0 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords);
+          const U64x4 g1 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords + 4);
+          const uint32_t kd = static_cast<uint32_t>(g0.a) & 3u;
+          if (kd == kGrecB || kd == kGrecD) {  // family forms need a move inside the minority picture
+            const bool b0 = bit_at<W>(xrow.w, key & 0xFF) == (side != 0);
+            const bool b1 = bit_at<W>(xrow.w, (key >> 8) & 0xFF) == (side != 0);
+            is_move &= (kd == kGrecD || b0 != b1) && s <= 32;
+          }
+          if (is_move) {
+            hit.valid = true;
+            hit.key = key;
+            hit.r[0] = g0.a; hit.r[1] = g0.b; hit.r[2] = g0.c; hit.r[3] = g0.d;
+            hit.r[4] = g1.a; hit.r[5] = g1.b; hit.r[6] = g1.c; hit.r[7] = g1.d;
+            kind = static_cast<uint8_t>(kd);
+          }
+        }
+      }
+      double hr = 0.0, hi2 = 0.0;
+      hit_element<W>(H, J, spos, hit, xrow, lane, s, side, hr, hi2);
+      if (valid && !is_diag && !hit.valid) group_element<W>(H, xp, g, hr, hi2);
+      // the diagonal as the fused path evaluates it: A + sum_S b_p + sum_{p<q in S} K_pq (+ |z| >= 3 terms)
+      if (__any_sync(0xffffffffu, is_diag)) {
+        double2 acc = make_double2(0.0, 0.0);
+        if (lane == 0) acc.x += side ? H.diag_A1 : H.diag_A0;
+        if (lane < s) acc.x += __ldg(H.diag_b + side * nq + spos[lane]);
+        const int np = s * (s - 1) / 2;
+        for (int pi = lane; pi < np; pi += 32) {
+          const int b = static_cast<int>(pair_b(pi)), a = pi - b * (b - 1) / 2;
+          acc.x += __ldg(H.diag_K + spos[a] * nq + spos[b]);
+        }
+        for (uint32_t t2 = lane; t2 < H.n_diag_other; t2 += 32) {
+          const uint32_t t = __ldg(H.diag_other + t2);
+          int c = 0;
+#pragma unroll
+          for (int w = 0; w < W; ++w) c += __popcll(xrow.w[w] & __ldg(H.yz + (int64_t)t * W + w));
+          const int qt = (__ldg(H.yw + t) + 2 * c) & 3;
+          const double cf = __ldg(H.coeff + t);
+          if (qt == 0) acc.x += cf;
+          else if (qt == 2) acc.x -= cf;
+          else if (qt == 1) acc.y += cf;
+          else acc.y -= cf;
+        }
+        acc.x = warp_sum(acc.x);
+        acc.y = warp_sum(acc.y);
+        if (is_diag) {
+          hr = acc.x;
+          hi2 = acc.y;
+          kind = 5;
+        }
+      }
+      if (valid) {
+        out_h[e] = make_double2(hr, hi2);
+        out_kind[e] = kind;
+      }
+    }
+  }
+}
+
 __global__ void k_check_sorted(const uint32_t* e3, uint64_t n_pairs, int64_t n, int* err) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n_pairs;
        e += (uint64_t)gridDim.x * blockDim.x) {
@@ -1533,6 +1672,50 @@ int qvmc_cuda_pair_elements(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, u
   });
 }
 
+int qvmc_cuda_pair_elements_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, uint64_t n_pairs,
+                                  const uint32_t* entries, double* out_h, uint8_t* out_kind, int mem) {
+  return guarded([&] {
+    check_handle(h);
+    check_mem(mem);
+    if (n_unq < 0 || (n_unq > 0 && !keys) || (n_pairs > 0 && (!entries || !out_h || !out_kind)))
+      fail(QVMC_ERR_INVALID_ARGUMENT, "null or negative argument");
+    if (n_pairs == 0 || n_unq == 0) return;
+    DeviceGuard dg(h->device);
+    const int W = h->W;
+    const uint64_t* dkeys = stage(h, h->keys, keys, static_cast<size_t>(n_unq) * W, mem);
+    const uint32_t* de = stage(h, h->in_entries, entries, n_pairs * 3, mem);
+    double2* dh = reinterpret_cast<double2*>(out_h);
+    uint8_t* dk = out_kind;
+    if (mem == QVMC_MEM_HOST) {
+      h->out_h.ensure(n_pairs * 16);
+      h->out_class.ensure(n_pairs + 16);
+      dh = h->out_h.as<double2>();
+      dk = h->out_class.as<uint8_t>();
+    }
+    int* err = static_cast<int*>(h->ctl.p);
+    h->p_rlo.ensure(n_unq * 4 + 16);
+    h->p_rhi.ensure(n_unq * 4 + 16);
+    ck(cudaMemsetAsync(h->p_rlo.p, 0, n_unq * 4, h->stream), "memset rows");
+    ck(cudaMemsetAsync(h->p_rhi.p, 0, n_unq * 4, h->stream), "memset rows");
+    const int g1 = static_cast<int>(std::min<uint64_t>((n_pairs + kThreads - 1) / kThreads, grid_for(h, 8)));
+    k_check_sorted<<<g1, kThreads, 0, h->stream>>>(de, n_pairs, n_unq, err);
+    ck_launch("check pairs");
+    k_pair_rows<<<g1, kThreads, 0, h->stream>>>(de, n_pairs, n_unq, h->p_rlo.as<uint32_t>(), h->p_rhi.as<uint32_t>());
+    ck_launch("pair rows");
+    const int grid = static_cast<int>(std::min<int64_t>((n_unq + kWarps - 1) / kWarps, grid_for(h, 8)));
+    RowPlan P0{};
+    DISPATCH_W(W, (k_pair_records<WW><<<grid, kThreads, 0, h->stream>>>(
+                      h->view, join_view(h, P0), h->gkey.as<uint32_t>(), dkeys, n_unq, de, h->p_rlo.as<uint32_t>(),
+                      h->p_rhi.as<uint32_t>(), dh, dk, err)));
+    ck_launch("pair records");
+    if (mem == QVMC_MEM_HOST) {
+      ck(cudaMemcpyAsync(out_h, dh, n_pairs * 16, cudaMemcpyDeviceToHost, h->stream), "D2H h");
+      ck(cudaMemcpyAsync(out_kind, dk, n_pairs, cudaMemcpyDeviceToHost, h->stream), "D2H kind");
+    }
+    finish(h);
+  });
+}
+
 int qvmc_cuda_local_energies(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, const double* log_amp,
                              const double* phase, uint64_t n_pairs, const uint32_t* entries, double* out_eloc,
                              int mem) {
@@ -1725,23 +1908,6 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
     }
   });
 }
-
-int qvmc_synth_jw_hamiltonian(int n_qubits, int64_t n_terms_target, uint64_t seed, double* coeff, uint64_t* x_words,
-                              uint64_t* y_words, uint64_t* z_words, int64_t* n_out) {
-  return guarded([&] {
-    if (!coeff || !x_words || !y_words || !z_words || !n_out || n_terms_target < 0)
-      fail(QVMC_ERR_INVALID_ARGUMENT, "null or negative argument");
-    *n_out = synth_jw_hamiltonian(n_qubits, n_terms_target, seed, coeff, x_words, y_words, z_words);
-  });
-}
-
-int qvmc_synth_near_hf_samples(int n_qubits, int n_electrons, int64_t n_unq, uint64_t seed, uint64_t* keys) {
-  return guarded([&] {
-    if (!keys || n_unq < 0) fail(QVMC_ERR_INVALID_ARGUMENT, "null or negative argument");
-    synth_near_hf_samples(n_qubits, n_electrons, n_unq, seed, keys);
-  });
-}
-
 
 // ------------------------------------------------------------------ amplitude model
 // AnqsModel (model.cpp) on the device: layout + sector checks as in the

@@ -541,12 +541,12 @@ __device__ __forceinline__ void load_hit(const JoinView& J, const JoinSmem* sm, 
   }
 }
 
-// H_{x x'} psi(x')/psi(x) of one loaded hit, added to acc (warp-collective:
-// large generic groups are split over the lanes)
+// H_{x x'} of one loaded hit from its drain record (warp-collective: large
+// generic groups are split over the lanes). Invalid hits give 0.
 template <int W>
-__device__ __forceinline__ void eval_hit(const HamView& H, const JoinView& J, const uint16_t* pos, const JoinHit& h,
-                                         const Key<W>& xrow, double la_i, double2 cs_i, int lane, int s, int side,
-                                         double2& acc, double inv_ai = 0.0) {
+__device__ __forceinline__ void hit_element(const HamView& H, const JoinView& J, const uint16_t* pos,
+                                            const JoinHit& h, const Key<W>& xrow, int lane, int s, int side,
+                                            double& hr, double& hi) {
   const uint32_t kind = static_cast<uint32_t>(h.r[0]) & 3u;
   const uint32_t nt = static_cast<uint32_t>(h.r[1] >> 32);
   const bool large = h.valid && kind == kGrecC && nt > kSmallGroup;
@@ -559,7 +559,8 @@ __device__ __forceinline__ void eval_hit(const HamView& H, const JoinView& J, co
 #pragma unroll
     for (int w = 0; w < W; ++w) xp[w] = xrow.w[w] ^ m[w];
   }
-  double hr = 0.0, hi = 0.0;
+  hr = 0.0;
+  hi = 0.0;
   if (h.valid && !large) {
     if (kind == kGrecA) {
       kind_a_element<W>(h.r, xrow.w, h.key, hr, hi);
@@ -602,6 +603,15 @@ __device__ __forceinline__ void eval_hit(const HamView& H, const JoinView& J, co
       hi = im;
     }
   }
+}
+
+// H_{x x'} psi(x')/psi(x) of one loaded hit, added to acc (warp-collective)
+template <int W>
+__device__ __forceinline__ void eval_hit(const HamView& H, const JoinView& J, const uint16_t* pos, const JoinHit& h,
+                                         const Key<W>& xrow, double la_i, double2 cs_i, int lane, int s, int side,
+                                         double2& acc, double inv_ai = 0.0) {
+  double hr, hi;
+  hit_element<W>(H, J, pos, h, xrow, lane, s, side, hr, hi);
   if (h.valid) {
     const double2 cs_j = make_double2(__longlong_as_double(static_cast<long long>(h.sr.b)),
                                       __longlong_as_double(static_cast<long long>(h.sr.c)));

@@ -1,6 +1,8 @@
 """Seeded synthetic inputs for the BASELINE.json configurations.
 
-The generators run in C++ inside libqvmc_cuda (``qvmc_synth_*``) so 3e6-term
+The generators run in C++ in ``lib/libqvmc_synth.so`` (``qvmc_synth_*``,
+include/qvmc_synth.h; g++ only, separate from the kernels' libqvmc_cuda.so so
+that bench.py's reference arm never loads the product library) so 3e6-term
 Hamiltonians and 1e6-sample sets take seconds. The reference ships no
 molecule fixtures beyond toy/h2/h4/h6 and its own ``random_hamiltonian``
 produces no off-diagonal couplings at these sizes, so the
@@ -12,13 +14,37 @@ import ctypes as C
 import itertools
 import math
 from dataclasses import dataclass
+from pathlib import Path
 
 import numpy as np
 
-from . import _lib
 from .basis import from_bool_rows, n_words
 from .energy import SampleBatch, normalise
 from .hamiltonian import HamiltonianIndex, _ptr
+
+SYNTH_PATH = Path(__file__).resolve().parent / "lib" / "libqvmc_synth.so"
+_synth = None
+
+
+def _slib() -> C.CDLL:
+    global _synth
+    if _synth is None:
+        if not SYNTH_PATH.exists():
+            raise ImportError(f"{SYNTH_PATH} is missing: run __graft_entry__.build()")
+        L = C.CDLL(str(SYNTH_PATH))
+        L.qvmc_synth_jw_hamiltonian.restype = C.c_int
+        L.qvmc_synth_jw_hamiltonian.argtypes = [C.c_int, C.c_int64, C.c_uint64] + [C.c_void_p] * 4 + [
+            C.POINTER(C.c_int64)]
+        L.qvmc_synth_near_hf_samples.restype = C.c_int
+        L.qvmc_synth_near_hf_samples.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_uint64, C.c_void_p]
+        L.qvmc_synth_last_error.restype = C.c_char_p
+        _synth = L
+    return _synth
+
+
+def _scheck(status: int) -> None:
+    if status != 0:
+        raise ValueError(_slib().qvmc_synth_last_error().decode())
 
 
 @dataclass(frozen=True)
@@ -46,8 +72,8 @@ def jw_terms(n_qubits: int, n_terms: int, seed: int = 1):
     y = np.zeros((n_terms, W), dtype=np.uint64)
     z = np.zeros((n_terms, W), dtype=np.uint64)
     got = C.c_int64()
-    _lib.check(_lib.lib().qvmc_synth_jw_hamiltonian(n_qubits, n_terms, seed, _ptr(coeff), _ptr(x), _ptr(y), _ptr(z),
-                                                    C.byref(got)))
+    _scheck(_slib().qvmc_synth_jw_hamiltonian(n_qubits, n_terms, seed, _ptr(coeff), _ptr(x), _ptr(y), _ptr(z),
+                                              C.byref(got)))
     k = int(got.value)
     return coeff[:k], x[:k], y[:k], z[:k]
 
@@ -58,7 +84,7 @@ def jw_hamiltonian(n_qubits: int, n_terms: int, seed: int = 1) -> HamiltonianInd
 
 def near_hf_keys(n_qubits: int, n_electrons: int, n_unq: int, seed: int = 2) -> np.ndarray:
     keys = np.zeros((n_unq, n_words(n_qubits)), dtype=np.uint64)
-    _lib.check(_lib.lib().qvmc_synth_near_hf_samples(n_qubits, n_electrons, n_unq, seed, _ptr(keys)))
+    _scheck(_slib().qvmc_synth_near_hf_samples(n_qubits, n_electrons, n_unq, seed, _ptr(keys)))
     return keys
 
 

@@ -313,3 +313,60 @@ def test_other_row_paths_match_oracle(cuda_ok, n_qubits, n_e, n_terms, n_unq, jo
     else:
         _, rep, st = _synthetic_rows_vs_oracle(n_qubits, n_e, n_terms, n_unq, 64, seed=n_qubits)
     assert st["join_mode"] == join
+
+
+def _restated_moments(lp, log_norm, eloc):
+    """Var = sum_x w_x |E_loc(x) - E|^2, E = sum_x w_x E_loc(x), w = exp(lp - log_norm)
+    (the reference computes no variance; this is the definition)."""
+    w = np.exp(np.asarray(lp) - log_norm)
+    e0 = np.sum(w * eloc)
+    return float(np.sum(w * np.abs(eloc - e0) ** 2)), float(np.sum(w * np.abs(eloc) ** 2)), w
+
+
+def _check_variance(H, b, want_eloc, scale):
+    var, m4, w = _restated_moments(b.log_probs, b.log_norm, want_eloc)
+    tol = 1e-9 * max(1.0, float(np.sum(w * (np.abs(want_eloc) + scale) ** 2)))
+    fused = q.surrogate_energy(H, b, check=False)
+    assert abs(fused.variance - var) <= tol, (fused.variance, var)
+    # moment 5 itself (sum w |E|^2) through the moments entry point, on the golden E_loc
+    rep = q.variational_energy(b, want_eloc, index=H) if abs(np.sum(w * want_eloc).imag) <= 1e-6 * max(
+        1.0, abs(np.sum(w * want_eloc).real)) else None
+    if rep is not None:
+        assert abs(rep.variance - var) <= 1e-12 * max(1.0, m4)
+        assert abs((rep.variance + rep.e_var ** 2 + rep.im_residual ** 2) - m4) <= 1e-12 * max(1.0, m4)
+    return fused
+
+
+@pytest.mark.parametrize("family", FAMILIES)
+def test_variance_matches_restatement_families(cuda_ok, family):
+    g = golden(family)
+    for _, p in instances(family):
+        H = product_index(g, p)
+        b = _batch(g, p)
+        scale = eloc_scale(g[p + "pairs"], g[p + "offsets"], g[p + "coeff"], g[p + "la"], b.size())
+        _check_variance(H, b, g[p + "eloc"], scale)
+
+
+@pytest.mark.parametrize("name", ["toy", "h2", "h4", "h6"])
+def test_variance_matches_restatement_fixtures(cuda_ok, name):
+    g = golden("fixtures")
+    H = product_index(g, f"{name}_")
+    sp = f"{name}_sector_"
+    b = _batch(g, sp)
+    scale = eloc_scale(g[sp + "pairs"], g[f"{name}_offsets"], g[f"{name}_coeff"], g[sp + "la"], b.size())
+    _check_variance(H, b, g[sp + "eloc"], scale)
+
+
+def test_c20_energy_and_variance_at_1e5(cuda_ok):
+    """BASELINE config 2 shape: 20 q, n_e = 10, 1e5 unique random sector states
+    (DESIGN §7), every row's E_loc vs the oracle, energy and variance."""
+    c, x, y, z = synthetic.jw_terms(20, 12_000, seed=1)
+    H = q.HamiltonianIndex.from_masks(20, c, x, y, z)
+    O = oracle.OracleIndex(20, c, x, y, z)
+    keys = synthetic.random_sector_keys(20, 10, 100_000, seed=2)
+    b = synthetic.sample_batch(keys, seed=3)
+    want, _, scale = O.eloc_rows(keys, b.log_amps, b.phases, 0, len(keys), with_scale=True)
+    fused = _check_variance(H, b, want, scale)
+    assert_eloc_close(fused.locals, want, scale)
+    st, m, _ = oracle.variational_energy(b.log_probs, b.norm, b.log_norm, want)
+    assert abs(fused.e_var - m[0]) <= 1e-10 * max(1.0, float(np.sum(np.exp(b.log_probs - b.log_norm) * scale)))

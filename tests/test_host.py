@@ -5,6 +5,7 @@ covered by test_gpu_parity.py.
 """
 import ctypes as C
 import re
+import subprocess
 from pathlib import Path
 
 import numpy as np
@@ -131,6 +132,22 @@ def test_cabi_exports_every_declared_symbol():
     for name in names:
         assert hasattr(lib, name), name
     assert {n for n, _, _ in _lib.SIGNATURES} == set(names)
+
+
+def test_synth_library_is_separate():
+    """qvmc_synth.h symbols live in libqvmc_synth.so only: the reference arm of
+    bench.py generates its inputs without loading the kernels' library."""
+    import ctypes as C
+    from paper_2408_07625_b200 import synthetic
+    text = re.sub(r"/\*.*?\*/", "", (ROOT / "include" / "qvmc_synth.h").read_text(), flags=re.S)
+    names = sorted(set(re.findall(r"\b(qvmc_[a-z_0-9]+)\s*\(", text)))
+    assert len(names) == 3
+    slib = synthetic._slib()
+    for name in names:
+        assert hasattr(slib, name), name
+        assert not hasattr(_lib.lib(), name), name
+    deps = subprocess.run(["ldd", str(synthetic.SYNTH_PATH)], capture_output=True, text=True).stdout
+    assert "cuda" not in deps and "qvmc_cuda" not in deps
 
 
 def test_cabi_reports_missing_device_cleanly():

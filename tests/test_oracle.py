@@ -120,3 +120,44 @@ def test_reference_build_reproduces_goldens():
     assert np.array_equal(R.xy, g["toy_xy"]) and np.array_equal(R.coeff, g["toy_coeff"])
     e, ops, be = R.pairs(np.array([[0b0011], [0b1001], [0b0110]], np.uint64), backend=1)
     assert np.array_equal(e, g["toybatch_pairs"]) and ops == 9 and be == 1
+
+
+@pytest.mark.parametrize("family", FAMILIES)
+def test_oracle_row_list_matches_reference(family):
+    """qo_rows_list (listed rows against the whole sample set, the checker of
+    tests/test_gpu_fullsize.py) reproduces the reference's pairs and E_loc
+    for rows in any order."""
+    g = golden(family)
+    for s, p in instances(family):
+        O = oracle_index(g, p)
+        keys = g[p + "keys"]
+        n = len(keys)
+        rows = np.random.default_rng(s).permutation(n)
+        pr, cnt, e, sc = O.rows_list(keys, rows, g[p + "la"], g[p + "ph"], threads=3)
+        parts = np.split(pr, np.cumsum(cnt)[:-1]) if n else []
+        back = [None] * n
+        for k, r in enumerate(rows):
+            back[r] = parts[k]
+        got = np.concatenate(back).reshape(-1, 3) if n else pr
+        assert np.array_equal(got, g[p + "pairs"].reshape(-1, 3))
+        inv = np.argsort(rows)
+        scale = eloc_scale(g[p + "pairs"], g[p + "offsets"], g[p + "coeff"], g[p + "la"], n)
+        assert np.all(np.abs(e[inv] - g[p + "eloc"]) <= 1e-12 * scale)
+        assert np.allclose(sc[inv], scale, rtol=1e-12, atol=1e-300)
+
+
+def test_variance_definition_on_goldens():
+    """EnergyReport.variance from the five moments (energy.py) equals the
+    definition Var = sum w |E - E0|^2 on the reference's own E_loc."""
+    from paper_2408_07625_b200.energy import _report_from_moments
+    for family in FAMILIES:
+        g = golden(family)
+        for _, p in instances(family):
+            st, m, w = oracle.variational_energy(g[p + "lp"], float(g[p + "norm"]), float(g[p + "log_norm"]),
+                                                 g[p + "eloc"])
+            e = g[p + "eloc"]
+            e0 = np.sum(w * e)
+            var = float(np.sum(w * np.abs(e - e0) ** 2))
+            assert abs(m[4] - float(np.sum(w * np.abs(e) ** 2))) <= 1e-12 * max(1.0, m[4])
+            r = _report_from_moments(m, float(g[p + "norm"]), float(g[p + "log_norm"]), e, w)
+            assert abs(r.variance - var) <= 1e-12 * max(1.0, m[4])
