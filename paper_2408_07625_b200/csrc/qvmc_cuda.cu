@@ -23,7 +23,6 @@
 
 #include "host_index.h"
 #include "qvmc_cuda.h"
-#include "qvmc_bucket.cuh"
 #include "qvmc_join.cuh"
 #include "qvmc_kernels.cuh"
 #include "qvmc_model.cuh"
@@ -141,12 +140,10 @@ struct qvmc_ham_s {
   HamView view{};
   // join path (per call): deletion-index workspace
   DBuf l_key, l_key2, l_idx, l_perm, l_keys, l_rec, l_flags, l_list, l_nsel, cs;
-  DBuf j_key, j_val, j_key2, j_val2, j_head, j_rid, j_lo, j_hi, j_mem, j_rng, j_tmp, j_pos_of;
+  DBuf j_key, j_val, j_key2, j_val2, j_head, j_rid, j_lo, j_hi, j_mem, j_rng, j_tmp;
   bool use_join = true;
-  int join_mode = 1;  // 0 fused row kernel, 1 row search + chunk eval (measured best), 2 bucket-centric search + row eval
   // split-evaluation workspace
-  DBuf s_hy, s_hg, s_hk, s_chunk, s_row_last, s_base, s_part, s_head, b_icnt, b_iincl, b_items, s_rowpos;
-  uint64_t hit_cap = 0, chunk_cap = 0;
+  DBuf s_row_last, s_base, s_rowpos;
   uint64_t hits_per_row = 320;  // split evaluation: running estimate that sizes the row batches
   DBuf gkey, p_rlo, p_rhi;      // per-group position key (pairs-based local_energies), row ranges
   // pipelined split evaluation (run_join_pipelined)
@@ -157,7 +154,6 @@ struct qvmc_ham_s {
   unsigned long long* log_host = nullptr;
   uint64_t log_cap = 0;
   int pipe_batches = 2, pipe_search_blocks = 0, pipe_eval_blocks = 0;  // measured: 2-3 batches best
-  bool pipelined = true;
   // workspace
   DBuf tab, ctl, keys, la, ph, lp, eloc, partials, moments, weights;
   DBuf counts, row_off, xp_a, g_a, xp_b, g_b, entries, cub_tmp, in_entries, out_h, out_class;
@@ -166,8 +162,6 @@ struct qvmc_ham_s {
   int64_t pairs_rows = 0;
   qvmc_stats last{};
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // fused-call stage timing
-  cudaEvent_t ev_k[3] = {nullptr, nullptr, nullptr};         // split evaluation: search | eval
-  bool timed_k = false;
   bool timed = false;
   std::vector<cudaEvent_t> ev_b;  // pipelined split evaluation: per batch search start/end, eval start/end
   int64_t timed_b = 0;            // batches timed by ev_b in the last call
@@ -600,7 +594,6 @@ struct RowPlan {
   int side = 0;
   int s = 0;
   int key_bits = 0;  // join: bits of the exact bucket rank, ceil(log2 C(n, s - 2))
-  bool want_pos_of = false;  // bucket-centric evaluation needs the entry position of every (sample, pair)
 };
 
 RowPlan plan_rows(qvmc_ham_s* h, int64_t n) {
@@ -637,7 +630,6 @@ void build_join_index_k(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const Ro
   h->j_hi.ensure(E * 4 + 16);
   h->j_mem.ensure(E * 8 + 16);
   h->j_rng.ensure(E * 8 + 16);
-  if (P.want_pos_of) h->j_pos_of.ensure(E * 4 + 16);
   const int grid = static_cast<int>(std::min<int64_t>((n + kWarps - 1) / kWarps, grid_for(h, 8)));
   k_join_keys<W, K><<<std::max(grid, 1), kThreads, 0, h->stream>>>(keys, n, h->n, P.side, P.s, h->binom.as<uint64_t>(),
                                                                    h->j_key.as<K>(), h->j_val.as<uint32_t>());
@@ -666,8 +658,7 @@ void build_join_index_k(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const Ro
   k_join_fill<W><<<std::max(egrid, 1), kThreads, 0, h->stream>>>(h->j_val2.as<uint32_t>(), h->j_rid.as<uint32_t>(), E,
                                                                C, h->j_lo.as<uint32_t>(), h->j_hi.as<uint32_t>(),
                                                                keys, h->n, P.side,
-                                                               h->j_mem.as<uint64_t>(), h->j_rng.as<uint2>(),
-                                                               P.want_pos_of ? h->j_pos_of.as<uint32_t>() : nullptr);
+                                                               h->j_mem.as<uint64_t>(), h->j_rng.as<uint2>());
   ck_launch("join fill");
 }
 
@@ -707,123 +698,6 @@ void launch_rows_join(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, cons
                                                          ctl_view(h), O);
     ck_launch("row kernel (join)");
   }
-}
-
-// Join rows with split evaluation: the search kernel streams each row's hits
-// into chunks, k_eval_chunks evaluates them (its own register budget), and
-// k_finalize_rows sums base + chunks per row in a fixed order. The hit
-// buffers grow (and the search reruns) when a call overflows them.
-template <int W>
-void run_join_split_batch(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const RowPlan& P, double2* eloc,
-                          uint64_t& hits_seen, unsigned long long* stats_before) {
-  const int64_t rows = R.n_rows;
-  int* ctl = static_cast<int*>(h->ctl.p);
-  unsigned long long rd[4] = {0, 0, 0, 0};  // stats[2] (candidates, pairs), hit and chunk cursors
-  unsigned long long* cur = rd + 2;
-  for (int attempt = 0;; ++attempt) {
-    h->hit_cap = std::min<uint64_t>(h->hit_cap, 0xFFFFFFFFull);
-    h->s_hy.ensure(h->hit_cap * 4 + 16);
-    h->s_hg.ensure(h->hit_cap * 4 + 16);
-    h->s_hk.ensure(h->hit_cap * 4 + 16);
-    h->s_chunk.ensure(h->chunk_cap * 16 + 16);
-    h->s_part.ensure(h->chunk_cap * 16 + 16);
-    ck(cudaMemsetAsync(ctl + 4, 0, 2 * sizeof(int), h->stream), "memset row counter");
-    ck(cudaMemsetAsync(ctl + 10, 0, 4 * sizeof(int), h->stream), "memset cursors");
-    RowOut O{};
-    O.hy = h->s_hy.as<uint32_t>();
-    O.hg = h->s_hg.as<uint32_t>();
-    O.hk = h->s_hk.as<uint32_t>();
-    O.chunk = h->s_chunk.as<uint4>();
-    O.row_last = h->s_row_last.as<uint32_t>();
-    O.base = h->s_base.as<double2>();
-    O.hit_cursor = reinterpret_cast<unsigned long long*>(ctl + 10);
-    O.chunk_cursor = reinterpret_cast<unsigned long long*>(ctl + 12);
-    O.hit_cap = h->hit_cap;
-    O.chunk_cap = h->chunk_cap;
-    O.rowpos = h->s_rowpos.as<uint8_t>();
-    int per_sm = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_join<W, kModeHits>, kThreads, 0), "occupancy");
-    const int64_t blocks_needed = (rows + kWarps - 1) / kWarps;
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_needed, grid_for(h, per_sm))));
-    TableView T{h->tab.as<uint64_t>(), h->tab_buckets - 1};
-    ck(cudaEventRecord(h->ev_k[0], h->stream), "event");
-    k_rows_join<W, kModeHits><<<grid, kThreads, 0, h->stream>>>(h->view, T, join_view(h, P), keys, R, P.side, P.s,
-                                                                ctl_view(h), O);
-    ck(cudaEventRecord(h->ev_k[1], h->stream), "event");
-    ck_launch("row kernel (join search)");
-    ck(cudaMemcpyAsync(rd, ctl + 6, sizeof(rd), cudaMemcpyDeviceToHost, h->stream), "D2H stats + cursors");
-    ck(cudaStreamSynchronize(h->stream), "sync");
-    if (cur[0] <= h->hit_cap && cur[1] <= h->chunk_cap) {
-      stats_before[0] = rd[0];
-      stats_before[1] = rd[1];
-      break;
-    }
-    // grow to the demand seen and rerun (counters restored); a batch never needs more than 2^32 hits
-    if (attempt >= 3 || h->hit_cap >= 0xFFFFFFFFull) fail(QVMC_ERR_RUNTIME, "join hit buffers keep overflowing");
-    ck(cudaMemcpy(ctl + 6, stats_before, 2 * sizeof(unsigned long long), cudaMemcpyHostToDevice), "restore stats");
-    h->hit_cap = std::max<uint64_t>(h->hit_cap, cur[0] + cur[0] / 4 + 1024);
-    h->chunk_cap = std::max<uint64_t>(h->chunk_cap, cur[1] + cur[1] / 4 + 1024);
-    int err = 0;
-    ck(cudaMemcpy(&err, ctl, sizeof(int), cudaMemcpyDeviceToHost), "read err");
-    err &= ~kErrHitOverflow;
-    ck(cudaMemcpy(ctl, &err, sizeof(int), cudaMemcpyHostToDevice), "reset overflow");
-  }
-  hits_seen += cur[0];
-  const uint64_t nc = cur[1];
-  if (nc > 0) {
-    int per_sm = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_chunks<W>, kThreads, 0), "occupancy");
-    const int grid = static_cast<int>(
-        std::max<uint64_t>(1, std::min<uint64_t>((nc + kWarps - 1) / kWarps, static_cast<uint64_t>(grid_for(h, per_sm)))));
-    k_eval_chunks<W><<<grid, kThreads, 0, h->stream>>>(
-        h->view, join_view(h, P), keys, h->s_chunk.as<uint4>(), reinterpret_cast<unsigned long long*>(ctl + 12),
-        h->s_hy.as<uint32_t>(), h->s_hg.as<uint32_t>(), h->s_hk.as<uint32_t>(), P.side, P.s, ctl + 14,
-        h->s_rowpos.as<uint8_t>(), h->s_part.as<double2>(), h->chunk_cap);
-    ck_launch("eval chunks");
-  }
-  ck(cudaEventRecord(h->ev_k[2], h->stream), "event");
-  h->timed_k = true;
-  const int fgrid = static_cast<int>(std::min<int64_t>((rows + kThreads - 1) / kThreads, grid_for(h, 8)));
-  k_finalize_rows<<<std::max(fgrid, 1), kThreads, 0, h->stream>>>(h->s_row_last.as<uint32_t>(), h->s_chunk.as<uint4>(),
-                                                                   h->s_part.as<double2>(), h->s_base.as<double2>(), R,
-                                                                   eloc);
-  ck_launch("finalize rows");
-}
-
-// Join rows with split evaluation: the search kernel streams each row's hits
-// into chunks, k_eval_chunks evaluates them (its own register budget), and
-// k_finalize_rows sums base + chunks per row in a fixed order. Rows run in
-// batches of at most ~2^31 expected hits (32-bit hit offsets, bounded hit
-// buffers); the buffers grow (and the batch's search reruns) on overflow.
-template <int W>
-void run_join_split(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, const RowSet& R, const RowPlan& P,
-                    double2* eloc) {
-  const int64_t rows = R.n_rows;
-  if (rows <= 0) return;
-  constexpr uint64_t kBatchHits = 1ull << 31;
-  const uint64_t per_row = std::max<uint64_t>(h->hits_per_row, 64);
-  const int64_t batch = static_cast<int64_t>(std::max<uint64_t>(1, std::min<uint64_t>(rows, kBatchHits / per_row)));
-  if (h->hit_cap == 0) {
-    h->hit_cap = std::max<uint64_t>(static_cast<uint64_t>(batch) * per_row * 5 / 4, 1u << 16);
-    h->chunk_cap = h->hit_cap / 64 + static_cast<uint64_t>(batch) + 1024;
-  }
-  h->s_row_last.ensure(rows * 4 + 16);
-  h->s_base.ensure(rows * 16 + 16);
-  h->s_rowpos.ensure(static_cast<size_t>(n_all) * 16 + 16);
-  uint64_t hits_seen = 0;
-  unsigned long long stats_before[2] = {0, 0};
-  ck(cudaMemcpyAsync(stats_before, static_cast<int*>(h->ctl.p) + 6, sizeof(stats_before), cudaMemcpyDeviceToHost,
-                     h->stream),
-     "D2H stats");
-  ck(cudaStreamSynchronize(h->stream), "sync");
-  for (int64_t b0 = 0; b0 < rows; b0 += batch) {
-    RowSet Rb = R;
-    Rb.n_rows = std::min<int64_t>(batch, rows - b0);
-    if (R.list) Rb.list = R.list + b0;
-    else Rb.base = R.base + b0;
-    run_join_split_batch<W>(h, keys, Rb, P, eloc, hits_seen, stats_before);
-  }
-  h->hits_per_row = std::max<uint64_t>(h->hits_per_row, hits_seen / static_cast<uint64_t>(rows) + 1);
 }
 
 // Pipelined split evaluation: rows in NB batches, the search of batch b+1
@@ -945,7 +819,6 @@ void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
       need_c = std::max<uint64_t>(need_c, h->log_host[2 * b + 1]);
       hits += h->log_host[2 * b];
     }
-    h->timed_k = false;
     h->timed_b = (rows + batch - 1) / batch;  // non-empty batches (each recorded its four events)
     if (need_h <= h->p_hit_cap && need_c <= h->p_chunk_cap) {
       h->hits_per_row = std::max<uint64_t>(h->hits_per_row, hits / static_cast<uint64_t>(rows) + 1);
@@ -960,104 +833,6 @@ void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
     ck(cudaMemcpy(ctl, &err, sizeof(int), cudaMemcpyHostToDevice), "reset overflow");
     ck(cudaMemset(ctl + 6, 0, 4 * sizeof(int)), "reset stats");
   }
-}
-
-// Bucket-centric join (qvmc_bucket.cuh): work items over the deletion-index
-// buckets, the bucket search (hits chained per member entry; buffers grow and
-// the search reruns on overflow), then one warp per row evaluates.
-template <int W>
-void run_join_bucket(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, const RowSet& R, const RowPlan& P,
-                     int64_t r_begin, int64_t r_end, double2* eloc) {
-  const int64_t rows = R.n_rows;
-  if (rows <= 0) return;
-  const uint32_t C = static_cast<uint32_t>(P.s * (P.s - 1) / 2);
-  const uint64_t E = static_cast<uint64_t>(n_all) * C;
-  int* ctl = static_cast<int*>(h->ctl.p);
-  // work items
-  h->b_icnt.ensure(E * 4 + 16);
-  h->b_iincl.ensure(E * 4 + 16);
-  const int egrid = static_cast<int>(std::min<uint64_t>((E + kThreads - 1) / kThreads, grid_for(h, 16)));
-  k_item_count<<<std::max(egrid, 1), kThreads, 0, h->stream>>>(h->j_lo.as<uint32_t>(), h->j_hi.as<uint32_t>(),
-                                                                h->j_rid.as<uint32_t>(), E, h->b_icnt.as<uint32_t>());
-  ck_launch("item count");
-  size_t tmp = 0;
-  ck(cub::DeviceScan::InclusiveSum(nullptr, tmp, h->b_icnt.as<uint32_t>(), h->b_iincl.as<uint32_t>(),
-                                   static_cast<int>(E), h->stream),
-     "scan size");
-  h->j_tmp.ensure(tmp + 16);
-  ck(cub::DeviceScan::InclusiveSum(h->j_tmp.p, tmp, h->b_icnt.as<uint32_t>(), h->b_iincl.as<uint32_t>(),
-                                   static_cast<int>(E), h->stream),
-     "scan");
-  ++g_launches;
-  uint32_t n_items = 0;
-  ck(cudaMemcpyAsync(&n_items, h->b_iincl.as<uint32_t>() + (E - 1), 4, cudaMemcpyDeviceToHost, h->stream), "D2H items");
-  ck(cudaStreamSynchronize(h->stream), "sync");
-  h->b_items.ensure(static_cast<size_t>(n_items) * 16 + 16);
-  k_item_emit<<<std::max(egrid, 1), kThreads, 0, h->stream>>>(h->j_lo.as<uint32_t>(), h->j_hi.as<uint32_t>(),
-                                                               h->b_icnt.as<uint32_t>(), h->b_iincl.as<uint32_t>(), E,
-                                                               h->b_items.as<uint4>());
-  ck_launch("item emit");
-  // search
-  if (h->hit_cap == 0) {
-    h->hit_cap = std::max<uint64_t>(static_cast<uint64_t>(rows) * 320, 1u << 16);
-    h->chunk_cap = h->hit_cap / 8 + static_cast<uint64_t>(rows) + 1024;
-  }
-  h->s_head.ensure(E * 4 + 16);
-  unsigned long long cur[2] = {0, 0};
-  const bool shard = r_begin != 0 || r_end != n_all;
-  for (int attempt = 0;; ++attempt) {
-    h->hit_cap = std::min<uint64_t>(h->hit_cap, 0xFFFFFFFFull);
-    h->chunk_cap = std::min<uint64_t>(h->chunk_cap, 0xFFFFFFFEull);
-    h->s_hy.ensure(h->hit_cap * 4 + 16);
-    h->s_hg.ensure(h->hit_cap * 4 + 16);
-    h->s_hk.ensure(h->hit_cap * 4 + 16);
-    h->s_chunk.ensure(h->chunk_cap * 16 + 16);
-    ck(cudaMemsetAsync(h->s_head.p, 0xFF, E * 4, h->stream), "memset heads");
-    ck(cudaMemsetAsync(ctl + 4, 0, 2 * sizeof(int), h->stream), "memset item counter");
-    ck(cudaMemsetAsync(ctl + 6, 0, 8 * sizeof(int), h->stream), "memset stats + cursors");
-    BucketOut O{};
-    O.hy = h->s_hy.as<uint32_t>();
-    O.hg = h->s_hg.as<uint32_t>();
-    O.hk = h->s_hk.as<uint32_t>();
-    O.chunk = h->s_chunk.as<uint4>();
-    O.head = h->s_head.as<uint32_t>();
-    O.hit_cursor = reinterpret_cast<unsigned long long*>(ctl + 10);
-    O.chunk_cursor = reinterpret_cast<unsigned long long*>(ctl + 12);
-    O.hit_cap = h->hit_cap;
-    O.chunk_cap = h->chunk_cap;
-    int per_sm = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bucket_search<W>, kThreads, 0), "occupancy");
-    const int grid = static_cast<int>(std::max<uint64_t>(
-        1, std::min<uint64_t>((n_items + kWarps - 1) / kWarps, static_cast<uint64_t>(grid_for(h, per_sm)))));
-    if (n_items > 0) {
-      k_bucket_search<W><<<grid, kThreads, 0, h->stream>>>(join_view(h, P), keys, h->n, h->b_items.as<uint4>(),
-                                                           h->b_iincl.as<uint32_t>() + (E - 1), P.side,
-                                                           shard ? R.perm : nullptr, r_begin, r_end, ctl_view(h), O);
-      ck_launch("bucket search");
-    }
-    ck(cudaMemcpyAsync(cur, ctl + 10, sizeof(cur), cudaMemcpyDeviceToHost, h->stream), "D2H cursors");
-    ck(cudaStreamSynchronize(h->stream), "sync");
-    if (cur[0] <= h->hit_cap && cur[1] <= h->chunk_cap) break;
-    if (attempt >= 3) fail(QVMC_ERR_RUNTIME, "join hit buffers keep overflowing");
-    h->hit_cap = std::max<uint64_t>(h->hit_cap, cur[0] + cur[0] / 4 + 1024);
-    h->chunk_cap = std::max<uint64_t>(h->chunk_cap, cur[1] + cur[1] / 4 + 1024);
-    int err = 0;
-    ck(cudaMemcpy(&err, ctl, sizeof(int), cudaMemcpyDeviceToHost), "read err");
-    err &= ~kErrHitOverflow;
-    ck(cudaMemcpy(ctl, &err, sizeof(int), cudaMemcpyHostToDevice), "reset overflow");
-  }
-  // evaluation, one warp per row
-  ck(cudaMemsetAsync(ctl + 4, 0, 2 * sizeof(int), h->stream), "memset row counter");
-  int per_sm = 0;
-  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bucket_eval<W>, kThreads, 0), "occupancy");
-  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((rows + kWarps - 1) / kWarps,
-                                                                           grid_for(h, per_sm))));
-  TableView T{h->tab.as<uint64_t>(), h->tab_buckets - 1};
-  k_bucket_eval<W><<<grid, kThreads, 0, h->stream>>>(h->view, T, join_view(h, P), keys, R, P.side, P.s,
-                                                     h->j_pos_of.as<uint32_t>(), h->s_head.as<uint32_t>(),
-                                                     h->s_chunk.as<uint4>(), h->s_hy.as<uint32_t>(),
-                                                     h->s_hg.as<uint32_t>(), h->s_hk.as<uint32_t>(), ctl_view(h), eloc);
-  ck_launch("bucket eval");
 }
 
 template <int W, int MODE>
@@ -1184,7 +959,6 @@ void compute_moments(qvmc_ham_s* h, const double* lp, double log_norm, const dou
 
 void record_stats(qvmc_ham_s* h, int64_t rows) {
   h->timed = false;
-  h->timed_k = false;
   h->timed_b = 0;
   h->last = qvmc_stats{};
   h->last.rows = static_cast<uint64_t>(rows);
@@ -1308,7 +1082,6 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     ck(cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking), "stream create");
     h->stream = h->own;
     for (auto& e : h->ev) ck(cudaEventCreate(&e), "event create");
-    for (auto& e : h->ev_k) ck(cudaEventCreate(&e), "event create");
     upload(h->xy, hi.xy);
     upload(h->xy_hash, p.xy_hash);
     upload(h->goff, p.offsets32);
@@ -1375,16 +1148,12 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
       upload(h->gkey, gk);
     }
     if (const char* e = std::getenv("QVMC_JOIN")) h->use_join = std::atoi(e) != 0;
-    if (const char* e = std::getenv("QVMC_JOIN_MODE")) h->join_mode = std::atoi(e);
-    if (const char* e = std::getenv("QVMC_PIPELINE")) h->pipelined = std::atoi(e) != 0;
     if (const char* e = std::getenv("QVMC_PIPE_BATCHES")) h->pipe_batches = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("QVMC_PIPE_SEARCH_BLOCKS")) h->pipe_search_blocks = std::atoi(e);
     if (const char* e = std::getenv("QVMC_PIPE_EVAL_BLOCKS")) h->pipe_eval_blocks = std::atoi(e);
     if (const char* e = std::getenv("QVMC_HIT_CAP")) {  // test hook: a small first capacity exercises the regrow path
-      h->hit_cap = std::strtoull(e, nullptr, 10);
-      h->chunk_cap = h->hit_cap / 8 + 64;
-      h->p_hit_cap = h->hit_cap;
-      h->p_chunk_cap = h->chunk_cap;
+      h->p_hit_cap = std::strtoull(e, nullptr, 10);
+      h->p_chunk_cap = h->p_hit_cap / 8 + 64;
     }
     h->ctl.ensure(kCtlInts * sizeof(int) * 2);
     ck(cudaMemset(h->ctl.p, 0, kCtlInts * sizeof(int) * 2), "memset ctl");
@@ -1451,8 +1220,6 @@ int qvmc_cuda_ham_destroy(qvmc_ham_t h) {
     }
     for (auto& e : h->ev)
       if (e) cudaEventDestroy(e);
-    for (auto& e : h->ev_k)
-      if (e) cudaEventDestroy(e);
     for (auto& e : h->ev_p)
       if (e) cudaEventDestroy(e);
     for (auto& e : h->ev_b) cudaEventDestroy(e);
@@ -1496,10 +1263,7 @@ int qvmc_cuda_last_stats(qvmc_ham_t h, qvmc_stats* out) {
       ck(cudaEventElapsedTime(&out->rows_ms, h->ev[1], h->ev[2]), "elapsed");
       ck(cudaEventElapsedTime(&out->moments_ms, h->ev[2], h->ev[3]), "elapsed");
     }
-    if (h->timed_k) {
-      ck(cudaEventElapsedTime(&out->search_ms, h->ev_k[0], h->ev_k[1]), "elapsed");
-      ck(cudaEventElapsedTime(&out->eval_ms, h->ev_k[1], h->ev_k[2]), "elapsed");
-    } else if (h->timed_b > 0) {  // pipelined: per-launch kernel times summed over the row batches
+    if (h->timed_b > 0) {  // pipelined: per-launch kernel times summed over the row batches
       out->search_ms = out->eval_ms = 0.f;
       for (int64_t b = 0; b < h->timed_b; ++b) {
         float ts = 0.f, te = 0.f;
@@ -1855,10 +1619,9 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       ck_launch("popcount range");
       P = plan_rows(h, n_unq);
       note_plan(h, P);
-      if (!P.join || h->join_mode == 2) DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
+      if (!P.join) DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
       wait_amplitudes();
       if (P.join) {
-        P.want_pos_of = h->join_mode == 2;
         DISPATCH_W(W, R = sort_for_locality<WW>(h, rkeys, dla, dph, n_unq, row_begin, row_end, P));
         if (h->view.n_res) DISPATCH_W(W, launch_table_build<WW>(h, rkeys, n_unq));  // residual probes: sorted ids
         DISPATCH_W(W, build_join_index<WW>(h, rkeys, n_unq, P));
@@ -1877,14 +1640,8 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       O.la = dla;
       O.ph = dph;
       O.cs = rcs;
-      if (P.join && h->join_mode == 2) {
-        DISPATCH_W(W, (run_join_bucket<WW>(h, rkeys, n_unq, R, P, row_begin, row_end, deloc)));
-      } else if (P.join && h->join_mode == 1 && h->pipelined) {
+      if (P.join) {
         DISPATCH_W(W, (run_join_pipelined<WW>(h, rkeys, n_unq, R, P, deloc)));
-      } else if (P.join && h->join_mode == 1) {
-        DISPATCH_W(W, (run_join_split<WW>(h, rkeys, n_unq, R, P, deloc)));
-      } else if (P.join) {
-        DISPATCH_W(W, (launch_rows_join<WW, kModeEloc>(h, rkeys, R, P, O)));
       } else {
         DISPATCH_W(W, (launch_rows<WW, kModeEloc>(h, dkeys, row_begin, row_end, O)));
       }

@@ -34,9 +34,6 @@ namespace qvmc_b200 {
 #define QVMC_JOIN_UNROLL 4  // bucket members in flight per lane
 #endif
 
-#ifndef QVMC_JOIN_DRAIN_ATTR
-#define QVMC_JOIN_DRAIN_ATTR __forceinline__
-#endif
 
 constexpr int kJoinMaxMinority = 16;  // s <= 16: at most 120 buckets per row
 constexpr int kJoinMaxRanges = kJoinMaxMinority * (kJoinMaxMinority - 1) / 2;
@@ -288,20 +285,18 @@ __device__ __forceinline__ int select_bit(const uint64_t* v, int k) {
   return -1;
 }
 
-// Member array + per-(sample, pair) bucket range (+ pos_of, optional: the
-// member position of every (sample, pair) entry). The sort carried only the
+// Member array + per-(sample, pair) bucket range. The sort carried only the
 // entry id y*C + t; the pair's orbitals come from y's key.
 template <int W>
 __global__ void k_join_fill(const uint32_t* __restrict__ val, const uint32_t* __restrict__ rid, uint64_t E, uint32_t C,
                             const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi,
                             const uint64_t* __restrict__ keys, int n_qubits, int side, uint64_t* __restrict__ mem,
-                            uint2* __restrict__ rng, uint32_t* __restrict__ pos_of) {
+                            uint2* __restrict__ rng) {
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < E; p += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t e = val[p];
     const uint32_t r = rid[p] - 1;
     const uint32_t y = e / C, t = e - y * C;
     rng[e] = make_uint2(lo[r], hi[r]);
-    if (pos_of) pos_of[e] = static_cast<uint32_t>(p);
     uint64_t S[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) {
@@ -512,10 +507,6 @@ __device__ __forceinline__ Key<W> row_key(const JoinSmem* sm) {
   return k;
 }
 
-#ifndef QVMC_JOIN_DRAIN_HITS
-#define QVMC_JOIN_DRAIN_HITS 1  // queued hits per lane whose records are loaded together (2+ spills)
-#endif
-
 // one queued hit: its sample record and drain record (loaded together)
 struct JoinHit {
   uint32_t key;
@@ -523,23 +514,6 @@ struct JoinHit {
   U64x4 sr;  // log psi, cos, sin of the partner
   uint64_t r[kGrecWords];
 };
-
-__device__ __forceinline__ void load_hit(const JoinView& J, const JoinSmem* sm, unsigned k, unsigned n, JoinHit& h) {
-  h.valid = k < n;
-  h.key = kNoKey;
-  h.sr = U64x4{0, 0, 0, 0};
-#pragma unroll
-  for (int i = 0; i < kGrecWords; ++i) h.r[i] = 0;
-  if (h.valid) {
-    const uint32_t y = sm->qy[k], g = sm->qg[k];
-    h.key = sm->qk[k];
-    h.sr = ldg256(J.rec + static_cast<int64_t>(y) * 4);
-    const U64x4 g0 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords);
-    const U64x4 g1 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords + 4);
-    h.r[0] = g0.a; h.r[1] = g0.b; h.r[2] = g0.c; h.r[3] = g0.d;
-    h.r[4] = g1.a; h.r[5] = g1.b; h.r[6] = g1.c; h.r[7] = g1.d;
-  }
-}
 
 // H_{x x'} of one loaded hit from its drain record (warp-collective: large
 // generic groups are split over the lanes). Invalid hits give 0.
@@ -623,33 +597,6 @@ __device__ __forceinline__ void eval_hit(const HamView& H, const JoinView& J, co
   }
 }
 
-// Drain the warp's hit queue: this lane's share of sum H_{xx'} psi(x')/psi(x).
-// QVMC_JOIN_DRAIN_HITS hits per lane per round have all their records in
-// flight before any is evaluated (the drain is load-latency bound).
-template <int W>
-__device__ QVMC_JOIN_DRAIN_ATTR double2 join_drain(const HamView& H, const JoinView& J, JoinSmem* sm, int lane, int s,
-                                                   int side) {
-  constexpr int DH = QVMC_JOIN_DRAIN_HITS;
-  double2 acc = make_double2(0.0, 0.0);
-  __syncwarp();
-  const Key<W> xrow = row_key<W>(sm);
-  const double la_i = *reinterpret_cast<const volatile double*>(&sm->la);
-  const double2 cs_i = make_double2(*reinterpret_cast<const volatile double*>(&sm->cs_c),
-                                    *reinterpret_cast<const volatile double*>(&sm->cs_s));
-  const unsigned n = sm->qn;
-  for (unsigned k0 = 0; k0 < n; k0 += 32 * DH) {
-    JoinHit h[DH];
-#pragma unroll
-    for (int d = 0; d < DH; ++d) load_hit(J, sm, k0 + 32 * d + lane, n, h[d]);
-#pragma unroll
-    for (int d = 0; d < DH; ++d) eval_hit<W>(H, J, sm->pos, h[d], xrow, la_i, cs_i, lane, s, side, acc);
-  }
-  __syncwarp();
-  if (lane == 0) sm->qn = 0;
-  __syncwarp();
-  return acc;
-}
-
 #ifndef QVMC_SEARCH_MINB
 #define QVMC_SEARCH_MINB 4  // split search kernel (no drain): 64 registers, 32 warps per SM (measured best, r01x)
 #endif
@@ -659,7 +606,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
     k_rows_join(const __grid_constant__ HamView H, const TableView T, const __grid_constant__ JoinView J,
                 const uint64_t* __restrict__ keys, const RowSet R, int side, int s, const __grid_constant__ Ctl C,
                 const __grid_constant__ RowOut O) {
-  constexpr bool kEval = MODE == kModeEloc || MODE == kModeHits;  // E_loc rows (fused or split)
+  static_assert(MODE == kModeHits || MODE == kModeCount || MODE == kModeEmit, "join modes: hits, count, emit");
+  constexpr bool kEval = MODE == kModeHits;  // E_loc rows (split evaluation)
   __shared__ JoinSmem s_w[kWarps];
   const int lane = threadIdx.x & 31;
   JoinSmem* sm = &s_w[threadIdx.x >> 5];
@@ -711,12 +659,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
       if (isinf(*reinterpret_cast<const volatile double*>(&sm->la))) {  // energy.cpp:32-33
         if (lane == 0) {
           atomicOr(C.err, kErrZeroAmp);
-          if (MODE == kModeEloc) {
-            O.eloc[orow - R.out_base] = make_double2(CUDART_NAN, CUDART_NAN);
-          } else {
-            O.base[orow - R.out_base] = make_double2(CUDART_NAN, CUDART_NAN);
-            O.row_last[orow - R.out_base] = ~0u;
-          }
+          O.base[orow - R.out_base] = make_double2(CUDART_NAN, CUDART_NAN);
+          O.row_last[orow - R.out_base] = ~0u;
         }
         continue;
       }
@@ -777,19 +721,14 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
       c_tb = sm->tb[rg];
       c_db = sm->dbase[rg];
     }
-    // the queue becomes E_loc (fused drain) or one chunk of this row (split
-    // evaluation) once it holds `thresh` hits
+    // the queue becomes one chunk of this row (split evaluation) once it holds `thresh` hits
     auto emit = [&](unsigned thresh) {
       if (kEval) {
         __syncwarp();
-        const unsigned qd = sm->qn, qsn = MODE == kModeHits ? sm->qs : 0u;
+        const unsigned qd = sm->qn, qsn = sm->qs;
         const unsigned qn = qd + qsn;
         if (qn >= thresh) {
-          if (MODE == kModeEloc) {
-            const double2 d = join_drain<W>(H, J, sm, lane, s, side);
-            acc.x += d.x;
-            acc.y += d.y;
-          } else {  // split evaluation: the queue becomes one chunk of this row
+          {
             unsigned long long off = 0, cid = 0;
             if (lane == 0) {
               off = atomicAdd(O.hit_cursor, static_cast<unsigned long long>(qn));
@@ -946,21 +885,15 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
               sm->qn = bd + __popc(hd);
               sm->qs = bs + __popc(hs);
             }
-          } else if (kEval || MODE == kModeEmit) {
+          } else if (MODE == kModeEmit) {
             unsigned base = 0;
-            if (lane == 0) base = atomicAdd(kEval ? &sm->qn : &sm->cursor, __popc(hm));
+            if (lane == 0) base = atomicAdd(&sm->cursor, __popc(hm));
             base = __shfl_sync(0xffffffffu, base, 0);
             if (hit) {
               const unsigned k = base + __popc(hm & ((1u << lane) - 1u));
-              if (kEval) {
-                sm->qy[k] = y;
-                sm->qg[k] = static_cast<uint32_t>(g);
-                sm->qk[k] = kk;
-              } else {
-                const uint64_t at = O.row_off[orow] + k;
-                O.xp_out[at] = R.perm ? __ldg(R.perm + y) : y;
-                O.g_out[at] = static_cast<uint32_t>(g);
-              }
+              const uint64_t at = O.row_off[orow] + k;
+              O.xp_out[at] = R.perm ? __ldg(R.perm + y) : y;
+              O.g_out[at] = static_cast<uint32_t>(g);
             }
           }
           hits += hit ? 1u : 0u;
@@ -1060,12 +993,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
       const double re = warp_sum(acc.x);
       const double im = warp_sum(acc.y);
       if (lane == 0) {
-        if (MODE == kModeEloc) {
-          O.eloc[orow - R.out_base] = make_double2(re, im);
-        } else {
-          O.base[orow - R.out_base] = make_double2(re, im);
-          O.row_last[orow - R.out_base] = prev_chunk;
-        }
+        O.base[orow - R.out_base] = make_double2(re, im);
+        O.row_last[orow - R.out_base] = prev_chunk;
       }
     }
     const uint32_t row_hits = warp_sum(hits) + (H.diag >= 0 ? 1u : 0u);

@@ -61,8 +61,9 @@ def benched(request, cuda_ok):
     pairs = q.loop_over_terms(keys, H).entries
     counts = np.bincount(pairs[:, 0].astype(np.int64), minlength=N_UNQ)
     rng = np.random.default_rng(n_qubits)
-    rows = np.unique(np.concatenate([np.arange(16), rng.choice(N_UNQ, 256, replace=False),
-                                     np.argsort(counts, kind="stable")[-16:]])).astype(np.int64)
+    fixed = np.unique(np.concatenate([np.arange(16), np.argsort(counts, kind="stable")[-16:]]))
+    pool = np.setdiff1d(np.arange(N_UNQ), fixed)
+    rows = np.sort(np.concatenate([fixed, rng.choice(pool, 256, replace=False)])).astype(np.int64)
     o_pairs, o_counts, o_eloc, o_scale = O.rows_list(keys, rows, b.log_amps, b.phases)
     return dict(name=request.param, H=H, O=O, keys=keys, b=b, fused=fused, fused_stats=fused_stats,
                 pairs=pairs, counts=counts, rows=rows, o_pairs=o_pairs, o_counts=o_counts, o_eloc=o_eloc,

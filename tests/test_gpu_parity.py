@@ -263,30 +263,32 @@ def test_ops_counters(cuda_ok):
     assert len(t.entries) == 2 and t.ops <= (4 * 40 + 4) * 2
 
 
-@pytest.mark.parametrize("mode,hit_cap", [("0", None), ("1", None), ("2", None), ("1", "4096"), ("2", "4096")])
-def test_join_evaluation_modes_agree(cuda_ok, monkeypatch, mode, hit_cap):
-    """The three join evaluations (fused row kernel, row search + chunk eval,
-    bucket search + row eval) give the same E_loc and pair count on a 118-qubit
-    synthetic; a tiny first hit-buffer capacity exercises the overflow regrow."""
+@pytest.mark.parametrize("hit_cap", ["4096", "100000"])
+def test_join_hit_buffer_regrow(cuda_ok, monkeypatch, hit_cap):
+    """A tiny first hit-buffer capacity exercises the overflow detection and
+    the rerun with grown buffers: same E_loc, pair count and moments as a
+    handle with the default capacity, and as the pairs-based evaluation."""
     n_unq = 20_000
     keys = synthetic.near_hf_keys(118, 110, n_unq, seed=7)
     b = synthetic.sample_batch(keys, seed=3)
     c, x, y, z = synthetic.jw_terms(118, 3_000_000, seed=1)
-    monkeypatch.setenv("QVMC_JOIN_MODE", "0")
     monkeypatch.delenv("QVMC_HIT_CAP", raising=False)
-    ref = q.surrogate_energy(q.HamiltonianIndex.from_masks(118, c, x, y, z), b)
-    monkeypatch.setenv("QVMC_JOIN_MODE", mode)
-    if hit_cap:
-        monkeypatch.setenv("QVMC_HIT_CAP", hit_cap)
+    H0 = q.HamiltonianIndex.from_masks(118, c, x, y, z)
+    ref = q.surrogate_energy(H0, b)
+    n_pairs = q.last_stats(H0)["pairs"]
+    monkeypatch.setenv("QVMC_HIT_CAP", hit_cap)
     H = q.HamiltonianIndex.from_masks(118, c, x, y, z)
     got = q.surrogate_energy(H, b)
     st = q.last_stats(H)
-    assert st["join_mode"] == 1
-    scale = np.maximum(np.abs(ref.locals), 1.0)
-    assert np.all(np.abs(got.locals - ref.locals) <= 1e-11 * scale)
-    assert abs(got.e_var - ref.e_var) <= 1e-12 * max(1.0, abs(ref.e_var))
+    assert st["join_mode"] == 1 and st["pairs"] == n_pairs
+    assert np.array_equal(got.locals, ref.locals)  # deterministic: same chunks, same order
+    assert got.e_var == ref.e_var
     half = q.surrogate_energy(H, b, 5_000, 15_000, check=False)  # a row shard: same rows, same values
     assert np.array_equal(half.locals, got.locals[5_000:15_000])
+    p = q.loop_over_terms(keys, H)
+    loc = q.local_energies(p, b, H)
+    scale = eloc_scale(p.entries, H.group_offsets, H.coeff, b.log_amps, n_unq)
+    assert_eloc_close(got.locals, loc, scale)
 
 
 @pytest.mark.parametrize("n_qubits,n_e,n_terms,n_unq,join", [
