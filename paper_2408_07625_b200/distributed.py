@@ -77,11 +77,14 @@ def device_evaluate(index: HamiltonianIndex, device: int) -> Callable:
         # NULL selects the handle's own non-blocking stream
         raw = torch.cuda.current_stream(device).cuda_stream or 0x1
         _lib.check(L.qvmc_cuda_set_stream(h, C.c_void_p(raw)))
-        _lib.check(L.qvmc_cuda_eloc_fused(
-            h, keys.shape[0], C.c_void_p(keys.data_ptr()), C.c_void_p(la.data_ptr()), C.c_void_p(ph.data_ptr()),
-            C.c_void_p(lp.data_ptr()), float(log_norm), r0, r1,
-            C.c_void_p(out_locals.data_ptr()) if out_locals is not None else None,
-            C.c_void_p(out_moments.data_ptr()), _lib.MEM_DEVICE))
+        try:
+            _lib.check(L.qvmc_cuda_eloc_fused(
+                h, keys.shape[0], C.c_void_p(keys.data_ptr()), C.c_void_p(la.data_ptr()), C.c_void_p(ph.data_ptr()),
+                C.c_void_p(lp.data_ptr()), float(log_norm), r0, r1,
+                C.c_void_p(out_locals.data_ptr()) if out_locals is not None else None,
+                C.c_void_p(out_moments.data_ptr()), _lib.MEM_DEVICE))
+        finally:  # later calls on the shared handle use its own stream again
+            _lib.check(L.qvmc_cuda_set_stream(h, None))
 
     return run
 
@@ -127,7 +130,10 @@ def model_evaluate(model, device: int) -> Callable:
     def run(keys, out_la, out_ph):
         raw = torch.cuda.current_stream(device).cuda_stream or 0x1  # 0x1 = cudaStreamLegacy
         _lib.check(_lib.lib().qvmc_cuda_model_set_stream(model._h, C.c_void_p(raw)))
-        model.log_psi_device(keys.data_ptr(), keys.shape[0], out_la.data_ptr(), out_ph.data_ptr())
+        try:
+            model.log_psi_device(keys.data_ptr(), keys.shape[0], out_la.data_ptr(), out_ph.data_ptr())
+        finally:
+            _lib.check(_lib.lib().qvmc_cuda_model_set_stream(model._h, None))
 
     return run
 

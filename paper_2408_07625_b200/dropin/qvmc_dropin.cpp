@@ -75,16 +75,27 @@ std::vector<std::uint64_t> pack(std::span<const BasisVector> batch, int n_words)
 }
 
 // Device copies of HamiltonianIndex objects, keyed by identity and checked
-// by a content fingerprint (the index is immutable, hamiltonian.hpp:41-45).
+// by a fingerprint of the full content the device uses (the index is
+// immutable, hamiltonian.hpp:41-45, but a new index can reuse the address of
+// a destroyed one). At most kCacheCap copies stay resident (least recently
+// used evicted first); qvmc_dropin_release_all() frees them explicitly.
 struct Cached {
   std::uint64_t fingerprint = 0;
   qvmc_ham_t handle = nullptr;
+  std::uint64_t last_use = 0;
 };
 
 std::mutex g_mu;
+std::uint64_t g_clock = 0;
 std::unordered_map<const HamiltonianIndex*, Cached>& cache() {
   static auto* m = new std::unordered_map<const HamiltonianIndex*, Cached>();
   return *m;
+}
+
+std::size_t cache_cap() {
+  const char* s = std::getenv("QVMC_DROPIN_CACHE");
+  const long v = s ? std::atol(s) : 4;
+  return static_cast<std::size_t>(v < 1 ? 1 : v);
 }
 
 std::uint64_t fingerprint(const HamiltonianIndex& h) {
@@ -92,13 +103,26 @@ std::uint64_t fingerprint(const HamiltonianIndex& h) {
   auto mix = [&f](std::uint64_t v) {
     f ^= v;
     f *= 0x100000001b3ull;
+    f ^= f >> 29;
   };
+  const int W = (h.n_qubits() + 63) / 64;
+  std::uint64_t w[BasisVector::kMaxWords];
   mix(h.n_terms());
   mix(h.xy_set().size());
-  for (const auto& t : h.terms()) {
+  const auto d = h.diagonal_xy_index();
+  mix(d ? static_cast<std::uint64_t>(*d) : ~0ull);
+  for (std::size_t g = 0; g < h.xy_set().size(); ++g) {  // flip masks and the grouping
+    std::memcpy(w, &h.xy_set()[g], sizeof(w));
+    for (int i = 0; i < W; ++i) mix(w[i]);
+    mix(static_cast<std::uint64_t>(h.group(g).size()));
+  }
+  for (const auto& t : h.terms()) {  // every term the device evaluates: coeff, yz mask, y weight
     std::uint64_t c;
     std::memcpy(&c, &t.coeff, 8);
     mix(c);
+    std::memcpy(w, &t.yz_mask, sizeof(w));
+    for (int i = 0; i < W; ++i) mix(w[i]);
+    mix(static_cast<std::uint64_t>(t.y_weight));
   }
   return f;
 }
@@ -108,10 +132,27 @@ int n_words_of(const HamiltonianIndex& h) { return (h.n_qubits() + 63) / 64; }
 qvmc_ham_t device_index(const HamiltonianIndex& h) {
   const std::uint64_t fp = fingerprint(h);
   std::lock_guard<std::mutex> lock(g_mu);
-  auto& c = cache()[&h];
-  if (c.handle && c.fingerprint == fp) return c.handle;
-  if (c.handle) qvmc_cuda_ham_destroy(c.handle);
-  c.handle = nullptr;
+  auto& m = cache();
+  {
+    auto it = m.find(&h);
+    if (it != m.end() && it->second.handle && it->second.fingerprint == fp) {
+      it->second.last_use = ++g_clock;
+      return it->second.handle;
+    }
+  }
+  // evict: a stale copy at this address, then least recently used copies beyond the cap
+  if (auto it = m.find(&h); it != m.end()) {
+    if (it->second.handle) qvmc_cuda_ham_destroy(it->second.handle);
+    m.erase(it);
+  }
+  while (m.size() >= cache_cap()) {
+    auto lru = m.begin();
+    for (auto it = m.begin(); it != m.end(); ++it)
+      if (it->second.last_use < lru->second.last_use) lru = it;
+    if (lru->second.handle) qvmc_cuda_ham_destroy(lru->second.handle);
+    m.erase(lru);
+  }
+  auto& c = m[&h];
   const int W = n_words_of(h);
   const auto& xy = h.xy_set();
   const auto& terms = h.terms();
@@ -136,6 +177,7 @@ qvmc_ham_t device_index(const HamiltonianIndex& h) {
         "HamiltonianIndex upload");
   c.handle = handle;
   c.fingerprint = fp;
+  c.last_use = ++g_clock;
   return handle;
 }
 
@@ -291,3 +333,13 @@ Eigen::VectorXd energy_gradient(const Eigen::VectorXd& weights, const Eigen::Vec
 }
 
 }  // namespace qvmc
+
+// Frees every cached device copy of a HamiltonianIndex (e.g. before the
+// caller destroys its indices, or to return device memory). Safe to call at
+// any time; later calls re-upload on demand.
+extern "C" void qvmc_dropin_release_all(void) {
+  std::lock_guard<std::mutex> lock(qvmc::g_mu);
+  for (auto& [k, c] : qvmc::cache())
+    if (c.handle) qvmc_cuda_ham_destroy(c.handle);
+  qvmc::cache().clear();
+}

@@ -213,8 +213,40 @@ static void random_family(std::uint32_t stream, int n_seeds, int max_n, int max_
   CHECK(ok == n_seeds);
 }
 
+extern "C" void qvmc_dropin_release_all(void);
+
+// Indices recreated at the same stack address with the same coefficients but
+// different strings must not reuse a stale device copy (the cache checks the
+// full content, not the address).
+static void reused_address_cases() {
+  const SampleBatch b = toy_batch();
+  const char* texts[3] = {"qubits: 4\n0.9 IIII\n-0.2 XIXI\n0.3 IYYI\n",
+                          "qubits: 4\n0.9 IIII\n-0.2 IXIX\n0.3 IYYI\n",
+                          "qubits: 4\n0.9 IIII\n-0.2 XIXI\n0.3 IXXI\n"};
+  for (int round = 0; round < 2; ++round) {
+    for (const char* t : texts) {
+      const HamiltonianIndex h = parse(t);
+      const CoupledPairs p = loop_over_batch(b.vectors, h);
+      const CoupledPairs want = brute(b.vectors, h);
+      CHECK(p.entries.size() == want.entries.size());
+      const Eigen::VectorXcd loc = local_energies(p, b, h);
+      for (int i = 0; i < 3; ++i) {
+        std::complex<double> e{0.0, 0.0};
+        for (const auto& en : want.entries)
+          if (en.x == static_cast<std::uint32_t>(i))
+            e += h.matrix_element(b.vectors[i], b.vectors[en.x_prime]) *
+                 std::exp(std::complex<double>(b.log_amps[en.x_prime] - b.log_amps[i],
+                                               b.phases[en.x_prime] - b.phases[i]));
+        CHECK(std::abs(loc[i] - e) <= 1e-12);
+      }
+    }
+    qvmc_dropin_release_all();
+  }
+}
+
 int main() {
   toy_cases();
+  reused_address_cases();
   degenerate_and_errors();
   random_family(1234, 40, 70, 80, 256, 1);       // test_coupling.cpp:138-168
   random_family(0xAC3, 200, 40, 120, 512, 1000); // acceptance_main.cpp criterion 3

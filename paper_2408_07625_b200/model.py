@@ -11,6 +11,8 @@ path. Errors follow the reference: ``std::invalid_argument`` -> ValueError.
 """
 from __future__ import annotations
 
+import re
+
 import ctypes as C
 from dataclasses import dataclass, field
 from typing import List
@@ -140,6 +142,18 @@ def _hexfloat(v: float) -> str:
     return f"{sign}0x{mant}p{exp if exp.startswith('-') else exp}"
 
 
+_HEX = re.compile(r"[+-]?0[xX]")
+
+
+def _parse_double(tok: str) -> float:
+    """strtod semantics (model.cpp:385-393 reads parameters with >>): hexfloat
+    only with a 0x prefix, decimal otherwise; malformed -> RuntimeError."""
+    try:
+        return float.fromhex(tok) if _HEX.match(tok) else float(tok)
+    except ValueError:
+        raise RuntimeError(f"checkpoint: malformed parameter '{tok}'") from None
+
+
 def load_checkpoint(text: str, device: int = 0):
     """load_checkpoint (model.cpp:359-396): (AnqsModel, seed); RuntimeError on malformed input."""
     toks = text.split()
@@ -164,7 +178,7 @@ def load_checkpoint(text: str, device: int = 0):
     vals = []
     for _ in range(n_params):
         try:
-            vals.append(float.fromhex(next(it)))
+            vals.append(_parse_double(next(it)))
         except StopIteration:
             raise RuntimeError("checkpoint: truncated parameters") from None
     model.set_params(np.array(vals))

@@ -240,3 +240,15 @@ def test_gpu_sharded_fill_amplitudes_world1(cuda_ok):
         assert abs(log_norm - want) <= 1e-12 * max(1.0, abs(want))
     finally:
         dist.destroy_process_group()
+
+
+def test_checkpoint_parameter_parsing_follows_strtod():
+    """Parameters parse like the reference's stream extraction: hexfloat only with a
+    0x prefix, decimal otherwise ('0.5' is 0.5, not hex 0.3125); malformed -> RuntimeError."""
+    from paper_2408_07625_b200.model import _parse_double
+    assert _parse_double("0.5") == 0.5
+    assert _parse_double("1e-3") == 1e-3
+    assert _parse_double("-0x1.8p+1") == -3.0
+    assert _parse_double("0X1p-2") == 0.25
+    with pytest.raises(RuntimeError):
+        _parse_double("abc")
