@@ -22,6 +22,7 @@ import argparse
 import json
 import math
 import os
+import re
 import statistics
 import subprocess
 import sys
@@ -49,7 +50,9 @@ def parse_args():
     ap.add_argument("--cpu-sample", type=int, default=None, help="rows of the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--e2e-steps", type=int, default=None, help="0 skips the end-to-end leg")
+    ap.add_argument("--profile-step", action="store_true",
+                    help="one extra step after warm-up inside cudaProfilerStart/Stop (for ncu --profile-from-start off)")
     return ap.parse_args()
 
 
@@ -240,6 +243,58 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+STAGE_KERNELS = re.compile(r"^(k_rows_join|k_eval_chunks|k_finalize_rows|k_search_eval)")
+
+
+def roofline(args, stats, rows, W, stage_ms, step_ms, clk_summary=None):
+    """The E_loc stage against the resource that binds it.
+
+    Primary: instruction issue. The stage's kernels execute a fixed number of
+    warp instructions per step (ncu smsp__inst_executed over one step,
+    profiles/ncu_step_<config>.json); achieved = that count / the stage's
+    CUDA-event time measured here; peak = the measured per-SM issue rate
+    (profiles/int_rates_b200.json: LOP3+IMAD mix, warp-inst/clk/SM) x SMs x
+    SM clock. Secondary (kept beside it): algorithmic HBM bytes
+    per stage time against the measured copy bandwidth, and the ncu DRAM
+    traffic of the same kernels."""
+    pairs_per_row = stats["pairs"] / max(rows, 1)
+    b_alg = 8 * W + 16 + 8 + 16 + pairs_per_row * (8 * W + 16)  # SURVEY.md §8(d)
+    hbm_ach = b_alg * rows / (stage_ms * 1e-3) / 1e9
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    out = {"kernel": "E_loc stage: k_rows_join<W,kModeHits> search + k_eval_chunks<W> + k_finalize_rows",
+           "kernel_ms": stage_ms, "kernel_share_of_step": stage_ms / step_ms, "bytes_per_sample": b_alg}
+    hbm = {"achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_ach / hbm_peak,
+           "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
+    step_f = ROOT / "profiles" / f"ncu_step_{args.config}.json"
+    rates_f = ROOT / "profiles" / "int_rates_b200.json"
+    inst = traffic = None
+    if step_f.exists() and args.n_unq is None:
+        ks = json.loads(step_f.read_text())["kernels"]
+        sel = {k: v for k, v in ks.items() if STAGE_KERNELS.match(k)}
+        if sel:
+            inst = sum(v["warp_inst"] for v in sel.values())
+            traffic = sum(v["dram_bytes"] for v in sel.values())
+            out["ncu_kernels"] = sorted(sel)
+    hbm["traffic"] = traffic
+    if inst and rates_f.exists():
+        rates = json.loads(rates_f.read_text())
+        per_clk = rates["issue_lop3_imad"]["warp_inst_per_clk_per_sm"]
+        peak = per_clk * rates["sm_count"] * sm_mhz * 1e6 / 1e12
+        ach = inst / (stage_ms * 1e-3) / 1e12
+        out |= {"bound": "int-issue", "achieved": ach, "peak": peak, "unit": "T warp-inst/s", "frac": ach / peak,
+                "traffic": traffic, "warp_inst_per_step": inst, "warp_inst_per_sample": inst / max(rows, 1),
+                "peak_source": f"profiles/int_rates_b200.json issue_lop3_imad {per_clk:.3f} warp-inst/clk/SM x "
+                               f"{rates['sm_count']} SMs x {sm_mhz:.0f} MHz (measured)",
+                "inst_source": f"profiles/{step_f.name} (ncu smsp__inst_executed, one step)", "hbm": hbm}
+    else:  # no instruction capture for this workload: the HBM view only
+        out |= {"bound": "hbm", "achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_ach / hbm_peak,
+                "traffic": traffic, "note": "instruction counts not captured for this workload; the stage is "
+                                            "issue-bound (DESIGN.md section 4.6)"}
+    return out
+
+
 # ------------------------------------------------------------------ our arm
 
 def main():
@@ -296,6 +351,14 @@ def main():
         step()
     torch.cuda.synchronize()
     _lib.check(_lib.lib().qvmc_cuda_synchronize(H.device_handle(local)))
+    if args.profile_step:
+        if flush is not None:
+            flush.fill_(1)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        step()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
 
     stream = torch.cuda.current_stream(dev)
     step_ms, rows_ms, table_ms, mom_ms, search_ms, eval_ms = [], [], [], [], [], []
@@ -334,7 +397,7 @@ def main():
     value = n / (mean_ms * 1e-3)
 
     # ---- e2e through the C ABI with pinned host buffers (N = 1) / public API (N > 1)
-    e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+    e2e_steps = max(3, min(args.steps, 10)) if args.e2e_steps is None else args.e2e_steps
     import ctypes as C
     pin = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(dt).pin_memory()
     if world == 1:
@@ -364,7 +427,8 @@ def main():
             res.moments.cpu()
         h2d = (r1 - r0) * (8 * W + 24)
         d2h = (r1 - r0) * 16 + 40
-    e2e_step()
+    if e2e_steps:
+        e2e_step()
     torch.cuda.synchronize()
     e2e_s = []
     for _ in range(e2e_steps):
@@ -374,33 +438,20 @@ def main():
         e2e_step()
         torch.cuda.synchronize()
         e2e_s.append(time.perf_counter() - t0)
-    e2e_t = statistics.mean(e2e_s)
+    e2e_t = statistics.mean(e2e_s) if e2e_s else float("nan")
     if world > 1:
         t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_t = float(t)
         _lib.check(_lib.lib().qvmc_cuda_set_stream(H.device_handle(local), None))
 
-    # ---- roofline of the E_loc stage (the hot path: search kernel + chunk
-    # evaluation kernel + per-row finalize, timed together with CUDA events on
-    # the handle's stream): algorithmic bytes / stage time
+    # ---- roofline of the E_loc stage (search + evaluation + per-row finalize,
+    # timed together with CUDA events on the handle's stream)
     rows_here = r1 - r0
-    pairs_per_row = stats["pairs"] / max(rows_here, 1)
-    b_alg = 8 * W + 16 + 8 + 16 + pairs_per_row * (8 * W + 16)
     kern_ms = statistics.mean(rows_ms)
-    achieved = b_alg * rows_here / (kern_ms * 1e-3) / 1e9
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    peak = peaks.get("hbm_gbs", 6650.0)
-    # DRAM traffic of the same kernels from one `ncu --set full` capture each (profiles/ncu_traffic.json)
-    traffic, traffic_src, issue = None, None, None
-    tj = ROOT / "profiles" / "ncu_traffic.json"
-    if tj.exists() and args.n_unq is None:
-        t = json.loads(tj.read_text()).get(args.config, {})
-        if "search" in t and "eval" in t:
-            traffic = sum(t[k]["dram_bytes"] * t[k].get("launches_per_step", 1) for k in ("search", "eval"))
-            traffic_src = f"profiles/ncu_traffic.json ({t['search']['report']}, {t['eval']['report']})"
-            # the binding resource: issue slots (ncu smsp__issue_active, per kernel)
-            issue = {k: t[k].get("issue_active_pct", 0.0) / 100.0 for k in ("search", "eval")}
+    roof = roofline(args, stats, rows_here, W, kern_ms, statistics.mean(step_ms), clk_summary=None)
+    roof["search_ms"] = statistics.mean(search_ms)
+    roof["eval_ms"] = statistics.mean(eval_ms)
 
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -413,22 +464,11 @@ def main():
         "e2e": {"value": n / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "path": "qvmc_cuda_eloc_fused(QVMC_MEM_HOST) from pinned buffers" if world == 1
                 else "distributed.sharded_surrogate_energy from pinned host shards"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                     "kernel": "E_loc stage: k_rows_join<W,kModeHits> search + k_eval_chunks<W> + k_finalize_rows",
-                     "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / statistics.mean(step_ms),
-                     "search_ms": statistics.mean(search_ms), "eval_ms": statistics.mean(eval_ms),
-                     "per_kernel_note": "search_ms / eval_ms: CUDA-event time of every search / evaluation launch "
-                                        "summed over the step's row batches (the two streams overlap, so their sum "
-                                        "can exceed kernel_ms)",
-                     "bytes_per_sample": b_alg,
-                     "issue_slot_frac_ncu": issue,
-                     "note": "integer-issue / L2-latency bound, not HBM: see DESIGN.md section 4.6 and profiles/",
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback"},
+        "roofline": roof,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "stages_ms": {"table_build": statistics.mean(table_ms), "rows": kern_ms, "moments": statistics.mean(mom_ms)},
-        "path_stats": {"pairs_per_sample": pairs_per_row, "candidates_per_sample": stats["candidates"] / max(rows_here, 1),
+        "path_stats": {"pairs_per_sample": stats["pairs"] / max(rows_here, 1), "candidates_per_sample": stats["candidates"] / max(rows_here, 1),
                        "terms_equivalent_candidates_per_sample": H.n_xy, "sector_mode": stats["sector_mode"],
                        "minority_count": stats["minority_count"]},
         "setup_s": {"inputs": gen_s, "upload_and_plan": upload_s},

@@ -22,7 +22,7 @@ rows against the WHOLE 1e6 sample set:
     oracle's rows.
 
 Rows checked: 256 uniformly drawn + the 16 rows with the most pairs + the
-first 16, at least 288 per configuration.
+first 16 (these two sets may overlap), at least 272 per configuration.
 """
 import numpy as np
 import pytest
@@ -72,7 +72,7 @@ def benched(request, cuda_ok):
 
 def test_pair_lists_bit_exact_on_sampled_rows(benched):
     d = benched
-    assert len(d["rows"]) >= 288
+    assert len(d["rows"]) >= 256 + 16
     got, got_counts = _rows_of(d["pairs"], d["rows"])
     assert np.array_equal(got_counts, d["o_counts"])
     assert np.array_equal(got, d["o_pairs"])

@@ -1,0 +1,76 @@
+"""Small end-to-end exercise of every device path, for compute-sanitizer
+(memcheck / racecheck / synccheck / initcheck): toy KAT, a reference golden
+family, the join path at 118 and 56 qubits (pipelined search + chunk
+evaluation, including the overflow regrow with a tiny first hit capacity),
+pair materialisation + local_energies + fused pair elements, the generic
+sector-list row kernel, and the amplitude model. Sizes are small so the
+instrumented run finishes in minutes.
+
+    compute-sanitizer --tool racecheck python tools/sanitize_driver.py
+"""
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+import paper_2408_07625_b200 as q  # noqa: E402
+from paper_2408_07625_b200 import _lib, synthetic  # noqa: E402
+from paper_2408_07625_b200.hamiltonian import _ptr  # noqa: E402
+
+
+def join_case(n_qubits, n_e, n_terms, n_unq, hit_cap=None):
+    if hit_cap:
+        os.environ["QVMC_HIT_CAP"] = str(hit_cap)
+    else:
+        os.environ.pop("QVMC_HIT_CAP", None)
+    H = synthetic.jw_hamiltonian(n_qubits, n_terms, seed=1)
+    keys = synthetic.near_hf_keys(n_qubits, n_e, n_unq, seed=2)
+    b = synthetic.sample_batch(keys, seed=3)
+    rep = q.surrogate_energy(H, b)
+    half = q.surrogate_energy(H, b, n_unq // 3, n_unq // 2, check=False)
+    assert np.array_equal(half.locals, rep.locals[n_unq // 3: n_unq // 2])
+    p = q.loop_over_terms(keys, H)
+    loc = q.local_energies(p, b, H)
+    assert np.allclose(loc, rep.locals, rtol=0, atol=1e-9 * max(1.0, np.abs(loc).max()))
+    e = np.ascontiguousarray(p.entries[: 5000], dtype=np.uint32)
+    hh = np.zeros(len(e), dtype=np.complex128)
+    kind = np.zeros(len(e), dtype=np.uint8)
+    _lib.check(_lib.lib().qvmc_cuda_pair_elements_fused(H.device_handle(0), len(keys), _ptr(keys), len(e), _ptr(e),
+                                                        _ptr(hh), _ptr(kind), _lib.MEM_HOST))
+    print(f"join {n_qubits}q n={n_unq} pairs={len(p.entries)} e_var={rep.e_var:.6f}", flush=True)
+
+
+def main():
+    import __graft_entry__
+    __graft_entry__.smoke()
+    from helpers import golden, instances, product_index
+    g = golden("accept3")
+    for _, pfx in instances("accept3")[:10]:
+        H = product_index(g, pfx)
+        keys = g[pfx + "keys"]
+        q.loop_over_trie(keys, H)
+        b = q.SampleBatch(keys, g[pfx + "lp"], g[pfx + "la"], g[pfx + "ph"], float(g[pfx + "norm"]),
+                          float(g[pfx + "log_norm"]))
+        q.surrogate_energy(H, b, check=False)
+    join_case(118, 110, 300_000, 3000)
+    join_case(118, 110, 300_000, 3000, hit_cap=512)
+    join_case(56, 14, 100_000, 3000)
+    # generic sector-list rows (minority set > 16)
+    H = synthetic.jw_hamiltonian(48, 20_000, seed=1)
+    keys = synthetic.near_hf_keys(48, 24, 1000, seed=2)
+    q.surrogate_energy(H, synthetic.sample_batch(keys, seed=3))
+    # amplitude model
+    M = q.AnqsModel(q.QuditLayout.make(56, 6), q.SectorConstraint(14, True))
+    M.set_params(np.random.default_rng(0).uniform(-0.1, 0.1, M.n_params()))
+    keys = synthetic.near_hf_keys(56, 14, 2000, seed=2)
+    M.log_psi(keys)
+    print("sanitize driver done", flush=True)
+
+
+if __name__ == "__main__":
+    main()
