@@ -164,6 +164,9 @@ struct qvmc_ham_s {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // fused-call stage timing
   bool timed = false;
   std::vector<cudaEvent_t> ev_b;  // pipelined split evaluation: per batch search start/end, eval start/end
+  cudaEvent_t ev_f[2] = {nullptr, nullptr};  // fused join kernel start/end
+  bool timed_f = false;
+  bool fused = true;  // QVMC_FUSED=0: the pipelined split search + chunk evaluation
   int64_t timed_b = 0;            // batches timed by ev_b in the last call
 };
 
@@ -700,6 +703,37 @@ void launch_rows_join(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, cons
   }
 }
 
+// Fused join rows (kModeFused): search warps hand hit chunks to evaluation
+// warps through shared memory inside one persistent kernel that writes E_loc
+// directly: no hit buffers, nothing to overflow, no host synchronisation.
+template <int W>
+void run_join_fused(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const RowPlan& P, double2* eloc) {
+  if (R.n_rows <= 0) return;
+  int* ctl = static_cast<int*>(h->ctl.p);
+  ck(cudaMemsetAsync(ctl + 4, 0, 2 * sizeof(int), h->stream), "memset row counter");
+  int per_sm = 0;
+  constexpr size_t dyn = sizeof(FusedSmem);
+  ck(cudaFuncSetAttribute(k_rows_join<W, kModeFused>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)),
+     "smem attribute");
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_join<W, kModeFused>, kFThreads, dyn), "occupancy");
+  const int64_t blocks_needed = (R.n_rows + kFSearch - 1) / kFSearch;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_needed, grid_for(h, per_sm))));
+  RowOut O{};
+  O.eloc = eloc;
+  O.exp_flag = ctl + 14;
+  TableView T{h->tab.as<uint64_t>(), h->tab_buckets - 1};
+  if (!h->ev_f[0]) {
+    ck(cudaEventCreate(&h->ev_f[0]), "event create");
+    ck(cudaEventCreate(&h->ev_f[1]), "event create");
+  }
+  ck(cudaEventRecord(h->ev_f[0], h->stream), "event");
+  k_rows_join<W, kModeFused><<<grid, kFThreads, dyn, h->stream>>>(h->view, T, join_view(h, P), keys, R, P.side,
+                                                                  P.s, ctl_view(h), O);
+  ck_launch("row kernel (join, fused search + evaluation)");
+  ck(cudaEventRecord(h->ev_f[1], h->stream), "event");
+  h->timed_f = true;
+}
+
 // Pipelined split evaluation: rows in NB batches, the search of batch b+1
 // (stream A) overlaps the evaluation of batch b (stream B), two buffer sets in
 // turn. The search is issue-bound and the evaluation latency-bound, so the
@@ -960,6 +994,7 @@ void compute_moments(qvmc_ham_s* h, const double* lp, double log_norm, const dou
 void record_stats(qvmc_ham_s* h, int64_t rows) {
   h->timed = false;
   h->timed_b = 0;
+  h->timed_f = false;
   h->last = qvmc_stats{};
   h->last.rows = static_cast<uint64_t>(rows);
   h->last.terms_equivalent = static_cast<uint64_t>(rows) * h->n_xy;
@@ -1148,6 +1183,7 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
       upload(h->gkey, gk);
     }
     if (const char* e = std::getenv("QVMC_JOIN")) h->use_join = std::atoi(e) != 0;
+    if (const char* e = std::getenv("QVMC_FUSED")) h->fused = std::atoi(e) != 0;
     if (const char* e = std::getenv("QVMC_PIPE_BATCHES")) h->pipe_batches = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("QVMC_PIPE_SEARCH_BLOCKS")) h->pipe_search_blocks = std::atoi(e);
     if (const char* e = std::getenv("QVMC_PIPE_EVAL_BLOCKS")) h->pipe_eval_blocks = std::atoi(e);
@@ -1223,6 +1259,8 @@ int qvmc_cuda_ham_destroy(qvmc_ham_t h) {
     for (auto& e : h->ev_p)
       if (e) cudaEventDestroy(e);
     for (auto& e : h->ev_b) cudaEventDestroy(e);
+    for (auto& e : h->ev_f)
+      if (e) cudaEventDestroy(e);
     if (h->side) {
       cudaStreamSynchronize(h->side);
       cudaStreamDestroy(h->side);
@@ -1263,7 +1301,10 @@ int qvmc_cuda_last_stats(qvmc_ham_t h, qvmc_stats* out) {
       ck(cudaEventElapsedTime(&out->rows_ms, h->ev[1], h->ev[2]), "elapsed");
       ck(cudaEventElapsedTime(&out->moments_ms, h->ev[2], h->ev[3]), "elapsed");
     }
-    if (h->timed_b > 0) {  // pipelined: per-launch kernel times summed over the row batches
+    if (h->timed_f) {  // fused: one kernel does both; reported as search_ms
+      ck(cudaEventElapsedTime(&out->search_ms, h->ev_f[0], h->ev_f[1]), "elapsed");
+      out->eval_ms = 0.f;
+    } else if (h->timed_b > 0) {  // pipelined: per-launch kernel times summed over the row batches
       out->search_ms = out->eval_ms = 0.f;
       for (int64_t b = 0; b < h->timed_b; ++b) {
         float ts = 0.f, te = 0.f;
@@ -1640,7 +1681,9 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       O.la = dla;
       O.ph = dph;
       O.cs = rcs;
-      if (P.join) {
+      if (P.join && h->fused) {
+        DISPATCH_W(W, (run_join_fused<WW>(h, rkeys, R, P, deloc)));
+      } else if (P.join) {
         DISPATCH_W(W, (run_join_pipelined<WW>(h, rkeys, n_unq, R, P, deloc)));
       } else {
         DISPATCH_W(W, (launch_rows<WW, kModeEloc>(h, dkeys, row_begin, row_end, O)));

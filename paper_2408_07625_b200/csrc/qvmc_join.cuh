@@ -22,6 +22,8 @@
 // Masks of weight >= 6 go through the residual scan (sample-set hash probes).
 #pragma once
 
+#include <type_traits>
+
 #include "qvmc_kernels.cuh"
 
 namespace qvmc_b200 {
@@ -597,20 +599,183 @@ __device__ __forceinline__ void eval_hit(const HamView& H, const JoinView& J, co
   }
 }
 
+// ---------------------------------------------------------------- fused search + evaluation
+// kModeFused: one kernel, warp-specialised. kFSearch search warps run the
+// join walk of k_rows_join and hand each full queue of hits (a "chunk") to an
+// evaluation warp through a ring of kFRing shared-memory slots per search
+// warp (no hit arrays in HBM, no capacity to overflow, no host round trip).
+// Evaluation warp e serves search warps e*kFPer .. e*kFPer+kFPer-1 and takes
+// each search warp's chunks in publish order, so a row's chunks are summed
+// in walk order: E_loc = sum of the row's chunk sums in order + the row base
+// (diagonal + residual) carried by the row's last chunk — deterministic, and
+// independent of which rows other warps process (row-shard invariant).
+#ifndef QVMC_FUSED_SEARCH
+#define QVMC_FUSED_SEARCH 8
+#endif
+#ifndef QVMC_FUSED_EVAL
+#define QVMC_FUSED_EVAL 4
+#endif
+#ifndef QVMC_FUSED_RING
+#define QVMC_FUSED_RING 3
+#endif
+#ifndef QVMC_FUSED_MINB
+#define QVMC_FUSED_MINB 2
+#endif
+constexpr int kFSearch = QVMC_FUSED_SEARCH;
+constexpr int kFEval = QVMC_FUSED_EVAL;
+constexpr int kFPer = kFSearch / kFEval;
+constexpr int kFRing = QVMC_FUSED_RING;
+constexpr int kFThreads = 32 * (kFSearch + kFEval);
+static_assert(kFSearch % kFEval == 0, "every evaluation warp serves the same number of search warps");
+
+struct FusedQ {  // one chunk: hits as the search queue holds them (doubles from the bottom, singles from the top)
+  uint32_t y[kJQueue];
+  uint32_t g[kJQueue];
+  uint32_t k[kJQueue];
+};
+
+struct FusedHdr {
+  double2 base;    // last chunk of a row: diagonal + residual part of E_loc (NaN: zero amplitude)
+  uint32_t row;    // sorted position of the row
+  uint32_t out;    // output index (caller row - out_base)
+  uint16_t n, nd;  // hits, of which doubles (queue bottom)
+  uint8_t last;    // 1: the row's last chunk
+  uint8_t pos[16]; // minority orbitals of the row (kind B elements)
+  volatile int state;  // 0 free (search warp owns it), 1 ready (evaluation warp owns it)
+};
+
+struct FusedSmem {
+  FusedQ q[kFSearch][kFRing];
+  FusedHdr h[kFSearch][kFRing];
+  double2 acc[kFEval][kFPer];   // evaluation warps: running row sums per served search warp
+  volatile int done[kFSearch];  // search warp finished all its rows
+};
+
+template <int W>
+__device__ __forceinline__ void fused_eval_loop(const HamView& H, const JoinView& J, const uint64_t* __restrict__ keys,
+                                             int side, int s, const int* __restrict__ exp_flag, double2* eloc,
+                                             FusedSmem* F, uint16_t* spos, int e, int lane) {
+  const bool mag = *exp_flag == 0;  // amplitude magnitudes from the records (k_gather_sorted)
+  int rp[kFPer];
+  double2* acc = F->acc[e];  // per served search warp: the current row's sum of chunk sums (lane 0 writes)
+#pragma unroll
+  for (int i = 0; i < kFPer; ++i) rp[i] = 0;
+  if (lane < kFPer) acc[lane] = make_double2(0.0, 0.0);
+  __syncwarp();
+  unsigned idle = 0;
+  for (;;) {
+    bool progressed = false, all_done = true;
+#pragma unroll
+    for (int i = 0; i < kFPer; ++i) {
+      const int sw = e * kFPer + i;
+      const int done = F->done[sw];
+      __threadfence_block();
+      FusedHdr& hd = F->h[sw][rp[i]];
+      if (hd.state != 1) {
+        all_done &= done != 0;
+        continue;
+      }
+      all_done = false;
+      progressed = true;
+      __threadfence_block();
+      const FusedQ& q = F->q[sw][rp[i]];
+      const int64_t row = hd.row;
+      const unsigned n_hits = hd.n, nd = hd.nd;
+      if (n_hits) {
+        Key<W> xrow;
+#pragma unroll
+        for (int w = 0; w < W; ++w) xrow.w[w] = __ldg(keys + row * W + w);
+        const U64x4 sr = ldg256(J.rec + row * 4);
+        const double la_i = __longlong_as_double(static_cast<long long>(sr.a));
+        const double2 cs_i = make_double2(__longlong_as_double(static_cast<long long>(sr.b)),
+                                          __longlong_as_double(static_cast<long long>(sr.c)));
+        const double inv_ai = mag ? 1.0 / __longlong_as_double(static_cast<long long>(sr.d)) : 0.0;
+        __syncwarp();
+        if (lane < s) spos[lane] = hd.pos[lane];
+        __syncwarp();
+        double2 a = make_double2(0.0, 0.0);
+        for (unsigned k0 = 0; k0 < n_hits; k0 += 32) {
+          const unsigned k = k0 + lane;
+          JoinHit h;
+          h.valid = k < n_hits;
+          h.key = kNoKey;
+          h.sr = U64x4{0, 0, 0, 0};
+#pragma unroll
+          for (int t = 0; t < kGrecWords; ++t) h.r[t] = 0;
+          if (h.valid) {
+            const unsigned src = k < nd ? k : kJQueue - 1 - (k - nd);
+            const uint32_t y = q.y[src], g = q.g[src];
+            h.key = q.k[src];
+            h.sr = ldg256(J.rec + static_cast<int64_t>(y) * 4);
+            const U64x4 g0 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords);
+            const U64x4 g1 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords + 4);
+            h.r[0] = g0.a; h.r[1] = g0.b; h.r[2] = g0.c; h.r[3] = g0.d;
+            h.r[4] = g1.a; h.r[5] = g1.b; h.r[6] = g1.c; h.r[7] = g1.d;
+          }
+          eval_hit<W>(H, J, spos, h, xrow, la_i, cs_i, lane, s, side, a, inv_ai);
+        }
+        const double sx = warp_sum(a.x), sy = warp_sum(a.y);
+        if (lane == 0) {
+          acc[i].x += sx;
+          acc[i].y += sy;
+        }
+      }
+      if (hd.last && lane == 0) {
+        eloc[hd.out] = make_double2(hd.base.x + acc[i].x, hd.base.y + acc[i].y);
+        acc[i] = make_double2(0.0, 0.0);
+      }
+      __syncwarp();
+      __threadfence_block();
+      if (lane == 0) hd.state = 0;  // the slot goes back to its search warp
+      rp[i] = rp[i] + 1 == kFRing ? 0 : rp[i] + 1;
+    }
+    if (!progressed) {
+      if (all_done) break;
+      __nanosleep(idle < 8 ? 32 : 256);
+      ++idle;
+    } else {
+      idle = 0;
+    }
+  }
+}
+
 #ifndef QVMC_SEARCH_MINB
 #define QVMC_SEARCH_MINB 4  // split search kernel (no drain): 64 registers, 32 warps per SM (measured best, r01x)
 #endif
 
 template <int W, int MODE>
-__global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB : QVMC_JOIN_MINB)
+__global__ void __launch_bounds__(MODE == kModeFused ? kFThreads : kThreads,
+                                  MODE == kModeFused ? QVMC_FUSED_MINB
+                                                     : (MODE == kModeHits ? QVMC_SEARCH_MINB : QVMC_JOIN_MINB))
     k_rows_join(const __grid_constant__ HamView H, const TableView T, const __grid_constant__ JoinView J,
                 const uint64_t* __restrict__ keys, const RowSet R, int side, int s, const __grid_constant__ Ctl C,
                 const __grid_constant__ RowOut O) {
-  static_assert(MODE == kModeHits || MODE == kModeCount || MODE == kModeEmit, "join modes: hits, count, emit");
-  constexpr bool kEval = MODE == kModeHits;  // E_loc rows (split evaluation)
-  __shared__ JoinSmem s_w[kWarps];
+  static_assert(MODE == kModeHits || MODE == kModeCount || MODE == kModeEmit || MODE == kModeFused,
+                "join modes: hits, count, emit, fused");
+  constexpr bool kFused = MODE == kModeFused;
+  constexpr bool kEval = MODE == kModeHits || kFused;  // E_loc rows (split or fused evaluation)
+  constexpr int kSearchWarps = kFused ? kFSearch : kWarps;
+  __shared__ JoinSmem s_w[kSearchWarps];
+  // kModeFused: the chunk rings live in dynamic shared memory (sizeof(FusedSmem))
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  FusedSmem* s_f = reinterpret_cast<FusedSmem*>(s_dyn);
+  __shared__ uint16_t s_epos[kFused ? kFEval : 1][32];
   const int lane = threadIdx.x & 31;
-  JoinSmem* sm = &s_w[threadIdx.x >> 5];
+  const int wid = threadIdx.x >> 5;
+  if constexpr (kFused) {
+    if (threadIdx.x < kFSearch * kFRing) {
+      s_f[0].h[threadIdx.x / kFRing][threadIdx.x % kFRing].state = 0;
+      if (threadIdx.x % kFRing == 0) s_f[0].done[threadIdx.x / kFRing] = 0;
+    }
+    __syncthreads();
+    if (wid >= kFSearch) {  // evaluation warps
+      fused_eval_loop<W>(H, J, keys, side, s, O.exp_flag, O.eloc, s_f, s_epos[wid - kFSearch], wid - kFSearch,
+                         lane);
+      return;
+    }
+  }
+  JoinSmem* sm = &s_w[wid];
+  unsigned qr = 0;  // kModeFused: the ring slot this search warp fills
   const int n = H.n;
   const int n_ranges = s * (s - 1) / 2;
   if (lane == 0) {
@@ -618,6 +783,35 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
     sm->qs = 0;
   }
   __syncwarp();
+  // the search warp hands its current slot to its evaluation warp and takes the
+  // next one once that is free again (kModeFused)
+  auto publish = [&](int64_t row, int64_t out, bool last, double2 base) {
+    if constexpr (kFused) {
+      FusedHdr& hd = s_f[0].h[wid][qr];
+      __syncwarp();
+      if (lane < 16) hd.pos[lane] = static_cast<uint8_t>(sm->pos[lane]);
+      if (lane == 0) {
+        hd.row = static_cast<uint32_t>(row);
+        hd.out = static_cast<uint32_t>(out);
+        hd.nd = static_cast<uint16_t>(sm->qn);
+        hd.n = static_cast<uint16_t>(sm->qn + sm->qs);
+        hd.last = last ? 1 : 0;
+        hd.base = base;
+        sm->qn = 0;
+        sm->qs = 0;
+      }
+      __syncwarp();
+      __threadfence_block();
+      if (lane == 0) hd.state = 1;
+      qr = qr + 1 == kFRing ? 0 : qr + 1;
+      if (lane == 0) {
+        unsigned w = 0;
+        while (s_f[0].h[wid][qr].state != 0) __nanosleep(w++ < 8 ? 32 : 128);
+      }
+      __syncwarp();
+      __threadfence_block();
+    }
+  };
 
   uint64_t tot_cand = 0, tot_hits = 0;
   for (;;) {
@@ -657,8 +851,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
     __syncwarp();
     if (kEval) {
       if (isinf(*reinterpret_cast<const volatile double*>(&sm->la))) {  // energy.cpp:32-33
-        if (lane == 0) {
-          atomicOr(C.err, kErrZeroAmp);
+        if (lane == 0) atomicOr(C.err, kErrZeroAmp);
+        if constexpr (kFused) {
+          publish(row, orow - R.out_base, true, make_double2(CUDART_NAN, CUDART_NAN));
+        } else if (lane == 0) {
           O.base[orow - R.out_base] = make_double2(CUDART_NAN, CUDART_NAN);
           O.row_last[orow - R.out_base] = ~0u;
         }
@@ -681,6 +877,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
     if (lane < s) {
       sm->pos[lane] = static_cast<uint16_t>(pos);
       if (MODE == kModeHits) O.rowpos[row * 16 + lane] = static_cast<uint8_t>(pos);
+      if (kFused && lane >= s && lane < 16) sm->pos[lane] = 0;
     }
     __syncwarp();
     const int pos0 = sm->pos[0], pos1 = sm->pos[1];
@@ -723,7 +920,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
     }
     // the queue becomes one chunk of this row (split evaluation) once it holds `thresh` hits
     auto emit = [&](unsigned thresh) {
-      if (kEval) {
+      if constexpr (kFused) {
+        __syncwarp();
+        if (sm->qn + sm->qs >= thresh) publish(row, orow - R.out_base, false, make_double2(0.0, 0.0));
+      } else if (kEval) {
         __syncwarp();
         const unsigned qd = sm->qn, qsn = sm->qs;
         const unsigned qn = qd + qsn;
@@ -869,16 +1069,23 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
         const bool hit = g >= 0;
         const unsigned hm = __ballot_sync(0xffffffffu, hit);
         if (hm) {
-          if (MODE == kModeHits) {  // doubles fill the queue from the bottom, singles from the top
+          if (kEval) {  // doubles fill the queue from the bottom, singles from the top
             const bool is_s = (kk >> 16) == 0xFFFFu;
             const unsigned lt = (1u << lane) - 1u;
             const unsigned hs = __ballot_sync(0xffffffffu, hit && is_s), hd = hm & ~hs;
             const unsigned bd = sm->qn, bs = sm->qs;
             if (hit) {
               const unsigned k = is_s ? kJQueue - 1 - (bs + __popc(hs & lt)) : bd + __popc(hd & lt);
-              sm->qy[k] = y;
-              sm->qg[k] = static_cast<uint32_t>(g);
-              sm->qk[k] = kk;
+              if constexpr (kFused) {
+                FusedQ& fq = s_f[0].q[wid][qr];
+                fq.y[k] = y;
+                fq.g[k] = static_cast<uint32_t>(g);
+                fq.k[k] = kk;
+              } else {
+                sm->qy[k] = y;
+                sm->qg[k] = static_cast<uint32_t>(g);
+                sm->qk[k] = kk;
+              }
             }
             __syncwarp();
             if (lane == 0) {
@@ -903,7 +1110,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
       }
       if (!walking) break;
     }
-    emit(1u);
+    if (!kFused) emit(1u);  // fused: the remaining hits travel in the row's last chunk with its base
 
     const Key<W> xrow = row_key<W>(sm);
     // even flip masks of weight >= 6: popcount filter + sample-set probe
@@ -992,7 +1199,9 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
     if (kEval) {  // the walk drained the queue; residual hits were evaluated in place
       const double re = warp_sum(acc.x);
       const double im = warp_sum(acc.y);
-      if (lane == 0) {
+      if constexpr (kFused) {
+        publish(row, orow - R.out_base, true, make_double2(re, im));
+      } else if (lane == 0) {
         O.base[orow - R.out_base] = make_double2(re, im);
         O.row_last[orow - R.out_base] = prev_chunk;
       }
@@ -1011,6 +1220,11 @@ __global__ void __launch_bounds__(kThreads, MODE == kModeHits ? QVMC_SEARCH_MINB
     tot_cand += cand;
     tot_hits += row_hits;
     if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr(C.err, kErrDuplicate);
+  }
+  if constexpr (kFused) {
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) s_f[0].done[wid] = 1;
   }
   tot_cand = warp_sum(tot_cand);
   if (lane == 0) {

@@ -22,7 +22,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kUnroll = 4;  // independent probes in flight per lane
 
 enum : int { kErrDuplicate = 1, kErrZeroAmp = 2, kErrBadPair = 4, kErrHitOverflow = 8 };
-enum : int { kModeEloc = 0, kModeCount = 1, kModeEmit = 2, kModeHits = 3 };
+enum : int { kModeEloc = 0, kModeCount = 1, kModeEmit = 2, kModeHits = 3, kModeFused = 4 };
 
 struct HamView {
   int n;        // qubits
@@ -257,6 +257,7 @@ struct RowOut {
   uint64_t hit_cap;
   uint64_t chunk_cap;
   uint8_t* rowpos;            // [key position][16] the row's minority orbitals (for the chunk evaluation)
+  const int* exp_flag;        // kModeFused: some |log psi| > 700 (amplitude ratios through exp)
 };
 
 __global__ void k_cos_sin(const double* __restrict__ ph, int64_t n, double2* cs) {

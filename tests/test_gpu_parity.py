@@ -265,13 +265,16 @@ def test_ops_counters(cuda_ok):
 
 @pytest.mark.parametrize("hit_cap", ["4096", "100000"])
 def test_join_hit_buffer_regrow(cuda_ok, monkeypatch, hit_cap):
-    """A tiny first hit-buffer capacity exercises the overflow detection and
-    the rerun with grown buffers: same E_loc, pair count and moments as a
-    handle with the default capacity, and as the pairs-based evaluation."""
+    """Split path (QVMC_FUSED=0: search kernel -> hit chunks in HBM -> chunk
+    evaluation): a tiny first hit-buffer capacity exercises the overflow
+    detection and the rerun with grown buffers: same E_loc, pair count and
+    moments as a handle with the default capacity, and as the pairs-based
+    evaluation."""
     n_unq = 20_000
     keys = synthetic.near_hf_keys(118, 110, n_unq, seed=7)
     b = synthetic.sample_batch(keys, seed=3)
     c, x, y, z = synthetic.jw_terms(118, 3_000_000, seed=1)
+    monkeypatch.setenv("QVMC_FUSED", "0")
     monkeypatch.delenv("QVMC_HIT_CAP", raising=False)
     H0 = q.HamiltonianIndex.from_masks(118, c, x, y, z)
     ref = q.surrogate_energy(H0, b)
@@ -289,6 +292,33 @@ def test_join_hit_buffer_regrow(cuda_ok, monkeypatch, hit_cap):
     loc = q.local_energies(p, b, H)
     scale = eloc_scale(p.entries, H.group_offsets, H.coeff, b.log_amps, n_unq)
     assert_eloc_close(got.locals, loc, scale)
+
+
+@pytest.mark.parametrize("n_qubits,n_e,n_terms,n_unq", [(118, 110, 3_000_000, 50_000), (56, 14, 300_000, 50_000)])
+def test_fused_matches_split_evaluation(cuda_ok, monkeypatch, n_qubits, n_e, n_terms, n_unq):
+    """The fused warp-specialised kernel (default) and the split search +
+    chunk-evaluation kernels give the same E_loc (to fp64 reordering: chunk
+    sums are added in a different order), the same pair count, and the
+    fused result is deterministic and row-shard invariant bit for bit."""
+    keys = synthetic.near_hf_keys(n_qubits, n_e, n_unq, seed=11)
+    b = synthetic.sample_batch(keys, seed=3)
+    c, x, y, z = synthetic.jw_terms(n_qubits, n_terms, seed=1)
+    monkeypatch.setenv("QVMC_FUSED", "0")
+    Hs = q.HamiltonianIndex.from_masks(n_qubits, c, x, y, z)
+    split = q.surrogate_energy(Hs, b)
+    n_pairs = q.last_stats(Hs)["pairs"]
+    monkeypatch.setenv("QVMC_FUSED", "1")
+    H = q.HamiltonianIndex.from_masks(n_qubits, c, x, y, z)
+    fused = q.surrogate_energy(H, b)
+    st = q.last_stats(H)
+    assert st["pairs"] == n_pairs and st["join_mode"] == 1
+    p = q.loop_over_terms(keys, H)
+    scale = eloc_scale(p.entries, H.group_offsets, H.coeff, b.log_amps, n_unq)
+    assert_eloc_close(fused.locals, split.locals, scale, rtol=1e-12)
+    again = q.surrogate_energy(H, b)
+    assert np.array_equal(again.locals, fused.locals) and again.e_var == fused.e_var
+    part = q.surrogate_energy(H, b, n_unq // 4, n_unq // 2, check=False)
+    assert np.array_equal(part.locals, fused.locals[n_unq // 4: n_unq // 2])
 
 
 @pytest.mark.parametrize("n_qubits,n_e,n_terms,n_unq,join", [

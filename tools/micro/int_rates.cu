@@ -35,7 +35,7 @@
 
 enum Op { kLop3 = 0, kIadd3 = 1, kPopc = 2, kShf = 3, kImad = 4, kIssue = 5, kFlo = 6 };
 
-constexpr int kIters = 4096;
+constexpr int kIters = 65536;
 constexpr int kChains = 8;
 
 template <int OP>
@@ -130,14 +130,17 @@ int run_rate(const char* name, int sms, int threads, int ctas_per_sm, double clk
   const int insts_per_op = OP == kIadd3 ? 2 : 1;  // ptxas fuses two dependent adds into one IADD3 (SASS-checked)
   const double warp_inst_per_cta = (double)kIters * kChains * (threads / 32) / insts_per_op;
   // CTAs of one SM run concurrently: per-SM rate = ctas_per_sm * per-CTA instructions / CTA cycles
-  const double per_clk_sm = ctas_per_sm * warp_inst_per_cta / cmed;
+  // chip rate from the CUDA events around the launch (all CTAs, launch overhead included: a lower bound);
+  // per-SM per-clock = chip rate / SMs / SM clock, with the clock implied by the slowest CTA's clock64 span
   const double per_s_chip_event = warp_inst_per_cta * grid / (ms * 1e-3);
-  std::printf("  \"%s\": {\"warp_inst_per_clk_per_sm\": %.4f, \"lane_ops_per_clk_per_sm\": %.2f, "
-              "\"warp_inst_per_s_chip_events\": %.5e, \"lane_ops_per_s_chip_events\": %.5e, "
+  const double implied_mhz = cmax / (ms * 1e3);
+  const double per_clk_sm = per_s_chip_event / sms / (implied_mhz * 1e6);
+  const double per_clk_sm_attr = per_s_chip_event / sms / (clk_mhz * 1e6);
+  std::printf("  \"%s\": {\"warp_inst_per_clk_per_sm\": %.4f, \"warp_inst_per_clk_per_sm_at_attr_clock\": %.4f, "
+              "\"lane_ops_per_clk_per_sm\": %.2f, \"warp_inst_per_s_chip\": %.5e, \"lane_ops_per_s_chip\": %.5e, "
               "\"implied_clock_mhz\": %.1f, \"cycles_median\": %.0f, \"cycles_max\": %.0f, \"ms\": %.4f}%s\n",
-              name, per_clk_sm, 32 * per_clk_sm, per_s_chip_event, 32 * per_s_chip_event,
-              cmax / (ms * 1e3), cmed, cmax, ms, last ? "" : ",");
-  (void)clk_mhz;
+              name, per_clk_sm, per_clk_sm_attr, 32 * per_clk_sm, per_s_chip_event, 32 * per_s_chip_event,
+              implied_mhz, cmed, cmax, ms, last ? "" : ",");
   cudaFree(sink);
   cudaFree(cyc);
   return 0;
@@ -188,8 +191,9 @@ int main() {
   const int sms = p.multiProcessorCount;
   std::printf("{\n  \"gpu\": \"%s\", \"sm_count\": %d, \"cc\": \"%d.%d\", \"attr_clock_mhz\": %.0f,\n", p.name, sms,
               p.major, p.minor, clk_mhz);
-  std::printf("  \"method\": \"8 independent chains/thread of one inline-PTX op, 4 CTAs x 256 threads per SM, "
-              "clock64 per CTA; rate = warp instructions per SM clock\",\n");
+  std::printf("  \"method\": \"8 independent chains/thread of one inline-PTX op (SASS-checked), 4 CTAs x 256 "
+              "threads per SM, 65536 iterations; chip rate = warp instructions / CUDA-event time of the launch; per SM "
+              "clock = chip rate / SMs / clock implied by the longest CTA clock64 span\",\n");
   int rc = 0;
   rc |= run_rate<kLop3>("lop3", sms, 256, 4, clk_mhz, false);
   rc |= run_rate<kIadd3>("iadd3", sms, 256, 4, clk_mhz, false);

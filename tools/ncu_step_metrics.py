@@ -21,6 +21,7 @@ from pathlib import Path
 
 OUT_DIR = Path(__file__).resolve().parents[1] / "profiles"
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
+         "ns": 1e-6, "us": 1e-3, "ms": 1.0, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9,
          "inst": 1, "Kinst": 1e3, "Minst": 1e6, "Ginst": 1e9, "": 1}
 
 
