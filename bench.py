@@ -188,14 +188,15 @@ def full_size_reference(cfg_name):
 
 
 def masks_to_strings(n_qubits, x, y, z):
-    from paper_2408_07625_b200 import basis
-    bx = basis.to_bool_rows(x, n_qubits)
-    by = basis.to_bool_rows(y, n_qubits)
-    bz = basis.to_bool_rows(z, n_qubits)
-    arr = np.full(bx.shape, ord("I"), dtype=np.uint8)
-    arr[bx == 1] = ord("X")
-    arr[by == 1] = ord("Y")
-    arr[bz == 1] = ord("Z")
+    """Pauli strings from (x, y, z) word masks (numpy only: the reference arm
+    imports nothing of this repo's package)."""
+    def bits(m):
+        m = np.ascontiguousarray(m, dtype="<u8")
+        return np.unpackbits(m.view(np.uint8).reshape(m.shape[0], -1), axis=1, bitorder="little")[:, :n_qubits]
+    arr = np.full((np.asarray(x).shape[0], n_qubits), ord("I"), dtype=np.uint8)
+    arr[bits(x) == 1] = ord("X")
+    arr[bits(y) == 1] = ord("Y")
+    arr[bits(z) == 1] = ord("Z")
     raw = arr.tobytes().decode("ascii")
     return [raw[i * n_qubits:(i + 1) * n_qubits] for i in range(arr.shape[0])]
 
@@ -209,10 +210,36 @@ def default_cpu_sample(cfg, arm="reference"):
 
 # ------------------------------------------------------------------ reference arm
 
+def _inputs_in_child(cfg_name, n_unq):
+    """make_inputs in a child process (the seeded generators live in the repo's
+    lib/libqvmc_synth.so): the reference arm's own process then maps only the
+    reference build (oracle/_ref), never a library of this repo."""
+    import tempfile
+    from types import SimpleNamespace
+    with tempfile.TemporaryDirectory() as td:
+        out = Path(td) / "inputs.npz"
+        code = ("import sys, numpy as np; sys.path.insert(0, sys.argv[1]); import bench; "
+                "cfg, (c, x, y, z), b, _ = bench.make_inputs(sys.argv[2], None if sys.argv[3] == '-' else int(sys.argv[3])); "
+                "np.savez(sys.argv[4], c=c, x=x, y=y, z=z, keys=b.vectors, lp=b.log_probs, la=b.log_amps, "
+                "ph=b.phases, norm=np.array([b.norm, b.log_norm]), "
+                "cfg=np.array([cfg.name, cfg.n_qubits, cfg.n_electrons, cfg.n_terms, cfg.n_unq], dtype=object))")
+        subprocess.run([sys.executable, "-c", code, str(ROOT), cfg_name, "-" if n_unq is None else str(n_unq),
+                        str(out)], check=True)
+        d = np.load(out, allow_pickle=True)
+        batch = SimpleNamespace(vectors=d["keys"], log_probs=d["lp"], log_amps=d["la"], phases=d["ph"],
+                                norm=float(d["norm"][0]), log_norm=float(d["norm"][1]))
+        batch.size = lambda: int(batch.vectors.shape[0])
+        cm = (d["c"], d["x"], d["y"], d["z"])
+        f = d["cfg"].tolist()
+        cfg = SimpleNamespace(name=str(f[0]), n_qubits=int(f[1]), n_electrons=int(f[2]), n_terms=int(f[3]),
+                              n_unq=int(f[4]))
+    return cfg, cm, batch
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
-    cfg, cm, batch, _ = make_inputs(args.config, args.n_unq)
+    cfg, cm, batch = _inputs_in_child(args.config, args.n_unq)
     threads = os.cpu_count() or 1
     ref = CpuReference(cfg, cm, batch, args.cpu_sample or default_cpu_sample(args.config), threads)
     for _ in range(min(args.warmup, 1)):

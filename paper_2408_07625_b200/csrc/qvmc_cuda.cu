@@ -166,7 +166,7 @@ struct qvmc_ham_s {
   std::vector<cudaEvent_t> ev_b;  // pipelined split evaluation: per batch search start/end, eval start/end
   cudaEvent_t ev_f[2] = {nullptr, nullptr};  // fused join kernel start/end
   bool timed_f = false;
-  bool fused = true;  // QVMC_FUSED=0: the pipelined split search + chunk evaluation
+  bool fused = false;  // QVMC_FUSED=1: one warp-specialised search + evaluation kernel (measured slower, r2a)
   int64_t timed_b = 0;            // batches timed by ev_b in the last call
 };
 

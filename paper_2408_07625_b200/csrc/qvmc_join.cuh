@@ -484,11 +484,13 @@ struct JoinSmem {
   uint32_t qy[kJQueue];  // hit queue: partner (sorted position), group, flip position key
   uint32_t qg[kJQueue];
   uint32_t qk[kJQueue];
-  uint32_t r_lo[kJoinMaxRanges];  // bucket ranges of the current row
-  uint32_t r_len[kJoinMaxRanges];
-  uint8_t ta[kJoinMaxRanges];     // the row's pair T_x of each bucket
-  uint8_t tb[kJoinMaxRanges];
-  uint32_t dbase[kJoinMaxRanges]; // P + pidx(T_x) * P: the doubles-bitmap row of each bucket
+  // the row's buckets: pre[t] = first walk index of bucket t (exclusive prefix
+  // of the bucket lengths), pre[C] = members walked; binfo[t] = (lo - pre[t]
+  // (mod 2^32: member of walk index j at mem[binfo.x + j]), doubles-bitmap row
+  // P + pidx(T_x) * P); tab[t] = T_x.a | T_x.b << 8
+  uint32_t pre[kJoinMaxRanges + 1];
+  uint2 binfo[kJoinMaxRanges];
+  uint16_t tab[kJoinMaxRanges];
   uint64_t x[4];                  // the current row: key, log psi, (cos, sin) of its phase; kept here
   double la, cs_c, cs_s;          // (not in registers) across the candidate walk
   uint16_t pos[32];               // minority orbitals of the current row
@@ -881,43 +883,45 @@ __global__ void __launch_bounds__(MODE == kModeFused ? kFThreads : kThreads,
     }
     __syncwarp();
     const int pos0 = sm->pos[0], pos1 = sm->pos[1];
-    // bucket t of this row: pair (a, b) of S(x), range from the index
-    for (int t = lane; t < n_ranges; t += 32) {
-      const uint32_t b = pair_b(t);
-      const int pa = sm->pos[t - b * (b - 1) / 2], pb = sm->pos[b];
-      sm->ta[t] = static_cast<uint8_t>(pa);
-      sm->tb[t] = static_cast<uint8_t>(pb);
-      sm->dbase[t] = J.P + pidx(pa, pb) * J.P;
-      const uint2 rg = __ldcs(J.rng + static_cast<uint64_t>(row) * J.C + t);  // read once per call
-      sm->r_lo[t] = rg.x;
-      sm->r_len[t] = rg.y - rg.x;
+    // bucket t of this row: pair (a, b) of S(x), range from the index; the
+    // lengths' exclusive prefix turns the C ranges into one walk index space
+    uint32_t M = 0;  // members walked by this row (warp-uniform)
+    for (int t0 = 0; t0 < n_ranges; t0 += 32) {
+      const int t = t0 + lane;
+      uint32_t len = 0, lo = 0, db = 0;
+      int pa = 0, pb = 0;
+      if (t < n_ranges) {
+        const uint32_t b = pair_b(t);
+        pa = sm->pos[t - b * (b - 1) / 2];
+        pb = sm->pos[b];
+        const uint2 rg = __ldcs(J.rng + static_cast<uint64_t>(row) * J.C + t);  // read once per call
+        lo = rg.x;
+        len = rg.y - rg.x;
+        db = J.P + pidx(pa, pb) * J.P;
+      }
+      uint32_t inc = len;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+      }
+      const uint32_t ex = M + inc - len;
+      if (t < n_ranges) {
+        sm->tab[t] = static_cast<uint16_t>(pa | pb << 8);
+        sm->pre[t] = ex;
+        sm->binfo[t] = make_uint2(lo - ex, db);
+      }
+      M += __shfl_sync(0xffffffffu, inc, 31);
     }
+    if (lane == 0) sm->pre[n_ranges] = M;
     __syncwarp();
 
     double2 acc = make_double2(0.0, 0.0);
     uint32_t hits = 0;
-    uint64_t cand = 0;
+    uint64_t cand = lane == 0 ? M : 0;
     uint32_t prev_chunk = ~0u;  // kModeHits: last flushed chunk of this row
     bool dup = false;           // a duplicate of this row's key in the sample set
     uint32_t s_head = 0, s_tail = 0;  // survivor ring (warp-uniform)
-    // per-lane cursor over the concatenated ranges: member pointer and the
-    // current range's (T_x, bitmap row) in registers, reloaded on a range change
-    int rg = 0;
-    uint32_t off = lane;
-    uint32_t len = sm->r_len[0];
-    while (rg < n_ranges && off >= len) {
-      off -= len;
-      if (++rg < n_ranges) len = sm->r_len[rg];
-    }
-    const uint64_t* mp = nullptr;
-    int c_ta = 0, c_tb = 0;
-    uint32_t c_db = 0;
-    if (rg < n_ranges) {
-      mp = J.mem + sm->r_lo[rg] + off;
-      c_ta = sm->ta[rg];
-      c_tb = sm->tb[rg];
-      c_db = sm->dbase[rg];
-    }
     // the queue becomes one chunk of this row (split evaluation) once it holds `thresh` hits
     auto emit = [&](unsigned thresh) {
       if constexpr (kFused) {
@@ -963,152 +967,153 @@ __global__ void __launch_bounds__(MODE == kModeFused ? kFThreads : kThreads,
         }
       }
     };
-    for (;;) {  // the walk: members -> accept rule + bitmap -> survivor ring -> lookups in batches of 32
-      const bool walking = __any_sync(0xffffffffu, rg < n_ranges);
-      if (walking) {
-      constexpr int U = QVMC_JOIN_UNROLL;
-      uint64_t v[U];
-      int uta[U], utb[U];
-      uint32_t udb[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        v[u] = ~0ull;
-        uta[u] = c_ta;
-        utb[u] = c_tb;
-        udb[u] = c_db;
-        if (rg < n_ranges) {
-          v[u] = __ldg(mp);
-          off += 32;
-          mp += 32;
-          if (off >= len) {
-            do {
-              off -= len;
-              if (++rg < n_ranges) len = sm->r_len[rg];
-            } while (rg < n_ranges && off >= len);
-            if (rg < n_ranges) {
-              mp = J.mem + sm->r_lo[rg] + off;
-              c_ta = sm->ta[rg];
-              c_tb = sm->tb[rg];
-              c_db = sm->dbase[rg];
+    // flip-table lookups of up to 32 survivors with every lane busy, hits queued
+    auto lookups = [&]() {
+      const uint32_t cntl = min(s_tail - s_head, 32u);
+      const bool valid = static_cast<uint32_t>(lane) < cntl;
+      uint32_t y = 0, kk = kNoKey;
+      int64_t g = -1;
+      if (valid) {
+        const uint32_t e = (s_head + lane) & (kJSurv - 1);
+        y = sm->sy[e];
+        kk = sm->sk[e];
+        const uint32_t bk = xy_bucket(kk, static_cast<uint32_t>(J.xy_mask));
+        g = xy_resolve(kk, ldg256(J.xy_tab + static_cast<uint64_t>(bk) * 4));
+        if (g == kChain) g = xy_chain(kk, bk, J.xy_tab, static_cast<uint32_t>(J.xy_mask));
+      }
+      s_head += cntl;
+      // warp-aggregated append of the hits
+      const bool hit = g >= 0;
+      const unsigned hm = __ballot_sync(0xffffffffu, hit);
+      if (hm) {
+        if (kEval) {  // doubles fill the queue from the bottom, singles from the top
+          const bool is_s = (kk >> 16) == 0xFFFFu;
+          const unsigned lt = (1u << lane) - 1u;
+          const unsigned hs = __ballot_sync(0xffffffffu, hit && is_s), hd = hm & ~hs;
+          const unsigned bd = sm->qn, bs = sm->qs;
+          if (hit) {
+            const unsigned k = is_s ? kJQueue - 1 - (bs + __popc(hs & lt)) : bd + __popc(hd & lt);
+            if constexpr (kFused) {
+              FusedQ& fq = s_f[0].q[wid][qr];
+              fq.y[k] = y;
+              fq.g[k] = static_cast<uint32_t>(g);
+              fq.k[k] = kk;
+            } else {
+              sm->qy[k] = y;
+              sm->qg[k] = static_cast<uint32_t>(g);
+              sm->qk[k] = kk;
             }
           }
-        }
-      }
-      // doubles-bitmap words of all U members in flight before the accept rule
-      uint32_t dw[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        dw[u] = ~0u;
-        if (J.pbits && v[u] != ~0ull) {
-          const uint32_t bi = udb[u] + static_cast<uint32_t>(v[u] >> 48);
-          dw[u] = __ldg(J.pbits + (bi >> 5)) >> (bi & 31);
-        }
-      }
-      // accept rule (header comment) -> exact position key of the flip mask
-      uint32_t key[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        key[u] = kNoKey;
-        if (v[u] == ~0ull) continue;
-        const int ya = static_cast<int>(v[u] >> 32) & 0xFF, yb = static_cast<int>(v[u] >> 40) & 0xFF;
-        const int ta = uta[u], tb = utb[u];
-        const bool ea = ya == ta || ya == tb, eb = yb == ta || yb == tb;
-        if (!ea && !eb) {  // disjoint pairs: double excitation; merge two sorted pairs
-          ++cand;
-          if (!(dw[u] & 1u)) continue;
-          int p0 = ta, p1 = tb, p2 = ya, p3 = yb;
-          sort2(p0, p2);
-          sort2(p1, p3);
-          sort2(p1, p2);
-          key[u] = static_cast<uint32_t>(p0) | static_cast<uint32_t>(p1) << 8 | static_cast<uint32_t>(p2) << 16 |
-                   static_cast<uint32_t>(p3) << 24;
-        } else if (ea != eb) {  // one shared orbital o: x loses c, gains a
-          const int o = ea ? ya : yb, a = ea ? yb : ya;
-          const int cc = (o == ta) ? tb : ta;
-          if (o == (cc == pos0 ? pos1 : pos0)) {
-            int p0 = cc, p1 = a;
-            sort2(p0, p1);
-            ++cand;
-            if (J.pbits && !pbit(J.pbits, pidx(p0, p1))) continue;
-            key[u] = static_cast<uint32_t>(p0) | static_cast<uint32_t>(p1) << 8 | 0xFFFF0000u;
+          __syncwarp();
+          if (lane == 0) {
+            sm->qn = bd + __popc(hd);
+            sm->qs = bs + __popc(hs);
           }
-        } else if (static_cast<uint32_t>(v[u]) != static_cast<uint32_t>(row)) {
-          dup = true;  // T_y = T_x in an exact bucket: the same key at another position
+        } else if (MODE == kModeEmit) {
+          unsigned base = 0;
+          if (lane == 0) base = atomicAdd(&sm->cursor, __popc(hm));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (hit) {
+            const unsigned k = base + __popc(hm & ((1u << lane) - 1u));
+            const uint64_t at = O.row_off[orow] + k;
+            O.xp_out[at] = R.perm ? __ldg(R.perm + y) : y;
+            O.g_out[at] = static_cast<uint32_t>(g);
+          }
         }
-      }
-      // survivors -> ring; the flip-table lookups then run 32 at a time with
-      // every lane busy (a lookup per candidate would execute on nearly every
-      // step for the ~1 in 7 candidates that survive)
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const unsigned smk = __ballot_sync(0xffffffffu, key[u] != kNoKey);
-        if (key[u] != kNoKey) {
-          const uint32_t e = (s_tail + __popc(smk & ((1u << lane) - 1u))) & (kJSurv - 1);
-          sm->sy[e] = static_cast<uint32_t>(v[u]);
-          sm->sk[e] = key[u];
-        }
-        s_tail += __popc(smk);
+        hits += hit ? 1u : 0u;
       }
       __syncwarp();
-      }
-      while (s_tail - s_head >= 32 || (!walking && s_tail != s_head)) {
-        const uint32_t cntl = min(s_tail - s_head, 32u);
-        const bool valid = static_cast<uint32_t>(lane) < cntl;
-        uint32_t y = 0, kk = kNoKey;
-        int64_t g = -1;
-        if (valid) {
-          const uint32_t e = (s_head + lane) & (kJSurv - 1);
-          y = sm->sy[e];
-          kk = sm->sk[e];
-          const uint32_t bk = xy_bucket(kk, static_cast<uint32_t>(J.xy_mask));
-          g = xy_resolve(kk, ldg256(J.xy_tab + static_cast<uint64_t>(bk) * 4));
-          if (g == kChain) g = xy_chain(kk, bk, J.xy_tab, static_cast<uint32_t>(J.xy_mask));
-        }
-        s_head += cntl;
-        // warp-aggregated append of the hits
-        const bool hit = g >= 0;
-        const unsigned hm = __ballot_sync(0xffffffffu, hit);
-        if (hm) {
-          if (kEval) {  // doubles fill the queue from the bottom, singles from the top
-            const bool is_s = (kk >> 16) == 0xFFFFu;
-            const unsigned lt = (1u << lane) - 1u;
-            const unsigned hs = __ballot_sync(0xffffffffu, hit && is_s), hd = hm & ~hs;
-            const unsigned bd = sm->qn, bs = sm->qs;
-            if (hit) {
-              const unsigned k = is_s ? kJQueue - 1 - (bs + __popc(hs & lt)) : bd + __popc(hd & lt);
-              if constexpr (kFused) {
-                FusedQ& fq = s_f[0].q[wid][qr];
-                fq.y[k] = y;
-                fq.g[k] = static_cast<uint32_t>(g);
-                fq.k[k] = kk;
-              } else {
-                sm->qy[k] = y;
-                sm->qg[k] = static_cast<uint32_t>(g);
-                sm->qk[k] = kk;
-              }
+      emit(kJDrainAt);
+    };
+    // the walk: lane l takes walk indices l, l+32, ...; its bucket cursor t only
+    // moves forward (a bucket holds ~75 members at c118, so a lane crosses a
+    // bucket end on fewer than half of its steps)
+    {
+      int t = 0;
+      uint32_t nxt = M ? sm->pre[1] : 0u;
+      uint2 bi = sm->binfo[0];
+      uint32_t tx = sm->tab[0];
+      constexpr int U = QVMC_JOIN_UNROLL;
+      for (uint32_t base = 0; base < M; base += 32 * U) {
+        uint64_t v[U];
+        uint32_t utx[U], udb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t j = base + 32 * u + lane;
+          v[u] = ~0ull;
+          utx[u] = 0;
+          udb[u] = 0;
+          if (j < M) {
+            if (nxt <= j) {
+              do {
+                ++t;
+                nxt = sm->pre[t + 1];
+              } while (nxt <= j);
+              bi = sm->binfo[t];
+              tx = sm->tab[t];
             }
-            __syncwarp();
-            if (lane == 0) {
-              sm->qn = bd + __popc(hd);
-              sm->qs = bs + __popc(hs);
-            }
-          } else if (MODE == kModeEmit) {
-            unsigned base = 0;
-            if (lane == 0) base = atomicAdd(&sm->cursor, __popc(hm));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (hit) {
-              const unsigned k = base + __popc(hm & ((1u << lane) - 1u));
-              const uint64_t at = O.row_off[orow] + k;
-              O.xp_out[at] = R.perm ? __ldg(R.perm + y) : y;
-              O.g_out[at] = static_cast<uint32_t>(g);
-            }
+            v[u] = __ldg(J.mem + (bi.x + j));
+            utx[u] = tx;
+            udb[u] = bi.y;
           }
-          hits += hit ? 1u : 0u;
+        }
+        // doubles-bitmap words of all U members in flight before the accept rule
+        uint32_t dw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          dw[u] = ~0u;
+          if (J.pbits && v[u] != ~0ull) {
+            const uint32_t bit = udb[u] + static_cast<uint32_t>(v[u] >> 48);
+            dw[u] = __ldg(J.pbits + (bit >> 5)) >> (bit & 31);
+          }
+        }
+        // accept rule (header comment) -> exact position key of the flip mask
+        uint32_t key[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          key[u] = kNoKey;
+          if (v[u] == ~0ull) continue;
+          const int ya = static_cast<int>(v[u] >> 32) & 0xFF, yb = static_cast<int>(v[u] >> 40) & 0xFF;
+          const int ta = utx[u] & 0xFF, tb = utx[u] >> 8;
+          const bool ea = ya == ta || ya == tb, eb = yb == ta || yb == tb;
+          if (!ea && !eb) {  // disjoint pairs: double excitation; merge two sorted pairs
+            if (!(dw[u] & 1u)) continue;
+            int p0 = ta, p1 = tb, p2 = ya, p3 = yb;
+            sort2(p0, p2);
+            sort2(p1, p3);
+            sort2(p1, p2);
+            key[u] = static_cast<uint32_t>(p0) | static_cast<uint32_t>(p1) << 8 | static_cast<uint32_t>(p2) << 16 |
+                     static_cast<uint32_t>(p3) << 24;
+          } else if (ea != eb) {  // one shared orbital o: x loses c, gains a
+            const int o = ea ? ya : yb, a = ea ? yb : ya;
+            const int cc = (o == ta) ? tb : ta;
+            if (o == (cc == pos0 ? pos1 : pos0)) {
+              int p0 = cc, p1 = a;
+              sort2(p0, p1);
+              if (J.pbits && !pbit(J.pbits, pidx(p0, p1))) continue;
+              key[u] = static_cast<uint32_t>(p0) | static_cast<uint32_t>(p1) << 8 | 0xFFFF0000u;
+            }
+          } else if (static_cast<uint32_t>(v[u]) != static_cast<uint32_t>(row)) {
+            dup = true;  // T_y = T_x in an exact bucket: the same key at another position
+          }
+        }
+        // survivors -> ring; the flip-table lookups then run 32 at a time with
+        // every lane busy (a lookup per candidate would execute on nearly every
+        // step for the ~1 in 7 candidates that survive)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const unsigned smk = __ballot_sync(0xffffffffu, key[u] != kNoKey);
+          if (key[u] != kNoKey) {
+            const uint32_t e = (s_tail + __popc(smk & ((1u << lane) - 1u))) & (kJSurv - 1);
+            sm->sy[e] = static_cast<uint32_t>(v[u]);
+            sm->sk[e] = key[u];
+          }
+          s_tail += __popc(smk);
         }
         __syncwarp();
-        emit(kJDrainAt);
+        while (s_tail - s_head >= 32) lookups();
       }
-      if (!walking) break;
+      while (s_tail != s_head) lookups();
     }
     if (!kFused) emit(1u);  // fused: the remaining hits travel in the row's last chunk with its base
 
@@ -1167,7 +1172,7 @@ __global__ void __launch_bounds__(MODE == kModeFused ? kFThreads : kThreads,
       if (H.diag_quad) {
         if (lane == 0) acc.x += side ? H.diag_A1 : H.diag_A0;
         if (lane < s) acc.x += __ldg(H.diag_b + side * n + pos);
-        for (int pi = lane; pi < n_ranges; pi += 32) acc.x += __ldg(H.diag_K + sm->ta[pi] * n + sm->tb[pi]);
+        for (int pi = lane; pi < n_ranges; pi += 32) acc.x += __ldg(H.diag_K + (sm->tab[pi] & 0xFF) * n + (sm->tab[pi] >> 8));
         for (uint32_t e = lane; e < H.n_diag_other; e += 32) {
           const uint32_t t = __ldg(H.diag_other + e);
           int pc = 0;
