@@ -51,6 +51,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None, help="0 skips the end-to-end leg")
+    ap.add_argument("--sharded", action="store_true",
+                    help="qvmc_cuda_eloc_sharded over NCCL even at one rank (run under torchrun)")
     ap.add_argument("--profile-step", action="store_true",
                     help="one extra step after warm-up inside cudaProfilerStart/Stop (for ncu --profile-from-start off)")
     return ap.parse_args()
@@ -337,11 +339,13 @@ def main():
     import torch.distributed as dist
     import paper_2408_07625_b200 as q
     from paper_2408_07625_b200 import _lib
-    from paper_2408_07625_b200.distributed import Shard, device_evaluate, shard_bounds, sharded_surrogate_energy
+    from paper_2408_07625_b200.distributed import (Communicator, Shard, device_evaluate, shard_bounds,
+                                                   sharded_surrogate_energy_capi)
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
         dist.init_process_group("nccl", device_id=dev)
 
     cfg, cm, batch, gen_s = make_inputs(args.config, args.n_unq)
@@ -362,7 +366,7 @@ def main():
     evaluate = device_evaluate(H, local)
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    if world == 1:
+    if not sharded:
         keys_d, la_d, ph_d, lp_d = shard.keys, shard.log_amps, shard.phases, shard.log_probs
         loc_d = torch.zeros(n, dtype=torch.complex128, device=dev)
         mom_d = torch.zeros(5, dtype=torch.float64, device=dev)
@@ -370,9 +374,11 @@ def main():
         def step():
             evaluate(keys_d, la_d, ph_d, lp_d, batch.log_norm, 0, n, loc_d, mom_d)
             return mom_d
-    else:
+    else:  # qvmc_cuda_eloc_sharded: all-gather, evaluation and moment merge inside libqvmc_cuda over NCCL
+        comm = Communicator.nccl(local)
+
         def step():
-            return sharded_surrogate_energy(shard, batch.log_norm, evaluate).moments
+            return sharded_surrogate_energy_capi(H, comm, local, n, shard, batch.log_norm).moments
 
     for _ in range(args.warmup):
         step()
@@ -427,7 +433,7 @@ def main():
     e2e_steps = max(3, min(args.steps, 10)) if args.e2e_steps is None else args.e2e_steps
     import ctypes as C
     pin = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(dt).pin_memory()
-    if world == 1:
+    if not sharded:
         hk, hla, hph, hlp = (pin(keys_all, torch.int64), pin(batch.log_amps, torch.float64),
                              pin(batch.phases, torch.float64), pin(batch.log_probs, torch.float64))
         hloc = torch.zeros(n, dtype=torch.complex128).pin_memory()
@@ -445,13 +451,16 @@ def main():
     else:
         hk, hla, hph, hlp = (pin(keys_all[r0:r1], torch.int64), pin(batch.log_amps[r0:r1], torch.float64),
                              pin(batch.phases[r0:r1], torch.float64), pin(batch.log_probs[r0:r1], torch.float64))
+        hloc = torch.zeros(max(r1 - r0, 1), dtype=torch.complex128).pin_memory()
+        hmom = torch.zeros(5, dtype=torch.float64).pin_memory()
+        h = H.device_handle(local)
+        _lib.check(_lib.lib().qvmc_cuda_set_stream(h, None))
 
         def e2e_step():
-            s = Shard(hk.to(dev, non_blocking=True), hla.to(dev, non_blocking=True),
-                      hph.to(dev, non_blocking=True), hlp.to(dev, non_blocking=True))
-            res = sharded_surrogate_energy(s, batch.log_norm, evaluate)
-            res.locals.cpu()
-            res.moments.cpu()
+            _lib.check(_lib.lib().qvmc_cuda_eloc_sharded(
+                h, comm._h, n, C.c_void_p(hk.data_ptr()), C.c_void_p(hla.data_ptr()), C.c_void_p(hph.data_ptr()),
+                C.c_void_p(hlp.data_ptr()), batch.log_norm, C.c_void_p(hloc.data_ptr()),
+                C.c_void_p(hmom.data_ptr()), _lib.MEM_HOST))
         h2d = (r1 - r0) * (8 * W + 24)
         d2h = (r1 - r0) * 16 + 40
     if e2e_steps:
@@ -485,12 +494,12 @@ def main():
         "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_desc(cfg, H.n_terms, H.n_xy, n) | {
-            "parallelism": f"rows sharded over {world} GPU(s); NCCL all-gather of shards + all-reduce of moments"
-            if world > 1 else "1 GPU",
+            "parallelism": f"rows sharded over {world} GPU(s): qvmc_cuda_eloc_sharded (NCCL all-gather of the "
+                           "packed shards and of the per-rank moments inside libqvmc_cuda)" if sharded else "1 GPU",
             "l2": "flushed between steps (256 MiB write outside the timed events)" if flush is not None else "not flushed"},
         "e2e": {"value": n / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "path": "qvmc_cuda_eloc_fused(QVMC_MEM_HOST) from pinned buffers" if world == 1
-                else "distributed.sharded_surrogate_energy from pinned host shards"},
+                "path": "qvmc_cuda_eloc_fused(QVMC_MEM_HOST) from pinned buffers" if not sharded
+                else "qvmc_cuda_eloc_sharded(QVMC_MEM_HOST) from pinned host shards"},
         "roofline": roof,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
@@ -512,7 +521,8 @@ def main():
             result["cpu_baseline_detail"]["full_size_run"] = full
     if rank == 0:
         print(json.dumps(result), flush=True)
-    if world > 1:
+    if sharded:
+        comm.close()
         dist.destroy_process_group()
 
 

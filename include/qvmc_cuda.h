@@ -20,6 +20,8 @@
  *                               variational_energy as run_optimisation chains
  *                               them (proj/src/optimizer.cpp:87-93), without
  *                               materialising the pairs
+ *   qvmc_cuda_eloc_sharded      the same with the samples sharded as rows over
+ *                               the ranks of a communicator
  *
  * Data layout (shared with the reference's BasisVector, basis_vector.hpp:16-26):
  * a basis vector of N qubits is n_words = ceil(N/64) uint64 words, qubit i at
@@ -188,6 +190,43 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
                          const double* phase, const double* log_prob, double log_norm, int64_t row_begin,
                          int64_t row_end, double* out_eloc, double* out_moments, int mem);
 
+/* ------------------------------------------------------------------ multi-GPU */
+
+/* Rows [begin, end) of `rank` in the contiguous balanced split of n_total rows
+ * over `world` ranks (the first n_total % world ranks hold one extra row): the
+ * shard each rank passes to qvmc_cuda_eloc_sharded. */
+int qvmc_shard_bounds(int64_t n_total, int world, int rank, int64_t* begin, int64_t* end);
+
+/* A communicator for the sharded path: NCCL over NVLink/NVSwitch (libnccl.so.2
+ * is opened at run time), or a host all-gather callback (MPI, gloo, tests).
+ * NCCL: rank 0 calls qvmc_cuda_comm_unique_id (ncclGetUniqueId, 128 bytes),
+ * the caller distributes the id, every rank calls qvmc_cuda_comm_init_nccl
+ * (ncclCommInitRank on `device`); or wrap an ncclComm_t the caller owns. */
+typedef struct qvmc_comm_s* qvmc_comm_t;
+/* all-gather bytes_per_rank bytes from every rank into recv[world][bytes_per_rank],
+ * host buffers; returns 0 on success */
+typedef int (*qvmc_host_allgather_fn)(void* ctx, const void* send, void* recv, uint64_t bytes_per_rank);
+int qvmc_cuda_comm_unique_id(void* out, uint64_t out_bytes);
+int qvmc_cuda_comm_init_nccl(int device, int world, int rank, const void* unique_id, qvmc_comm_t* out);
+int qvmc_cuda_comm_wrap_nccl(void* nccl_comm, int world, int rank, qvmc_comm_t* out);
+int qvmc_cuda_comm_init_host(int world, int rank, qvmc_host_allgather_fn all_gather, void* ctx, qvmc_comm_t* out);
+int qvmc_cuda_comm_destroy(qvmc_comm_t c);
+
+/* The sharded throughput path: find_coupled_pairs + local_energies +
+ * variational_energy as run_optimisation chains them
+ * (proj/src/optimizer.cpp:87-93), with the unique samples split over the
+ * ranks of `comm` as rows. Each rank passes its own shard
+ * (qvmc_shard_bounds rows of an n_total-row sample set: keys, log|psi|,
+ * phase, log p); the call all-gathers the shards (one all-gather of packed
+ * [W + 3]-word records), evaluates E_loc of its rows against the whole set
+ * with the fused kernels, and gathers the per-rank moments and sums them in
+ * rank order (deterministic). out_eloc: this rank's rows [rows][2];
+ * out_moments[5]: global, as qvmc_cuda_eloc_fused. With QVMC_MEM_DEVICE and
+ * the NCCL backend every step is enqueued on the handle's stream. */
+int qvmc_cuda_eloc_sharded(qvmc_ham_t h, qvmc_comm_t comm, int64_t n_total, const uint64_t* keys,
+                           const double* log_amp, const double* phase, const double* log_prob, double log_norm,
+                           double* out_eloc, double* out_moments, int mem);
+
 /* Message of the last failure on the calling thread ("" if none). */
 /* ------------------------------------------------------------------ amplitude model */
 
@@ -218,6 +257,15 @@ int qvmc_cuda_log_psi(qvmc_model_t m, int64_t n, const uint64_t* keys, int mem, 
 int qvmc_cuda_fill_amplitudes(qvmc_model_t m, int64_t n, const uint64_t* keys, const double* log_probs, int mem,
                               double* out_log_amp, double* out_phase, double* out_norm2);
 int qvmc_cuda_model_synchronize(qvmc_model_t m);
+/* sample_without_replacement (proj/src/sampler.cpp:37-102): the ancestral
+ * Gumbel top-K beam with CounterRng(seed, stream) (rng.hpp:30-63) and the
+ * iteration index, the model's conditionals evaluated on the device. Writes
+ * *out_n = min(K, sector size) distinct keys [*out_n][ceil(N/64)] and their
+ * log-probabilities in the reference's order (conditioned perturbed value
+ * descending, ties by key). out_keys / out_log_probs hold K entries, host or
+ * device memory per `mem`. Synchronises. */
+int qvmc_cuda_sample(qvmc_model_t m, int k_samples, uint64_t seed, uint32_t stream, uint32_t iteration, int mem,
+                     uint64_t* out_keys, double* out_log_probs, int64_t* out_n);
 
 const char* qvmc_cuda_last_error(void);
 /* Kernels launched by this library since load (for launch accounting). */

@@ -234,6 +234,11 @@ def rlib():
         L.qref_model_set_params.argtypes = [_P, _I64, _P]
         L.qref_model_log_psi.argtypes = [_P, _I64, _INT, _P, _INT, _P, _P]
         L.qref_fill_amplitudes.argtypes = [_P, _I64, _INT, _P, _P, _INT, _P, _P, _P]
+        L.qref_sample.argtypes = [_P, _INT, _U64, C.c_uint32, C.c_uint32, _INT, _INT, _P, _P, C.POINTER(_I64)]
+        L.qref_condition_max.restype = C.c_double
+        L.qref_condition_max.argtypes = [C.c_double] * 3
+        L.qref_gumbel.restype = C.c_double
+        L.qref_gumbel.argtypes = [_U64] + [C.c_uint32] * 5
         _rlib = L
     return _rlib
 
@@ -455,3 +460,20 @@ class RefModel:
         _rcheck(rlib().qref_fill_amplitudes(self._h, n, self.W, _ptr(keys), _ptr(lp), threads, _ptr(la), _ptr(ph),
                                             _ptr(out2)))
         return la, ph, float(out2[0]), float(out2[1])
+
+    def sample(self, k_samples: int, seed: int, stream: int = 0, iteration: int = 0, threads: int = 1):
+        """sample_without_replacement (sampler.cpp:37-102): (keys [n][W], log_probs [n])."""
+        keys = np.zeros((k_samples, self.W), dtype=np.uint64)
+        lp = np.zeros(k_samples)
+        n = C.c_int64()
+        _rcheck(rlib().qref_sample(self._h, k_samples, seed, stream, iteration, threads, self.W, _ptr(keys), _ptr(lp),
+                                   C.byref(n)))
+        return keys[: n.value], lp[: n.value]
+
+
+def ref_condition_max(parent, z, child):
+    return float(rlib().qref_condition_max(parent, z, child))
+
+
+def ref_gumbel(seed, stream, c0, c1, c2, c3):
+    return float(rlib().qref_gumbel(seed, stream, c0, c1, c2, c3))

@@ -13,6 +13,10 @@ numpy restatement (fp64, vectorised over samples) of ``AnqsModel`` and
 * ``conditional``                src/model.cpp:203-252 (mean shift, log-softmax of 2*amp over allowed values)
 * ``in_sector`` / ``log_psi``    src/model.cpp:254-271
 * ``fill_amplitudes``            src/sampler.cpp:104-120
+* ``Philox4x32::block``          src/rng.cpp:15-44 (10 rounds, Weyl key bumps)
+* ``CounterRng::gumbel``         include/qvmc/rng.hpp:38-63 (bits64 -> 53-bit uniform, clamp, -log(-log u))
+* ``condition_max``              src/sampler.cpp:15-23
+* ``sample_without_replacement`` src/sampler.cpp:37-102 (ancestral Gumbel top-K beam, ChildLess order)
 
 It is pinned against the reference itself (``oracle/_ref``, model.cpp and
 sampler.cpp compiled with the Eigen shim) by tests/test_model.py. Only tests/,
@@ -129,3 +133,112 @@ class ModelOracle:
         mx = lp.max()
         log_norm = mx + np.log(np.exp(lp - mx).sum())
         return la, ph, float(np.exp(log_norm)), float(log_norm)
+
+
+# ---------------------------------------------------------------- sampler restatement
+
+_M0, _M1, _W0, _W1 = 0xD2511F53, 0xCD9E8D57, 0x9E3779B9, 0xBB67AE85
+_U32 = 0xFFFFFFFF
+
+
+def philox4x32(counter, key):
+    """Philox4x32::block (rng.cpp:15-44): 10 rounds, key bumped by the Weyl constants."""
+    c = list(counter)
+    k0, k1 = key
+    for r in range(10):
+        if r:
+            k0 = (k0 + _W0) & _U32
+            k1 = (k1 + _W1) & _U32
+        p0 = _M0 * c[0]
+        p1 = _M1 * c[2]
+        hi0, lo0, hi1, lo1 = p0 >> 32, p0 & _U32, p1 >> 32, p1 & _U32
+        c = [hi1 ^ c[1] ^ k0, lo1, hi0 ^ c[3] ^ k1, lo0]
+    return c
+
+
+def counter_gumbel(seed, stream, c0, c1, c2, c3):
+    """CounterRng(seed, stream).gumbel(c0..c3) (rng.hpp:38-63)."""
+    key = (seed & _U32, ((seed >> 32) & _U32) ^ stream)
+    out = philox4x32((c0, c1, c2, c3), key)
+    b = (out[1] << 32) | out[0]
+    u = (b >> 11) * 2.0 ** -53
+    u = 1e-300 if u < 1e-300 else (1.0 - 1e-16 if u > 1.0 - 1e-16 else u)
+    return -np.log(-np.log(u))
+
+
+def condition_max(parent, z, child):
+    """condition_max (sampler.cpp:15-23)."""
+    if child == z:
+        return parent
+    m = max(-parent, -child)
+    v = np.exp(-parent - m) - np.exp(-z - m) + np.exp(-child - m)
+    if not v > 0.0:
+        return parent
+    return min(-(m + np.log(v)), parent)
+
+
+def _key_tuple(k):
+    return tuple(int(w) for w in k)  # BasisVector operator< = std::array words_ order (basis_vector.hpp:109-111)
+
+
+def _deposit(key, offset, count, value):
+    """deposit_bits (basis_vector.cpp:47-50): qubit offset+t <- bit count-1-t of value."""
+    out = np.array(key, dtype=np.uint64)
+    for t in range(count):
+        q = offset + t
+        bit = (value >> (count - 1 - t)) & 1
+        w, b = q // 64, np.uint64(q % 64)
+        if bit:
+            out[w] |= np.uint64(1) << b
+        else:
+            out[w] &= ~(np.uint64(1) << b)
+    return out
+
+
+
+def conditional_log_probs(model: "ModelOracle", prefixes, j):
+    """conditional(prefix, j).log_prob (model.cpp:203-252) for a batch of prefixes: [N][2^k], -inf if disallowed."""
+    prefixes = np.ascontiguousarray(prefixes, dtype=np.uint64)
+    N = prefixes.shape[0]
+    bits = np.unpackbits(prefixes.view(np.uint8).reshape(N, -1), axis=1, bitorder="little")[:, :model.n].astype(np.int64)
+    o = model.offsets[j]
+    e = np.zeros((N, model.n))
+    e[:, :o] = np.where(bits[:, :o] == 1, 1.0, -1.0)
+    amp = ModelOracle._mlp(model.blocks[j][0], e)
+    amp = amp - amp.mean(axis=1, keepdims=True)
+    ok = model.allowed(j, bits[:, :o].sum(1), bits[:, 0:o:2].sum(1))
+    if not ok.any(axis=1).all():
+        raise RuntimeError("AnqsModel::conditional: unreachable prefix")
+    two = np.where(ok, 2.0 * amp, -np.inf)
+    mx = two.max(axis=1)
+    lse = mx + np.log(np.where(ok, np.exp(two - mx[:, None]), 0.0).sum(1))
+    return np.where(ok, two - lse[:, None], -np.inf)
+
+
+def sample_without_replacement(model: "ModelOracle", k_samples, seed, stream=0, iteration=0):
+    """sample_without_replacement (sampler.cpp:37-102): (keys [n][W], log_probs [n]) in ChildLess order."""
+    if k_samples < 1:
+        raise ValueError("sample_without_replacement: K must be >= 1")
+    W = (model.n + 63) // 64
+    beam = [(np.zeros(W, dtype=np.uint64), 0.0, 0.0)]  # (prefix, log_prob, perturbed)
+    for level, (off, k) in enumerate(zip(model.offsets, model.sizes)):
+        cond = conditional_log_probs(model, np.stack([b[0] for b in beam]), level)
+        children = []
+        for b, (prefix, lp, pert) in enumerate(beam):
+            out = []
+            z = -np.inf
+            for v in range(1 << k):
+                if cond[b, v] == -np.inf:
+                    continue
+                clp = lp + cond[b, v]
+                u = clp + counter_gumbel(seed, stream, iteration, level, b, v)
+                z = max(z, u)
+                out.append([_deposit(prefix, off, k, v), clp, u])
+            for c in out:
+                c[2] = condition_max(pert, z, c[2])
+            children += out
+        if not children:
+            raise RuntimeError("sample_without_replacement: empty sector")
+        children.sort(key=lambda c: (-c[2], _key_tuple(c[0])))  # ChildLess (sampler.cpp:27-33)
+        beam = [tuple(c) for c in children[:k_samples]]
+    return np.stack([b[0] for b in beam]), np.array([b[1] for b in beam])

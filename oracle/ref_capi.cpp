@@ -538,4 +538,26 @@ int qref_fill_amplitudes(void* m, std::int64_t n, int n_words, const std::uint64
   });
 }
 
+// sample_without_replacement (sampler.cpp:37-102), unmodified: CounterRng(seed,
+// stream), iteration; out_keys [K][n_words], out_log_probs [K]; *out_n = size
+int qref_sample(void* m, int k_samples, std::uint64_t seed, std::uint32_t stream, std::uint32_t iteration,
+                int threads, int n_words, std::uint64_t* out_keys, double* out_log_probs, std::int64_t* out_n) {
+  return guarded([&] {
+    const auto& model = *static_cast<qvmc::AnqsModel*>(m);
+    const qvmc::CounterRng rng(seed, stream);
+    const qvmc::SampleBatch b = qvmc::sample_without_replacement(model, k_samples, rng, iteration, threads);
+    for (int i = 0; i < b.size(); ++i) {
+      read_words(b.vectors[static_cast<std::size_t>(i)], out_keys + static_cast<std::int64_t>(i) * n_words, n_words);
+      out_log_probs[i] = b.log_probs[i];
+    }
+    *out_n = b.size();
+  });
+}
+// condition_max (sampler.cpp:15-23) and CounterRng::gumbel (rng.hpp) for the restatement's pins
+double qref_condition_max(double parent, double z, double child) { return qvmc::condition_max(parent, z, child); }
+double qref_gumbel(std::uint64_t seed, std::uint32_t stream, std::uint32_t c0, std::uint32_t c1, std::uint32_t c2,
+                   std::uint32_t c3) {
+  return qvmc::CounterRng(seed, stream).gumbel(c0, c1, c2, c3);
+}
+
 }  // extern "C"

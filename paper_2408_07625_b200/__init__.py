@@ -14,10 +14,11 @@ from .coupling import (CoupledPairs, CouplingBackend, CouplingOptions, backend_n
 from .energy import (EnergyReport, SampleBatch, last_stats, local_energies, normalise, surrogate_energy,
                      variational_energy)
 from .hamiltonian import HamiltonianIndex, encode_strings
-from .model import AnqsModel, QuditLayout, SectorConstraint, fill_amplitudes, load_checkpoint
+from .model import (AnqsModel, CounterRng, QuditLayout, SectorConstraint, fill_amplitudes, load_checkpoint,
+                    sample_without_replacement)
 
 __all__ = [
-    "basis", "QvmcLogicError", "launch_count", "CoupledPairs", "CouplingBackend", "CouplingOptions",
+    "basis", "CounterRng", "sample_without_replacement", "QvmcLogicError", "launch_count", "CoupledPairs", "CouplingBackend", "CouplingOptions",
     "backend_name", "find_coupled_pairs", "loop_over_batch", "loop_over_terms", "loop_over_trie", "parse_backend",
     "EnergyReport", "SampleBatch", "last_stats", "local_energies", "normalise", "surrogate_energy",
     "variational_energy", "HamiltonianIndex", "encode_strings", "AnqsModel", "QuditLayout", "SectorConstraint",

@@ -77,6 +77,13 @@ SIGNATURES = [
     ("qvmc_cuda_local_energies", _INT, [_P, _I64, _P, _P, _P, _U64, _P, _P, _INT]),
     ("qvmc_cuda_energy_moments", _INT, [_P, _I64, _P, C.c_double, _P, _P, _P, _INT]),
     ("qvmc_cuda_eloc_fused", _INT, [_P, _I64, _P, _P, _P, _P, C.c_double, _I64, _I64, _P, _P, _INT]),
+    ("qvmc_shard_bounds", _INT, [_I64, _INT, _INT, C.POINTER(_I64), C.POINTER(_I64)]),
+    ("qvmc_cuda_comm_unique_id", _INT, [_P, _U64]),
+    ("qvmc_cuda_comm_init_nccl", _INT, [_INT, _INT, _INT, _P, C.POINTER(_P)]),
+    ("qvmc_cuda_comm_wrap_nccl", _INT, [_P, _INT, _INT, C.POINTER(_P)]),
+    ("qvmc_cuda_comm_init_host", _INT, [_INT, _INT, _P, _P, C.POINTER(_P)]),
+    ("qvmc_cuda_comm_destroy", _INT, [_P]),
+    ("qvmc_cuda_eloc_sharded", _INT, [_P, _P, _I64, _P, _P, _P, _P, C.c_double, _P, _P, _INT]),
     ("qvmc_cuda_last_error", C.c_char_p, []),
     ("qvmc_cuda_launch_count", _U64, []),
     ("qvmc_cuda_model_create", _INT, [_INT, _INT, _INT, _INT, _INT, _INT, C.POINTER(_P)]),
@@ -87,6 +94,7 @@ SIGNATURES = [
     ("qvmc_cuda_log_psi", _INT, [_P, _I64, _P, _INT, _P, _P]),
     ("qvmc_cuda_fill_amplitudes", _INT, [_P, _I64, _P, _P, _INT, _P, _P, _P]),
     ("qvmc_cuda_model_synchronize", _INT, [_P]),
+    ("qvmc_cuda_sample", _INT, [_P, _INT, _U64, C.c_uint32, C.c_uint32, _INT, _P, _P, C.POINTER(_I64)]),
 ]
 
 _lib = None
@@ -127,6 +135,10 @@ def check(status: int) -> None:
     if status == QVMC_ERR_NO_DEVICE:
         raise RuntimeError(f"no B200 device: {msg}")
     raise RuntimeError(msg)
+
+
+# qvmc_host_allgather_fn (include/qvmc_cuda.h)
+HOST_ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
 
 
 def launch_count() -> int:

@@ -22,10 +22,12 @@
 #include <vector>
 
 #include "host_index.h"
+#include "qvmc_comm.cuh"
 #include "qvmc_cuda.h"
 #include "qvmc_join.cuh"
 #include "qvmc_kernels.cuh"
 #include "qvmc_model.cuh"
+#include "qvmc_sampler.cuh"
 
 using namespace qvmc_b200;
 
@@ -116,6 +118,54 @@ struct qvmc_index_s {
   HostIndex idx;
 };
 
+struct qvmc_comm_s {
+  int world = 1, rank = 0;
+  ncclComm_t nccl = nullptr;
+  bool owns = false;                      // created here (destroyed with the comm)
+  qvmc_host_allgather_fn host_ag = nullptr;  // host backend
+  void* ctx = nullptr;
+  void* hsend = nullptr;                  // pinned staging of the host backend
+  void* hrecv = nullptr;
+  size_t hsend_bytes = 0, hrecv_bytes = 0;
+};
+
+namespace {
+
+void nccl_ck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(QVMC_ERR_RUNTIME, std::string(what) + ": " + nccl_api().GetErrorString(r));
+}
+
+const NcclApi& nccl_or_fail() {
+  const NcclApi& a = nccl_api();
+  if (a.error) fail(QVMC_ERR_RUNTIME, a.error);
+  return a;
+}
+
+void pinned_ensure(void*& p, size_t& have, size_t want) {
+  if (want <= have) return;
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  have = 0;
+  ck(cudaMallocHost(&p, want), "cudaMallocHost");
+  have = want;
+}
+
+// all-gather `bytes` per rank (multiple of 8) from device send to device recv on `stream`
+void comm_all_gather(qvmc_comm_s* c, const void* send, void* recv, size_t bytes, cudaStream_t stream) {
+  if (c->nccl) {
+    nccl_ck(nccl_api().AllGather(send, recv, bytes / 8, ncclUint64, c->nccl, stream), "ncclAllGather");
+    return;
+  }
+  pinned_ensure(c->hsend, c->hsend_bytes, std::max<size_t>(bytes, 8));
+  pinned_ensure(c->hrecv, c->hrecv_bytes, std::max<size_t>(bytes * c->world, 8));
+  if (bytes) ck(cudaMemcpyAsync(c->hsend, send, bytes, cudaMemcpyDeviceToHost, stream), "D2H shard");
+  ck(cudaStreamSynchronize(stream), "sync");
+  if (c->host_ag(c->ctx, c->hsend, c->hrecv, bytes) != 0) fail(QVMC_ERR_RUNTIME, "host all-gather callback failed");
+  if (bytes) ck(cudaMemcpyAsync(recv, c->hrecv, bytes * c->world, cudaMemcpyHostToDevice, stream), "H2D gathered");
+}
+
+}  // namespace
+
 struct qvmc_ham_s {
   int device = 0;
   int n = 0, W = 0;
@@ -157,6 +207,7 @@ struct qvmc_ham_s {
   // workspace
   DBuf tab, ctl, keys, la, ph, lp, eloc, partials, moments, weights;
   DBuf counts, row_off, xp_a, g_a, xp_b, g_b, entries, cub_tmp, in_entries, out_h, out_class;
+  DBuf s_keys, s_la, s_ph, s_lp, g_send, g_recv, g_keys, g_la, g_ph, g_lp, g_mom, g_moms;  // sharded calls
   uint64_t tab_buckets = 0;
   uint64_t n_pairs = 0;
   int64_t pairs_rows = 0;
@@ -1709,6 +1760,154 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
   });
 }
 
+// ------------------------------------------------------------------ sharded path
+
+int qvmc_shard_bounds(int64_t n_total, int world, int rank, int64_t* begin, int64_t* end) {
+  return guarded([&] {
+    if (n_total < 0 || world < 1 || rank < 0 || rank >= world) fail(QVMC_ERR_INVALID_ARGUMENT, "bad shard request");
+    int64_t b, e;
+    shard_range(n_total, world, rank, b, e);
+    if (begin) *begin = b;
+    if (end) *end = e;
+  });
+}
+
+int qvmc_cuda_comm_unique_id(void* out, uint64_t out_bytes) {
+  return guarded([&] {
+    if (!out || out_bytes < sizeof(ncclUniqueId)) fail(QVMC_ERR_INVALID_ARGUMENT, "unique id buffer < 128 bytes");
+    ncclUniqueId id;
+    nccl_ck(nccl_or_fail().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+int qvmc_cuda_comm_init_nccl(int device, int world, int rank, const void* unique_id, qvmc_comm_t* out) {
+  return guarded([&] {
+    if (!out || !unique_id) fail(QVMC_ERR_INVALID_ARGUMENT, "null argument");
+    if (world < 1 || rank < 0 || rank >= world) fail(QVMC_ERR_INVALID_ARGUMENT, "bad world/rank");
+    const NcclApi& a = nccl_or_fail();
+    DeviceGuard dg(device);
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    auto c = std::make_unique<qvmc_comm_s>();
+    c->world = world;
+    c->rank = rank;
+    nccl_ck(a.CommInitRank(&c->nccl, world, id, rank), "ncclCommInitRank");
+    c->owns = true;
+    *out = c.release();
+  });
+}
+
+int qvmc_cuda_comm_wrap_nccl(void* nccl_comm, int world, int rank, qvmc_comm_t* out) {
+  return guarded([&] {
+    if (!out || !nccl_comm) fail(QVMC_ERR_INVALID_ARGUMENT, "null argument");
+    if (world < 1 || rank < 0 || rank >= world) fail(QVMC_ERR_INVALID_ARGUMENT, "bad world/rank");
+    nccl_or_fail();
+    auto c = std::make_unique<qvmc_comm_s>();
+    c->world = world;
+    c->rank = rank;
+    c->nccl = static_cast<ncclComm_t>(nccl_comm);
+    *out = c.release();
+  });
+}
+
+int qvmc_cuda_comm_init_host(int world, int rank, qvmc_host_allgather_fn all_gather, void* ctx, qvmc_comm_t* out) {
+  return guarded([&] {
+    if (!out || !all_gather) fail(QVMC_ERR_INVALID_ARGUMENT, "null argument");
+    if (world < 1 || rank < 0 || rank >= world) fail(QVMC_ERR_INVALID_ARGUMENT, "bad world/rank");
+    auto c = std::make_unique<qvmc_comm_s>();
+    c->world = world;
+    c->rank = rank;
+    c->host_ag = all_gather;
+    c->ctx = ctx;
+    *out = c.release();
+  });
+}
+
+int qvmc_cuda_comm_destroy(qvmc_comm_t c) {
+  return guarded([&] {
+    if (!c) return;
+    std::unique_ptr<qvmc_comm_s> own(c);
+    if (c->hsend) cudaFreeHost(c->hsend);
+    if (c->hrecv) cudaFreeHost(c->hrecv);
+    if (c->owns && c->nccl) nccl_ck(nccl_api().CommDestroy(c->nccl), "ncclCommDestroy");
+  });
+}
+
+int qvmc_cuda_eloc_sharded(qvmc_ham_t h, qvmc_comm_t comm, int64_t n_total, const uint64_t* keys,
+                           const double* log_amp, const double* phase, const double* log_prob, double log_norm,
+                           double* out_eloc, double* out_moments, int mem) {
+  return guarded([&] {
+    check_handle(h);
+    check_mem(mem);
+    if (!comm) fail(QVMC_ERR_INVALID_ARGUMENT, "null communicator");
+    if (n_total < 0 || n_total >= 0xFFFFFFFFll) fail(QVMC_ERR_INVALID_ARGUMENT, "n_unq out of range");
+    const int world = comm->world, rank = comm->rank;
+    int64_t r0, r1;
+    shard_range(n_total, world, rank, r0, r1);
+    const int64_t rows = r1 - r0;
+    const int64_t max_rows = (n_total + world - 1) / world;
+    if (rows > 0 && (!keys || !log_amp || !phase)) fail(QVMC_ERR_INVALID_ARGUMENT, "null sample arrays");
+    if (out_moments && n_total > 0 && !log_prob) fail(QVMC_ERR_INVALID_ARGUMENT, "moments need log_prob");
+    DeviceGuard dg(h->device);
+    const int W = h->W;
+    const uint64_t* dk = stage(h, h->s_keys, keys, static_cast<size_t>(rows) * W, mem);
+    const double* dla = stage(h, h->s_la, log_amp, rows, mem);
+    const double* dph = stage(h, h->s_ph, phase, rows, mem);
+    const double* dlp = log_prob ? stage(h, h->s_lp, log_prob, rows, mem) : nullptr;
+    const size_t rec = static_cast<size_t>(W + 3) * 8;
+    const size_t block = std::max<size_t>(static_cast<size_t>(max_rows) * rec, 8);
+    h->g_send.ensure(block + 16);
+    h->g_recv.ensure(block * world + 16);
+    const int pgrid = static_cast<int>(std::min<int64_t>((std::max<int64_t>(rows, 1) + kThreads - 1) / kThreads,
+                                                         grid_for(h, 8)));
+    if (rows > 0) {
+      DISPATCH_W(W, (k_pack_shard<WW><<<pgrid, kThreads, 0, h->stream>>>(dk, dla, dph, dlp, rows,
+                                                                         h->g_send.as<uint64_t>())));
+      ck_launch("pack shard");
+    }
+    comm_all_gather(comm, h->g_send.p, h->g_recv.p, block, h->stream);
+    h->g_keys.ensure(static_cast<size_t>(n_total) * W * 8 + 16);
+    h->g_la.ensure(static_cast<size_t>(n_total) * 8 + 16);
+    h->g_ph.ensure(static_cast<size_t>(n_total) * 8 + 16);
+    h->g_lp.ensure(static_cast<size_t>(n_total) * 8 + 16);
+    if (n_total > 0) {
+      const int ugrid = static_cast<int>(std::min<int64_t>((n_total + kThreads - 1) / kThreads, grid_for(h, 8)));
+      DISPATCH_W(W, (k_unpack_shards<WW><<<ugrid, kThreads, 0, h->stream>>>(
+                        h->g_recv.as<uint64_t>(), world, max_rows, n_total, h->g_keys.as<uint64_t>(),
+                        h->g_la.as<double>(), h->g_ph.as<double>(), h->g_lp.as<double>())));
+      ck_launch("unpack shards");
+    }
+    // E_loc of this rank's rows against the gathered set + its moments
+    double* deloc = (mem == QVMC_MEM_DEVICE) ? out_eloc : nullptr;
+    h->g_mom.ensure(8 * sizeof(double));
+    ck(cudaMemsetAsync(h->g_mom.p, 0, 8 * sizeof(double), h->stream), "memset moments");
+    const int st = qvmc_cuda_eloc_fused(h, n_total, h->g_keys.as<uint64_t>(), h->g_la.as<double>(),
+                                        h->g_ph.as<double>(), log_prob ? h->g_lp.as<double>() : nullptr, log_norm,
+                                        r0, r1, deloc, out_moments ? h->g_mom.as<double>() : nullptr,
+                                        QVMC_MEM_DEVICE);
+    if (st != QVMC_OK) fail(st, g_error);
+    if (out_moments) {  // per-rank moments gathered, summed in rank order
+      h->g_moms.ensure(static_cast<size_t>(world) * 8 * sizeof(double) + 16);
+      comm_all_gather(comm, h->g_mom.p, h->g_moms.p, 8 * sizeof(double), h->stream);
+      double* dm = out_moments;
+      if (mem == QVMC_MEM_HOST) {
+        h->moments.ensure(8 * sizeof(double));
+        dm = h->moments.as<double>();
+      }
+      k_sum_rank_moments<<<1, 32, 0, h->stream>>>(h->g_moms.as<double>(), world, dm);
+      ck_launch("rank moments");
+      if (mem == QVMC_MEM_HOST)
+        ck(cudaMemcpyAsync(out_moments, dm, 5 * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "D2H");
+    }
+    if (mem == QVMC_MEM_HOST) {
+      if (out_eloc && rows)
+        ck(cudaMemcpyAsync(out_eloc, h->eloc.p, rows * 16, cudaMemcpyDeviceToHost, h->stream), "D2H eloc");
+      finish(h);
+    }
+  });
+}
+
 // ------------------------------------------------------------------ amplitude model
 // AnqsModel (model.cpp) on the device: layout + sector checks as in the
 // reference constructor (model.cpp:33-45, :47-97), parameters re-laid out per
@@ -1724,6 +1923,8 @@ struct qvmc_model_s {
   int sms = 148;
   cudaStream_t own = nullptr, stream = nullptr;
   DBuf P, keys, la, ph, lp, part, out2, lse;
+  // sampler (sample_without_replacement): two beams, the conditional table, candidates
+  DBuf bk[2], blp[2], bpert[2], cond, c_key, c_key2, c_slot, c_slot2, c_bv, c_lp, c_pert, c_count, c_tmp;
 };
 
 namespace {
@@ -1904,6 +2105,109 @@ int qvmc_cuda_model_set_params(qvmc_model_t m, int64_t n_params, const double* p
     ck(cudaMemcpyAsync(m->P.p, dev.data(), dev.size() * sizeof(double), cudaMemcpyHostToDevice, m->stream), "H2D params");
     ck(cudaStreamSynchronize(m->stream), "sync");  // the host staging vector goes out of scope
     m->has_params = true;
+  });
+}
+
+// sample_without_replacement (sampler.cpp:37-102) on the device; see
+// qvmc_sampler.cuh. Returns the batch size; the keys and log-probabilities are
+// in the reference's ChildLess order.
+int qvmc_cuda_sample(qvmc_model_t m, int k_samples, uint64_t seed, uint32_t stream, uint32_t iteration, int mem,
+                     uint64_t* out_keys, double* out_log_probs, int64_t* out_n) {
+  return guarded([&] {
+    check_model(m);
+    check_mem(mem);
+    if (k_samples < 1) fail(QVMC_ERR_INVALID_ARGUMENT, "sample_without_replacement: K must be >= 1");
+    if (k_samples > (1 << 25)) fail(QVMC_ERR_INVALID_ARGUMENT, "sample_without_replacement: K above 2^25");
+    if (!out_keys || !out_log_probs || !out_n) fail(QVMC_ERR_INVALID_ARGUMENT, "null output");
+    if (!m->has_params) fail(QVMC_ERR_INVALID_ARGUMENT, "model parameters not set");
+    using namespace qvmc_model;
+    using namespace qvmc_sampler;
+    DeviceGuard dg(m->device);
+    const int W = m->W;
+    const int64_t K = k_samples;
+    const size_t maxc = static_cast<size_t>(K) * 64;
+    for (int i = 0; i < 2; ++i) {
+      m->bk[i].ensure(K * W * 8 + 16);
+      m->blp[i].ensure(K * 8 + 16);
+      m->bpert[i].ensure(K * 8 + 16);
+    }
+    m->cond.ensure(K * 64 * 8 + 16);
+    m->c_key.ensure(maxc * 8 + 16);
+    m->c_key2.ensure(maxc * 8 + 16);
+    m->c_slot.ensure(maxc * 4 + 16);
+    m->c_slot2.ensure(maxc * 4 + 16);
+    m->c_bv.ensure(maxc * 4 + 16);
+    m->c_lp.ensure(maxc * 8 + 16);
+    m->c_pert.ensure(maxc * 8 + 16);
+    m->c_count.ensure(16);
+    // root: the empty prefix, log p = 0, perturbed = 0 (sampler.cpp:45-46)
+    ck(cudaMemsetAsync(m->bk[0].p, 0, W * 8, m->stream), "memset");
+    ck(cudaMemsetAsync(m->blp[0].p, 0, 8, m->stream), "memset");
+    ck(cudaMemsetAsync(m->bpert[0].p, 0, 8, m->stream), "memset");
+    int cur = 0;
+    int64_t B = 1;
+    ModelView V{m->P.as<double>(), m->n, m->n_qudits, m->bits, m->n_e, m->spin, m->n_up};
+    Candidates Cd{m->c_key.as<uint64_t>(), m->c_slot.as<uint32_t>(), m->c_bv.as<uint32_t>(), m->c_lp.as<double>(),
+                  m->c_pert.as<double>(), m->c_count.as<unsigned long long>()};
+    for (int level = 0; level < m->n_qudits; ++level) {
+      const int off = level * m->bits, k = std::min(m->bits, m->n - off);
+      // 1. conditional log-probabilities of every beam prefix (amplitude head of this qudit)
+      const int64_t per = static_cast<int64_t>(kWT) * kPWarps;
+      const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>((B + per - 1) / per, 4 * m->sms));
+      int64_t chunk = (B + chunks - 1) / chunks;
+      chunk = (chunk + kWT - 1) / kWT * kWT;
+      const int64_t S = (B + chunk - 1) / chunk;
+      DISPATCH_W(W, {
+        const size_t dyn = (8448 + kPWarps * 64 * kWT) * sizeof(double) + kPWarps * kWT * WW * sizeof(uint64_t);
+        ck(cudaFuncSetAttribute(k_log_psi_part<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(dyn)), "smem attribute");
+        k_log_psi_part<WW><<<static_cast<unsigned>(S), kPThreads, dyn, m->stream>>>(
+            V, m->bk[cur].as<uint64_t>(), B, chunk, nullptr, level, m->cond.as<double>());
+        ck_launch("sampler conditional");
+      });
+      // 2. children + Gumbel + condition_max
+      ck(cudaMemsetAsync(m->c_count.p, 0, 8, m->stream), "memset");
+      const int eg = static_cast<int>(std::min<int64_t>((B * 32 + 255) / 256, 8LL * m->sms));
+      k_expand<<<std::max(eg, 1), 256, 0, m->stream>>>(m->cond.as<double>(), m->blp[cur].as<double>(),
+                                                        m->bpert[cur].as<double>(), B, 1 << k, seed, stream,
+                                                        iteration, static_cast<uint32_t>(level), Cd);
+      ck_launch("sampler expand");
+      unsigned long long nc = 0;
+      ck(cudaMemcpyAsync(&nc, m->c_count.p, 8, cudaMemcpyDeviceToHost, m->stream), "D2H count");
+      ck(cudaStreamSynchronize(m->stream), "sync");
+      if (nc == 0) fail(QVMC_ERR_RUNTIME, "sample_without_replacement: empty sector");
+      // 3. ChildLess order: conditioned value descending, ties by child prefix
+      const int n = static_cast<int>(nc);
+      size_t tb = 0;
+      ck(cub::DeviceRadixSort::SortPairs(nullptr, tb, m->c_key.as<uint64_t>(), m->c_key2.as<uint64_t>(),
+                                         m->c_slot.as<uint32_t>(), m->c_slot2.as<uint32_t>(), n, 0, 64, m->stream),
+         "sort size");
+      m->c_tmp.ensure(tb + 16);
+      ck(cub::DeviceRadixSort::SortPairs(m->c_tmp.p, tb, m->c_key.as<uint64_t>(), m->c_key2.as<uint64_t>(),
+                                         m->c_slot.as<uint32_t>(), m->c_slot2.as<uint32_t>(), n, 0, 64, m->stream),
+         "sort");
+      ++g_launches;
+      const int64_t keep = std::min<int64_t>(K, n);
+      const int tg = static_cast<int>(std::min<int64_t>((keep + 255) / 256, 8LL * m->sms));
+      DISPATCH_W(W, {
+        k_ties<WW><<<std::max(tg, 1), 256, 0, m->stream>>>(m->c_key2.as<uint64_t>(), m->c_slot2.as<uint32_t>(), n,
+                                                          keep, m->c_bv.as<uint32_t>(), m->bk[cur].as<uint64_t>(),
+                                                          off, k);
+        ck_launch("sampler ties");
+        // 4. the next beam
+        k_gather_beam<WW><<<std::max(tg, 1), 256, 0, m->stream>>>(
+            m->c_slot2.as<uint32_t>(), keep, Cd, m->bk[cur].as<uint64_t>(), off, k, m->bk[1 - cur].as<uint64_t>(),
+            m->blp[1 - cur].as<double>(), m->bpert[1 - cur].as<double>());
+        ck_launch("sampler gather");
+      });
+      cur = 1 - cur;
+      B = keep;
+    }
+    const cudaMemcpyKind kind = mem == QVMC_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    ck(cudaMemcpyAsync(out_keys, m->bk[cur].p, B * W * 8, kind, m->stream), "copy keys");
+    ck(cudaMemcpyAsync(out_log_probs, m->blp[cur].p, B * 8, kind, m->stream), "copy log_probs");
+    ck(cudaStreamSynchronize(m->stream), "sync");
+    *out_n = B;
   });
 }
 

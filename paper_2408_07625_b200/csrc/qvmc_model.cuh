@@ -415,7 +415,10 @@ __device__ __forceinline__ int pidx(int k, int s) {
 template <int W>
 __global__ void __launch_bounds__(kPThreads, 1)
     k_log_psi_part(const ModelView M, const uint64_t* __restrict__ keys, int64_t N, int64_t chunk,
-                   double* __restrict__ part) {
+                   double* __restrict__ part, int only_j = -1, double* __restrict__ cond = nullptr) {
+  // only_j >= 0 (the sampler, sampler.cpp:53-55): the amplitude head of qudit only_j
+  // for every key (a beam prefix), writing the whole conditional log-probability
+  // table cond[s][64] (model.cpp:226-249; -inf for disallowed values) instead of part
   extern __shared__ __align__(16) double smem[];
   double* w2 = smem;                   // [64 k][64 h]
   double* w3 = smem + 4096;            // [64 k][64 v]
@@ -423,8 +426,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
   double* acts = smem + 8448;          // [16 warps][64][16]
   uint64_t* skeys = reinterpret_cast<uint64_t*>(acts + kPWarps * 64 * kWT);  // [16 warps][16][W]
 
-  const int n_jh = 2 * M.n_qudits;
-  const int jh = static_cast<int>(blockIdx.x % n_jh), j = jh >> 1, hd = jh & 1;
+  const int n_jh = only_j >= 0 ? 1 : 2 * M.n_qudits;
+  const int jh = only_j >= 0 ? 2 * only_j : static_cast<int>(blockIdx.x % n_jh), j = jh >> 1, hd = jh & 1;
   const int64_t c0 = static_cast<int64_t>(blockIdx.x / n_jh) * chunk;
   const int64_t c1 = min(N, c0 + chunk);
   const BlockLayout L{M.n};
@@ -641,6 +644,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
       for (int o = 4; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
       const int v = val[si];
       const int64_t g = t0 + sq * 4 + si;
+      if (cond) {  // sampler: every value's log-probability (model.cpp:236-247)
+        if (g < c1) {
+          const double lse = mx + log(se);
+#pragma unroll
+          for (int f = 0; f < 8; ++f)
+            cond[g * 64 + 16 * (f >> 1) + 2 * hq + (f & 1)] = (okm >> f & 1u) ? acc[si][f] - lse : -CUDART_INF;
+        }
+        continue;
+      }
       if (((v >> 1) & 7) == hq && g < c1) {  // the lane holding out[v]
         const int fv = 2 * (v >> 4) + (v & 1);
         double tv = acc[si][0];

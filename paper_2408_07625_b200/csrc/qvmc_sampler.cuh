@@ -1,0 +1,196 @@
+// Exact autoregressive sampling without replacement on the device: the
+// ancestral Gumbel top-K beam of sample_without_replacement
+// (/root/reference/proj/src/sampler.cpp:37-102), so the sampled keys never
+// leave HBM between sampling, amplitudes and the local energies (SURVEY §8f
+// item 3).
+//
+// Per qudit level (host loop, one level at a time):
+//   1. k_log_psi_part(only_j = level, cond): the amplitude head's conditional
+//      log-probability table of every beam prefix (model.cpp:203-252);
+//   2. k_expand: one warp per beam entry b. Each allowed child value v gets
+//      log p = parent + cond[b][v] and the Gumbel draw of the counter
+//      (iteration, level, b, v) (Philox4x32-10, rng.cpp / rng.hpp), the
+//      warp max z, then condition_max (sampler.cpp:15-23); children are
+//      appended to the candidate list (warp-aggregated atomics);
+//   3. CUB radix sort of the candidates by conditioned value, descending;
+//      runs of equal values (rare) are ordered by child prefix (k_ties) —
+//      together exactly ChildLess (sampler.cpp:27-33);
+//   4. k_gather_beam: the first min(K, candidates) become the next beam,
+//      in that order (the beam slot b feeds the next level's counters).
+#pragma once
+
+#include <cstdint>
+
+namespace qvmc_sampler {
+
+// Philox4x32-10 (rng.cpp:15-44)
+__device__ __forceinline__ void philox(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+  }
+}
+
+// CounterRng(seed, stream).gumbel(c0, c1, c2, c3) (rng.hpp:38-63)
+__device__ __forceinline__ double counter_gumbel(uint64_t seed, uint32_t stream, uint32_t c0, uint32_t c1,
+                                                 uint32_t c2, uint32_t c3) {
+  uint32_t c[4] = {c0, c1, c2, c3};
+  philox(c, static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32) ^ stream);
+  const uint64_t b = (static_cast<uint64_t>(c[1]) << 32) | c[0];
+  double u = static_cast<double>(b >> 11) * 0x1.0p-53;
+  if (u < 1e-300) u = 1e-300;
+  if (u > 1.0 - 1e-16) u = 1.0 - 1e-16;
+  return -log(-log(u));
+}
+
+// condition_max (sampler.cpp:15-23)
+__device__ __forceinline__ double condition_max(double parent, double z, double child) {
+  if (child == z) return parent;
+  const double m = fmax(-parent, -child);
+  const double v = exp(-parent - m) - exp(-z - m) + exp(-child - m);
+  if (!(v > 0.0)) return parent;
+  const double r = -(m + log(v));
+  return fmin(r, parent);
+}
+
+// sort key: ascending order of the key = descending conditioned value
+__device__ __forceinline__ uint64_t desc_key(double d) {
+  const uint64_t b = static_cast<uint64_t>(__double_as_longlong(d));
+  const uint64_t asc = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+  return ~asc;
+}
+
+struct Candidates {
+  uint64_t* key;   // desc_key(conditioned perturbed value)
+  uint32_t* slot;  // 0..n-1 (sort payload)
+  uint32_t* bv;    // beam entry << 6 | value
+  double* lp;      // child log-probability
+  double* pert;    // conditioned perturbed value
+  unsigned long long* count;
+};
+
+// one warp per beam entry (sampler.cpp:53-74)
+__global__ void __launch_bounds__(256)
+    k_expand(const double* __restrict__ cond, const double* __restrict__ beam_lp, const double* __restrict__ beam_pert,
+             int64_t B, int n_out, uint64_t seed, uint32_t stream, uint32_t iteration, uint32_t level, Candidates C) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t b = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; b < B; b += n_warps) {
+    const double plp = beam_lp[b], ppert = beam_pert[b];
+    double clp[2], u[2];
+    bool ok[2];
+    double z = -CUDART_INF;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int v = lane + 32 * h;
+      ok[h] = false;
+      clp[h] = 0.0;
+      u[h] = -CUDART_INF;
+      if (v < n_out) {
+        const double c = cond[b * 64 + v];
+        if (c != -CUDART_INF) {
+          ok[h] = true;
+          clp[h] = plp + c;
+          u[h] = clp[h] + counter_gumbel(seed, stream, iteration, level, static_cast<uint32_t>(b),
+                                         static_cast<uint32_t>(v));
+          z = fmax(z, u[h]);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) z = fmax(z, __shfl_xor_sync(0xffffffffu, z, o));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const unsigned m = __ballot_sync(0xffffffffu, ok[h]);
+      unsigned long long base = 0;
+      if (lane == 0 && m) base = atomicAdd(C.count, static_cast<unsigned long long>(__popc(m)));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (ok[h]) {
+        const uint64_t s = base + __popc(m & ((1u << lane) - 1u));
+        const double cp = condition_max(ppert, z, u[h]);
+        C.key[s] = desc_key(cp);
+        C.slot[s] = static_cast<uint32_t>(s);
+        C.bv[s] = static_cast<uint32_t>(b) << 6 | static_cast<uint32_t>(lane + 32 * h);
+        C.lp[s] = clp[h];
+        C.pert[s] = cp;
+      }
+    }
+  }
+}
+
+// child prefix: the parent's key with value v deposited at [off, off + k)
+// (deposit_bits, basis_vector.cpp:47-50: qubit off+t <- bit k-1-t of v)
+template <int W>
+__device__ __forceinline__ void child_key(const uint64_t* __restrict__ beam_keys, uint32_t bv, int off, int k,
+                                          uint64_t* out) {
+  const uint32_t b = bv >> 6, v = bv & 63u;
+#pragma unroll
+  for (int w = 0; w < W; ++w) out[w] = beam_keys[static_cast<int64_t>(b) * W + w];
+  for (int t = 0; t < k; ++t)
+    if ((v >> (k - 1 - t)) & 1u) {
+      const int q = off + t;
+      out[q >> 6] |= 1ull << (q & 63);
+    }
+}
+
+template <int W>
+__device__ __forceinline__ bool key_less(const uint64_t* a, const uint64_t* b) {  // std::array words_ order
+#pragma unroll
+  for (int w = 0; w < W; ++w)
+    if (a[w] != b[w]) return a[w] < b[w];
+  return false;
+}
+
+// runs of equal conditioned values that start inside the kept prefix [0, keep):
+// order them by child prefix (ChildLess ties, sampler.cpp:31). One thread per run.
+template <int W>
+__global__ void k_ties(const uint64_t* __restrict__ skey, uint32_t* __restrict__ sslot, int64_t n, int64_t keep,
+                       const uint32_t* __restrict__ bv, const uint64_t* __restrict__ beam_keys, int off, int k) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < keep;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (i + 1 >= n || skey[i + 1] != skey[i] || (i > 0 && skey[i - 1] == skey[i])) continue;
+    int64_t e = i + 1;
+    while (e < n && skey[e] == skey[i]) ++e;
+    for (int64_t a = i + 1; a < e; ++a) {  // insertion sort by prefix
+      const uint32_t s = sslot[a];
+      uint64_t ks[W], kb[W];
+      child_key<W>(beam_keys, bv[s], off, k, ks);
+      int64_t c = a;
+      while (c > i) {
+        child_key<W>(beam_keys, bv[sslot[c - 1]], off, k, kb);
+        if (!key_less<W>(ks, kb)) break;
+        sslot[c] = sslot[c - 1];
+        --c;
+      }
+      sslot[c] = s;
+    }
+  }
+}
+
+template <int W>
+__global__ void k_gather_beam(const uint32_t* __restrict__ sslot, int64_t keep, const Candidates C,
+                              const uint64_t* __restrict__ beam_keys, int off, int k, uint64_t* __restrict__ out_keys,
+                              double* __restrict__ out_lp, double* __restrict__ out_pert) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < keep;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t s = sslot[i];
+    uint64_t kk[W];
+    child_key<W>(beam_keys, C.bv[s], off, k, kk);
+#pragma unroll
+    for (int w = 0; w < W; ++w) out_keys[i * W + w] = kk[w];
+    out_lp[i] = C.lp[s];
+    out_pert[i] = C.pert[s];
+  }
+}
+
+}  // namespace qvmc_sampler

@@ -25,6 +25,7 @@ import math
 from dataclasses import dataclass
 from typing import Callable, List, Optional
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -118,10 +119,97 @@ def sharded_surrogate_energy(shard: Shard, log_norm: float, evaluate: Callable, 
 
 
 def shard_bounds(n: int, world: int, rank: int) -> tuple:
-    """Contiguous, balanced row shard [begin, end) of rank."""
+    """Contiguous, balanced row shard [begin, end) of rank (= qvmc_shard_bounds)."""
     base, rem = divmod(n, world)
     begin = rank * base + min(rank, rem)
     return begin, begin + base + (1 if rank < rem else 0)
+
+
+class Communicator:
+    """qvmc_comm_t: the collectives of qvmc_cuda_eloc_sharded inside libqvmc_cuda.
+
+    ``nccl(group, device)``: rank 0 draws an NCCL unique id
+    (qvmc_cuda_comm_unique_id), the process group broadcasts it, every rank
+    calls qvmc_cuda_comm_init_nccl: all-gathers run inside the library on the
+    handle's stream over NVLink. ``host(group)``: a host all-gather callback
+    over the process group (gloo works): the library stages through pinned
+    host memory. Several ranks may then share one GPU (tests)."""
+
+    def __init__(self, handle, world: int, rank: int, keepalive=None):
+        self._h = handle
+        self.world = world
+        self.rank = rank
+        self._keep = keepalive
+
+    @classmethod
+    def nccl(cls, device: int, group=None) -> "Communicator":
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        uid = (C.c_uint8 * 128)()
+        if rank == 0:
+            _lib.check(_lib.lib().qvmc_cuda_comm_unique_id(uid, 128))
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+        uid = (C.c_uint8 * 128).from_buffer_copy(box[0])
+        h = C.c_void_p()
+        _lib.check(_lib.lib().qvmc_cuda_comm_init_nccl(device, world, rank, uid, C.byref(h)))
+        return cls(h, world, rank)
+
+    @classmethod
+    def host(cls, group=None) -> "Communicator":
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+
+        def all_gather(ctx, send, recv, nbytes):
+            try:
+                src = np.ctypeslib.as_array((C.c_uint8 * max(nbytes, 1)).from_address(send))[:nbytes]
+                t = torch.from_numpy(src.copy())
+                outs = [torch.empty_like(t) for _ in range(world)]
+                dist.all_gather(outs, t, group=group)
+                dst = np.ctypeslib.as_array((C.c_uint8 * max(nbytes * world, 1)).from_address(recv))
+                dst[: nbytes * world] = torch.cat(outs).numpy()
+                return 0
+            except Exception:  # noqa: BLE001 - reported to the library as a failed collective
+                return 1
+
+        cb = _lib.HOST_ALLGATHER_FN(all_gather)
+        h = C.c_void_p()
+        _lib.check(_lib.lib().qvmc_cuda_comm_init_host(world, rank, cb, None, C.byref(h)))
+        return cls(h, world, rank, keepalive=cb)
+
+    def close(self) -> None:
+        if self._h:
+            _lib.check(_lib.lib().qvmc_cuda_comm_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def sharded_surrogate_energy_capi(index: HamiltonianIndex, comm: Communicator, device: int, n_total: int,
+                                  shard: Shard, log_norm: float) -> ShardResult:
+    """qvmc_cuda_eloc_sharded on device pointers (torch's current stream): the
+    gather, the fused evaluation of this rank's rows and the rank-order moment
+    sum all run inside libqvmc_cuda. ``shard`` = rows qvmc_shard_bounds(rank)."""
+    r0, r1 = shard_bounds(n_total, comm.world, comm.rank)
+    if shard.keys.shape[0] != r1 - r0:
+        raise ValueError(f"rank {comm.rank} holds {shard.keys.shape[0]} rows, its shard is {r1 - r0}")
+    h = index.device_handle(device)
+    L = _lib.lib()
+    dev = shard.keys.device
+    locals_ = torch.zeros(max(r1 - r0, 1), dtype=torch.complex128, device=dev)
+    moments = torch.zeros(5, dtype=torch.float64, device=dev)
+    raw = torch.cuda.current_stream(device).cuda_stream or 0x1  # 0x1 = cudaStreamLegacy
+    _lib.check(L.qvmc_cuda_set_stream(h, C.c_void_p(raw)))
+    try:
+        _lib.check(L.qvmc_cuda_eloc_sharded(
+            h, comm._h, n_total, C.c_void_p(shard.keys.data_ptr()), C.c_void_p(shard.log_amps.data_ptr()),
+            C.c_void_p(shard.phases.data_ptr()), C.c_void_p(shard.log_probs.data_ptr()), float(log_norm),
+            C.c_void_p(locals_.data_ptr()), C.c_void_p(moments.data_ptr()), _lib.MEM_DEVICE))
+    finally:
+        _lib.check(L.qvmc_cuda_set_stream(h, None))
+    return ShardResult(locals_[: r1 - r0], moments, r0, r1, n_total)
 
 
 def model_evaluate(model, device: int) -> Callable:

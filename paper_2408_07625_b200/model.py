@@ -197,3 +197,27 @@ def fill_amplitudes(batch, model: AnqsModel, threads: int = 1) -> None:
                                                     _ptr(la), _ptr(ph), _ptr(out2)))
     batch.log_amps, batch.phases = la, ph
     batch.norm, batch.log_norm = float(out2[0]), float(out2[1])
+
+
+@dataclass(frozen=True)
+class CounterRng:
+    """CounterRng (rng.hpp:30-63): the keyed Philox4x32-10 stream the sampler draws from."""
+    seed: int
+    stream: int = 0
+
+
+def sample_without_replacement(model: AnqsModel, k_samples: int, rng: CounterRng, iteration: int,
+                               threads: int = 1, device_out: bool = False):
+    """sample_without_replacement (sampler.cpp:37-102) on the device: a SampleBatch of
+    min(K, sector size) distinct keys and their log-probabilities in the reference's order
+    (log_amps / phases unfilled, as the reference leaves them for fill_amplitudes).
+    ``threads`` is accepted for signature parity and ignored."""
+    from .energy import SampleBatch
+    if k_samples < 1:
+        raise ValueError("sample_without_replacement: K must be >= 1")
+    keys = np.zeros((k_samples, model.W), dtype=np.uint64)
+    lp = np.zeros(k_samples)
+    n = C.c_int64()
+    _lib.check(_lib.lib().qvmc_cuda_sample(model._h, k_samples, rng.seed, rng.stream, iteration, _lib.MEM_HOST,
+                                           _ptr(keys), _ptr(lp), C.byref(n)))
+    return SampleBatch(keys[: n.value], lp[: n.value], np.zeros(0), np.zeros(0))

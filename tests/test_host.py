@@ -267,3 +267,22 @@ def test_device_plan_synthetic_jw_structure():
     assert ps["bitmap_bits"] == ps["singles"] + 6 * ps["doubles"]
     big = synthetic.jw_hamiltonian(130, 2_000, seed=1)  # N > 128: no pair bitmaps
     assert big.plan_summary()["bitmap_bits"] == 0
+
+
+def test_shard_bounds_match_python():
+    """qvmc_shard_bounds (C ABI, no device needed) == distributed.shard_bounds."""
+    import ctypes as C
+
+    from paper_2408_07625_b200 import _lib
+    from paper_2408_07625_b200.distributed import shard_bounds
+    L = _lib.lib()
+    for n, world in ((0, 1), (5, 8), (1_000_003, 8), (17, 3)):
+        tot = 0
+        for r in range(world):
+            b, e = C.c_int64(), C.c_int64()
+            _lib.check(L.qvmc_shard_bounds(n, world, r, C.byref(b), C.byref(e)))
+            assert (b.value, e.value) == shard_bounds(n, world, r)
+            tot += e.value - b.value
+        assert tot == n
+    with pytest.raises(ValueError):
+        _lib.check(L.qvmc_shard_bounds(10, 2, 2, None, None))
