@@ -257,6 +257,17 @@ int qvmc_cuda_log_psi(qvmc_model_t m, int64_t n, const uint64_t* keys, int mem, 
 int qvmc_cuda_fill_amplitudes(qvmc_model_t m, int64_t n, const uint64_t* keys, const double* log_probs, int mem,
                               double* out_log_amp, double* out_phase, double* out_norm2);
 int qvmc_cuda_model_synchronize(qvmc_model_t m);
+/* energy_gradient (proj/src/energy.cpp:93-107, GradientAccumulator :80-91)
+ * over the rows of batched_grad_log_psi (proj/src/model.cpp:273-336) of the
+ * n keys, as run_optimisation streams them (optimizer.cpp:105-140):
+ * grad = sum_i 2 Re{ w_i (E_i - E) O_i }, E = sum_i w_i E_i, O_i = d log|psi|
+ * - i d phase. The Jacobian is never materialised: per-sample backward
+ * vectors are contracted on the device (strided-batched DGEMMs). locals
+ * [n][2] (re, im); out_grad [n_params] in the reference's flat layout. Keys
+ * outside the model's sector: QVMC_ERR_INVALID_ARGUMENT (grad_log_psi's
+ * "state is masked"). Synchronises. */
+int qvmc_cuda_energy_gradient(qvmc_model_t m, int64_t n, const uint64_t* keys, const double* weights,
+                              const double* locals, int mem, double* out_grad);
 /* sample_without_replacement (proj/src/sampler.cpp:37-102): the ancestral
  * Gumbel top-K beam with CounterRng(seed, stream) (rng.hpp:30-63) and the
  * iteration index, the model's conditionals evaluated on the device. Writes

@@ -235,6 +235,8 @@ def rlib():
         L.qref_model_log_psi.argtypes = [_P, _I64, _INT, _P, _INT, _P, _P]
         L.qref_fill_amplitudes.argtypes = [_P, _I64, _INT, _P, _P, _INT, _P, _P, _P]
         L.qref_sample.argtypes = [_P, _INT, _U64, C.c_uint32, C.c_uint32, _INT, _INT, _P, _P, C.POINTER(_I64)]
+        L.qref_grad_log_psi.argtypes = [_P, _I64, _INT, _P, _INT, _P]
+        L.qref_energy_gradient.argtypes = [_P, _I64, _INT, _P, _P, _P, _INT, _P]
         L.qref_condition_max.restype = C.c_double
         L.qref_condition_max.argtypes = [C.c_double] * 3
         L.qref_gumbel.restype = C.c_double
@@ -469,6 +471,30 @@ class RefModel:
         _rcheck(rlib().qref_sample(self._h, k_samples, seed, stream, iteration, threads, self.W, _ptr(keys), _ptr(lp),
                                    C.byref(n)))
         return keys[: n.value], lp[: n.value]
+
+
+def _ref_model_grad(self, keys, threads: int = 1):
+    """batched_grad_log_psi (model.cpp:273-336): complex rows [n][n_params]."""
+    keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, self.W)
+    n = keys.shape[0]
+    out = np.zeros((n, self.n_params), dtype=np.complex128)
+    _rcheck(rlib().qref_grad_log_psi(self._h, n, self.W, _ptr(keys), threads, _ptr(out)))
+    return out
+
+
+def _ref_energy_gradient(self, keys, weights, locals_, threads: int = 1):
+    """energy_gradient (energy.cpp:93-107) over batched_grad_log_psi rows."""
+    keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, self.W)
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    loc = np.ascontiguousarray(locals_, dtype=np.complex128)
+    g = np.zeros(self.n_params)
+    _rcheck(rlib().qref_energy_gradient(self._h, keys.shape[0], self.W, _ptr(keys), _ptr(w), _ptr(loc), threads,
+                                        _ptr(g)))
+    return g
+
+
+RefModel.grad_log_psi = _ref_model_grad
+RefModel.energy_gradient = _ref_energy_gradient
 
 
 def ref_condition_max(parent, z, child):

@@ -242,3 +242,61 @@ def sample_without_replacement(model: "ModelOracle", k_samples, seed, stream=0, 
         children.sort(key=lambda c: (-c[2], _key_tuple(c[0])))  # ChildLess (sampler.cpp:27-33)
         beam = [tuple(c) for c in children[:k_samples]]
     return np.stack([b[0] for b in beam]), np.array([b[1] for b in beam])
+
+
+# ---------------------------------------------------------------- gradient restatement
+
+def _mlp_fwd(b, e):
+    h1 = np.tanh(e @ b["W1"].T + b["b1"])
+    h2 = np.tanh(h1 @ b["W2"].T + b["b2"] + h1)
+    return h1, h2, h2 @ b["W3"].T + b["b3"]
+
+
+def _mlp_bwd(b, e, h1, h2, g):
+    """mlp_backward (model.cpp:177-201), rows = samples: per-sample blocks (W1, b1, W2, b2, W3, b3)."""
+    gz2 = (g @ b["W3"]) * (1.0 - h2 ** 2)
+    gh1 = gz2 @ b["W2"] + gz2
+    gz1 = gh1 * (1.0 - h1 ** 2)
+    N = e.shape[0]
+    return [np.einsum("sh,si->shi", gz1, e).reshape(N, -1), gz1, np.einsum("sh,sk->shk", gz2, h1).reshape(N, -1),
+            gz2, np.einsum("sv,sh->svh", g, h2).reshape(N, -1), g]
+
+
+def grad_log_psi(model: "ModelOracle", keys):
+    """batched_grad_log_psi (model.cpp:273-336): complex rows [N][n_params], d log|psi| - i d phase."""
+    keys = np.ascontiguousarray(keys, dtype=np.uint64)
+    N = keys.shape[0]
+    bits = np.unpackbits(keys.view(np.uint8).reshape(N, -1), axis=1, bitorder="little")[:, :model.n].astype(np.int64)
+    la, _ = model.log_psi(keys)
+    if not np.all(np.isfinite(la)):
+        raise ValueError("grad_log_psi: state is masked (zero amplitude)")
+    rows = []
+    for j, (o, k) in enumerate(zip(model.offsets, model.sizes)):
+        e = np.zeros((N, model.n))
+        e[:, :o] = np.where(bits[:, :o] == 1, 1.0, -1.0)
+        v = np.zeros(N, dtype=np.int64)
+        for t in range(k):
+            v |= bits[:, o + t] << (k - 1 - t)
+        onehot = np.zeros((N, 1 << k))
+        onehot[np.arange(N), v] = 1.0
+        ab, pb = model.blocks[j]
+        h1, h2, out = _mlp_fwd(ab, e)
+        out = out - out.mean(axis=1, keepdims=True)
+        ok = model.allowed(j, bits[:, :o].sum(1), bits[:, 0:o:2].sum(1))
+        two = np.where(ok, 2.0 * out, -np.inf)
+        mx = two.max(axis=1, keepdims=True)
+        ex = np.where(ok, np.exp(two - mx), 0.0)
+        g = onehot - ex / ex.sum(axis=1, keepdims=True)
+        g = g - g.mean(axis=1, keepdims=True)
+        rows += [blk.astype(np.complex128) for blk in _mlp_bwd(ab, e, h1, h2, g)]
+        h1p, h2p, _ = _mlp_fwd(pb, e)
+        rows += [-1j * blk for blk in _mlp_bwd(pb, e, h1p, h2p, onehot)]
+    return np.concatenate(rows, axis=1)
+
+
+def energy_gradient(weights, locals_, jacobian):
+    """energy_gradient (energy.cpp:93-107): sum_i 2 Re{w_i (E_i - E) row_i}, E = sum_i w_i E_i."""
+    w = np.asarray(weights, dtype=np.float64)
+    loc = np.asarray(locals_, dtype=np.complex128)
+    c = w * (loc - (w * loc).sum())
+    return 2.0 * (c.real @ jacobian.real - c.imag @ jacobian.imag)

@@ -553,6 +553,38 @@ int qref_sample(void* m, int k_samples, std::uint64_t seed, std::uint32_t stream
     *out_n = b.size();
   });
 }
+// AnqsModel::batched_grad_log_psi (model.cpp:273-336): out_rows [n][n_params] complex (re, im)
+int qref_grad_log_psi(void* m, std::int64_t n, int n_words, const std::uint64_t* keys, int threads, double* out_rows) {
+  return guarded([&] {
+    const auto& model = *static_cast<qvmc::AnqsModel*>(m);
+    const auto vs = make_batch(model.layout().n_qubits, n_words, n, keys);
+    const Eigen::MatrixXcd jac = model.batched_grad_log_psi(vs, threads);
+    const std::int64_t P = model.n_params();
+    for (std::int64_t i = 0; i < n; ++i)
+      for (std::int64_t t = 0; t < P; ++t) {
+        const std::complex<double> v = jac(i, t);
+        out_rows[2 * (i * P + t)] = v.real();
+        out_rows[2 * (i * P + t) + 1] = v.imag();
+      }
+  });
+}
+// energy_gradient (energy.cpp:93-107) over the rows of batched_grad_log_psi
+int qref_energy_gradient(void* m, std::int64_t n, int n_words, const std::uint64_t* keys, const double* weights,
+                         const double* locals2, int threads, double* out_grad) {
+  return guarded([&] {
+    const auto& model = *static_cast<qvmc::AnqsModel*>(m);
+    const auto vs = make_batch(model.layout().n_qubits, n_words, n, keys);
+    const Eigen::MatrixXcd jac = model.batched_grad_log_psi(vs, threads);
+    Eigen::VectorXd w(n);
+    Eigen::VectorXcd loc(n);
+    for (std::int64_t i = 0; i < n; ++i) {
+      w[i] = weights[i];
+      loc[i] = std::complex<double>(locals2[2 * i], locals2[2 * i + 1]);
+    }
+    const Eigen::VectorXd g = qvmc::energy_gradient(w, loc, jac);
+    for (Eigen::Index t = 0; t < g.size(); ++t) out_grad[t] = g[t];
+  });
+}
 // condition_max (sampler.cpp:15-23) and CounterRng::gumbel (rng.hpp) for the restatement's pins
 double qref_condition_max(double parent, double z, double child) { return qvmc::condition_max(parent, z, child); }
 double qref_gumbel(std::uint64_t seed, std::uint32_t stream, std::uint32_t c0, std::uint32_t c1, std::uint32_t c2,

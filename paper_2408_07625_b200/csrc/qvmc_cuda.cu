@@ -1,6 +1,7 @@
 // libqvmc_cuda: C ABI (include/qvmc_cuda.h) over the sm_100a kernels in
 // qvmc_kernels.cuh. Host code here only validates, sizes workspaces, copies
 // and launches; there is no CPU compute path for the per-sample work.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1925,6 +1926,13 @@ struct qvmc_model_s {
   DBuf P, keys, la, ph, lp, part, out2, lse;
   // sampler (sample_without_replacement): two beams, the conditional table, candidates
   DBuf bk[2], blp[2], bpert[2], cond, c_key, c_key2, c_slot, c_slot2, c_bv, c_lp, c_pert, c_count, c_tmp;
+  // gradient: chunk buffers, block sums, coefficients
+  DBuf g_h1, g_h2, g_g, g_gz2, g_gz1, g_x, g_ones, g_w1, g_w2, g_w3, g_b, g_coef, g_mean, g_part, g_flag, g_out,
+      g_keys, g_w, g_loc;
+  cublasHandle_t blas = nullptr;
+  ~qvmc_model_s() {
+    if (blas) cublasDestroy(blas);
+  }
 };
 
 namespace {
@@ -2208,6 +2216,165 @@ int qvmc_cuda_sample(qvmc_model_t m, int k_samples, uint64_t seed, uint32_t stre
     ck(cudaMemcpyAsync(out_log_probs, m->blp[cur].p, B * 8, kind, m->stream), "copy log_probs");
     ck(cudaStreamSynchronize(m->stream), "sync");
     *out_n = B;
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+void blas_ck(cublasStatus_t st, const char* what) {
+  if (st != CUBLAS_STATUS_SUCCESS) fail(QVMC_ERR_CUDA, std::string(what) + ": cuBLAS status " + std::to_string(st));
+}
+
+template <int W>
+__global__ void k_sector_flags(const uint64_t* __restrict__ keys, int64_t n, int n_e, int spin, int n_up,
+                               int* __restrict__ bad) {
+  for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < n;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int pc = 0, pe = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const uint64_t x = keys[s * W + w];
+      pc += __popcll(x);
+      pe += __popcll(x & 0x5555555555555555ull);
+    }
+    if (pc != n_e || (spin && pe != n_up)) atomicOr(bad, 1);
+  }
+}
+
+// Σ over samples of coefficient-scaled gradient blocks (k_grad_part + strided-batched DGEMMs)
+// into m->g_w1/g_w2/g_w3/g_b; coef [n] device (2 Re c, 2 Im c); keys device
+void grad_accumulate(qvmc_model_s* m, const uint64_t* keys, int64_t n, const double2* coef) {
+  using namespace qvmc_model;
+  const int nb = 2 * m->n_qudits, nq = m->n, W = m->W;
+  ModelView V{m->P.as<double>(), m->n, m->n_qudits, m->bits, m->n_e, m->spin, m->n_up};
+  if (!m->blas) blas_ck(cublasCreate(&m->blas), "cublasCreate");
+  blas_ck(cublasSetStream(m->blas, m->stream), "cublasSetStream");
+  const int64_t Nc = std::min<int64_t>(std::max<int64_t>(n, 1), 32768);
+  const size_t vb = static_cast<size_t>(nb) * Nc * 64 * 8;
+  m->g_h1.ensure(vb);
+  m->g_h2.ensure(vb);
+  m->g_g.ensure(vb);
+  m->g_gz2.ensure(vb);
+  m->g_gz1.ensure(vb);
+  m->g_x.ensure(static_cast<size_t>(Nc) * nq * 8);
+  m->g_ones.ensure(static_cast<size_t>(Nc) * 8);
+  m->g_w1.ensure(static_cast<size_t>(nb) * 64 * nq * 8);
+  m->g_w2.ensure(static_cast<size_t>(nb) * 4096 * 8);
+  m->g_w3.ensure(static_cast<size_t>(nb) * 4096 * 8);
+  m->g_b.ensure(static_cast<size_t>(nb) * 3 * 64 * 8);
+  {
+    std::vector<double> ones(static_cast<size_t>(Nc), 1.0);
+    ck(cudaMemcpyAsync(m->g_ones.p, ones.data(), Nc * 8, cudaMemcpyHostToDevice, m->stream), "H2D ones");
+    ck(cudaStreamSynchronize(m->stream), "sync");
+  }
+  const size_t dyn = (16640 + kGWarps * 64 * kWT) * sizeof(double) + kGWarps * kWT * W * sizeof(uint64_t);
+  const double one = 1.0, zero = 0.0;
+  for (int64_t c0 = 0; c0 < n; c0 += Nc) {
+    const int64_t nc = std::min<int64_t>(Nc, n - c0);
+    const int64_t per = 512;  // samples per CTA
+    const int64_t S = (nc + per - 1) / per;
+    DISPATCH_W(W, {
+      ck(cudaFuncSetAttribute(k_grad_part<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)),
+         "smem attribute");
+      k_grad_part<WW><<<static_cast<unsigned>(S * nb), kGThreads, dyn, m->stream>>>(
+          V, keys + c0 * WW, nc, per, coef + c0, m->g_h1.as<double>(), m->g_h2.as<double>(), m->g_g.as<double>(),
+          m->g_gz2.as<double>(), m->g_gz1.as<double>());
+      ck_launch("grad part");
+      const int xg = static_cast<int>(std::min<int64_t>((nc * nq + 255) / 256, 8LL * m->sms));
+      k_pm_bits<WW><<<xg, 256, 0, m->stream>>>(keys + c0 * WW, nc, nq, m->g_x.as<double>());
+      ck_launch("pm bits");
+    });
+    const double* beta = c0 == 0 ? &zero : &one;
+    const long long sv = static_cast<long long>(nc) * 64;  // chunk stride of a block's vectors (ld 64)
+    // gW1[jh] (col-major n x 64) = X (n x nc) . GZ1ᵀ
+    blas_ck(cublasDgemmStridedBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, nq, 64, static_cast<int>(nc), &one,
+                                      m->g_x.as<double>(), nq, 0, m->g_gz1.as<double>(), 64, sv, beta,
+                                      m->g_w1.as<double>(), nq, 64LL * nq, nb), "dgemm w1");
+    // gW2[jh] (64 k x 64 h) = H1 . GZ2ᵀ ; gW3[jh] (64 h x 64 v) = H2 . Gᵀ
+    blas_ck(cublasDgemmStridedBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, 64, 64, static_cast<int>(nc), &one,
+                                      m->g_h1.as<double>(), 64, sv, m->g_gz2.as<double>(), 64, sv, beta,
+                                      m->g_w2.as<double>(), 64, 4096, nb), "dgemm w2");
+    blas_ck(cublasDgemmStridedBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, 64, 64, static_cast<int>(nc), &one,
+                                      m->g_h2.as<double>(), 64, sv, m->g_g.as<double>(), 64, sv, beta,
+                                      m->g_w3.as<double>(), 64, 4096, nb), "dgemm w3");
+    // biases: Σ_s of gz1, gz2, g
+    const double* vecs[3] = {m->g_gz1.as<double>(), m->g_gz2.as<double>(), m->g_g.as<double>()};
+    for (int q = 0; q < 3; ++q)
+      blas_ck(cublasDgemmStridedBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_N, 64, 1, static_cast<int>(nc), &one,
+                                        vecs[q], 64, sv, m->g_ones.as<double>(), static_cast<int>(nc), 0, beta,
+                                        m->g_b.as<double>() + 64 * q, 64, 192, nb), "dgemm bias");
+    g_launches += 6;
+  }
+}
+
+void check_in_sector(qvmc_model_s* m, const uint64_t* keys, int64_t n) {
+  m->g_flag.ensure(16);
+  ck(cudaMemsetAsync(m->g_flag.p, 0, 4, m->stream), "memset");
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 8LL * m->sms));
+  DISPATCH_W(m->W, (k_sector_flags<WW><<<std::max(grid, 1), 256, 0, m->stream>>>(keys, n, m->n_e, m->spin, m->n_up,
+                                                                                   m->g_flag.as<int>())));
+  ck_launch("sector flags");
+  int bad = 0;
+  ck(cudaMemcpyAsync(&bad, m->g_flag.p, 4, cudaMemcpyDeviceToHost, m->stream), "D2H");
+  ck(cudaStreamSynchronize(m->stream), "sync");
+  if (bad) fail(QVMC_ERR_INVALID_ARGUMENT, "grad_log_psi: state is masked (zero amplitude)");
+}
+
+}  // namespace
+
+extern "C" {
+
+// energy_gradient (energy.cpp:93-107) with batched_grad_log_psi rows (model.cpp:273-336)
+// contracted on the device, never materialised.
+int qvmc_cuda_energy_gradient(qvmc_model_t m, int64_t n, const uint64_t* keys, const double* weights,
+                              const double* locals, int mem, double* out_grad) {
+  return guarded([&] {
+    check_model(m);
+    check_mem(mem);
+    if (n < 1) fail(QVMC_ERR_INVALID_ARGUMENT, "energy_gradient: misaligned inputs");
+    if (!keys || !weights || !locals || !out_grad) fail(QVMC_ERR_INVALID_ARGUMENT, "null array");
+    if (!m->has_params) fail(QVMC_ERR_INVALID_ARGUMENT, "model parameters not set");
+    using namespace qvmc_model;
+    DeviceGuard dg(m->device);
+    const uint64_t* dk = keys;
+    const double* dw = weights;
+    const double2* dl = reinterpret_cast<const double2*>(locals);
+    if (mem == QVMC_MEM_HOST) {
+      m->g_keys.ensure(n * m->W * 8);
+      m->g_w.ensure(n * 8);
+      m->g_loc.ensure(n * 16);
+      ck(cudaMemcpyAsync(m->g_keys.p, keys, n * m->W * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
+      ck(cudaMemcpyAsync(m->g_w.p, weights, n * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
+      ck(cudaMemcpyAsync(m->g_loc.p, locals, n * 16, cudaMemcpyHostToDevice, m->stream), "H2D");
+      dk = m->g_keys.as<uint64_t>();
+      dw = m->g_w.as<double>();
+      dl = m->g_loc.as<double2>();
+    }
+    check_in_sector(m, dk, n);
+    m->g_part.ensure(kLseBlocks * 16);
+    m->g_mean.ensure(16);
+    m->g_coef.ensure(n * 16);
+    k_wmean_partial<<<kLseBlocks, 256, 0, m->stream>>>(dw, dl, n, m->g_part.as<double2>());
+    k_wmean_final<<<1, 32, 0, m->stream>>>(m->g_part.as<double2>(), kLseBlocks, m->g_mean.as<double2>());
+    const int cg = static_cast<int>(std::min<int64_t>((n + 255) / 256, 8LL * m->sms));
+    k_grad_coef<<<cg, 256, 0, m->stream>>>(dw, dl, n, m->g_mean.as<double2>(), m->g_coef.as<double2>());
+    ck_launch("gradient coefficients");
+    g_launches += 2;
+    grad_accumulate(m, dk, n, m->g_coef.as<double2>());
+    ModelView V{m->P.as<double>(), m->n, m->n_qudits, m->bits, m->n_e, m->spin, m->n_up};
+    double* dout = out_grad;
+    if (mem == QVMC_MEM_HOST) {
+      m->g_out.ensure(m->n_params * 8);
+      dout = m->g_out.as<double>();
+    }
+    k_grad_scatter<<<2 * m->n_qudits, 256, 0, m->stream>>>(V, m->g_w1.as<double>(), m->g_w2.as<double>(),
+                                                            m->g_w3.as<double>(), m->g_b.as<double>(), dout);
+    ck_launch("gradient scatter");
+    if (mem == QVMC_MEM_HOST)
+      ck(cudaMemcpyAsync(out_grad, dout, m->n_params * 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
+    ck(cudaStreamSynchronize(m->stream), "sync");
   });
 }
 

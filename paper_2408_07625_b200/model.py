@@ -121,6 +121,20 @@ class AnqsModel:
     def synchronize(self) -> None:
         _lib.check(_lib.lib().qvmc_cuda_model_synchronize(self._h))
 
+    def energy_gradient(self, keys: np.ndarray, weights, locals_) -> np.ndarray:
+        """energy_gradient (energy.cpp:93-107) over batched_grad_log_psi rows (model.cpp:273-336) of
+        ``keys``, contracted on the device (the Jacobian is never formed): [n_params], reference layout."""
+        keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, self.W)
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        loc = np.ascontiguousarray(locals_, dtype=np.complex128)
+        n = keys.shape[0]
+        if w.shape != (n,) or loc.shape != (n,):
+            raise ValueError("energy_gradient: misaligned inputs")
+        g = np.zeros(self.n_params())
+        _lib.check(_lib.lib().qvmc_cuda_energy_gradient(self._h, n, _ptr(keys), _ptr(w), _ptr(loc), _lib.MEM_HOST,
+                                                        _ptr(g)))
+        return g
+
     def save_checkpoint(self, seed: int) -> str:
         """Text checkpoint, format of AnqsModel::save_checkpoint (model.cpp:345-357)."""
         lines = ["qvmc-checkpoint v1", f"n_qubits {self.layout.n_qubits}",
