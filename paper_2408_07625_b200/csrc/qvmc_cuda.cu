@@ -2157,8 +2157,13 @@ int qvmc_cuda_sample(qvmc_model_t m, int k_samples, uint64_t seed, uint32_t stre
     ModelView V{m->P.as<double>(), m->n, m->n_qudits, m->bits, m->n_e, m->spin, m->n_up};
     Candidates Cd{m->c_key.as<uint64_t>(), m->c_slot.as<uint32_t>(), m->c_bv.as<uint32_t>(), m->c_lp.as<double>(),
                   m->c_pert.as<double>(), m->c_count.as<unsigned long long>()};
+    const bool trace = std::getenv("QVMC_SAMPLER_TRACE") != nullptr;
+    cudaEvent_t tev[6];
+    if (trace)
+      for (auto& e : tev) ck(cudaEventCreate(&e), "event");
     for (int level = 0; level < m->n_qudits; ++level) {
       const int off = level * m->bits, k = std::min(m->bits, m->n - off);
+      if (trace) ck(cudaEventRecord(tev[0], m->stream), "event");
       // 1. conditional log-probabilities of every beam prefix (amplitude head of this qudit)
       const int64_t per = static_cast<int64_t>(kWT) * kPWarps;
       const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>((B + per - 1) / per, 4 * m->sms));
@@ -2174,6 +2179,7 @@ int qvmc_cuda_sample(qvmc_model_t m, int k_samples, uint64_t seed, uint32_t stre
         ck_launch("sampler conditional");
       });
       // 2. children + Gumbel + condition_max
+      if (trace) ck(cudaEventRecord(tev[1], m->stream), "event");
       ck(cudaMemsetAsync(m->c_count.p, 0, 8, m->stream), "memset");
       const int eg = static_cast<int>(std::min<int64_t>((B * 32 + 255) / 256, 8LL * m->sms));
       k_expand<<<std::max(eg, 1), 256, 0, m->stream>>>(m->cond.as<double>(), m->blp[cur].as<double>(),
@@ -2185,6 +2191,7 @@ int qvmc_cuda_sample(qvmc_model_t m, int k_samples, uint64_t seed, uint32_t stre
       ck(cudaStreamSynchronize(m->stream), "sync");
       if (nc == 0) fail(QVMC_ERR_RUNTIME, "sample_without_replacement: empty sector");
       // 3. ChildLess order: conditioned value descending, ties by child prefix
+      if (trace) ck(cudaEventRecord(tev[2], m->stream), "event");
       const int n = static_cast<int>(nc);
       size_t tb = 0;
       ck(cub::DeviceRadixSort::SortPairs(nullptr, tb, m->c_key.as<uint64_t>(), m->c_key2.as<uint64_t>(),
@@ -2197,6 +2204,7 @@ int qvmc_cuda_sample(qvmc_model_t m, int k_samples, uint64_t seed, uint32_t stre
       ++g_launches;
       const int64_t keep = std::min<int64_t>(K, n);
       const int tg = static_cast<int>(std::min<int64_t>((keep + 255) / 256, 8LL * m->sms));
+      if (trace) ck(cudaEventRecord(tev[3], m->stream), "event");
       DISPATCH_W(W, {
         k_ties<WW><<<std::max(tg, 1), 256, 0, m->stream>>>(m->c_key2.as<uint64_t>(), m->c_slot2.as<uint32_t>(), n,
                                                           keep, m->c_bv.as<uint32_t>(), m->bk[cur].as<uint64_t>(),
@@ -2208,9 +2216,19 @@ int qvmc_cuda_sample(qvmc_model_t m, int k_samples, uint64_t seed, uint32_t stre
             m->blp[1 - cur].as<double>(), m->bpert[1 - cur].as<double>());
         ck_launch("sampler gather");
       });
+      if (trace) {
+        ck(cudaEventRecord(tev[4], m->stream), "event");
+        ck(cudaEventSynchronize(tev[4]), "sync");
+        float t[4];
+        for (int q = 0; q < 4; ++q) ck(cudaEventElapsedTime(&t[q], tev[q], tev[q + 1]), "elapsed");
+        std::fprintf(stderr, "sampler level %d: beam %lld candidates %llu | cond %.3f expand+count %.3f sort %.3f "
+                     "ties+gather %.3f ms\n", level, static_cast<long long>(B), nc, t[0], t[1], t[2], t[3]);
+      }
       cur = 1 - cur;
       B = keep;
     }
+    if (trace)
+      for (auto& e : tev) cudaEventDestroy(e);
     const cudaMemcpyKind kind = mem == QVMC_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     ck(cudaMemcpyAsync(out_keys, m->bk[cur].p, B * W * 8, kind, m->stream), "copy keys");
     ck(cudaMemcpyAsync(out_log_probs, m->blp[cur].p, B * 8, kind, m->stream), "copy log_probs");
