@@ -268,6 +268,22 @@ int qvmc_cuda_model_synchronize(qvmc_model_t m);
  * "state is masked"). Synchronises. */
 int qvmc_cuda_energy_gradient(qvmc_model_t m, int64_t n, const uint64_t* keys, const double* weights,
                               const double* locals, int mem, double* out_grad);
+/* sr_direction (proj/src/sr.cpp:74-95) for a given SrContext: stacked
+ * row-major [rows][cols] (rows = 2 n_sr), lambda > 0, grad [cols]: the
+ * push-through solve with the Gram eigensystem (cuSOLVER syevd); the
+ * reference's conditioning check (runtime_error "ill-conditioned system,
+ * cond ~ ...", QVMC_ERR_RUNTIME). out_direction [cols]. Synchronises. */
+int qvmc_cuda_sr_solve(qvmc_model_t m, int64_t rows, int64_t cols, const double* stacked, double lambda,
+                       const double* grad, int mem, double* out_direction);
+/* The SR step of run_optimisation (optimizer.cpp:105-143): the n_sr samples
+ * of highest log p (top_probability_indices, sr.cpp:15-23, ties in sample
+ * order), their grad_log_psi rows (model.cpp:273-325), build_sr_context
+ * (sr.cpp:25-72; lambda <= 0 picks 1e-4 (1 + ||stacked||_F^2 / n_sr)) and
+ * sr_direction applied to grad [n_params]. locals [n][2]. out_lambda may be
+ * NULL. Synchronises. */
+int qvmc_cuda_sr_direction(qvmc_model_t m, int64_t n, const uint64_t* keys, const double* log_probs,
+                           const double* locals, int n_sr, double lambda, const double* grad, int mem,
+                           double* out_direction, double* out_lambda);
 /* sample_without_replacement (proj/src/sampler.cpp:37-102): the ancestral
  * Gumbel top-K beam with CounterRng(seed, stream) (rng.hpp:30-63) and the
  * iteration index, the model's conditionals evaluated on the device. Writes

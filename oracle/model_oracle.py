@@ -17,6 +17,10 @@ numpy restatement (fp64, vectorised over samples) of ``AnqsModel`` and
 * ``CounterRng::gumbel``         include/qvmc/rng.hpp:38-63 (bits64 -> 53-bit uniform, clamp, -log(-log u))
 * ``condition_max``              src/sampler.cpp:15-23
 * ``sample_without_replacement`` src/sampler.cpp:37-102 (ancestral Gumbel top-K beam, ChildLess order)
+* ``grad_log_psi`` / ``mlp_backward`` src/model.cpp:177-325, ``energy_gradient`` src/energy.cpp:93-107
+* ``top_probability_indices``, ``build_sr_context``, ``sr_direction`` src/sr.cpp:15-95 (numpy eigh; sr.cpp
+  needs Eigen's eigensolver and is not compiled here: pinned to the dense regularised solve, the reference's
+  own acceptance check, checks.cpp "SR solve", and its tests in test_energy_sr.cpp)
 
 It is pinned against the reference itself (``oracle/_ref``, model.cpp and
 sampler.cpp compiled with the Eigen shim) by tests/test_model.py. Only tests/,
@@ -300,3 +304,43 @@ def energy_gradient(weights, locals_, jacobian):
     loc = np.asarray(locals_, dtype=np.complex128)
     c = w * (loc - (w * loc).sum())
     return 2.0 * (c.real @ jacobian.real - c.imag @ jacobian.imag)
+
+
+# ---------------------------------------------------------------- SR restatement
+
+def top_probability_indices(log_probs, n_sr):
+    """top_probability_indices (sr.cpp:15-23): stable sort by log p descending."""
+    lp = np.asarray(log_probs, dtype=np.float64)
+    return np.argsort(-lp, kind="stable")[: min(n_sr, lp.size)]
+
+
+def build_sr_context(log_probs, locals_, selected, jac_rows, lam=0.0):
+    """build_sr_context (sr.cpp:25-72): (stacked [2n][P], f_stacked [2n], lambda)."""
+    lp = np.asarray(log_probs, dtype=np.float64)[selected]
+    n = len(selected)
+    if n < 1:
+        raise ValueError("build_sr_context: empty selection")
+    w = np.exp(lp - lp.max())
+    w /= w.sum()
+    row_mean = (w[:, None] * jac_rows).sum(0)
+    loc = np.asarray(locals_, dtype=np.complex128)[selected]
+    e_mean = (w * loc).sum()
+    s = np.sqrt(w)
+    centered = (jac_rows - row_mean) * s[:, None]
+    stacked = np.concatenate([centered.real, centered.imag])
+    f = s * np.conj(loc - e_mean)
+    f_stacked = np.concatenate([f.real, f.imag])
+    lam = lam if lam > 0.0 else 1e-4 * (1.0 + (stacked ** 2).sum() / n)
+    return stacked, f_stacked, lam
+
+
+def sr_direction(stacked, lam, grad):
+    """sr_direction (sr.cpp:74-95): push-through identity with the Gram eigensystem."""
+    gram = stacked @ stacked.T + lam * np.eye(stacked.shape[0])
+    ev, V = np.linalg.eigh(gram)
+    lo, hi = ev.min(), ev.max()
+    if not lo > 0.0 or hi / lo > 1e14:
+        raise RuntimeError(f"sr_direction: ill-conditioned system, cond ~ {hi / max(lo, 1e-300)}")
+    t = stacked @ grad
+    s = V @ ((V.T @ t) / ev)
+    return (grad - stacked.T @ s) / lam

@@ -2,6 +2,7 @@
 // qvmc_kernels.cuh. Host code here only validates, sizes workspaces, copies
 // and launches; there is no CPU compute path for the per-sample work.
 #include <cublas_v2.h>
+#include <cusolverDn.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1930,8 +1931,13 @@ struct qvmc_model_s {
   DBuf g_h1, g_h2, g_g, g_gz2, g_gz1, g_x, g_ones, g_w1, g_w2, g_w3, g_b, g_coef, g_mean, g_part, g_flag, g_out,
       g_keys, g_w, g_loc;
   cublasHandle_t blas = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  // SR: selection, Jacobian rows, stacked matrix, Gram eigensystem
+  DBuf s_lpk, s_lpk2, s_idx, s_idx2, s_keys, s_sw, s_R, s_mean, s_S, s_gram, s_w, s_t, s_u, s_dir, s_boff, s_info,
+      s_work, s_grad, s_coef1, s_tmp;
   ~qvmc_model_s() {
     if (blas) cublasDestroy(blas);
+    if (solver) cusolverDnDestroy(solver);
   }
 };
 
@@ -2327,6 +2333,103 @@ void grad_accumulate(qvmc_model_s* m, const uint64_t* keys, int64_t n, const dou
   }
 }
 
+// flat offsets of the (qudit, head) parameter blocks (model.cpp:65-80), nb + 1 entries
+std::vector<int64_t> block_offsets(const qvmc_model_s* m) {
+  std::vector<int64_t> b(1, 0);
+  for (int jh = 0; jh < 2 * m->n_qudits; ++jh) {
+    const int k = std::min(m->bits, m->n - (jh >> 1) * m->bits);
+    b.push_back(b.back() + 64LL * m->n + 64 + 4096 + 64 + (64LL << k) + (1 << k));
+  }
+  return b;
+}
+
+void solver_ck(cusolverStatus_t st, const char* what) {
+  if (st != CUSOLVER_STATUS_SUCCESS) fail(QVMC_ERR_CUDA, std::string(what) + ": cuSOLVER status " + std::to_string(st));
+}
+
+__global__ void k_iota_u32(uint32_t* p, int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = static_cast<uint32_t>(i);
+}
+
+__global__ void k_gather_rows_u64(const uint64_t* __restrict__ src, const uint32_t* __restrict__ idx, int64_t n, int W,
+                                  uint64_t* __restrict__ dst) {
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n * W;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[e] = src[static_cast<int64_t>(idx[e / W]) * W + e % W];
+}
+
+__global__ void k_fill_f64(double* p, int64_t n, double v) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+// sr_direction (sr.cpp:74-95) on device buffers: S row-major [rows][cols] (= col-major cols x rows),
+// grad [cols] -> out [cols]; lambda > 0. The Gram eigensystem is cuSOLVER syevd.
+void sr_solve_device(qvmc_model_s* m, int64_t rows, int64_t cols, const double* S, double lambda, const double* grad,
+                     double* out) {
+  if (!m->blas) blas_ck(cublasCreate(&m->blas), "cublasCreate");
+  if (!m->solver) solver_ck(cusolverDnCreate(&m->solver), "cusolverDnCreate");
+  blas_ck(cublasSetStream(m->blas, m->stream), "cublasSetStream");
+  solver_ck(cusolverDnSetStream(m->solver, m->stream), "cusolverDnSetStream");
+  const int r = static_cast<int>(rows), c = static_cast<int>(cols);
+  const double one = 1.0, zero = 0.0, mone = -1.0;
+  m->s_gram.ensure(static_cast<size_t>(r) * r * 8 + 16);
+  m->s_w.ensure(static_cast<size_t>(r) * 8 + 16);
+  m->s_t.ensure(static_cast<size_t>(r) * 8 + 16);
+  m->s_u.ensure(static_cast<size_t>(r) * 8 + 16);
+  m->s_info.ensure(16);
+  double* gram = m->s_gram.as<double>();
+  // gram = S S^T + lambda I   (S^T S in col-major terms of the c x r matrix)
+  blas_ck(cublasDgemm(m->blas, CUBLAS_OP_T, CUBLAS_OP_N, r, r, c, &one, S, c, S, c, &zero, gram, r), "dgemm gram");
+  {
+    std::vector<double> eye(static_cast<size_t>(r), lambda);
+    m->s_tmp.ensure(static_cast<size_t>(r) * 8 + 16);
+    ck(cudaMemcpyAsync(m->s_tmp.p, eye.data(), r * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
+    blas_ck(cublasDaxpy(m->blas, r, &one, m->s_tmp.as<double>(), 1, gram, r + 1), "daxpy diag");
+    ck(cudaStreamSynchronize(m->stream), "sync");
+  }
+  int lwork = 0;
+  solver_ck(cusolverDnDsyevd_bufferSize(m->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, r, gram, r,
+                                        m->s_w.as<double>(), &lwork), "syevd size");
+  m->s_work.ensure(static_cast<size_t>(lwork) * 8 + 16);
+  solver_ck(cusolverDnDsyevd(m->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, r, gram, r,
+                             m->s_w.as<double>(), m->s_work.as<double>(), lwork, m->s_info.as<int>()), "syevd");
+  int info = 0;
+  std::vector<double> ev(static_cast<size_t>(r));
+  ck(cudaMemcpyAsync(&info, m->s_info.p, 4, cudaMemcpyDeviceToHost, m->stream), "D2H");
+  ck(cudaMemcpyAsync(ev.data(), m->s_w.p, r * 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
+  ck(cudaStreamSynchronize(m->stream), "sync");
+  if (info != 0) fail(QVMC_ERR_RUNTIME, "sr_direction: eigendecomposition failed");
+  const double lo = *std::min_element(ev.begin(), ev.end()), hi = *std::max_element(ev.begin(), ev.end());
+  if (!(lo > 0.0) || hi / lo > 1e14) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%f", hi / std::max(lo, 1e-300));
+    fail(QVMC_ERR_RUNTIME, std::string("sr_direction: ill-conditioned system, cond ~ ") + buf);
+  }
+  // t = S grad; u = (V^T t) ./ evals; s = V u; out = (grad - S^T s) / lambda
+  blas_ck(cublasDgemv(m->blas, CUBLAS_OP_T, c, r, &one, S, c, grad, 1, &zero, m->s_t.as<double>(), 1), "gemv t");
+  blas_ck(cublasDgemv(m->blas, CUBLAS_OP_T, r, r, &one, gram, r, m->s_t.as<double>(), 1, &zero,
+                      m->s_u.as<double>(), 1), "gemv u");
+  {
+    std::vector<double> inv(static_cast<size_t>(r));
+    for (int i = 0; i < r; ++i) inv[i] = 1.0 / ev[i];
+    ck(cudaMemcpyAsync(m->s_tmp.p, inv.data(), r * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
+    blas_ck(cublasDdgmm(m->blas, CUBLAS_SIDE_LEFT, r, 1, m->s_u.as<double>(), r, m->s_tmp.as<double>(), 1,
+                        m->s_u.as<double>(), r), "ddgmm");
+    ck(cudaStreamSynchronize(m->stream), "sync");
+  }
+  blas_ck(cublasDgemv(m->blas, CUBLAS_OP_N, r, r, &one, gram, r, m->s_u.as<double>(), 1, &zero,
+                      m->s_t.as<double>(), 1), "gemv s");
+  ck(cudaMemcpyAsync(out, grad, static_cast<size_t>(c) * 8, cudaMemcpyDeviceToDevice, m->stream), "copy grad");
+  blas_ck(cublasDgemv(m->blas, CUBLAS_OP_N, c, r, &mone, S, c, m->s_t.as<double>(), 1, &one, out, 1), "gemv out");
+  const double il = 1.0 / lambda;
+  blas_ck(cublasDscal(m->blas, c, &il, out, 1), "dscal");
+  g_launches += 8;
+}
+
 void check_in_sector(qvmc_model_s* m, const uint64_t* keys, int64_t n) {
   m->g_flag.ensure(16);
   ck(cudaMemsetAsync(m->g_flag.p, 0, 4, m->stream), "memset");
@@ -2393,6 +2496,180 @@ int qvmc_cuda_energy_gradient(qvmc_model_t m, int64_t n, const uint64_t* keys, c
     if (mem == QVMC_MEM_HOST)
       ck(cudaMemcpyAsync(out_grad, dout, m->n_params * 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
     ck(cudaStreamSynchronize(m->stream), "sync");
+  });
+}
+
+// sr_direction (sr.cpp:74-95) for a given stacked matrix (SrContext::stacked,
+// row-major [rows][cols] here) and lambda > 0.
+int qvmc_cuda_sr_solve(qvmc_model_t m, int64_t rows, int64_t cols, const double* stacked, double lambda,
+                       const double* grad, int mem, double* out_direction) {
+  return guarded([&] {
+    check_model(m);
+    check_mem(mem);
+    if (rows < 1 || cols < 1 || rows > 65536 || cols > (1LL << 31) / std::max<int64_t>(rows, 1))
+      fail(QVMC_ERR_INVALID_ARGUMENT, "sr_direction: bad system size");
+    if (!stacked || !grad || !out_direction) fail(QVMC_ERR_INVALID_ARGUMENT, "null array");
+    if (!(lambda > 0.0)) fail(QVMC_ERR_INVALID_ARGUMENT, "sr_direction: lambda must be positive");
+    DeviceGuard dg(m->device);
+    const double* dS = stacked;
+    const double* dg2 = grad;
+    double* dout = out_direction;
+    if (mem == QVMC_MEM_HOST) {
+      m->s_S.ensure(static_cast<size_t>(rows) * cols * 8);
+      m->s_grad.ensure(static_cast<size_t>(cols) * 8);
+      m->s_dir.ensure(static_cast<size_t>(cols) * 8);
+      ck(cudaMemcpyAsync(m->s_S.p, stacked, rows * cols * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
+      ck(cudaMemcpyAsync(m->s_grad.p, grad, cols * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
+      dS = m->s_S.as<double>();
+      dg2 = m->s_grad.as<double>();
+      dout = m->s_dir.as<double>();
+    }
+    sr_solve_device(m, rows, cols, dS, lambda, dg2, dout);
+    if (mem == QVMC_MEM_HOST)
+      ck(cudaMemcpyAsync(out_direction, dout, cols * 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
+    ck(cudaStreamSynchronize(m->stream), "sync");
+  });
+}
+
+// The SR step of run_optimisation (optimizer.cpp:105-143) on the device:
+// top_probability_indices (sr.cpp:15-23) -> grad_log_psi rows of the selected
+// samples -> build_sr_context (sr.cpp:25-72) -> sr_direction (sr.cpp:74-95).
+int qvmc_cuda_sr_direction(qvmc_model_t m, int64_t n, const uint64_t* keys, const double* log_probs,
+                           const double* locals, int n_sr, double lambda, const double* grad, int mem,
+                           double* out_direction, double* out_lambda) {
+  return guarded([&] {
+    check_model(m);
+    check_mem(mem);
+    if (n < 1 || n_sr < 1) fail(QVMC_ERR_INVALID_ARGUMENT, "build_sr_context: empty selection");
+    if (!keys || !log_probs || !locals || !grad || !out_direction) fail(QVMC_ERR_INVALID_ARGUMENT, "null array");
+    if (!m->has_params) fail(QVMC_ERR_INVALID_ARGUMENT, "model parameters not set");
+    using namespace qvmc_model;
+    DeviceGuard dg(m->device);
+    const int W = m->W;
+    const int64_t P = m->n_params, ns = std::min<int64_t>(n_sr, n);
+    const uint64_t* dk = keys;
+    const double *dlp = log_probs, *dgr = grad;
+    const double2* dl = reinterpret_cast<const double2*>(locals);
+    if (mem == QVMC_MEM_HOST) {
+      m->g_keys.ensure(n * W * 8);
+      m->g_w.ensure(n * 8);
+      m->g_loc.ensure(n * 16);
+      m->s_grad.ensure(P * 8);
+      ck(cudaMemcpyAsync(m->g_keys.p, keys, n * W * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
+      ck(cudaMemcpyAsync(m->g_w.p, log_probs, n * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
+      ck(cudaMemcpyAsync(m->g_loc.p, locals, n * 16, cudaMemcpyHostToDevice, m->stream), "H2D");
+      ck(cudaMemcpyAsync(m->s_grad.p, grad, P * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
+      dk = m->g_keys.as<uint64_t>();
+      dlp = m->g_w.as<double>();
+      dl = m->g_loc.as<double2>();
+      dgr = m->s_grad.as<double>();
+    }
+    // 1. top_probability_indices: stable sort by log p descending (ties keep sample order)
+    m->s_lpk.ensure(n * 8 + 16);
+    m->s_lpk2.ensure(n * 8 + 16);
+    m->s_idx.ensure(n * 4 + 16);
+    m->s_idx2.ensure(n * 4 + 16);
+    k_iota_u32<<<std::max(1, static_cast<int>(std::min<int64_t>((n + 255) / 256, 4096))), 256, 0, m->stream>>>(
+        m->s_idx.as<uint32_t>(), n);
+    ck_launch("iota");
+    ck(cudaMemcpyAsync(m->s_lpk.p, dlp, n * 8, cudaMemcpyDeviceToDevice, m->stream), "copy lp");
+    size_t tb = 0;
+    ck(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, m->s_lpk.as<double>(), m->s_lpk2.as<double>(),
+                                                 m->s_idx.as<uint32_t>(), m->s_idx2.as<uint32_t>(),
+                                                 static_cast<int>(n), 0, 64, m->stream), "sort size");
+    m->s_work.ensure(tb + 16);
+    ck(cub::DeviceRadixSort::SortPairsDescending(m->s_work.p, tb, m->s_lpk.as<double>(), m->s_lpk2.as<double>(),
+                                                 m->s_idx.as<uint32_t>(), m->s_idx2.as<uint32_t>(),
+                                                 static_cast<int>(n), 0, 64, m->stream), "sort");
+    ++g_launches;
+    std::vector<uint32_t> sel(static_cast<size_t>(ns));
+    std::vector<double> slp(static_cast<size_t>(ns));
+    ck(cudaMemcpyAsync(sel.data(), m->s_idx2.p, ns * 4, cudaMemcpyDeviceToHost, m->stream), "D2H");
+    ck(cudaMemcpyAsync(slp.data(), m->s_lpk2.p, ns * 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
+    ck(cudaStreamSynchronize(m->stream), "sync");
+    // 2. weights re-renormalised over the subset, Ē (sr.cpp:36-53), gathered keys
+    double mx = slp[0];
+    for (double v : slp) mx = std::max(mx, v);
+    std::vector<double> w(static_cast<size_t>(ns)), sw(static_cast<size_t>(ns));
+    double sum = 0.0;
+    for (int64_t i = 0; i < ns; ++i) sum += (w[i] = std::exp(slp[i] - mx));
+    for (int64_t i = 0; i < ns; ++i) {
+      w[i] /= sum;
+      sw[i] = std::sqrt(w[i]);
+    }
+    m->s_keys.ensure(ns * W * 8 + 16);
+    k_gather_rows_u64<<<std::max(1, static_cast<int>(std::min<int64_t>((ns * W + 255) / 256, 4096))), 256, 0,
+                        m->stream>>>(dk, m->s_idx2.as<uint32_t>(), ns, W, m->s_keys.as<uint64_t>());
+    ck_launch("gather keys");
+    check_in_sector(m, m->s_keys.as<uint64_t>(), ns);
+    // 3. Jacobian rows R [ns][P] (k_grad_part with coefficients (1, 1), then the outer products)
+    m->s_coef1.ensure(ns * 16 + 16);
+    {
+      std::vector<double> ones(static_cast<size_t>(2 * ns), 1.0);
+      ck(cudaMemcpyAsync(m->s_coef1.p, ones.data(), ns * 16, cudaMemcpyHostToDevice, m->stream), "H2D");
+    }
+    const int nb = 2 * m->n_qudits, nq = m->n;
+    const size_t vb = static_cast<size_t>(nb) * ns * 64 * 8;
+    m->g_h1.ensure(vb);
+    m->g_h2.ensure(vb);
+    m->g_g.ensure(vb);
+    m->g_gz2.ensure(vb);
+    m->g_gz1.ensure(vb);
+    m->g_x.ensure(static_cast<size_t>(ns) * nq * 8);
+    ModelView V{m->P.as<double>(), m->n, m->n_qudits, m->bits, m->n_e, m->spin, m->n_up};
+    const auto boff = block_offsets(m);
+    m->s_boff.ensure(boff.size() * 8);
+    ck(cudaMemcpyAsync(m->s_boff.p, boff.data(), boff.size() * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
+    const size_t dyn = (16640 + kGWarps * 64 * kWT) * sizeof(double) + kGWarps * kWT * W * sizeof(uint64_t);
+    DISPATCH_W(W, {
+      ck(cudaFuncSetAttribute(k_grad_part<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)),
+         "smem attribute");
+      const int64_t per = 512, S = (ns + per - 1) / per;
+      k_grad_part<WW><<<static_cast<unsigned>(S * nb), kGThreads, dyn, m->stream>>>(
+          V, m->s_keys.as<uint64_t>(), ns, per, m->s_coef1.as<double2>(), m->g_h1.as<double>(), m->g_h2.as<double>(),
+          m->g_g.as<double>(), m->g_gz2.as<double>(), m->g_gz1.as<double>());
+      ck_launch("sr grad part");
+      k_pm_bits<WW><<<std::max(1, static_cast<int>(std::min<int64_t>((ns * nq + 255) / 256, 4096))), 256, 0,
+                      m->stream>>>(m->s_keys.as<uint64_t>(), ns, nq, m->g_x.as<double>());
+      ck_launch("sr pm bits");
+    });
+    m->s_R.ensure(static_cast<size_t>(ns) * P * 8);
+    k_jac_real<<<dim3(static_cast<unsigned>(ns), nb), 256, 0, m->stream>>>(
+        V, m->s_boff.as<int64_t>(), ns, m->g_h1.as<double>(), m->g_h2.as<double>(), m->g_g.as<double>(),
+        m->g_gz2.as<double>(), m->g_gz1.as<double>(), m->g_x.as<double>(), P, m->s_R.as<double>());
+    ck_launch("jacobian rows");
+    // 4. mean row, stacked [2 ns][P]
+    if (!m->blas) blas_ck(cublasCreate(&m->blas), "cublasCreate");
+    blas_ck(cublasSetStream(m->blas, m->stream), "cublasSetStream");
+    m->s_sw.ensure(ns * 16 + 16);
+    ck(cudaMemcpyAsync(m->s_sw.p, w.data(), ns * 8, cudaMemcpyHostToDevice, m->stream), "H2D w");
+    ck(cudaMemcpyAsync(m->s_sw.as<double>() + ns, sw.data(), ns * 8, cudaMemcpyHostToDevice, m->stream), "H2D sw");
+    m->s_mean.ensure(P * 8);
+    const double one = 1.0, zero = 0.0;
+    blas_ck(cublasDgemv(m->blas, CUBLAS_OP_N, static_cast<int>(P), static_cast<int>(ns), &one, m->s_R.as<double>(),
+                        static_cast<int>(P), m->s_sw.as<double>(), 1, &zero, m->s_mean.as<double>(), 1), "gemv mean");
+    m->s_S.ensure(static_cast<size_t>(2 * ns) * P * 8);
+    k_sr_stack<<<dim3(static_cast<unsigned>(ns), nb), 256, 0, m->stream>>>(
+        V, m->s_boff.as<int64_t>(), ns, m->s_R.as<double>(), m->s_mean.as<double>(), m->s_sw.as<double>() + ns, P,
+        m->s_S.as<double>());
+    ck_launch("sr stack");
+    // 5. lambda: given, or 1e-4 (1 + ||stacked||_F^2 / n_sr) (sr.cpp:68-71)
+    double lam = lambda;
+    if (!(lam > 0.0)) {
+      double nrm = 0.0;
+      blas_ck(cublasSetPointerMode(m->blas, CUBLAS_POINTER_MODE_HOST), "pointer mode");
+      blas_ck(cublasDnrm2(m->blas, static_cast<int>(2 * ns * P), m->s_S.as<double>(), 1, &nrm), "dnrm2");
+      lam = 1e-4 * (1.0 + nrm * nrm / static_cast<double>(ns));
+    }
+    double* dout = out_direction;
+    if (mem == QVMC_MEM_HOST) {
+      m->s_dir.ensure(P * 8);
+      dout = m->s_dir.as<double>();
+    }
+    sr_solve_device(m, 2 * ns, P, m->s_S.as<double>(), lam, dgr, dout);
+    if (mem == QVMC_MEM_HOST) ck(cudaMemcpyAsync(out_direction, dout, P * 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
+    ck(cudaStreamSynchronize(m->stream), "sync");
+    if (out_lambda) *out_lambda = lam;
   });
 }
 

@@ -1059,6 +1059,57 @@ __global__ void k_grad_scatter(const ModelView M, const double* __restrict__ gw1
   for (int e = threadIdx.x; e < n_out; e += blockDim.x) o[e] = gb[(jh * 3 + 2) * kHid + e];
 }
 
+// Jacobian rows of selected samples (grad_log_psi, model.cpp:273-325) from
+// k_grad_part's buffers run with coefficients (1, 1): R[i][t] = d log|ψ| / dθ_t
+// for amplitude-block parameters and d φ / dθ_t for phase-block ones (the
+// complex row is R on the amplitude blocks and -i R on the phase blocks).
+// Block jh of the flat layout starts at boff[jh]. One CTA per (row, block).
+__global__ void k_jac_real(const ModelView M, const int64_t* __restrict__ boff, int64_t N, const double* __restrict__ H1,
+                           const double* __restrict__ H2, const double* __restrict__ G, const double* __restrict__ GZ2,
+                           const double* __restrict__ GZ1, const double* __restrict__ X, int64_t ld,
+                           double* __restrict__ R) {
+  const int64_t i = blockIdx.x;
+  const int jh = blockIdx.y, j = jh >> 1;
+  const int n = M.n, off = j * M.bits, k = min(M.bits, n - off), n_out = 1 << k;
+  const int64_t v0 = (static_cast<int64_t>(jh) * N + i) * 64;
+  const double *h1 = H1 + v0, *h2 = H2 + v0, *g = G + v0, *gz2 = GZ2 + v0, *gz1 = GZ1 + v0, *x = X + i * n;
+  double* o = R + i * ld + boff[jh];
+  for (int e = threadIdx.x; e < kHid * n; e += blockDim.x) {  // W1[h][c] = gz1[h] e[c], e = ±1 before the offset
+    const int h = e / n, c = e - h * n;
+    o[e] = c < off ? gz1[h] * x[c] : 0.0;
+  }
+  o += kHid * n;
+  for (int e = threadIdx.x; e < kHid; e += blockDim.x) o[e] = gz1[e];
+  o += kHid;
+  for (int e = threadIdx.x; e < kHid * kHid; e += blockDim.x) o[e] = gz2[e >> 6] * h1[e & 63];
+  o += kHid * kHid;
+  for (int e = threadIdx.x; e < kHid; e += blockDim.x) o[e] = gz2[e];
+  o += kHid;
+  for (int e = threadIdx.x; e < n_out * kHid; e += blockDim.x) o[e] = g[e >> 6] * h2[e & 63];
+  o += n_out * kHid;
+  for (int e = threadIdx.x; e < n_out; e += blockDim.x) o[e] = g[e];
+}
+
+// build_sr_context (sr.cpp:25-72) rows: stacked[i] = Re(sqrt(w_i)(row_i - mean)),
+// stacked[n+i] = Im(...). The row is real on the amplitude blocks and -i R on
+// the phase blocks, so stacked[i] holds only amplitude columns and
+// stacked[n+i] only phase columns (negated). One CTA per (row, block).
+__global__ void k_sr_stack(const ModelView M, const int64_t* __restrict__ boff, int64_t n_sr,
+                           const double* __restrict__ R, const double* __restrict__ mean,
+                           const double* __restrict__ sw, int64_t ld, double* __restrict__ S) {
+  const int64_t i = blockIdx.x;
+  const int jh = blockIdx.y, hd = jh & 1;
+  const int64_t b0 = boff[jh], b1 = boff[jh + 1];
+  const double si = sw[i];
+  double* re = S + i * ld;
+  double* im = S + (n_sr + i) * ld;
+  for (int64_t t = b0 + threadIdx.x; t < b1; t += blockDim.x) {
+    const double c = si * (R[i * ld + t] - mean[t]);
+    re[t] = hd ? 0.0 : c;
+    im[t] = hd ? -c : 0.0;
+  }
+}
+
 // log ψ = Σ_j log_amp_j[v_j], φ = Σ_j phase_j[v_j] in qudit order; masked
 // states (-inf, 0) (model.cpp:254-271)
 template <int W>

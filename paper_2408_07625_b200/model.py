@@ -121,6 +121,28 @@ class AnqsModel:
     def synchronize(self) -> None:
         _lib.check(_lib.lib().qvmc_cuda_model_synchronize(self._h))
 
+    def sr_direction(self, keys: np.ndarray, log_probs, locals_, n_sr: int, grad, lam: float = 0.0):
+        """The SR step of run_optimisation (optimizer.cpp:105-143) on the device: top_probability_indices,
+        grad_log_psi rows, build_sr_context and sr_direction (sr.cpp:15-95). Returns (direction, lambda)."""
+        keys = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1, self.W)
+        lp = np.ascontiguousarray(log_probs, dtype=np.float64)
+        loc = np.ascontiguousarray(locals_, dtype=np.complex128)
+        g = np.ascontiguousarray(grad, dtype=np.float64)
+        out = np.zeros(self.n_params())
+        lam_out = C.c_double()
+        _lib.check(_lib.lib().qvmc_cuda_sr_direction(self._h, keys.shape[0], _ptr(keys), _ptr(lp), _ptr(loc), n_sr,
+                                                     lam, _ptr(g), _lib.MEM_HOST, _ptr(out), C.byref(lam_out)))
+        return out, lam_out.value
+
+    def sr_solve(self, stacked, lam: float, grad) -> np.ndarray:
+        """sr_direction (sr.cpp:74-95) for a given stacked matrix [2 n_sr][cols] and lambda > 0."""
+        S = np.ascontiguousarray(stacked, dtype=np.float64)
+        g = np.ascontiguousarray(grad, dtype=np.float64)
+        out = np.zeros(S.shape[1])
+        _lib.check(_lib.lib().qvmc_cuda_sr_solve(self._h, S.shape[0], S.shape[1], _ptr(S), lam, _ptr(g),
+                                                 _lib.MEM_HOST, _ptr(out)))
+        return out
+
     def energy_gradient(self, keys: np.ndarray, weights, locals_) -> np.ndarray:
         """energy_gradient (energy.cpp:93-107) over batched_grad_log_psi rows (model.cpp:273-336) of
         ``keys``, contracted on the device (the Jacobian is never formed): [n_params], reference layout."""
