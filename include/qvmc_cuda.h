@@ -268,6 +268,17 @@ int qvmc_cuda_model_synchronize(qvmc_model_t m);
  * "state is masked"). Synchronises. */
 int qvmc_cuda_energy_gradient(qvmc_model_t m, int64_t n, const uint64_t* keys, const double* weights,
                               const double* locals, int mem, double* out_grad);
+/* AnqsModel::params() (model.hpp:66): the flat parameter vector (the model
+ * keeps a device copy next to the kernels' layout). */
+int qvmc_cuda_model_get_params(qvmc_model_t m, int mem, double* out);
+/* adam_step (proj/src/optimizer.cpp:17-31) followed by model.set_params
+ * (optimizer.cpp:157), all on the device: bias-corrected Adam with the
+ * model's own state (zero on first use, step counter kept), then the
+ * kernels' layout refreshed from the updated flat vector. A non-finite
+ * direction entry: QVMC_ERR_RUNTIME "adam_step: non-finite direction entry",
+ * nothing updated. direction [n_params] in host or device memory. */
+int qvmc_cuda_model_adam_step(qvmc_model_t m, const double* direction, double learning_rate, double beta1,
+                              double beta2, double epsilon, int mem);
 /* sr_direction (proj/src/sr.cpp:74-95) for a given SrContext: stacked
  * row-major [rows][cols] (rows = 2 n_sr), lambda > 0, grad [cols]: the
  * push-through solve with the Gram eigensystem (cuSOLVER syevd); the

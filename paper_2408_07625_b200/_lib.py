@@ -95,6 +95,8 @@ SIGNATURES = [
     ("qvmc_cuda_fill_amplitudes", _INT, [_P, _I64, _P, _P, _INT, _P, _P, _P]),
     ("qvmc_cuda_model_synchronize", _INT, [_P]),
     ("qvmc_cuda_energy_gradient", _INT, [_P, _I64, _P, _P, _P, _INT, _P]),
+    ("qvmc_cuda_model_get_params", _INT, [_P, _INT, _P]),
+    ("qvmc_cuda_model_adam_step", _INT, [_P, _P, C.c_double, C.c_double, C.c_double, C.c_double, _INT]),
     ("qvmc_cuda_sr_solve", _INT, [_P, _I64, _I64, _P, C.c_double, _P, _INT, _P]),
     ("qvmc_cuda_sr_direction", _INT, [_P, _I64, _P, _P, _P, _INT, C.c_double, _P, _INT, _P, C.POINTER(C.c_double)]),
     ("qvmc_cuda_sample", _INT, [_P, _INT, _U64, C.c_uint32, C.c_uint32, _INT, _P, _P, C.POINTER(_I64)]),

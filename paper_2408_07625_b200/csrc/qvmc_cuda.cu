@@ -1935,6 +1935,9 @@ struct qvmc_model_s {
   // SR: selection, Jacobian rows, stacked matrix, Gram eigensystem
   DBuf s_lpk, s_lpk2, s_idx, s_idx2, s_keys, s_sw, s_R, s_mean, s_S, s_gram, s_w, s_t, s_u, s_dir, s_boff, s_info,
       s_work, s_grad, s_coef1, s_tmp;
+  // device-resident flat parameters (AnqsModel::params) and Adam state (optimizer.cpp:17-31)
+  DBuf theta, adam_m, adam_v, adam_d, adam_bad, p_boff;
+  long adam_t = 0;
   ~qvmc_model_s() {
     if (blas) cublasDestroy(blas);
     if (solver) cusolverDnDestroy(solver);
@@ -2117,6 +2120,8 @@ int qvmc_cuda_model_set_params(qvmc_model_t m, int64_t n_params, const double* p
     DeviceGuard dg(m->device);
     m->P.ensure(dev.size() * sizeof(double));
     ck(cudaMemcpyAsync(m->P.p, dev.data(), dev.size() * sizeof(double), cudaMemcpyHostToDevice, m->stream), "H2D params");
+    m->theta.ensure(m->n_params * 8);  // the flat vector stays on the device too (Adam, get_params)
+    ck(cudaMemcpyAsync(m->theta.p, params, m->n_params * 8, cudaMemcpyHostToDevice, m->stream), "H2D theta");
     ck(cudaStreamSynchronize(m->stream), "sync");  // the host staging vector goes out of scope
     m->has_params = true;
   });
@@ -2670,6 +2675,72 @@ int qvmc_cuda_sr_direction(qvmc_model_t m, int64_t n, const uint64_t* keys, cons
     if (mem == QVMC_MEM_HOST) ck(cudaMemcpyAsync(out_direction, dout, P * 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
     ck(cudaStreamSynchronize(m->stream), "sync");
     if (out_lambda) *out_lambda = lam;
+  });
+}
+
+// AnqsModel::params() (model.hpp:66): the flat vector, host or device copy.
+int qvmc_cuda_model_get_params(qvmc_model_t m, int mem, double* out) {
+  return guarded([&] {
+    check_model(m);
+    check_mem(mem);
+    if (!out) fail(QVMC_ERR_INVALID_ARGUMENT, "null output");
+    if (!m->has_params) fail(QVMC_ERR_INVALID_ARGUMENT, "model parameters not set");
+    DeviceGuard dg(m->device);
+    ck(cudaMemcpyAsync(out, m->theta.p, m->n_params * 8,
+                       mem == QVMC_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, m->stream), "copy");
+    ck(cudaStreamSynchronize(m->stream), "sync");
+  });
+}
+
+// adam_step (optimizer.cpp:17-31) + model.set_params(theta) (optimizer.cpp:157) with
+// the parameters, the Adam state (created zero on first use) and the kernels' layout
+// all on the device.
+int qvmc_cuda_model_adam_step(qvmc_model_t m, const double* direction, double learning_rate, double beta1,
+                              double beta2, double epsilon, int mem) {
+  return guarded([&] {
+    check_model(m);
+    check_mem(mem);
+    if (!direction) fail(QVMC_ERR_INVALID_ARGUMENT, "null direction");
+    if (!m->has_params) fail(QVMC_ERR_INVALID_ARGUMENT, "model parameters not set");
+    using namespace qvmc_model;
+    DeviceGuard dg(m->device);
+    const int64_t P = m->n_params;
+    if (m->adam_m.bytes < static_cast<size_t>(P) * 8) {
+      m->adam_m.ensure(P * 8);
+      m->adam_v.ensure(P * 8);
+      ck(cudaMemsetAsync(m->adam_m.p, 0, P * 8, m->stream), "memset");
+      ck(cudaMemsetAsync(m->adam_v.p, 0, P * 8, m->stream), "memset");
+      m->adam_t = 0;
+    }
+    const double* dd = direction;
+    if (mem == QVMC_MEM_HOST) {
+      m->adam_d.ensure(P * 8);
+      ck(cudaMemcpyAsync(m->adam_d.p, direction, P * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
+      dd = m->adam_d.as<double>();
+    }
+    m->adam_bad.ensure(16);
+    ck(cudaMemsetAsync(m->adam_bad.p, 0, 4, m->stream), "memset");
+    const int grid = static_cast<int>(std::min<int64_t>((P + 255) / 256, 8LL * m->sms));
+    k_adam_check<<<grid, 256, 0, m->stream>>>(dd, P, m->adam_bad.as<int>());
+    ck_launch("adam check");
+    const long t = m->adam_t + 1;
+    const double c1 = 1.0 - std::pow(beta1, static_cast<double>(t)), c2 = 1.0 - std::pow(beta2, static_cast<double>(t));
+    k_adam<<<grid, 256, 0, m->stream>>>(dd, P, learning_rate, beta1, beta2, epsilon, c1, c2, m->adam_bad.as<int>(),
+                                        m->adam_m.as<double>(), m->adam_v.as<double>(), m->theta.as<double>());
+    ck_launch("adam");
+    int bad = 0;
+    ck(cudaMemcpyAsync(&bad, m->adam_bad.p, 4, cudaMemcpyDeviceToHost, m->stream), "D2H");
+    ck(cudaStreamSynchronize(m->stream), "sync");
+    if (bad) fail(QVMC_ERR_RUNTIME, "adam_step: non-finite direction entry");
+    m->adam_t = t;
+    const auto boff = block_offsets(m);
+    m->p_boff.ensure(boff.size() * 8);
+    ck(cudaMemcpyAsync(m->p_boff.p, boff.data(), boff.size() * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
+    ModelView V{m->P.as<double>(), m->n, m->n_qudits, m->bits, m->n_e, m->spin, m->n_up};
+    k_params_relayout<<<2 * m->n_qudits, 256, 0, m->stream>>>(V, m->p_boff.as<int64_t>(), m->theta.as<double>(),
+                                                              m->P.as<double>());
+    ck_launch("params relayout");
+    ck(cudaStreamSynchronize(m->stream), "sync");
   });
 }
 

@@ -1110,6 +1110,65 @@ __global__ void k_sr_stack(const ModelView M, const int64_t* __restrict__ boff, 
   }
 }
 
+// adam_step (optimizer.cpp:17-31) on the device-resident flat parameters;
+// c1, c2 = bias corrections of this step. A non-finite direction entry sets *bad
+// and leaves everything unchanged (the reference throws before updating).
+__global__ void k_adam_check(const double* __restrict__ d, int64_t n, int* __restrict__ bad) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (!isfinite(d[i])) atomicOr(bad, 1);
+}
+
+__global__ void k_adam(const double* __restrict__ d, int64_t n, double lr, double b1, double b2, double eps, double c1,
+                       double c2, const int* __restrict__ bad, double* __restrict__ m, double* __restrict__ v,
+                       double* __restrict__ theta) {
+  if (*bad) return;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double g = d[i];
+    const double mi = b1 * m[i] + (1.0 - b1) * g;
+    const double vi = b2 * v[i] + (1.0 - b2) * (g * g);
+    m[i] = mi;
+    v[i] = vi;
+    theta[i] -= lr * (mi / c1) / (sqrt(vi / c2) + eps);
+  }
+}
+
+// set_params on the device: the flat layout (model.cpp:65-80) -> the kernels'
+// block layout (BlockLayout: W1ᵀ, prefix column sums, W2ᵀ, W3ᵀ zero-padded),
+// the same arithmetic as the host re-layout (column sums in i order). One CTA per block.
+__global__ void k_params_relayout(const ModelView M, const int64_t* __restrict__ boff, const double* __restrict__ theta,
+                                  double* __restrict__ P) {
+  const int jh = blockIdx.x, j = jh >> 1;
+  const int n = M.n, off = j * M.bits, k = min(M.bits, n - off), n_out = 1 << k;
+  const BlockLayout L{n};
+  const double* w1 = theta + boff[jh];
+  const double* b1 = w1 + kHid * n;
+  const double* w2 = b1 + kHid;
+  const double* b2 = w2 + kHid * kHid;
+  const double* w3 = b2 + kHid;
+  const double* b3 = w3 + n_out * kHid;
+  double* B = P + static_cast<int64_t>(jh) * L.size();
+  for (int e = threadIdx.x; e < kHid * n; e += blockDim.x) {
+    const int h = e / n, i = e - h * n;
+    B[L.w1t() + i * kHid + h] = w1[e];
+  }
+  for (int h = threadIdx.x; h < kHid; h += blockDim.x) {
+    double c = 0.0;
+    for (int i = 0; i < off; ++i) c += w1[h * n + i];
+    B[L.csum() + h] = c;
+    B[L.b1() + h] = b1[h];
+    B[L.b2() + h] = b2[h];
+    B[L.b3() + h] = h < n_out ? b3[h] : 0.0;
+  }
+  for (int e = threadIdx.x; e < kHid * kHid; e += blockDim.x) {
+    const int h = e >> 6, kk = e & 63;
+    B[L.w2t() + kk * kHid + h] = w2[e];
+    const int v = e >> 6;  // W3[v][kk]
+    B[L.w3t() + kk * kHid + v] = v < n_out ? w3[v * kHid + kk] : 0.0;
+  }
+}
+
 // log ψ = Σ_j log_amp_j[v_j], φ = Σ_j phase_j[v_j] in qudit order; masked
 // states (-inf, 0) (model.cpp:254-271)
 template <int W>

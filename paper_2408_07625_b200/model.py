@@ -121,6 +121,19 @@ class AnqsModel:
     def synchronize(self) -> None:
         _lib.check(_lib.lib().qvmc_cuda_model_synchronize(self._h))
 
+    def adam_step(self, direction, learning_rate: float = 1e-3, beta1: float = 0.9, beta2: float = 0.999,
+                  epsilon: float = 1e-8) -> None:
+        """adam_step (optimizer.cpp:17-31) + set_params (optimizer.cpp:157) on the device, with the
+        model's own Adam state; the host copy of the parameters is refreshed from the device."""
+        d = np.ascontiguousarray(direction, dtype=np.float64)
+        if d.shape != (self.n_params(),):
+            raise ValueError("adam_step: size mismatch")
+        _lib.check(_lib.lib().qvmc_cuda_model_adam_step(self._h, _ptr(d), learning_rate, beta1, beta2, epsilon,
+                                                        _lib.MEM_HOST))
+        out = np.zeros(self.n_params())
+        _lib.check(_lib.lib().qvmc_cuda_model_get_params(self._h, _lib.MEM_HOST, _ptr(out)))
+        self._params = out
+
     def sr_direction(self, keys: np.ndarray, log_probs, locals_, n_sr: int, grad, lam: float = 0.0):
         """The SR step of run_optimisation (optimizer.cpp:105-143) on the device: top_probability_indices,
         grad_log_psi rows, build_sr_context and sr_direction (sr.cpp:15-95). Returns (direction, lambda)."""
