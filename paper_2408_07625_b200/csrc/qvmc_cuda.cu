@@ -2276,65 +2276,96 @@ __global__ void k_sector_flags(const uint64_t* __restrict__ keys, int64_t n, int
 // into m->g_w1/g_w2/g_w3/g_b; coef [n] device (2 Re c, 2 Im c); keys device
 void grad_accumulate(qvmc_model_s* m, const uint64_t* keys, int64_t n, const double2* coef) {
   using namespace qvmc_model;
-  const int nb = 2 * m->n_qudits, nq = m->n, W = m->W;
+  const int nb = 2 * m->n_qudits, nq = m->n, W = m->W, nx = nq + 2;
   ModelView V{m->P.as<double>(), m->n, m->n_qudits, m->bits, m->n_e, m->spin, m->n_up};
   if (!m->blas) blas_ck(cublasCreate(&m->blas), "cublasCreate");
   blas_ck(cublasSetStream(m->blas, m->stream), "cublasSetStream");
+  // split-K: every chunk's sample range is cut into `parts` slices so the
+  // batched GEMMs (64 x 64 outputs, one per block) fill the SMs; partial sums
+  // are added in part order by k_sum_parts (deterministic)
+  const int parts = nb <= 24 ? 16 : 8;
   const int64_t Nc = std::min<int64_t>(std::max<int64_t>(n, 1), 32768);
-  const size_t vb = static_cast<size_t>(nb) * Nc * 64 * 8;
-  m->g_h1.ensure(vb);
-  m->g_h2.ensure(vb);
-  m->g_g.ensure(vb);
-  m->g_gz2.ensure(vb);
-  m->g_gz1.ensure(vb);
-  m->g_x.ensure(static_cast<size_t>(Nc) * nq * 8);
-  m->g_ones.ensure(static_cast<size_t>(Nc) * 8);
-  m->g_w1.ensure(static_cast<size_t>(nb) * 64 * nq * 8);
-  m->g_w2.ensure(static_cast<size_t>(nb) * 4096 * 8);
-  m->g_w3.ensure(static_cast<size_t>(nb) * 4096 * 8);
-  m->g_b.ensure(static_cast<size_t>(nb) * 3 * 64 * 8);
-  {
-    std::vector<double> ones(static_cast<size_t>(Nc), 1.0);
-    ck(cudaMemcpyAsync(m->g_ones.p, ones.data(), Nc * 8, cudaMemcpyHostToDevice, m->stream), "H2D ones");
-    ck(cudaStreamSynchronize(m->stream), "sync");
-  }
+  const int64_t Kp_max = ((Nc + parts - 1) / parts + 7) / 8 * 8;
+  const int64_t Ncp = Kp_max * parts;  // padded chunk rows
+  m->g_h1.ensure(static_cast<size_t>(nb) * Ncp * kHS * 8);
+  m->g_h2.ensure(static_cast<size_t>(nb) * Ncp * kHS * 8);
+  m->g_g.ensure(static_cast<size_t>(nb) * Ncp * 64 * 8);
+  m->g_gz2.ensure(static_cast<size_t>(nb) * Ncp * 64 * 8);
+  m->g_gz1.ensure(static_cast<size_t>(nb) * Ncp * 64 * 8);
+  m->g_x.ensure(static_cast<size_t>(Ncp) * nx * 8);
+  const size_t l1 = static_cast<size_t>(64) * nx, l2 = static_cast<size_t>(64) * kHS;
+  m->g_ones.ensure(static_cast<size_t>(nb) * parts * std::max(l1, l2) * 8);  // split-K partials (reused)
+  m->g_w1.ensure(static_cast<size_t>(nb) * l1 * 8);
+  m->g_w2.ensure(static_cast<size_t>(nb) * l2 * 8);
+  m->g_w3.ensure(static_cast<size_t>(nb) * l2 * 8);
   const size_t dyn = (16640 + kGWarps * 64 * kWT) * sizeof(double) + kGWarps * kWT * W * sizeof(uint64_t);
   const double one = 1.0, zero = 0.0;
+  // pointer arrays of the W1 GEMMs (X is shared by the blocks, so its slice depends on the part only)
+  std::vector<const double*> pa(static_cast<size_t>(nb) * parts), pb(pa.size());
+  std::vector<double*> pc(pa.size());
+  m->s_tmp.ensure(pa.size() * 3 * sizeof(void*) + 16);
   for (int64_t c0 = 0; c0 < n; c0 += Nc) {
     const int64_t nc = std::min<int64_t>(Nc, n - c0);
+    const int64_t Kp = ((nc + parts - 1) / parts + 7) / 8 * 8;
+    const int64_t Ncur = Kp * parts;  // this chunk's padded rows: rows >= nc must be zero
+    if (Ncur > nc) {
+      ck(cudaMemsetAsync(m->g_h1.p, 0, static_cast<size_t>(nb) * Ncur * kHS * 8, m->stream), "memset");
+      ck(cudaMemsetAsync(m->g_h2.p, 0, static_cast<size_t>(nb) * Ncur * kHS * 8, m->stream), "memset");
+      ck(cudaMemsetAsync(m->g_g.p, 0, static_cast<size_t>(nb) * Ncur * 64 * 8, m->stream), "memset");
+      ck(cudaMemsetAsync(m->g_gz2.p, 0, static_cast<size_t>(nb) * Ncur * 64 * 8, m->stream), "memset");
+      ck(cudaMemsetAsync(m->g_gz1.p, 0, static_cast<size_t>(nb) * Ncur * 64 * 8, m->stream), "memset");
+      ck(cudaMemsetAsync(m->g_x.p, 0, static_cast<size_t>(Ncur) * nx * 8, m->stream), "memset");
+    }
     const int64_t per = 512;  // samples per CTA
     const int64_t S = (nc + per - 1) / per;
     DISPATCH_W(W, {
       ck(cudaFuncSetAttribute(k_grad_part<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)),
          "smem attribute");
+      // block stride Ncur rows: the kernel indexes block jh at jh * N * stride with N = Ncur
       k_grad_part<WW><<<static_cast<unsigned>(S * nb), kGThreads, dyn, m->stream>>>(
           V, keys + c0 * WW, nc, per, coef + c0, m->g_h1.as<double>(), m->g_h2.as<double>(), m->g_g.as<double>(),
-          m->g_gz2.as<double>(), m->g_gz1.as<double>());
+          m->g_gz2.as<double>(), m->g_gz1.as<double>(), Ncur);
       ck_launch("grad part");
-      const int xg = static_cast<int>(std::min<int64_t>((nc * nq + 255) / 256, 8LL * m->sms));
+      const int xg = static_cast<int>(std::min<int64_t>((nc * nx + 255) / 256, 8LL * m->sms));
       k_pm_bits<WW><<<xg, 256, 0, m->stream>>>(keys + c0 * WW, nc, nq, m->g_x.as<double>());
       ck_launch("pm bits");
     });
-    const double* beta = c0 == 0 ? &zero : &one;
-    const long long sv = static_cast<long long>(nc) * 64;  // chunk stride of a block's vectors (ld 64)
-    // gW1[jh] (col-major n x 64) = X (n x nc) . GZ1ᵀ
-    blas_ck(cublasDgemmStridedBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, nq, 64, static_cast<int>(nc), &one,
-                                      m->g_x.as<double>(), nq, 0, m->g_gz1.as<double>(), 64, sv, beta,
-                                      m->g_w1.as<double>(), nq, 64LL * nq, nb), "dgemm w1");
-    // gW2[jh] (64 k x 64 h) = H1 . GZ2ᵀ ; gW3[jh] (64 h x 64 v) = H2 . Gᵀ
-    blas_ck(cublasDgemmStridedBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, 64, 64, static_cast<int>(nc), &one,
-                                      m->g_h1.as<double>(), 64, sv, m->g_gz2.as<double>(), 64, sv, beta,
-                                      m->g_w2.as<double>(), 64, 4096, nb), "dgemm w2");
-    blas_ck(cublasDgemmStridedBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, 64, 64, static_cast<int>(nc), &one,
-                                      m->g_h2.as<double>(), 64, sv, m->g_g.as<double>(), 64, sv, beta,
-                                      m->g_w3.as<double>(), 64, 4096, nb), "dgemm w3");
-    // biases: Σ_s of gz1, gz2, g
-    const double* vecs[3] = {m->g_gz1.as<double>(), m->g_gz2.as<double>(), m->g_g.as<double>()};
-    for (int q = 0; q < 3; ++q)
-      blas_ck(cublasDgemmStridedBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_N, 64, 1, static_cast<int>(nc), &one,
-                                        vecs[q], 64, sv, m->g_ones.as<double>(), static_cast<int>(nc), 0, beta,
-                                        m->g_b.as<double>() + 64 * q, 64, 192, nb), "dgemm bias");
-    g_launches += 6;
+    const int first = c0 == 0 ? 1 : 0;
+    double* part = m->g_ones.as<double>();
+    // gW2 / gW3 (+ gb2 / gb3 in row 64): batch b = jh * parts + p, A = H[b * Kp rows], B = vectors[b * Kp rows]
+    blas_ck(cublasDgemmStridedBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, kHS, 64, static_cast<int>(Kp), &one,
+                                      m->g_h1.as<double>(), kHS, Kp * kHS, m->g_gz2.as<double>(), 64, Kp * 64,
+                                      &zero, part, kHS, static_cast<long long>(l2), nb * parts), "dgemm w2");
+    k_sum_parts<<<static_cast<int>(std::min<size_t>((nb * l2 + 255) / 256, 4096)), 256, 0, m->stream>>>(
+        part, nb, parts, static_cast<int64_t>(l2), first, m->g_w2.as<double>());
+    blas_ck(cublasDgemmStridedBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, kHS, 64, static_cast<int>(Kp), &one,
+                                      m->g_h2.as<double>(), kHS, Kp * kHS, m->g_g.as<double>(), 64, Kp * 64,
+                                      &zero, part, kHS, static_cast<long long>(l2), nb * parts), "dgemm w3");
+    k_sum_parts<<<static_cast<int>(std::min<size_t>((nb * l2 + 255) / 256, 4096)), 256, 0, m->stream>>>(
+        part, nb, parts, static_cast<int64_t>(l2), first, m->g_w3.as<double>());
+    // gW1 (+ gb1 in row n): pointer-array batch, X slice by part
+    for (int jh = 0; jh < nb; ++jh)
+      for (int q = 0; q < parts; ++q) {
+        const size_t b2 = static_cast<size_t>(jh) * parts + q;
+        pa[b2] = m->g_x.as<double>() + q * Kp * nx;
+        pb[b2] = m->g_gz1.as<double>() + (static_cast<int64_t>(jh) * Ncur + q * Kp) * 64;
+        pc[b2] = part + b2 * l1;
+      }
+    void** dp = static_cast<void**>(m->s_tmp.p);
+    ck(cudaMemcpyAsync(dp, pa.data(), pa.size() * sizeof(void*), cudaMemcpyHostToDevice, m->stream), "H2D ptrs");
+    ck(cudaMemcpyAsync(dp + pa.size(), pb.data(), pb.size() * sizeof(void*), cudaMemcpyHostToDevice, m->stream),
+       "H2D ptrs");
+    ck(cudaMemcpyAsync(dp + 2 * pa.size(), pc.data(), pc.size() * sizeof(void*), cudaMemcpyHostToDevice, m->stream),
+       "H2D ptrs");
+    blas_ck(cublasDgemmBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, nx, 64, static_cast<int>(Kp), &one,
+                               reinterpret_cast<const double* const*>(dp), nx,
+                               reinterpret_cast<const double* const*>(dp + pa.size()), 64, &zero,
+                               reinterpret_cast<double* const*>(dp + 2 * pa.size()), nx, nb * parts), "dgemm w1");
+    k_sum_parts<<<static_cast<int>(std::min<size_t>((nb * l1 + 255) / 256, 4096)), 256, 0, m->stream>>>(
+        part, nb, parts, static_cast<int64_t>(l1), first, m->g_w1.as<double>());
+    ck_launch("split-K sums");
+    ck(cudaStreamSynchronize(m->stream), "sync");  // the host pointer arrays are reused by the next chunk
+    g_launches += 5;
   }
 }
 
@@ -2496,7 +2527,7 @@ int qvmc_cuda_energy_gradient(qvmc_model_t m, int64_t n, const uint64_t* keys, c
       dout = m->g_out.as<double>();
     }
     k_grad_scatter<<<2 * m->n_qudits, 256, 0, m->stream>>>(V, m->g_w1.as<double>(), m->g_w2.as<double>(),
-                                                            m->g_w3.as<double>(), m->g_b.as<double>(), dout);
+                                                            m->g_w3.as<double>(), dout);
     ck_launch("gradient scatter");
     if (mem == QVMC_MEM_HOST)
       ck(cudaMemcpyAsync(out_grad, dout, m->n_params * 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
@@ -2615,12 +2646,12 @@ int qvmc_cuda_sr_direction(qvmc_model_t m, int64_t n, const uint64_t* keys, cons
     }
     const int nb = 2 * m->n_qudits, nq = m->n;
     const size_t vb = static_cast<size_t>(nb) * ns * 64 * 8;
-    m->g_h1.ensure(vb);
-    m->g_h2.ensure(vb);
+    m->g_h1.ensure(static_cast<size_t>(nb) * ns * kHS * 8);
+    m->g_h2.ensure(static_cast<size_t>(nb) * ns * kHS * 8);
     m->g_g.ensure(vb);
     m->g_gz2.ensure(vb);
     m->g_gz1.ensure(vb);
-    m->g_x.ensure(static_cast<size_t>(ns) * nq * 8);
+    m->g_x.ensure(static_cast<size_t>(ns) * (nq + 2) * 8);
     ModelView V{m->P.as<double>(), m->n, m->n_qudits, m->bits, m->n_e, m->spin, m->n_up};
     const auto boff = block_offsets(m);
     m->s_boff.ensure(boff.size() * 8);
@@ -2632,9 +2663,9 @@ int qvmc_cuda_sr_direction(qvmc_model_t m, int64_t n, const uint64_t* keys, cons
       const int64_t per = 512, S = (ns + per - 1) / per;
       k_grad_part<WW><<<static_cast<unsigned>(S * nb), kGThreads, dyn, m->stream>>>(
           V, m->s_keys.as<uint64_t>(), ns, per, m->s_coef1.as<double2>(), m->g_h1.as<double>(), m->g_h2.as<double>(),
-          m->g_g.as<double>(), m->g_gz2.as<double>(), m->g_gz1.as<double>());
+          m->g_g.as<double>(), m->g_gz2.as<double>(), m->g_gz1.as<double>(), ns);
       ck_launch("sr grad part");
-      k_pm_bits<WW><<<std::max(1, static_cast<int>(std::min<int64_t>((ns * nq + 255) / 256, 4096))), 256, 0,
+      k_pm_bits<WW><<<std::max(1, static_cast<int>(std::min<int64_t>((ns * (nq + 2) + 255) / 256, 4096))), 256, 0,
                       m->stream>>>(m->s_keys.as<uint64_t>(), ns, nq, m->g_x.as<double>());
       ck_launch("sr pm bits");
     });

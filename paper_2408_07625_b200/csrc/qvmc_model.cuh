@@ -681,12 +681,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
 // staged once per CTA next to the forward transposes.
 constexpr int kGWarps = 8;
 constexpr int kGThreads = kGWarps * 32;
+// row stride of the h1 / h2 chunk buffers: 64 activations, a constant 1 (so the
+// weight-gradient GEMM also yields the next layer's bias gradient as its last
+// row) and a zero pad
+constexpr int kHS = 66;
 
 template <int W>
 __global__ void __launch_bounds__(kGThreads, 1)
     k_grad_part(const ModelView M, const uint64_t* __restrict__ keys, int64_t N, int64_t chunk,
                 const double2* __restrict__ coef, double* __restrict__ H1, double* __restrict__ H2,
-                double* __restrict__ G, double* __restrict__ GZ2, double* __restrict__ GZ1) {
+                double* __restrict__ G, double* __restrict__ GZ2, double* __restrict__ GZ1, int64_t N_blk) {
+  // N: samples of this call; N_blk: rows per block in the buffers (>= N, padded for split-K)
   extern __shared__ __align__(16) double smem[];
   double* w2 = smem;            // [64 k][64 h]  (W2 transposed)
   double* w3 = smem + 4096;     // [64 k][64 v]  (W3 transposed)
@@ -731,8 +736,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
   uint32_t up_value_mask = 0;
   for (int t = 0; t < k; ++t)
     if ((off + t) % 2 == 0) up_value_mask |= 1u << (k - 1 - t);
-  const int64_t blk = static_cast<int64_t>(jh) * N * 64;
-  double *h1o = H1 + blk, *h2o = H2 + blk, *go = G + blk, *gz2o = GZ2 + blk, *gz1o = GZ1 + blk;
+  const int64_t blk = static_cast<int64_t>(jh) * N_blk * 64, blkh = static_cast<int64_t>(jh) * N_blk * kHS;
+  double *h1o = H1 + blkh, *h2o = H2 + blkh, *go = G + blk, *gz2o = GZ2 + blk, *gz1o = GZ1 + blk;
   auto feat = [&](int f) { return 16 * (f >> 1) + 2 * hq + (f & 1); };
 
   for (int64_t t0 = c0 + static_cast<int64_t>(warp) * kWT; t0 < c1; t0 += static_cast<int64_t>(kWT) * kGWarps) {
@@ -768,9 +773,16 @@ __global__ void __launch_bounds__(kGThreads, 1)
       cf[si] = hd ? c2.y : c2.x;
     }
     auto row = [&](int si) { return t0 + sq * 4 + si; };
-    auto put = [&](double* o, int si, int f, double v0, double v1) {  // features f, f+1 of sample si
-      if (row(si) < c1) *reinterpret_cast<double2*>(o + row(si) * 64 + feat(f)) = make_double2(v0, v1);
+    auto put = [&](double* o, int si, int f, double v0, double v1, int ld = 64) {  // features f, f+1 of sample si
+      if (row(si) < c1) *reinterpret_cast<double2*>(o + row(si) * ld + feat(f)) = make_double2(v0, v1);
     };
+    if (hq == 0)  // bias columns of this lane's 4 samples
+#pragma unroll
+      for (int si = 0; si < 4; ++si)
+        if (row(si) < c1) {
+          *reinterpret_cast<double2*>(h1o + row(si) * kHS + 64) = make_double2(1.0, 0.0);
+          *reinterpret_cast<double2*>(h2o + row(si) * kHS + 64) = make_double2(1.0, 0.0);
+        }
 
     // layer 1 -> h1 (model.cpp:171), as in k_log_psi_part
 #pragma unroll
@@ -807,7 +819,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
           a[u][f] = tanh_fast((ones ? 2.0 * a[u][f] - cs : cs - 2.0 * a[u][f]) + bias[feat(f)]);
         }
 #pragma unroll
-        for (int f = 0; f < 8; f += 2) put(h1o, si, f, a[u][f], a[u][f + 1]);
+        for (int f = 0; f < 8; f += 2) put(h1o, si, f, a[u][f], a[u][f + 1], kHS);
       }
 #pragma unroll
       for (int f = 0; f < 8; ++f)
@@ -867,7 +879,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
 #pragma unroll
     for (int si = 0; si < 4; ++si)
 #pragma unroll
-      for (int f = 0; f < 8; f += 2) put(h2o, si, f, h2[si][f], h2[si][f + 1]);
+      for (int f = 0; f < 8; f += 2) put(h2o, si, f, h2[si][f], h2[si][f + 1], kHS);
 
     // output gradient g (d/d raw output), scaled by the sample's coefficient
     double g[4][8];
@@ -967,7 +979,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
       if (row(si) >= c1) continue;
 #pragma unroll
       for (int f = 0; f < 8; f += 2) {
-        const double2 h = *reinterpret_cast<const double2*>(h1o + row(si) * 64 + feat(f));
+        const double2 h = *reinterpret_cast<const double2*>(h1o + row(si) * kHS + feat(f));
         const double v0 = (acc[si][f] + gz2[si][f]) * (1.0 - h.x * h.x);
         const double v1 = (acc[si][f + 1] + gz2[si][f + 1]) * (1.0 - h.y * h.y);
         *reinterpret_cast<double2*>(gz1o + row(si) * 64 + feat(f)) = make_double2(v0, v1);
@@ -978,14 +990,29 @@ __global__ void __launch_bounds__(kGThreads, 1)
 
 // ±1 encoding of every qubit of a chunk's keys: X[s][i] (model.cpp:153-158
 // before the prefix cut; gW1 of qudit j keeps only columns i < offset_j)
+// row stride n + 2: column n is a constant 1 (the gW1 GEMM then also yields gb1), n + 1 a zero pad
 template <int W>
 __global__ void k_pm_bits(const uint64_t* __restrict__ keys, int64_t N, int n, double* __restrict__ X) {
-  const int64_t total = N * n;
+  const int ld = n + 2;
+  const int64_t total = N * ld;
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t s = e / n;
-    const int i = static_cast<int>(e - s * n);
-    X[e] = (__ldg(keys + s * W + (i >> 6)) >> (i & 63)) & 1ull ? 1.0 : -1.0;
+    const int64_t s = e / ld;
+    const int i = static_cast<int>(e - s * ld);
+    X[e] = i == n ? 1.0 : i > n ? 0.0 : ((__ldg(keys + s * W + (i >> 6)) >> (i & 63)) & 1ull ? 1.0 : -1.0);
+  }
+}
+
+// split-K partial sums [nb][parts][len] -> acc [nb][len] in part order (deterministic); first = overwrite
+__global__ void k_sum_parts(const double* __restrict__ part, int nb, int parts, int64_t len, int first,
+                            double* __restrict__ acc) {
+  const int64_t total = static_cast<int64_t>(nb) * len;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t jh = e / len, t = e - jh * len;
+    double sum = 0.0;
+    for (int q = 0; q < parts; ++q) sum += part[(jh * parts + q) * len + t];
+    acc[e] = first ? sum : acc[e] + sum;
   }
 }
 
@@ -1034,9 +1061,10 @@ __global__ void k_wmean_final(const double2* __restrict__ part, int nb, double2*
 
 // accumulated block sums -> the reference's flat parameter layout (model.cpp:65-80)
 //   gw1 [jh][64 h][n] (columns >= offset zeroed), gw2 [jh][64 h][64 k], gw3 [jh][64 v][64 h], gb [jh][3][64]
+//   acc1 [jh][64 h][n + 2] (column n = gb1), acc2 [jh][64 h][66] (row... column 64 = gb2),
+//   acc3 [jh][64 v][66] (column 64 = gb3)
 __global__ void k_grad_scatter(const ModelView M, const double* __restrict__ gw1, const double* __restrict__ gw2,
-                               const double* __restrict__ gw3, const double* __restrict__ gb,
-                               double* __restrict__ out) {
+                               const double* __restrict__ gw3, double* __restrict__ out) {
   const int jh = blockIdx.x, j = jh >> 1;
   const int n = M.n, off = j * M.bits, k = min(M.bits, n - off), n_out = 1 << k;
   int64_t base = 0;  // flat offset of block jh
@@ -1045,18 +1073,24 @@ __global__ void k_grad_scatter(const ModelView M, const double* __restrict__ gw1
     base += static_cast<int64_t>(kHid) * n + kHid + kHid * kHid + kHid + (1 << kq) * kHid + (1 << kq);
   }
   double* o = out + base;
-  const double* a1 = gw1 + static_cast<int64_t>(jh) * kHid * n;
-  for (int e = threadIdx.x; e < kHid * n; e += blockDim.x) o[e] = (e % n) < off ? a1[e] : 0.0;
+  const int nx = n + 2;
+  const double* a1 = gw1 + static_cast<int64_t>(jh) * kHid * nx;
+  const double* a2 = gw2 + static_cast<int64_t>(jh) * kHid * kHS;
+  const double* a3 = gw3 + static_cast<int64_t>(jh) * kHid * kHS;
+  for (int e = threadIdx.x; e < kHid * n; e += blockDim.x) {
+    const int h = e / n, i = e - h * n;
+    o[e] = i < off ? a1[h * nx + i] : 0.0;
+  }
   o += kHid * n;
-  for (int e = threadIdx.x; e < kHid; e += blockDim.x) o[e] = gb[(jh * 3 + 0) * kHid + e];
+  for (int e = threadIdx.x; e < kHid; e += blockDim.x) o[e] = a1[e * nx + n];
   o += kHid;
-  for (int e = threadIdx.x; e < kHid * kHid; e += blockDim.x) o[e] = gw2[static_cast<int64_t>(jh) * 4096 + e];
+  for (int e = threadIdx.x; e < kHid * kHid; e += blockDim.x) o[e] = a2[(e >> 6) * kHS + (e & 63)];
   o += kHid * kHid;
-  for (int e = threadIdx.x; e < kHid; e += blockDim.x) o[e] = gb[(jh * 3 + 1) * kHid + e];
+  for (int e = threadIdx.x; e < kHid; e += blockDim.x) o[e] = a2[e * kHS + 64];
   o += kHid;
-  for (int e = threadIdx.x; e < n_out * kHid; e += blockDim.x) o[e] = gw3[static_cast<int64_t>(jh) * 4096 + e];
+  for (int e = threadIdx.x; e < n_out * kHid; e += blockDim.x) o[e] = a3[(e >> 6) * kHS + (e & 63)];
   o += n_out * kHid;
-  for (int e = threadIdx.x; e < n_out; e += blockDim.x) o[e] = gb[(jh * 3 + 2) * kHid + e];
+  for (int e = threadIdx.x; e < n_out; e += blockDim.x) o[e] = a3[e * kHS + 64];
 }
 
 // Jacobian rows of selected samples (grad_log_psi, model.cpp:273-325) from
@@ -1071,8 +1105,8 @@ __global__ void k_jac_real(const ModelView M, const int64_t* __restrict__ boff, 
   const int64_t i = blockIdx.x;
   const int jh = blockIdx.y, j = jh >> 1;
   const int n = M.n, off = j * M.bits, k = min(M.bits, n - off), n_out = 1 << k;
-  const int64_t v0 = (static_cast<int64_t>(jh) * N + i) * 64;
-  const double *h1 = H1 + v0, *h2 = H2 + v0, *g = G + v0, *gz2 = GZ2 + v0, *gz1 = GZ1 + v0, *x = X + i * n;
+  const int64_t v0 = (static_cast<int64_t>(jh) * N + i) * 64, vh = (static_cast<int64_t>(jh) * N + i) * kHS;
+  const double *h1 = H1 + vh, *h2 = H2 + vh, *g = G + v0, *gz2 = GZ2 + v0, *gz1 = GZ1 + v0, *x = X + i * (n + 2);
   double* o = R + i * ld + boff[jh];
   for (int e = threadIdx.x; e < kHid * n; e += blockDim.x) {  // W1[h][c] = gz1[h] e[c], e = ±1 before the offset
     const int h = e / n, c = e - h * n;
