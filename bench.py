@@ -51,6 +51,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None, help="0 skips the end-to-end leg")
+    ap.add_argument("--graph", action="store_true",
+                    help="one GPU: speculative (host-sync-free) calls, each timed step one CUDA-graph replay")
     ap.add_argument("--sharded", action="store_true",
                     help="qvmc_cuda_eloc_sharded over NCCL even at one rank (run under torchrun)")
     ap.add_argument("--profile-step", action="store_true",
@@ -380,6 +382,31 @@ def main():
         def step():
             return sharded_surrogate_energy_capi(H, comm, local, n, shard, batch.log_norm).moments
 
+    graph = None
+    if args.graph and not sharded:
+        # speculative calls: the sector plan of the warm-up steps is reused and checked on the device,
+        # so a step has no host synchronisation and is captured once as a CUDA graph
+        hd = H.device_handle(local)
+        _lib.check(_lib.lib().qvmc_cuda_set_speculative(hd, 1))
+        gs = torch.cuda.Stream(dev)
+        inner = step
+        with torch.cuda.stream(gs):
+            for _ in range(max(args.warmup, 2)):
+                inner()
+                _lib.check(_lib.lib().qvmc_cuda_synchronize(hd))
+            torch.cuda.synchronize()
+            graph_stats = q.last_stats(H, local)  # stage events recorded inside a graph are not readable
+            graph = torch.cuda.CUDAGraph()
+            l0 = q.launch_count()
+            with torch.cuda.graph(graph, stream=gs):
+                inner()
+            graph_launches = q.launch_count() - l0  # kernels in one replay
+        torch.cuda.synchronize()
+        _lib.check(_lib.lib().qvmc_cuda_synchronize(hd))
+
+        def step():
+            graph.replay()
+            return mom_d
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -410,7 +437,7 @@ def main():
             e1.record(stream)
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
-            st = q.last_stats(H, local)
+            st = graph_stats if graph is not None else q.last_stats(H, local)
             rows_ms.append(st["rows_ms"])
             table_ms.append(st["table_ms"])
             mom_ms.append(st["moments_ms"])
@@ -420,8 +447,10 @@ def main():
         if world > 1:
             dist.barrier()
     launches = q.launch_count() - launches0
+    if graph is not None:  # replays launch the captured kernels without host launch calls
+        launches = graph_launches * args.steps
     _lib.check(_lib.lib().qvmc_cuda_synchronize(H.device_handle(local)))
-    stats = q.last_stats(H, local)
+    stats = graph_stats if graph is not None else q.last_stats(H, local)
     mean_ms = statistics.mean(step_ms)
     if world > 1:
         t = torch.tensor([mean_ms], dtype=torch.float64, device=dev)

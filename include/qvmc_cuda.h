@@ -134,6 +134,17 @@ int qvmc_cuda_ham_destroy(qvmc_ham_t h);
 int qvmc_cuda_set_stream(qvmc_ham_t h, void* stream);
 /* Wait for the handle's stream and report deferred device-side errors. */
 int qvmc_cuda_synchronize(qvmc_ham_t h);
+/* Opt in (on = 1) to speculative device-memory calls of qvmc_cuda_eloc_fused:
+ * once a call has planned the sample set (particle sector and minority size,
+ * one host read), later QVMC_MEM_DEVICE calls with the same n_unq reuse that
+ * plan and check it on the device, and the split evaluation checks its hit
+ * buffers on the device too: such a call performs no host synchronisation
+ * at all (it can be captured in a CUDA graph once its buffers are sized).
+ * The next qvmc_cuda_synchronize (or any synchronising call on the handle)
+ * verifies it and, if the plan did not hold or a buffer overflowed, reruns
+ * it synchronously from the same arguments, so the caller must keep the
+ * arguments valid until then. Off by default. */
+int qvmc_cuda_set_speculative(qvmc_ham_t h, int on);
 int qvmc_cuda_last_stats(qvmc_ham_t h, qvmc_stats* out); /* synchronises */
 
 /* ------------------------------------------------------------ coupled pairs */

@@ -69,6 +69,7 @@ SIGNATURES = [
     ("qvmc_cuda_ham_destroy", _INT, [_P]),
     ("qvmc_cuda_set_stream", _INT, [_P, _P]),
     ("qvmc_cuda_synchronize", _INT, [_P]),
+    ("qvmc_cuda_set_speculative", _INT, [_P, _INT]),
     ("qvmc_cuda_last_stats", _INT, [_P, C.POINTER(QvmcStats)]),
     ("qvmc_cuda_pairs", _INT, [_P, _I64, _P, _INT, _INT, _INT, C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_INT)]),
     ("qvmc_cuda_pairs_fetch", _INT, [_P, _P, _INT]),

@@ -197,6 +197,25 @@ struct qvmc_ham_s {
   // split-evaluation workspace
   DBuf s_row_last, s_base, s_rowpos;
   uint64_t hits_per_row = 320;  // split evaluation: running estimate that sizes the row batches
+  // speculative device-memory calls (no host synchronisation): the last call's sector plan,
+  // checked on the device; a call that needs a re-plan or larger hit buffers is rerun by the
+  // next qvmc_cuda_synchronize with the arguments kept here
+  bool plan_ok = false;
+  int plan_mm[2] = {0, 0};
+  int64_t plan_n = -1;
+  bool plan_sector = false, plan_join = false;
+  int plan_side = 0, plan_s = 0, plan_key_bits = 0;
+  bool no_spec = true;  // speculation is opt-in: qvmc_cuda_set_speculative / QVMC_SPECULATE=1
+  bool pending = false;
+  struct {
+    int64_t n_unq, r0, r1;
+    const uint64_t* keys;
+    const double *la, *ph, *lp;
+    double log_norm;
+    double *eloc, *moments;
+  } pend{};
+  int64_t pend_nb = 0;
+  cudaStream_t pend_stream = nullptr;  // the stream the speculative call ran on
   DBuf gkey, p_rlo, p_rhi;      // per-group position key (pairs-based local_energies), row ranges
   // pipelined split evaluation (run_join_pipelined)
   DBuf p_hy[2], p_hg[2], p_hk[2], p_chunk[2], p_part[2];
@@ -222,6 +241,10 @@ struct qvmc_ham_s {
   bool fused = false;  // QVMC_FUSED=1: one warp-specialised search + evaluation kernel (measured slower, r2a)
   int64_t timed_b = 0;            // batches timed by ev_b in the last call
 };
+
+// the speculative-call rerun (resolve_pending) calls the C entry point
+extern "C" int qvmc_cuda_eloc_fused(qvmc_ham_t, int64_t, const uint64_t*, const double*, const double*,
+                                    const double*, double, int64_t, int64_t, double*, double*, int);
 
 namespace {
 
@@ -652,10 +675,41 @@ struct RowPlan {
   int key_bits = 0;  // join: bits of the exact bucket rank, ceil(log2 C(n, s - 2))
 };
 
+RowPlan plan_from_mm(qvmc_ham_s* h, int64_t n, const int* mm);
+
 RowPlan plan_rows(qvmc_ham_s* h, int64_t n) {
   int mm[2] = {0, 0};
   ck(cudaMemcpyAsync(mm, static_cast<int*>(h->ctl.p) + 2, sizeof(mm), cudaMemcpyDeviceToHost, h->stream), "mm");
   ck(cudaStreamSynchronize(h->stream), "sync");
+  const RowPlan P = plan_from_mm(h, n, mm);
+  h->plan_ok = true;  // cached for speculative device-memory calls
+  h->plan_mm[0] = mm[0];
+  h->plan_mm[1] = mm[1];
+  h->plan_n = n;
+  h->plan_sector = P.sector;
+  h->plan_join = P.join;
+  h->plan_side = P.side;
+  h->plan_s = P.s;
+  h->plan_key_bits = P.key_bits;
+  return P;
+}
+
+RowPlan cached_plan(const qvmc_ham_s* h) {
+  RowPlan P;
+  P.sector = h->plan_sector;
+  P.join = h->plan_join;
+  P.side = h->plan_side;
+  P.s = h->plan_s;
+  P.key_bits = h->plan_key_bits;
+  return P;
+}
+
+// the speculative plan holds iff the popcount range equals the cached one
+__global__ void k_plan_check(const int* __restrict__ mm, int m0, int m1, int* __restrict__ err) {
+  if (mm[0] != m0 || mm[1] != m1) atomicOr(err, kErrReplan);
+}
+
+RowPlan plan_from_mm(qvmc_ham_s* h, int64_t n, const int* mm) {
   RowPlan P;
   const int pmax = mm[0], pmin = 1024 - mm[1];
   P.side = (pmin <= h->n - pmin) ? 1 : 0;
@@ -795,7 +849,7 @@ void run_join_fused(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const 
 // whole pipeline then reruns with larger buffers.
 template <int W>
 void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, const RowSet& R, const RowPlan& P,
-                        double2* eloc) {
+                        double2* eloc, bool spec = false) {
   const int64_t rows = R.n_rows;
   if (rows <= 0) return;
   constexpr uint64_t kBatchHits = 1ull << 31;
@@ -899,6 +953,11 @@ void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
     }
     ck(cudaEventRecord(ev_join, B), "event");
     ck(cudaStreamWaitEvent(A, ev_join, 0), "wait");
+    if (spec) {  // no host round trip: an overflow (kErrHitOverflow) is handled by qvmc_cuda_synchronize
+      h->timed_b = (rows + batch - 1) / batch;
+      h->pend_nb = NB;
+      return;
+    }
     ck(cudaStreamSynchronize(A), "sync");
     uint64_t need_h = 0, need_c = 0, hits = 0;
     for (int64_t b = 0; b < NB; ++b) {
@@ -1007,7 +1066,10 @@ void raise_device_err(int err) {
   if (err & kErrZeroAmp) fail(QVMC_ERR_LOGIC, "local_energies: sampled state has zero amplitude");
 }
 
+void resolve_pending(qvmc_ham_s* h);
+
 void finish(qvmc_ham_s* h) {
+  if (h->pending) resolve_pending(h);
   const int err = read_err_and_reset(h);
   if (err) raise_device_err(err);
 }
@@ -1042,6 +1104,43 @@ void compute_moments(qvmc_ham_s* h, const double* lp, double log_norm, const dou
   ck_launch("moments partial");
   k_moments_final<<<1, 32, 0, h->stream>>>(h->partials.as<double>(), kMomentBlocks, out_dev);
   ck_launch("moments final");
+}
+
+// Check a speculative call (synchronises): if its cached plan did not hold or a hit
+// buffer overflowed, grow the buffers / drop the plan and rerun it synchronously from
+// the kept arguments (the caller keeps them valid until qvmc_cuda_synchronize).
+void resolve_pending(qvmc_ham_s* h) {
+  h->pending = false;
+  ck(cudaStreamSynchronize(h->pend_stream), "sync");  // the stream may have been switched since the call
+  cudaStream_t cur = h->stream;
+  h->stream = h->pend_stream;  // a rerun goes to the same stream
+  int err = 0;
+  ck(cudaMemcpy(&err, h->ctl.p, sizeof(int), cudaMemcpyDeviceToHost), "read err");
+  uint64_t need_h = 0, need_c = 0, hits = 0;
+  for (int64_t b = 0; b < h->pend_nb && h->log_host; ++b) {
+    need_h = std::max<uint64_t>(need_h, h->log_host[2 * b]);
+    need_c = std::max<uint64_t>(need_c, h->log_host[2 * b + 1]);
+    hits += h->log_host[2 * b];
+  }
+  h->pend_nb = 0;
+  if (!(err & (kErrReplan | kErrHitOverflow))) {
+    h->stream = cur;
+    const int64_t rows = h->pend.r1 - h->pend.r0;
+    if (rows > 0 && hits) h->hits_per_row = std::max<uint64_t>(h->hits_per_row, hits / static_cast<uint64_t>(rows) + 1);
+    return;  // other device errors are reported by finish()
+  }
+  if (err & kErrHitOverflow) {
+    h->p_hit_cap = std::min<uint64_t>(std::max<uint64_t>(h->p_hit_cap, need_h + need_h / 4 + 1024), 0xFFFFFFFFull);
+    h->p_chunk_cap = std::max<uint64_t>(h->p_chunk_cap, need_c + need_c / 4 + 1024);
+  }
+  h->plan_ok = false;  // the rerun plans synchronously (and re-caches the plan)
+  ck(cudaMemset(h->ctl.p, 0, sizeof(int)), "reset err");
+  const auto a = h->pend;
+  const int st = qvmc_cuda_eloc_fused(h, a.n_unq, a.keys, a.la, a.ph, a.lp, a.log_norm, a.r0, a.r1, a.eloc,
+                                      a.moments, QVMC_MEM_DEVICE);
+  ck(cudaStreamSynchronize(h->stream), "sync");
+  h->stream = cur;
+  if (st != QVMC_OK) fail(st, g_error);
 }
 
 void record_stats(qvmc_ham_s* h, int64_t rows) {
@@ -1237,6 +1336,7 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     }
     if (const char* e = std::getenv("QVMC_JOIN")) h->use_join = std::atoi(e) != 0;
     if (const char* e = std::getenv("QVMC_FUSED")) h->fused = std::atoi(e) != 0;
+    if (const char* e = std::getenv("QVMC_SPECULATE")) h->no_spec = std::atoi(e) == 0;  // opt-in
     if (const char* e = std::getenv("QVMC_PIPE_BATCHES")) h->pipe_batches = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("QVMC_PIPE_SEARCH_BLOCKS")) h->pipe_search_blocks = std::atoi(e);
     if (const char* e = std::getenv("QVMC_PIPE_EVAL_BLOCKS")) h->pipe_eval_blocks = std::atoi(e);
@@ -1330,10 +1430,20 @@ int qvmc_cuda_set_stream(qvmc_ham_t h, void* stream) {
   });
 }
 
+int qvmc_cuda_set_speculative(qvmc_ham_t h, int on) {
+  return guarded([&] {
+    check_handle(h);
+    DeviceGuard dg(h->device);
+    if (!on && h->pending) resolve_pending(h);
+    h->no_spec = on == 0;
+  });
+}
+
 int qvmc_cuda_synchronize(qvmc_ham_t h) {
   return guarded([&] {
     check_handle(h);
     DeviceGuard dg(h->device);
+    if (h->pending) resolve_pending(h);
     finish(h);
   });
 }
@@ -1666,6 +1776,10 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
     if (n_unq > 0 && (!keys || !log_amp || !phase)) fail(QVMC_ERR_INVALID_ARGUMENT, "null sample arrays");
     if (out_moments && row_end > row_begin && !log_prob) fail(QVMC_ERR_INVALID_ARGUMENT, "moments need log_prob");
     DeviceGuard dg(h->device);
+    if (h->pending) resolve_pending(h);  // an earlier speculative call is checked first
+    // speculative: device memory and a cached sector plan for this sample-set size -> no host
+    // synchronisation anywhere in the call (CUDA-graph capturable once the buffers are sized)
+    const bool spec = mem == QVMC_MEM_DEVICE && !h->no_spec && h->plan_ok && h->plan_n == n_unq && n_unq > 0;
     const int W = h->W;
     const int64_t rows = row_end - row_begin;
     const uint64_t* dkeys = stage(h, h->keys, keys, static_cast<size_t>(n_unq) * W, mem);
@@ -1711,7 +1825,14 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       DISPATCH_W(W, (k_popc_range<WW><<<std::max(pgrid, 1), kThreads, 0, h->stream>>>(dkeys, n_unq,
                                                                                       static_cast<int*>(h->ctl.p) + 2)));
       ck_launch("popcount range");
-      P = plan_rows(h, n_unq);
+      if (spec) {
+        P = cached_plan(h);
+        k_plan_check<<<1, 1, 0, h->stream>>>(static_cast<int*>(h->ctl.p) + 2, h->plan_mm[0], h->plan_mm[1],
+                                             static_cast<int*>(h->ctl.p));
+        ck_launch("plan check");
+      } else {
+        P = plan_rows(h, n_unq);
+      }
       note_plan(h, P);
       if (!P.join) DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
       wait_amplitudes();
@@ -1737,7 +1858,7 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       if (P.join && h->fused) {
         DISPATCH_W(W, (run_join_fused<WW>(h, rkeys, R, P, deloc)));
       } else if (P.join) {
-        DISPATCH_W(W, (run_join_pipelined<WW>(h, rkeys, n_unq, R, P, deloc)));
+        DISPATCH_W(W, (run_join_pipelined<WW>(h, rkeys, n_unq, R, P, deloc, spec)));
       } else {
         DISPATCH_W(W, (launch_rows<WW, kModeEloc>(h, dkeys, row_begin, row_end, O)));
       }
@@ -1753,6 +1874,11 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
     }
     ck(cudaEventRecord(h->ev[3], h->stream), "event");
     h->timed = true;
+    if (spec) {
+      h->pending = true;
+      h->pend = {n_unq, row_begin, row_end, keys, log_amp, phase, log_prob, log_norm, out_eloc, out_moments};
+      h->pend_stream = h->stream;
+    }
     if (mem == QVMC_MEM_HOST) {
       if (out_eloc && rows)
         ck(cudaMemcpyAsync(out_eloc, deloc, rows * 16, cudaMemcpyDeviceToHost, h->stream), "D2H eloc");

@@ -21,7 +21,8 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kUnroll = 4;  // independent probes in flight per lane
 
-enum : int { kErrDuplicate = 1, kErrZeroAmp = 2, kErrBadPair = 4, kErrHitOverflow = 8 };
+enum : int { kErrDuplicate = 1, kErrZeroAmp = 2, kErrBadPair = 4, kErrHitOverflow = 8,
+             kErrReplan = 16 };  // a speculative call's cached sector plan did not hold
 enum : int { kModeEloc = 0, kModeCount = 1, kModeEmit = 2, kModeHits = 3, kModeFused = 4 };
 
 struct HamView {
