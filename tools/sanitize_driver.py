@@ -69,6 +69,31 @@ def main():
     M.set_params(np.random.default_rng(0).uniform(-0.1, 0.1, M.n_params()))
     keys = synthetic.near_hf_keys(56, 14, 2000, seed=2)
     M.log_psi(keys)
+    # sampler, energy gradient, SR, Adam (round 2)
+    b = q.sample_without_replacement(M, 3000, q.CounterRng(5), 1)
+    q.fill_amplitudes(b, M)
+    w = np.exp(b.log_probs - b.log_norm)
+    loc = np.random.default_rng(1).normal(size=b.size()) + 0j
+    grad = M.energy_gradient(b.vectors, w, loc)
+    d, _ = M.sr_direction(b.vectors, b.log_probs, loc, 64, grad)
+    M.adam_step(d)
+    print(f"model paths: sampled {b.size()}, |grad| {np.linalg.norm(grad):.4f}", flush=True)
+    # sharded path through the C ABI, world 1 over NCCL
+    import ctypes as C
+    H = synthetic.jw_hamiltonian(56, 100_000, seed=1)
+    keys = synthetic.near_hf_keys(56, 14, 3000, seed=2)
+    bb = synthetic.sample_batch(keys, seed=3)
+    L = _lib.lib()
+    uid = (C.c_uint8 * 128)()
+    _lib.check(L.qvmc_cuda_comm_unique_id(uid, 128))
+    comm = C.c_void_p()
+    _lib.check(L.qvmc_cuda_comm_init_nccl(0, 1, 0, uid, C.byref(comm)))
+    out = np.zeros(len(keys), dtype=np.complex128)
+    mom = np.zeros(5)
+    _lib.check(L.qvmc_cuda_eloc_sharded(H.device_handle(0), comm, len(keys), _ptr(bb.vectors), _ptr(bb.log_amps),
+                                        _ptr(bb.phases), _ptr(bb.log_probs), bb.log_norm, _ptr(out), _ptr(mom),
+                                        _lib.MEM_HOST))
+    _lib.check(L.qvmc_cuda_comm_destroy(comm))
     print("sanitize driver done", flush=True)
 
 
