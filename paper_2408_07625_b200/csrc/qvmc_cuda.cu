@@ -238,6 +238,9 @@ struct qvmc_ham_s {
   std::vector<cudaEvent_t> ev_b;  // pipelined split evaluation: per batch search start/end, eval start/end
   cudaEvent_t ev_f[2] = {nullptr, nullptr};  // fused join kernel start/end
   bool timed_f = false;
+  bool sym = true;     // QVMC_SYMMETRIC=0: every row walks all its partners (no exchange symmetry)
+  bool sym_last = false;  // the last index build was symmetric
+  DBuf s_fix;             // symmetric mode: per row 2 x 128-bit fixed-point sums of mirrored contributions
   bool fused = false;  // QVMC_FUSED=1: one warp-specialised search + evaluation kernel (measured slower, r2a)
   int64_t timed_b = 0;            // batches timed by ev_b in the last call
 };
@@ -727,7 +730,7 @@ RowPlan plan_from_mm(qvmc_ham_s* h, int64_t n, const int* mm) {
 
 // deletion index: exact keys -> radix sort -> runs -> member array + per-(sample, pair) bucket ranges
 template <int W, typename K>
-void build_join_index_k(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowPlan& P) {
+void build_join_index_k(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowPlan& P, bool sym) {
   const uint32_t C = static_cast<uint32_t>(P.s * (P.s - 1) / 2);
   const uint64_t E = static_cast<uint64_t>(n) * C;
   h->j_key.ensure(E * sizeof(K) + 16);
@@ -768,16 +771,18 @@ void build_join_index_k(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const Ro
   k_join_fill<W><<<std::max(egrid, 1), kThreads, 0, h->stream>>>(h->j_val2.as<uint32_t>(), h->j_rid.as<uint32_t>(), E,
                                                                C, h->j_lo.as<uint32_t>(), h->j_hi.as<uint32_t>(),
                                                                keys, h->n, P.side,
-                                                               h->j_mem.as<uint64_t>(), h->j_rng.as<uint2>());
+                                                               h->j_mem.as<uint64_t>(), h->j_rng.as<uint2>(),
+                                                               sym ? 1 : 0);
   ck_launch("join fill");
 }
 
 template <int W>
-void build_join_index(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowPlan& P) {
+void build_join_index(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowPlan& P, bool sym = false) {
+  h->sym_last = sym;
   if (P.key_bits <= 32)
-    build_join_index_k<W, uint32_t>(h, keys, n, P);
+    build_join_index_k<W, uint32_t>(h, keys, n, P, sym);
   else
-    build_join_index_k<W, uint64_t>(h, keys, n, P);
+    build_join_index_k<W, uint64_t>(h, keys, n, P, sym);
 }
 
 JoinView join_view(qvmc_ham_s* h, const RowPlan& P) {
@@ -792,6 +797,7 @@ JoinView join_view(qvmc_ham_s* h, const RowPlan& P) {
   J.famvi = h->p_famvi;
   J.pbits = h->pbits_P ? h->p_pbits : nullptr;
   J.P = h->pbits_P;
+  J.sym = h->sym_last ? 1 : 0;
   return J;
 }
 
@@ -850,6 +856,14 @@ void run_join_fused(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const 
 template <int W>
 void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, const RowSet& R, const RowPlan& P,
                         double2* eloc, bool spec = false) {
+  // symmetric index (h->sym_last): mirrored contributions accumulate exactly in s_fix; the row
+  // batches are contiguous sorted positions evaluated in order, so a row's mirrored sums from
+  // rows x < y are complete when its own batch has been evaluated
+  unsigned long long* fix = nullptr;
+  if (h->sym_last) {
+    h->s_fix.ensure(static_cast<size_t>(n_all) * 32 + 16);
+    fix = h->s_fix.as<unsigned long long>();
+  }
   const int64_t rows = R.n_rows;
   if (rows <= 0) return;
   constexpr uint64_t kBatchHits = 1ull << 31;
@@ -885,6 +899,7 @@ void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
   }
   h->timed_b = 0;
   for (int attempt = 0;; ++attempt) {
+    if (fix) ck(cudaMemsetAsync(fix, 0, static_cast<size_t>(n_all) * 32, h->stream), "memset fix");
     for (int k = 0; k < 2; ++k) {
       h->p_hy[k].ensure(h->p_hit_cap * 4 + 16);
       h->p_hg[k].ensure(h->p_hit_cap * 4 + 16);
@@ -941,13 +956,13 @@ void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
       k_eval_chunks<W><<<grid_for(h, per_sm_e), kThreads, 0, B>>>(
           h->view, join_view(h, P), keys, h->p_chunk[k].as<uint4>(), reinterpret_cast<unsigned long long*>(cur + 2),
           h->p_hy[k].as<uint32_t>(), h->p_hg[k].as<uint32_t>(), h->p_hk[k].as<uint32_t>(), P.side, P.s, ctl + 14,
-          h->s_rowpos.as<uint8_t>(), h->p_part[k].as<double2>(), h->p_chunk_cap);
+          h->s_rowpos.as<uint8_t>(), h->p_part[k].as<double2>(), h->p_chunk_cap, fix);
       ck_launch("eval chunks");
       ck(cudaEventRecord(h->ev_b[4 * b + 3], B), "event");
       const int fgrid = static_cast<int>(std::min<int64_t>((Rb.n_rows + kThreads - 1) / kThreads, grid_for(h, 8)));
       k_finalize_rows<<<std::max(fgrid, 1), kThreads, 0, B>>>(h->s_row_last.as<uint32_t>(), h->p_chunk[k].as<uint4>(),
                                                               h->p_part[k].as<double2>(), h->s_base.as<double2>(), Rb,
-                                                              eloc);
+                                                              eloc, fix);
       ck_launch("finalize rows");
       ck(cudaEventRecord(ev_e[k], B), "event");
     }
@@ -1336,6 +1351,7 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     }
     if (const char* e = std::getenv("QVMC_JOIN")) h->use_join = std::atoi(e) != 0;
     if (const char* e = std::getenv("QVMC_FUSED")) h->fused = std::atoi(e) != 0;
+    if (const char* e = std::getenv("QVMC_SYMMETRIC")) h->sym = std::atoi(e) != 0;
     if (const char* e = std::getenv("QVMC_SPECULATE")) h->no_spec = std::atoi(e) == 0;  // opt-in
     if (const char* e = std::getenv("QVMC_PIPE_BATCHES")) h->pipe_batches = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("QVMC_PIPE_SEARCH_BLOCKS")) h->pipe_search_blocks = std::atoi(e);
@@ -1839,7 +1855,8 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       if (P.join) {
         DISPATCH_W(W, R = sort_for_locality<WW>(h, rkeys, dla, dph, n_unq, row_begin, row_end, P));
         if (h->view.n_res) DISPATCH_W(W, launch_table_build<WW>(h, rkeys, n_unq));  // residual probes: sorted ids
-        DISPATCH_W(W, build_join_index<WW>(h, rkeys, n_unq, P));
+        const bool sym = h->sym && !h->fused && R.list == nullptr;  // every row of the set in this call
+        DISPATCH_W(W, build_join_index<WW>(h, rkeys, n_unq, P, sym));
       } else {
         h->cs.ensure(n_unq * 16 + 16);
         const int grid = static_cast<int>(std::min<int64_t>((n_unq + kThreads - 1) / kThreads, grid_for(h, 8)));

@@ -71,6 +71,7 @@ struct JoinView {
   // P + pidx(A) * P + pidx(B) = double A u B (every split into two pairs)
   const uint32_t* pbits;
   uint32_t P;              // n(n-1)/2
+  int sym;                 // symmetric index: each row walks only its partners y > x (hits count twice)
 };
 
 __device__ __forceinline__ uint32_t pidx(int a, int b) {  // a < b
@@ -293,12 +294,14 @@ template <int W>
 __global__ void k_join_fill(const uint32_t* __restrict__ val, const uint32_t* __restrict__ rid, uint64_t E, uint32_t C,
                             const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi,
                             const uint64_t* __restrict__ keys, int n_qubits, int side, uint64_t* __restrict__ mem,
-                            uint2* __restrict__ rng) {
+                            uint2* __restrict__ rng, int sym) {
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < E; p += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t e = val[p];
     const uint32_t r = rid[p] - 1;
     const uint32_t y = e / C, t = e - y * C;
-    rng[e] = make_uint2(lo[r], hi[r]);
+    // symmetric mode: members of an exact bucket are in sample order (stable sort of
+    // entry ids), so the partners y' > y of this entry are the run after its own position
+    rng[e] = make_uint2(sym ? static_cast<uint32_t>(p) + 1u : lo[r], hi[r]);
     uint64_t S[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) {
@@ -514,6 +517,7 @@ __device__ __forceinline__ Key<W> row_key(const JoinSmem* sm) {
 // one queued hit: its sample record and drain record (loaded together)
 struct JoinHit {
   uint32_t key;
+  uint32_t y;  // partner (sorted position)
   bool valid;
   U64x4 sr;  // log psi, cos, sin of the partner
   uint64_t r[kGrecWords];
@@ -1020,7 +1024,7 @@ __global__ void __launch_bounds__(MODE == kModeFused ? kFThreads : kThreads,
             O.g_out[at] = static_cast<uint32_t>(g);
           }
         }
-        hits += hit ? 1u : 0u;
+        hits += hit ? (J.sym ? 2u : 1u) : 0u;
       }
       __syncwarp();
       emit(kJDrainAt);
@@ -1238,6 +1242,37 @@ __global__ void __launch_bounds__(MODE == kModeFused ? kFThreads : kThreads,
   }
 }
 
+// Exact, order-independent accumulation (symmetric mode): a contribution v is
+// rounded once to the 128-bit fixed-point integer round(v * 2^48) and added
+// with two 64-bit atomics (the low word's carry goes into the high word), so
+// the sum is the same whatever order the pairs arrive in.
+__device__ __forceinline__ void fix_add(unsigned long long* a, double v) {
+  if (v == 0.0) return;
+  const double sc = v * 0x1.0p48;
+  unsigned long long lo;
+  long long hi;
+  if (fabs(sc) < 0x1.0p62) {
+    const long long q = __double2ll_rn(sc);
+    lo = static_cast<unsigned long long>(q);
+    hi = q < 0 ? -1 : 0;
+  } else {  // |v| >= 2^14: split exactly at 2^64
+    const double qh = floor(sc * 0x1.0p-64);
+    hi = static_cast<long long>(qh);
+    lo = __double2ull_rn(sc - qh * 0x1.0p64);
+  }
+  const unsigned long long old = atomicAdd(a, lo);
+  if (old + lo < old) ++hi;
+  if (hi) atomicAdd(a + 1, static_cast<unsigned long long>(hi));
+}
+
+__device__ __forceinline__ double fix_value(const unsigned long long* a) {
+  const long long hi = static_cast<long long>(a[1]);
+  const long long lo = static_cast<long long>(a[0]);
+  if ((hi == 0 && lo >= 0) || (hi == -1 && lo < 0))  // fits 64 bits: one rounding
+    return static_cast<double>(lo) * 0x1.0p-48;
+  return static_cast<double>(hi) * 0x1.0p16 + static_cast<double>(a[0]) * 0x1.0p-48;  // |sum| >= 2^15
+}
+
 #ifndef QVMC_EVAL_MINB
 #define QVMC_EVAL_MINB 3  // 80 registers (measured best, r01z)
 #endif
@@ -1255,7 +1290,9 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
                   const unsigned long long* __restrict__ n_chunks, const uint32_t* __restrict__ hy,
                   const uint32_t* __restrict__ hg, const uint32_t* __restrict__ hk, int side, int s,
                   const int* __restrict__ exp_flag, const uint8_t* __restrict__ rowpos, double2* __restrict__ part,
-                  uint64_t chunk_cap) {
+                  uint64_t chunk_cap, unsigned long long* __restrict__ fix) {
+  // fix != null (symmetric mode): the search walked only partners y > x, so every
+  // hit also adds H_yx psi(x)/psi(y) = conj(H_xy) psi(x)/psi(y) to row y, exactly
   constexpr int DH = QVMC_EVAL_HITS;
   __shared__ uint16_t s_pos[kWarps][32];
   const int lane = threadIdx.x & 31;
@@ -1289,6 +1326,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
         JoinHit& q = h[d];
         q.valid = k < n_hits;
         q.key = kNoKey;
+        q.y = 0;
         q.sr = U64x4{0, 0, 0, 0};
 #pragma unroll
         for (int i = 0; i < kGrecWords; ++i) q.r[i] = 0;
@@ -1296,6 +1334,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
           const uint64_t at = static_cast<uint64_t>(ch.y) + k;
           const uint32_t y = __ldcs(hy + at), g = __ldcs(hg + at);  // streaming, see the search's flush
           q.key = __ldcs(hk + at);
+          q.y = y;
           q.sr = ldg256(J.rec + static_cast<int64_t>(y) * 4);
           const U64x4 g0 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords);
           const U64x4 g1 = ldg256(J.grec + static_cast<int64_t>(g) * kGrecWords + 4);
@@ -1304,7 +1343,31 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
         }
       }
 #pragma unroll
-      for (int d = 0; d < DH; ++d) eval_hit<W>(H, J, spos, h[d], xrow, la_i, cs_i, lane, s, side, acc, inv_ai);
+      for (int d = 0; d < DH; ++d) {
+        if (!fix) {
+          eval_hit<W>(H, J, spos, h[d], xrow, la_i, cs_i, lane, s, side, acc, inv_ai);
+          continue;
+        }
+        double hr, hi;
+        hit_element<W>(H, J, spos, h[d], xrow, lane, s, side, hr, hi);
+        if (h[d].valid) {
+          const double la_j = __longlong_as_double(static_cast<long long>(h[d].sr.a));
+          const double2 cs_j = make_double2(__longlong_as_double(static_cast<long long>(h[d].sr.b)),
+                                            __longlong_as_double(static_cast<long long>(h[d].sr.c)));
+          double2 m = make_double2(0.0, 0.0);
+          if (mag) {
+            const double ej = __longlong_as_double(static_cast<long long>(h[d].sr.d));
+            add_ratio_mag(ej * inv_ai, cs_j, cs_i, hr, hi, acc);
+            add_ratio_mag(__longlong_as_double(static_cast<long long>(sr.d)) * (1.0 / ej), cs_i, cs_j, hr, -hi, m);
+          } else {
+            add_ratio(la_j, cs_j, la_i, cs_i, hr, hi, acc);
+            add_ratio(la_i, cs_i, la_j, cs_j, hr, -hi, m);
+          }
+          unsigned long long* fy = fix + 4 * static_cast<uint64_t>(h[d].y);
+          fix_add(fy, m.x);
+          fix_add(fy + 2, m.y);
+        }
+      }
     }
     const double re = warp_sum(acc.x);
     const double im = warp_sum(acc.y);
@@ -1316,7 +1379,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
 // first (a fixed order: deterministic). Rows of one batch (RowSet).
 __global__ void k_finalize_rows(const uint32_t* __restrict__ row_last, const uint4* __restrict__ chunk,
                                 const double2* __restrict__ part, const double2* __restrict__ base, const RowSet R,
-                                double2* __restrict__ eloc) {
+                                double2* __restrict__ eloc, const unsigned long long* __restrict__ fix) {
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < R.n_rows;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t row = R.list ? static_cast<int64_t>(__ldg(R.list + r)) : R.base + r;
@@ -1326,6 +1389,10 @@ __global__ void k_finalize_rows(const uint32_t* __restrict__ row_last, const uin
       const double2 p = part[c];
       e.x += p.x;
       e.y += p.y;
+    }
+    if (fix) {  // symmetric mode: the partners y < x, exactly accumulated
+      e.x += fix_value(fix + 4 * row);
+      e.y += fix_value(fix + 4 * row + 2);
     }
     eloc[i] = e;
   }

@@ -19,6 +19,11 @@ import paper_2408_07625_b200 as q
 from paper_2408_07625_b200 import synthetic
 from helpers import assert_eloc_close, eloc_scale, golden, instances, product_index
 
+
+def scale_rows(H, b, keys):
+    p = q.loop_over_terms(keys, H)
+    return eloc_scale(p.entries, H.group_offsets, H.coeff, b.log_amps, len(keys))
+
 pytestmark = pytest.mark.gpu
 
 FAMILIES = ["coupling", "accept3", "checks"]
@@ -208,10 +213,14 @@ def test_synthetic_configs_match_oracle(cuda_ok, n_qubits, n_e, n_terms, n_unq):
     _synthetic_rows_vs_oracle(n_qubits, n_e, n_terms, n_unq, 96, seed=n_qubits)
 
 
-def test_pairs_symmetric_and_shard_invariant(cuda_ok):
+def test_pairs_symmetric_and_shard_invariant(cuda_ok, monkeypatch):
     """Size-independent properties at a medium synthetic size: the pair set is
     exchange-symmetric, the fused pair count equals the materialised one, and
-    row-sharded fused calls reproduce the unsharded E_loc and moments."""
+    row-sharded fused calls reproduce each other bit for bit whatever the split
+    (every row walks all its partners) and the whole-set call (symmetric mode:
+    each unordered pair once, mirrored contributions summed exactly) to fp64
+    reordering; with QVMC_SYMMETRIC=0 the whole-set call is the shards' own
+    arithmetic, bit for bit."""
     H = synthetic.jw_hamiltonian(56, 300_000, seed=1)
     keys = synthetic.near_hf_keys(56, 14, 50_000, seed=2)
     b = synthetic.sample_batch(keys, seed=3)
@@ -224,11 +233,18 @@ def test_pairs_symmetric_and_shard_invariant(cuda_ok):
     st = q.last_stats(H)
     assert st["pairs"] == len(e)
     parts = [q.surrogate_energy(H, b, r0, r1, check=False) for r0, r1 in ((0, 17_000), (17_000, 33_333), (33_333, 50_000))]
-    assert np.array_equal(np.concatenate([r.locals for r in parts]), full.locals)
+    parts2 = [q.surrogate_energy(H, b, r0, r1, check=False) for r0, r1 in ((0, 5_000), (5_000, 50_000))]
+    cat = np.concatenate([r.locals for r in parts])
+    assert np.array_equal(cat, np.concatenate([r.locals for r in parts2]))
     assert abs(sum(r.e_var for r in parts) - full.e_var) <= 1e-12 * max(1, abs(full.e_var))
     loc = q.local_energies(p, b, H)
     scale = eloc_scale(p.entries, H.group_offsets, H.coeff, b.log_amps, len(keys))
     assert_eloc_close(full.locals, loc, scale)
+    assert_eloc_close(full.locals, cat, scale, rtol=1e-12)
+    assert np.array_equal(q.surrogate_energy(H, b).locals, full.locals)  # deterministic (exact fixed point)
+    monkeypatch.setenv("QVMC_SYMMETRIC", "0")
+    H2 = synthetic.jw_hamiltonian(56, 300_000, seed=1)
+    assert np.array_equal(q.surrogate_energy(H2, b).locals, cat)
 
 
 def test_cpp_dropin_acceptance(cuda_ok):
@@ -286,8 +302,8 @@ def test_join_hit_buffer_regrow(cuda_ok, monkeypatch, hit_cap):
     assert st["join_mode"] == 1 and st["pairs"] == n_pairs
     assert np.array_equal(got.locals, ref.locals)  # deterministic: same chunks, same order
     assert got.e_var == ref.e_var
-    half = q.surrogate_energy(H, b, 5_000, 15_000, check=False)  # a row shard: same rows, same values
-    assert np.array_equal(half.locals, got.locals[5_000:15_000])
+    half = q.surrogate_energy(H, b, 5_000, 15_000, check=False)  # a row shard: same rows, the full walk
+    assert_eloc_close(half.locals, got.locals[5_000:15_000], scale_rows(H, b, keys)[5_000:15_000], rtol=1e-12)
     p = q.loop_over_terms(keys, H)
     loc = q.local_energies(p, b, H)
     scale = eloc_scale(p.entries, H.group_offsets, H.coeff, b.log_amps, n_unq)

@@ -33,7 +33,8 @@ def join_case(n_qubits, n_e, n_terms, n_unq, hit_cap=None):
     b = synthetic.sample_batch(keys, seed=3)
     rep = q.surrogate_energy(H, b)
     half = q.surrogate_energy(H, b, n_unq // 3, n_unq // 2, check=False)
-    assert np.array_equal(half.locals, rep.locals[n_unq // 3: n_unq // 2])
+    assert np.allclose(half.locals, rep.locals[n_unq // 3: n_unq // 2], rtol=0,
+                       atol=1e-10 * max(1.0, np.abs(rep.locals).max()))
     p = q.loop_over_terms(keys, H)
     loc = q.local_energies(p, b, H)
     assert np.allclose(loc, rep.locals, rtol=0, atol=1e-9 * max(1.0, np.abs(loc).max()))
