@@ -1243,34 +1243,36 @@ __global__ void __launch_bounds__(MODE == kModeFused ? kFThreads : kThreads,
 }
 
 // Exact, order-independent accumulation (symmetric mode): a contribution v is
-// rounded once to the 128-bit fixed-point integer round(v * 2^48) and added
-// with two 64-bit atomics (the low word's carry goes into the high word), so
-// the sum is the same whatever order the pairs arrive in.
+// rounded once to the integer q = round(v * 2^48) and added as two 64-bit
+// words, q mod 2^32 (unsigned) to a[0] and floor(q / 2^32) (signed) to a[1],
+// with fire-and-forget atomics (no returned value on the critical path). The
+// low word has 32 bits of headroom, so the exact sum a[1] * 2^32 + a[0] does
+// not depend on the order the pairs arrive in.
 __device__ __forceinline__ void fix_add(unsigned long long* a, double v) {
   if (v == 0.0) return;
   const double sc = v * 0x1.0p48;
-  unsigned long long lo;
   long long hi;
+  unsigned long long lo;
   if (fabs(sc) < 0x1.0p62) {
     const long long q = __double2ll_rn(sc);
-    lo = static_cast<unsigned long long>(q);
-    hi = q < 0 ? -1 : 0;
-  } else {  // |v| >= 2^14: split exactly at 2^64
-    const double qh = floor(sc * 0x1.0p-64);
+    lo = static_cast<unsigned long long>(q) & 0xFFFFFFFFull;
+    hi = q >> 32;  // arithmetic shift: floor
+  } else {  // |v| >= 2^14
+    const double qh = floor(sc * 0x1.0p-32);
     hi = static_cast<long long>(qh);
-    lo = __double2ull_rn(sc - qh * 0x1.0p64);
+    lo = __double2ull_rn(sc - qh * 0x1.0p32);
   }
-  const unsigned long long old = atomicAdd(a, lo);
-  if (old + lo < old) ++hi;
+  if (lo) atomicAdd(a, lo);
   if (hi) atomicAdd(a + 1, static_cast<unsigned long long>(hi));
 }
 
 __device__ __forceinline__ double fix_value(const unsigned long long* a) {
   const long long hi = static_cast<long long>(a[1]);
-  const long long lo = static_cast<long long>(a[0]);
-  if ((hi == 0 && lo >= 0) || (hi == -1 && lo < 0))  // fits 64 bits: one rounding
-    return static_cast<double>(lo) * 0x1.0p-48;
-  return static_cast<double>(hi) * 0x1.0p16 + static_cast<double>(a[0]) * 0x1.0p-48;  // |sum| >= 2^15
+  const unsigned long long lo = a[0];
+  if (hi > -(1ll << 30) && hi < (1ll << 30))  // |sum * 2^48| < 2^62: exact in 64 bits, one rounding
+    return static_cast<double>(static_cast<long long>((static_cast<unsigned long long>(hi) << 32) + lo)) *
+           0x1.0p-48;
+  return static_cast<double>(hi) * 0x1.0p-16 + static_cast<double>(lo) * 0x1.0p-48;
 }
 
 #ifndef QVMC_EVAL_MINB
