@@ -21,6 +21,8 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   const char* error = nullptr;  // why loading failed (null: loaded)
 };
@@ -38,8 +40,9 @@ inline const NcclApi& nccl_api() {
     a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
     a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
     a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
-    if (!a.GetUniqueId || !a.CommInitRank || !a.CommDestroy || !a.AllGather || !a.GetErrorString)
+    if (!a.GetUniqueId || !a.CommInitRank || !a.CommDestroy || !a.AllGather || !a.AllReduce || !a.GetErrorString)
       a.error = "libnccl.so.2 lacks a required symbol";
     return a;
   }();
@@ -90,6 +93,17 @@ __global__ void k_unpack_shards(const uint64_t* __restrict__ in, int world, int6
     la[j] = __longlong_as_double(s[W]);
     ph[j] = __longlong_as_double(s[W + 1]);
     lp[j] = __longlong_as_double(s[W + 2]);
+  }
+}
+
+// [world][n] uint64 -> sum (integer: exact in any order); the host backend's all-reduce
+__global__ void k_sum_ranks_u64(const unsigned long long* __restrict__ in, int world, int64_t n,
+                                unsigned long long* __restrict__ out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    unsigned long long s = 0;
+    for (int r = 0; r < world; ++r) s += in[static_cast<int64_t>(r) * n + i];
+    out[i] = s;
   }
 }
 

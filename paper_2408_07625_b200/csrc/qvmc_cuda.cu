@@ -166,6 +166,20 @@ void comm_all_gather(qvmc_comm_s* c, const void* send, void* recv, size_t bytes,
   if (bytes) ck(cudaMemcpyAsync(recv, c->hrecv, bytes * c->world, cudaMemcpyHostToDevice, stream), "H2D gathered");
 }
 
+// in-place sum over the ranks of a uint64 array (exact: integer); the host backend all-gathers into tmp
+void comm_all_reduce_u64(qvmc_comm_s* c, unsigned long long* buf, size_t count, cudaStream_t stream, DBuf& tmp) {
+  if (c->world == 1 || count == 0) return;
+  if (c->nccl) {
+    nccl_ck(nccl_api().AllReduce(buf, buf, count, ncclUint64, ncclSum, c->nccl, stream), "ncclAllReduce");
+    return;
+  }
+  tmp.ensure(count * 8 * c->world + 16);
+  comm_all_gather(c, buf, tmp.p, count * 8, stream);
+  k_sum_ranks_u64<<<static_cast<int>(std::min<size_t>((count + 255) / 256, 4096)), 256, 0, stream>>>(
+      tmp.as<unsigned long long>(), c->world, static_cast<int64_t>(count), buf);
+  ck_launch("sum ranks");
+}
+
 }  // namespace
 
 struct qvmc_ham_s {
@@ -241,6 +255,10 @@ struct qvmc_ham_s {
   bool sym = true;     // QVMC_SYMMETRIC=0: every row walks all its partners (no exchange symmetry)
   bool sym_last = false;  // the last index build was symmetric
   DBuf s_fix;             // symmetric mode: per row 2 x 128-bit fixed-point sums of mirrored contributions
+  bool shard_sym_active = false;  // the last fused call left its mirrored sums in s_fix
+  bool shard_sym = false;  // set by qvmc_cuda_eloc_sharded: symmetric over a row subset, mirrored sums
+                           // left in s_fix for the cross-rank reduction (not added by finalize)
+  RowSet last_rows{};      // the row set of the last fused call (sorted positions -> caller rows)
   bool fused = false;  // QVMC_FUSED=1: one warp-specialised search + evaluation kernel (measured slower, r2a)
   int64_t timed_b = 0;            // batches timed by ev_b in the last call
 };
@@ -962,7 +980,7 @@ void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
       const int fgrid = static_cast<int>(std::min<int64_t>((Rb.n_rows + kThreads - 1) / kThreads, grid_for(h, 8)));
       k_finalize_rows<<<std::max(fgrid, 1), kThreads, 0, B>>>(h->s_row_last.as<uint32_t>(), h->p_chunk[k].as<uint4>(),
                                                               h->p_part[k].as<double2>(), h->s_base.as<double2>(), Rb,
-                                                              eloc, fix);
+                                                              eloc, h->shard_sym ? nullptr : fix);
       ck_launch("finalize rows");
       ck(cudaEventRecord(ev_e[k], B), "event");
     }
@@ -1855,7 +1873,9 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       if (P.join) {
         DISPATCH_W(W, R = sort_for_locality<WW>(h, rkeys, dla, dph, n_unq, row_begin, row_end, P));
         if (h->view.n_res) DISPATCH_W(W, launch_table_build<WW>(h, rkeys, n_unq));  // residual probes: sorted ids
-        const bool sym = h->sym && !h->fused && R.list == nullptr;  // every row of the set in this call
+        // symmetric when every row of the set is evaluated by this call, or by the ranks of a sharded call
+        const bool sym = h->sym && !h->fused && (R.list == nullptr || h->shard_sym);
+        h->shard_sym_active = sym && h->shard_sym;
         DISPATCH_W(W, build_join_index<WW>(h, rkeys, n_unq, P, sym));
       } else {
         h->cs.ensure(n_unq * 16 + 16);
@@ -1872,6 +1892,7 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       O.la = dla;
       O.ph = dph;
       O.cs = rcs;
+      h->last_rows = R;
       if (P.join && h->fused) {
         DISPATCH_W(W, (run_join_fused<WW>(h, rkeys, R, P, deloc)));
       } else if (P.join) {
@@ -1891,6 +1912,7 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
     }
     ck(cudaEventRecord(h->ev[3], h->stream), "event");
     h->timed = true;
+    if (!P.join) h->shard_sym_active = false;
     if (spec) {
       h->pending = true;
       h->pend = {n_unq, row_begin, row_end, keys, log_amp, phase, log_prob, log_norm, out_eloc, out_moments};
@@ -2023,15 +2045,32 @@ int qvmc_cuda_eloc_sharded(qvmc_ham_t h, qvmc_comm_t comm, int64_t n_total, cons
                         h->g_la.as<double>(), h->g_ph.as<double>(), h->g_lp.as<double>())));
       ck_launch("unpack shards");
     }
-    // E_loc of this rank's rows against the gathered set + its moments
+    // E_loc of this rank's rows against the gathered set + its moments. Symmetric across ranks:
+    // each rank walks its rows' partners after them, the mirrored fixed-point sums of all ranks are
+    // added (exact integer all-reduce), so every row gets exactly the single-GPU symmetric result
     double* deloc = (mem == QVMC_MEM_DEVICE) ? out_eloc : nullptr;
     h->g_mom.ensure(8 * sizeof(double));
     ck(cudaMemsetAsync(h->g_mom.p, 0, 8 * sizeof(double), h->stream), "memset moments");
+    h->shard_sym = world > 1;
     const int st = qvmc_cuda_eloc_fused(h, n_total, h->g_keys.as<uint64_t>(), h->g_la.as<double>(),
                                         h->g_ph.as<double>(), log_prob ? h->g_lp.as<double>() : nullptr, log_norm,
                                         r0, r1, deloc, out_moments ? h->g_mom.as<double>() : nullptr,
                                         QVMC_MEM_DEVICE);
+    h->shard_sym = false;
     if (st != QVMC_OK) fail(st, g_error);
+    if (h->shard_sym_active) {
+      h->shard_sym_active = false;
+      comm_all_reduce_u64(comm, h->s_fix.as<unsigned long long>(), static_cast<size_t>(n_total) * 4, h->stream,
+                          h->g_recv);
+      double2* de = deloc ? reinterpret_cast<double2*>(deloc) : h->eloc.as<double2>();
+      const RowSet R = h->last_rows;
+      const int fg = static_cast<int>(std::min<int64_t>((R.n_rows + kThreads - 1) / kThreads, grid_for(h, 8)));
+      k_add_fix<<<std::max(fg, 1), kThreads, 0, h->stream>>>(R, h->s_fix.as<unsigned long long>(), de);
+      ck_launch("add mirrored sums");
+      if (out_moments)  // the moments of the finished rows (the fused call's were taken before the fix)
+        compute_moments(h, log_prob ? h->g_lp.as<double>() + r0 : nullptr, log_norm, de, rows,
+                        h->g_mom.as<double>(), nullptr);
+    }
     if (out_moments) {  // per-rank moments gathered, summed in rank order
       h->g_moms.ensure(static_cast<size_t>(world) * 8 * sizeof(double) + 16);
       comm_all_gather(comm, h->g_mom.p, h->g_moms.p, 8 * sizeof(double), h->stream);

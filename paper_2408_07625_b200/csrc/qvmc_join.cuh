@@ -1377,6 +1377,20 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
   }
 }
 
+// Sharded symmetric mode: the rank's rows get the mirrored sums of every rank
+// (all-reduced fixed point) after their own evaluation has finished.
+__global__ void k_add_fix(const RowSet R, const unsigned long long* __restrict__ fix, double2* __restrict__ eloc) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < R.n_rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = R.list ? static_cast<int64_t>(__ldg(R.list + r)) : R.base + r;
+    const int64_t i = (R.perm ? static_cast<int64_t>(__ldg(R.perm + row)) : row) - R.out_base;
+    double2 e = eloc[i];
+    e.x += fix_value(fix + 4 * row);
+    e.y += fix_value(fix + 4 * row + 2);
+    eloc[i] = e;
+  }
+}
+
 // Split evaluation, part 3: E_loc = base + the row's chunk sums, newest chunk
 // first (a fixed order: deterministic). Rows of one batch (RowSet).
 __global__ void k_finalize_rows(const uint32_t* __restrict__ row_last, const uint4* __restrict__ chunk,
