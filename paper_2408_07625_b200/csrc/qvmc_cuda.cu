@@ -2341,6 +2341,14 @@ int qvmc_cuda_sample(qvmc_model_t m, int k_samples, uint64_t seed, uint32_t stre
     m->c_lp.ensure(maxc * 8 + 16);
     m->c_pert.ensure(maxc * 8 + 16);
     m->c_count.ensure(16);
+    {  // CUB temporary storage for the largest possible candidate count, once (no growth mid-call)
+      size_t tb_max = 0;
+      ck(cub::DeviceRadixSort::SortPairs(nullptr, tb_max, m->c_key.as<uint64_t>(), m->c_key2.as<uint64_t>(),
+                                         m->c_slot.as<uint32_t>(), m->c_slot2.as<uint32_t>(),
+                                         static_cast<int>(std::min<size_t>(maxc, 0x7FFFFFFF)), 0, 64, m->stream),
+         "sort size");
+      m->c_tmp.ensure(tb_max + 16);
+    }
     // root: the empty prefix, log p = 0, perturbed = 0 (sampler.cpp:45-46)
     ck(cudaMemsetAsync(m->bk[0].p, 0, W * 8, m->stream), "memset");
     ck(cudaMemsetAsync(m->blp[0].p, 0, 8, m->stream), "memset");
