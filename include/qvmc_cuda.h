@@ -79,7 +79,8 @@ typedef struct {
   int32_t sector_mode;      /* 1 = particle-sector candidate lists, 0 = full flip-mask scan */
   int32_t sector_side;      /* 1 = occupied orbitals are the minority set, 0 = holes */
   int32_t minority_count;   /* |minority set| per key in sector mode */
-  int32_t join_mode;        /* 1 = candidates from the per-call deletion index (join path) */
+  int32_t join_mode;        /* 1 = candidates from the per-call deletion index (join path),
+                               2 = that index built across the ranks of a sharded call */
   float table_ms;           /* CUDA-event times of the last fused call's stages on the */
   float rows_ms;            /* handle's stream: sample-set hash build, row kernel,     */
   float moments_ms;         /* moment reduction                                       */

@@ -256,6 +256,10 @@ struct qvmc_ham_s {
   bool sym_last = false;  // the last index build was symmetric
   DBuf s_fix;             // symmetric mode: per row 2 x 128-bit fixed-point sums of mirrored contributions
   bool shard_sym_active = false;  // the last fused call left its mirrored sums in s_fix
+  qvmc_comm_s* dist_comm = nullptr;  // set by qvmc_cuda_eloc_sharded: build the deletion index across ranks
+  bool dist_index = true;            // QVMC_DIST_INDEX=0: every rank builds the whole index
+  bool dist_active = false;          // the last index was built across ranks (members in j_memg)
+  DBuf j_flags, j_count, j_memg, j_rtmp;
   bool shard_sym = false;  // set by qvmc_cuda_eloc_sharded: symmetric over a row subset, mirrored sums
                            // left in s_fix for the cross-rank reduction (not added by finalize)
   RowSet last_rows{};      // the row set of the last fused call (sorted positions -> caller rows)
@@ -748,7 +752,15 @@ RowPlan plan_from_mm(qvmc_ham_s* h, int64_t n, const int* mm) {
 
 // deletion index: exact keys -> radix sort -> runs -> member array + per-(sample, pair) bucket ranges
 template <int W, typename K>
+void build_join_index_dist(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowPlan& P, bool sym);
+
+template <int W, typename K>
 void build_join_index_k(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowPlan& P, bool sym) {
+  h->dist_active = false;
+  if (h->dist_comm && h->dist_comm->world > 1) {
+    build_join_index_dist<W, K>(h, keys, n, P, sym);
+    return;
+  }
   const uint32_t C = static_cast<uint32_t>(P.s * (P.s - 1) / 2);
   const uint64_t E = static_cast<uint64_t>(n) * C;
   h->j_key.ensure(E * sizeof(K) + 16);
@@ -794,10 +806,92 @@ void build_join_index_k(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const Ro
   ck_launch("join fill");
 }
 
+// Deletion index built across the ranks of a sharded call: every rank computes
+// the bucket keys of all entries (cheap), keeps the entries of the buckets it
+// owns (a hash of the key; order-preserving selection, so members stay in entry
+// order), sorts only those, writes their members and, for every entry of its
+// buckets, the bucket range in global positions; one all-gather assembles the
+// member array (rank r's slice at r * cap) and one integer all-reduce the
+// per-(sample, pair) ranges (each entry is written by exactly one rank). The
+// result is the single-GPU index up to where each bucket sits, so the walk, the
+// hits and E_loc are bit-identical to it.
+template <int W, typename K>
+void build_join_index_dist(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowPlan& P, bool sym) {
+  qvmc_comm_s* cm = h->dist_comm;
+  const uint32_t world = static_cast<uint32_t>(cm->world), rank = static_cast<uint32_t>(cm->rank);
+  const uint32_t C = static_cast<uint32_t>(P.s * (P.s - 1) / 2);
+  const uint64_t E = static_cast<uint64_t>(n) * C;
+  const uint64_t cap = std::min<uint64_t>(E, E / world + E / (2 * world) + 4096);  // 1.5x the mean share
+  h->j_key.ensure(E * sizeof(K) + 16);
+  h->j_key2.ensure(E * sizeof(K) + 16);
+  h->j_val.ensure(E * 4 + 16);
+  h->j_val2.ensure(E * 4 + 16);
+  h->j_head.ensure(cap * 4 + 16);
+  h->j_rid.ensure(cap * 4 + 16);
+  h->j_lo.ensure(cap * 4 + 16);
+  h->j_hi.ensure(cap * 4 + 16);
+  h->j_mem.ensure(cap * 8 + 16);
+  h->j_memg.ensure(cap * world * 8 + 16);
+  h->j_rng.ensure(E * 8 + 16);
+  h->j_flags.ensure(E + 16);
+  h->j_count.ensure(16);
+  const int grid = static_cast<int>(std::min<int64_t>((n + kWarps - 1) / kWarps, grid_for(h, 8)));
+  k_join_keys<W, K><<<std::max(grid, 1), kThreads, 0, h->stream>>>(keys, n, h->n, P.side, P.s, h->binom.as<uint64_t>(),
+                                                                   h->j_key.as<K>(), h->j_val.as<uint32_t>());
+  ck_launch("join keys");
+  const int egrid = static_cast<int>(std::min<uint64_t>((E + kThreads - 1) / kThreads, grid_for(h, 16)));
+  k_part_flags<K><<<std::max(egrid, 1), kThreads, 0, h->stream>>>(h->j_key.as<K>(), E, world, rank,
+                                                                   h->j_flags.as<uint8_t>());
+  ck_launch("partition flags");
+  const int ne = static_cast<int>(E), nc = static_cast<int>(cap);
+  const int key_bits = P.key_bits + 1;  // one more bit: the padding key sorts after every real key
+  size_t b0 = 0, b1 = 0, b2 = 0;
+  ck(cub::DeviceSelect::Flagged(nullptr, b0, h->j_key.as<K>(), h->j_flags.as<uint8_t>(), h->j_key2.as<K>(),
+                                h->j_count.as<uint32_t>(), ne, h->stream), "select size");
+  ck(cub::DeviceRadixSort::SortPairs(nullptr, b1, h->j_key2.as<K>(), h->j_key.as<K>(), h->j_val2.as<uint32_t>(),
+                                     h->j_val.as<uint32_t>(), nc, 0, key_bits, h->stream), "sort size");
+  ck(cub::DeviceScan::InclusiveSum(nullptr, b2, h->j_head.as<uint32_t>(), h->j_rid.as<uint32_t>(), nc, h->stream),
+     "scan size");
+  h->j_tmp.ensure(std::max({b0, b1, b2}) + 16);
+  ck(cub::DeviceSelect::Flagged(h->j_tmp.p, b0, h->j_key.as<K>(), h->j_flags.as<uint8_t>(), h->j_key2.as<K>(),
+                                h->j_count.as<uint32_t>(), ne, h->stream), "select keys");
+  ck(cub::DeviceSelect::Flagged(h->j_tmp.p, b0, h->j_val.as<uint32_t>(), h->j_flags.as<uint8_t>(),
+                                h->j_val2.as<uint32_t>(), h->j_count.as<uint32_t>(), ne, h->stream), "select ids");
+  g_launches += 2;
+  const int pgrid = static_cast<int>(std::min<uint64_t>((cap + kThreads - 1) / kThreads, grid_for(h, 16)));
+  k_pad_slice<K><<<std::max(pgrid, 1), kThreads, 0, h->stream>>>(h->j_key2.as<K>(), h->j_val2.as<uint32_t>(),
+                                                                  h->j_count.as<uint32_t>(), cap,
+                                                                  static_cast<K>(K{1} << P.key_bits),
+                                                                  static_cast<int*>(h->ctl.p));
+  ck_launch("pad slice");
+  ck(cub::DeviceRadixSort::SortPairs(h->j_tmp.p, b1, h->j_key2.as<K>(), h->j_key.as<K>(), h->j_val2.as<uint32_t>(),
+                                     h->j_val.as<uint32_t>(), nc, 0, key_bits, h->stream), "sort slice");
+  ++g_launches;
+  k_run_heads<K><<<std::max(pgrid, 1), kThreads, 0, h->stream>>>(h->j_key.as<K>(), cap, h->j_head.as<uint32_t>());
+  ck_launch("run heads");
+  ck(cub::DeviceScan::InclusiveSum(h->j_tmp.p, b2, h->j_head.as<uint32_t>(), h->j_rid.as<uint32_t>(), nc, h->stream),
+     "scan");
+  ++g_launches;
+  k_run_bounds<<<std::max(pgrid, 1), kThreads, 0, h->stream>>>(h->j_rid.as<uint32_t>(), cap, h->j_lo.as<uint32_t>(),
+                                                                h->j_hi.as<uint32_t>());
+  ck_launch("run bounds");
+  ck(cudaMemsetAsync(h->j_rng.p, 0, E * 8, h->stream), "memset ranges");
+  k_join_fill<W><<<std::max(pgrid, 1), kThreads, 0, h->stream>>>(
+      h->j_val.as<uint32_t>(), h->j_rid.as<uint32_t>(), cap, C, h->j_lo.as<uint32_t>(), h->j_hi.as<uint32_t>(), keys,
+      h->n, P.side, h->j_mem.as<uint64_t>(), h->j_rng.as<uint2>(), sym ? 1 : 0, h->j_count.as<uint32_t>(),
+      static_cast<uint32_t>(rank * cap));
+  ck_launch("join fill (slice)");
+  comm_all_gather(cm, h->j_mem.p, h->j_memg.p, cap * 8, h->stream);
+  comm_all_reduce_u64(cm, h->j_rng.as<unsigned long long>(), E, h->stream, h->j_rtmp);
+  h->dist_active = true;
+  h->last.join_mode = 2;
+}
+
 template <int W>
 void build_join_index(qvmc_ham_s* h, const uint64_t* keys, int64_t n, const RowPlan& P, bool sym = false) {
   h->sym_last = sym;
-  if (P.key_bits <= 32)
+  const int extra = (h->dist_comm && h->dist_comm->world > 1) ? 1 : 0;  // the slice's padding key
+  if (P.key_bits + extra <= 32)
     build_join_index_k<W, uint32_t>(h, keys, n, P, sym);
   else
     build_join_index_k<W, uint64_t>(h, keys, n, P, sym);
@@ -807,7 +901,7 @@ JoinView join_view(qvmc_ham_s* h, const RowPlan& P) {
   JoinView J{};
   J.C = static_cast<uint32_t>(P.s * (P.s - 1) / 2);
   J.rng = h->j_rng.as<uint2>();
-  J.mem = h->j_mem.as<uint64_t>();
+  J.mem = h->dist_active ? h->j_memg.as<uint64_t>() : h->j_mem.as<uint64_t>();
   J.xy_tab = h->p_xy_tab;
   J.xy_mask = h->xy_tab_mask;
   J.rec = h->l_rec.as<uint64_t>();
@@ -1094,6 +1188,8 @@ int read_err_and_reset(qvmc_ham_s* h) {
 }
 
 void raise_device_err(int err) {
+  if (err & kErrSliceOverflow)
+    fail(QVMC_ERR_RUNTIME, "distributed deletion index: a rank's share exceeded its capacity (QVMC_DIST_INDEX=0)");
   if (err & kErrDuplicate) fail(QVMC_ERR_INVALID_ARGUMENT, "sample set contains duplicate basis vectors");
   if (err & kErrBadPair) fail(QVMC_ERR_INVALID_ARGUMENT, "pair entry out of range or not in canonical order");
   if (err & kErrZeroAmp) fail(QVMC_ERR_LOGIC, "local_energies: sampled state has zero amplitude");
@@ -1370,6 +1466,7 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     if (const char* e = std::getenv("QVMC_JOIN")) h->use_join = std::atoi(e) != 0;
     if (const char* e = std::getenv("QVMC_FUSED")) h->fused = std::atoi(e) != 0;
     if (const char* e = std::getenv("QVMC_SYMMETRIC")) h->sym = std::atoi(e) != 0;
+    if (const char* e = std::getenv("QVMC_DIST_INDEX")) h->dist_index = std::atoi(e) != 0;
     if (const char* e = std::getenv("QVMC_SPECULATE")) h->no_spec = std::atoi(e) == 0;  // opt-in
     if (const char* e = std::getenv("QVMC_PIPE_BATCHES")) h->pipe_batches = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("QVMC_PIPE_SEARCH_BLOCKS")) h->pipe_search_blocks = std::atoi(e);
@@ -2052,11 +2149,13 @@ int qvmc_cuda_eloc_sharded(qvmc_ham_t h, qvmc_comm_t comm, int64_t n_total, cons
     h->g_mom.ensure(8 * sizeof(double));
     ck(cudaMemsetAsync(h->g_mom.p, 0, 8 * sizeof(double), h->stream), "memset moments");
     h->shard_sym = world > 1;
+    h->dist_comm = (world > 1 && h->dist_index) ? comm : nullptr;
     const int st = qvmc_cuda_eloc_fused(h, n_total, h->g_keys.as<uint64_t>(), h->g_la.as<double>(),
                                         h->g_ph.as<double>(), log_prob ? h->g_lp.as<double>() : nullptr, log_norm,
                                         r0, r1, deloc, out_moments ? h->g_mom.as<double>() : nullptr,
                                         QVMC_MEM_DEVICE);
     h->shard_sym = false;
+    h->dist_comm = nullptr;
     if (st != QVMC_OK) fail(st, g_error);
     if (h->shard_sym_active) {
       h->shard_sym_active = false;

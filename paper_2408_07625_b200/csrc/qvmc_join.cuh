@@ -294,14 +294,18 @@ template <int W>
 __global__ void k_join_fill(const uint32_t* __restrict__ val, const uint32_t* __restrict__ rid, uint64_t E, uint32_t C,
                             const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi,
                             const uint64_t* __restrict__ keys, int n_qubits, int side, uint64_t* __restrict__ mem,
-                            uint2* __restrict__ rng, int sym) {
-  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < E; p += (uint64_t)gridDim.x * blockDim.x) {
+                            uint2* __restrict__ rng, int sym, const uint32_t* __restrict__ count = nullptr,
+                            uint32_t off = 0) {
+  // distributed build (count != null): this rank's slice of the entries, [count, E) is padding;
+  // ranges are global positions (the slice lands at `off` in the all-gathered member array)
+  const uint64_t En = count ? (static_cast<uint64_t>(*count) < E ? static_cast<uint64_t>(*count) : E) : E;
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < En; p += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t e = val[p];
     const uint32_t r = rid[p] - 1;
     const uint32_t y = e / C, t = e - y * C;
     // symmetric mode: members of an exact bucket are in sample order (stable sort of
     // entry ids), so the partners y' > y of this entry are the run after its own position
-    rng[e] = make_uint2(sym ? static_cast<uint32_t>(p) + 1u : lo[r], hi[r]);
+    rng[e] = make_uint2(off + (sym ? static_cast<uint32_t>(p) + 1u : lo[r]), off + hi[r]);
     uint64_t S[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) {
@@ -313,6 +317,30 @@ __global__ void k_join_fill(const uint32_t* __restrict__ val, const uint32_t* __
     const uint32_t pa = static_cast<uint32_t>(select_bit<W>(S, a)), pb = static_cast<uint32_t>(select_bit<W>(S, b));
     mem[p] = static_cast<uint64_t>(y) | static_cast<uint64_t>(pa) << 32 | static_cast<uint64_t>(pb) << 40 |
              static_cast<uint64_t>(pb * (pb - 1) / 2 + pa) << 48;
+  }
+}
+
+// distributed index build: the rank that owns an exact bucket (a hash of its key)
+template <typename K>
+__global__ void k_part_flags(const K* __restrict__ key, uint64_t E, uint32_t world, uint32_t rank,
+                             uint8_t* __restrict__ flags) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < E; p += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t h = static_cast<uint64_t>(key[p]) * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 29;
+    flags[p] = static_cast<uint32_t>((h * 0xBF58476D1CE4E5B9ull) >> 33) % world == rank ? 1 : 0;
+  }
+}
+
+// pad the selected slice [count, cap) with a key above every real key (sorted last), flag overflow
+template <typename K>
+__global__ void k_pad_slice(K* __restrict__ key, uint32_t* __restrict__ val, const uint32_t* __restrict__ count,
+                            uint64_t cap, K pad, int* __restrict__ err) {
+  const uint64_t c = *count;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && c > cap) atomicOr(err, kErrSliceOverflow);
+  for (uint64_t p = c + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < cap;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    key[p] = pad;
+    val[p] = 0;
   }
 }
 

@@ -89,14 +89,18 @@ def _worker(rank, world, port, out_q):
         comm = Communicator.host()
         res = sharded_surrogate_energy_capi(H, comm, 0, b.size(), sh, b.log_norm)
         torch.cuda.synchronize()
-        out_q.put((rank, res.row_begin, res.row_end, res.locals.cpu().numpy(), res.moments.cpu().numpy()))
+        mode = q.last_stats(H)["join_mode"]
+        out_q.put((rank, res.row_begin, res.row_end, res.locals.cpu().numpy(), res.moments.cpu().numpy(), mode))
         comm.close()
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_multi_rank_host_backend_matches_unsharded(cuda_ok, world):
+@pytest.mark.parametrize("world,dist", [(2, "1"), (3, "1"), (2, "0")])
+def test_multi_rank_host_backend_matches_unsharded(cuda_ok, monkeypatch, world, dist):
+    """dist = 1: the deletion index is built across the ranks (each sorts the buckets it owns,
+    all-gather of members, all-reduce of ranges); 0: every rank builds the whole index."""
+    monkeypatch.setenv("QVMC_DIST_INDEX", dist)
     import torch.multiprocessing as mp
     import paper_2408_07625_b200 as q
     n_qubits, masks, b = _problem()
@@ -114,7 +118,8 @@ def test_multi_rank_host_backend_matches_unsharded(cuda_ok, world):
         p.join(timeout=120)
         assert p.exitcode == 0
     covered = 0
-    for rank, r0, r1, loc, mom in outs:
+    for rank, r0, r1, loc, mom, mode in outs:
+        assert mode == (2 if dist == "1" else 1)
         # symmetric across ranks (each unordered pair once, mirrored sums all-reduced exactly):
         # every row is the single-GPU result bit for bit
         assert np.array_equal(loc, ref.locals[r0:r1])
