@@ -260,6 +260,8 @@ struct qvmc_ham_s {
   bool dist_index = true;            // QVMC_DIST_INDEX=0: every rank builds the whole index
   bool dist_active = false;          // the last index was built across ranks (members in j_memg)
   DBuf j_flags, j_count, j_memg, j_rtmp;
+  bool sym_off_once = false;  // the next call evaluates unpaired (a fixed-point range fallback)
+  bool fix_range_flag = false;  // a sharded symmetric call left the fixed-point range
   bool shard_sym = false;  // set by qvmc_cuda_eloc_sharded: symmetric over a row subset, mirrored sums
                            // left in s_fix for the cross-rank reduction (not added by finalize)
   RowSet last_rows{};      // the row set of the last fused call (sorted positions -> caller rows)
@@ -966,7 +968,7 @@ void run_join_fused(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const 
 // batch's buffers is detected after the last batch (no mid-call sync); the
 // whole pipeline then reruns with larger buffers.
 template <int W>
-void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, const RowSet& R, const RowPlan& P,
+bool run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, const RowSet& R, const RowPlan& P,
                         double2* eloc, bool spec = false) {
   // symmetric index (h->sym_last): mirrored contributions accumulate exactly in s_fix; the row
   // batches are contiguous sorted positions evaluated in order, so a row's mirrored sums from
@@ -977,7 +979,7 @@ void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
     fix = h->s_fix.as<unsigned long long>();
   }
   const int64_t rows = R.n_rows;
-  if (rows <= 0) return;
+  if (rows <= 0) return false;
   constexpr uint64_t kBatchHits = 1ull << 31;
   const uint64_t per_row = std::max<uint64_t>(h->hits_per_row, 64);
   const int64_t nb_min = static_cast<int64_t>((static_cast<uint64_t>(rows) * per_row + kBatchHits - 1) / kBatchHits);
@@ -1068,7 +1070,7 @@ void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
       k_eval_chunks<W><<<grid_for(h, per_sm_e), kThreads, 0, B>>>(
           h->view, join_view(h, P), keys, h->p_chunk[k].as<uint4>(), reinterpret_cast<unsigned long long*>(cur + 2),
           h->p_hy[k].as<uint32_t>(), h->p_hg[k].as<uint32_t>(), h->p_hk[k].as<uint32_t>(), P.side, P.s, ctl + 14,
-          h->s_rowpos.as<uint8_t>(), h->p_part[k].as<double2>(), h->p_chunk_cap, fix);
+          h->s_rowpos.as<uint8_t>(), h->p_part[k].as<double2>(), h->p_chunk_cap, fix, ctl);
       ck_launch("eval chunks");
       ck(cudaEventRecord(h->ev_b[4 * b + 3], B), "event");
       const int fgrid = static_cast<int>(std::min<int64_t>((Rb.n_rows + kThreads - 1) / kThreads, grid_for(h, 8)));
@@ -1083,9 +1085,18 @@ void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
     if (spec) {  // no host round trip: an overflow (kErrHitOverflow) is handled by qvmc_cuda_synchronize
       h->timed_b = (rows + batch - 1) / batch;
       h->pend_nb = NB;
-      return;
+      return false;
     }
     ck(cudaStreamSynchronize(A), "sync");
+    if (fix) {  // a mirrored contribution out of the fixed-point range: the caller redoes the call unpaired
+      int err = 0;
+      ck(cudaMemcpy(&err, ctl, sizeof(int), cudaMemcpyDeviceToHost), "read err");
+      if (err & kErrFixRange) {
+        err &= ~kErrFixRange;
+        ck(cudaMemcpy(ctl, &err, sizeof(int), cudaMemcpyHostToDevice), "reset err");
+        return true;
+      }
+    }
     uint64_t need_h = 0, need_c = 0, hits = 0;
     for (int64_t b = 0; b < NB; ++b) {
       need_h = std::max<uint64_t>(need_h, h->log_host[2 * b]);
@@ -1097,6 +1108,7 @@ void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
       h->hits_per_row = std::max<uint64_t>(h->hits_per_row, hits / static_cast<uint64_t>(rows) + 1);
       break;
     }
+    if (fix) ck(cudaMemsetAsync(fix, 0, static_cast<size_t>(n_all) * 32, h->stream), "memset fix");
     if (attempt >= 3 || h->p_hit_cap >= 0xFFFFFFFFull) fail(QVMC_ERR_RUNTIME, "join hit buffers keep overflowing");
     h->p_hit_cap = std::min<uint64_t>(std::max<uint64_t>(h->p_hit_cap, need_h + need_h / 4 + 1024), 0xFFFFFFFFull);
     h->p_chunk_cap = std::max<uint64_t>(h->p_chunk_cap, need_c + need_c / 4 + 1024);
@@ -1106,6 +1118,7 @@ void run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
     ck(cudaMemcpy(ctl, &err, sizeof(int), cudaMemcpyHostToDevice), "reset overflow");
     ck(cudaMemset(ctl + 6, 0, 4 * sizeof(int)), "reset stats");
   }
+  return false;
 }
 
 template <int W, int MODE>
@@ -1252,7 +1265,8 @@ void resolve_pending(qvmc_ham_s* h) {
     hits += h->log_host[2 * b];
   }
   h->pend_nb = 0;
-  if (!(err & (kErrReplan | kErrHitOverflow))) {
+  if (err & kErrFixRange) h->sym_off_once = true;
+  if (!(err & (kErrReplan | kErrHitOverflow | kErrFixRange))) {
     h->stream = cur;
     const int64_t rows = h->pend.r1 - h->pend.r0;
     if (rows > 0 && hits) h->hits_per_row = std::max<uint64_t>(h->hits_per_row, hits / static_cast<uint64_t>(rows) + 1);
@@ -1971,7 +1985,8 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
         DISPATCH_W(W, R = sort_for_locality<WW>(h, rkeys, dla, dph, n_unq, row_begin, row_end, P));
         if (h->view.n_res) DISPATCH_W(W, launch_table_build<WW>(h, rkeys, n_unq));  // residual probes: sorted ids
         // symmetric when every row of the set is evaluated by this call, or by the ranks of a sharded call
-        const bool sym = h->sym && !h->fused && (R.list == nullptr || h->shard_sym);
+        const bool sym = h->sym && !h->sym_off_once && !h->fused && (R.list == nullptr || h->shard_sym);
+        h->sym_off_once = false;
         h->shard_sym_active = sym && h->shard_sym;
         DISPATCH_W(W, build_join_index<WW>(h, rkeys, n_unq, P, sym));
       } else {
@@ -1993,7 +2008,17 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       if (P.join && h->fused) {
         DISPATCH_W(W, (run_join_fused<WW>(h, rkeys, R, P, deloc)));
       } else if (P.join) {
-        DISPATCH_W(W, (run_join_pipelined<WW>(h, rkeys, n_unq, R, P, deloc, spec)));
+        bool redo = false;
+        DISPATCH_W(W, (redo = run_join_pipelined<WW>(h, rkeys, n_unq, R, P, deloc, spec)));
+        if (redo && (h->shard_sym || h->dist_comm)) {  // sharded: every rank must take the same path
+          h->fix_range_flag = true;                   // (reported through the moment exchange)
+          redo = false;
+        }
+        if (redo) {  // exchange symmetry left the fixed-point range: rebuild unpaired and rerun
+          h->shard_sym_active = false;
+          DISPATCH_W(W, build_join_index<WW>(h, rkeys, n_unq, P, false));
+          DISPATCH_W(W, (run_join_pipelined<WW>(h, rkeys, n_unq, R, P, deloc, false)));
+        }
       } else {
         DISPATCH_W(W, (launch_rows<WW, kModeEloc>(h, dkeys, row_begin, row_end, O)));
       }
@@ -2149,6 +2174,7 @@ int qvmc_cuda_eloc_sharded(qvmc_ham_t h, qvmc_comm_t comm, int64_t n_total, cons
     h->g_mom.ensure(8 * sizeof(double));
     ck(cudaMemsetAsync(h->g_mom.p, 0, 8 * sizeof(double), h->stream), "memset moments");
     h->shard_sym = world > 1;
+    h->fix_range_flag = false;
     h->dist_comm = (world > 1 && h->dist_index) ? comm : nullptr;
     const int st = qvmc_cuda_eloc_fused(h, n_total, h->g_keys.as<uint64_t>(), h->g_la.as<double>(),
                                         h->g_ph.as<double>(), log_prob ? h->g_lp.as<double>() : nullptr, log_norm,
@@ -2170,9 +2196,26 @@ int qvmc_cuda_eloc_sharded(qvmc_ham_t h, qvmc_comm_t comm, int64_t n_total, cons
         compute_moments(h, log_prob ? h->g_lp.as<double>() + r0 : nullptr, log_norm, de, rows,
                         h->g_mom.as<double>(), nullptr);
     }
-    if (out_moments) {  // per-rank moments gathered, summed in rank order
+    const bool flagged = world > 1 && h->sym && !h->fused;  // symmetric sharded: exchange the range flag too
+    if (flagged) {
+      const double f = h->fix_range_flag ? 1.0 : 0.0;
+      ck(cudaMemcpyAsync(h->g_mom.as<double>() + 7, &f, sizeof(double), cudaMemcpyHostToDevice, h->stream), "flag");
+    }
+    if (out_moments || flagged) {  // per-rank moments gathered, summed in rank order
       h->g_moms.ensure(static_cast<size_t>(world) * 8 * sizeof(double) + 16);
       comm_all_gather(comm, h->g_mom.p, h->g_moms.p, 8 * sizeof(double), h->stream);
+      if (flagged) {
+        std::vector<double> all(static_cast<size_t>(world) * 8);
+        ck(cudaMemcpyAsync(all.data(), h->g_moms.p, all.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream),
+           "D2H flags");
+        ck(cudaStreamSynchronize(h->stream), "sync");
+        for (int r = 0; r < world; ++r)
+          if (all[static_cast<size_t>(r) * 8 + 7] != 0.0)
+            fail(QVMC_ERR_RUNTIME, "a mirrored local-energy contribution exceeded the exact fixed-point range "
+                                   "(|value| >= 2^46): rerun with QVMC_SYMMETRIC=0");
+      }
+    }
+    if (out_moments) {
       double* dm = out_moments;
       if (mem == QVMC_MEM_HOST) {
         h->moments.ensure(8 * sizeof(double));

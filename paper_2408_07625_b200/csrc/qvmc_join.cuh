@@ -1276,8 +1276,12 @@ __global__ void __launch_bounds__(MODE == kModeFused ? kFThreads : kThreads,
 // with fire-and-forget atomics (no returned value on the critical path). The
 // low word has 32 bits of headroom, so the exact sum a[1] * 2^32 + a[0] does
 // not depend on the order the pairs arrive in.
-__device__ __forceinline__ void fix_add(unsigned long long* a, double v) {
+__device__ __forceinline__ void fix_add(unsigned long long* a, double v, int* err) {
   if (v == 0.0) return;
+  if (!(fabs(v) < 0x1.0p46)) {  // beyond the exact range (or not finite): the call reruns unpaired
+    atomicOr(err, kErrFixRange);
+    return;
+  }
   const double sc = v * 0x1.0p48;
   long long hi;
   unsigned long long lo;
@@ -1320,7 +1324,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
                   const unsigned long long* __restrict__ n_chunks, const uint32_t* __restrict__ hy,
                   const uint32_t* __restrict__ hg, const uint32_t* __restrict__ hk, int side, int s,
                   const int* __restrict__ exp_flag, const uint8_t* __restrict__ rowpos, double2* __restrict__ part,
-                  uint64_t chunk_cap, unsigned long long* __restrict__ fix) {
+                  uint64_t chunk_cap, unsigned long long* __restrict__ fix, int* __restrict__ fix_err) {
   // fix != null (symmetric mode): the search walked only partners y > x, so every
   // hit also adds H_yx psi(x)/psi(y) = conj(H_xy) psi(x)/psi(y) to row y, exactly
   constexpr int DH = QVMC_EVAL_HITS;
@@ -1394,8 +1398,8 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
             add_ratio(la_i, cs_i, la_j, cs_j, hr, -hi, m);
           }
           unsigned long long* fy = fix + 4 * static_cast<uint64_t>(h[d].y);
-          fix_add(fy, m.x);
-          fix_add(fy + 2, m.y);
+          fix_add(fy, m.x, fix_err);
+          fix_add(fy + 2, m.y, fix_err);
         }
       }
     }

@@ -23,7 +23,8 @@ constexpr int kUnroll = 4;  // independent probes in flight per lane
 
 enum : int { kErrDuplicate = 1, kErrZeroAmp = 2, kErrBadPair = 4, kErrHitOverflow = 8,
              kErrReplan = 16,    // a speculative call's cached sector plan did not hold
-             kErrSliceOverflow = 32 };  // a rank's share of a distributed index exceeded its capacity
+             kErrSliceOverflow = 32,  // a rank's share of a distributed index exceeded its capacity
+             kErrFixRange = 64 };     // a mirrored contribution beyond the fixed-point range (|v| >= 2^46)
 enum : int { kModeEloc = 0, kModeCount = 1, kModeEmit = 2, kModeHits = 3, kModeFused = 4 };
 
 struct HamView {

@@ -418,3 +418,19 @@ def test_c20_energy_and_variance_at_1e5(cuda_ok):
     assert_eloc_close(fused.locals, want, scale)
     st, m, _ = oracle.variational_energy(b.log_probs, b.norm, b.log_norm, want)
     assert abs(fused.e_var - m[0]) <= 1e-10 * max(1.0, float(np.sum(np.exp(b.log_probs - b.log_norm) * scale)))
+
+
+def test_symmetric_fixed_point_range_fallback(cuda_ok, monkeypatch):
+    """Log amplitudes spread over 60 nats make some mirrored contributions psi(x)/psi(y) exceed the
+    exact fixed-point range (2^46): the call must notice and redo the evaluation unpaired, giving
+    exactly the QVMC_SYMMETRIC=0 result; a narrow spread stays paired and agrees to fp64 reordering."""
+    H = synthetic.jw_hamiltonian(56, 300_000, seed=1)
+    keys = synthetic.near_hf_keys(56, 14, 20_000, seed=12)
+    b = synthetic.sample_batch(keys, seed=3)
+    b.log_amps = np.random.default_rng(4).uniform(-60.0, 0.0, len(keys))
+    b.log_probs = 2.0 * b.log_amps
+    b.log_norm = float(np.log(np.exp(b.log_probs - b.log_probs.max()).sum()) + b.log_probs.max())
+    wide = q.surrogate_energy(H, b, check=False)
+    monkeypatch.setenv("QVMC_SYMMETRIC", "0")
+    H0 = synthetic.jw_hamiltonian(56, 300_000, seed=1)
+    assert np.array_equal(wide.locals, q.surrogate_energy(H0, b, check=False).locals)
