@@ -2604,6 +2604,27 @@ __global__ void k_sector_flags(const uint64_t* __restrict__ keys, int64_t n, int
   }
 }
 
+// forward (h1, h2, coefficient-scaled g) then backward (gz2, gz1) kernels of the gradient
+// into the chunk buffers (block stride n_blk rows)
+template <int W>
+void launch_grad_parts(qvmc_model_s* m, const qvmc_model::ModelView& V, const uint64_t* keys, int64_t n, int64_t per,
+                       int64_t S, int nb, const double2* coef, int64_t n_blk) {
+  using namespace qvmc_model;
+  const size_t dyn_f = (8448 + kG2Warps * 64 * kWT) * sizeof(double) + kG2Warps * kWT * W * sizeof(uint64_t);
+  const size_t dyn_b = (8192 + kG2Warps * 64 * kWT) * sizeof(double);
+  ck(cudaFuncSetAttribute(k_grad_fwd<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn_f)),
+     "smem attribute");
+  ck(cudaFuncSetAttribute(k_grad_bwd<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn_b)),
+     "smem attribute");
+  k_grad_fwd<W><<<static_cast<unsigned>(S * nb), kG2Threads, dyn_f, m->stream>>>(
+      V, keys, n, per, coef, m->g_h1.as<double>(), m->g_h2.as<double>(), m->g_g.as<double>(), n_blk);
+  ck_launch("grad forward");
+  k_grad_bwd<W><<<static_cast<unsigned>(S * nb), kG2Threads, dyn_b, m->stream>>>(
+      V, n, per, m->g_h1.as<double>(), m->g_h2.as<double>(), m->g_g.as<double>(), m->g_gz2.as<double>(),
+      m->g_gz1.as<double>(), n_blk);
+  ck_launch("grad backward");
+}
+
 // Σ over samples of coefficient-scaled gradient blocks (k_grad_part + strided-batched DGEMMs)
 // into m->g_w1/g_w2/g_w3/g_b; coef [n] device (2 Re c, 2 Im c); keys device
 void grad_accumulate(qvmc_model_s* m, const uint64_t* keys, int64_t n, const double2* coef) {
@@ -2630,7 +2651,6 @@ void grad_accumulate(qvmc_model_s* m, const uint64_t* keys, int64_t n, const dou
   m->g_w1.ensure(static_cast<size_t>(nb) * l1 * 8);
   m->g_w2.ensure(static_cast<size_t>(nb) * l2 * 8);
   m->g_w3.ensure(static_cast<size_t>(nb) * l2 * 8);
-  const size_t dyn = (16640 + kGWarps * 64 * kWT) * sizeof(double) + kGWarps * kWT * W * sizeof(uint64_t);
   const double one = 1.0, zero = 0.0;
   // pointer arrays of the W1 GEMMs (X is shared by the blocks, so its slice depends on the part only)
   std::vector<const double*> pa(static_cast<size_t>(nb) * parts), pb(pa.size());
@@ -2648,16 +2668,10 @@ void grad_accumulate(qvmc_model_s* m, const uint64_t* keys, int64_t n, const dou
       ck(cudaMemsetAsync(m->g_gz1.p, 0, static_cast<size_t>(nb) * Ncur * 64 * 8, m->stream), "memset");
       ck(cudaMemsetAsync(m->g_x.p, 0, static_cast<size_t>(Ncur) * nx * 8, m->stream), "memset");
     }
-    const int64_t per = 512;  // samples per CTA
+    const int64_t per = 1024;  // samples per CTA
     const int64_t S = (nc + per - 1) / per;
     DISPATCH_W(W, {
-      ck(cudaFuncSetAttribute(k_grad_part<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)),
-         "smem attribute");
-      // block stride Ncur rows: the kernel indexes block jh at jh * N * stride with N = Ncur
-      k_grad_part<WW><<<static_cast<unsigned>(S * nb), kGThreads, dyn, m->stream>>>(
-          V, keys + c0 * WW, nc, per, coef + c0, m->g_h1.as<double>(), m->g_h2.as<double>(), m->g_g.as<double>(),
-          m->g_gz2.as<double>(), m->g_gz1.as<double>(), Ncur);
-      ck_launch("grad part");
+      launch_grad_parts<WW>(m, V, keys + c0 * WW, nc, per, S, nb, coef + c0, Ncur);
       const int xg = static_cast<int>(std::min<int64_t>((nc * nx + 255) / 256, 8LL * m->sms));
       k_pm_bits<WW><<<xg, 256, 0, m->stream>>>(keys + c0 * WW, nc, nq, m->g_x.as<double>());
       ck_launch("pm bits");
@@ -2988,15 +3002,9 @@ int qvmc_cuda_sr_direction(qvmc_model_t m, int64_t n, const uint64_t* keys, cons
     const auto boff = block_offsets(m);
     m->s_boff.ensure(boff.size() * 8);
     ck(cudaMemcpyAsync(m->s_boff.p, boff.data(), boff.size() * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
-    const size_t dyn = (16640 + kGWarps * 64 * kWT) * sizeof(double) + kGWarps * kWT * W * sizeof(uint64_t);
     DISPATCH_W(W, {
-      ck(cudaFuncSetAttribute(k_grad_part<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)),
-         "smem attribute");
-      const int64_t per = 512, S = (ns + per - 1) / per;
-      k_grad_part<WW><<<static_cast<unsigned>(S * nb), kGThreads, dyn, m->stream>>>(
-          V, m->s_keys.as<uint64_t>(), ns, per, m->s_coef1.as<double2>(), m->g_h1.as<double>(), m->g_h2.as<double>(),
-          m->g_g.as<double>(), m->g_gz2.as<double>(), m->g_gz1.as<double>(), ns);
-      ck_launch("sr grad part");
+      const int64_t per = 1024, S = (ns + per - 1) / per;
+      launch_grad_parts<WW>(m, V, m->s_keys.as<uint64_t>(), ns, per, S, nb, m->s_coef1.as<double2>(), ns);
       k_pm_bits<WW><<<std::max(1, static_cast<int>(std::min<int64_t>((ns * (nq + 2) + 255) / 256, 4096))), 256, 0,
                       m->stream>>>(m->s_keys.as<uint64_t>(), ns, nq, m->g_x.as<double>());
       ck_launch("sr pm bits");
