@@ -2625,7 +2625,7 @@ void launch_grad_parts(qvmc_model_s* m, const qvmc_model::ModelView& V, const ui
   ck_launch("grad backward");
 }
 
-// Σ over samples of coefficient-scaled gradient blocks (k_grad_part + strided-batched DGEMMs)
+// Σ over samples of coefficient-scaled gradient blocks (k_grad_fwd / k_grad_bwd + strided-batched DGEMMs)
 // into m->g_w1/g_w2/g_w3/g_b; coef [n] device (2 Re c, 2 Im c); keys device
 void grad_accumulate(qvmc_model_s* m, const uint64_t* keys, int64_t n, const double2* coef) {
   using namespace qvmc_model;
@@ -2984,7 +2984,7 @@ int qvmc_cuda_sr_direction(qvmc_model_t m, int64_t n, const uint64_t* keys, cons
                         m->stream>>>(dk, m->s_idx2.as<uint32_t>(), ns, W, m->s_keys.as<uint64_t>());
     ck_launch("gather keys");
     check_in_sector(m, m->s_keys.as<uint64_t>(), ns);
-    // 3. Jacobian rows R [ns][P] (k_grad_part with coefficients (1, 1), then the outer products)
+    // 3. Jacobian rows R [ns][P] (k_grad_fwd / k_grad_bwd with coefficients (1, 1), then the outer products)
     m->s_coef1.ensure(ns * 16 + 16);
     {
       std::vector<double> ones(static_cast<size_t>(2 * ns), 1.0);

@@ -671,17 +671,322 @@ __global__ void __launch_bounds__(kPThreads, 1)
 //   grad = Σ_i 2 Re{c_i O_i},  c_i = w_i (E_i − Ē),  O_i = [d log|ψ| ; −i d φ].
 // The amplitude blocks collect 2 Re c_i · (d log|ψ|), the phase blocks
 // 2 Im c_i · (d φ). Every weight gradient is an outer product summed over
-// samples, so k_grad_fwd / k_grad_bwd write, per (qudit, head) block and
-// sample, the forward activations h1, h2 and the coefficient-scaled backward
-// vectors g (output), gz2, gz1 (64 doubles each) to chunk buffers, and the host
-// sums them with strided-batched DGEMMs (gW1 = Σ gz1 eᵀ, gW2 = Σ gz2 h1ᵀ,
+// samples, so this kernel writes, per (qudit, head) block and sample, the
+// forward activations h1, h2 and the coefficient-scaled backward vectors g
+// (output), gz2, gz1 (64 doubles each) to chunk buffers, and the host sums
+// them with strided-batched DGEMMs (gW1 = Σ gz1 eᵀ, gW2 = Σ gz2 h1ᵀ,
 // gW3 = Σ g h2ᵀ; biases = Σ of the vectors). Same warp tiling as
 // k_log_psi_part (16-sample tiles, lane = 4 samples × 8 features); the
-// backward GEMMs read W3 / W2 in their original (v, h) / (h, k) layouts.
+// backward GEMMs read W3 / W2 in their original (v, h) / (h, k) layouts,
+// staged once per CTA next to the forward transposes.
+constexpr int kGWarps = 8;
+constexpr int kGThreads = kGWarps * 32;
 // row stride of the h1 / h2 chunk buffers: 64 activations, a constant 1 (so the
 // weight-gradient GEMM also yields the next layer's bias gradient as its last
 // row) and a zero pad
 constexpr int kHS = 66;
+
+template <int W>
+__global__ void __launch_bounds__(kGThreads, 1)
+    k_grad_part(const ModelView M, const uint64_t* __restrict__ keys, int64_t N, int64_t chunk,
+                const double2* __restrict__ coef, double* __restrict__ H1, double* __restrict__ H2,
+                double* __restrict__ G, double* __restrict__ GZ2, double* __restrict__ GZ1, int64_t N_blk) {
+  // N: samples of this call; N_blk: rows per block in the buffers (>= N, padded for split-K)
+  extern __shared__ __align__(16) double smem[];
+  double* w2 = smem;            // [64 k][64 h]  (W2 transposed)
+  double* w3 = smem + 4096;     // [64 k][64 v]  (W3 transposed)
+  double* w2o = smem + 8192;    // [64 h][64 k]  (W2)
+  double* w3o = smem + 12288;   // [64 v][64 h]  (W3)
+  double* bias = smem + 16384;  // b1 | csum | b2 | b3
+  double* acts = smem + 16640;  // [warps][64][16]
+  uint64_t* skeys = reinterpret_cast<uint64_t*>(acts + kGWarps * 64 * kWT);
+
+  const int n_jh = 2 * M.n_qudits;
+  const int jh = static_cast<int>(blockIdx.x % n_jh), j = jh >> 1, hd = jh & 1;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x / n_jh) * chunk;
+  const int64_t c1 = min(N, c0 + chunk);
+  const BlockLayout L{M.n};
+  const double* B = M.P + static_cast<int64_t>(jh) * L.size();
+  for (int e = threadIdx.x; e < 4096; e += kGThreads) {
+    const double a = __ldg(B + L.w2t() + e), b = __ldg(B + L.w3t() + e);
+    w2[e] = a;
+    w3[e] = b;
+    const int r = e >> 6, c = e & 63;  // (k, h) -> (h, k)
+    w2o[c * 64 + r] = a;
+    w3o[c * 64 + r] = b;
+  }
+  if (threadIdx.x < 64) {
+    bias[threadIdx.x] = __ldg(B + L.b1() + threadIdx.x);
+    bias[64 + threadIdx.x] = __ldg(B + L.csum() + threadIdx.x);
+    bias[128 + threadIdx.x] = __ldg(B + L.b2() + threadIdx.x);
+    bias[192 + threadIdx.x] = __ldg(B + L.b3() + threadIdx.x);
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sq = lane >> 3, hq = lane & 7;
+  double* act = acts + warp * 64 * kWT;
+  uint64_t* sk = skeys + warp * kWT * W;
+  const int off = j * M.bits;
+  const int k = min(M.bits, M.n - off);
+  const int n_out = 1 << k;
+  const int rem_after = M.n - off - k;
+  int rem_up_after = 0;
+  for (int i = off + k; i < M.n; ++i) rem_up_after += (i % 2 == 0);
+  uint32_t up_value_mask = 0;
+  for (int t = 0; t < k; ++t)
+    if ((off + t) % 2 == 0) up_value_mask |= 1u << (k - 1 - t);
+  const int64_t blk = static_cast<int64_t>(jh) * N_blk * 64, blkh = static_cast<int64_t>(jh) * N_blk * kHS;
+  double *h1o = H1 + blkh, *h2o = H2 + blkh, *go = G + blk, *gz2o = GZ2 + blk, *gz1o = GZ1 + blk;
+  auto feat = [&](int f) { return 16 * (f >> 1) + 2 * hq + (f & 1); };
+
+  for (int64_t t0 = c0 + static_cast<int64_t>(warp) * kWT; t0 < c1; t0 += static_cast<int64_t>(kWT) * kGWarps) {
+    __syncwarp();
+    for (int e = lane; e < kWT * W; e += 32) {
+      const int64_t g = t0 + e / W;
+      sk[e] = g < c1 ? __ldg(keys + g * W + (e % W)) : 0ull;
+    }
+    __syncwarp();
+    int pw[4], pu[4], val[4];
+    double cf[4];
+#pragma unroll
+    for (int si = 0; si < 4; ++si) {
+      const uint64_t* x = sk + (sq * 4 + si) * W;
+      int c = 0, cu = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const int lo = 64 * w;
+        if (off > lo) {
+          const uint64_t msk = (off - lo >= 64) ? ~0ull : ((1ull << (off - lo)) - 1);
+          c += __popcll(x[w] & msk);
+          cu += __popcll(x[w] & msk & 0x5555555555555555ull);
+        }
+      }
+      pw[si] = c;
+      pu[si] = cu;
+      const int wq = off >> 6, bq = off & 63;
+      uint64_t fld = x[wq] >> bq;
+      if (bq + k > 64 && wq + 1 < W) fld |= x[wq + 1] << (64 - bq);
+      val[si] = static_cast<int>(__brev(static_cast<uint32_t>(fld)) >> (32 - k));
+      const int64_t g = t0 + sq * 4 + si;
+      const double2 c2 = g < c1 ? coef[g] : make_double2(0.0, 0.0);
+      cf[si] = hd ? c2.y : c2.x;
+    }
+    auto row = [&](int si) { return t0 + sq * 4 + si; };
+    auto put = [&](double* o, int si, int f, double v0, double v1, int ld = 64) {  // features f, f+1 of sample si
+      if (row(si) < c1) *reinterpret_cast<double2*>(o + row(si) * ld + feat(f)) = make_double2(v0, v1);
+    };
+    if (hq == 0)  // bias columns of this lane's 4 samples
+#pragma unroll
+      for (int si = 0; si < 4; ++si)
+        if (row(si) < c1) {
+          *reinterpret_cast<double2*>(h1o + row(si) * kHS + 64) = make_double2(1.0, 0.0);
+          *reinterpret_cast<double2*>(h2o + row(si) * kHS + 64) = make_double2(1.0, 0.0);
+        }
+
+    // layer 1 -> h1 (model.cpp:171), as in k_log_psi_part
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      double a[2][8];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int si = 2 * p + u;
+        const uint64_t* x = sk + (sq * 4 + si) * W;
+        const bool ones = 2 * pw[si] <= off;
+#pragma unroll
+        for (int f = 0; f < 8; ++f) a[u][f] = 0.0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const int lo = 64 * w;
+          if (off <= lo) break;
+          const uint64_t msk = (off - lo >= 64) ? ~0ull : ((1ull << (off - lo)) - 1);
+          uint64_t xm = (ones ? x[w] : ~x[w]) & msk;
+          while (xm) {
+            const int i = lo + __ffsll(static_cast<long long>(xm)) - 1;
+            xm &= xm - 1;
+            const double* rw = B + L.w1t() + i * kHid + 2 * hq;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              const double2 wv = __ldg(reinterpret_cast<const double2*>(rw + 16 * m));
+              a[u][2 * m] += wv.x;
+              a[u][2 * m + 1] += wv.y;
+            }
+          }
+        }
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+          const double cs = bias[64 + feat(f)];
+          a[u][f] = tanh_fast((ones ? 2.0 * a[u][f] - cs : cs - 2.0 * a[u][f]) + bias[feat(f)]);
+        }
+#pragma unroll
+        for (int f = 0; f < 8; f += 2) put(h1o, si, f, a[u][f], a[u][f + 1], kHS);
+      }
+#pragma unroll
+      for (int f = 0; f < 8; ++f)
+        *reinterpret_cast<double2*>(act + pidx(feat(f), sq * 4 + 2 * p)) = make_double2(a[0][f], a[1][f]);
+    }
+    __syncwarp();
+
+    double acc[4][8];
+    auto gemm = [&](const double* wm) {
+#pragma unroll
+      for (int si = 0; si < 4; ++si)
+#pragma unroll
+        for (int f = 0; f < 8; ++f) acc[si][f] = 0.0;
+#pragma unroll 4
+      for (int kk = 0; kk < kHid; ++kk) {
+        const double2 a01 = *reinterpret_cast<const double2*>(act + pidx(kk, sq * 4));
+        const double2 a23 = *reinterpret_cast<const double2*>(act + pidx(kk, sq * 4 + 2));
+        const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+        double wv[8];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const double2 t = *reinterpret_cast<const double2*>(wm + kk * kHid + 16 * m + 2 * hq);
+          wv[2 * m] = t.x;
+          wv[2 * m + 1] = t.y;
+        }
+#pragma unroll
+        for (int si = 0; si < 4; ++si)
+#pragma unroll
+          for (int f = 0; f < 8; ++f) acc[si][f] = fma(av[si], wv[f], acc[si][f]);
+      }
+    };
+    // acc tile -> act (k-major) for the next GEMM
+    auto to_act = [&](double (*v)[8]) {
+      __syncwarp();
+#pragma unroll
+      for (int f = 0; f < 8; ++f) {
+        *reinterpret_cast<double2*>(act + pidx(feat(f), sq * 4)) = make_double2(v[0][f], v[1][f]);
+        *reinterpret_cast<double2*>(act + pidx(feat(f), sq * 4 + 2)) = make_double2(v[2][f], v[3][f]);
+      }
+      __syncwarp();
+    };
+
+    // layer 2: h2 = tanh(W2 h1 + b2 + h1) (model.cpp:172)
+    gemm(w2);
+    double h2[4][8];
+#pragma unroll
+    for (int f = 0; f < 8; ++f) {
+      const int h = feat(f);
+      const double2 r01 = *reinterpret_cast<const double2*>(act + pidx(h, sq * 4));
+      const double2 r23 = *reinterpret_cast<const double2*>(act + pidx(h, sq * 4 + 2));
+      const double b2 = bias[128 + h];
+      h2[0][f] = tanh_fast(acc[0][f] + b2 + r01.x);
+      h2[1][f] = tanh_fast(acc[1][f] + b2 + r01.y);
+      h2[2][f] = tanh_fast(acc[2][f] + b2 + r23.x);
+      h2[3][f] = tanh_fast(acc[3][f] + b2 + r23.y);
+    }
+#pragma unroll
+    for (int si = 0; si < 4; ++si)
+#pragma unroll
+      for (int f = 0; f < 8; f += 2) put(h2o, si, f, h2[si][f], h2[si][f + 1], kHS);
+
+    // output gradient g (d/d raw output), scaled by the sample's coefficient
+    double g[4][8];
+    if (hd == 0) {
+      // amplitude head: onehot(v) - softmax(2 out) over allowed, minus its mean (model.cpp:288-310)
+      to_act(h2);
+      gemm(w3);
+#pragma unroll
+      for (int si = 0; si < 4; ++si) {
+        double sum = 0.0;
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+          acc[si][f] += bias[192 + feat(f)];
+          sum += acc[si][f];
+        }
+#pragma unroll
+        for (int o = 4; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        const double mean = sum / static_cast<double>(n_out);
+        double mx = -CUDART_INF;
+        uint32_t okm = 0;
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+          const int v = feat(f);
+          acc[si][f] = 2.0 * (acc[si][f] - mean);
+          const int w = pw[si] + __popc(v);
+          bool a = v < n_out && w <= M.n_e && w + rem_after >= M.n_e;
+          if (a && M.spin) {
+            const int wu = pu[si] + __popc(static_cast<uint32_t>(v) & up_value_mask);
+            const int wd = w - wu;
+            const int n_down = M.n_e - M.n_up;
+            const int rem_down = rem_after - rem_up_after;
+            a = wu <= M.n_up && wu + rem_up_after >= M.n_up && wd <= n_down && wd + rem_down >= n_down;
+          }
+          if (a) {
+            okm |= 1u << f;
+            mx = fmax(mx, acc[si][f]);
+          }
+        }
+#pragma unroll
+        for (int o = 4; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        double se = 0.0;
+        double ex[8];
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+          ex[f] = (okm >> f & 1u) ? exp(acc[si][f] - mx) : 0.0;
+          se += ex[f];
+        }
+#pragma unroll
+        for (int o = 4; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+        double gs = 0.0;
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+          const int v = feat(f);
+          g[si][f] = (v == val[si] ? 1.0 : 0.0) - ex[f] / se;
+          gs += g[si][f];  // v >= n_out: 0
+        }
+#pragma unroll
+        for (int o = 4; o; o >>= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
+        const double gm = gs / static_cast<double>(n_out);
+#pragma unroll
+        for (int f = 0; f < 8; ++f) g[si][f] = feat(f) < n_out ? (g[si][f] - gm) * cf[si] : 0.0;
+      }
+    } else {
+      // phase head: d phase / d raw = onehot(v) (model.cpp:316-320)
+#pragma unroll
+      for (int si = 0; si < 4; ++si)
+#pragma unroll
+        for (int f = 0; f < 8; ++f) g[si][f] = feat(f) == val[si] ? cf[si] : 0.0;
+    }
+#pragma unroll
+    for (int si = 0; si < 4; ++si)
+#pragma unroll
+      for (int f = 0; f < 8; f += 2) put(go, si, f, g[si][f], g[si][f + 1]);
+
+    // gz2 = (W3ᵀ g) ⊙ (1 − h2²)
+    to_act(g);
+    gemm(w3o);
+#pragma unroll
+    for (int si = 0; si < 4; ++si)
+#pragma unroll
+      for (int f = 0; f < 8; ++f) acc[si][f] *= 1.0 - h2[si][f] * h2[si][f];
+    double gz2[4][8];
+#pragma unroll
+    for (int si = 0; si < 4; ++si)
+#pragma unroll
+      for (int f = 0; f < 8; ++f) gz2[si][f] = acc[si][f];
+#pragma unroll
+    for (int si = 0; si < 4; ++si)
+#pragma unroll
+      for (int f = 0; f < 8; f += 2) put(gz2o, si, f, gz2[si][f], gz2[si][f + 1]);
+
+    // gz1 = (W2ᵀ gz2 + gz2) ⊙ (1 − h1²), h1 re-read from this lane's own stores
+    to_act(gz2);
+    gemm(w2o);
+#pragma unroll
+    for (int si = 0; si < 4; ++si) {
+      if (row(si) >= c1) continue;
+#pragma unroll
+      for (int f = 0; f < 8; f += 2) {
+        const double2 h = *reinterpret_cast<const double2*>(h1o + row(si) * kHS + feat(f));
+        const double v0 = (acc[si][f] + gz2[si][f]) * (1.0 - h.x * h.x);
+        const double v1 = (acc[si][f + 1] + gz2[si][f + 1]) * (1.0 - h.y * h.y);
+        *reinterpret_cast<double2*>(gz1o + row(si) * 64 + feat(f)) = make_double2(v0, v1);
+      }
+    }
+  }
+}
 
 // ±1 encoding of every qubit of a chunk's keys: X[s][i] (model.cpp:153-158
 // before the prefix cut; gW1 of qudit j keeps only columns i < offset_j)
@@ -789,7 +1094,7 @@ __global__ void k_grad_scatter(const ModelView M, const double* __restrict__ gw1
 }
 
 // Jacobian rows of selected samples (grad_log_psi, model.cpp:273-325) from
-// k_grad_part's buffers run with coefficients (1, 1): R[i][t] = d log|ψ| / dθ_t
+// the gradient kernels' buffers run with coefficients (1, 1): R[i][t] = d log|ψ| / dθ_t
 // for amplitude-block parameters and d φ / dθ_t for phase-block ones (the
 // complex row is R on the amplitude blocks and -i R on the phase blocks).
 // Block jh of the flat layout starts at boff[jh]. One CTA per (row, block).
