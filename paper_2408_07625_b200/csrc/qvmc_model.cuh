@@ -671,35 +671,37 @@ __global__ void __launch_bounds__(kPThreads, 1)
 //   grad = Σ_i 2 Re{c_i O_i},  c_i = w_i (E_i − Ē),  O_i = [d log|ψ| ; −i d φ].
 // The amplitude blocks collect 2 Re c_i · (d log|ψ|), the phase blocks
 // 2 Im c_i · (d φ). Every weight gradient is an outer product summed over
-// samples, so this kernel writes, per (qudit, head) block and sample, the
-// forward activations h1, h2 and the coefficient-scaled backward vectors g
-// (output), gz2, gz1 (64 doubles each) to chunk buffers, and the host sums
-// them with strided-batched DGEMMs (gW1 = Σ gz1 eᵀ, gW2 = Σ gz2 h1ᵀ,
+// samples, so k_grad_fwd / k_grad_bwd write, per (qudit, head) block and
+// sample, the forward activations h1, h2 and the coefficient-scaled backward
+// vectors g (output), gz2, gz1 (64 doubles each) to chunk buffers, and the host
+// sums them with strided-batched DGEMMs (gW1 = Σ gz1 eᵀ, gW2 = Σ gz2 h1ᵀ,
 // gW3 = Σ g h2ᵀ; biases = Σ of the vectors). Same warp tiling as
 // k_log_psi_part (16-sample tiles, lane = 4 samples × 8 features); the
-// backward GEMMs read W3 / W2 in their original (v, h) / (h, k) layouts,
-// staged once per CTA next to the forward transposes.
-constexpr int kGWarps = 8;
-constexpr int kGThreads = kGWarps * 32;
+// backward GEMMs read W3 / W2 in their original (v, h) / (h, k) layouts.
 // row stride of the h1 / h2 chunk buffers: 64 activations, a constant 1 (so the
 // weight-gradient GEMM also yields the next layer's bias gradient as its last
 // row) and a zero pad
 constexpr int kHS = 66;
 
+// the forward / backward split of the gradient kernels: 16 warps per CTA each
+#ifndef QVMC_G2_WARPS
+#define QVMC_G2_WARPS 16
+#endif
+constexpr int kG2Warps = QVMC_G2_WARPS;
+constexpr int kG2Threads = kG2Warps * 32;
+
 template <int W>
-__global__ void __launch_bounds__(kGThreads, 1)
-    k_grad_part(const ModelView M, const uint64_t* __restrict__ keys, int64_t N, int64_t chunk,
+__global__ void __launch_bounds__(kG2Threads, 1)
+    k_grad_fwd(const ModelView M, const uint64_t* __restrict__ keys, int64_t N, int64_t chunk,
                 const double2* __restrict__ coef, double* __restrict__ H1, double* __restrict__ H2,
-                double* __restrict__ G, double* __restrict__ GZ2, double* __restrict__ GZ1, int64_t N_blk) {
+                double* __restrict__ G, int64_t N_blk) {
   // N: samples of this call; N_blk: rows per block in the buffers (>= N, padded for split-K)
   extern __shared__ __align__(16) double smem[];
   double* w2 = smem;            // [64 k][64 h]  (W2 transposed)
   double* w3 = smem + 4096;     // [64 k][64 v]  (W3 transposed)
-  double* w2o = smem + 8192;    // [64 h][64 k]  (W2)
-  double* w3o = smem + 12288;   // [64 v][64 h]  (W3)
-  double* bias = smem + 16384;  // b1 | csum | b2 | b3
-  double* acts = smem + 16640;  // [warps][64][16]
-  uint64_t* skeys = reinterpret_cast<uint64_t*>(acts + kGWarps * 64 * kWT);
+  double* bias = smem + 8192;   // b1 | csum | b2 | b3
+  double* acts = smem + 8448;   // [warps][64][16]
+  uint64_t* skeys = reinterpret_cast<uint64_t*>(acts + kG2Warps * 64 * kWT);
 
   const int n_jh = 2 * M.n_qudits;
   const int jh = static_cast<int>(blockIdx.x % n_jh), j = jh >> 1, hd = jh & 1;
@@ -707,13 +709,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
   const int64_t c1 = min(N, c0 + chunk);
   const BlockLayout L{M.n};
   const double* B = M.P + static_cast<int64_t>(jh) * L.size();
-  for (int e = threadIdx.x; e < 4096; e += kGThreads) {
-    const double a = __ldg(B + L.w2t() + e), b = __ldg(B + L.w3t() + e);
-    w2[e] = a;
-    w3[e] = b;
-    const int r = e >> 6, c = e & 63;  // (k, h) -> (h, k)
-    w2o[c * 64 + r] = a;
-    w3o[c * 64 + r] = b;
+  for (int e = threadIdx.x; e < 4096; e += kG2Threads) {
+    w2[e] = __ldg(B + L.w2t() + e);
+    w3[e] = __ldg(B + L.w3t() + e);
   }
   if (threadIdx.x < 64) {
     bias[threadIdx.x] = __ldg(B + L.b1() + threadIdx.x);
@@ -737,10 +735,10 @@ __global__ void __launch_bounds__(kGThreads, 1)
   for (int t = 0; t < k; ++t)
     if ((off + t) % 2 == 0) up_value_mask |= 1u << (k - 1 - t);
   const int64_t blk = static_cast<int64_t>(jh) * N_blk * 64, blkh = static_cast<int64_t>(jh) * N_blk * kHS;
-  double *h1o = H1 + blkh, *h2o = H2 + blkh, *go = G + blk, *gz2o = GZ2 + blk, *gz1o = GZ1 + blk;
+  double *h1o = H1 + blkh, *h2o = H2 + blkh, *go = G + blk;
   auto feat = [&](int f) { return 16 * (f >> 1) + 2 * hq + (f & 1); };
 
-  for (int64_t t0 = c0 + static_cast<int64_t>(warp) * kWT; t0 < c1; t0 += static_cast<int64_t>(kWT) * kGWarps) {
+  for (int64_t t0 = c0 + static_cast<int64_t>(warp) * kWT; t0 < c1; t0 += static_cast<int64_t>(kWT) * kG2Warps) {
     __syncwarp();
     for (int e = lane; e < kWT * W; e += 32) {
       const int64_t g = t0 + e / W;
@@ -954,37 +952,115 @@ __global__ void __launch_bounds__(kGThreads, 1)
 #pragma unroll
       for (int f = 0; f < 8; f += 2) put(go, si, f, g[si][f], g[si][f + 1]);
 
-    // gz2 = (W3ᵀ g) ⊙ (1 − h2²)
-    to_act(g);
-    gemm(w3o);
-#pragma unroll
-    for (int si = 0; si < 4; ++si)
-#pragma unroll
-      for (int f = 0; f < 8; ++f) acc[si][f] *= 1.0 - h2[si][f] * h2[si][f];
-    double gz2[4][8];
-#pragma unroll
-    for (int si = 0; si < 4; ++si)
-#pragma unroll
-      for (int f = 0; f < 8; ++f) gz2[si][f] = acc[si][f];
-#pragma unroll
-    for (int si = 0; si < 4; ++si)
-#pragma unroll
-      for (int f = 0; f < 8; f += 2) put(gz2o, si, f, gz2[si][f], gz2[si][f + 1]);
+  }
+}
 
-    // gz1 = (W2ᵀ gz2 + gz2) ⊙ (1 − h1²), h1 re-read from this lane's own stores
-    to_act(gz2);
-    gemm(w2o);
+// Backward half (mlp_backward, model.cpp:177-201) of the gradient vectors:
+// gz2 = (W3ᵀ g) ⊙ (1 − h2²), gz1 = (W2ᵀ gz2 + gz2) ⊙ (1 − h1²) from the g,
+// h1, h2 rows k_grad_fwd wrote; W3 and W2 staged in their original (v, h) /
+// (h, k) orientation, the same warp tiling and GEMM as the forward kernels.
+template <int W>
+__global__ void __launch_bounds__(kG2Threads, 1)
+    k_grad_bwd(const ModelView M, int64_t N, int64_t chunk, const double* __restrict__ H1,
+               const double* __restrict__ H2, const double* __restrict__ G, double* __restrict__ GZ2,
+               double* __restrict__ GZ1, int64_t N_blk) {
+  extern __shared__ __align__(16) double smem[];
+  double* w2o = smem;           // [64 h][64 k]  (W2)
+  double* w3o = smem + 4096;    // [64 v][64 h]  (W3)
+  double* acts = smem + 8192;   // [warps][64][16]
+  const int n_jh = 2 * M.n_qudits;
+  const int jh = static_cast<int>(blockIdx.x % n_jh);
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x / n_jh) * chunk;
+  const int64_t c1 = min(N, c0 + chunk);
+  const BlockLayout L{M.n};
+  const double* B = M.P + static_cast<int64_t>(jh) * L.size();
+  for (int e = threadIdx.x; e < 4096; e += kG2Threads) {
+    const int r = e >> 6, c = e & 63;  // (k, h) -> (h, k)
+    w2o[c * 64 + r] = __ldg(B + L.w2t() + e);
+    w3o[c * 64 + r] = __ldg(B + L.w3t() + e);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sq = lane >> 3, hq = lane & 7;
+  double* act = acts + warp * 64 * kWT;
+  const int64_t blk = static_cast<int64_t>(jh) * N_blk * 64, blkh = static_cast<int64_t>(jh) * N_blk * kHS;
+  const double *h1i = H1 + blkh, *h2i = H2 + blkh, *gi = G + blk;
+  double *gz2o = GZ2 + blk, *gz1o = GZ1 + blk;
+  auto feat = [&](int f) { return 16 * (f >> 1) + 2 * hq + (f & 1); };
+  for (int64_t t0 = c0 + static_cast<int64_t>(warp) * kWT; t0 < c1; t0 += static_cast<int64_t>(kWT) * kG2Warps) {
+    auto row = [&](int si) { return t0 + sq * 4 + si; };
+    double acc[4][8], v[4][8];
+    auto load = [&](const double* src, int ld) {
 #pragma unroll
-    for (int si = 0; si < 4; ++si) {
-      if (row(si) >= c1) continue;
+      for (int si = 0; si < 4; ++si)
 #pragma unroll
-      for (int f = 0; f < 8; f += 2) {
-        const double2 h = *reinterpret_cast<const double2*>(h1o + row(si) * kHS + feat(f));
-        const double v0 = (acc[si][f] + gz2[si][f]) * (1.0 - h.x * h.x);
-        const double v1 = (acc[si][f + 1] + gz2[si][f + 1]) * (1.0 - h.y * h.y);
-        *reinterpret_cast<double2*>(gz1o + row(si) * 64 + feat(f)) = make_double2(v0, v1);
+        for (int f = 0; f < 8; f += 2) {
+          double2 x = make_double2(0.0, 0.0);
+          if (row(si) < c1) x = *reinterpret_cast<const double2*>(src + row(si) * ld + feat(f));
+          v[si][f] = x.x;
+          v[si][f + 1] = x.y;
+        }
+    };
+    auto to_act = [&]() {
+      __syncwarp();
+#pragma unroll
+      for (int f = 0; f < 8; ++f) {
+        *reinterpret_cast<double2*>(act + pidx(feat(f), sq * 4)) = make_double2(v[0][f], v[1][f]);
+        *reinterpret_cast<double2*>(act + pidx(feat(f), sq * 4 + 2)) = make_double2(v[2][f], v[3][f]);
       }
-    }
+      __syncwarp();
+    };
+    auto gemm = [&](const double* wm) {
+#pragma unroll
+      for (int si = 0; si < 4; ++si)
+#pragma unroll
+        for (int f = 0; f < 8; ++f) acc[si][f] = 0.0;
+#pragma unroll 4
+      for (int kk = 0; kk < kHid; ++kk) {
+        const double2 a01 = *reinterpret_cast<const double2*>(act + pidx(kk, sq * 4));
+        const double2 a23 = *reinterpret_cast<const double2*>(act + pidx(kk, sq * 4 + 2));
+        const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+        double wv[8];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const double2 t = *reinterpret_cast<const double2*>(wm + kk * kHid + 16 * m + 2 * hq);
+          wv[2 * m] = t.x;
+          wv[2 * m + 1] = t.y;
+        }
+#pragma unroll
+        for (int si = 0; si < 4; ++si)
+#pragma unroll
+          for (int f = 0; f < 8; ++f) acc[si][f] = fma(av[si], wv[f], acc[si][f]);
+      }
+    };
+    load(gi, 64);  // g -> act
+    to_act();
+    gemm(w3o);     // W3ᵀ g
+    load(h2i, kHS);
+#pragma unroll
+    for (int si = 0; si < 4; ++si)
+#pragma unroll
+      for (int f = 0; f < 8; ++f) v[si][f] = acc[si][f] * (1.0 - v[si][f] * v[si][f]);  // gz2
+#pragma unroll
+    for (int si = 0; si < 4; ++si)
+      if (row(si) < c1)
+#pragma unroll
+        for (int f = 0; f < 8; f += 2)
+          *reinterpret_cast<double2*>(gz2o + row(si) * 64 + feat(f)) = make_double2(v[si][f], v[si][f + 1]);
+    to_act();
+    gemm(w2o);     // W2ᵀ gz2; v still holds gz2 (the residual)
+#pragma unroll
+    for (int si = 0; si < 4; ++si)
+#pragma unroll
+      for (int f = 0; f < 8; ++f) acc[si][f] += v[si][f];
+    load(h1i, kHS);
+#pragma unroll
+    for (int si = 0; si < 4; ++si)
+      if (row(si) < c1)
+#pragma unroll
+        for (int f = 0; f < 8; f += 2)
+          *reinterpret_cast<double2*>(gz1o + row(si) * 64 + feat(f)) =
+              make_double2(acc[si][f] * (1.0 - v[si][f] * v[si][f]), acc[si][f + 1] * (1.0 - v[si][f + 1] * v[si][f + 1]));
   }
 }
 
