@@ -1133,8 +1133,8 @@ void run_rows(qvmc_ham_s* h, const uint64_t* keys, int64_t r0, int64_t r1, const
 // (locality), rebuild the index on the sorted copy, process rows in that
 // order. Returns the row set; keys/la/ph are redirected to the sorted copies.
 template <int W>
-RowSet sort_for_locality(qvmc_ham_s* h, const uint64_t*& keys, const double* la, const double* ph, int64_t n,
-                         int64_t r0, int64_t r1, const RowPlan& P) {
+RowSet sort_for_locality(qvmc_ham_s* h, const uint64_t*& keys, int64_t n, int64_t r0, int64_t r1,
+                         const RowPlan& P) {
   h->l_key.ensure(n * 8 + 16);
   h->l_key2.ensure(n * 8 + 16);
   h->l_idx.ensure(n * 4 + 16);
@@ -1155,11 +1155,9 @@ RowSet sort_for_locality(qvmc_ham_s* h, const uint64_t*& keys, const double* la,
                                      h->l_idx.as<uint32_t>(), h->l_perm.as<uint32_t>(), ni, 0, 64, h->stream),
      "sort");
   ++g_launches;
-  ck(cudaMemsetAsync(static_cast<int*>(h->ctl.p) + 14, 0, sizeof(int), h->stream), "memset exp flag");
-  k_gather_sorted<W><<<std::max(grid, 1), kThreads, 0, h->stream>>>(
-      h->l_perm.as<uint32_t>(), n, keys, la, ph, h->l_keys.as<uint64_t>(), h->l_rec.as<double>(),
-      static_cast<int*>(h->ctl.p) + 14);
-  ck_launch("gather sorted");
+  k_gather_keys<W><<<std::max(grid, 1), kThreads, 0, h->stream>>>(h->l_perm.as<uint32_t>(), n, keys,
+                                                                  h->l_keys.as<uint64_t>());
+  ck_launch("gather sorted keys");
   keys = h->l_keys.as<uint64_t>();
   RowSet R{n, 0, nullptr, h->l_perm.as<uint32_t>(), r0};
   if (r0 != 0 || r1 != n) {  // a row shard: the sorted positions of its rows
@@ -1183,6 +1181,16 @@ RowSet sort_for_locality(qvmc_ham_s* h, const uint64_t*& keys, const double* la,
     R.n_rows = r1 - r0;
   }
   return R;
+}
+
+// the sample records in the order sort_for_locality chose (needs the amplitudes)
+void gather_records(qvmc_ham_s* h, const double* la, const double* ph, int64_t n) {
+  const int grid = static_cast<int>(std::min<int64_t>((n + kThreads - 1) / kThreads, grid_for(h, 8)));
+  ck(cudaMemsetAsync(static_cast<int*>(h->ctl.p) + 14, 0, sizeof(int), h->stream), "memset exp flag");
+  k_gather_records<<<std::max(grid, 1), kThreads, 0, h->stream>>>(h->l_perm.as<uint32_t>(), n, la, ph,
+                                                                   h->l_rec.as<double>(),
+                                                                   static_cast<int*>(h->ctl.p) + 14);
+  ck_launch("gather sorted records");
 }
 
 void note_plan(qvmc_ham_s* h, const RowPlan& P) {
@@ -1980,16 +1988,18 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       }
       note_plan(h, P);
       if (!P.join) DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
-      wait_amplitudes();
       if (P.join) {
-        DISPATCH_W(W, R = sort_for_locality<WW>(h, rkeys, dla, dph, n_unq, row_begin, row_end, P));
+        DISPATCH_W(W, R = sort_for_locality<WW>(h, rkeys, n_unq, row_begin, row_end, P));
         if (h->view.n_res) DISPATCH_W(W, launch_table_build<WW>(h, rkeys, n_unq));  // residual probes: sorted ids
         // symmetric when every row of the set is evaluated by this call, or by the ranks of a sharded call
         const bool sym = h->sym && !h->sym_off_once && !h->fused && (R.list == nullptr || h->shard_sym);
         h->sym_off_once = false;
         h->shard_sym_active = sym && h->shard_sym;
         DISPATCH_W(W, build_join_index<WW>(h, rkeys, n_unq, P, sym));
+        wait_amplitudes();  // a host caller's amplitude upload ran beside the index build
+        gather_records(h, dla, dph, n_unq);
       } else {
+        wait_amplitudes();
         h->cs.ensure(n_unq * 16 + 16);
         const int grid = static_cast<int>(std::min<int64_t>((n_unq + kThreads - 1) / kThreads, grid_for(h, 8)));
         k_cos_sin<<<std::max(grid, 1), kThreads, 0, h->stream>>>(dph, n_unq, h->cs.as<double2>());

@@ -164,13 +164,21 @@ __global__ void __launch_bounds__(kThreads)
 // multiply by the row's 1/e^{log psi} instead of an exp per pair, unless some
 // |log psi| > 700 (then exp_flag is set and the exp path is used).
 template <int W>
-__global__ void k_gather_sorted(const uint32_t* __restrict__ perm, int64_t n, const uint64_t* __restrict__ keys,
-                                const double* __restrict__ la, const double* __restrict__ ph, uint64_t* keys_s,
-                                double* rec, int* exp_flag) {
+__global__ void k_gather_keys(const uint32_t* __restrict__ perm, int64_t n, const uint64_t* __restrict__ keys,
+                              uint64_t* __restrict__ keys_s) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t o = perm[i];
 #pragma unroll
     for (int w = 0; w < W; ++w) keys_s[i * W + w] = keys[(int64_t)o * W + w];
+  }
+}
+
+// sample records in locality order (log|psi|, cos phi, sin phi, e^log|psi|); gathered after the
+// deletion index is built, so a host caller's amplitude upload overlaps the build
+__global__ void k_gather_records(const uint32_t* __restrict__ perm, int64_t n, const double* __restrict__ la,
+                                 const double* __restrict__ ph, double* __restrict__ rec, int* __restrict__ exp_flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t o = perm[i];
     double sn, c;
     sincos(ph[o], &sn, &c);
     const double l = la[o];

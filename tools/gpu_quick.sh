@@ -1,6 +1,7 @@
 #!/bin/bash
 # quick iteration: selected GPU tests (-k EXPR) then c118/c56 bench lines
 TAG=$1; K=${2:-large_bucket}; OUT=gpurun_out/$TAG; mkdir -p $OUT
+make -s -C paper_2408_07625_b200/csrc > $OUT/make.log 2>&1 || { echo 'build failed'; tail $OUT/make.log; exit 1; }  # never measure a stale .so
 timeout 1200 python -m pytest tests -m gpu -x -q -k "$K" > $OUT/pytest_sel.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_sel.log
 tail -n 15 $OUT/pytest_sel.log
 for cfg in c118 c56; do
