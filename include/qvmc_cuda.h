@@ -230,9 +230,13 @@ int qvmc_cuda_comm_destroy(qvmc_comm_t c);
  * ranks of `comm` as rows. Each rank passes its own shard
  * (qvmc_shard_bounds rows of an n_total-row sample set: keys, log|psi|,
  * phase, log p); the call all-gathers the shards (one all-gather of packed
- * [W + 3]-word records), evaluates E_loc of its rows against the whole set
- * with the fused kernels, and gathers the per-rank moments and sums them in
- * rank order (deterministic). out_eloc: this rank's rows [rows][2];
+ * [W + 3]-word records) and evaluates E_loc against the whole set with the
+ * fused kernels. The walk is balanced independently of the caller's sample
+ * order: rank r walks every world-th sample of the locality-sorted set
+ * (QVMC_STRIDED_SHARDS=0: its own rows), and one integer all-reduce assembles
+ * the rows (each written by exactly one rank, so the result is exact); the
+ * per-rank moments of its own rows are gathered and summed in rank order
+ * (deterministic). out_eloc: this rank's rows [rows][2];
  * out_moments[5]: global, as qvmc_cuda_eloc_fused. With QVMC_MEM_DEVICE and
  * the NCCL backend every step is enqueued on the handle's stream. */
 int qvmc_cuda_eloc_sharded(qvmc_ham_t h, qvmc_comm_t comm, int64_t n_total, const uint64_t* keys,

@@ -266,6 +266,8 @@ struct qvmc_ham_s {
                            // left in s_fix for the cross-rank reduction (not added by finalize)
   RowSet last_rows{};      // the row set of the last fused call (sorted positions -> caller rows)
   bool fused = false;  // QVMC_FUSED=1: one warp-specialised search + evaluation kernel (measured slower, r2a)
+  bool strided_shards = true;  // QVMC_STRIDED_SHARDS=0: a sharded call walks its own (contiguous) caller rows
+  int walk_world = 0, walk_rank = 0;  // set by qvmc_cuda_eloc_sharded: walk sorted positions rank, rank + world, ...
   int64_t timed_b = 0;            // batches timed by ev_b in the last call
 };
 
@@ -989,8 +991,10 @@ bool run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
     h->p_hit_cap = std::min<uint64_t>(static_cast<uint64_t>(batch) * per_row * 5 / 4 + (1u << 16), 0xFFFFFFFFull);
     h->p_chunk_cap = h->p_hit_cap / 32 + static_cast<uint64_t>(batch) + 1024;
   }
-  h->s_row_last.ensure(rows * 4 + 16);
-  h->s_base.ensure(rows * 16 + 16);
+  // per-row outputs are indexed by caller row - R.out_base: a strided sharded walk spans every row
+  const int64_t span = h->walk_world > 1 ? n_all : rows;
+  h->s_row_last.ensure(span * 4 + 16);
+  h->s_base.ensure(span * 16 + 16);
   h->s_rowpos.ensure(static_cast<size_t>(n_all) * 16 + 16);
   if (!h->side) {
     ck(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking), "stream create");
@@ -1160,7 +1164,19 @@ RowSet sort_for_locality(qvmc_ham_s* h, const uint64_t*& keys, int64_t n, int64_
   ck_launch("gather sorted keys");
   keys = h->l_keys.as<uint64_t>();
   RowSet R{n, 0, nullptr, h->l_perm.as<uint32_t>(), r0};
-  if (r0 != 0 || r1 != n) {  // a row shard: the sorted positions of its rows
+  if (h->walk_world > 1) {  // sharded call, strided walk: every world-th sorted position (balanced
+    // whatever the caller's sample order: neighbours in locality order cost about the same)
+    const int64_t nr = n > h->walk_rank ? (n - h->walk_rank + h->walk_world - 1) / h->walk_world : 0;
+    h->l_list.ensure(std::max<int64_t>(nr, 1) * 4 + 16);
+    const int sg = static_cast<int>(std::min<int64_t>((std::max<int64_t>(nr, 1) + kThreads - 1) / kThreads,
+                                                      grid_for(h, 8)));
+    k_strided_rows<<<sg, kThreads, 0, h->stream>>>(h->l_list.as<uint32_t>(), nr,
+                                                   static_cast<uint32_t>(h->walk_rank),
+                                                   static_cast<uint32_t>(h->walk_world));
+    ck_launch("strided rows");
+    R.list = h->l_list.as<uint32_t>();
+    R.n_rows = nr;
+  } else if (r0 != 0 || r1 != n) {  // a row shard: the sorted positions of its rows
     h->l_flags.ensure(n + 16);
     h->l_list.ensure(n * 4 + 16);
     h->l_nsel.ensure(16);
@@ -1489,6 +1505,7 @@ int qvmc_cuda_ham_create(int n_qubits, int n_words, uint32_t n_xy, const uint64_
     if (const char* e = std::getenv("QVMC_FUSED")) h->fused = std::atoi(e) != 0;
     if (const char* e = std::getenv("QVMC_SYMMETRIC")) h->sym = std::atoi(e) != 0;
     if (const char* e = std::getenv("QVMC_DIST_INDEX")) h->dist_index = std::atoi(e) != 0;
+    if (const char* e = std::getenv("QVMC_STRIDED_SHARDS")) h->strided_shards = std::atoi(e) != 0;
     if (const char* e = std::getenv("QVMC_SPECULATE")) h->no_spec = std::atoi(e) == 0;  // opt-in
     if (const char* e = std::getenv("QVMC_PIPE_BATCHES")) h->pipe_batches = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("QVMC_PIPE_SEARCH_BLOCKS")) h->pipe_search_blocks = std::atoi(e);
@@ -1932,7 +1949,8 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
     if (h->pending) resolve_pending(h);  // an earlier speculative call is checked first
     // speculative: device memory and a cached sector plan for this sample-set size -> no host
     // synchronisation anywhere in the call (CUDA-graph capturable once the buffers are sized)
-    const bool spec = mem == QVMC_MEM_DEVICE && !h->no_spec && h->plan_ok && h->plan_n == n_unq && n_unq > 0;
+    const bool spec = mem == QVMC_MEM_DEVICE && !h->no_spec && h->plan_ok && h->plan_n == n_unq && n_unq > 0 &&
+                      h->walk_world <= 1;
     const int W = h->W;
     const int64_t rows = row_end - row_begin;
     const uint64_t* dkeys = stage(h, h->keys, keys, static_cast<size_t>(n_unq) * W, mem);
@@ -2030,7 +2048,13 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
           DISPATCH_W(W, (run_join_pipelined<WW>(h, rkeys, n_unq, R, P, deloc, false)));
         }
       } else {
-        DISPATCH_W(W, (launch_rows<WW, kModeEloc>(h, dkeys, row_begin, row_end, O)));
+        int64_t b = row_begin, e = row_end;
+        RowOut Os = O;
+        if (h->walk_world > 1) {  // sharded, strided mode: rows without the join are split contiguously
+          shard_range(n_unq, h->walk_world, h->walk_rank, b, e);
+          Os.eloc = deloc + (b - row_begin);
+        }
+        DISPATCH_W(W, (launch_rows<WW, kModeEloc>(h, dkeys, b, e, Os)));
       }
     }
     ck(cudaEventRecord(h->ev[2], h->stream), "event");
@@ -2186,14 +2210,46 @@ int qvmc_cuda_eloc_sharded(qvmc_ham_t h, qvmc_comm_t comm, int64_t n_total, cons
     h->shard_sym = world > 1;
     h->fix_range_flag = false;
     h->dist_comm = (world > 1 && h->dist_index) ? comm : nullptr;
-    const int st = qvmc_cuda_eloc_fused(h, n_total, h->g_keys.as<uint64_t>(), h->g_la.as<double>(),
-                                        h->g_ph.as<double>(), log_prob ? h->g_lp.as<double>() : nullptr, log_norm,
-                                        r0, r1, deloc, out_moments ? h->g_mom.as<double>() : nullptr,
-                                        QVMC_MEM_DEVICE);
+    // strided walk (default for world > 1): this rank walks sorted positions rank, rank + world, ...
+    // into a zeroed n_total-row vector in caller order; each row is written by exactly one rank, so an
+    // integer all-reduce of the bit patterns assembles the single-GPU result exactly on every rank
+    const bool strided = world > 1 && h->strided_shards && n_total > 0;
+    if (strided) {
+      h->eloc.ensure(static_cast<size_t>(n_total) * 16);
+      ck(cudaMemsetAsync(h->eloc.p, 0, static_cast<size_t>(n_total) * 16, h->stream), "memset rows");
+      h->walk_world = world;
+      h->walk_rank = rank;
+    }
+    const int st = strided ? qvmc_cuda_eloc_fused(h, n_total, h->g_keys.as<uint64_t>(), h->g_la.as<double>(),
+                                                  h->g_ph.as<double>(), nullptr, log_norm, 0, n_total, nullptr,
+                                                  nullptr, QVMC_MEM_DEVICE)
+                           : qvmc_cuda_eloc_fused(h, n_total, h->g_keys.as<uint64_t>(), h->g_la.as<double>(),
+                                                  h->g_ph.as<double>(), log_prob ? h->g_lp.as<double>() : nullptr,
+                                                  log_norm, r0, r1, deloc,
+                                                  out_moments ? h->g_mom.as<double>() : nullptr, QVMC_MEM_DEVICE);
     h->shard_sym = false;
     h->dist_comm = nullptr;
+    h->walk_world = 0;
     if (st != QVMC_OK) fail(st, g_error);
-    if (h->shard_sym_active) {
+    if (strided) {
+      double2* de = h->eloc.as<double2>();
+      if (h->shard_sym_active) {
+        h->shard_sym_active = false;
+        comm_all_reduce_u64(comm, h->s_fix.as<unsigned long long>(), static_cast<size_t>(n_total) * 4, h->stream,
+                            h->g_recv);
+        const RowSet R = h->last_rows;
+        const int fg = static_cast<int>(std::min<int64_t>((R.n_rows + kThreads - 1) / kThreads, grid_for(h, 8)));
+        k_add_fix<<<std::max(fg, 1), kThreads, 0, h->stream>>>(R, h->s_fix.as<unsigned long long>(), de);
+        ck_launch("add mirrored sums");
+      }
+      comm_all_reduce_u64(comm, h->eloc.as<unsigned long long>(), static_cast<size_t>(n_total) * 2, h->stream,
+                          h->g_recv);
+      if (out_moments && rows > 0)
+        compute_moments(h, log_prob ? h->g_lp.as<double>() + r0 : nullptr, log_norm, de + r0, rows,
+                        h->g_mom.as<double>(), nullptr);
+      if (mem == QVMC_MEM_DEVICE && out_eloc && rows > 0)
+        ck(cudaMemcpyAsync(out_eloc, de + r0, rows * 16, cudaMemcpyDeviceToDevice, h->stream), "copy rows");
+    } else if (h->shard_sym_active) {
       h->shard_sym_active = false;
       comm_all_reduce_u64(comm, h->s_fix.as<unsigned long long>(), static_cast<size_t>(n_total) * 4, h->stream,
                           h->g_recv);
@@ -2238,7 +2294,8 @@ int qvmc_cuda_eloc_sharded(qvmc_ham_t h, qvmc_comm_t comm, int64_t n_total, cons
     }
     if (mem == QVMC_MEM_HOST) {
       if (out_eloc && rows)
-        ck(cudaMemcpyAsync(out_eloc, h->eloc.p, rows * 16, cudaMemcpyDeviceToHost, h->stream), "D2H eloc");
+        ck(cudaMemcpyAsync(out_eloc, h->eloc.as<double2>() + (strided ? r0 : 0), rows * 16, cudaMemcpyDeviceToHost,
+                           h->stream), "D2H eloc");
       finish(h);
     }
   });

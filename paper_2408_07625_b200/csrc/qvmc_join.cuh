@@ -189,6 +189,12 @@ __global__ void k_gather_records(const uint32_t* __restrict__ perm, int64_t n, c
 
 // per-sample records in the caller's order (pairs-free fused path without the
 // locality sort is not used; kept for the row-shard gather)
+// strided walk assignment of a sharded call: sorted positions phase, phase + stride, ...
+__global__ void k_strided_rows(uint32_t* __restrict__ list, int64_t n_rows, uint32_t phase, uint32_t stride) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows; i += (int64_t)gridDim.x * blockDim.x)
+    list[i] = phase + static_cast<uint32_t>(i) * stride;
+}
+
 __global__ void k_flag_rows(const uint32_t* __restrict__ perm, int64_t n, int64_t r0, int64_t r1, uint8_t* flags) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     flags[i] = perm[i] >= r0 && perm[i] < r1;

@@ -7,8 +7,9 @@ per-rank moments in rank order. Checked on one B200:
     to qvmc_cuda_eloc_fused, host and device memory;
   * world 2 and 3 with the host all-gather backend over gloo, every rank a
     process on cuda:0 (NCCL refuses two ranks on one GPU): each rank walks
-    its rows' partners after them and the mirrored fixed-point sums are
-    all-reduced exactly, so each rank's rows are bit-identical to the
+    every world-th row of the locality order (or its own rows), partners
+    after them, the mirrored fixed-point sums are all-reduced exactly and
+    the rows assembled exactly, so each rank's rows are bit-identical to the
     unsharded (symmetric) E_loc; moments to fp64 reordering.
 """
 import ctypes as C
@@ -21,10 +22,15 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _problem(n_qubits=56, n_e=14, n_terms=300_000, n_unq=20_011):
+def _problem(n_qubits=56, n_e=14, n_terms=300_000, n_unq=20_011, by_excitation=False):
     from paper_2408_07625_b200 import synthetic
     c, x, y, z = synthetic.jw_terms(n_qubits, n_terms, seed=1)
     keys = synthetic.near_hf_keys(n_qubits, n_e, n_unq, seed=4)
+    if by_excitation:  # samples ordered by excitation rank (as a sampler's beam order can be):
+        # contiguous shards then carry very different pair counts
+        hf = (1 << n_e) - 1
+        rank = np.array([bin(int(k) ^ hf).count("1") for k in keys[:, 0]])
+        keys = keys[np.argsort(rank, kind="stable")]
     return n_qubits, (c, x, y, z), synthetic.sample_batch(keys, seed=3)
 
 
@@ -71,7 +77,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out_q):
+def _worker(rank, world, port, out_q, by_excitation=False):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -79,7 +85,7 @@ def _worker(rank, world, port, out_q):
     try:
         import paper_2408_07625_b200 as q
         from paper_2408_07625_b200.distributed import Communicator, Shard, shard_bounds, sharded_surrogate_energy_capi
-        n_qubits, masks, b = _problem()
+        n_qubits, masks, b = _problem(by_excitation=by_excitation)
         H = q.HamiltonianIndex.from_masks(n_qubits, *masks)
         r0, r1 = shard_bounds(b.size(), world, rank)
         dev = torch.device("cuda", 0)
@@ -89,28 +95,35 @@ def _worker(rank, world, port, out_q):
         comm = Communicator.host()
         res = sharded_surrogate_energy_capi(H, comm, 0, b.size(), sh, b.log_norm)
         torch.cuda.synchronize()
-        mode = q.last_stats(H)["join_mode"]
-        out_q.put((rank, res.row_begin, res.row_end, res.locals.cpu().numpy(), res.moments.cpu().numpy(), mode))
+        st = q.last_stats(H)
+        out_q.put((rank, res.row_begin, res.row_end, res.locals.cpu().numpy(), res.moments.cpu().numpy(),
+                   st["join_mode"], st["pairs"]))
         comm.close()
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,dist", [(2, "1"), (3, "1"), (2, "0")])
-def test_multi_rank_host_backend_matches_unsharded(cuda_ok, monkeypatch, world, dist):
+@pytest.mark.parametrize("world,dist,strided,by_exc", [
+    (2, "1", "1", False), (3, "1", "1", False), (2, "0", "1", False),
+    (3, "1", "0", False), (3, "1", "1", True), (3, "1", "0", True)])
+def test_multi_rank_host_backend_matches_unsharded(cuda_ok, monkeypatch, world, dist, strided, by_exc):
     """dist = 1: the deletion index is built across the ranks (each sorts the buckets it owns,
-    all-gather of members, all-reduce of ranges); 0: every rank builds the whole index."""
+    all-gather of members, all-reduce of ranges); 0: every rank builds the whole index.
+    strided = 1 (default): rank r walks sorted positions r, r + world, ... and the rows are
+    assembled by an exact all-reduce; 0: each rank walks its own caller rows. by_exc: samples
+    ordered by excitation rank, where contiguous walks are unbalanced and strided ones are not."""
     monkeypatch.setenv("QVMC_DIST_INDEX", dist)
+    monkeypatch.setenv("QVMC_STRIDED_SHARDS", strided)
     import torch.multiprocessing as mp
     import paper_2408_07625_b200 as q
-    n_qubits, masks, b = _problem()
+    n_qubits, masks, b = _problem(by_excitation=by_exc)
     H = q.HamiltonianIndex.from_masks(n_qubits, *masks)
     ref = q.surrogate_energy(H, b)
     w = np.exp(b.log_probs - b.log_norm)
     ctx = mp.get_context("spawn")
     qu = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, qu)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, qu, by_exc)) for r in range(world)]
     for p in procs:
         p.start()
     outs = sorted(qu.get(timeout=600) for _ in procs)
@@ -118,7 +131,14 @@ def test_multi_rank_host_backend_matches_unsharded(cuda_ok, monkeypatch, world, 
         p.join(timeout=120)
         assert p.exitcode == 0
     covered = 0
-    for rank, r0, r1, loc, mom, mode in outs:
+    pairs = [o[6] for o in outs]
+    if strided == "1":  # neighbours in locality order cost about the same: balanced walks
+        assert max(pairs) <= 1.1 * min(pairs), pairs
+    bad = [(o[0], [(int(i) + o[1], complex(o[3][i]), complex(ref.locals[o[1] + i]))
+                   for i in np.flatnonzero(o[3] != ref.locals[o[1]:o[2]])[:4]]) for o in outs]
+    bad = [(r, v) for r, v in bad if v]
+    assert not bad, bad  # rows differing from the unsharded E_loc, per rank
+    for rank, r0, r1, loc, mom, mode, _ in outs:
         assert mode == (2 if dist == "1" else 1)
         # symmetric across ranks (each unordered pair once, mirrored sums all-reduced exactly):
         # every row is the single-GPU result bit for bit
