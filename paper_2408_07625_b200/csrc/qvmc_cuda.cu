@@ -917,17 +917,38 @@ JoinView join_view(qvmc_ham_s* h, const RowPlan& P) {
   return J;
 }
 
+// dynamic shared memory of a k_rows_join launch (kModeFused's rings, then one
+// bucket-table region per search warp sized by this call's s), with the
+// function's limit raised once per device when it exceeds the default
+template <int W, int MODE>
+size_t join_smem(int s) {
+  constexpr bool fused = MODE == kModeFused;
+  const int nr = s * (s - 1) / 2;
+  const size_t dyn = (fused ? sizeof(FusedSmem) : 0) + static_cast<size_t>(fused ? kFSearch : kWarps) *
+                                                          join_range_bytes(nr);
+  static size_t set_to[64] = {};
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "device");
+  if (dev >= 0 && dev < 64 && dyn > set_to[dev]) {
+    ck(cudaFuncSetAttribute(k_rows_join<W, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)),
+       "smem attribute");
+    set_to[dev] = dyn;
+  }
+  return dyn;
+}
+
 template <int W, int MODE>
 void launch_rows_join(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const RowPlan& P, const RowOut& O) {
   ck(cudaMemsetAsync(static_cast<int*>(h->ctl.p) + 4, 0, 2 * sizeof(int), h->stream), "memset row counter");
   int per_sm = 0;
-  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_join<W, MODE>, kThreads, 0), "occupancy");
+  const size_t dyn = join_smem<W, MODE>(P.s);
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_join<W, MODE>, kThreads, dyn), "occupancy");
   const int64_t blocks_needed = (R.n_rows + kWarps - 1) / kWarps;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_needed, grid_for(h, per_sm))));
   TableView T{h->tab.as<uint64_t>(), h->tab_buckets - 1};
   if (R.n_rows > 0) {
-    k_rows_join<W, MODE><<<grid, kThreads, 0, h->stream>>>(h->view, T, join_view(h, P), keys, R, P.side, P.s,
-                                                         ctl_view(h), O);
+    k_rows_join<W, MODE><<<grid, kThreads, dyn, h->stream>>>(h->view, T, join_view(h, P), keys, R, P.side, P.s,
+                                                           ctl_view(h), O);
     ck_launch("row kernel (join)");
   }
 }
@@ -941,9 +962,7 @@ void run_join_fused(qvmc_ham_s* h, const uint64_t* keys, const RowSet& R, const 
   int* ctl = static_cast<int*>(h->ctl.p);
   ck(cudaMemsetAsync(ctl + 4, 0, 2 * sizeof(int), h->stream), "memset row counter");
   int per_sm = 0;
-  constexpr size_t dyn = sizeof(FusedSmem);
-  ck(cudaFuncSetAttribute(k_rows_join<W, kModeFused>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)),
-     "smem attribute");
+  const size_t dyn = join_smem<W, kModeFused>(P.s);
   ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_join<W, kModeFused>, kFThreads, dyn), "occupancy");
   const int64_t blocks_needed = (R.n_rows + kFSearch - 1) / kFSearch;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_needed, grid_for(h, per_sm))));
@@ -995,7 +1014,7 @@ bool run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
   const int64_t span = h->walk_world > 1 ? n_all : rows;
   h->s_row_last.ensure(span * 4 + 16);
   h->s_base.ensure(span * 16 + 16);
-  h->s_rowpos.ensure(static_cast<size_t>(n_all) * 16 + 16);
+  h->s_rowpos.ensure(static_cast<size_t>(n_all) * 32 + 16);
   if (!h->side) {
     ck(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking), "stream create");
     for (auto& e : h->ev_p) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
@@ -1026,7 +1045,9 @@ bool run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
       h->p_part[k].ensure(h->p_chunk_cap * 16 + 16);
     }
     int per_sm_s = 0, per_sm_e = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, k_rows_join<W, kModeHits>, kThreads, 0), "occupancy");
+    const size_t dyn_s = join_smem<W, kModeHits>(P.s);
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, k_rows_join<W, kModeHits>, kThreads, dyn_s),
+       "occupancy");
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_e, k_eval_chunks<W>, kThreads, 0), "occupancy");
     if (h->pipe_search_blocks > 0) per_sm_s = std::min(per_sm_s, h->pipe_search_blocks);
     if (h->pipe_eval_blocks > 0) per_sm_e = std::min(per_sm_e, h->pipe_eval_blocks);
@@ -1062,7 +1083,7 @@ bool run_join_pipelined(qvmc_ham_s* h, const uint64_t* keys, int64_t n_all, cons
       const int grid_s = static_cast<int>(
           std::max<int64_t>(1, std::min<int64_t>((Rb.n_rows + kWarps - 1) / kWarps, grid_for(h, per_sm_s))));
       ck(cudaEventRecord(h->ev_b[4 * b], A), "event");
-      k_rows_join<W, kModeHits><<<grid_s, kThreads, 0, A>>>(h->view, T, join_view(h, P), keys, Rb, P.side, P.s,
+      k_rows_join<W, kModeHits><<<grid_s, kThreads, dyn_s, A>>>(h->view, T, join_view(h, P), keys, Rb, P.side, P.s,
                                                             ctl_view(h), O);
       ck_launch("row kernel (join search)");
       ck(cudaEventRecord(h->ev_b[4 * b + 1], A), "event");
@@ -1985,6 +2006,7 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
     ck(cudaMemsetAsync(static_cast<int*>(h->ctl.p) + 6, 0, 4 * sizeof(int), h->stream), "memset stats");
     ck(cudaEventRecord(h->ev[0], h->stream), "event");
     RowPlan P;
+    bool fused_ok = false;  // QVMC_FUSED=1 and a minority set the fused rings carry
     RowSet R{};
     const uint64_t* rkeys = dkeys;
     const double2* rcs = nullptr;
@@ -2005,12 +2027,13 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
         P = plan_rows(h, n_unq);
       }
       note_plan(h, P);
+      fused_ok = h->fused && P.s <= kFusedMaxMinority;
       if (!P.join) DISPATCH_W(W, launch_table_build<WW>(h, dkeys, n_unq));
       if (P.join) {
         DISPATCH_W(W, R = sort_for_locality<WW>(h, rkeys, n_unq, row_begin, row_end, P));
         if (h->view.n_res) DISPATCH_W(W, launch_table_build<WW>(h, rkeys, n_unq));  // residual probes: sorted ids
         // symmetric when every row of the set is evaluated by this call, or by the ranks of a sharded call
-        const bool sym = h->sym && !h->sym_off_once && !h->fused && (R.list == nullptr || h->shard_sym);
+        const bool sym = h->sym && !h->sym_off_once && !fused_ok && (R.list == nullptr || h->shard_sym);
         h->sym_off_once = false;
         h->shard_sym_active = sym && h->shard_sym;
         DISPATCH_W(W, build_join_index<WW>(h, rkeys, n_unq, P, sym));
@@ -2033,7 +2056,7 @@ int qvmc_cuda_eloc_fused(qvmc_ham_t h, int64_t n_unq, const uint64_t* keys, cons
       O.ph = dph;
       O.cs = rcs;
       h->last_rows = R;
-      if (P.join && h->fused) {
+      if (P.join && fused_ok) {
         DISPATCH_W(W, (run_join_fused<WW>(h, rkeys, R, P, deloc)));
       } else if (P.join) {
         bool redo = false;
@@ -2262,7 +2285,7 @@ int qvmc_cuda_eloc_sharded(qvmc_ham_t h, qvmc_comm_t comm, int64_t n_total, cons
         compute_moments(h, log_prob ? h->g_lp.as<double>() + r0 : nullptr, log_norm, de, rows,
                         h->g_mom.as<double>(), nullptr);
     }
-    const bool flagged = world > 1 && h->sym && !h->fused;  // symmetric sharded: exchange the range flag too
+    const bool flagged = world > 1 && h->sym && !(h->fused && h->last.minority_count <= kFusedMaxMinority);  // symmetric: the range flag too
     if (flagged) {
       const double f = h->fix_range_flag ? 1.0 : 0.0;
       ck(cudaMemcpyAsync(h->g_mom.as<double>() + 7, &f, sizeof(double), cudaMemcpyHostToDevice, h->stream), "flag");

@@ -37,9 +37,17 @@ namespace qvmc_b200 {
 #endif
 
 
-constexpr int kJoinMaxMinority = 16;  // s <= 16: at most 120 buckets per row
+constexpr int kJoinMaxMinority = 24;  // s <= 24: at most 276 buckets per row
 constexpr int kJoinMaxRanges = kJoinMaxMinority * (kJoinMaxMinority - 1) / 2;
-constexpr int kBinomK = kJoinMaxMinority + 1;  // binomial table C[n][k], k <= 16
+constexpr int kBinomK = kJoinMaxMinority + 1;  // binomial table C[n][k], k <= 24
+constexpr int kFusedMaxMinority = 16;            // kModeFused hands at most 16 minority orbitals per row
+
+// A row's bucket tables (k_rows_join) live in dynamic shared memory, one region
+// per search warp sized by the call's bucket count nr = s(s - 1)/2:
+// binfo[nr] (uint2), pre[nr + 1] (uint32), tab[nr] (uint16), 16-byte aligned.
+__host__ __device__ constexpr uint32_t join_range_bytes(int nr) {
+  return (8u * nr + 4u * (nr + 1) + 2u * nr + 15u) & ~15u;
+}
 constexpr uint32_t kNoKey = 0xFFFFFFFFu;
 
 // Per-group drain record, 8 words (two 32-byte sectors), host_index.cpp:
@@ -529,13 +537,7 @@ struct JoinSmem {
   uint32_t qy[kJQueue];  // hit queue: partner (sorted position), group, flip position key
   uint32_t qg[kJQueue];
   uint32_t qk[kJQueue];
-  // the row's buckets: pre[t] = first walk index of bucket t (exclusive prefix
-  // of the bucket lengths), pre[C] = members walked; binfo[t] = (lo - pre[t]
-  // (mod 2^32: member of walk index j at mem[binfo.x + j]), doubles-bitmap row
-  // P + pidx(T_x) * P); tab[t] = T_x.a | T_x.b << 8
-  uint32_t pre[kJoinMaxRanges + 1];
-  uint2 binfo[kJoinMaxRanges];
-  uint16_t tab[kJoinMaxRanges];
+  // (the row's bucket tables pre / binfo / tab: dynamic shared memory, join_range_bytes)
   uint64_t x[4];                  // the current row: key, log psi, (cos, sin) of its phase; kept here
   double la, cs_c, cs_s;          // (not in registers) across the candidate walk
   uint16_t pos[32];               // minority orbitals of the current row
@@ -804,7 +806,7 @@ __global__ void __launch_bounds__(MODE == kModeFused ? kFThreads : kThreads,
   constexpr bool kEval = MODE == kModeHits || kFused;  // E_loc rows (split or fused evaluation)
   constexpr int kSearchWarps = kFused ? kFSearch : kWarps;
   __shared__ JoinSmem s_w[kSearchWarps];
-  // kModeFused: the chunk rings live in dynamic shared memory (sizeof(FusedSmem))
+  // dynamic shared memory: kModeFused's chunk rings (sizeof(FusedSmem)), then the bucket tables
   extern __shared__ __align__(16) unsigned char s_dyn[];
   FusedSmem* s_f = reinterpret_cast<FusedSmem*>(s_dyn);
   __shared__ uint16_t s_epos[kFused ? kFEval : 1][32];
@@ -826,6 +828,14 @@ __global__ void __launch_bounds__(MODE == kModeFused ? kFThreads : kThreads,
   unsigned qr = 0;  // kModeFused: the ring slot this search warp fills
   const int n = H.n;
   const int n_ranges = s * (s - 1) / 2;
+  // the row's buckets: pre[t] = first walk index of bucket t (exclusive prefix
+  // of the bucket lengths), pre[C] = members walked; binfo[t] = (lo - pre[t]
+  // (mod 2^32: member of walk index j at mem[binfo.x + j]), doubles-bitmap row
+  // P + pidx(T_x) * P); tab[t] = T_x.a | T_x.b << 8
+  unsigned char* rg_base = s_dyn + (kFused ? sizeof(FusedSmem) : 0) + wid * join_range_bytes(n_ranges);
+  uint2* const s_binfo = reinterpret_cast<uint2*>(rg_base);
+  uint32_t* const s_pre = reinterpret_cast<uint32_t*>(rg_base + 8 * n_ranges);
+  uint16_t* const s_tab = reinterpret_cast<uint16_t*>(rg_base + 8 * n_ranges + 4 * (n_ranges + 1));
   if (lane == 0) {
     sm->qn = 0;
     sm->qs = 0;
@@ -924,7 +934,7 @@ __global__ void __launch_bounds__(MODE == kModeFused ? kFThreads : kThreads,
     }
     if (lane < s) {
       sm->pos[lane] = static_cast<uint16_t>(pos);
-      if (MODE == kModeHits) O.rowpos[row * 16 + lane] = static_cast<uint8_t>(pos);
+      if (MODE == kModeHits) O.rowpos[row * 32 + lane] = static_cast<uint8_t>(pos);
       if (kFused && lane >= s && lane < 16) sm->pos[lane] = 0;
     }
     __syncwarp();
@@ -953,13 +963,13 @@ __global__ void __launch_bounds__(MODE == kModeFused ? kFThreads : kThreads,
       }
       const uint32_t ex = M + inc - len;
       if (t < n_ranges) {
-        sm->tab[t] = static_cast<uint16_t>(pa | pb << 8);
-        sm->pre[t] = ex;
-        sm->binfo[t] = make_uint2(lo - ex, db);
+        s_tab[t] = static_cast<uint16_t>(pa | pb << 8);
+        s_pre[t] = ex;
+        s_binfo[t] = make_uint2(lo - ex, db);
       }
       M += __shfl_sync(0xffffffffu, inc, 31);
     }
-    if (lane == 0) sm->pre[n_ranges] = M;
+    if (lane == 0) s_pre[n_ranges] = M;
     __syncwarp();
 
     double2 acc = make_double2(0.0, 0.0);
@@ -1076,9 +1086,9 @@ __global__ void __launch_bounds__(MODE == kModeFused ? kFThreads : kThreads,
     // bucket end on fewer than half of its steps)
     {
       int t = 0;
-      uint32_t nxt = M ? sm->pre[1] : 0u;
-      uint2 bi = sm->binfo[0];
-      uint32_t tx = sm->tab[0];
+      uint32_t nxt = M ? s_pre[1] : 0u;
+      uint2 bi = s_binfo[0];
+      uint32_t tx = s_tab[0];
       constexpr int U = QVMC_JOIN_UNROLL;
       for (uint32_t base = 0; base < M; base += 32 * U) {
         uint64_t v[U];
@@ -1093,10 +1103,10 @@ __global__ void __launch_bounds__(MODE == kModeFused ? kFThreads : kThreads,
             if (nxt <= j) {
               do {
                 ++t;
-                nxt = sm->pre[t + 1];
+                nxt = s_pre[t + 1];
               } while (nxt <= j);
-              bi = sm->binfo[t];
-              tx = sm->tab[t];
+              bi = s_binfo[t];
+              tx = s_tab[t];
             }
             v[u] = __ldg(J.mem + (bi.x + j));
             utx[u] = tx;
@@ -1218,7 +1228,7 @@ __global__ void __launch_bounds__(MODE == kModeFused ? kFThreads : kThreads,
       if (H.diag_quad) {
         if (lane == 0) acc.x += side ? H.diag_A1 : H.diag_A0;
         if (lane < s) acc.x += __ldg(H.diag_b + side * n + pos);
-        for (int pi = lane; pi < n_ranges; pi += 32) acc.x += __ldg(H.diag_K + (sm->tab[pi] & 0xFF) * n + (sm->tab[pi] >> 8));
+        for (int pi = lane; pi < n_ranges; pi += 32) acc.x += __ldg(H.diag_K + (s_tab[pi] & 0xFF) * n + (s_tab[pi] >> 8));
         for (uint32_t e = lane; e < H.n_diag_other; e += 32) {
           const uint32_t t = __ldg(H.diag_other + e);
           int pc = 0;
@@ -1362,7 +1372,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
     const double inv_ai = mag ? 1.0 / __longlong_as_double(static_cast<long long>(sr.d)) : 0.0;
     // minority orbitals of the row (kind B elements), as the search kernel listed them
     __syncwarp();
-    if (lane < s) spos[lane] = __ldg(rowpos + row * 16 + lane);
+    if (lane < s) spos[lane] = __ldg(rowpos + row * 32 + lane);
     __syncwarp();
     double2 acc = make_double2(0.0, 0.0);
     const unsigned n_hits = ch.z;

@@ -61,8 +61,8 @@ CONFIGS = {
     "c56": Config("synthetic 56q (N2 cc-pVDZ-sized), 1e6 samples", 56, 14, 300_000, 1_000_000),
     "c118": Config("synthetic 118q (BeI2 STO-3G-sized), 1e6 samples", 118, 110, 3_000_000, 1_000_000),
     "c20": Config("synthetic 20q (N2 STO-3G-sized), 1e5 samples", 20, 10, 12_000, 100_000),
-    # not a BASELINE config: half filling puts 20 orbitals in the minority set (> 16), so rows take the
-    # sector candidate lists (k_rows) instead of the deletion-index join; measured so that path has a number
+    # not a BASELINE config: half filling, 20 orbitals in the minority set (190 deletion buckets per row,
+    # the join's tables sized per call; QVMC_JOIN=0 measures the sector candidate lists instead)
     "c40h": Config("synthetic 40q half-filled (20 e-), 1e5 samples", 40, 20, 100_000, 100_000),
 }
 

@@ -338,11 +338,15 @@ def test_fused_matches_split_evaluation(cuda_ok, monkeypatch, n_qubits, n_e, n_t
 
 
 @pytest.mark.parametrize("n_qubits,n_e,n_terms,n_unq,join", [
-    (48, 24, 200_000, 5_000, 0),    # minority set of 24 > 16: sector candidate lists (k_rows), not the join
+    (48, 24, 200_000, 5_000, 1),    # minority set of 24: the join's largest bucket tables (276 per row)
+    (48, 24, 200_000, 5_000, 0),    # the same through the sector candidate lists (k_rows, QVMC_JOIN=0)
+    (40, 20, 100_000, 5_000, 1),    # half filling (c40h shape), 190 buckets per row
     (130, 122, 400_000, 10_000, 1),  # 3 key words, n > 128: join without the pair-existence bitmaps
     (20, 10, 12_000, 20_000, 1),     # BASELINE config 2 shape (c20), random sector states
 ])
-def test_other_row_paths_match_oracle(cuda_ok, n_qubits, n_e, n_terms, n_unq, join):
+def test_other_row_paths_match_oracle(cuda_ok, monkeypatch, n_qubits, n_e, n_terms, n_unq, join):
+    if not join:
+        monkeypatch.setenv("QVMC_JOIN", "0")
     if n_qubits == 20:
         c, x, y, z = synthetic.jw_terms(20, n_terms, seed=1)
         H = q.HamiltonianIndex.from_masks(20, c, x, y, z)
