@@ -14,7 +14,7 @@ constexpr int kMaxMinority = 32;    // sector lists are used when min(n_e, N - n
 constexpr uint32_t kSmallGroupHost = 16;  // groups above this size are candidates for compression
 constexpr int kMaxFamilies = 4;
 constexpr int kGrecWordsHost = 8;   // qvmc_join.cuh kGrecWords
-constexpr int kBinomKHost = 25;     // qvmc_join.cuh kBinomK
+constexpr int kBinomKHost = 33;     // qvmc_join.cuh kBinomK
 
 // C(n, k) for n <= 256, k < kBinomKHost, saturating at UINT64_MAX
 // ([257][kBinomKHost], the combinadic ranks of the join's bucket keys)

@@ -743,14 +743,16 @@ RowPlan plan_from_mm(qvmc_ham_s* h, int64_t n, const int* mm) {
   const int pmax = mm[0], pmin = 1024 - mm[1];
   P.side = (pmin <= h->n - pmin) ? 1 : 0;
   P.s = P.side ? pmin : h->n - pmin;
-  P.sector = n > 0 && pmin == pmax && P.s <= kMaxMinorityDev;
+  const bool uniform = n > 0 && pmin == pmax;  // one particle sector
   const uint64_t entries = static_cast<uint64_t>(n) * (P.s * (P.s - 1) / 2);
-  P.join = h->use_join && P.sector && P.s >= 2 && P.s <= kJoinMaxMinority && entries < (1ull << 31);
+  P.join = h->use_join && uniform && P.s >= 2 && P.s <= kJoinMaxMinority && entries < (1ull << 31);
   if (P.join) {  // exact bucket keys need C(n, s - 2) < 2^64
     const uint64_t nb = h->binom_host[static_cast<size_t>(h->n) * kBinomK + (P.s - 2)];
     if (nb == ~uint64_t{0}) P.join = false;
     P.key_bits = nb <= 1 ? 1 : 64 - __builtin_clzll(nb - 1);
   }
+  // sector structure in use: the join (s <= 32) or the sector candidate lists (s <= 24)
+  P.sector = uniform && (P.join || P.s <= kMaxMinorityDev);
   return P;
 }
 

@@ -37,9 +37,9 @@ namespace qvmc_b200 {
 #endif
 
 
-constexpr int kJoinMaxMinority = 24;  // s <= 24: at most 276 buckets per row
+constexpr int kJoinMaxMinority = 32;  // s <= 32 (a warp's lanes hold the orbitals): <= 496 buckets per row
 constexpr int kJoinMaxRanges = kJoinMaxMinority * (kJoinMaxMinority - 1) / 2;
-constexpr int kBinomK = kJoinMaxMinority + 1;  // binomial table C[n][k], k <= 24
+constexpr int kBinomK = kJoinMaxMinority + 1;  // binomial table C[n][k], k <= 32
 constexpr int kFusedMaxMinority = 16;            // kModeFused hands at most 16 minority orbitals per row
 
 // A row's bucket tables (k_rows_join) live in dynamic shared memory, one region

@@ -341,6 +341,7 @@ def test_fused_matches_split_evaluation(cuda_ok, monkeypatch, n_qubits, n_e, n_t
     (48, 24, 200_000, 5_000, 1),    # minority set of 24: the join's largest bucket tables (276 per row)
     (48, 24, 200_000, 5_000, 0),    # the same through the sector candidate lists (k_rows, QVMC_JOIN=0)
     (40, 20, 100_000, 5_000, 1),    # half filling (c40h shape), 190 buckets per row
+    (64, 32, 200_000, 4_000, 1),    # half filling at 64 q: s = 32 (a warp's lanes), 496 buckets per row
     (130, 122, 400_000, 10_000, 1),  # 3 key words, n > 128: join without the pair-existence bitmaps
     (20, 10, 12_000, 20_000, 1),     # BASELINE config 2 shape (c20), random sector states
 ])
