@@ -4,6 +4,7 @@
 # usage: gpurun --timeout 3000 -- 'bash tools/gpu_profile_r2.sh TAG [full]'
 TAG=${1:-prof}; FULL=${2:-}
 OUT=gpurun_out/$TAG; mkdir -p $OUT
+make -s -C paper_2408_07625_b200/csrc > $OUT/make.log 2>&1 || { echo build failed; exit 1; }
 ( cd tools/micro && nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o int_rates int_rates.cu ) > $OUT/int_rates_build.log 2>&1
 ./tools/micro/int_rates > $OUT/int_rates_b200.json 2> $OUT/int_rates.err
 cat $OUT/int_rates_b200.json
