@@ -2344,7 +2344,7 @@ struct qvmc_model_s {
   // sampler (sample_without_replacement): two beams, the conditional table, candidates
   DBuf bk[2], blp[2], bpert[2], cond, c_key, c_key2, c_slot, c_slot2, c_bv, c_lp, c_pert, c_count, c_tmp;
   // gradient: chunk buffers, block sums, coefficients
-  DBuf g_h1, g_h2, g_g, g_gz2, g_gz1, g_x, g_ones, g_w1, g_w2, g_w3, g_b, g_coef, g_mean, g_part, g_flag, g_out,
+  DBuf g_h1, g_h2, g_g, g_gz2, g_gz1, g_x, g_ones, g_bsum, g_w1, g_w2, g_w3, g_b, g_coef, g_mean, g_part, g_flag, g_out,
       g_keys, g_w, g_loc;
   cublasHandle_t blas = nullptr;
   cusolverDnHandle_t solver = nullptr;
@@ -2702,18 +2702,21 @@ template <int W>
 void launch_grad_parts(qvmc_model_s* m, const qvmc_model::ModelView& V, const uint64_t* keys, int64_t n, int64_t per,
                        int64_t S, int nb, const double2* coef, int64_t n_blk) {
   using namespace qvmc_model;
-  const size_t dyn_f = (8448 + kG2Warps * 64 * kWT) * sizeof(double) + kG2Warps * kWT * W * sizeof(uint64_t);
-  const size_t dyn_b = (8192 + kG2Warps * 64 * kWT) * sizeof(double);
+  const size_t dyn_f = (8448 + kG2Warps * 64 * kWT + kG2Warps * 64) * sizeof(double) +
+                       kG2Warps * kWT * W * sizeof(uint64_t);
+  const size_t dyn_b = (8192 + kG2Warps * 64 * kWT + kG2Warps * 64) * sizeof(double);
+  m->g_bsum.ensure(static_cast<size_t>(2 * S * nb) * 64 * sizeof(double));  // Σ g, Σ gz2 per (block, CTA)
   ck(cudaFuncSetAttribute(k_grad_fwd<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn_f)),
      "smem attribute");
   ck(cudaFuncSetAttribute(k_grad_bwd<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn_b)),
      "smem attribute");
   k_grad_fwd<W><<<static_cast<unsigned>(S * nb), kG2Threads, dyn_f, m->stream>>>(
-      V, keys, n, per, coef, m->g_h1.as<double>(), m->g_h2.as<double>(), m->g_g.as<double>(), n_blk);
+      V, keys, n, per, coef, m->g_h1.as<double>(), m->g_h2.as<double>(), m->g_g.as<double>(), n_blk,
+      m->g_bsum.as<double>());
   ck_launch("grad forward");
   k_grad_bwd<W><<<static_cast<unsigned>(S * nb), kG2Threads, dyn_b, m->stream>>>(
       V, n, per, m->g_h1.as<double>(), m->g_h2.as<double>(), m->g_g.as<double>(), m->g_gz2.as<double>(),
-      m->g_gz1.as<double>(), n_blk);
+      m->g_gz1.as<double>(), n_blk, m->g_bsum.as<double>() + static_cast<size_t>(S * nb) * 64);
   ck_launch("grad backward");
 }
 
@@ -2732,8 +2735,8 @@ void grad_accumulate(qvmc_model_s* m, const uint64_t* keys, int64_t n, const dou
   const int64_t Nc = std::min<int64_t>(std::max<int64_t>(n, 1), 32768);
   const int64_t Kp_max = ((Nc + parts - 1) / parts + 7) / 8 * 8;
   const int64_t Ncp = Kp_max * parts;  // padded chunk rows
-  m->g_h1.ensure(static_cast<size_t>(nb) * Ncp * kHS * 8);
-  m->g_h2.ensure(static_cast<size_t>(nb) * Ncp * kHS * 8);
+  m->g_h1.ensure(static_cast<size_t>(nb) * Ncp * 64 * 8);
+  m->g_h2.ensure(static_cast<size_t>(nb) * Ncp * 64 * 8);
   m->g_g.ensure(static_cast<size_t>(nb) * Ncp * 64 * 8);
   m->g_gz2.ensure(static_cast<size_t>(nb) * Ncp * 64 * 8);
   m->g_gz1.ensure(static_cast<size_t>(nb) * Ncp * 64 * 8);
@@ -2753,8 +2756,8 @@ void grad_accumulate(qvmc_model_s* m, const uint64_t* keys, int64_t n, const dou
     const int64_t Kp = ((nc + parts - 1) / parts + 7) / 8 * 8;
     const int64_t Ncur = Kp * parts;  // this chunk's padded rows: rows >= nc must be zero
     if (Ncur > nc) {
-      ck(cudaMemsetAsync(m->g_h1.p, 0, static_cast<size_t>(nb) * Ncur * kHS * 8, m->stream), "memset");
-      ck(cudaMemsetAsync(m->g_h2.p, 0, static_cast<size_t>(nb) * Ncur * kHS * 8, m->stream), "memset");
+      ck(cudaMemsetAsync(m->g_h1.p, 0, static_cast<size_t>(nb) * Ncur * 64 * 8, m->stream), "memset");
+      ck(cudaMemsetAsync(m->g_h2.p, 0, static_cast<size_t>(nb) * Ncur * 64 * 8, m->stream), "memset");
       ck(cudaMemsetAsync(m->g_g.p, 0, static_cast<size_t>(nb) * Ncur * 64 * 8, m->stream), "memset");
       ck(cudaMemsetAsync(m->g_gz2.p, 0, static_cast<size_t>(nb) * Ncur * 64 * 8, m->stream), "memset");
       ck(cudaMemsetAsync(m->g_gz1.p, 0, static_cast<size_t>(nb) * Ncur * 64 * 8, m->stream), "memset");
@@ -2771,14 +2774,21 @@ void grad_accumulate(qvmc_model_s* m, const uint64_t* keys, int64_t n, const dou
     const int first = c0 == 0 ? 1 : 0;
     double* part = m->g_ones.as<double>();
     // gW2 / gW3 (+ gb2 / gb3 in row 64): batch b = jh * parts + p, A = H[b * Kp rows], B = vectors[b * Kp rows]
-    blas_ck(cublasDgemmStridedBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, kHS, 64, static_cast<int>(Kp), &one,
-                                      m->g_h1.as<double>(), kHS, Kp * kHS, m->g_gz2.as<double>(), 64, Kp * 64,
+    // W2 / W3: M = 64 (the h rows carry no bias column); the bias rows (64) come from the kernels' sums
+    const int n_cta = static_cast<int>((nc + 1023) / 1024);
+    const int bgrid = static_cast<int>(std::min<int64_t>((nb * parts * 64 + 255) / 256, 1024));
+    blas_ck(cublasDgemmStridedBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, 64, 64, static_cast<int>(Kp), &one,
+                                      m->g_h1.as<double>(), 64, Kp * 64, m->g_gz2.as<double>(), 64, Kp * 64,
                                       &zero, part, kHS, static_cast<long long>(l2), nb * parts), "dgemm w2");
+    k_bias_rows<<<bgrid, 256, 0, m->stream>>>(m->g_bsum.as<double>() + static_cast<size_t>(n_cta) * nb * 64, nb,
+                                              n_cta, parts, static_cast<int64_t>(l2), part);
     k_sum_parts<<<static_cast<int>(std::min<size_t>((nb * l2 + 255) / 256, 4096)), 256, 0, m->stream>>>(
         part, nb, parts, static_cast<int64_t>(l2), first, m->g_w2.as<double>());
-    blas_ck(cublasDgemmStridedBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, kHS, 64, static_cast<int>(Kp), &one,
-                                      m->g_h2.as<double>(), kHS, Kp * kHS, m->g_g.as<double>(), 64, Kp * 64,
+    blas_ck(cublasDgemmStridedBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, 64, 64, static_cast<int>(Kp), &one,
+                                      m->g_h2.as<double>(), 64, Kp * 64, m->g_g.as<double>(), 64, Kp * 64,
                                       &zero, part, kHS, static_cast<long long>(l2), nb * parts), "dgemm w3");
+    k_bias_rows<<<bgrid, 256, 0, m->stream>>>(m->g_bsum.as<double>(), nb, n_cta, parts, static_cast<int64_t>(l2),
+                                              part);
     k_sum_parts<<<static_cast<int>(std::min<size_t>((nb * l2 + 255) / 256, 4096)), 256, 0, m->stream>>>(
         part, nb, parts, static_cast<int64_t>(l2), first, m->g_w3.as<double>());
     // gW1 (+ gb1 in row n): pointer-array batch, X slice by part
@@ -2803,7 +2813,7 @@ void grad_accumulate(qvmc_model_s* m, const uint64_t* keys, int64_t n, const dou
         part, nb, parts, static_cast<int64_t>(l1), first, m->g_w1.as<double>());
     ck_launch("split-K sums");
     ck(cudaStreamSynchronize(m->stream), "sync");  // the host pointer arrays are reused by the next chunk
-    g_launches += 5;
+    g_launches += 7;
   }
 }
 
@@ -3084,8 +3094,8 @@ int qvmc_cuda_sr_direction(qvmc_model_t m, int64_t n, const uint64_t* keys, cons
     }
     const int nb = 2 * m->n_qudits, nq = m->n;
     const size_t vb = static_cast<size_t>(nb) * ns * 64 * 8;
-    m->g_h1.ensure(static_cast<size_t>(nb) * ns * kHS * 8);
-    m->g_h2.ensure(static_cast<size_t>(nb) * ns * kHS * 8);
+    m->g_h1.ensure(static_cast<size_t>(nb) * ns * 64 * 8);
+    m->g_h2.ensure(static_cast<size_t>(nb) * ns * 64 * 8);
     m->g_g.ensure(vb);
     m->g_gz2.ensure(vb);
     m->g_gz1.ensure(vb);

@@ -678,9 +678,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
 // gW3 = Σ g h2ᵀ; biases = Σ of the vectors). Same warp tiling as
 // k_log_psi_part (16-sample tiles, lane = 4 samples × 8 features); the
 // backward GEMMs read W3 / W2 in their original (v, h) / (h, k) layouts.
-// row stride of the h1 / h2 chunk buffers: 64 activations, a constant 1 (so the
-// weight-gradient GEMM also yields the next layer's bias gradient as its last
-// row) and a zero pad
+// row stride of the W2 / W3 gradient accumulators [block][out][kHS]: 64 inputs,
+// the bias gradient (row 64 of each output's column) and a zero pad. The h1 / h2
+// chunk rows are 64 wide: the GEMMs run at M = 64 (whole 32-row tiles) and the
+// bias rows come from the kernels' per-warp sums (k_bias_rows)
 constexpr int kHS = 66;
 
 // the forward / backward split of the gradient kernels: 16 warps per CTA each
@@ -690,18 +691,44 @@ constexpr int kHS = 66;
 constexpr int kG2Warps = QVMC_G2_WARPS;
 constexpr int kG2Threads = kG2Warps * 32;
 
+// bias sums: a warp adds its tile's 4 samples x 8 features per lane, summed over the
+// 4 sample groups, into its own shared row (lanes 0-7 hold distinct features)
+// (samples past the chunk end are masked: their softmax can be 0/0)
+__device__ __forceinline__ void add_tile_sums(const double (&v)[4][8], unsigned valid, double* row, int lane) {
+  const int hq = lane & 7;
+#pragma unroll
+  for (int f = 0; f < 8; ++f) {
+    double t = ((valid & 1u) ? v[0][f] : 0.0) + ((valid & 2u) ? v[1][f] : 0.0);
+    t += ((valid & 4u) ? v[2][f] : 0.0) + ((valid & 8u) ? v[3][f] : 0.0);
+    t += __shfl_xor_sync(0xffffffffu, t, 8);
+    t += __shfl_xor_sync(0xffffffffu, t, 16);
+    if (lane < 8) row[16 * (f >> 1) + 2 * hq + (f & 1)] += t;
+  }
+}
+
+// the CTA's sums, warps in order, to out[jh][cta][64] (summed over CTAs by k_bias_rows)
+__device__ __forceinline__ void write_cta_sums(const double* bsum, double* out, int jh, int cta, int n_cta) {
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    double t = 0.0;
+    for (int w = 0; w < kG2Warps; ++w) t += bsum[w * 64 + threadIdx.x];
+    out[(static_cast<int64_t>(jh) * n_cta + cta) * 64 + threadIdx.x] = t;
+  }
+}
+
 template <int W>
 __global__ void __launch_bounds__(kG2Threads, 1)
     k_grad_fwd(const ModelView M, const uint64_t* __restrict__ keys, int64_t N, int64_t chunk,
                 const double2* __restrict__ coef, double* __restrict__ H1, double* __restrict__ H2,
-                double* __restrict__ G, int64_t N_blk) {
+                double* __restrict__ G, int64_t N_blk, double* __restrict__ GSUM) {
   // N: samples of this call; N_blk: rows per block in the buffers (>= N, padded for split-K)
   extern __shared__ __align__(16) double smem[];
   double* w2 = smem;            // [64 k][64 h]  (W2 transposed)
   double* w3 = smem + 4096;     // [64 k][64 v]  (W3 transposed)
   double* bias = smem + 8192;   // b1 | csum | b2 | b3
   double* acts = smem + 8448;   // [warps][64][16]
-  uint64_t* skeys = reinterpret_cast<uint64_t*>(acts + kG2Warps * 64 * kWT);
+  double* bsum = acts + kG2Warps * 64 * kWT;  // [warps][64]: Σ g of the warp's tiles (gb3)
+  uint64_t* skeys = reinterpret_cast<uint64_t*>(bsum + kG2Warps * 64);
 
   const int n_jh = 2 * M.n_qudits;
   const int jh = static_cast<int>(blockIdx.x % n_jh), j = jh >> 1, hd = jh & 1;
@@ -713,6 +740,7 @@ __global__ void __launch_bounds__(kG2Threads, 1)
     w2[e] = __ldg(B + L.w2t() + e);
     w3[e] = __ldg(B + L.w3t() + e);
   }
+  for (int e = threadIdx.x; e < kG2Warps * 64; e += kG2Threads) bsum[e] = 0.0;
   if (threadIdx.x < 64) {
     bias[threadIdx.x] = __ldg(B + L.b1() + threadIdx.x);
     bias[64 + threadIdx.x] = __ldg(B + L.csum() + threadIdx.x);
@@ -734,8 +762,8 @@ __global__ void __launch_bounds__(kG2Threads, 1)
   uint32_t up_value_mask = 0;
   for (int t = 0; t < k; ++t)
     if ((off + t) % 2 == 0) up_value_mask |= 1u << (k - 1 - t);
-  const int64_t blk = static_cast<int64_t>(jh) * N_blk * 64, blkh = static_cast<int64_t>(jh) * N_blk * kHS;
-  double *h1o = H1 + blkh, *h2o = H2 + blkh, *go = G + blk;
+  const int64_t blk = static_cast<int64_t>(jh) * N_blk * 64;
+  double *h1o = H1 + blk, *h2o = H2 + blk, *go = G + blk;
   auto feat = [&](int f) { return 16 * (f >> 1) + 2 * hq + (f & 1); };
 
   for (int64_t t0 = c0 + static_cast<int64_t>(warp) * kWT; t0 < c1; t0 += static_cast<int64_t>(kWT) * kG2Warps) {
@@ -774,13 +802,6 @@ __global__ void __launch_bounds__(kG2Threads, 1)
     auto put = [&](double* o, int si, int f, double v0, double v1, int ld = 64) {  // features f, f+1 of sample si
       if (row(si) < c1) *reinterpret_cast<double2*>(o + row(si) * ld + feat(f)) = make_double2(v0, v1);
     };
-    if (hq == 0)  // bias columns of this lane's 4 samples
-#pragma unroll
-      for (int si = 0; si < 4; ++si)
-        if (row(si) < c1) {
-          *reinterpret_cast<double2*>(h1o + row(si) * kHS + 64) = make_double2(1.0, 0.0);
-          *reinterpret_cast<double2*>(h2o + row(si) * kHS + 64) = make_double2(1.0, 0.0);
-        }
 
     // layer 1 -> h1 (model.cpp:171), as in k_log_psi_part
 #pragma unroll
@@ -817,7 +838,7 @@ __global__ void __launch_bounds__(kG2Threads, 1)
           a[u][f] = tanh_fast((ones ? 2.0 * a[u][f] - cs : cs - 2.0 * a[u][f]) + bias[feat(f)]);
         }
 #pragma unroll
-        for (int f = 0; f < 8; f += 2) put(h1o, si, f, a[u][f], a[u][f + 1], kHS);
+        for (int f = 0; f < 8; f += 2) put(h1o, si, f, a[u][f], a[u][f + 1]);
       }
 #pragma unroll
       for (int f = 0; f < 8; ++f)
@@ -877,7 +898,7 @@ __global__ void __launch_bounds__(kG2Threads, 1)
 #pragma unroll
     for (int si = 0; si < 4; ++si)
 #pragma unroll
-      for (int f = 0; f < 8; f += 2) put(h2o, si, f, h2[si][f], h2[si][f + 1], kHS);
+      for (int f = 0; f < 8; f += 2) put(h2o, si, f, h2[si][f], h2[si][f + 1]);
 
     // output gradient g (d/d raw output), scaled by the sample's coefficient
     double g[4][8];
@@ -951,8 +972,10 @@ __global__ void __launch_bounds__(kG2Threads, 1)
     for (int si = 0; si < 4; ++si)
 #pragma unroll
       for (int f = 0; f < 8; f += 2) put(go, si, f, g[si][f], g[si][f + 1]);
-
+    add_tile_sums(g, (row(0) < c1) | (row(1) < c1) << 1 | (row(2) < c1) << 2 | (row(3) < c1) << 3, bsum + warp * 64,
+                  lane);
   }
+  write_cta_sums(bsum, GSUM, jh, static_cast<int>(blockIdx.x / n_jh), static_cast<int>(gridDim.x / n_jh));
 }
 
 // Backward half (mlp_backward, model.cpp:177-201) of the gradient vectors:
@@ -963,11 +986,12 @@ template <int W>
 __global__ void __launch_bounds__(kG2Threads, 1)
     k_grad_bwd(const ModelView M, int64_t N, int64_t chunk, const double* __restrict__ H1,
                const double* __restrict__ H2, const double* __restrict__ G, double* __restrict__ GZ2,
-               double* __restrict__ GZ1, int64_t N_blk) {
+               double* __restrict__ GZ1, int64_t N_blk, double* __restrict__ GZ2SUM) {
   extern __shared__ __align__(16) double smem[];
   double* w2o = smem;           // [64 h][64 k]  (W2)
   double* w3o = smem + 4096;    // [64 v][64 h]  (W3)
   double* acts = smem + 8192;   // [warps][64][16]
+  double* bsum = acts + kG2Warps * 64 * kWT;  // [warps][64]: Σ gz2 of the warp's tiles (gb2)
   const int n_jh = 2 * M.n_qudits;
   const int jh = static_cast<int>(blockIdx.x % n_jh);
   const int64_t c0 = static_cast<int64_t>(blockIdx.x / n_jh) * chunk;
@@ -979,12 +1003,13 @@ __global__ void __launch_bounds__(kG2Threads, 1)
     w2o[c * 64 + r] = __ldg(B + L.w2t() + e);
     w3o[c * 64 + r] = __ldg(B + L.w3t() + e);
   }
+  for (int e = threadIdx.x; e < kG2Warps * 64; e += kG2Threads) bsum[e] = 0.0;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sq = lane >> 3, hq = lane & 7;
   double* act = acts + warp * 64 * kWT;
-  const int64_t blk = static_cast<int64_t>(jh) * N_blk * 64, blkh = static_cast<int64_t>(jh) * N_blk * kHS;
-  const double *h1i = H1 + blkh, *h2i = H2 + blkh, *gi = G + blk;
+  const int64_t blk = static_cast<int64_t>(jh) * N_blk * 64;
+  const double *h1i = H1 + blk, *h2i = H2 + blk, *gi = G + blk;
   double *gz2o = GZ2 + blk, *gz1o = GZ1 + blk;
   auto feat = [&](int f) { return 16 * (f >> 1) + 2 * hq + (f & 1); };
   for (int64_t t0 = c0 + static_cast<int64_t>(warp) * kWT; t0 < c1; t0 += static_cast<int64_t>(kWT) * kG2Warps) {
@@ -1036,7 +1061,7 @@ __global__ void __launch_bounds__(kG2Threads, 1)
     load(gi, 64);  // g -> act
     to_act();
     gemm(w3o);     // W3ᵀ g
-    load(h2i, kHS);
+    load(h2i, 64);
 #pragma unroll
     for (int si = 0; si < 4; ++si)
 #pragma unroll
@@ -1047,13 +1072,15 @@ __global__ void __launch_bounds__(kG2Threads, 1)
 #pragma unroll
         for (int f = 0; f < 8; f += 2)
           *reinterpret_cast<double2*>(gz2o + row(si) * 64 + feat(f)) = make_double2(v[si][f], v[si][f + 1]);
+    add_tile_sums(v, (row(0) < c1) | (row(1) < c1) << 1 | (row(2) < c1) << 2 | (row(3) < c1) << 3, bsum + warp * 64,
+                  lane);
     to_act();
     gemm(w2o);     // W2ᵀ gz2; v still holds gz2 (the residual)
 #pragma unroll
     for (int si = 0; si < 4; ++si)
 #pragma unroll
       for (int f = 0; f < 8; ++f) acc[si][f] += v[si][f];
-    load(h1i, kHS);
+    load(h1i, 64);
 #pragma unroll
     for (int si = 0; si < 4; ++si)
       if (row(si) < c1)
@@ -1061,6 +1088,24 @@ __global__ void __launch_bounds__(kG2Threads, 1)
         for (int f = 0; f < 8; f += 2)
           *reinterpret_cast<double2*>(gz1o + row(si) * 64 + feat(f)) =
               make_double2(acc[si][f] * (1.0 - v[si][f] * v[si][f]), acc[si][f + 1] * (1.0 - v[si][f + 1] * v[si][f + 1]));
+  }
+  write_cta_sums(bsum, GZ2SUM, jh, static_cast<int>(blockIdx.x / n_jh), static_cast<int>(gridDim.x / n_jh));
+}
+
+// bias rows of the W2 / W3 split-K partials (row 64 of every output column, ld kHS):
+// part 0 gets the CTA sums of this chunk in CTA order, the other parts 0 (the
+// GEMMs write rows 0-63 only); row 65 is the zero pad
+__global__ void k_bias_rows(const double* __restrict__ sums, int nb, int n_cta, int parts, int64_t len,
+                            double* __restrict__ part) {
+  const int total = nb * parts * 64;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int o = e & 63, bq = e >> 6, jh = bq / parts, q = bq - jh * parts;
+    double t = 0.0;
+    if (q == 0)
+      for (int c = 0; c < n_cta; ++c) t += sums[(static_cast<int64_t>(jh) * n_cta + c) * 64 + o];
+    double* col = part + static_cast<int64_t>(bq) * len + static_cast<int64_t>(o) * kHS;
+    col[64] = t;
+    col[65] = 0.0;
   }
 }
 
@@ -1181,8 +1226,8 @@ __global__ void k_jac_real(const ModelView M, const int64_t* __restrict__ boff, 
   const int64_t i = blockIdx.x;
   const int jh = blockIdx.y, j = jh >> 1;
   const int n = M.n, off = j * M.bits, k = min(M.bits, n - off), n_out = 1 << k;
-  const int64_t v0 = (static_cast<int64_t>(jh) * N + i) * 64, vh = (static_cast<int64_t>(jh) * N + i) * kHS;
-  const double *h1 = H1 + vh, *h2 = H2 + vh, *g = G + v0, *gz2 = GZ2 + v0, *gz1 = GZ1 + v0, *x = X + i * (n + 2);
+  const int64_t v0 = (static_cast<int64_t>(jh) * N + i) * 64;
+  const double *h1 = H1 + v0, *h2 = H2 + v0, *g = G + v0, *gz2 = GZ2 + v0, *gz1 = GZ1 + v0, *x = X + i * (n + 2);
   double* o = R + i * ld + boff[jh];
   for (int e = threadIdx.x; e < kHid * n; e += blockDim.x) {  // W1[h][c] = gz1[h] e[c], e = ±1 before the offset
     const int h = e / n, c = e - h * n;
