@@ -750,6 +750,7 @@ RowPlan plan_from_mm(qvmc_ham_s* h, int64_t n, const int* mm) {
     const uint64_t nb = h->binom_host[static_cast<size_t>(h->n) * kBinomK + (P.s - 2)];
     if (nb == ~uint64_t{0}) P.join = false;
     P.key_bits = nb <= 1 ? 1 : 64 - __builtin_clzll(nb - 1);
+    if (P.key_bits > 62) P.join = false;  // the distributed build pads with key 1 << key_bits
   }
   // sector structure in use: the join (s <= 32) or the sector candidate lists (s <= 24)
   P.sector = uniform && (P.join || P.s <= kMaxMinorityDev);
