@@ -2748,10 +2748,31 @@ void grad_accumulate(qvmc_model_s* m, const uint64_t* keys, int64_t n, const dou
   m->g_w2.ensure(static_cast<size_t>(nb) * l2 * 8);
   m->g_w3.ensure(static_cast<size_t>(nb) * l2 * 8);
   const double one = 1.0, zero = 0.0;
-  // pointer arrays of the W1 GEMMs (X is shared by the blocks, so its slice depends on the part only)
-  std::vector<const double*> pa(static_cast<size_t>(nb) * parts), pb(pa.size());
-  std::vector<double*> pc(pa.size());
-  m->s_tmp.ensure(pa.size() * 3 * sizeof(void*) + 16);
+  // pointer arrays of the W1 GEMMs (X is shared by the blocks, so its slice depends on the part only);
+  // they depend on the chunk geometry alone: one set for full chunks, one for the last, uploaded once
+  // (no host round trip between chunks)
+  const size_t np = static_cast<size_t>(nb) * parts;
+  m->s_tmp.ensure(np * 6 * sizeof(void*) + 16);
+  {
+    std::vector<void*> ptrs(np * 6);
+    const int64_t last = n - (n > 0 ? (n - 1) / Nc * Nc : 0);
+    for (int set = 0; set < 2; ++set) {
+      const int64_t nc = set == 0 ? Nc : last;
+      const int64_t Kp = ((nc + parts - 1) / parts + 7) / 8 * 8;
+      const int64_t Ncur = Kp * parts;
+      void** pp = ptrs.data() + set * np * 3;
+      for (int jh = 0; jh < nb; ++jh)
+        for (int q = 0; q < parts; ++q) {
+          const size_t b2 = static_cast<size_t>(jh) * parts + q;
+          pp[b2] = m->g_x.as<double>() + q * Kp * nx;
+          pp[np + b2] = m->g_gz1.as<double>() + (static_cast<int64_t>(jh) * Ncur + q * Kp) * 64;
+          pp[2 * np + b2] = m->g_ones.as<double>() + b2 * l1;
+        }
+    }
+    ck(cudaMemcpyAsync(m->s_tmp.p, ptrs.data(), ptrs.size() * sizeof(void*), cudaMemcpyHostToDevice, m->stream),
+       "H2D ptrs");
+    ck(cudaStreamSynchronize(m->stream), "sync");  // the host vector goes out of scope
+  }
   for (int64_t c0 = 0; c0 < n; c0 += Nc) {
     const int64_t nc = std::min<int64_t>(Nc, n - c0);
     const int64_t Kp = ((nc + parts - 1) / parts + 7) / 8 * 8;
@@ -2793,27 +2814,14 @@ void grad_accumulate(qvmc_model_s* m, const uint64_t* keys, int64_t n, const dou
     k_sum_parts<<<static_cast<int>(std::min<size_t>((nb * l2 + 255) / 256, 4096)), 256, 0, m->stream>>>(
         part, nb, parts, static_cast<int64_t>(l2), first, m->g_w3.as<double>());
     // gW1 (+ gb1 in row n): pointer-array batch, X slice by part
-    for (int jh = 0; jh < nb; ++jh)
-      for (int q = 0; q < parts; ++q) {
-        const size_t b2 = static_cast<size_t>(jh) * parts + q;
-        pa[b2] = m->g_x.as<double>() + q * Kp * nx;
-        pb[b2] = m->g_gz1.as<double>() + (static_cast<int64_t>(jh) * Ncur + q * Kp) * 64;
-        pc[b2] = part + b2 * l1;
-      }
-    void** dp = static_cast<void**>(m->s_tmp.p);
-    ck(cudaMemcpyAsync(dp, pa.data(), pa.size() * sizeof(void*), cudaMemcpyHostToDevice, m->stream), "H2D ptrs");
-    ck(cudaMemcpyAsync(dp + pa.size(), pb.data(), pb.size() * sizeof(void*), cudaMemcpyHostToDevice, m->stream),
-       "H2D ptrs");
-    ck(cudaMemcpyAsync(dp + 2 * pa.size(), pc.data(), pc.size() * sizeof(void*), cudaMemcpyHostToDevice, m->stream),
-       "H2D ptrs");
+    void** dp = static_cast<void**>(m->s_tmp.p) + (nc == Nc ? 0 : np * 3);
     blas_ck(cublasDgemmBatched(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, nx, 64, static_cast<int>(Kp), &one,
                                reinterpret_cast<const double* const*>(dp), nx,
-                               reinterpret_cast<const double* const*>(dp + pa.size()), 64, &zero,
-                               reinterpret_cast<double* const*>(dp + 2 * pa.size()), nx, nb * parts), "dgemm w1");
+                               reinterpret_cast<const double* const*>(dp + np), 64, &zero,
+                               reinterpret_cast<double* const*>(dp + 2 * np), nx, nb * parts), "dgemm w1");
     k_sum_parts<<<static_cast<int>(std::min<size_t>((nb * l1 + 255) / 256, 4096)), 256, 0, m->stream>>>(
         part, nb, parts, static_cast<int64_t>(l1), first, m->g_w1.as<double>());
     ck_launch("split-K sums");
-    ck(cudaStreamSynchronize(m->stream), "sync");  // the host pointer arrays are reused by the next chunk
     g_launches += 7;
   }
 }

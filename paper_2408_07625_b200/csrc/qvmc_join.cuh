@@ -340,6 +340,9 @@ __global__ void k_join_fill(const uint32_t* __restrict__ val, const uint32_t* __
     mem[p] = static_cast<uint64_t>(y) | static_cast<uint64_t>(pa) << 32 | static_cast<uint64_t>(pb) << 40 |
              static_cast<uint64_t>(pb * (pb - 1) / 2 + pa) << 48;
   }
+  // the slice's padding travels in the members all-gather: defined bytes (never walked)
+  for (uint64_t p = En + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < E; p += (uint64_t)gridDim.x * blockDim.x)
+    mem[p] = 0;
 }
 
 // distributed index build: the rank that owns an exact bucket (a hash of its key)

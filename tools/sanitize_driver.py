@@ -2,8 +2,10 @@
 (memcheck / racecheck / synccheck / initcheck): toy KAT, a reference golden
 family, the join path at 118 and 56 qubits (pipelined search + chunk
 evaluation, including the overflow regrow with a tiny first hit capacity),
-pair materialisation + local_energies + fused pair elements, the generic
-sector-list row kernel, and the amplitude model. Sizes are small so the
+pair materialisation + local_energies + fused pair elements, the join at
+minority sets of 24 and 32 and the sector-list row kernel, the amplitude
+model, sampler, gradient, SR and Adam, and the sharded call at world 1 (NCCL)
+and world 2 (two threads, host all-gather: strided walk, distributed index). Sizes are small so the
 instrumented run finishes in minutes.
 
     compute-sanitizer --tool racecheck python tools/sanitize_driver.py
@@ -46,6 +48,56 @@ def join_case(n_qubits, n_e, n_terms, n_unq, hit_cap=None):
     print(f"join {n_qubits}q n={n_unq} pairs={len(p.entries)} e_var={rep.e_var:.6f}", flush=True)
 
 
+def sharded_threads(world=2, n_unq=3000):
+    """world ranks as threads of this process, each with its own device handle on cuda:0 and a
+    host all-gather over a thread barrier: the strided walk, the distributed deletion index and
+    the exact all-reduces of qvmc_cuda_eloc_sharded under the sanitizer in one process."""
+    import ctypes as C
+    import threading
+    c, x, y, z = synthetic.jw_terms(56, 100_000, seed=1)
+    keys = synthetic.near_hf_keys(56, 14, n_unq, seed=4)
+    bb = synthetic.sample_batch(keys, seed=3)
+    ref = q.surrogate_energy(q.HamiltonianIndex.from_masks(56, c, x, y, z), bb)
+    barrier, bufs, outs = threading.Barrier(world), [None] * world, [None] * world
+    L = _lib.lib()
+
+    def make_fn(rank):
+        def fn(ctx, send, recv, nbytes):
+            bufs[rank] = C.string_at(send, nbytes)
+            barrier.wait()
+            C.memmove(recv, b"".join(bufs), nbytes * world)
+            barrier.wait()
+            return 0
+        return _lib.HOST_ALLGATHER_FN(fn)
+
+    fns = [make_fn(r) for r in range(world)]
+    Hs = [q.HamiltonianIndex.from_masks(56, c, x, y, z) for _ in range(world)]
+
+    def run(rank):
+        comm = C.c_void_p()
+        _lib.check(L.qvmc_cuda_comm_init_host(world, rank, fns[rank], None, C.byref(comm)))
+        r0, r1 = C.c_int64(), C.c_int64()
+        _lib.check(L.qvmc_shard_bounds(n_unq, world, rank, C.byref(r0), C.byref(r1)))
+        r0, r1 = r0.value, r1.value
+        out = np.zeros(r1 - r0, dtype=np.complex128)
+        mom = np.zeros(5)
+        sl = lambda a: np.ascontiguousarray(a[r0:r1])
+        _lib.check(L.qvmc_cuda_eloc_sharded(Hs[rank].device_handle(0), comm, n_unq, _ptr(sl(bb.vectors)),
+                                            _ptr(sl(bb.log_amps)), _ptr(sl(bb.phases)), _ptr(sl(bb.log_probs)),
+                                            bb.log_norm, _ptr(out), _ptr(mom), _lib.MEM_HOST))
+        _lib.check(L.qvmc_cuda_comm_destroy(comm))
+        outs[rank] = (r0, r1, out)
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for r0, r1, out in outs:
+        assert np.array_equal(out, ref.locals[r0:r1])
+    print(f"sharded world {world} (threads, host all-gather): rows bit-identical", flush=True)
+
+
 def main():
     import __graft_entry__
     __graft_entry__.smoke()
@@ -61,10 +113,17 @@ def main():
     join_case(118, 110, 300_000, 3000)
     join_case(118, 110, 300_000, 3000, hit_cap=512)
     join_case(56, 14, 100_000, 3000)
-    # generic sector-list rows (minority set > 16)
-    H = synthetic.jw_hamiltonian(48, 20_000, seed=1)
+    # minority set of 24: the join with 276 buckets per row, and the sector-list row kernel (QVMC_JOIN=0)
     keys = synthetic.near_hf_keys(48, 24, 1000, seed=2)
+    H = synthetic.jw_hamiltonian(48, 20_000, seed=1)
     q.surrogate_energy(H, synthetic.sample_batch(keys, seed=3))
+    os.environ["QVMC_JOIN"] = "0"
+    H = synthetic.jw_hamiltonian(48, 20_000, seed=1)
+    q.surrogate_energy(H, synthetic.sample_batch(keys, seed=3))
+    os.environ.pop("QVMC_JOIN")
+    # half filling at 64 qubits: s = 32, the join's largest tables (496 buckets per row)
+    H = synthetic.jw_hamiltonian(64, 30_000, seed=1)
+    q.surrogate_energy(H, synthetic.sample_batch(synthetic.near_hf_keys(64, 32, 800, seed=2), seed=3))
     # amplitude model
     M = q.AnqsModel(q.QuditLayout.make(56, 6), q.SectorConstraint(14, True))
     M.set_params(np.random.default_rng(0).uniform(-0.1, 0.1, M.n_params()))
@@ -95,6 +154,7 @@ def main():
                                         _ptr(bb.phases), _ptr(bb.log_probs), bb.log_norm, _ptr(out), _ptr(mom),
                                         _lib.MEM_HOST))
     _lib.check(L.qvmc_cuda_comm_destroy(comm))
+    sharded_threads(2)
     print("sanitize driver done", flush=True)
 
 
