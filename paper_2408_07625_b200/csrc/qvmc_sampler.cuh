@@ -79,14 +79,21 @@ struct Candidates {
   unsigned long long* count;
 };
 
-// one warp per beam entry (sampler.cpp:53-74)
+// one warp per beam entry (sampler.cpp:53-74); the 8 warps of a block take 8
+// consecutive entries per step and reserve their children's output slots with
+// one atomic per block step (a block-level scan of the warps' counts), not one
+// per warp: a single global counter hit by every warp serialised the kernel
 __global__ void __launch_bounds__(256)
     k_expand(const double* __restrict__ cond, const double* __restrict__ beam_lp, const double* __restrict__ beam_pert,
              int64_t B, int n_out, uint64_t seed, uint32_t stream, uint32_t iteration, uint32_t level, Candidates C) {
-  const int lane = threadIdx.x & 31;
-  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t b = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; b < B; b += n_warps) {
-    const double plp = beam_lp[b], ppert = beam_pert[b];
+  __shared__ unsigned s_cnt[2][8];
+  __shared__ unsigned long long s_base[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int ph = 0;
+  for (int64_t b0 = static_cast<int64_t>(blockIdx.x) * 8; b0 < B; b0 += static_cast<int64_t>(gridDim.x) * 8) {
+    const int64_t b = b0 + warp;
+    const bool live = b < B;
+    const double plp = live ? beam_lp[b] : 0.0, ppert = live ? beam_pert[b] : 0.0;
     double clp[2], u[2];
     bool ok[2];
     double z = -CUDART_INF;
@@ -96,7 +103,7 @@ __global__ void __launch_bounds__(256)
       ok[h] = false;
       clp[h] = 0.0;
       u[h] = -CUDART_INF;
-      if (v < n_out) {
+      if (live && v < n_out) {
         const double c = cond[b * 64 + v];
         if (c != -CUDART_INF) {
           ok[h] = true;
@@ -109,14 +116,23 @@ __global__ void __launch_bounds__(256)
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) z = fmax(z, __shfl_xor_sync(0xffffffffu, z, o));
+    const unsigned m0 = __ballot_sync(0xffffffffu, ok[0]), m1 = __ballot_sync(0xffffffffu, ok[1]);
+    if (lane == 0) s_cnt[ph][warp] = __popc(m0) + __popc(m1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned tot = 0;
+      for (int w = 0; w < 8; ++w) tot += s_cnt[ph][w];
+      s_base[ph] = tot ? atomicAdd(C.count, static_cast<unsigned long long>(tot)) : 0ull;
+    }
+    __syncthreads();
+    unsigned long long base = s_base[ph];
+    for (int w = 0; w < warp; ++w) base += s_cnt[ph][w];
+    ph ^= 1;  // the next step writes the other buffers: one barrier per step suffices
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const unsigned m = __ballot_sync(0xffffffffu, ok[h]);
-      unsigned long long base = 0;
-      if (lane == 0 && m) base = atomicAdd(C.count, static_cast<unsigned long long>(__popc(m)));
-      base = __shfl_sync(0xffffffffu, base, 0);
+      const unsigned m = h ? m1 : m0;
       if (ok[h]) {
-        const uint64_t s = base + __popc(m & ((1u << lane) - 1u));
+        const uint64_t s = base + (h ? __popc(m0) : 0u) + __popc(m & ((1u << lane) - 1u));
         const double cp = condition_max(ppert, z, u[h]);
         C.key[s] = desc_key(cp);
         C.slot[s] = static_cast<uint32_t>(s);
