@@ -94,30 +94,37 @@ __global__ void __launch_bounds__(256)
     const int64_t b = b0 + warp;
     const bool live = b < B;
     const double plp = live ? beam_lp[b] : 0.0, ppert = live ? beam_pert[b] : 0.0;
+    // the entry's allowed values (cond > -inf), compacted onto lanes in value order: the k-th
+    // allowed value goes to lane k % 32 of pass k / 32 (one pass unless more than 32 are allowed)
+    const double c0 = (live && lane < n_out) ? cond[b * 64 + lane] : -CUDART_INF;
+    const double c1 = (live && lane + 32 < n_out) ? cond[b * 64 + 32 + lane] : -CUDART_INF;
+    const unsigned m0 = __ballot_sync(0xffffffffu, c0 != -CUDART_INF);
+    const unsigned m1 = __ballot_sync(0xffffffffu, c1 != -CUDART_INF);
+    const int n0 = __popc(m0), n = n0 + __popc(m1);
     double clp[2], u[2];
-    bool ok[2];
+    int vv[2];
     double z = -CUDART_INF;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int v = lane + 32 * h;
-      ok[h] = false;
-      clp[h] = 0.0;
       u[h] = -CUDART_INF;
-      if (live && v < n_out) {
-        const double c = cond[b * 64 + v];
-        if (c != -CUDART_INF) {
-          ok[h] = true;
-          clp[h] = plp + c;
-          u[h] = clp[h] + counter_gumbel(seed, stream, iteration, level, static_cast<uint32_t>(b),
-                                         static_cast<uint32_t>(v));
-          z = fmax(z, u[h]);
-        }
+      clp[h] = 0.0;
+      vv[h] = 0;
+      if (32 * h >= n) continue;  // warp-uniform
+      const int k = 32 * h + lane;
+      int v = 0;
+      if (k < n) v = k < n0 ? static_cast<int>(__fns(m0, 0, k + 1)) : 32 + static_cast<int>(__fns(m1, 0, k - n0 + 1));
+      const double s0 = __shfl_sync(0xffffffffu, c0, v & 31), s1 = __shfl_sync(0xffffffffu, c1, v & 31);
+      if (k < n) {
+        vv[h] = v;
+        clp[h] = plp + (v < 32 ? s0 : s1);
+        u[h] = clp[h] + counter_gumbel(seed, stream, iteration, level, static_cast<uint32_t>(b),
+                                       static_cast<uint32_t>(v));
+        z = fmax(z, u[h]);
       }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) z = fmax(z, __shfl_xor_sync(0xffffffffu, z, o));
-    const unsigned m0 = __ballot_sync(0xffffffffu, ok[0]), m1 = __ballot_sync(0xffffffffu, ok[1]);
-    if (lane == 0) s_cnt[ph][warp] = __popc(m0) + __popc(m1);
+    if (lane == 0) s_cnt[ph][warp] = static_cast<unsigned>(n);
     __syncthreads();
     if (threadIdx.x == 0) {
       unsigned tot = 0;
@@ -130,13 +137,13 @@ __global__ void __launch_bounds__(256)
     ph ^= 1;  // the next step writes the other buffers: one barrier per step suffices
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const unsigned m = h ? m1 : m0;
-      if (ok[h]) {
-        const uint64_t s = base + (h ? __popc(m0) : 0u) + __popc(m & ((1u << lane) - 1u));
+      const int k = 32 * h + lane;
+      if (k < n) {
+        const uint64_t s = base + static_cast<uint64_t>(k);
         const double cp = condition_max(ppert, z, u[h]);
         C.key[s] = desc_key(cp);
         C.slot[s] = static_cast<uint32_t>(s);
-        C.bv[s] = static_cast<uint32_t>(b) << 6 | static_cast<uint32_t>(lane + 32 * h);
+        C.bv[s] = static_cast<uint32_t>(b) << 6 | static_cast<uint32_t>(vv[h]);
         C.lp[s] = clp[h];
         C.pert[s] = cp;
       }
