@@ -533,7 +533,10 @@ __device__ __forceinline__ void kind_b_element(const double* __restrict__ famvi,
 // Per-warp state of the join kernel.
 constexpr int kJQueue = 128;
 constexpr int kJDrainAt = kJQueue - 32;  // checked after every lookup batch (<= 32 hits)
-constexpr int kJSurv = 256;  // ring of candidates that passed the accept rule and the bitmap: >= 31 + 32 U
+#ifndef QVMC_JSURV
+#define QVMC_JSURV 256
+#endif
+constexpr int kJSurv = QVMC_JSURV;  // ring of candidates that passed the accept rule and the bitmap: >= 31 + 32 U
 static_assert(kJSurv >= 31 + 32 * QVMC_JOIN_UNROLL, "survivor ring too small for the unroll");
 
 struct JoinSmem {
