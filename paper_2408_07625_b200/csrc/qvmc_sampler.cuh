@@ -90,14 +90,24 @@ __global__ void __launch_bounds__(256)
   __shared__ unsigned long long s_base[2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int ph = 0;
-  for (int64_t b0 = static_cast<int64_t>(blockIdx.x) * 8; b0 < B; b0 += static_cast<int64_t>(gridDim.x) * 8) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * 8;
+  // the entry's conditional row and parent values, loaded one step ahead (the kernel waits on them)
+  auto fetch = [&](int64_t e, double& a0, double& a1, double& lp, double& pt) {
+    const bool lv = e < B;
+    a0 = (lv && lane < n_out) ? cond[e * 64 + lane] : -CUDART_INF;
+    a1 = (lv && lane + 32 < n_out) ? cond[e * 64 + 32 + lane] : -CUDART_INF;
+    lp = lv ? beam_lp[e] : 0.0;
+    pt = lv ? beam_pert[e] : 0.0;
+  };
+  double n0c, n1c, nlp, npt;
+  fetch(static_cast<int64_t>(blockIdx.x) * 8 + warp, n0c, n1c, nlp, npt);
+  for (int64_t b0 = static_cast<int64_t>(blockIdx.x) * 8; b0 < B; b0 += stride) {
     const int64_t b = b0 + warp;
     const bool live = b < B;
-    const double plp = live ? beam_lp[b] : 0.0, ppert = live ? beam_pert[b] : 0.0;
+    const double c0 = n0c, c1 = n1c, plp = nlp, ppert = npt;
+    fetch(b + stride, n0c, n1c, nlp, npt);
     // the entry's allowed values (cond > -inf), compacted onto lanes in value order: the k-th
     // allowed value goes to lane k % 32 of pass k / 32 (one pass unless more than 32 are allowed)
-    const double c0 = (live && lane < n_out) ? cond[b * 64 + lane] : -CUDART_INF;
-    const double c1 = (live && lane + 32 < n_out) ? cond[b * 64 + 32 + lane] : -CUDART_INF;
     const unsigned m0 = __ballot_sync(0xffffffffu, c0 != -CUDART_INF);
     const unsigned m1 = __ballot_sync(0xffffffffu, c1 != -CUDART_INF);
     const int n0 = __popc(m0), n = n0 + __popc(m1);
