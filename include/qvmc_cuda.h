@@ -306,8 +306,9 @@ int qvmc_cuda_sr_solve(qvmc_model_t m, int64_t rows, int64_t cols, const double*
  * of highest log p (top_probability_indices, sr.cpp:15-23, ties in sample
  * order), their grad_log_psi rows (model.cpp:273-325), build_sr_context
  * (sr.cpp:25-72; lambda <= 0 picks 1e-4 (1 + ||stacked||_F^2 / n_sr)) and
- * sr_direction applied to grad [n_params]. locals [n][2]. out_lambda may be
- * NULL. Synchronises. */
+ * sr_direction applied to grad [n_params]. locals [n][2] is accepted for the
+ * optimiser's call shape but not read (the SR context needs the samples and
+ * their weights only). out_lambda may be NULL. Synchronises. */
 int qvmc_cuda_sr_direction(qvmc_model_t m, int64_t n, const uint64_t* keys, const double* log_probs,
                            const double* locals, int n_sr, double lambda, const double* grad, int mem,
                            double* out_direction, double* out_lambda);

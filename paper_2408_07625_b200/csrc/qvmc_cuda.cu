@@ -2853,12 +2853,6 @@ __global__ void k_gather_rows_u64(const uint64_t* __restrict__ src, const uint32
     dst[e] = src[static_cast<int64_t>(idx[e / W]) * W + e % W];
 }
 
-__global__ void k_fill_f64(double* p, int64_t n, double v) {
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    p[i] = v;
-}
-
 // sr_direction (sr.cpp:74-95) on device buffers: S row-major [rows][cols] (= col-major cols x rows),
 // grad [cols] -> out [cols]; lambda > 0. The Gram eigensystem is cuSOLVER syevd.
 void sr_solve_device(qvmc_model_s* m, int64_t rows, int64_t cols, const double* S, double lambda, const double* grad,
@@ -3042,19 +3036,16 @@ int qvmc_cuda_sr_direction(qvmc_model_t m, int64_t n, const uint64_t* keys, cons
     const int64_t P = m->n_params, ns = std::min<int64_t>(n_sr, n);
     const uint64_t* dk = keys;
     const double *dlp = log_probs, *dgr = grad;
-    const double2* dl = reinterpret_cast<const double2*>(locals);
+    (void)locals;  // sr_direction's context needs the samples and weights only (sr.cpp:25-72)
     if (mem == QVMC_MEM_HOST) {
       m->g_keys.ensure(n * W * 8);
       m->g_w.ensure(n * 8);
-      m->g_loc.ensure(n * 16);
       m->s_grad.ensure(P * 8);
       ck(cudaMemcpyAsync(m->g_keys.p, keys, n * W * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
       ck(cudaMemcpyAsync(m->g_w.p, log_probs, n * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
-      ck(cudaMemcpyAsync(m->g_loc.p, locals, n * 16, cudaMemcpyHostToDevice, m->stream), "H2D");
       ck(cudaMemcpyAsync(m->s_grad.p, grad, P * 8, cudaMemcpyHostToDevice, m->stream), "H2D");
       dk = m->g_keys.as<uint64_t>();
       dlp = m->g_w.as<double>();
-      dl = m->g_loc.as<double2>();
       dgr = m->s_grad.as<double>();
     }
     // 1. top_probability_indices: stable sort by log p descending (ties keep sample order)

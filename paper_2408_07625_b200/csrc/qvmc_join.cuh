@@ -1361,7 +1361,6 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
   __shared__ uint16_t s_pos[kWarps][32];
   const int lane = threadIdx.x & 31;
   uint16_t* spos = s_pos[threadIdx.x >> 5];
-  const int n = H.n;
   const uint64_t nc = min(static_cast<uint64_t>(*n_chunks), chunk_cap);  // an overflowed batch is rerun
   const bool mag = *exp_flag == 0;  // amplitude magnitudes from the records (k_gather_sorted)
   const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;

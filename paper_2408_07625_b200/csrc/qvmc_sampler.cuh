@@ -102,8 +102,7 @@ __global__ void __launch_bounds__(256)
   double n0c, n1c, nlp, npt;
   fetch(static_cast<int64_t>(blockIdx.x) * 8 + warp, n0c, n1c, nlp, npt);
   for (int64_t b0 = static_cast<int64_t>(blockIdx.x) * 8; b0 < B; b0 += stride) {
-    const int64_t b = b0 + warp;
-    const bool live = b < B;
+    const int64_t b = b0 + warp;  // b >= B: the fetch gave -inf rows, so no children
     const double c0 = n0c, c1 = n1c, plp = nlp, ppert = npt;
     fetch(b + stride, n0c, n1c, nlp, npt);
     // the entry's allowed values (cond > -inf), compacted onto lanes in value order: the k-th
