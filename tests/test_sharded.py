@@ -148,3 +148,97 @@ def test_multi_rank_host_backend_matches_unsharded(cuda_ok, monkeypatch, world, 
         np.testing.assert_array_equal(mom, outs[0][4])  # every rank holds the same rank-order sum
         covered += r1 - r0
     assert covered == b.size()
+
+
+def _sharded_threads(world, n_qubits, c, x, y, z, b):
+    """world ranks as threads of this process, each with its own device handle on cuda:0 and a
+    host all-gather over a thread barrier (the in-process form of the gloo tests above)."""
+    import ctypes as C
+    import threading
+    import paper_2408_07625_b200 as q
+    from paper_2408_07625_b200 import _lib
+    from paper_2408_07625_b200.hamiltonian import _ptr
+    n = b.size()
+    barrier, bufs, outs = threading.Barrier(world), [None] * world, [None] * world
+    L = _lib.lib()
+
+    def make_fn(rank):
+        def fn(ctx, send, recv, nbytes):
+            bufs[rank] = C.string_at(send, nbytes)
+            barrier.wait()
+            C.memmove(recv, b"".join(bufs), nbytes * world)
+            barrier.wait()
+            return 0
+        return _lib.HOST_ALLGATHER_FN(fn)
+
+    fns = [make_fn(r) for r in range(world)]
+    Hs = [q.HamiltonianIndex.from_masks(n_qubits, c, x, y, z) for _ in range(world)]
+    errors = []
+
+    def run(rank):
+        try:
+            comm = C.c_void_p()
+            _lib.check(L.qvmc_cuda_comm_init_host(world, rank, fns[rank], None, C.byref(comm)))
+            r0, r1 = C.c_int64(), C.c_int64()
+            _lib.check(L.qvmc_shard_bounds(n, world, rank, C.byref(r0), C.byref(r1)))
+            r0, r1 = r0.value, r1.value
+            out = np.zeros(max(r1 - r0, 1), dtype=np.complex128)
+            mom = np.zeros(5)
+            sl = lambda a: np.ascontiguousarray(a[r0:r1])
+            _lib.check(L.qvmc_cuda_eloc_sharded(Hs[rank].device_handle(0), comm, n, _ptr(sl(b.vectors)),
+                                                _ptr(sl(b.log_amps)), _ptr(sl(b.phases)), _ptr(sl(b.log_probs)),
+                                                b.log_norm, _ptr(out), _ptr(mom), _lib.MEM_HOST))
+            _lib.check(L.qvmc_cuda_comm_destroy(comm))
+            outs[rank] = (r0, r1, out[: r1 - r0], mom, q.last_stats(Hs[rank]))
+        except Exception as e:  # noqa: BLE001 - surfaced by the test below
+            errors.append(e)
+            barrier.abort()
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errors:
+        raise errors[0]
+    return outs
+
+
+@pytest.mark.parametrize("case,world", [("join56", 2), ("join56", 3), ("sector_lists", 2), ("mixed_popcount", 3),
+                                        ("join_s32", 2)])
+def test_sharded_row_paths_in_process(cuda_ok, monkeypatch, case, world):
+    """Every row path under the sharded call: the join (strided walk, distributed index), the
+    sector candidate lists (QVMC_JOIN=0) and a mixed-popcount set (flip-mask scan over a sample
+    hash table) — the last two split contiguously. Each rank's rows bit-identical to the
+    unsharded E_loc, the global moments equal on every rank and to 1e-12 of the unsharded ones."""
+    import paper_2408_07625_b200 as q
+    from paper_2408_07625_b200 import synthetic
+    if case == "join56":
+        n_qubits, (c, x, y, z) = 56, synthetic.jw_terms(56, 100_000, seed=1)
+        keys = synthetic.near_hf_keys(56, 14, 3001, seed=4)
+    elif case == "sector_lists":
+        monkeypatch.setenv("QVMC_JOIN", "0")
+        n_qubits, (c, x, y, z) = 48, synthetic.jw_terms(48, 20_000, seed=1)
+        keys = synthetic.near_hf_keys(48, 24, 1201, seed=2)
+    elif case == "mixed_popcount":
+        n_qubits, (c, x, y, z) = 20, synthetic.jw_terms(20, 12_000, seed=1)
+        keys = np.unique(np.concatenate([synthetic.random_sector_keys(20, 10, 1500, seed=2),
+                                         synthetic.random_sector_keys(20, 9, 700, seed=3)]), axis=0)
+        keys = keys[np.random.default_rng(5).permutation(len(keys))]
+    else:
+        n_qubits, (c, x, y, z) = 64, synthetic.jw_terms(64, 30_000, seed=1)
+        keys = synthetic.near_hf_keys(64, 32, 800, seed=2)
+    b = synthetic.sample_batch(keys, seed=3)
+    H = q.HamiltonianIndex.from_masks(n_qubits, c, x, y, z)
+    ref = q.surrogate_energy(H, b)
+    st = q.last_stats(H)
+    assert (st["join_mode"] == 1) == case.startswith("join")
+    assert (st["sector_mode"] == 1) == (case != "mixed_popcount")
+    outs = _sharded_threads(world, n_qubits, c, x, y, z, b)
+    covered = 0
+    for r0, r1, loc, mom, _ in outs:
+        assert np.array_equal(loc, ref.locals[r0:r1])
+        assert abs(mom[0] - ref.e_var) <= 1e-12 * max(1.0, abs(ref.e_var))
+        np.testing.assert_array_equal(mom, outs[0][3])
+        covered += r1 - r0
+    assert covered == b.size()
