@@ -711,7 +711,7 @@ template <int W>
 __device__ __forceinline__ void fused_eval_loop(const HamView& H, const JoinView& J, const uint64_t* __restrict__ keys,
                                              int side, int s, const int* __restrict__ exp_flag, double2* eloc,
                                              FusedSmem* F, uint16_t* spos, int e, int lane) {
-  const bool mag = *exp_flag == 0;  // amplitude magnitudes from the records (k_gather_sorted)
+  const bool mag = *exp_flag == 0;  // amplitude magnitudes from the records (k_gather_records)
   int rp[kFPer];
   double2* acc = F->acc[e];  // per served search warp: the current row's sum of chunk sums (lane 0 writes)
 #pragma unroll
@@ -1362,7 +1362,7 @@ __global__ void __launch_bounds__(kThreads, QVMC_EVAL_MINB)
   const int lane = threadIdx.x & 31;
   uint16_t* spos = s_pos[threadIdx.x >> 5];
   const uint64_t nc = min(static_cast<uint64_t>(*n_chunks), chunk_cap);  // an overflowed batch is rerun
-  const bool mag = *exp_flag == 0;  // amplitude magnitudes from the records (k_gather_sorted)
+  const bool mag = *exp_flag == 0;  // amplitude magnitudes from the records (k_gather_records)
   const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t c = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; c < nc; c += n_warps) {
     const uint4 ch = __ldg(chunk + c);
