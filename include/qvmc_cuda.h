@@ -272,6 +272,12 @@ int qvmc_cuda_log_psi(qvmc_model_t m, int64_t n, const uint64_t* keys, int mem, 
  * Synchronises. */
 int qvmc_cuda_fill_amplitudes(qvmc_model_t m, int64_t n, const uint64_t* keys, const double* log_probs, int mem,
                               double* out_log_amp, double* out_phase, double* out_norm2);
+/* 1 when the last qvmc_cuda_fill_amplitudes call recognised the batch as the one
+ * qvmc_cuda_sample produced under the current parameters (same size, parameter
+ * version and device fingerprint of keys and log p): log|psi| = 0.5 log p exactly
+ * (the sampler summed the same amplitude-head values in qudit order) and only the
+ * phase heads were evaluated; 0 when both heads ran. QVMC_FAST_FILL=0 disables. */
+int qvmc_cuda_model_last_fill_sampled(qvmc_model_t m);
 int qvmc_cuda_model_synchronize(qvmc_model_t m);
 /* energy_gradient (proj/src/energy.cpp:93-107, GradientAccumulator :80-91)
  * over the rows of batched_grad_log_psi (proj/src/model.cpp:273-336) of the

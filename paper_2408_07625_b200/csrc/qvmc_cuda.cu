@@ -2355,6 +2355,13 @@ struct qvmc_model_s {
   // device-resident flat parameters (AnqsModel::params) and Adam state (optimizer.cpp:17-31)
   DBuf theta, adam_m, adam_v, adam_d, adam_bad, p_boff;
   long adam_t = 0;
+  // fill_amplitudes of the sampler's own batch (qvmc_cuda_fill_amplitudes): parameter version,
+  // the last sampled batch's size / version and device fingerprints [sample, fill]
+  uint64_t params_version = 0, samp_version = ~uint64_t{0};
+  int64_t samp_n = -1;
+  bool fast_fill = true;   // QVMC_FAST_FILL=0: always evaluate both heads
+  int last_fill_sampled = 0;
+  DBuf fpb;
   ~qvmc_model_s() {
     if (blas) cublasDestroy(blas);
     if (solver) cusolverDnDestroy(solver);
@@ -2376,11 +2383,13 @@ int64_t model_param_count(int n, int bits, int hidden) {
   return c;
 }
 
-void launch_log_psi(qvmc_model_s* m, const uint64_t* keys, int64_t n, double* la, double* ph) {
+// half_lp != null: the batch is the sampler's own (log|psi| = 0.5 log p), only the phase heads run
+void launch_log_psi(qvmc_model_s* m, const uint64_t* keys, int64_t n, double* la, double* ph,
+                    const double* half_lp = nullptr) {
   if (n == 0) return;
   using namespace qvmc_model;
   ModelView V{m->P.as<double>(), m->n, m->n_qudits, m->bits, m->n_e, m->spin, m->n_up};
-  if (!m->tiled) {  // CTA-per-sample-tile kernel (all qudits in one CTA)
+  if (!m->tiled && !half_lp) {  // CTA-per-sample-tile kernel (all qudits in one CTA)
     const int grid = static_cast<int>((n + kTile - 1) / kTile);
     const size_t dyn = static_cast<size_t>((1 + kWBufs) * kHid * kTile) * sizeof(double);
     DISPATCH_W(m->W, {
@@ -2392,7 +2401,7 @@ void launch_log_psi(qvmc_model_s* m, const uint64_t* keys, int64_t n, double* la
     return;
   }
   // warp-tiled: CTAs = (qudit, head) blocks x sample chunks, sized to whole waves of 148 SMs
-  const int n_jh = 2 * m->n_qudits;
+  const int n_jh = half_lp ? m->n_qudits : 2 * m->n_qudits;
   const int64_t max_chunks = std::max<int64_t>(1, (n + kWT * kPWarps - 1) / (kWT * kPWarps));
   int64_t best_s = 1;
   double best_eff = -1.0;
@@ -2409,16 +2418,20 @@ void launch_log_psi(qvmc_model_s* m, const uint64_t* keys, int64_t n, double* la
   int64_t chunk = (n + best_s - 1) / best_s;
   chunk = (chunk + kWT - 1) / kWT * kWT;
   const int64_t S = (n + chunk - 1) / chunk;
-  m->part.ensure(static_cast<size_t>(n_jh) * n * sizeof(double));
+  m->part.ensure(static_cast<size_t>(2 * m->n_qudits) * n * sizeof(double));
   DISPATCH_W(m->W, {
     const size_t dyn = (8448 + kPWarps * 64 * kWT) * sizeof(double) + kPWarps * kWT * WW * sizeof(uint64_t);
     ck(cudaFuncSetAttribute(k_log_psi_part<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)),
        "smem attribute");
-    k_log_psi_part<WW><<<static_cast<unsigned>(S * n_jh), kPThreads, dyn, m->stream>>>(V, keys, n, chunk,
-                                                                                       m->part.as<double>());
+    k_log_psi_part<WW><<<static_cast<unsigned>(S * n_jh), kPThreads, dyn, m->stream>>>(
+        V, keys, n, chunk, m->part.as<double>(), -1, nullptr, half_lp ? 1 : 0);
     ck_launch("log_psi part");
-    k_sum_qudits<WW><<<static_cast<unsigned>((n + 255) / 256), 256, 0, m->stream>>>(V, keys, n, m->part.as<double>(),
-                                                                                  la, ph);
+    if (half_lp)
+      k_sum_phases<WW><<<static_cast<unsigned>((n + 255) / 256), 256, 0, m->stream>>>(V, keys, n, m->part.as<double>(),
+                                                                                     half_lp, la, ph);
+    else
+      k_sum_qudits<WW><<<static_cast<unsigned>((n + 255) / 256), 256, 0, m->stream>>>(V, keys, n,
+                                                                                    m->part.as<double>(), la, ph);
     ck_launch("log_psi sum");
   });
 }
@@ -2460,6 +2473,7 @@ int qvmc_cuda_model_create(int n_qubits, int bits_per_qudit, int n_electrons, in
     m->n_params = model_param_count(n_qubits, bits_per_qudit, hidden);
     m->sms = prop.multiProcessorCount;
     if (const char* e = std::getenv("QVMC_MODEL_TILED")) m->tiled = std::atoi(e) != 0;
+    if (const char* e = std::getenv("QVMC_FAST_FILL")) m->fast_fill = std::atoi(e) != 0;
     ck(cudaStreamCreateWithFlags(&m->own, cudaStreamNonBlocking), "stream create");
     m->stream = m->own;
     *out = m.release();
@@ -2541,6 +2555,7 @@ int qvmc_cuda_model_set_params(qvmc_model_t m, int64_t n_params, const double* p
     ck(cudaMemcpyAsync(m->theta.p, params, m->n_params * 8, cudaMemcpyHostToDevice, m->stream), "H2D theta");
     ck(cudaStreamSynchronize(m->stream), "sync");  // the host staging vector goes out of scope
     m->has_params = true;
+    ++m->params_version;
   });
 }
 
@@ -2668,8 +2683,19 @@ int qvmc_cuda_sample(qvmc_model_t m, int k_samples, uint64_t seed, uint32_t stre
     const cudaMemcpyKind kind = mem == QVMC_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     ck(cudaMemcpyAsync(out_keys, m->bk[cur].p, B * W * 8, kind, m->stream), "copy keys");
     ck(cudaMemcpyAsync(out_log_probs, m->blp[cur].p, B * 8, kind, m->stream), "copy log_probs");
+    // fingerprint of this batch: fill_amplitudes recognises it and halves its log p (k_sum_phases)
+    m->fpb.ensure(4 * sizeof(unsigned long long));
+    ck(cudaMemsetAsync(m->fpb.p, 0, sizeof(unsigned long long), m->stream), "memset fingerprint");
+    if (B > 0)
+      DISPATCH_W(W, (qvmc_model::k_fingerprint<WW><<<static_cast<unsigned>(std::min<int64_t>((B + 255) / 256,
+                                                                                             4 * m->sms)),
+                                                     256, 0, m->stream>>>(m->bk[cur].as<uint64_t>(),
+                                                                          m->blp[cur].as<double>(), B,
+                                                                          m->fpb.as<unsigned long long>())));
     ck(cudaStreamSynchronize(m->stream), "sync");
     *out_n = B;
+    m->samp_n = B;
+    m->samp_version = m->params_version;
   });
 }
 
@@ -3213,6 +3239,7 @@ int qvmc_cuda_model_adam_step(qvmc_model_t m, const double* direction, double le
     k_params_relayout<<<2 * m->n_qudits, 256, 0, m->stream>>>(V, m->p_boff.as<int64_t>(), m->theta.as<double>(),
                                                               m->P.as<double>());
     ck_launch("params relayout");
+    ++m->params_version;
     ck(cudaStreamSynchronize(m->stream), "sync");
   });
 }
@@ -3265,15 +3292,41 @@ int qvmc_cuda_fill_amplitudes(qvmc_model_t m, int64_t n, const uint64_t* keys, c
       out_norm2[1] = -std::numeric_limits<double>::infinity();
       return;
     }
-    const int st = qvmc_cuda_log_psi(m, n, keys, mem, out_log_amp, out_phase);
-    if (st != QVMC_OK) throw Failure{st, g_error};
+    if (!keys || !out_log_amp || !out_phase) fail(QVMC_ERR_INVALID_ARGUMENT, "null array");
+    if (!m->has_params) fail(QVMC_ERR_INVALID_ARGUMENT, "model parameters not set");
     DeviceGuard dg(m->device);
+    const uint64_t* dk = keys;
     const double* dlp = log_probs;
+    double *dla = out_log_amp, *dph = out_phase;
     if (mem == QVMC_MEM_HOST) {
+      m->keys.ensure(std::max<size_t>(n * m->W * 8, 16));
+      m->la.ensure(std::max<size_t>(n * 8, 16));
+      m->ph.ensure(std::max<size_t>(n * 8, 16));
       m->lp.ensure(n * 8);
+      ck(cudaMemcpyAsync(m->keys.p, keys, n * m->W * 8, cudaMemcpyHostToDevice, m->stream), "H2D keys");
       ck(cudaMemcpyAsync(m->lp.p, log_probs, n * 8, cudaMemcpyHostToDevice, m->stream), "H2D log_probs");
+      dk = m->keys.as<uint64_t>();
       dlp = m->lp.as<double>();
+      dla = m->la.as<double>();
+      dph = m->ph.as<double>();
     }
+    // the batch qvmc_cuda_sample produced under the current parameters (same size and version,
+    // same fingerprint of keys and log p): log|psi| = 0.5 log p exactly, phase heads only
+    bool sampled = false;
+    if (m->fast_fill && m->tiled && n == m->samp_n && m->params_version == m->samp_version) {
+      ck(cudaMemsetAsync(m->fpb.as<unsigned long long>() + 1, 0, sizeof(unsigned long long), m->stream), "memset");
+      DISPATCH_W(m->W, (qvmc_model::k_fingerprint<WW><<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256,
+                                                                                                4 * m->sms)),
+                                                        256, 0, m->stream>>>(dk, dlp, n,
+                                                                             m->fpb.as<unsigned long long>() + 1)));
+      ck_launch("fingerprint");
+      unsigned long long fp[2] = {0, 0};
+      ck(cudaMemcpyAsync(fp, m->fpb.p, sizeof(fp), cudaMemcpyDeviceToHost, m->stream), "D2H fingerprints");
+      ck(cudaStreamSynchronize(m->stream), "sync");
+      sampled = fp[0] == fp[1];
+    }
+    m->last_fill_sampled = sampled ? 1 : 0;
+    launch_log_psi(m, dk, n, dla, dph, sampled ? dlp : nullptr);
     using namespace qvmc_model;
     m->lse.ensure(kLseBlocks * sizeof(double2));
     m->out2.ensure(2 * sizeof(double));
@@ -3281,10 +3334,17 @@ int qvmc_cuda_fill_amplitudes(qvmc_model_t m, int64_t n, const uint64_t* keys, c
     ck_launch("lse partial");
     k_lse_final<<<1, 32, 0, m->stream>>>(m->lse.as<double2>(), kLseBlocks, m->out2.as<double>());
     ck_launch("lse final");
+    if (mem == QVMC_MEM_HOST) {
+      ck(cudaMemcpyAsync(out_log_amp, dla, n * 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
+      ck(cudaMemcpyAsync(out_phase, dph, n * 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
+    }
     ck(cudaMemcpyAsync(out_norm2, m->out2.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, m->stream), "D2H norm");
     ck(cudaStreamSynchronize(m->stream), "sync");
   });
 }
+
+// 1 when the last qvmc_cuda_fill_amplitudes recognised the sampler's own batch (phase heads only)
+int qvmc_cuda_model_last_fill_sampled(qvmc_model_t m) { return m ? m->last_fill_sampled : 0; }
 
 int qvmc_cuda_model_synchronize(qvmc_model_t m) {
   return guarded([&] {

@@ -415,7 +415,8 @@ __device__ __forceinline__ int pidx(int k, int s) {
 template <int W>
 __global__ void __launch_bounds__(kPThreads, 1)
     k_log_psi_part(const ModelView M, const uint64_t* __restrict__ keys, int64_t N, int64_t chunk,
-                   double* __restrict__ part, int only_j = -1, double* __restrict__ cond = nullptr) {
+                   double* __restrict__ part, int only_j = -1, double* __restrict__ cond = nullptr,
+                   int phase_only = 0) {
   // only_j >= 0 (the sampler, sampler.cpp:53-55): the amplitude head of qudit only_j
   // for every key (a beam prefix), writing the whole conditional log-probability
   // table cond[s][64] (model.cpp:226-249; -inf for disallowed values) instead of part
@@ -426,8 +427,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
   double* acts = smem + 8448;          // [16 warps][64][16]
   uint64_t* skeys = reinterpret_cast<uint64_t*>(acts + kPWarps * 64 * kWT);  // [16 warps][16][W]
 
-  const int n_jh = only_j >= 0 ? 1 : 2 * M.n_qudits;
-  const int jh = only_j >= 0 ? 2 * only_j : static_cast<int>(blockIdx.x % n_jh), j = jh >> 1, hd = jh & 1;
+  // phase_only: the phase heads alone (a freshly sampled batch's log|psi| is half its log p)
+  const int n_jh = only_j >= 0 ? 1 : (phase_only ? M.n_qudits : 2 * M.n_qudits);
+  const int jh = only_j >= 0 ? 2 * only_j
+                             : (phase_only ? 2 * static_cast<int>(blockIdx.x % n_jh) + 1
+                                           : static_cast<int>(blockIdx.x % n_jh)),
+            j = jh >> 1, hd = jh & 1;
   const int64_t c0 = static_cast<int64_t>(blockIdx.x / n_jh) * chunk;
   const int64_t c1 = min(N, c0 + chunk);
   const BlockLayout L{M.n};
@@ -1347,6 +1352,53 @@ __global__ void k_sum_qudits(const ModelView M, const uint64_t* __restrict__ key
   const bool ins = pc == M.n_e && (!M.spin || pe == M.n_up);
   out_la[s] = ins ? la : -CUDART_INF;
   out_ph[s] = ins ? ph : 0.0;
+}
+
+// fill_amplitudes of a batch qvmc_cuda_sample just produced with the current
+// parameters: the sampler accumulated log p = Σ_j c_j in qudit order from the
+// same amplitude-head arithmetic whose halves 0.5 c_j k_sum_qudits would add in
+// that order, so log|ψ| = 0.5 log p exactly (scaling by 2^-1 commutes with the
+// rounded sums); φ from the phase heads as in k_sum_qudits
+template <int W>
+__global__ void k_sum_phases(const ModelView M, const uint64_t* __restrict__ keys, int64_t N,
+                             const double* __restrict__ part, const double* __restrict__ lp,
+                             double* __restrict__ out_la, double* __restrict__ out_ph) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= N) return;
+  int pc = 0, pe = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const uint64_t x = __ldg(keys + s * W + w);
+    pc += __popcll(x);
+    pe += __popcll(x & 0x5555555555555555ull);
+  }
+  double ph = 0.0;
+  for (int j = 0; j < M.n_qudits; ++j) ph += __ldcs(part + static_cast<int64_t>(2 * j + 1) * N + s);
+  const bool ins = pc == M.n_e && (!M.spin || pe == M.n_up);
+  out_la[s] = ins ? 0.5 * lp[s] : -CUDART_INF;
+  out_ph[s] = ins ? ph : 0.0;
+}
+
+// order-independent fingerprint of a batch (keys, log p): wrapping sum of mixed
+// (index, words, bits) per sample, for recognising the sampler's own output
+template <int W>
+__global__ void k_fingerprint(const uint64_t* __restrict__ keys, const double* __restrict__ lp, int64_t N,
+                              unsigned long long* __restrict__ out) {
+  unsigned long long acc = 0;
+  for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < N;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint64_t z = static_cast<uint64_t>(s) * 0x9E3779B97F4A7C15ull ^ static_cast<uint64_t>(__double_as_longlong(lp[s]));
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      z ^= keys[s * W + w] + 0x632BE59BD9B4E019ull * (w + 1);
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      z ^= z >> 31;
+    }
+    acc += z;
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
 
 // log_norm = logsumexp(log_probs) (sampler.cpp:114-119), deterministic:

@@ -140,3 +140,40 @@ def test_device_sampler_ranked_law_chi_square(cuda_ok):
     expect = trials * probs
     stat = float(((counts - expect) ** 2 / expect).sum())
     assert stat < 11.345  # chi-square 99 % critical value, 3 degrees of freedom
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["h56", "t8"])
+def test_fill_amplitudes_of_the_sampled_batch(cuda_ok, monkeypatch, name):
+    """fill_amplitudes of the batch qvmc_cuda_sample just produced (same parameters): the sampler
+    summed the amplitude heads' conditional log-probabilities in qudit order, so log|psi| = 0.5 log p
+    bit for bit and only the phase heads run. Same amplitudes, phases and norm as the full
+    evaluation (QVMC_FAST_FILL=0); any other batch, or changed parameters, takes the full path."""
+    import paper_2408_07625_b200 as q
+    from paper_2408_07625_b200 import _lib
+    L = _lib.lib()
+    monkeypatch.setenv("QVMC_FAST_FILL", "0")
+    full = _model(name)
+    monkeypatch.delenv("QVMC_FAST_FILL")
+    M = _model(name)
+    k = 20_000 if name == "h56" else 40
+    b = q.sample_without_replacement(M, k, q.CounterRng(9, 2), 3)
+    ref = q.SampleBatch(b.vectors.copy(), b.log_probs.copy(), np.zeros(b.size()), np.zeros(b.size()), 0.0, 0.0)
+    q.fill_amplitudes(b, M)
+    assert L.qvmc_cuda_model_last_fill_sampled(M._h) == 1
+    q.fill_amplitudes(ref, full)
+    assert L.qvmc_cuda_model_last_fill_sampled(full._h) == 0
+    assert np.array_equal(b.log_amps, ref.log_amps) and np.array_equal(b.phases, ref.phases)
+    assert np.array_equal(b.log_amps, 0.5 * b.log_probs)
+    assert b.norm == ref.norm and b.log_norm == ref.log_norm
+    # a different batch (one sample dropped), then the same batch after a parameter update
+    other = q.SampleBatch(b.vectors[:-1].copy(), b.log_probs[:-1].copy(), np.zeros(b.size() - 1),
+                          np.zeros(b.size() - 1), 0.0, 0.0)
+    q.fill_amplitudes(other, M)
+    assert L.qvmc_cuda_model_last_fill_sampled(M._h) == 0
+    q.sample_without_replacement(M, k, q.CounterRng(9, 2), 3)
+    M.set_params(_cfg(name)[5])
+    again = q.SampleBatch(b.vectors.copy(), b.log_probs.copy(), np.zeros(b.size()), np.zeros(b.size()), 0.0, 0.0)
+    q.fill_amplitudes(again, M)
+    assert L.qvmc_cuda_model_last_fill_sampled(M._h) == 0
+    assert np.array_equal(again.log_amps, ref.log_amps)
