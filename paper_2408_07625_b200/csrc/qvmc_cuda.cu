@@ -2742,7 +2742,7 @@ void launch_grad_parts(qvmc_model_s* m, const qvmc_model::ModelView& V, const ui
       m->g_bsum.as<double>());
   ck_launch("grad forward");
   k_grad_bwd<W><<<static_cast<unsigned>(S * nb), kG2Threads, dyn_b, m->stream>>>(
-      V, n, per, m->g_h1.as<double>(), m->g_h2.as<double>(), m->g_g.as<double>(), m->g_gz2.as<double>(),
+      V, keys, n, per, m->g_h1.as<double>(), m->g_h2.as<double>(), m->g_g.as<double>(), m->g_gz2.as<double>(),
       m->g_gz1.as<double>(), n_blk, m->g_bsum.as<double>() + static_cast<size_t>(S * nb) * 64);
   ck_launch("grad backward");
 }

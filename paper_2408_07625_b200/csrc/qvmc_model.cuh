@@ -989,16 +989,17 @@ __global__ void __launch_bounds__(kG2Threads, 1)
 // (h, k) orientation, the same warp tiling and GEMM as the forward kernels.
 template <int W>
 __global__ void __launch_bounds__(kG2Threads, 1)
-    k_grad_bwd(const ModelView M, int64_t N, int64_t chunk, const double* __restrict__ H1,
-               const double* __restrict__ H2, const double* __restrict__ G, double* __restrict__ GZ2,
-               double* __restrict__ GZ1, int64_t N_blk, double* __restrict__ GZ2SUM) {
+    k_grad_bwd(const ModelView M, const uint64_t* __restrict__ keys, int64_t N, int64_t chunk,
+               const double* __restrict__ H1, const double* __restrict__ H2, const double* __restrict__ G,
+               double* __restrict__ GZ2, double* __restrict__ GZ1, int64_t N_blk, double* __restrict__ GZ2SUM) {
   extern __shared__ __align__(16) double smem[];
   double* w2o = smem;           // [64 h][64 k]  (W2)
   double* w3o = smem + 4096;    // [64 v][64 h]  (W3)
   double* acts = smem + 8192;   // [warps][64][16]
   double* bsum = acts + kG2Warps * 64 * kWT;  // [warps][64]: Σ gz2 of the warp's tiles (gb2)
   const int n_jh = 2 * M.n_qudits;
-  const int jh = static_cast<int>(blockIdx.x % n_jh);
+  const int jh = static_cast<int>(blockIdx.x % n_jh), hd = jh & 1;
+  const int off = (jh >> 1) * M.bits, kb = min(M.bits, M.n - off);
   const int64_t c0 = static_cast<int64_t>(blockIdx.x / n_jh) * chunk;
   const int64_t c1 = min(N, c0 + chunk);
   const BlockLayout L{M.n};
@@ -1063,9 +1064,27 @@ __global__ void __launch_bounds__(kG2Threads, 1)
           for (int f = 0; f < 8; ++f) acc[si][f] = fma(av[si], wv[f], acc[si][f]);
       }
     };
-    load(gi, 64);  // g -> act
-    to_act();
-    gemm(w3o);     // W3ᵀ g
+    if (hd) {  // phase head: g = coefficient * onehot(v), so W3ᵀ g = g[v] * row v of W3
+#pragma unroll
+      for (int si = 0; si < 4; ++si) {
+        int val = 0;
+        double gv = 0.0;
+        if (row(si) < c1) {  // the sampled value of this qudit (extract_bits, basis_vector.cpp:40-45)
+          const uint64_t* x = keys + row(si) * W;
+          const int wq = off >> 6, bq = off & 63;
+          uint64_t fld = __ldg(x + wq) >> bq;
+          if (bq + kb > 64 && wq + 1 < W) fld |= __ldg(x + wq + 1) << (64 - bq);
+          val = static_cast<int>(__brev(static_cast<uint32_t>(fld)) >> (32 - kb));
+          gv = gi[row(si) * 64 + val];
+        }
+#pragma unroll
+        for (int f = 0; f < 8; ++f) acc[si][f] = gv * w3o[val * 64 + feat(f)];
+      }
+    } else {
+      load(gi, 64);  // g -> act
+      to_act();
+      gemm(w3o);     // W3ᵀ g
+    }
     load(h2i, 64);
 #pragma unroll
     for (int si = 0; si < 4; ++si)
