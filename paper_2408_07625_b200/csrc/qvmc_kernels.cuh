@@ -519,6 +519,7 @@ __global__ void __launch_bounds__(kThreads) k_rows(const __grid_constant__ HamVi
     r = __shfl_sync(0xffffffffu, r, 0);
     const int64_t row = row_begin + static_cast<int64_t>(r);
     if (row >= row_end) break;
+    __syncwarp();  // the previous row's reads of the warp's shared tables are done before they are rewritten
 
     uint64_t x[W];
 #pragma unroll
