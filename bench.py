@@ -542,8 +542,10 @@ def main():
         "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_desc(cfg, H.n_terms, H.n_xy, n) | {
-            "parallelism": f"rows sharded over {world} GPU(s): qvmc_cuda_eloc_sharded (NCCL all-gather of the "
-                           "packed shards and of the per-rank moments inside libqvmc_cuda)" if sharded else "1 GPU",
+            "parallelism": f"rows sharded over {world} GPU(s): qvmc_cuda_eloc_sharded over NCCL inside libqvmc_cuda "
+                           "(all-gather of the packed shards, deletion index built across the ranks, strided walk of "
+                           "the locality order, exact integer all-reduces of the mirrored sums and rows, rank-order "
+                           "moments)" if sharded else "1 GPU",
             "l2": "flushed between steps (256 MiB write outside the timed events)" if flush is not None else "not flushed"},
         "e2e": {"value": n / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "path": "qvmc_cuda_eloc_fused(QVMC_MEM_HOST) from pinned buffers" if not sharded
