@@ -278,6 +278,11 @@ int qvmc_cuda_fill_amplitudes(qvmc_model_t m, int64_t n, const uint64_t* keys, c
  * (the sampler summed the same amplitude-head values in qudit order) and only the
  * phase heads were evaluated; 0 when both heads ran. QVMC_FAST_FILL=0 disables. */
 int qvmc_cuda_model_last_fill_sampled(qvmc_model_t m);
+/* 1 when the last qvmc_cuda_energy_gradient call found the phase heads' h1 / h2
+ * activations of its batch kept by the sampled-batch fill (same size, parameter
+ * version and keys fingerprint) and copied them instead of recomputing the phase
+ * blocks' forward pass (bit-identical); 0 otherwise. QVMC_GRAD_CACHE=0 disables. */
+int qvmc_cuda_model_last_gradient_cached(qvmc_model_t m);
 int qvmc_cuda_model_synchronize(qvmc_model_t m);
 /* energy_gradient (proj/src/energy.cpp:93-107, GradientAccumulator :80-91)
  * over the rows of batched_grad_log_psi (proj/src/model.cpp:273-336) of the

@@ -95,6 +95,7 @@ SIGNATURES = [
     ("qvmc_cuda_log_psi", _INT, [_P, _I64, _P, _INT, _P, _P]),
     ("qvmc_cuda_fill_amplitudes", _INT, [_P, _I64, _P, _P, _INT, _P, _P, _P]),
     ("qvmc_cuda_model_last_fill_sampled", _INT, [_P]),
+    ("qvmc_cuda_model_last_gradient_cached", _INT, [_P]),
     ("qvmc_cuda_model_synchronize", _INT, [_P]),
     ("qvmc_cuda_energy_gradient", _INT, [_P, _I64, _P, _P, _P, _INT, _P]),
     ("qvmc_cuda_model_get_params", _INT, [_P, _INT, _P]),

@@ -2362,6 +2362,14 @@ struct qvmc_model_s {
   bool fast_fill = true;   // QVMC_FAST_FILL=0: always evaluate both heads
   int last_fill_sampled = 0;
   DBuf fpb;
+  // the phase heads' activations of the last sampled-batch fill, for the gradient of that batch
+  // (QVMC_GRAD_CACHE=0 disables): rows, parameter version, keys fingerprint
+  DBuf hcache;
+  bool grad_cache = true;
+  int64_t hc_n = -1;
+  uint64_t hc_version = ~uint64_t{0};
+  unsigned long long hc_fp = 0;
+  int last_grad_cached = 0;
   ~qvmc_model_s() {
     if (blas) cublasDestroy(blas);
     if (solver) cusolverDnDestroy(solver);
@@ -2385,7 +2393,7 @@ int64_t model_param_count(int n, int bits, int hidden) {
 
 // half_lp != null: the batch is the sampler's own (log|psi| = 0.5 log p), only the phase heads run
 void launch_log_psi(qvmc_model_s* m, const uint64_t* keys, int64_t n, double* la, double* ph,
-                    const double* half_lp = nullptr) {
+                    const double* half_lp = nullptr, double* hcache = nullptr) {
   if (n == 0) return;
   using namespace qvmc_model;
   ModelView V{m->P.as<double>(), m->n, m->n_qudits, m->bits, m->n_e, m->spin, m->n_up};
@@ -2424,7 +2432,7 @@ void launch_log_psi(qvmc_model_s* m, const uint64_t* keys, int64_t n, double* la
     ck(cudaFuncSetAttribute(k_log_psi_part<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)),
        "smem attribute");
     k_log_psi_part<WW><<<static_cast<unsigned>(S * n_jh), kPThreads, dyn, m->stream>>>(
-        V, keys, n, chunk, m->part.as<double>(), -1, nullptr, half_lp ? 1 : 0);
+        V, keys, n, chunk, m->part.as<double>(), -1, nullptr, half_lp ? 1 : 0, half_lp ? hcache : nullptr);
     ck_launch("log_psi part");
     if (half_lp)
       k_sum_phases<WW><<<static_cast<unsigned>((n + 255) / 256), 256, 0, m->stream>>>(V, keys, n, m->part.as<double>(),
@@ -2474,6 +2482,7 @@ int qvmc_cuda_model_create(int n_qubits, int bits_per_qudit, int n_electrons, in
     m->sms = prop.multiProcessorCount;
     if (const char* e = std::getenv("QVMC_MODEL_TILED")) m->tiled = std::atoi(e) != 0;
     if (const char* e = std::getenv("QVMC_FAST_FILL")) m->fast_fill = std::atoi(e) != 0;
+    if (const char* e = std::getenv("QVMC_GRAD_CACHE")) m->grad_cache = std::atoi(e) != 0;
     ck(cudaStreamCreateWithFlags(&m->own, cudaStreamNonBlocking), "stream create");
     m->stream = m->own;
     *out = m.release();
@@ -2727,7 +2736,8 @@ __global__ void k_sector_flags(const uint64_t* __restrict__ keys, int64_t n, int
 // into the chunk buffers (block stride n_blk rows)
 template <int W>
 void launch_grad_parts(qvmc_model_s* m, const qvmc_model::ModelView& V, const uint64_t* keys, int64_t n, int64_t per,
-                       int64_t S, int nb, const double2* coef, int64_t n_blk) {
+                       int64_t S, int nb, const double2* coef, int64_t n_blk, const double* hc = nullptr,
+                       int64_t hc_rows = 0) {
   using namespace qvmc_model;
   const size_t dyn_f = (8448 + kG2Warps * 64 * kWT + kG2Warps * 64) * sizeof(double) +
                        kG2Warps * kWT * W * sizeof(uint64_t);
@@ -2739,7 +2749,7 @@ void launch_grad_parts(qvmc_model_s* m, const qvmc_model::ModelView& V, const ui
      "smem attribute");
   k_grad_fwd<W><<<static_cast<unsigned>(S * nb), kG2Threads, dyn_f, m->stream>>>(
       V, keys, n, per, coef, m->g_h1.as<double>(), m->g_h2.as<double>(), m->g_g.as<double>(), n_blk,
-      m->g_bsum.as<double>());
+      m->g_bsum.as<double>(), hc, hc_rows);
   ck_launch("grad forward");
   k_grad_bwd<W><<<static_cast<unsigned>(S * nb), kG2Threads, dyn_b, m->stream>>>(
       V, keys, n, per, m->g_h1.as<double>(), m->g_h2.as<double>(), m->g_g.as<double>(), m->g_gz2.as<double>(),
@@ -2755,6 +2765,21 @@ void grad_accumulate(qvmc_model_s* m, const uint64_t* keys, int64_t n, const dou
   ModelView V{m->P.as<double>(), m->n, m->n_qudits, m->bits, m->n_e, m->spin, m->n_up};
   if (!m->blas) blas_ck(cublasCreate(&m->blas), "cublasCreate");
   blas_ck(cublasSetStream(m->blas, m->stream), "cublasSetStream");
+  // the batch of the last sampled-batch fill under the current parameters (same size, version and keys
+  // fingerprint): its phase blocks copy the cached activations instead of recomputing them
+  bool cached = false;
+  if (m->hc_n == n && n > 0 && m->hc_version == m->params_version) {
+    m->fpb.ensure(4 * sizeof(unsigned long long));
+    ck(cudaMemsetAsync(m->fpb.as<unsigned long long>() + 3, 0, sizeof(unsigned long long), m->stream), "memset");
+    DISPATCH_W(W, (k_fingerprint<WW><<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4 * m->sms)), 256, 0,
+                                       m->stream>>>(keys, nullptr, n, m->fpb.as<unsigned long long>() + 3)));
+    ck_launch("keys fingerprint");
+    unsigned long long fp = 0;
+    ck(cudaMemcpyAsync(&fp, m->fpb.as<unsigned long long>() + 3, 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
+    ck(cudaStreamSynchronize(m->stream), "sync");
+    cached = fp == m->hc_fp;
+  }
+  m->last_grad_cached = cached ? 1 : 0;
   // split-K: every chunk's sample range is cut into `parts` slices so the
   // batched GEMMs (64 x 64 outputs, one per block) fill the SMs; partial sums
   // are added in part order by k_sum_parts (deterministic)
@@ -2814,7 +2839,8 @@ void grad_accumulate(qvmc_model_s* m, const uint64_t* keys, int64_t n, const dou
     const int64_t per = 1024;  // samples per CTA
     const int64_t S = (nc + per - 1) / per;
     DISPATCH_W(W, {
-      launch_grad_parts<WW>(m, V, keys + c0 * WW, nc, per, S, nb, coef + c0, Ncur);
+      launch_grad_parts<WW>(m, V, keys + c0 * WW, nc, per, S, nb, coef + c0, Ncur,
+                            cached ? m->hcache.as<double>() + c0 * 128 : nullptr, n);
       const int xg = static_cast<int>(std::min<int64_t>((nc * nx + 255) / 256, 8LL * m->sms));
       k_pm_bits<WW><<<xg, 256, 0, m->stream>>>(keys + c0 * WW, nc, nq, m->g_x.as<double>());
       ck_launch("pm bits");
@@ -3326,7 +3352,20 @@ int qvmc_cuda_fill_amplitudes(qvmc_model_t m, int64_t n, const uint64_t* keys, c
       sampled = fp[0] == fp[1];
     }
     m->last_fill_sampled = sampled ? 1 : 0;
-    launch_log_psi(m, dk, n, dla, dph, sampled ? dlp : nullptr);
+    // keep the phase heads' activations for the gradient of this batch (at most 48 GB)
+    const size_t hc_bytes = static_cast<size_t>(m->n_qudits) * static_cast<size_t>(n) * 128 * sizeof(double);
+    const bool keep = sampled && m->grad_cache && hc_bytes <= (size_t{48} << 30);
+    m->hc_n = -1;
+    if (keep) {
+      m->hcache.ensure(hc_bytes);
+      ck(cudaMemsetAsync(m->fpb.as<unsigned long long>() + 2, 0, sizeof(unsigned long long), m->stream), "memset");
+      DISPATCH_W(m->W, (qvmc_model::k_fingerprint<WW><<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256,
+                                                                                                4 * m->sms)),
+                                                        256, 0, m->stream>>>(dk, nullptr, n,
+                                                                             m->fpb.as<unsigned long long>() + 2)));
+      ck_launch("keys fingerprint");
+    }
+    launch_log_psi(m, dk, n, dla, dph, sampled ? dlp : nullptr, keep ? m->hcache.as<double>() : nullptr);
     using namespace qvmc_model;
     m->lse.ensure(kLseBlocks * sizeof(double2));
     m->out2.ensure(2 * sizeof(double));
@@ -3339,12 +3378,22 @@ int qvmc_cuda_fill_amplitudes(qvmc_model_t m, int64_t n, const uint64_t* keys, c
       ck(cudaMemcpyAsync(out_phase, dph, n * 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
     }
     ck(cudaMemcpyAsync(out_norm2, m->out2.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, m->stream), "D2H norm");
+    unsigned long long kfp = 0;
+    if (keep) ck(cudaMemcpyAsync(&kfp, m->fpb.as<unsigned long long>() + 2, 8, cudaMemcpyDeviceToHost, m->stream), "D2H");
     ck(cudaStreamSynchronize(m->stream), "sync");
+    if (keep) {
+      m->hc_n = n;
+      m->hc_version = m->params_version;
+      m->hc_fp = kfp;
+    }
   });
 }
 
 // 1 when the last qvmc_cuda_fill_amplitudes recognised the sampler's own batch (phase heads only)
 int qvmc_cuda_model_last_fill_sampled(qvmc_model_t m) { return m ? m->last_fill_sampled : 0; }
+
+// 1 when the last qvmc_cuda_energy_gradient reused the sampled-batch fill's phase-head activations
+int qvmc_cuda_model_last_gradient_cached(qvmc_model_t m) { return m ? m->last_grad_cached : 0; }
 
 int qvmc_cuda_model_synchronize(qvmc_model_t m) {
   return guarded([&] {

@@ -416,7 +416,9 @@ template <int W>
 __global__ void __launch_bounds__(kPThreads, 1)
     k_log_psi_part(const ModelView M, const uint64_t* __restrict__ keys, int64_t N, int64_t chunk,
                    double* __restrict__ part, int only_j = -1, double* __restrict__ cond = nullptr,
-                   int phase_only = 0) {
+                   int phase_only = 0, double* __restrict__ hcache = nullptr) {
+  // hcache (phase_only): the phase heads' activations per sample, [qudit][N][h1 64 | h2 64], kept for
+  // the energy gradient of the same batch (k_grad_fwd copies them instead of recomputing)
   // only_j >= 0 (the sampler, sampler.cpp:53-55): the amplitude head of qudit only_j
   // for every key (a beam prefix), writing the whole conditional log-probability
   // table cond[s][64] (model.cpp:226-249; -inf for disallowed values) instead of part
@@ -536,6 +538,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
         const int h = 16 * (f >> 1) + 2 * hq + (f & 1);
         *reinterpret_cast<double2*>(act + pidx(h, sq * 4 + 2 * p)) = make_double2(a[0][f], a[1][f]);
       }
+      if (hcache) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int64_t g = t0 + sq * 4 + 2 * p + u;
+          if (g < c1)
+#pragma unroll
+            for (int f = 0; f < 8; f += 2)
+              *reinterpret_cast<double2*>(hcache + (static_cast<int64_t>(j) * N + g) * 128 + 16 * (f >> 1) + 2 * hq) =
+                  make_double2(a[u][f], a[u][f + 1]);
+        }
+      }
     }
     __syncwarp();
 
@@ -579,6 +592,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
 
     if (hd == 1) {
+      if (hcache) {
+#pragma unroll
+        for (int si = 0; si < 4; ++si) {
+          const int64_t g = t0 + sq * 4 + si;
+          if (g < c1)
+#pragma unroll
+            for (int f = 0; f < 8; f += 2)
+              *reinterpret_cast<double2*>(hcache + (static_cast<int64_t>(j) * N + g) * 128 + 64 + 16 * (f >> 1) +
+                                          2 * hq) = make_double2(acc[si][f], acc[si][f + 1]);
+        }
+      }
       // phase head: only out[v] of the sampled value (model.cpp:173-174, :250)
 #pragma unroll
       for (int si = 0; si < 4; ++si) {
@@ -725,7 +749,10 @@ template <int W>
 __global__ void __launch_bounds__(kG2Threads, 1)
     k_grad_fwd(const ModelView M, const uint64_t* __restrict__ keys, int64_t N, int64_t chunk,
                 const double2* __restrict__ coef, double* __restrict__ H1, double* __restrict__ H2,
-                double* __restrict__ G, int64_t N_blk, double* __restrict__ GSUM) {
+                double* __restrict__ G, int64_t N_blk, double* __restrict__ GSUM,
+                const double* __restrict__ HC = nullptr, int64_t hc_rows = 0) {
+  // HC (phase blocks): this chunk's cached activations [qudit][hc_rows][h1 | h2] from the sampled-batch
+  // fill (bit-identical to recomputing them): copied to the chunk rows, only the one-hot g formed
   // N: samples of this call; N_blk: rows per block in the buffers (>= N, padded for split-K)
   extern __shared__ __align__(16) double smem[];
   double* w2 = smem;            // [64 k][64 h]  (W2 transposed)
@@ -808,6 +835,25 @@ __global__ void __launch_bounds__(kG2Threads, 1)
       if (row(si) < c1) *reinterpret_cast<double2*>(o + row(si) * ld + feat(f)) = make_double2(v0, v1);
     };
 
+    double g[4][8];
+    if (HC != nullptr && hd) {  // phase block of the sampled batch: cached h1 / h2, one-hot g
+#pragma unroll
+      for (int si = 0; si < 4; ++si)
+        if (row(si) < c1) {
+          const double* hr = HC + (static_cast<int64_t>(j) * hc_rows + row(si)) * 128;
+#pragma unroll
+          for (int f = 0; f < 8; f += 2) {
+            const double2 x1 = *reinterpret_cast<const double2*>(hr + feat(f));
+            const double2 x2 = *reinterpret_cast<const double2*>(hr + 64 + feat(f));
+            put(h1o, si, f, x1.x, x1.y);
+            put(h2o, si, f, x2.x, x2.y);
+          }
+        }
+#pragma unroll
+      for (int si = 0; si < 4; ++si)
+#pragma unroll
+        for (int f = 0; f < 8; ++f) g[si][f] = feat(f) == val[si] ? cf[si] : 0.0;
+    } else {
     // layer 1 -> h1 (model.cpp:171), as in k_log_psi_part
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
@@ -906,7 +952,6 @@ __global__ void __launch_bounds__(kG2Threads, 1)
       for (int f = 0; f < 8; f += 2) put(h2o, si, f, h2[si][f], h2[si][f + 1]);
 
     // output gradient g (d/d raw output), scaled by the sample's coefficient
-    double g[4][8];
     if (hd == 0) {
       // amplitude head: onehot(v) - softmax(2 out) over allowed, minus its mean (model.cpp:288-310)
       to_act(h2);
@@ -972,6 +1017,7 @@ __global__ void __launch_bounds__(kG2Threads, 1)
       for (int si = 0; si < 4; ++si)
 #pragma unroll
         for (int f = 0; f < 8; ++f) g[si][f] = feat(f) == val[si] ? cf[si] : 0.0;
+    }
     }
 #pragma unroll
     for (int si = 0; si < 4; ++si)
@@ -1406,7 +1452,8 @@ __global__ void k_fingerprint(const uint64_t* __restrict__ keys, const double* _
   unsigned long long acc = 0;
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < N;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    uint64_t z = static_cast<uint64_t>(s) * 0x9E3779B97F4A7C15ull ^ static_cast<uint64_t>(__double_as_longlong(lp[s]));
+    uint64_t z = static_cast<uint64_t>(s) * 0x9E3779B97F4A7C15ull ^
+                 (lp ? static_cast<uint64_t>(__double_as_longlong(lp[s])) : 0ull);  // lp null: keys only
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       z ^= keys[s * W + w] + 0x632BE59BD9B4E019ull * (w + 1);

@@ -177,3 +177,39 @@ def test_fill_amplitudes_of_the_sampled_batch(cuda_ok, monkeypatch, name):
     q.fill_amplitudes(again, M)
     assert L.qvmc_cuda_model_last_fill_sampled(M._h) == 0
     assert np.array_equal(again.log_amps, ref.log_amps)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["h56", "t8"])
+def test_gradient_reuses_the_sampled_fill(cuda_ok, monkeypatch, name):
+    """The sampled-batch fill keeps the phase heads' h1 / h2; the energy gradient of that batch
+    copies them instead of recomputing the phase blocks' forward pass, bit for bit (a model with
+    QVMC_GRAD_CACHE=0 recomputes); another key set, or new parameters, recompute."""
+    import paper_2408_07625_b200 as q
+    from paper_2408_07625_b200 import _lib
+    L = _lib.lib()
+    monkeypatch.setenv("QVMC_GRAD_CACHE", "0")
+    ref = _model(name)
+    monkeypatch.delenv("QVMC_GRAD_CACHE")
+    M = _model(name)
+    k = 20_000 if name == "h56" else 40
+    grads = []
+    for model in (M, ref):
+        b = q.sample_without_replacement(model, k, q.CounterRng(4, 1), 2)
+        q.fill_amplitudes(b, model)
+        assert L.qvmc_cuda_model_last_fill_sampled(model._h) == 1
+        w = np.exp(b.log_probs - b.log_norm)
+        loc = np.random.default_rng(3).normal(size=b.size()) + 1j * np.random.default_rng(4).normal(size=b.size())
+        grads.append(model.energy_gradient(b.vectors, w, loc))
+        assert L.qvmc_cuda_model_last_gradient_cached(model._h) == (1 if model is M else 0)
+    assert np.array_equal(grads[0], grads[1])
+    # a different key set: recomputed, and equal to the reference model's gradient of it
+    g2 = M.energy_gradient(b.vectors[:-1], w[:-1], loc[:-1])
+    assert L.qvmc_cuda_model_last_gradient_cached(M._h) == 0
+    assert np.array_equal(g2, ref.energy_gradient(b.vectors[:-1], w[:-1], loc[:-1]))
+    # new parameters invalidate the activations
+    b = q.sample_without_replacement(M, k, q.CounterRng(4, 1), 2)
+    q.fill_amplitudes(b, M)
+    M.set_params(_cfg(name)[5])
+    M.energy_gradient(b.vectors, w, loc)
+    assert L.qvmc_cuda_model_last_gradient_cached(M._h) == 0
